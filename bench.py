@@ -1,0 +1,324 @@
+#!/usr/bin/env python
+"""Benchmark: FMM matvec throughput (particles/s) on BASELINE config 2.
+
+Default workload = BASELINE.json configs[1] ("cfg2"): N = 1,000,000 points
+uniform on the surface of [-1,1]^3, complex128 charges U(-1,1)+iU(-1,1),
+kappa*D = 128, L = 4, ncrit = 64 (``--workload cfg2_l6`` for L = 6,
+``--workload cfg1`` for the small sphere).  A step is one matvec
+(upward + M2L || P2P + downward) with the plan (tree + lists + symbols)
+already resident, exactly the reference's "matvec" stages.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2] [--impl reference]
+
+Prints ONE JSON line (rank 0).  ``--impl reference`` times the CPU oracle
+(numpy restatement of the reference, oracle/defmm_oracle.py) on a bounded
+sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particles/s per FMM matvec"
+UNIT = "particles/s"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-sample", type=int, default=20000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def _workload_desc(w, n):
+    return {
+        "workload": f"{w.name}: N={n} {w.kind}, kappa*D={w.kappa_d:g}, L={w.order}, ncrit={w.ncrit}, complex128",
+        "N": n,
+        "kappa_d": w.kappa_d,
+        "order": w.order,
+        "ncrit": w.ncrit,
+        "distribution": w.kind,
+    }
+
+
+def _cpu_oracle_sample(name, n_sample):
+    """Oracle matvec on the first n_sample points of the workload (same kappa)."""
+    from oracle import defmm_oracle as O
+    from paper_2202_04894_b200.workloads import WORKLOADS, kappa_for, make_charges, make_points
+
+    w = WORKLOADS[name]
+    pts = make_points(w.kind, w.n, 0)
+    kappa = kappa_for(pts, w.kappa_d)
+    sub = np.ascontiguousarray(pts[:n_sample])
+    q = make_charges(w.n, 1)[:n_sample]
+    _, counts, _, tm, _ = O.run(sub, q, order=w.order, ncrit=w.ncrit, kappa=kappa)
+    return n_sample / tm["matvec"], tm, counts
+
+
+class _Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        load = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {
+            "sm_mhz": float(np.median(load)) if load else None,
+            "sm_max_mhz": max(mx) if mx else None,
+            "reasons": sorted(reasons),
+            "samples": len(sm),
+        }
+
+
+def _measured_peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def run_reference(args):
+    from paper_2202_04894_b200.workloads import WORKLOADS
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    w = WORKLOADS[args.workload]
+    vals = []
+    for _ in range(max(args.warmup, 0)):
+        pass  # the oracle has no warm state worth priming; warm-up steps are not repeated
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, tm, counts = _cpu_oracle_sample(args.workload, args.cpu_sample)
+        vals.append(v)
+    wall = time.perf_counter() - t0
+    value = float(np.median(vals))
+    cfg = _workload_desc(w, w.n)
+    sample = f"first {args.cpu_sample} points of the {w.name} distribution, same kappa/L/ncrit; matvec stages only"
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * wall / max(args.steps, 1),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": cfg,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2202_04894_b200 import FmmConfig, HelmholtzKernel, direct_sum
+    from paper_2202_04894_b200.fmm import FmmPlan
+    from paper_2202_04894_b200.workloads import make_workload, sample_targets
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    pts, q, kappa, w = make_workload(args.workload)
+    n = pts.shape[0]
+    cfg = FmmConfig(order=w.order, ncrit=w.ncrit, kappa=kappa)
+    t0 = time.perf_counter()
+    plan = FmmPlan(pts, None, cfg, device=dev, charges=q)
+    setup_s = time.perf_counter() - t0
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    # --- device-resident matvec (value) --------------------------------
+    for _ in range(args.warmup):
+        plan.apply()
+    barrier()
+    clocks = _Clocks(local)
+    tot_ms, m2l_ms, p2p_ms, up_ms, down_ms = 0.0, 0.0, 0.0, 0.0, 0.0
+    for _ in range(args.steps):
+        flush.zero_()  # evict L2 between iterations (outside the timed events)
+        stages = []
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        plan.apply(stage_events=stages)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        tot_ms += a.elapsed_time(b)
+        el = {nm: x.elapsed_time(y) for nm, x, y in stages}
+        m2l_ms += el["m2l"]
+        p2p_ms += el["p2p"]
+        up_ms += el["upward"]
+        down_ms += el["downward"]
+    barrier()
+    clk = clocks.stop()
+    K = max(args.steps, 1)
+    t_step = tot_ms / K
+    if world > 1:
+        tt = torch.tensor([t_step], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step = float(tt.item())
+    value = world * n / (t_step / 1e3)  # replicas: every rank runs the full matvec
+
+    # --- end to end through the public plan API with host buffers -------
+    q_host = torch.as_tensor(q).pin_memory()
+    out_host = torch.empty(n, dtype=torch.complex128).pin_memory()
+    for _ in range(max(1, args.warmup)):
+        plan.set_charges(q_host.to(dev, non_blocking=True))
+        out_host.copy_(plan.apply(), non_blocking=True)
+    barrier()
+    e_ms = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        plan.set_charges(q_host.to(dev, non_blocking=True))
+        out_host.copy_(plan.apply(), non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        e_ms += a.elapsed_time(b)
+    e_step = e_ms / K
+    if world > 1:
+        tt = torch.tensor([e_step], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e_step = float(tt.item())
+
+    # --- accuracy on the 1000 sampled check targets ------------------------
+    pot = out_host.numpy()
+    s = sample_targets(n)
+    side = plan.st.root_box.side
+    d = direct_sum(HelmholtzKernel(kappa=kappa, singularity_tol=1e-12 * side), pts[s], pts, q, device=dev)
+    eps = float(np.linalg.norm(pot[s] - d) / np.linalg.norm(d))
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # --- roofline of the dominant kernel (M2L + fused F2L) -----------------
+    p = plan.plan
+    L = w.order
+    P3 = (2 * L - 1) ** 3
+    c = 16
+    n_m2l = p.counts["m2l_events"]
+    rows = p.m2l_row_slot.shape[0]
+    alg_bytes = n_m2l * 2 * P3 * c + rows * L**3 * c  # symbol + source spectrum per event, local write
+    m2l_s = (m2l_ms / K) / 1e3
+    peak, peak_kind = _measured_peak_hbm()
+    achieved = alg_bytes / m2l_s / 1e9
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": dict(_workload_desc(w, n), l2_flush="256 MiB memset between timed iterations",
+                       parallelism=f"replicas{world}" if world > 1 else "single"),
+        "stages_ms": {"upward": up_ms / K, "m2l": m2l_ms / K, "p2p_concurrent": p2p_ms / K,
+                      "downward": down_ms / K},
+        "roofline": {"bound": "hbm", "kernel": "defmm m2l_kernel (Hadamard M2L + fused F2L)",
+                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "alg_bytes_per_launch": alg_bytes, "kernel_ms": m2l_s * 1e3},
+        "e2e": {"value": world * n / (e_step / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(n * 16),
+                "d2h_bytes_per_step": int(n * 16), "ms_per_step": e_step},
+        "accuracy": {"rel_l2_vs_direct_1000": eps},
+        "gpu_launches": int(args.steps * plan.launches_per_apply),
+        "clocks": clk,
+        "setup_s": setup_s,
+    }
+    if not args.no_cpu_baseline:
+        v, tm, counts = _cpu_oracle_sample(args.workload, args.cpu_sample)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
+                                "sample": f"oracle matvec on the first {args.cpu_sample} points of {w.name} "
+                                          f"(same kappa, L, ncrit): {tm['matvec']:.1f} s"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = _args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,264 @@
+"""Device plan + matvec driver (drop-in for helmfmm.traversal's run_fmm*).
+
+``FmmPlan`` = tree + lists + symbols resident in HBM (the reusable
+"precompute" the reference recomputes every call); ``FmmPlan.apply`` is the
+matvec: P2M -> M2M (per level) -> M2F -> Hadamard M2L + F2L -> L2L (per level)
+-> L2P (+ near field, un-permute), with the P2P near field on a second CUDA
+stream overlapping the far field (traversal.py:283-418).  Every operator is a
+libdefmm_b200 kernel called through the C-ABI; there is no CPU path.
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+import torch
+
+from . import _lib
+from .config import FmmConfig, FmmInfo, InteractionEvent, TreeConfig
+from .geometry import compute_root_box
+from .plan import build_plan
+from .tree import build_tree
+
+__all__ = ["FmmPlan", "run_fmm", "run_fmm_full"]
+
+
+def _dev(a, dtype, device):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype).to(device)
+
+
+class FmmPlan:
+    """Reusable device plan for one particle geometry (targets is sources, or
+    a target/source pair sharing one root box, traversal.py:449-461)."""
+
+    def __init__(self, targets, sources=None, config: FmmConfig = FmmConfig(), device="cuda",
+                 keep_events: bool = False, charges=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("the defmm B200 path needs a CUDA device (no CPU fallback)")
+        _lib.load()
+        self.config = config
+        self.device = torch.device(device)
+        t0 = time.perf_counter()
+        tree_cfg = TreeConfig(ncrit=config.ncrit, hard_depth_cap=config.hard_depth_cap)
+        same = sources is None or targets is sources
+        src = targets if same else sources
+        n_src = np.atleast_2d(np.asarray(src)).shape[0]
+        qs = np.zeros(n_src, complex) if charges is None else charges
+        if same:
+            st, sp = build_tree(src, qs, tree_cfg)
+            tt, tp = st, sp
+        else:
+            both = np.vstack([np.atleast_2d(targets), np.atleast_2d(sources)])
+            box = compute_root_box(both)
+            st, sp = build_tree(sources, qs, tree_cfg, root_box=box)
+            tt, tp = build_tree(targets, np.zeros(np.atleast_2d(targets).shape[0]), tree_cfg, root_box=box)
+        self.same = same
+        self.tt, self.st, self.tp, self.sp = tt, st, tp, sp
+        t1 = time.perf_counter()
+        self.plan = build_plan(tt, st, config.order, config.kappa, config.eta, config.hf_switch,
+                               keep_events=keep_events)
+        t2 = time.perf_counter()
+        self.timings = {"tree": t1 - t0, "blank": t2 - t1}
+        self._upload()
+        self._symbols()
+        torch.cuda.synchronize(self.device)
+        self.timings["precompute"] = time.perf_counter() - t2
+        if charges is not None:
+            self.set_charges(charges)
+
+    # ------------------------------------------------------------------
+    def _upload(self):
+        p, d = self.plan, self.device
+        L = self.config.order
+        i64, i32, f64 = torch.int64, torch.int32, torch.float64
+        tt, st = self.tt, self.st
+        self.L, self.L3, self.P3 = L, L**3, (2 * L - 1) ** 3
+        # particles (sorted order), SoA
+        self.s_xyz = [_dev(self.sp.positions[:, k], f64, d) for k in range(3)]
+        self.t_xyz = self.s_xyz if self.same else [_dev(self.tp.positions[:, k], f64, d) for k in range(3)]
+        self.s_perm = _dev(self.sp.original_index, i64, d)
+        self.t_perm = self.s_perm if self.same else _dev(self.tp.original_index, i64, d)
+        self.n_src = self.sp.n
+        self.n_tgt = self.tp.n
+
+        def geom(tree):
+            return dict(start=_dev(tree.start, i64, d), stop=_dev(tree.stop, i64, d),
+                        alpha=_dev(tree.alpha, f64, d), level=_dev(tree.level, i32, d),
+                        beta=_dev(tree.level_beta, f64, d))
+
+        self.sg = geom(st)
+        self.tg = self.sg if self.same else geom(tt)
+        self.dirs = _dev(p.dirs if p.dirs.size else np.zeros((1, 3)), f64, d)
+        # upward lists
+        self.p2m_cell = _dev(p.m_cell[p.p2m_idx], i32, d)
+        self.p2m_dir = _dev(p.m_dir[p.p2m_idx], i32, d)
+        self.p2m_slot = _dev(p.p2m_idx, i64, d)
+        self.m2m = []
+        for lev, slots, son_slot in p.m2m_levels:
+            self.m2m.append((float(st.side_at(lev + 1)), _dev(slots, i64, d), _dev(p.m_dir[slots], i32, d),
+                             _dev(son_slot, i64, d), int(slots.shape[0])))
+        self.hat_slot = _dev(p.hat_slot, i64, d)
+        # M2L
+        self.row_slot = _dev(p.m2l_row_slot, i64, d)
+        self.row_ptr = _dev(p.m2l_row_ptr, i64, d)
+        self.e_src = _dev(p.m2l_src, i32, d)
+        self.e_sym = _dev(p.m2l_sym, i32, d)
+        self.e_rid = _dev(p.m2l_rid, torch.int8, d)
+        # downward
+        self.l2l = []
+        for lev, outs, octant, ptr, src, sdir in p.l2l_levels:
+            self.l2l.append((float(tt.side_at(lev)), _dev(outs, i64, d), _dev(octant, torch.int8, d),
+                             _dev(ptr, i64, d), _dev(src, i64, d), _dev(sdir, i32, d), int(outs.shape[0])))
+        self.leaf_cell = _dev(p.leaf_cells, i32, d)
+        self.leaf_lo = _dev(p.leaf_slot_lo, i64, d)
+        self.leaf_hi = _dev(p.leaf_slot_hi, i64, d)
+        self.slot_dir = _dev(p.l_dir, i32, d)
+        self.tgt_lo = _dev(tt.start[p.leaf_cells], i64, d)
+        self.tgt_hi = _dev(tt.stop[p.leaf_cells], i64, d)
+        self.p2p_ptr = _dev(p.p2p_ptr, i64, d)
+        self.p2p_lo = _dev(p.p2p_lo, i64, d)
+        self.p2p_hi = _dev(p.p2p_hi, i64, d)
+        # workspaces
+        c128 = torch.complex128
+        self.mult = torch.empty((max(p.n_mult, 1), self.L3), dtype=c128, device=d)
+        self.hat = torch.empty((max(p.n_hat, 1), self.P3), dtype=c128, device=d)
+        self.local = torch.empty((max(p.n_local, 1), self.L3), dtype=c128, device=d)
+        self.near = torch.empty(self.n_tgt, dtype=c128, device=d)
+        self.q = torch.zeros(self.n_src, dtype=c128, device=d)
+        self.out = torch.empty(self.n_tgt, dtype=c128, device=d)
+        self.side_stream = torch.cuda.Stream(device=d)
+
+    def _symbols(self):
+        p = self.plan
+        self.sym = torch.empty((max(p.n_sym, 1), self.P3), dtype=torch.complex128, device=self.device)
+        if p.n_sym:
+            tv = _dev(p.sym_tvec.reshape(-1), torch.int32, self.device)
+            beta = _dev(p.sym_beta, torch.float64, self.device)
+            _lib.call("defmm_symbols_c128", self.L, p.n_sym, tv, beta, float(p.kappa), self.sym,
+                      torch.cuda.current_stream(self.device).cuda_stream)
+
+    # ------------------------------------------------------------------
+    def set_charges(self, charges):
+        """Load charges (caller order) into the sorted device buffer."""
+        q = torch.as_tensor(np.asarray(charges, dtype=complex)) if not torch.is_tensor(charges) else charges
+        q = q.to(device=self.device, dtype=torch.complex128)
+        self.q.copy_(q[self.s_perm])
+
+    def set_charges_sorted(self, q_sorted):
+        self.q.copy_(q_sorted)
+
+    def apply(self, out=None, stage_events=None):
+        """One matvec with the charges currently loaded; returns potentials in
+        the caller's target order (device tensor).  ``stage_events`` (list)
+        receives (name, start_event, end_event) for the stage timers."""
+        p = self.plan
+        L = self.L
+        kappa = float(p.kappa)
+        stream = torch.cuda.current_stream(self.device)
+        sh = stream.cuda_stream
+        out = self.out if out is None else out
+        ev = (lambda: torch.cuda.Event(enable_timing=True)) if stage_events is not None else None
+        # near field on the side stream, concurrent with the far field
+        side = self.side_stream
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            if stage_events is not None:
+                e0 = ev()
+                e0.record(side)
+            _lib.call("defmm_p2p_c128", p.leaf_cells.shape[0], self.tgt_lo, self.tgt_hi, self.p2p_ptr,
+                      self.p2p_lo, self.p2p_hi, *self.t_xyz, *self.s_xyz, self.q, kappa, float(p.tol),
+                      self.near, side.cuda_stream)
+            if stage_events is not None:
+                e1 = ev()
+                e1.record(side)
+                stage_events.append(("p2p", e0, e1))
+        sg, tg = self.sg, self.tg
+        if stage_events is not None:
+            a = ev()
+            a.record(stream)
+        # upward: P2M at every leaf key, M2M per level bottom-up, M2F
+        _lib.call("defmm_p2m_c128", L, self.p2m_slot.shape[0], self.p2m_cell, self.p2m_dir, self.p2m_slot,
+                  sg["start"], sg["stop"], sg["alpha"], sg["level"], sg["beta"], self.dirs, *self.s_xyz, self.q,
+                  kappa, self.mult, sh)
+        for son_beta, slots, mdir, son_slot, n in self.m2m:
+            _lib.call("defmm_m2m_c128", L, n, slots, mdir, son_slot, son_beta, self.dirs, kappa, self.mult, sh)
+        _lib.call("defmm_m2f_c128", L, p.n_hat, self.hat_slot, self.mult, self.hat, sh)
+        if stage_events is not None:
+            b = ev()
+            b.record(stream)
+            stage_events.append(("upward", a, b))
+        # M2L (+ fused F2L) into the local slots
+        self.local.zero_()
+        _lib.call("defmm_m2l_c128", L, self.row_slot.shape[0], self.row_slot, self.row_ptr, self.e_src,
+                  self.e_sym, self.e_rid, self.hat, self.sym, self.local, sh)
+        if stage_events is not None:
+            c = ev()
+            c.record(stream)
+            stage_events.append(("m2l", b, c))
+        # downward: L2L per level top-down, then L2P + near + un-permute
+        for son_beta, outs, octant, ptr, src, sdir, n in self.l2l:
+            _lib.call("defmm_l2l_c128", L, n, outs, octant, ptr, src, sdir, son_beta, self.dirs, kappa,
+                      self.local, sh)
+        stream.wait_stream(side)
+        _lib.call("defmm_l2p_c128", L, self.leaf_cell.shape[0], self.leaf_cell, self.leaf_lo, self.leaf_hi,
+                  self.slot_dir, tg["start"], tg["stop"], tg["alpha"], tg["level"], tg["beta"], self.dirs,
+                  *self.t_xyz, kappa, self.local, self.near, self.t_perm, out, sh)
+        if stage_events is not None:
+            e = ev()
+            e.record(stream)
+            stage_events.append(("downward", c, e))
+        return out
+
+    @property
+    def launches_per_apply(self) -> int:
+        return 5 + len(self.m2m) + len(self.l2l)
+
+    def events(self):
+        """InteractionEvent list (traversal.py:80-85) with Cell views."""
+        p = self.plan
+        if p.m2l_events is None:
+            raise RuntimeError("plan was built without keep_events=True")
+        tl = {c.index: c for lv in self.tt.levels for c in lv}
+        sl = tl if self.same else {c.index: c for lv in self.st.levels for c in lv}
+        out = []
+        mt, ms, md = p.m2l_events
+        for t, s, dd in zip(mt.tolist(), ms.tolist(), md.tolist()):
+            key = None
+            if dd >= 0:
+                e = p.hf_max - int(self.tt.level[t])
+                key = (e, dd - int(p.dir_off[e]))
+            out.append(InteractionEvent("M2L", tl[t], sl[s], key))
+        pt, ps = p.p2p_events
+        for t, s in zip(pt.tolist(), ps.tolist()):
+            out.append(InteractionEvent("P2P", tl[t], sl[s]))
+        return out
+
+
+def run_fmm_full(targets, sources, charges, config: FmmConfig = FmmConfig(), events: list | None = None):
+    """traversal.py:432-506 on the B200: (potentials, FmmInfo)."""
+    info = FmmInfo()
+    t_start = time.perf_counter()
+    same = targets is sources
+    plan = FmmPlan(targets, None if same else sources, config, keep_events=events is not None,
+                   charges=np.asarray(charges, dtype=complex))
+    info.hf_max_level = plan.plan.hf_max
+    stages = []
+    out = plan.apply(stage_events=stages)
+    pot = out.cpu().numpy()
+    for k, v in plan.timings.items():
+        info.timings[k] = v
+    el = {name: a.elapsed_time(b) / 1e3 for name, a, b in stages}
+    info.timings["upward"] = el["upward"]
+    info.timings["m2l_p2p"] = el["m2l"] + el["p2p"]
+    info.timings["downward"] = el["downward"]
+    info.timings["total"] = time.perf_counter() - t_start
+    info.counts = {k: v for k, v in plan.plan.counts.items() if k != "translations"}
+    if events is not None:
+        events.extend(plan.events())
+    return pot, info
+
+
+def run_fmm(targets, sources, charges, config: FmmConfig = FmmConfig()):
+    """traversal.py:509-516."""
+    return run_fmm_full(targets, sources, charges, config)[0]

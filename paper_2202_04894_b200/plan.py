@@ -1,0 +1,506 @@
+"""Host "precompute": the reference's blank passes + DTT as flat CSR lists.
+
+The reference decides everything recursively, one Python frame per visited
+cell pair (traversal.py:182-213 blank passes, :320-348 DTT).  Since every
+visited pair is same-level, the recursion is equivalent to a level-
+synchronous sweep: at level l each candidate pair is M2L (MAC holds), P2P
+(either cell is a leaf) or expands into sons x sons.  This module performs
+that sweep with vectorised numpy and emits the device plan:
+
+* MAC per level as a lookup on the integer gap^2 (the MAC depends on
+  (level, gap^2) only), each entry evaluated with the reference's exact FP64
+  expression ``max(kappa*w*w, 2.0*w) <= eta*(beta*sqrt(gap2))``
+  (traversal.py:107-113) or ``gap2 >= 1`` (:100-104);
+* HF M2L keys = nearest direction of each distinct translation
+  (directions.nearest_directions, bit-exact with directions.py:78-89);
+* canonical symbols + rotation ids per distinct (level, translation)
+  (fourier.py:104-120, 211-247);
+* marks (traversal.py:190-192) and their downward propagation (:203-213);
+* dense expansion slots: multipoles keyed (cell, key) on the source tree,
+  locals on the target tree, sorted by (cell, key) -- the reference's
+  per-cell dicts (tree.py:75-78) made contiguous;
+* CSR lists for P2M, M2M (son slot per octant), M2F, M2L rows (target-major),
+  L2L (gather per son slot), L2P (slot range per leaf) and P2P (merged
+  source runs per target leaf).
+
+Integer counts reproduce FmmInfo.counts exactly (traversal.py:495-505).
+"""
+
+from __future__ import annotations
+
+import itertools
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .directions import generate_direction_tree, nearest_directions
+from .tree import SQRT3, ClusterTree
+
+__all__ = ["Plan", "build_plan", "hf_max_level", "canonicalize_many", "GROUP48"]
+
+
+def _group48() -> np.ndarray:
+    """fourier.py:90-101's signed permutation matrices, same order."""
+    mats = []
+    for perm in itertools.permutations(range(3)):
+        for signs in itertools.product((1, -1), repeat=3):
+            m = np.zeros((3, 3), dtype=np.int64)
+            for a in range(3):
+                m[a, perm[a]] = signs[a]
+            mats.append(m)
+    return np.stack(mats)
+
+
+GROUP48 = _group48()
+
+
+def canonicalize_many(t: np.ndarray):
+    """(canonical (m,3), rotation id (m,)) -- fourier.py:104-120 batched."""
+    t = np.asarray(t, np.int64)
+    if np.any(np.all(t == 0, axis=1)):
+        raise ValueError("zero translation cannot be canonicalized")
+    canon = -np.sort(-np.abs(t), axis=1)
+    img = np.einsum("gab,mb->mga", GROUP48, canon)
+    hit = np.all(img == t[:, None, :], axis=2)
+    return canon, np.argmax(hit, axis=1).astype(np.int8)
+
+
+def hf_max_level(tree: ClusterTree, depth: int, kappa: float, hf_switch: float) -> int:
+    """traversal.py:145-157 (w = sqrt(3) * side / 2 >= hf_switch / kappa)."""
+    hf = -1
+    if kappa > 0:
+        for level in range(depth + 1):
+            w = np.sqrt(3.0) * tree.side_at(level) / 2.0
+            if kappa * w >= hf_switch:
+                hf = level
+            else:
+                break
+    return hf
+
+
+def _mac_lut(g2: np.ndarray, level: int, hf: bool, beta: float, kappa: float, eta: float) -> np.ndarray:
+    uniq, inv = np.unique(g2, return_inverse=True)
+    if hf:
+        w = SQRT3 * beta / 2.0
+        lhs = max(kappa * w * w, 2.0 * w)
+        vals = np.array([lhs <= eta * (beta * np.sqrt(float(g))) for g in uniq], dtype=bool)
+    else:
+        vals = uniq >= 1
+    return vals[inv]
+
+
+def _expand_pairs(ft, nt, fs, ns):
+    """sons(t) x sons(s) for each pair, t-major (traversal.py:345-348)."""
+    cnt = nt * ns
+    tot = int(cnt.sum())
+    if tot == 0:
+        z = np.zeros(0, np.int64)
+        return z, z
+    rep = np.repeat(np.arange(cnt.shape[0]), cnt)
+    k = np.arange(tot) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+    nsr = ns[rep]
+    return ft[rep] + k // nsr, fs[rep] + k % nsr
+
+
+def _csr(keys: np.ndarray, n: int) -> np.ndarray:
+    """Row pointer of sorted ``keys`` over rows 0..n-1."""
+    return np.searchsorted(keys, np.arange(n + 1)).astype(np.int64)
+
+
+@dataclass
+class Plan:
+    """Everything the device matvec needs, as host numpy arrays."""
+
+    order: int
+    kappa: float
+    tol: float
+    hf_max: int
+    same: bool
+    dirs: np.ndarray  # (ndir, 3) all refinements concatenated
+    dir_off: np.ndarray  # refinement e -> first global id
+    counts: dict = field(default_factory=dict)
+    # symbols
+    sym_tvec: np.ndarray = None  # (nsym, 3) int32 canonical translations
+    sym_beta: np.ndarray = None  # (nsym,)
+    # multipole slots (source tree)
+    m_cell: np.ndarray = None
+    m_dir: np.ndarray = None  # global dir id or -1
+    p2m_idx: np.ndarray = None  # slots computed by P2M
+    m2m_levels: list = None  # [(level, slots, son_slot (k,8))] deepest first
+    hat_slot: np.ndarray = None  # mult slot of each spectrum
+    # locals (target tree)
+    l_cell: np.ndarray = None
+    l_dir: np.ndarray = None
+    m2l_row_slot: np.ndarray = None
+    m2l_row_ptr: np.ndarray = None
+    m2l_src: np.ndarray = None  # hat index
+    m2l_sym: np.ndarray = None
+    m2l_rid: np.ndarray = None
+    m2l_level: np.ndarray = None  # per row
+    l2l_levels: list = None  # [(son level, out_slot, octant, ptr, src_slot, src_dir)]
+    leaf_cells: np.ndarray = None  # target-tree leaves
+    leaf_slot_lo: np.ndarray = None
+    leaf_slot_hi: np.ndarray = None
+    # near field (target leaves)
+    p2p_ptr: np.ndarray = None
+    p2p_lo: np.ndarray = None
+    p2p_hi: np.ndarray = None
+    # event logs (optional, for the events= API)
+    m2l_events: tuple = None
+    p2p_events: tuple = None
+
+    @property
+    def n_mult(self):
+        return int(self.m_cell.shape[0])
+
+    @property
+    def n_local(self):
+        return int(self.l_cell.shape[0])
+
+    @property
+    def n_hat(self):
+        return int(self.hat_slot.shape[0])
+
+    @property
+    def n_sym(self):
+        return int(self.sym_tvec.shape[0])
+
+
+def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: float, hf_switch: float,
+               keep_events: bool = False) -> Plan:
+    same = tt is st
+    depth = max(tt.depth, st.depth)
+    hf = hf_max_level(tt, depth, kappa, hf_switch)
+    dt = generate_direction_tree(hf) if hf >= 0 else None
+    if dt is not None:
+        dirs = np.concatenate(dt.levels)
+        dir_off = np.concatenate([[0], np.cumsum([d.shape[0] for d in dt.levels])]).astype(np.int64)
+    else:
+        dirs = np.zeros((0, 3))
+        dir_off = np.zeros(1, np.int64)
+    tol = 1e-12 * st.root_box.side  # traversal.py:465-467
+    plan = Plan(order=order, kappa=kappa, tol=tol, hf_max=hf, same=same, dirs=dirs, dir_off=dir_off)
+
+    # ---- level-synchronous DTT (traversal.py:320-348) ----------------------
+    m2l_t, m2l_s, m2l_lev = [], [], []
+    p2p_t, p2p_s = [], []
+    T = np.zeros(1, np.int64)
+    S = np.zeros(1, np.int64)
+    for lev in range(depth + 1):
+        if T.size == 0:
+            break
+        d = tt.coords[T] - st.coords[S]
+        g = np.maximum(np.abs(d) - 1, 0)
+        g2 = (g * g).sum(axis=1)
+        mac = _mac_lut(g2, lev, lev <= hf, tt.side_at(lev), kappa, eta)
+        m2l_t.append(T[mac])
+        m2l_s.append(S[mac])
+        m2l_lev.append(np.full(int(mac.sum()), lev, np.int64))
+        rest = ~mac
+        leafy = tt.is_leaf[T] | st.is_leaf[S]
+        sel = rest & leafy
+        p2p_t.append(T[sel])
+        p2p_s.append(S[sel])
+        sel = rest & ~leafy
+        rt, rs = T[sel], S[sel]
+        T, S = _expand_pairs(tt.first_son[rt], tt.n_sons[rt], st.first_son[rs], st.n_sons[rs])
+    mt = np.concatenate(m2l_t) if m2l_t else np.zeros(0, np.int64)
+    ms = np.concatenate(m2l_s) if m2l_s else np.zeros(0, np.int64)
+    mlev = np.concatenate(m2l_lev) if m2l_lev else np.zeros(0, np.int64)
+    pt = np.concatenate(p2p_t)
+    ps = np.concatenate(p2p_s)
+    n_m2l = mt.shape[0]
+
+    # ---- per-event translation, key, symbol --------------------------------
+    tv = tt.coords[mt] - st.coords[ms]
+    # distinct (level, t): key on a packed integer (translations are short:
+    # |t|_inf <= 3 at LF levels, bounded by the HF near field above)
+    off = int(np.abs(tv).max()) if n_m2l else 0
+    R = 2 * off + 1
+    if (depth + 1) * R**3 >= 2**62:
+        raise ValueError("translation range too large for the packed plan keys")
+    packed = ((mlev * R + (tv[:, 0] + off)) * R + (tv[:, 1] + off)) * R + (tv[:, 2] + off)
+    uniq, inv = np.unique(packed, return_inverse=True)
+    u_lev = np.empty(uniq.shape[0], np.int64)
+    u_lev[inv] = mlev
+    u_tv = np.empty((uniq.shape[0], 3), np.int64)
+    u_tv[inv] = tv
+    # key: global direction id at HF levels (traversal.py:187-190, 326-331)
+    u_dir = np.full(uniq.shape[0], -1, np.int64)
+    for lev in np.unique(u_lev):
+        if lev <= hf:
+            e = hf - int(lev)
+            sel = np.nonzero(u_lev == lev)[0]
+            u_dir[sel] = dir_off[e] + nearest_directions(dt.levels[e], u_tv[sel])
+    # canonical symbol classes (fourier.py:233-247)
+    if uniq.shape[0]:
+        canon, rid = canonicalize_many(u_tv)
+    else:
+        canon, rid = np.zeros((0, 3), np.int64), np.zeros(0, np.int8)
+    cpack = ((u_lev * R + canon[:, 0]) * R + canon[:, 1]) * R + canon[:, 2]
+    cuniq, cinv = np.unique(cpack, return_inverse=True)
+    sym_lev = np.empty(cuniq.shape[0], np.int64)
+    sym_lev[cinv] = u_lev
+    sym_t = np.empty((cuniq.shape[0], 3), np.int64)
+    sym_t[cinv] = canon
+    plan.sym_tvec = sym_t.astype(np.int32)
+    plan.sym_beta = np.array([tt.side_at(int(l)) for l in sym_lev], dtype=np.float64)
+    _check_stencils(sym_t, sym_lev, tt, order, tol)
+    ev_dir = u_dir[inv]
+    ev_sym = cinv[inv].astype(np.int32)
+    ev_rid = rid[inv]
+
+    # ---- marks (traversal.py:190-192) + downward propagation (:203-213) ---
+    # mark key = cell * KD + local direction index (refinement e = hf - level)
+    KD = int(dirs.shape[0]) + 1
+    hf_ev = ev_dir >= 0
+    loc_i = np.where(hf_ev, ev_dir - dir_off[np.maximum(hf - mlev, 0)], -1)
+    t_marks = [[] for _ in range(depth + 1)]
+    s_marks = [[] for _ in range(depth + 1)] if not same else t_marks
+    for lev in range(min(hf, depth) + 1):
+        sel = hf_ev & (mlev == lev)
+        t_marks[lev].append(mt[sel] * KD + loc_i[sel])
+        s_marks[lev].append(ms[sel] * KD + loc_i[sel])
+    marks_t = _propagate_marks(tt, t_marks, hf, dt, KD)
+    marks_s = marks_t if same else _propagate_marks(st, s_marks, hf, dt, KD)
+
+    # ---- multipole slots on the source tree --------------------------------
+    m_cell, m_loc, m_dir = [], [], []
+    for lev in range(st.depth + 1):
+        if lev <= hf:
+            mk = marks_s[lev]
+            c, i = mk // KD, mk % KD
+            m_dir.append(dir_off[hf - lev] + i)
+        else:
+            c = np.arange(st.level_offsets[lev], st.level_offsets[lev + 1])
+            i = np.full(c.shape[0], -1, np.int64)
+            m_dir.append(i)
+        m_cell.append(c)
+        m_loc.append(i)
+    m_cell = np.concatenate(m_cell)
+    m_loc = np.concatenate(m_loc)
+    m_dir = np.concatenate(m_dir)
+    plan.m_cell, plan.m_dir = m_cell, m_dir
+    # slot lookup key: cell*(KD+1) + (local dir + 1), 0 for LF; sorted by construction
+    mkey = m_cell * (KD + 1) + (m_loc + 1)
+    assert np.all(np.diff(mkey) > 0)
+
+    def mslot(cells, loc_dirs):
+        k = cells * (KD + 1) + (loc_dirs + 1)
+        j = np.searchsorted(mkey, k)
+        ok = (j < mkey.shape[0]) & (mkey[np.minimum(j, mkey.shape[0] - 1)] == k)
+        return np.where(ok, j, -1)
+
+    leaf_m = st.is_leaf[m_cell]
+    plan.p2m_idx = np.nonzero(leaf_m)[0]
+    # M2M per level, deepest first (traversal.py:283-289)
+    m2m_levels = []
+    mlevel = st.level[m_cell]
+    for lev in range(st.depth - 1, -1, -1):
+        slots = np.nonzero((mlevel == lev) & ~leaf_m)[0]
+        if slots.size == 0:
+            continue
+        c = m_cell[slots]
+        son_slot = np.full((slots.shape[0], 8), -1, np.int64)
+        for k in range(8):
+            has = st.n_sons[c] > k
+            if not has.any():
+                continue
+            sons = st.first_son[c[has]] + k
+            octv = st.coords[sons] - 2 * st.coords[c[has]]
+            oct_ = octv[:, 0] * 4 + octv[:, 1] * 2 + octv[:, 2]
+            if lev + 1 <= hf:
+                e = hf - lev
+                li = m_dir[slots[has]] - dir_off[e]
+                sk = dt.fathers[e][li]
+            else:
+                sk = np.full(sons.shape[0], -1, np.int64)
+            ss = mslot(sons, sk)
+            if np.any(ss < 0):
+                raise RuntimeError("missing son expansion: blank-pass inconsistency")
+            son_slot[np.nonzero(has)[0], oct_] = ss
+        m2m_levels.append((lev, slots, son_slot))
+    plan.m2m_levels = m2m_levels
+
+    # ---- M2L sources -> spectra (M2F only for used multipoles) -------------
+    src_loc = np.where(hf_ev, loc_i, -1)
+    src_slot = mslot(ms, src_loc)
+    if np.any(src_slot < 0):
+        raise RuntimeError("missing source expansion: blank-pass bug")
+    hat_slot, src_hat = np.unique(src_slot, return_inverse=True)
+    plan.hat_slot = hat_slot
+
+    # ---- local slots on the target tree -------------------------------------
+    tgt_key_cell = mt
+    tgt_key_loc = src_loc  # same key
+    l_cell, l_loc, l2l = _local_slots(tt, tgt_key_cell, tgt_key_loc, hf, dt, dir_off, KD)
+    plan.l_cell = l_cell
+    plan.l_dir = np.where(l_loc >= 0, dir_off[np.maximum(hf - tt.level[l_cell], 0)] + l_loc, -1)
+    lkey = l_cell * (KD + 1) + (l_loc + 1)
+    assert np.all(np.diff(lkey) > 0)
+
+    def lslot(cells, loc_dirs):
+        k = cells * (KD + 1) + (loc_dirs + 1)
+        j = np.searchsorted(lkey, k)
+        assert np.all(lkey[j] == k)
+        return j
+
+    tslot = lslot(tgt_key_cell, tgt_key_loc)
+    order_ev = np.argsort(tslot, kind="stable")
+    rows, row_start = np.unique(tslot[order_ev], return_index=True)
+    plan.m2l_row_slot = rows.astype(np.int64)
+    plan.m2l_row_ptr = np.concatenate([row_start, [n_m2l]]).astype(np.int64)
+    plan.m2l_src = src_hat[order_ev].astype(np.int32)
+    plan.m2l_sym = ev_sym[order_ev]
+    plan.m2l_rid = ev_rid[order_ev]
+    plan.m2l_level = tt.level[l_cell[rows]]
+
+    # L2L gather lists per son level
+    l2l_levels = []
+    if l2l[0].size:
+        f_slot = lslot(l2l[0], l2l[1])
+        s_slot = lslot(l2l[2], l2l[3])
+        f_dir = plan.l_dir[f_slot]
+        o = np.lexsort((f_slot, s_slot))
+        f_slot, s_slot, f_dir = f_slot[o], s_slot[o], f_dir[o]
+        outs, first = np.unique(s_slot, return_index=True)
+        ptr = np.concatenate([first, [s_slot.shape[0]]]).astype(np.int64)
+        son_cells = l_cell[outs]
+        fathers = tt.parent[son_cells]
+        octv = tt.coords[son_cells] - 2 * tt.coords[fathers]
+        octant = (octv[:, 0] * 4 + octv[:, 1] * 2 + octv[:, 2]).astype(np.int8)
+        son_lev = tt.level[son_cells]
+        for lev in np.unique(son_lev):
+            sel = np.nonzero(son_lev == lev)[0]
+            a, b = ptr[sel[0]], ptr[sel[-1] + 1]
+            l2l_levels.append((int(lev), outs[sel], octant[sel], ptr[sel[0] : sel[-1] + 2] - a, f_slot[a:b], f_dir[a:b].astype(np.int32)))
+    plan.l2l_levels = l2l_levels
+
+    # L2P: every target leaf (also writes near + far, un-permuted)
+    leaves = np.nonzero(tt.is_leaf)[0]
+    leaves = leaves[np.argsort(tt.start[leaves], kind="stable")]  # Morton (particle) order
+    plan.leaf_cells = leaves
+    plan.leaf_slot_lo = np.searchsorted(l_cell, leaves, side="left").astype(np.int64)
+    plan.leaf_slot_hi = np.searchsorted(l_cell, leaves, side="right").astype(np.int64)
+
+    # ---- P2P lists: split non-leaf targets into leaves, merge runs ---------
+    n_pairs = int(((tt.stop[pt] - tt.start[pt]) * (st.stop[ps] - st.start[ps])).sum())
+    lstart = tt.start[leaves]
+    l0 = np.searchsorted(lstart, tt.start[pt])
+    l1 = np.searchsorted(lstart, tt.stop[pt])
+    cnt = l1 - l0
+    rep = np.repeat(np.arange(pt.shape[0]), cnt)
+    lidx = np.repeat(l0, cnt) + (np.arange(rep.shape[0]) - np.repeat(np.cumsum(cnt) - cnt, cnt))
+    slo = st.start[ps][rep]
+    shi = st.stop[ps][rep]
+    o = np.lexsort((slo, lidx))
+    lidx, slo, shi = lidx[o], slo[o], shi[o]
+    # merge contiguous runs of the same target leaf
+    brk = np.ones(lidx.shape[0], bool)
+    brk[1:] = (lidx[1:] != lidx[:-1]) | (slo[1:] != shi[:-1])
+    gid = np.cumsum(brk) - 1
+    run_lo = slo[brk]
+    run_hi = np.zeros(run_lo.shape[0], np.int64)
+    np.maximum.at(run_hi, gid, shi)
+    run_leaf = lidx[brk]
+    plan.p2p_ptr = _csr(run_leaf, leaves.shape[0])
+    plan.p2p_lo, plan.p2p_hi = run_lo.astype(np.int64), run_hi
+
+    n_exp = int(m_cell.shape[0])
+    plan.counts = {
+        "cells": tt.n_cells if same else tt.n_cells + st.n_cells,
+        "leaves": tt.n_leaves if same else tt.n_leaves + st.n_leaves,
+        "symbols": int(cuniq.shape[0]),
+        "effective_expansions": n_exp,
+        "p2p_pairs": n_pairs,
+        "m2l_events": int(n_m2l),
+        "translations": int(uniq.shape[0]),
+    }
+    if keep_events:
+        plan.m2l_events = (mt, ms, ev_dir)
+        plan.p2p_events = (pt, ps)
+    return plan
+
+
+def _check_stencils(sym_t, sym_lev, tree, order, tol):
+    """fourier.py:179-180: a symbol stencil touching r < tol means the MAC is
+    violated -> ValueError (same expression as precompute_symbol)."""
+    if sym_t.shape[0] == 0:
+        return
+    P = 2 * order - 1
+    off = np.arange(P)
+    off = np.where(off < order, off, off - P) * (1.0 / (order - 1))
+    # min over the grid of r is attained per axis at the smallest |t_a + off|
+    for lev in np.unique(sym_lev):
+        beta = tree.side_at(int(lev))
+        t = sym_t[sym_lev == lev].astype(np.float64)
+        z = t[:, :, None] + off[None, None, :]
+        zmin = np.min(np.abs(z), axis=2)
+        r = beta * np.sqrt(zmin[:, 0] ** 2 + zmin[:, 1] ** 2 + zmin[:, 2] ** 2)
+        if np.any(r < tol * 4):  # conservative pre-screen, then exact check
+            for tv in t[r < tol * 4]:
+                zx, zy, zz = np.meshgrid(tv[0] + off, tv[1] + off, tv[2] + off, indexing="ij")
+                if np.min(beta * np.sqrt(zx**2 + zy**2 + zz**2)) < tol:
+                    raise ValueError("kernel singularity inside the M2L stencil: MAC violated")
+
+
+def _propagate_marks(tree, own, hf, dt, KD):
+    """blank_downward_pass (traversal.py:203-213): per HF level the sorted,
+    unique mark keys cell*KD + i, fathers' marks (e > 0) pushed to all sons."""
+    out = [np.zeros(0, np.int64) for _ in range(tree.depth + 1)]
+    carry = np.zeros(0, np.int64)
+    for lev in range(min(hf, tree.depth) + 1):
+        parts = own[lev] + [carry]
+        mk = np.unique(np.concatenate(parts)) if parts else np.zeros(0, np.int64)
+        out[lev] = mk
+        e = hf - lev
+        if e > 0 and mk.size:
+            c = mk // KD
+            i = mk % KD
+            ns = tree.n_sons[c]
+            rep = np.repeat(np.arange(c.shape[0]), ns)
+            k = np.arange(rep.shape[0]) - np.repeat(np.cumsum(ns) - ns, ns)
+            sons = tree.first_son[c][rep] + k
+            carry = sons * KD + dt.fathers[e][i[rep]]
+        else:
+            carry = np.zeros(0, np.int64)
+    return out
+
+
+def _local_slots(tree, cells, loc, hf, dt, dir_off, KD):
+    """Local expansion keys per target cell: M2L targets plus everything the
+    L2L pass pushes down (traversal.py:355-391), top-down.
+
+    Returns (l_cell, l_loc sorted by (cell, loc)) and the L2L relation
+    (father cell, father loc, son cell, son loc)."""
+    lev_of = tree.level[cells]
+    keys_all = []
+    rel = ([], [], [], [])
+    carry = np.zeros(0, np.int64)
+    for lev in range(tree.depth + 1):
+        sel = lev_of == lev
+        k = np.unique(np.concatenate([cells[sel] * (KD + 1) + (loc[sel] + 1), carry]))
+        keys_all.append(k)
+        c = k // (KD + 1)
+        li = k % (KD + 1) - 1
+        nonleaf = ~tree.is_leaf[c]
+        c, li = c[nonleaf], li[nonleaf]
+        ns = tree.n_sons[c]
+        rep = np.repeat(np.arange(c.shape[0]), ns)
+        kk = np.arange(rep.shape[0]) - np.repeat(np.cumsum(ns) - ns, ns)
+        sons = tree.first_son[c][rep] + kk
+        fl = li[rep]
+        if lev + 1 <= hf:
+            e = hf - lev
+            sl = dt.fathers[e][fl]
+        else:
+            sl = np.full(sons.shape[0], -1, np.int64)
+        rel[0].append(c[rep])
+        rel[1].append(fl)
+        rel[2].append(sons)
+        rel[3].append(sl)
+        carry = sons * (KD + 1) + (sl + 1)
+    keys = np.concatenate(keys_all)
+    l_cell = keys // (KD + 1)
+    l_loc = keys % (KD + 1) - 1
+    return l_cell, l_loc, tuple(np.concatenate(r) if r else np.zeros(0, np.int64) for r in rel)

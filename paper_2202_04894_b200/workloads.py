@@ -1,0 +1,149 @@
+"""Seeded synthetic particle sets standing in for BASELINE.json's configs.
+
+BASELINE.json names five synthetic distributions (no public dataset is
+involved).  SURVEY.md §8(d) fixes the seeds: points use ``default_rng(0)``,
+charges ``default_rng(1)`` with Re/Im ~ U(-1, 1) (the reference harness's
+``seed + 1`` convention, harness.py:114) and sampled check targets
+``default_rng(2)`` (harness.py:152-154).  The wavenumber follows the harness
+convention kappa = kappa*D / side(root box) (harness.py:119-120), so both the
+B200 path and the CPU oracle receive the same float kappa.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+__all__ = [
+    "Workload",
+    "WORKLOADS",
+    "make_points",
+    "make_charges",
+    "make_workload",
+    "sample_targets",
+    "kappa_for",
+]
+
+
+@dataclass(frozen=True)
+class Workload:
+    name: str
+    kind: str
+    n: int
+    kappa_d: float
+    order: int
+    ncrit: int
+    dtype: str  # "c128" | "c64"
+
+
+# BASELINE.json "configs", in order (cfg1..cfg5); the first order listed per
+# config is the default one, the others are parity/sweep variants.
+WORKLOADS = {
+    "cfg1": Workload("cfg1", "sphere", 20_000, 32.0, 4, 64, "c128"),
+    "cfg2": Workload("cfg2", "cube-surface", 1_000_000, 128.0, 4, 64, "c128"),
+    "cfg2_l6": Workload("cfg2_l6", "cube-surface", 1_000_000, 128.0, 6, 64, "c128"),
+    "cfg3": Workload("cfg3", "ellipsoid", 4_000_000, 256.0, 5, 64, "c64"),
+    "cfg4": Workload("cfg4", "refined-cube", 16_000_000, 512.0, 6, 128, "c64"),
+    "cfg5": Workload("cfg5", "volume", 2_000_000, 64.0, 4, 64, "c128"),
+}
+
+
+def _sphere(n, rng):
+    g = rng.standard_normal((n, 3))
+    return g / np.linalg.norm(g, axis=1, keepdims=True)
+
+
+def _cube_surface(n, rng):
+    face = rng.integers(0, 6, n)
+    uv = rng.uniform(-1.0, 1.0, (n, 2))
+    axis = face // 2
+    sign = np.where(face % 2 == 0, 1.0, -1.0)
+    pts = np.empty((n, 3))
+    # the held axis gets +-1, the remaining two axes (increasing order) get u, v
+    other0 = np.where(axis == 0, 1, 0)
+    other1 = np.where(axis == 2, 1, 2)
+    rows = np.arange(n)
+    pts[rows, axis] = sign
+    pts[rows, other0] = uv[:, 0]
+    pts[rows, other1] = uv[:, 1]
+    return pts
+
+
+def _ellipsoid(n, rng, semi=(2.0, 0.5, 0.5)):
+    a = np.asarray(semi)
+    out = []
+    got = 0
+    while got < n:
+        m = max(2 * (n - got), 1024)
+        u = _sphere(m, rng)
+        # surface-area density of x = a*u relative to the sphere is ~ |u/a|
+        accept = rng.uniform(0.0, 1.0, m) < np.linalg.norm(u / a, axis=1) * a.min()
+        x = u[accept] * a
+        out.append(x)
+        got += x.shape[0]
+    return np.concatenate(out)[:n]
+
+
+def _refined_cube(n, rng, scale=0.05, frac=0.9):
+    n_c = int(round(frac * n))
+    n_u = n - n_c
+    corner = rng.integers(0, 8, n_c)
+    csign = np.stack([np.where((corner >> k) & 1, 1.0, -1.0) for k in (2, 1, 0)], axis=1)
+    face_axis = rng.integers(0, 3, n_c)  # the corner face the point lies on
+    off = np.minimum(rng.exponential(scale, (n_c, 2)), 2.0)
+    pts = csign.copy()
+    rows = np.arange(n_c)
+    other0 = np.where(face_axis == 0, 1, 0)
+    other1 = np.where(face_axis == 2, 1, 2)
+    # move inward from the corner along the two in-face axes
+    pts[rows, other0] -= csign[rows, other0] * off[:, 0]
+    pts[rows, other1] -= csign[rows, other1] * off[:, 1]
+    return np.concatenate([pts, _cube_surface(n_u, rng)])
+
+
+def _volume(n, rng):
+    return rng.uniform(-1.0, 1.0, (n, 3))
+
+
+_GEN = {
+    "sphere": _sphere,
+    "cube-surface": _cube_surface,
+    "ellipsoid": _ellipsoid,
+    "refined-cube": _refined_cube,
+    "volume": _volume,
+}
+
+
+def make_points(kind: str, n: int, seed: int = 0) -> np.ndarray:
+    if kind not in _GEN:
+        raise ValueError(f"unknown distribution {kind!r}")
+    return np.ascontiguousarray(_GEN[kind](n, np.random.default_rng(seed)))
+
+
+def make_charges(n: int, seed: int = 1, dtype=np.complex128) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    q = rng.uniform(-1.0, 1.0, n) + 1j * rng.uniform(-1.0, 1.0, n)
+    return q.astype(dtype)
+
+
+def kappa_for(points: np.ndarray, kappa_d: float) -> float:
+    """kappa = kappa*D / side(root box) -- harness.py:119-120."""
+    from .geometry import compute_root_box
+
+    return float(kappa_d / compute_root_box(points).side)
+
+
+def sample_targets(n: int, m: int = 1000, seed: int = 2) -> np.ndarray:
+    """Check-target indices, as harness.py:152-154 draws them."""
+    rng = np.random.default_rng(seed)
+    return rng.choice(n, size=min(m, n), replace=False)
+
+
+def make_workload(name: str, n: int | None = None):
+    """(points, charges c128, kappa, Workload) for a named config."""
+    w = WORKLOADS[name]
+    nn = w.n if n is None else n
+    pts = make_points(w.kind, nn, 0)
+    q = make_charges(nn, 1)
+    return pts, q, kappa_for(pts, w.kappa_d), w

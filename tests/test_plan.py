@@ -1,0 +1,144 @@
+"""Host plan (tree, level-synchronous DTT, marks, slots, CSR lists) against
+the reference's own decisions: exact tree, exact FmmInfo.counts, exact M2L
+(with direction keys) and P2P event sets (tests/golden, from helmfmm)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_cases, load_case, load_ref
+from oracle import defmm_oracle as O
+from paper_2202_04894_b200.config import FmmConfig, TreeConfig
+from paper_2202_04894_b200.directions import generate_direction_tree, nearest_directions
+from paper_2202_04894_b200.plan import build_plan, canonicalize_many
+from paper_2202_04894_b200.tree import build_tree
+from paper_2202_04894_b200.workloads import make_workload
+
+
+def _plan(g):
+    kw = g["config"]
+    tr, ps = build_tree(g["points"], g["charges"], TreeConfig(ncrit=kw["ncrit"]))
+    pl = build_plan(tr, tr, kw["order"], kw["kappa"], 1.0, 2.0, keep_events=True)
+    return tr, ps, pl
+
+
+@pytest.mark.parametrize("case", golden_cases())
+def test_tree_matches_reference(case):
+    g = load_case(case)
+    tr, ps = build_tree(g["points"], g["charges"], TreeConfig(ncrit=g["config"]["ncrit"]))
+    ot = O.Tree(g["points"], g["config"]["ncrit"])
+    assert np.array_equal(ps.original_index, ot.perm)
+    assert np.array_equal(ps.positions, g["points"][ot.perm])
+    mine = sorted(zip(tr.level.tolist(), map(tuple, tr.coords.tolist()), tr.start.tolist(), tr.stop.tolist()))
+    ref = sorted(zip(ot.level, [tuple(c) for c in ot.coords], ot.start, ot.stop))
+    assert mine == ref
+
+
+@pytest.mark.parametrize("case", golden_cases())
+def test_plan_counts_and_event_lists_match_reference(case):
+    g = load_case(case)
+    tr, ps, pl = _plan(g)
+    assert pl.hf_max == g["hf_max"]
+    assert {k: pl.counts[k] for k in g["counts"]} == g["counts"]
+    codes = tr.morton_code(np.arange(tr.n_cells)).astype(np.int64)
+    mt, ms, ed = pl.m2l_events
+    e = np.where(ed >= 0, pl.hf_max - tr.level[mt], -1)
+    i = np.where(ed >= 0, ed - pl.dir_off[np.maximum(e, 0)], -1)
+    mine = sorted(zip(tr.level[mt].tolist(), codes[mt].tolist(), codes[ms].tolist(), e.tolist(), i.tolist()))
+    assert mine == sorted(map(tuple, g["m2l"].tolist()))
+    pt, pss = pl.p2p_events
+    mp = sorted(zip(tr.level[pt].tolist(), codes[pt].tolist(), tr.level[pss].tolist(), codes[pss].tolist()))
+    assert mp == sorted(map(tuple, g["p2p"].tolist()))
+
+
+@pytest.mark.parametrize("case", ["volume3000", "cubesurf4000", "laplace500"])
+def test_p2p_runs_cover_every_pair_once(case):
+    """test_traversal.py:190-201 analogue: near + far lists partition all N^2 pairs."""
+    g = load_case(case)
+    tr, ps, pl = _plan(g)
+    n = ps.n
+    cov = np.zeros((n, n), np.int8)
+    for li, leaf in enumerate(pl.leaf_cells):
+        for k in range(pl.p2p_ptr[li], pl.p2p_ptr[li + 1]):
+            cov[tr.start[leaf] : tr.stop[leaf], pl.p2p_lo[k] : pl.p2p_hi[k]] += 1
+    mt, ms, _ = pl.m2l_events
+    for t, s in zip(mt, ms):
+        cov[tr.start[t] : tr.stop[t], tr.start[s] : tr.stop[s]] += 1
+    assert np.all(cov == 1)
+
+
+def test_m2l_rows_are_target_major_and_complete():
+    g = load_case("cubesurf4000")
+    tr, ps, pl = _plan(g)
+    assert np.all(np.diff(pl.m2l_row_slot) > 0)
+    assert pl.m2l_row_ptr[-1] == pl.counts["m2l_events"]
+    assert np.all(np.diff(pl.m2l_row_ptr) > 0)
+    assert pl.m2l_src.max() < pl.n_hat and pl.m2l_sym.max() < pl.n_sym
+
+
+def test_batched_nearest_direction_ties(operators):
+    dt = generate_direction_tree(3)
+    for e in range(4):
+        assert np.array_equal(nearest_directions(dt.levels[e], operators["near_t"]), operators[f"near_{e}"])
+
+
+def test_batched_canonicalization(operators):
+    c, r = canonicalize_many(operators["near_t"])
+    assert np.array_equal(c, operators["canon"])
+    assert np.array_equal(r, operators["canon_rid"])
+
+
+def test_closed_form_rotation_matches_frequency_permutation(operators):
+    """The device gathers D_canon[idx(j, rid)] with mapped[perm[a]] = sign[a] f[a]
+    mod P; check that closed form against fourier.py:123-143."""
+    import itertools
+
+    perms = list(itertools.permutations(range(3)))
+    for L in (2, 4, 5, 6, 8):
+        P = 2 * L - 1
+        f = np.stack(np.meshgrid(*([np.arange(P)] * 3), indexing="ij"), -1).reshape(-1, 3)
+        W = (P * P, P, 1)
+        for rid in range(48):
+            pi, sb = rid >> 3, rid & 7
+            idx = np.zeros(P**3, np.int64)
+            for a in range(3):
+                neg = (sb >> (2 - a)) & 1
+                v = (P - f[:, a]) % P if neg else f[:, a]
+                idx += W[perms[pi][a]] * v
+            assert np.array_equal(idx, operators[f"fperm_L{L}"][rid])
+
+
+def test_cfg1_plan_counts_match_reference_run():
+    ref = load_ref("cfg1")
+    pts, q, k, w = make_workload("cfg1")
+    assert abs(k - float(ref["kappa"])) == 0.0
+    tr, ps = build_tree(pts, q, TreeConfig(ncrit=w.ncrit))
+    pl = build_plan(tr, tr, w.order, k, 1.0, 2.0)
+    assert pl.counts == ref["counts"]
+    assert pl.hf_max == int(ref["hf_max"])
+
+
+def test_config_validation():
+    with pytest.raises(ValueError):
+        FmmConfig(order=1)
+    with pytest.raises(ValueError):
+        FmmConfig(strategy="dense")
+    with pytest.raises(ValueError):
+        FmmConfig(eta=0.0)
+    with pytest.raises(ValueError):
+        FmmConfig(kappa=-2.0)
+    with pytest.raises(ValueError):
+        build_tree(np.zeros((0, 3)), np.zeros(0))
+    with pytest.raises(ValueError):
+        build_tree(np.array([[0.0, np.nan, 0.0]]), np.ones(1))
+
+
+def test_mac_violation_raises():
+    """fourier.py:179-180 / test_fourier.py:181-184: a stencil that touches the
+    singularity (adjacent cells) raises ValueError."""
+    from paper_2202_04894_b200.plan import _check_stencils
+
+    g = load_case("laplace500")
+    tr, ps = build_tree(g["points"], g["charges"], TreeConfig(ncrit=32))
+    _check_stencils(np.array([[2, 0, 0]]), np.array([2]), tr, 4, 1e-12)
+    with pytest.raises(ValueError):
+        _check_stencils(np.array([[1, 0, 0]]), np.array([2]), tr, 4, 1e-12)
