@@ -83,6 +83,24 @@ int defmm_m2l_c128(int32_t L, int64_t nrows, const int64_t* row_slot, const int6
                    const int32_t* e_src, const int32_t* e_sym, const int8_t* e_rid,
                    const void* hat, const void* sym, void* local, void* stream);
 
+/* K9b derived symbols -- fourier.py:186-196 (permute_symbol) materialised:
+ * sym_derived[i] = sym_canon[canon[i]] gathered through rotation rid[i]. */
+int defmm_expand_symbols_c128(int32_t L, int64_t n, const int32_t* canon, const int8_t* rid,
+                              const void* sym_canon, void* sym_derived, void* stream);
+
+/* rows per M2L group compiled for order L (8, 4 or 2) */
+int defmm_m2l_group_size(int32_t L);
+
+/* K7+K8 v2 (product path): grouped Hadamard M2L + fused F2L.  Group g owns
+ * the target rows grp_rows[G*g .. G*g+G) (-1 padded, G = defmm_m2l_group_size),
+ * siblings sharing a parent cell and a key.  Its runs [grp_ptr[g], grp_ptr[g+1])
+ * are records of G+2 int32: {source spectrum index, row mask, derived-symbol
+ * index for each row of the mask}, one per distinct source.
+ * local[grp_rows[..]] = F2L(sum D (*) hat). */
+int defmm_m2l_grouped_c128(int32_t L, int64_t ngroups, const int64_t* grp_rows,
+                           const int64_t* grp_ptr, const int32_t* runs, const void* hat,
+                           const void* sym_derived, void* local, void* stream);
+
 /* K5 L2L -- traversal.py:355-391 in gather form.
  * For i < n: local[out_slot[i]] += sum_{e in [ptr[i], ptr[i+1])}
  *   (C'0 (x) C'1 (x) C'2) local[src_slot[e]], C' the transposed/conjugate-

@@ -463,6 +463,167 @@ __global__ void __launch_bounds__(m2l_threads<L>()) m2l_kernel(
     }
 }
 
+// Derived symbols: D_t[j] = D_canon[perm_rid(j)] materialised once per plan so
+// that the M2L inner loop streams them with coalesced 16-B loads (the v1
+// in-loop gather cost ~20 L1 wavefronts per warp and event, see
+// profiles/r01_summary_v1.md).
+template <int L>
+__global__ void __launch_bounds__(256) expand_symbols_kernel(int64_t n, const int32_t* __restrict__ canon,
+                                                             const int8_t* __restrict__ rid,
+                                                             const double2* __restrict__ symc,
+                                                             double2* __restrict__ symd) {
+    constexpr int P = pad<L>(), P3 = P * P * P;
+    const int64_t i = blockIdx.x;
+    const int r = rid[i];
+    const int pi = r >> 3;
+    const int wt[3] = {P * P, P, 1};
+    int w[3], ng[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        w[a] = wt[c_perm[pi][a]];
+        ng[a] = (r >> (2 - a)) & 1;
+    }
+    const double2* src = symc + (int64_t)canon[i] * P3;
+    double2* dst = symd + i * P3;
+    for (int j = threadIdx.x; j < P3; j += blockDim.x) {
+        const int f[3] = {j / (P * P), (j / P) % P, j % P};
+        int idx = 0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) idx += w[a] * (ng[a] ? (f[a] ? P - f[a] : 0) : f[a]);
+        dst[j] = src[idx];
+    }
+}
+
+// M2L v2: one CTA per group of <= G target rows that share a parent cell and a
+// key (siblings), entries sorted by source so each source spectrum is loaded
+// once per group into registers; derived symbols streamed coalesced; G
+// register accumulators; F2L epilogue per row.  Entry = {src hat index,
+// translation id | a << 29} (a = row index inside the group).
+template <int L>
+__host__ __device__ constexpr int m2l_group_size() { return L <= 5 ? 8 : (L == 6 ? 4 : 2); }
+
+template <int L>
+__device__ __forceinline__ void f2l_row(const double2* tw, double2* X, double2* Z1, double2* out) {
+    constexpr int P = pad<L>(), L3 = cube<L>();
+    const int NT = blockDim.x;
+    for (int t = threadIdx.x; t < L * P * P; t += NT) {
+        const int a = t / (P * P), f12 = t % (P * P);
+        double2 v = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int f0 = 0; f0 < P; ++f0) v = cfma(X[f0 * P * P + f12], cconj(tw[(f0 * a) % P]), v);
+        Z1[t] = v;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < L * L * P; t += NT) {
+        const int a = t / (L * P), b = (t / P) % L, f2 = t % P;
+        double2 v = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int f1 = 0; f1 < P; ++f1) v = cfma(Z1[(a * P + f1) * P + f2], cconj(tw[(f1 * b) % P]), v);
+        X[t] = v;
+    }
+    __syncthreads();
+    const double scale = 1.0 / (P * sqrt((double)P));
+    for (int t = threadIdx.x; t < L3; t += NT) {
+        const int ab = t / L, c = t % L;
+        double2 v = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int f2 = 0; f2 < P; ++f2) v = cfma(X[ab * P + f2], cconj(tw[(f2 * c) % P]), v);
+        out[t] = cscale(v, scale);
+    }
+}
+
+// Run record of the grouped M2L: {source spectrum index, target mask, G
+// derived-symbol ids (one per row of the group; unused where the mask bit is 0)}.
+template <int L>
+__host__ __device__ constexpr int m2l_run_words() { return m2l_group_size<L>() + 2; }
+
+template <int L>
+__global__ void __launch_bounds__(m2l_threads<L>()) m2l_grouped_kernel(
+    int64_t ngroups, const int64_t* __restrict__ grp_rows, const int64_t* __restrict__ grp_ptr,
+    const int32_t* __restrict__ runs, const double2* __restrict__ hat, const double2* __restrict__ symd,
+    double2* __restrict__ local) {
+    constexpr int P = pad<L>(), L3 = cube<L>(), P3 = P * P * P;
+    constexpr int NT = m2l_threads<L>();
+    constexpr int PER = (P3 + NT - 1) / NT;
+    constexpr int G = m2l_group_size<L>();
+    constexpr int W = m2l_run_words<L>();
+    constexpr int CHUNK = 128;  // run records staged in shared memory per pass
+    extern __shared__ double2 sm[];
+    double2* tw = sm;
+    double2* X = tw + P;
+    double2* Z1 = X + P3;
+    int32_t* rec = reinterpret_cast<int32_t*>(Z1 + L * P * P);  // CHUNK * W ints
+    const int64_t g = blockIdx.x;
+    make_twiddles<P>(tw);
+    double2 acc[G][PER];
+#pragma unroll
+    for (int k = 0; k < G; ++k)
+#pragma unroll
+        for (int m = 0; m < PER; ++m) acc[k][m] = make_double2(0.0, 0.0);
+    const int64_t r0 = grp_ptr[g], r1 = grp_ptr[g + 1];
+    for (int64_t cb = r0; cb < r1; cb += CHUNK) {
+        const int n = (int)((r1 - cb) < CHUNK ? (r1 - cb) : CHUNK);
+        __syncthreads();
+        for (int t = threadIdx.x; t < n * W; t += NT) rec[t] = runs[cb * W + t];
+        __syncthreads();
+        double2 S[PER], Sn[PER];
+        {
+            const double2* Sp = hat + (int64_t)rec[0] * P3;
+#pragma unroll
+            for (int m = 0; m < PER; ++m) {
+                const int j = threadIdx.x + m * NT;
+                S[m] = j < P3 ? __ldg(Sp + j) : make_double2(0.0, 0.0);
+            }
+        }
+        for (int r = 0; r < n; ++r) {
+            const int32_t* rr = rec + r * W;
+            const unsigned mask = (unsigned)rr[1];
+            // prefetch the next source spectrum
+            if (r + 1 < n) {
+                const double2* Sp = hat + (int64_t)rr[W] * P3;
+#pragma unroll
+                for (int m = 0; m < PER; ++m) {
+                    const int j = threadIdx.x + m * NT;
+                    Sn[m] = j < P3 ? __ldg(Sp + j) : make_double2(0.0, 0.0);
+                }
+            }
+            // all symbol loads of this run in flight together
+            double2 D[G][PER];
+#pragma unroll
+            for (int k = 0; k < G; ++k) {
+                const double2* Dp = symd + (int64_t)rr[2 + k] * P3;
+#pragma unroll
+                for (int m = 0; m < PER; ++m) {
+                    const int j = threadIdx.x + m * NT;
+                    D[k][m] = ((mask >> k) & 1) && j < P3 ? __ldg(Dp + j) : make_double2(0.0, 0.0);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < G; ++k) {
+                if ((mask >> k) & 1) {
+#pragma unroll
+                    for (int m = 0; m < PER; ++m) acc[k][m] = cfma(D[k][m], S[m], acc[k][m]);
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < PER; ++m) S[m] = Sn[m];
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+        const int64_t row = grp_rows[g * G + k];
+        if (row < 0) break;
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < PER; ++m) {
+            const int j = threadIdx.x + m * NT;
+            if (j < P3) X[j] = acc[k][m];
+        }
+        __syncthreads();
+        f2l_row<L>(tw, X, Z1, local + row * L3);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K3: L2P + near-field add + un-permute.  One CTA per target leaf, one thread
 // per particle; L2P(x) = sum_abc loc[abc] conj(W0_a W1_b W2_c) with the same
@@ -748,6 +909,39 @@ int defmm_m2l_c128(int32_t L, int64_t nrows, const int64_t* row_slot, const int6
             (double2*)local);
     });
     return report(cudaGetLastError(), "m2l");
+}
+
+int defmm_expand_symbols_c128(int32_t L, int64_t n, const int32_t* canon, const int8_t* rid, const void* sym_canon,
+                               void* sym_derived, void* stream) {
+    if (n == 0) return 0;
+    if (!grid_ok(n)) return -1;
+    cudaStream_t s = (cudaStream_t)stream;
+    DEFMM_DISPATCH_L(L, (expand_symbols_kernel<LL><<<(unsigned)n, 256, 0, s>>>(
+                            n, canon, rid, (const double2*)sym_canon, (double2*)sym_derived)));
+    return report(cudaGetLastError(), "expand_symbols");
+}
+
+int defmm_m2l_group_size(int32_t L) {
+    int g = -3;
+    DEFMM_DISPATCH_L(L, g = m2l_group_size<LL>());
+    return g;
+}
+
+int defmm_m2l_grouped_c128(int32_t L, int64_t ngroups, const int64_t* grp_rows, const int64_t* grp_ptr,
+                           const int32_t* runs, const void* hat, const void* sym_derived, void* local,
+                           void* stream) {
+    if (ngroups == 0) return 0;
+    if (!grid_ok(ngroups)) return -1;
+    cudaStream_t s = (cudaStream_t)stream;
+    DEFMM_DISPATCH_L(L, {
+        constexpr int P = 2 * LL - 1;
+        const size_t bytes = sizeof(double2) * (P + P * P * P + LL * P * P) + sizeof(int32_t) * 128 * m2l_run_words<LL>();
+        int rc = set_smem(m2l_grouped_kernel<LL>, bytes);
+        if (rc) return rc;
+        m2l_grouped_kernel<LL><<<(unsigned)ngroups, m2l_threads<LL>(), bytes, s>>>(
+            ngroups, grp_rows, grp_ptr, runs, (const double2*)hat, (const double2*)sym_derived, (double2*)local);
+    });
+    return report(cudaGetLastError(), "m2l_grouped");
 }
 
 int defmm_l2p_c128(int32_t L, int64_t n, const int32_t* leaf_cell, const int64_t* slot_lo, const int64_t* slot_hi,

@@ -99,7 +99,15 @@ class FmmPlan:
             self.m2m.append((float(st.side_at(lev + 1)), _dev(slots, i64, d), _dev(p.m_dir[slots], i32, d),
                              _dev(son_slot, i64, d), int(slots.shape[0])))
         self.hat_slot = _dev(p.hat_slot, i64, d)
-        # M2L
+        # M2L (v2: sibling groups over derived symbols)
+        G = int(_lib.load().defmm_m2l_group_size(L))
+        if G != p.group_size:
+            raise _lib.DefmmLibraryError(f"library M2L group size {G} != plan {p.group_size}")
+        self.grp_rows = _dev(p.grp_rows.reshape(-1), i64, d)
+        self.grp_ptr = _dev(p.grp_ptr, i64, d)
+        self.grp_runs = _dev(p.grp_runs.reshape(-1), i32, d)
+        self.n_groups = int(p.grp_rows.shape[0])
+        # v1 row CSR (kept for the operator tests)
         self.row_slot = _dev(p.m2l_row_slot, i64, d)
         self.row_ptr = _dev(p.m2l_row_ptr, i64, d)
         self.e_src = _dev(p.m2l_src, i32, d)
@@ -128,6 +136,7 @@ class FmmPlan:
         self.q = torch.zeros(self.n_src, dtype=c128, device=d)
         self.out = torch.empty(self.n_tgt, dtype=c128, device=d)
         self.side_stream = torch.cuda.Stream(device=d)
+        self.m2l_variant = "grouped"
 
     def _symbols(self):
         p = self.plan
@@ -135,7 +144,13 @@ class FmmPlan:
         if p.n_sym:
             tv = _dev(p.sym_tvec.reshape(-1), torch.int32, self.device)
             beta = _dev(p.sym_beta, torch.float64, self.device)
-            _lib.call("defmm_symbols_c128", self.L, p.n_sym, tv, beta, float(p.kappa), self.sym,
+            st = torch.cuda.current_stream(self.device).cuda_stream
+            _lib.call("defmm_symbols_c128", self.L, p.n_sym, tv, beta, float(p.kappa), self.sym, st)
+        n_tr = int(p.trans_canon.shape[0])
+        self.sym_derived = torch.empty((max(n_tr, 1), self.P3), dtype=torch.complex128, device=self.device)
+        if n_tr:
+            _lib.call("defmm_expand_symbols_c128", self.L, n_tr, _dev(p.trans_canon, torch.int32, self.device),
+                      _dev(p.trans_rid, torch.int8, self.device), self.sym, self.sym_derived,
                       torch.cuda.current_stream(self.device).cuda_stream)
 
     # ------------------------------------------------------------------
@@ -190,8 +205,12 @@ class FmmPlan:
             stage_events.append(("upward", a, b))
         # M2L (+ fused F2L) into the local slots
         self.local.zero_()
-        _lib.call("defmm_m2l_c128", L, self.row_slot.shape[0], self.row_slot, self.row_ptr, self.e_src,
-                  self.e_sym, self.e_rid, self.hat, self.sym, self.local, sh)
+        if self.m2l_variant == "rows":
+            _lib.call("defmm_m2l_c128", L, self.row_slot.shape[0], self.row_slot, self.row_ptr, self.e_src,
+                      self.e_sym, self.e_rid, self.hat, self.sym, self.local, sh)
+        else:
+            _lib.call("defmm_m2l_grouped_c128", L, self.n_groups, self.grp_rows, self.grp_ptr, self.grp_runs,
+                      self.hat, self.sym_derived, self.local, sh)
         if stage_events is not None:
             c = ev()
             c.record(stream)
