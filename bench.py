@@ -42,6 +42,7 @@ def _args():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=20000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--m2l", default=None, help="M2L kernel variant (rows | rows_derived | grouped)")
     return ap.parse_args()
 
 
@@ -188,6 +189,8 @@ def run_b200(args):
     t0 = time.perf_counter()
     plan = FmmPlan(pts, None, cfg, device=dev, charges=q)
     setup_s = time.perf_counter() - t0
+    if args.m2l:
+        plan.m2l_variant = args.m2l
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
 

@@ -101,6 +101,13 @@ int defmm_m2l_grouped_c128(int32_t L, int64_t ngroups, const int64_t* grp_rows,
                            const int64_t* grp_ptr, const int32_t* runs, const void* hat,
                            const void* sym_derived, void* local, void* stream);
 
+/* K7+K8 v1b: row-major Hadamard M2L over derived symbols + fused F2L.  Row r
+ * (target slot row_slot[r]) owns entries [row_ptr[r], row_ptr[r+1]), int32
+ * pairs {source spectrum index, derived-symbol index}. */
+int defmm_m2l_rows_c128(int32_t L, int64_t nrows, const int64_t* row_slot, const int64_t* row_ptr,
+                        const int32_t* entries, const void* hat, const void* sym_derived,
+                        void* local, void* stream);
+
 /* K5 L2L -- traversal.py:355-391 in gather form.
  * For i < n: local[out_slot[i]] += sum_{e in [ptr[i], ptr[i+1])}
  *   (C'0 (x) C'1 (x) C'2) local[src_slot[e]], C' the transposed/conjugate-

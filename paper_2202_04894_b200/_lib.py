@@ -31,6 +31,7 @@ _SIGS = {
     "defmm_expand_symbols_c128": [_i32, _i64, _vp, _vp, _vp, _vp, _vp],
     "defmm_m2l_group_size": [_i32],
     "defmm_m2l_grouped_c128": [_i32, _i64] + [_vp] * 7,
+    "defmm_m2l_rows_c128": [_i32, _i64] + [_vp] * 7,
     "defmm_l2l_c128": [_i32, _i64, _vp, _vp, _vp, _vp, _vp, _f64, _vp, _f64, _vp, _vp],
     "defmm_l2p_c128": [_i32, _i64] + [_vp] * 13 + [_f64, _vp, _vp, _vp, _vp, _vp],
     "defmm_p2p_c128": [_i64] + [_vp] * 12 + [_f64, _f64, _vp, _vp],

@@ -49,6 +49,18 @@ __device__ __forceinline__ double2 cexpi(double ph) {
     return make_double2(c, s);
 }
 
+// Predicated 16-B read-only load that the compiler cannot sink below later
+// code: keeps all loads of an M2L run in flight together.
+__device__ __forceinline__ double2 ldg_pred(const double2* p, bool pred) {
+    double2 v;
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\tmov.f64 %0, 0d0000000000000000;\n\t"
+        "mov.f64 %1, 0d0000000000000000;\n\t@q ld.global.nc.v2.f64 {%0, %1}, [%2];\n\t}"
+        : "=d"(v.x), "=d"(v.y)
+        : "l"(p), "r"((int)pred));
+    return v;
+}
+
 // Equispaced nodes x_j = j/(L-1) (interpolation.py:51-56) and the Lagrange
 // cardinal functions S_k(x) = prod_{j != k} (x - x_j)/(x_k - x_j) (:59-69).
 template <int L>
@@ -532,6 +544,62 @@ __device__ __forceinline__ void f2l_row(const double2* tw, double2* X, double2* 
     }
 }
 
+// M2L v1b: one CTA per target row (high occupancy), derived symbols streamed
+// coalesced; two entries in flight per iteration.
+template <int L>
+__global__ void __launch_bounds__(m2l_threads<L>()) m2l_rows_kernel(
+    int64_t nrows, const int64_t* __restrict__ row_slot, const int64_t* __restrict__ row_ptr,
+    const int2* __restrict__ ent, const double2* __restrict__ hat, const double2* __restrict__ symd,
+    double2* __restrict__ local) {
+    constexpr int P = pad<L>(), L3 = cube<L>(), P3 = P * P * P;
+    constexpr int NT = m2l_threads<L>();
+    constexpr int PER = (P3 + NT - 1) / NT;
+    extern __shared__ double2 sm[];
+    double2* tw = sm;
+    double2* X = tw + P;
+    double2* Z1 = X + P3;
+    const int64_t row = blockIdx.x;
+    make_twiddles<P>(tw);
+    double2 acc[PER], acc2[PER];
+#pragma unroll
+    for (int m = 0; m < PER; ++m) acc[m] = acc2[m] = make_double2(0.0, 0.0);
+    const int64_t e0 = row_ptr[row], e1 = row_ptr[row + 1];
+    int64_t e = e0;
+    for (; e + 2 <= e1; e += 2) {
+        const int2 a = ent[e], b = ent[e + 1];
+        const double2* Sa = hat + (int64_t)a.x * P3;
+        const double2* Da = symd + (int64_t)a.y * P3;
+        const double2* Sb = hat + (int64_t)b.x * P3;
+        const double2* Db = symd + (int64_t)b.y * P3;
+#pragma unroll
+        for (int m = 0; m < PER; ++m) {
+            const int j = threadIdx.x + m * NT;
+            if (j < P3) {
+                const double2 sa = __ldg(Sa + j), da = __ldg(Da + j), sb = __ldg(Sb + j), db = __ldg(Db + j);
+                acc[m] = cfma(da, sa, acc[m]);
+                acc2[m] = cfma(db, sb, acc2[m]);
+            }
+        }
+    }
+    if (e < e1) {
+        const int2 a = ent[e];
+        const double2* Sa = hat + (int64_t)a.x * P3;
+        const double2* Da = symd + (int64_t)a.y * P3;
+#pragma unroll
+        for (int m = 0; m < PER; ++m) {
+            const int j = threadIdx.x + m * NT;
+            if (j < P3) acc[m] = cfma(__ldg(Da + j), __ldg(Sa + j), acc[m]);
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < PER; ++m) {
+        const int j = threadIdx.x + m * NT;
+        if (j < P3) X[j] = cadd(acc[m], acc2[m]);
+    }
+    __syncthreads();
+    f2l_row<L>(tw, X, Z1, local + row_slot[row] * L3);
+}
+
 // Run record of the grouped M2L: {source spectrum index, target mask, G
 // derived-symbol ids (one per row of the group; unused where the mask bit is 0)}.
 template <int L>
@@ -579,15 +647,7 @@ __global__ void __launch_bounds__(m2l_threads<L>()) m2l_grouped_kernel(
             const int32_t* rr = rec + r * W;
             const unsigned mask = (unsigned)rr[1];
             // prefetch the next source spectrum
-            if (r + 1 < n) {
-                const double2* Sp = hat + (int64_t)rr[W] * P3;
-#pragma unroll
-                for (int m = 0; m < PER; ++m) {
-                    const int j = threadIdx.x + m * NT;
-                    Sn[m] = j < P3 ? __ldg(Sp + j) : make_double2(0.0, 0.0);
-                }
-            }
-            // all symbol loads of this run in flight together
+            // all symbol loads of this run + the next source in flight together
             double2 D[G][PER];
 #pragma unroll
             for (int k = 0; k < G; ++k) {
@@ -595,9 +655,23 @@ __global__ void __launch_bounds__(m2l_threads<L>()) m2l_grouped_kernel(
 #pragma unroll
                 for (int m = 0; m < PER; ++m) {
                     const int j = threadIdx.x + m * NT;
-                    D[k][m] = ((mask >> k) & 1) && j < P3 ? __ldg(Dp + j) : make_double2(0.0, 0.0);
+                    D[k][m] = ldg_pred(Dp + j, ((mask >> k) & 1) && j < P3);
                 }
             }
+            {
+                const bool more = r + 1 < n;
+                const double2* Sp = hat + (int64_t)(more ? rr[W] : 0) * P3;
+#pragma unroll
+                for (int m = 0; m < PER; ++m) {
+                    const int j = threadIdx.x + m * NT;
+                    Sn[m] = ldg_pred(Sp + j, more && j < P3);
+                }
+            }
+            // register fence: every D load above is issued before any FMA below
+#pragma unroll
+            for (int k = 0; k < G; ++k)
+#pragma unroll
+                for (int m = 0; m < PER; ++m) asm volatile("" : "+d"(D[k][m].x), "+d"(D[k][m].y));
 #pragma unroll
             for (int k = 0; k < G; ++k) {
                 if ((mask >> k) & 1) {
@@ -942,6 +1016,24 @@ int defmm_m2l_grouped_c128(int32_t L, int64_t ngroups, const int64_t* grp_rows, 
             ngroups, grp_rows, grp_ptr, runs, (const double2*)hat, (const double2*)sym_derived, (double2*)local);
     });
     return report(cudaGetLastError(), "m2l_grouped");
+}
+
+int defmm_m2l_rows_c128(int32_t L, int64_t nrows, const int64_t* row_slot, const int64_t* row_ptr,
+                        const int32_t* entries, const void* hat, const void* sym_derived, void* local,
+                        void* stream) {
+    if (nrows == 0) return 0;
+    if (!grid_ok(nrows)) return -1;
+    cudaStream_t s = (cudaStream_t)stream;
+    DEFMM_DISPATCH_L(L, {
+        constexpr int P = 2 * LL - 1;
+        const size_t bytes = sizeof(double2) * (P + P * P * P + LL * P * P);
+        int rc = set_smem(m2l_rows_kernel<LL>, bytes);
+        if (rc) return rc;
+        m2l_rows_kernel<LL><<<(unsigned)nrows, m2l_threads<LL>(), bytes, s>>>(
+            nrows, row_slot, row_ptr, (const int2*)entries, (const double2*)hat, (const double2*)sym_derived,
+            (double2*)local);
+    });
+    return report(cudaGetLastError(), "m2l_rows");
 }
 
 int defmm_l2p_c128(int32_t L, int64_t n, const int32_t* leaf_cell, const int64_t* slot_lo, const int64_t* slot_hi,

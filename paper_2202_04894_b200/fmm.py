@@ -113,6 +113,7 @@ class FmmPlan:
         self.e_src = _dev(p.m2l_src, i32, d)
         self.e_sym = _dev(p.m2l_sym, i32, d)
         self.e_rid = _dev(p.m2l_rid, torch.int8, d)
+        self.row_entries = _dev(p.m2l_rows_entries.reshape(-1), i32, d)
         # downward
         self.l2l = []
         for lev, outs, octant, ptr, src, sdir in p.l2l_levels:
@@ -136,7 +137,7 @@ class FmmPlan:
         self.q = torch.zeros(self.n_src, dtype=c128, device=d)
         self.out = torch.empty(self.n_tgt, dtype=c128, device=d)
         self.side_stream = torch.cuda.Stream(device=d)
-        self.m2l_variant = "grouped"
+        self.m2l_variant = "rows_derived"
 
     def _symbols(self):
         p = self.plan
@@ -205,7 +206,10 @@ class FmmPlan:
             stage_events.append(("upward", a, b))
         # M2L (+ fused F2L) into the local slots
         self.local.zero_()
-        if self.m2l_variant == "rows":
+        if self.m2l_variant == "rows_derived":
+            _lib.call("defmm_m2l_rows_c128", L, self.row_slot.shape[0], self.row_slot, self.row_ptr,
+                      self.row_entries, self.hat, self.sym_derived, self.local, sh)
+        elif self.m2l_variant == "rows":
             _lib.call("defmm_m2l_c128", L, self.row_slot.shape[0], self.row_slot, self.row_ptr, self.e_src,
                       self.e_sym, self.e_rid, self.hat, self.sym, self.local, sh)
         else:

@@ -137,6 +137,7 @@ class Plan:
     m2l_sym: np.ndarray = None
     m2l_rid: np.ndarray = None
     m2l_level: np.ndarray = None  # per row
+    m2l_rows_entries: np.ndarray = None  # (n_m2l, 2) int32 {hat, derived symbol} in row order
     l2l_levels: list = None  # [(son level, out_slot, octant, ptr, src_slot, src_dir)]
     leaf_cells: np.ndarray = None  # target-tree leaves
     leaf_slot_lo: np.ndarray = None
@@ -360,6 +361,10 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
     plan.m2l_src = src_hat[order_ev].astype(np.int32)
     plan.m2l_sym = ev_sym[order_ev]
     plan.m2l_rid = ev_rid[order_ev]
+    ent = np.empty((n_m2l, 2), np.int32)
+    ent[:, 0] = src_hat[order_ev]
+    ent[:, 1] = inv[order_ev]
+    plan.m2l_rows_entries = ent
     plan.m2l_level = tt.level[l_cell[rows]]
     # derived-symbol table (one per distinct (level, t)) and sibling groups
     plan.trans_canon = cinv.astype(np.int32)

@@ -125,6 +125,9 @@ def test_m2l_v1_rows_and_v2_groups_agree(case):
     plan.m2l_variant = "grouped"
     b = plan.apply().cpu().numpy()
     assert _rel(b, a) <= 1e-13
+    plan.m2l_variant = "rows_derived"
+    c = plan.apply().cpu().numpy()
+    assert _rel(c, a) <= 1e-13
     assert _rel(b, g["pot"]) <= FP64_TOL
 
 
