@@ -777,12 +777,12 @@ constexpr int P2P_TILE = 256;
 __device__ __forceinline__ double2 helm_pair(double dx, double dy, double dz, double2 qs, double kpi,
                                              double tol) {
     const double r2 = dx * dx + dy * dy + dz * dz;
-    const double r = sqrt(r2);
-    const bool ok = r >= tol;
-    const double rr = ok ? r : 1.0;
+    const double rinv = rsqrt(r2);  // r2 = 0 -> inf -> r = NaN -> masked below
+    const double r = r2 * rinv;
+    const bool ok = r >= tol;     // kernel.py:40-43 singularity suppression
     double s, c;
-    sincospi(kpi * rr, &s, &c);
-    const double g = ok ? (1.0 / (4.0 * 3.141592653589793)) / rr : 0.0;
+    sincospi(kpi * (ok ? r : 0.0), &s, &c);
+    const double g = ok ? rinv * (1.0 / (4.0 * 3.141592653589793)) : 0.0;
     const double gr = g * c, gi = g * s;
     return make_double2(gr * qs.x - gi * qs.y, gr * qs.y + gi * qs.x);
 }

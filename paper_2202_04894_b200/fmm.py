@@ -175,20 +175,6 @@ class FmmPlan:
         sh = stream.cuda_stream
         out = self.out if out is None else out
         ev = (lambda: torch.cuda.Event(enable_timing=True)) if stage_events is not None else None
-        # near field on the side stream, concurrent with the far field
-        side = self.side_stream
-        side.wait_stream(stream)
-        with torch.cuda.stream(side):
-            if stage_events is not None:
-                e0 = ev()
-                e0.record(side)
-            _lib.call("defmm_p2p_c128", p.leaf_cells.shape[0], self.tgt_lo, self.tgt_hi, self.p2p_ptr,
-                      self.p2p_lo, self.p2p_hi, *self.t_xyz, *self.s_xyz, self.q, kappa, float(p.tol),
-                      self.near, side.cuda_stream)
-            if stage_events is not None:
-                e1 = ev()
-                e1.record(side)
-                stage_events.append(("p2p", e0, e1))
         sg, tg = self.sg, self.tg
         if stage_events is not None:
             a = ev()
@@ -204,6 +190,21 @@ class FmmPlan:
             b = ev()
             b.record(stream)
             stage_events.append(("upward", a, b))
+        # near field on the side stream, concurrent with the (L2-bound) M2L:
+        # P2P is FP64-pipe bound, so the two overlap on the SMs
+        side = self.side_stream
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            if stage_events is not None:
+                e0 = ev()
+                e0.record(side)
+            _lib.call("defmm_p2p_c128", p.leaf_cells.shape[0], self.tgt_lo, self.tgt_hi, self.p2p_ptr,
+                      self.p2p_lo, self.p2p_hi, *self.t_xyz, *self.s_xyz, self.q, kappa, float(p.tol),
+                      self.near, side.cuda_stream)
+            if stage_events is not None:
+                e1 = ev()
+                e1.record(side)
+                stage_events.append(("p2p", e0, e1))
         # M2L (+ fused F2L) into the local slots
         self.local.zero_()
         if self.m2l_variant == "rows_derived":
