@@ -42,13 +42,17 @@ def _args():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=20000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--m2l", default=None, help="M2L kernel variant (rows | rows_derived | grouped)")
+    ap.add_argument("--dtype", default=None, choices=[None, "c128", "c64"], help="override the workload dtype")
+    ap.add_argument("--m2l", default=None, help="M2L kernel variant (derived | canonical)")
     return ap.parse_args()
 
 
-def _workload_desc(w, n):
+def _workload_desc(w, n, dtype=None):
+    dtype = dtype or w.dtype
     return {
-        "workload": f"{w.name}: N={n} {w.kind}, kappa*D={w.kappa_d:g}, L={w.order}, ncrit={w.ncrit}, complex128",
+        "workload": f"{w.name}: N={n} {w.kind}, kappa*D={w.kappa_d:g}, L={w.order}, ncrit={w.ncrit}, "
+                    f"{'complex128' if dtype == 'c128' else 'complex64'}",
+        "dtype": dtype,
         "N": n,
         "kappa_d": w.kappa_d,
         "order": w.order,
@@ -185,7 +189,8 @@ def run_b200(args):
 
     pts, q, kappa, w = make_workload(args.workload)
     n = pts.shape[0]
-    cfg = FmmConfig(order=w.order, ncrit=w.ncrit, kappa=kappa)
+    dtype = args.dtype or w.dtype
+    cfg = FmmConfig(order=w.order, ncrit=w.ncrit, kappa=kappa, dtype=dtype)
     t0 = time.perf_counter()
     plan = FmmPlan(pts, None, cfg, device=dev, charges=q)
     setup_s = time.perf_counter() - t0
@@ -231,8 +236,8 @@ def run_b200(args):
     value = world * n / (t_step / 1e3)  # replicas: every rank runs the full matvec
 
     # --- end to end through the public plan API with host buffers -------
-    q_host = torch.as_tensor(q).pin_memory()
-    out_host = torch.empty(n, dtype=torch.complex128).pin_memory()
+    q_host = torch.as_tensor(q).to(plan.cdtype).pin_memory()
+    out_host = torch.empty(n, dtype=plan.cdtype).pin_memory()
     for _ in range(max(1, args.warmup)):
         plan.set_charges(q_host.to(dev, non_blocking=True))
         out_host.copy_(plan.apply(), non_blocking=True)
@@ -270,7 +275,7 @@ def run_b200(args):
     p = plan.plan
     L = w.order
     P3 = (2 * L - 1) ** 3
-    c = 16
+    c = 16 if dtype == "c128" else 8
     n_m2l = p.counts["m2l_events"]
     rows = p.m2l_row_slot.shape[0]
     alg_bytes = n_m2l * 2 * P3 * c + rows * L**3 * c  # symbol + source spectrum per event, local write
@@ -288,9 +293,9 @@ def run_b200(args):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f64",
+        "dtype": "f64" if dtype == "c128" else "f32 (FP64 sums)",
         "data": "synthetic",
-        "config": dict(_workload_desc(w, n), l2_flush="256 MiB memset between timed iterations",
+        "config": dict(_workload_desc(w, n, dtype), l2_flush="256 MiB memset between timed iterations",
                        parallelism=f"replicas{world}" if world > 1 else "single"),
         "stages_ms": {"upward": up_ms / K, "m2l": m2l_ms / K, "p2p_concurrent": p2p_ms / K,
                       "downward": down_ms / K},
@@ -298,8 +303,8 @@ def run_b200(args):
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None,
                      "alg_bytes_per_launch": alg_bytes, "kernel_ms": m2l_s * 1e3},
-        "e2e": {"value": world * n / (e_step / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(n * 16),
-                "d2h_bytes_per_step": int(n * 16), "ms_per_step": e_step},
+        "e2e": {"value": world * n / (e_step / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(n * c),
+                "d2h_bytes_per_step": int(n * c), "ms_per_step": e_step},
         "accuracy": {"rel_l2_vs_direct_1000": eps},
         "gpu_launches": int(args.steps * plan.launches_per_apply),
         "clocks": clk,

@@ -42,104 +42,106 @@ int defmm_tree_fetch(const defmm_tree* t, int64_t* perm, double* sorted_pts, int
                      int64_t* coords, int64_t* start, int64_t* stop, int64_t* parent);
 void defmm_tree_free(defmm_tree* t);
 
-/* ---- device operators (complex128) --------------------------------------
+/* ---- device operators ------------------------------------------------------
+ * Every operator exists as *_c128 (complex arrays are double2 = interleaved
+ * FP64 re/im, exactly the reference's complex128) and *_c64 (float2; phases,
+ * coordinate differences and the M2L/L2P/P2P accumulations stay FP64).
  * Shared geometry arrays: cell_alpha[ncell*3] lower corners, cell_level[ncell],
  * level_beta[depth+1] side lengths, cell_start/stop particle ranges (sorted
  * order), dirs[ndir*3] unit directions (global ids; -1 = low frequency),
- * particles px/py/pz (sorted order), q (double2). */
-
-/* K2 P2M -- interpolation.py:109-124 via traversal.py:224-236.
- * For i < n: mult[out_slot[i]] = P2M(cell[i], direction dir[i]). */
-int defmm_p2m_c128(int32_t L, int64_t n, const int32_t* cell, const int32_t* dir,
-                   const int64_t* out_slot, const int64_t* cell_start, const int64_t* cell_stop,
-                   const double* cell_alpha, const int32_t* cell_level, const double* level_beta,
-                   const double* dirs, const double* px, const double* py, const double* pz,
-                   const void* q, double kappa, void* mult, void* stream);
-
-/* K4 M2M -- traversal.py:239-280 + interpolation.py:140-200.
- * For i < n: mult[out_slot[i]] = sum over octants o with son_slot[8i+o] >= 0
- * of (C0 (x) C1 (x) C2) mult[son_slot[8i+o]], C the modulated per-axis factors
- * (dir[i] < 0: plain Lagrange factors).  son_beta = side of the son level. */
-int defmm_m2m_c128(int32_t L, int64_t n, const int64_t* out_slot, const int32_t* dir,
-                   const int64_t* son_slot, double son_beta, const double* dirs, double kappa,
-                   void* mult, void* stream);
-
-/* K6 M2F -- fourier.py:67-72 (pad L^3 -> P^3 corner, fftn / P^1.5).
- * For i < n: hat[i] = M2F(mult[src_slot[i]]). */
-int defmm_m2f_c128(int32_t L, int64_t n, const int64_t* src_slot, const void* mult, void* hat,
-                   void* stream);
-
-/* K9 symbols -- fourier.py:156-183 (unnormalised fftn of G(beta (t + z))).
- * For i < n: sym[i] = symbol(t = tvec[3i..3i+2], beta[i]). */
-int defmm_symbols_c128(int32_t L, int64_t n, const int32_t* tvec, const double* beta,
-                       double kappa, void* sym, void* stream);
-
-/* K7+K8 Hadamard M2L + fused F2L -- traversal.py:320-342 (m2l_hadamard,
- * fourier.py:83-87) and traversal.py:405-414 (f2l, fourier.py:74-80).
- * For row r < nrows: local[row_slot[r]] = F2L( sum_{e in [row_ptr[r], row_ptr[r+1])}
- *   Dperm(sym[e_sym[e]], e_rid[e]) (*) hat[e_src[e]] ), Dperm = canonical symbol
- * gathered through the 48-element cube-group frequency map (fourier.py:123-143). */
-int defmm_m2l_c128(int32_t L, int64_t nrows, const int64_t* row_slot, const int64_t* row_ptr,
-                   const int32_t* e_src, const int32_t* e_sym, const int8_t* e_rid,
-                   const void* hat, const void* sym, void* local, void* stream);
-
-/* K9b derived symbols -- fourier.py:186-196 (permute_symbol) materialised:
- * sym_derived[i] = sym_canon[canon[i]] gathered through rotation rid[i]. */
-int defmm_expand_symbols_c128(int32_t L, int64_t n, const int32_t* canon, const int8_t* rid,
-                              const void* sym_canon, void* sym_derived, void* stream);
-
-/* rows per M2L group compiled for order L (8, 4 or 2) */
-int defmm_m2l_group_size(int32_t L);
-
-/* K7+K8 v2 (product path): grouped Hadamard M2L + fused F2L.  Group g owns
- * the target rows grp_rows[G*g .. G*g+G) (-1 padded, G = defmm_m2l_group_size),
- * siblings sharing a parent cell and a key.  Its runs [grp_ptr[g], grp_ptr[g+1])
- * are records of G+2 int32: {source spectrum index, row mask, derived-symbol
- * index for each row of the mask}, one per distinct source.
- * local[grp_rows[..]] = F2L(sum D (*) hat). */
-int defmm_m2l_grouped_c128(int32_t L, int64_t ngroups, const int64_t* grp_rows,
-                           const int64_t* grp_ptr, const int32_t* runs, const void* hat,
-                           const void* sym_derived, void* local, void* stream);
-
-/* K7+K8 v1b: row-major Hadamard M2L over derived symbols + fused F2L.  Row r
- * (target slot row_slot[r]) owns entries [row_ptr[r], row_ptr[r+1]), int32
- * pairs {source spectrum index, derived-symbol index}. */
-int defmm_m2l_rows_c128(int32_t L, int64_t nrows, const int64_t* row_slot, const int64_t* row_ptr,
-                        const int32_t* entries, const void* hat, const void* sym_derived,
-                        void* local, void* stream);
-
-/* K5 L2L -- traversal.py:355-391 in gather form.
- * For i < n: local[out_slot[i]] += sum_{e in [ptr[i], ptr[i+1])}
+ * particles px/py/pz (FP64, sorted order), q charges.
+ *
+ * K2 P2M -- interpolation.py:109-124 via traversal.py:224-236.
+ *   for i < n: mult[out_slot[i]] = P2M(cell[i], direction dir[i])
+ * K4 M2M -- traversal.py:239-280 + interpolation.py:140-200.
+ *   for i < n: mult[out_slot[i]] = sum over octants o with son_slot[8i+o] >= 0 of
+ *   (C0 (x) C1 (x) C2) mult[son_slot[8i+o]], C the modulated per-axis factors of
+ *   direction dir[i] (< 0: plain Lagrange factors); son_beta = son-level side.
+ * K6 M2F -- fourier.py:67-72 (pad L^3 -> P^3 corner, fftn / P^1.5).
+ *   for i < n: hat[i] = M2F(mult[src_slot[i]])
+ * K9 symbols -- fourier.py:156-183 (unnormalised fftn of G(beta (t + z))).
+ *   for i < n: sym[i] = symbol(t = tvec[3i..3i+2], beta[i]) (computed in FP64)
+ * K9b derived symbols -- fourier.py:186-196 (permute_symbol) materialised:
+ *   sym_derived[i] = sym_canon[canon[i]] gathered through rotation rid[i]
+ * K7+K8 Hadamard M2L + fused F2L -- traversal.py:320-342 (m2l_hadamard,
+ *   fourier.py:83-87) and traversal.py:405-414 (f2l, fourier.py:74-80).
+ *   Row r (target slot row_slot[r]) owns entries [row_ptr[r], row_ptr[r+1]),
+ *   int32 pairs {source spectrum index, derived-symbol index}:
+ *   local[row_slot[r]] = F2L(sum_e sym_derived[e.sym] (*) hat[e.src])
+ * K5 L2L -- traversal.py:355-391 in gather form.
+ *   for i < n: local[out_slot[i]] += sum_{e in [ptr[i], ptr[i+1])}
  *   (C'0 (x) C'1 (x) C'2) local[src_slot[e]], C' the transposed/conjugate-
- * modulated factors of direction src_dir[e] for son octant octant[i]. */
-int defmm_l2l_c128(int32_t L, int64_t n, const int64_t* out_slot, const int8_t* octant,
-                   const int64_t* ptr, const int64_t* src_slot, const int32_t* src_dir,
-                   double son_beta, const double* dirs, double kappa, void* local, void* stream);
+ *   modulated factors of direction src_dir[e] for son octant octant[i].
+ * K3 L2P + un-permute -- interpolation.py:127-137 via traversal.py:394-402,
+ *   tree.py:224-228.  For leaf i < n, p in [cell_start, cell_stop):
+ *   out[perm[p]] = near[p] + sum_{s in [slot_lo[i], slot_hi[i])} L2P(local[s], slot_dir[s]).
+ * K1 P2P -- traversal.py:303-317 + kernel.py:37-55.  For target leaf i < n:
+ *   near[p] = sum over source ranges [src_lo[e], src_hi[e]), e in [ptr[i], ptr[i+1]),
+ *   of G(|x_p - y_s|) q_s for p in [tgt_lo[i], tgt_hi[i]); G = 0 for r < tol.
+ *   Targets t*, sources s* (the same arrays in single-tree mode).
+ */
+#define DEFMM_DECLARE_TYPED(SUFFIX)                                                              \
+    int defmm_p2m_##SUFFIX(int32_t L, int64_t n, const int32_t* cell, const int32_t* dir,        \
+                           const int64_t* out_slot, const int64_t* cell_start,                  \
+                           const int64_t* cell_stop, const double* cell_alpha,                  \
+                           const int32_t* cell_level, const double* level_beta,                 \
+                           const double* dirs, const double* px, const double* py,              \
+                           const double* pz, const void* q, double kappa, void* mult,           \
+                           void* stream);                                                       \
+    int defmm_m2m_##SUFFIX(int32_t L, int64_t n, const int64_t* out_slot, const int32_t* dir,    \
+                           const int64_t* son_slot, double son_beta, const double* dirs,        \
+                           double kappa, void* mult, void* stream);                             \
+    int defmm_m2f_##SUFFIX(int32_t L, int64_t n, const int64_t* src_slot, const void* mult,      \
+                           void* hat, void* stream);                                            \
+    int defmm_symbols_##SUFFIX(int32_t L, int64_t n, const int32_t* tvec, const double* beta,    \
+                               double kappa, void* sym, void* stream);                          \
+    int defmm_expand_symbols_##SUFFIX(int32_t L, int64_t n, const int32_t* canon,                \
+                                      const int8_t* rid, const void* sym_canon,                 \
+                                      void* sym_derived, void* stream);                         \
+    int defmm_m2l_rows_##SUFFIX(int32_t L, int64_t nrows, const int64_t* row_slot,               \
+                                const int64_t* row_ptr, const int32_t* entries,                 \
+                                const void* hat, const void* sym_derived, void* local,          \
+                                void* stream);                                                  \
+    int defmm_l2l_##SUFFIX(int32_t L, int64_t n, const int64_t* out_slot, const int8_t* octant,  \
+                           const int64_t* ptr, const int64_t* src_slot, const int32_t* src_dir, \
+                           double son_beta, const double* dirs, double kappa, void* local,      \
+                           void* stream);                                                       \
+    int defmm_l2p_##SUFFIX(int32_t L, int64_t n, const int32_t* leaf_cell,                       \
+                           const int64_t* slot_lo, const int64_t* slot_hi,                      \
+                           const int32_t* slot_dir, const int64_t* cell_start,                  \
+                           const int64_t* cell_stop, const double* cell_alpha,                  \
+                           const int32_t* cell_level, const double* level_beta,                 \
+                           const double* dirs, const double* px, const double* py,              \
+                           const double* pz, double kappa, const void* local, const void* near, \
+                           const int64_t* perm, void* out, void* stream);                       \
+    int defmm_p2p_##SUFFIX(int64_t n, const int64_t* tgt_lo, const int64_t* tgt_hi,              \
+                           const int64_t* ptr, const int64_t* src_lo, const int64_t* src_hi,    \
+                           const double* tx, const double* ty, const double* tz,                \
+                           const double* sx, const double* sy, const double* sz, const void* q, \
+                           double kappa, double tol, void* near, void* stream);
 
-/* K3 L2P + un-permute -- interpolation.py:127-137 via traversal.py:394-402,
- * tree.py:224-228.  For leaf i < n: for p in [cell_start, cell_stop):
- *   out[perm[p]] = near[p] + sum_{s in [slot_lo[i], slot_hi[i])} L2P(local[s], slot_dir[s]). */
-int defmm_l2p_c128(int32_t L, int64_t n, const int32_t* leaf_cell, const int64_t* slot_lo,
-                   const int64_t* slot_hi, const int32_t* slot_dir, const int64_t* cell_start,
-                   const int64_t* cell_stop, const double* cell_alpha, const int32_t* cell_level,
-                   const double* level_beta, const double* dirs, const double* px,
-                   const double* py, const double* pz, double kappa, const void* local,
-                   const void* near, const int64_t* perm, void* out, void* stream);
+/* expands to: defmm_p2m_c128 defmm_m2m_c128 defmm_m2f_c128 defmm_symbols_c128
+ * defmm_expand_symbols_c128 defmm_m2l_rows_c128 defmm_l2l_c128 defmm_l2p_c128
+ * defmm_p2p_c128 */
+DEFMM_DECLARE_TYPED(c128)
+/* expands to: defmm_p2m_c64 defmm_m2m_c64 defmm_m2f_c64 defmm_symbols_c64
+ * defmm_expand_symbols_c64 defmm_m2l_rows_c64 defmm_l2l_c64 defmm_l2p_c64
+ * defmm_p2p_c64 */
+DEFMM_DECLARE_TYPED(c64)
 
-/* K1 P2P -- traversal.py:303-317 + kernel.py:37-55.  For target leaf i < n:
- * near[p] = sum over source ranges [src_lo[e], src_hi[e]), e in [ptr[i], ptr[i+1]),
- * of G(|x_p - y_s|) q_s for p in [tgt_lo[i], tgt_hi[i]); G = 0 for r < tol.
- * Targets t*, sources s* (the same arrays in single-tree mode). */
-int defmm_p2p_c128(int64_t n, const int64_t* tgt_lo, const int64_t* tgt_hi, const int64_t* ptr,
-                   const int64_t* src_lo, const int64_t* src_hi, const double* tx,
-                   const double* ty, const double* tz, const double* sx, const double* sy,
-                   const double* sz, const void* q, double kappa, double tol, void* near,
-                   void* stream);
+/* K7 reference variant (c128): canonical symbols gathered through the closed-
+ * form rotation inside the loop (e_sym canonical id, e_rid rotation id). */
+int defmm_m2l_canon_c128(int32_t L, int64_t nrows, const int64_t* row_slot, const int64_t* row_ptr,
+                         const int32_t* e_src, const int32_t* e_sym, const int8_t* e_rid,
+                         const void* hat, const void* sym, void* local, void* stream);
 
-/* K10 direct sum -- kernel.py:58-75: out[i] = sum_s G(|t_i - y_s|) q_s. */
+/* K10 direct sum -- kernel.py:58-75: out[i] = sum_s G(|t_i - y_s|) q_s (FP64).
+ * workspace: defmm_direct_workspace_bytes(nt) bytes of device memory. */
+int64_t defmm_direct_workspace_bytes(int64_t nt);
 int defmm_direct_c128(int64_t nt, const double* tx, const double* ty, const double* tz,
                       int64_t ns, const double* sx, const double* sy, const double* sz,
-                      const void* q, double kappa, double tol, void* out, void* stream);
+                      const void* q, double kappa, double tol, void* workspace, void* out,
+                      void* stream);
 
 #ifdef __cplusplus
 }

@@ -23,20 +23,22 @@ _SIGS = {
     "defmm_tree_ncells": [_vp],
     "defmm_tree_fetch": [_vp] + [_vp] * 7,
     "defmm_tree_free": [_vp],
-    "defmm_p2m_c128": [_i32, _i64] + [_vp] * 12 + [_vp, _f64, _vp, _vp],
-    "defmm_m2m_c128": [_i32, _i64, _vp, _vp, _vp, _f64, _vp, _f64, _vp, _vp],
-    "defmm_m2f_c128": [_i32, _i64, _vp, _vp, _vp, _vp],
-    "defmm_symbols_c128": [_i32, _i64, _vp, _vp, _f64, _vp, _vp],
-    "defmm_m2l_c128": [_i32, _i64] + [_vp] * 8 + [_vp],
-    "defmm_expand_symbols_c128": [_i32, _i64, _vp, _vp, _vp, _vp, _vp],
-    "defmm_m2l_group_size": [_i32],
-    "defmm_m2l_grouped_c128": [_i32, _i64] + [_vp] * 7,
-    "defmm_m2l_rows_c128": [_i32, _i64] + [_vp] * 7,
-    "defmm_l2l_c128": [_i32, _i64, _vp, _vp, _vp, _vp, _vp, _f64, _vp, _f64, _vp, _vp],
-    "defmm_l2p_c128": [_i32, _i64] + [_vp] * 13 + [_f64, _vp, _vp, _vp, _vp, _vp],
-    "defmm_p2p_c128": [_i64] + [_vp] * 12 + [_f64, _f64, _vp, _vp],
-    "defmm_direct_c128": [_i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _f64, _f64, _vp, _vp],
+    "defmm_m2l_canon_c128": [_i32, _i64] + [_vp] * 9,
+    "defmm_direct_workspace_bytes": [_i64],
+    "defmm_direct_c128": [_i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _f64, _f64, _vp, _vp, _vp],
 }
+for _t in ("c128", "c64"):
+    _SIGS.update({
+        f"defmm_p2m_{_t}": [_i32, _i64] + [_vp] * 12 + [_vp, _f64, _vp, _vp],
+        f"defmm_m2m_{_t}": [_i32, _i64, _vp, _vp, _vp, _f64, _vp, _f64, _vp, _vp],
+        f"defmm_m2f_{_t}": [_i32, _i64, _vp, _vp, _vp, _vp],
+        f"defmm_symbols_{_t}": [_i32, _i64, _vp, _vp, _f64, _vp, _vp],
+        f"defmm_expand_symbols_{_t}": [_i32, _i64, _vp, _vp, _vp, _vp, _vp],
+        f"defmm_m2l_rows_{_t}": [_i32, _i64] + [_vp] * 7,
+        f"defmm_l2l_{_t}": [_i32, _i64, _vp, _vp, _vp, _vp, _vp, _f64, _vp, _f64, _vp, _vp],
+        f"defmm_l2p_{_t}": [_i32, _i64] + [_vp] * 13 + [_f64, _vp, _vp, _vp, _vp, _vp],
+        f"defmm_p2p_{_t}": [_i64] + [_vp] * 12 + [_f64, _f64, _vp, _vp],
+    })
 
 EXPORTED = tuple(_SIGS)
 
@@ -63,6 +65,7 @@ def load():
         fn.argtypes = args
         fn.restype = _i32
     lib.defmm_tree_ncells.restype = _i64
+    lib.defmm_direct_workspace_bytes.restype = _i64
     lib.defmm_tree_free.restype = None
     lib.defmm_last_error.restype = C.c_char_p
     _lib = lib

@@ -2,8 +2,10 @@
 
 FmmConfig/MacParams/FmmInfo/InteractionEvent keep the fields, defaults and
 validation of traversal.py:46-85; TreeConfig those of tree.py:36-45.  The
-extra FmmConfig field ``dtype`` selects the device arithmetic ("c128"; the
-reference always computes in complex128, kernel.py:68, tree.py:147).
+extra FmmConfig field ``dtype`` selects the device storage precision: "c128"
+(the reference's complex128, kernel.py:68, tree.py:147) or "c64" (complex64
+storage and streams; P2P coordinate differences and the M2L/P2P/L2P sums in
+FP64; cell-relative phases and Lagrange weights in FP32).
 """
 
 from __future__ import annotations
@@ -11,7 +13,7 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 
 STRATEGIES = ("t", "t+s", "t+s+r")  # interpolation.py:36
-DTYPES = ("c128",)
+DTYPES = ("c128", "c64")
 
 
 @dataclass(frozen=True)

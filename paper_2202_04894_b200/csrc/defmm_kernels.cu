@@ -1,17 +1,23 @@
 // B200 (sm_100a) kernels of the defmm FMM matvec, behind the C-ABI declared
-// in include/defmm_b200.h.  complex128 path (double2 interleaved complex).
+// in include/defmm_b200.h.  Every operator is templated on the storage real
+// type R (double -> "c128", float -> "c64") and on the interpolation order L.
 //
-// Design notes (see DESIGN.md for the roofline of each kernel):
-//  * every kernel owns its outputs -- one CTA per output object (expansion
-//    slot, M2L row, target leaf) -- so there are no atomics and reruns are
-//    bitwise deterministic (test_traversal.py:224-231's contract);
-//  * all plane-wave modulations are applied in CELL-RELATIVE form
-//    (e^{i kappa <xi - y, u>} factorised per axis), which equals the
-//    reference's absolute-coordinate products (interpolation.py:104-137,
-//    traversal.py:245-280, 362-391) in exact arithmetic and keeps phases small;
-//  * the Fourier-domain M2L gathers canonical symbols through the closed form
-//    of the cube-group frequency permutation (fourier.py:123-143) instead of
-//    materialising one P^3 spectrum per translation.
+// Design notes (DESIGN.md has the roofline of each kernel):
+//  * every kernel owns its outputs -- one CTA or warp per output object
+//    (expansion slot, M2L row, target leaf) -- so there are no atomics and
+//    reruns are bitwise deterministic (test_traversal.py:224-231's contract);
+//  * plane-wave modulations are applied in CELL-RELATIVE form
+//    (e^{i kappa <xi - y, u>} factorised per axis), equal to the reference's
+//    absolute-coordinate products (interpolation.py:104-137,
+//    traversal.py:245-280, 362-391) in exact arithmetic and keeping every
+//    phase small -- which is what makes the FP32 (c64) path accurate;
+//  * the modulated M2M/L2L Kronecker factor C[k][j] = A[k][j] e^{i th (2x_k -
+//    bit - x_j)} is split as diag(e^{i th 2x_k}) A diag(e^{-i th (bit+x_j)}):
+//    real Lagrange factors (the reference's "t+s+r" strategy,
+//    interpolation.py:194-200) between two diagonal phase scalings;
+//  * the Fourier-domain M2L streams per-translation ("derived") symbols that
+//    are materialised once per plan from the canonical ones through the
+//    closed form of the cube-group frequency permutation (fourier.py:123-196).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -29,52 +35,105 @@ int report(cudaError_t e, const char* where) {
     return (int)e;
 }
 
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+// ---------------------------------------------------------------------------
+// complex helpers (V = double2 | float2)
+
+template <typename R>
+struct Cx;
+template <>
+struct Cx<double> {
+    using t = double2;
+};
+template <>
+struct Cx<float> {
+    using t = float2;
+};
+template <typename R>
+using cx = typename Cx<R>::t;
+
+template <typename V>
+__device__ __forceinline__ V cz() {
+    V v;
+    v.x = 0;
+    v.y = 0;
+    return v;
+}
+template <typename V, typename S>
+__device__ __forceinline__ V cmk(S re, S im) {
+    V v;
+    v.x = re;
+    v.y = im;
+    return v;
+}
+template <typename V>
+__device__ __forceinline__ V cmul(V a, V b) {
+    return cmk<V>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 // c + a*b
-__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
+template <typename V>
+__device__ __forceinline__ V cfma(V a, V b, V c) {
     c.x = fma(a.x, b.x, c.x);
     c.x = fma(-a.y, b.y, c.x);
     c.y = fma(a.x, b.y, c.y);
     c.y = fma(a.y, b.x, c.y);
     return c;
 }
-__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
-__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+// c + s*a, s real
+template <typename V, typename S>
+__device__ __forceinline__ V crfma(S s, V a, V c) {
+    c.x = fma(s, a.x, c.x);
+    c.y = fma(s, a.y, c.y);
+    return c;
+}
+template <typename V>
+__device__ __forceinline__ V cadd(V a, V b) {
+    return cmk<V>(a.x + b.x, a.y + b.y);
+}
+template <typename V, typename S>
+__device__ __forceinline__ V cscale(V a, S s) {
+    return cmk<V>(a.x * s, a.y * s);
+}
+template <typename V>
+__device__ __forceinline__ V cconj(V a) {
+    return cmk<V>(a.x, -a.y);
+}
 __device__ __forceinline__ double2 cexpi(double ph) {
     double s, c;
     sincos(ph, &s, &c);
     return make_double2(c, s);
 }
-
-// Predicated 16-B read-only load that the compiler cannot sink below later
-// code: keeps all loads of an M2L run in flight together.
-__device__ __forceinline__ double2 ldg_pred(const double2* p, bool pred) {
-    double2 v;
-    asm volatile(
-        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\tmov.f64 %0, 0d0000000000000000;\n\t"
-        "mov.f64 %1, 0d0000000000000000;\n\t@q ld.global.nc.v2.f64 {%0, %1}, [%2];\n\t}"
-        : "=d"(v.x), "=d"(v.y)
-        : "l"(p), "r"((int)pred));
+__device__ __forceinline__ float2 cexpi(float ph) {
+    float s, c;
+    sincosf(ph, &s, &c);
+    return make_float2(c, s);
+}
+__device__ __forceinline__ double2 to_d(double2 v) { return v; }
+__device__ __forceinline__ double2 to_d(float2 v) { return make_double2(v.x, v.y); }
+template <typename V>
+__device__ __forceinline__ V from_d(double2 v);
+template <>
+__device__ __forceinline__ double2 from_d<double2>(double2 v) {
     return v;
+}
+template <>
+__device__ __forceinline__ float2 from_d<float2>(double2 v) {
+    return make_float2((float)v.x, (float)v.y);
 }
 
 // Equispaced nodes x_j = j/(L-1) (interpolation.py:51-56) and the Lagrange
 // cardinal functions S_k(x) = prod_{j != k} (x - x_j)/(x_k - x_j) (:59-69).
-template <int L>
-__device__ __forceinline__ double node(int j) {
-    return (double)j / (double)(L - 1);
+template <int L, typename R>
+__device__ __forceinline__ R node(int j) {
+    return (R)j / (R)(L - 1);
 }
-template <int L>
-__device__ __forceinline__ void lagrange(double x, double* S) {
+template <int L, typename R>
+__device__ __forceinline__ void lagrange(R x, R* S) {
 #pragma unroll
     for (int k = 0; k < L; ++k) {
-        double v = 1.0;
+        R v = 1;
 #pragma unroll
         for (int j = 0; j < L; ++j)
-            if (j != k) v = v * (x - node<L>(j)) / (node<L>(k) - node<L>(j));
+            if (j != k) v = v * (x - node<L, R>(j)) / (node<L, R>(k) - node<L, R>(j));
         S[k] = v;
     }
 }
@@ -83,60 +142,77 @@ template <int L>
 __host__ __device__ constexpr int cube() { return L * L * L; }
 template <int L>
 __host__ __device__ constexpr int pad() { return 2 * L - 1; }
-__host__ __device__ constexpr int round32(int x) { return (x + 31) / 32 * 32; }
-
-// threads per CTA for the L^3-shaped operators (one thread per nodal entry)
 template <int L>
-__host__ __device__ constexpr int nodal_threads() { return round32(cube<L>()) < 64 ? 64 : round32(cube<L>()); }
+__host__ __device__ constexpr int per_lane() { return (cube<L>() + 31) / 32; }
+
+// M2M/L2L factor tables A_bit[k][j] = S_k((bit + x_j)/2), bit in {0,1}
+// (interpolation.py:140-148), computed once per CTA in shared memory.
+template <int L, typename R>
+__device__ __forceinline__ void make_factor_tables(R* A) {
+    for (int t = threadIdx.x; t < 2 * L * L; t += blockDim.x) {
+        const int bit = t / (L * L), k = (t / L) % L, j = t % L;
+        double S[L];
+        lagrange<L, double>(((double)bit + node<L, double>(j)) / 2.0, S);
+        A[t] = (R)S[k];
+    }
+}
+
+// tw[k] = e^{-2 pi i k / P}
+template <int P, typename V>
+__device__ __forceinline__ void make_twiddles(V* tw) {
+    for (int k = threadIdx.x; k < P; k += blockDim.x) {
+        double s, c;
+        sincospi(2.0 * (double)k / (double)P, &s, &c);
+        tw[k] = from_d<V>(make_double2(c, -s));
+    }
+}
 
 // ---------------------------------------------------------------------------
 // K2: P2M.  One CTA per (leaf, key).  Per particle and axis the modulated 1D
 // weights W_a = S_a(xh) e^{i kappa beta u (x_a - xh)} are staged in shared
-// memory; the L^3 output entries are then tensor sums over the particles.
+// memory; the L^3 output entries are tensor sums over the particles.
 
-template <int L>
+template <typename R, int L>
 __global__ void __launch_bounds__(128) p2m_kernel(
     int64_t n, const int32_t* __restrict__ cell, const int32_t* __restrict__ dir,
     const int64_t* __restrict__ out_slot, const int64_t* __restrict__ cstart,
     const int64_t* __restrict__ cstop, const double* __restrict__ calpha,
     const int32_t* __restrict__ clevel, const double* __restrict__ lbeta,
     const double* __restrict__ dirs, const double* __restrict__ px, const double* __restrict__ py,
-    const double* __restrict__ pz, const double2* __restrict__ q, double kappa,
-    double2* __restrict__ mult) {
+    const double* __restrict__ pz, const cx<R>* __restrict__ q, double kappa, cx<R>* __restrict__ mult) {
+    using V = cx<R>;
     constexpr int L3 = cube<L>();
     constexpr int NT = 128;
     constexpr int PER = (L3 + NT - 1) / NT;
     constexpr int CH = 32;
-    __shared__ double2 W[3][CH][L];
+    __shared__ V W[3][CH][L];
     const int64_t i = blockIdx.x;
     const int c = cell[i];
     const int d = dir[i];
     const double beta = lbeta[clevel[c]];
-    double al[3], ku[3];
+    double al[3];
+    R ku[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         al[k] = calpha[3 * c + k];
-        ku[k] = d >= 0 ? kappa * beta * dirs[3 * d + k] : 0.0;
+        ku[k] = (R)(d >= 0 ? kappa * beta * dirs[3 * d + k] : 0.0);
     }
     const int64_t s0 = cstart[c], s1 = cstop[c];
-    double2 acc[PER];
+    V acc[PER];
 #pragma unroll
-    for (int m = 0; m < PER; ++m) acc[m] = make_double2(0.0, 0.0);
+    for (int m = 0; m < PER; ++m) acc[m] = cz<V>();
     for (int64_t base = s0; base < s1; base += CH) {
-        const int cnt = (int)((s1 - base) < (int64_t)(CH) ? (s1 - base) : (int64_t)(CH));
+        const int cnt = (int)((s1 - base) < CH ? (s1 - base) : CH);
         __syncthreads();
         for (int t = threadIdx.x; t < cnt * 3; t += NT) {
             const int p = t / 3, ax = t - 3 * (t / 3);
             const double* pp = ax == 0 ? px : (ax == 1 ? py : pz);
-            const double xh = (pp[base + p] - al[ax]) / beta;
-            double S[L];
-            lagrange<L>(xh, S);
-            const double2 qq = ax == 0 ? q[base + p] : make_double2(1.0, 0.0);
+            const R xh = (R)((pp[base + p] - al[ax]) / beta);
+            R S[L];
+            lagrange<L, R>(xh, S);
+            const V qq = ax == 0 ? q[base + p] : cmk<V>((R)1, (R)0);
 #pragma unroll
-            for (int k = 0; k < L; ++k) {
-                const double2 w = cscale(cexpi(ku[ax] * (node<L>(k) - xh)), S[k]);
-                W[ax][p][k] = cmul(qq, w);
-            }
+            for (int k = 0; k < L; ++k) W[ax][p][k] = cmul(qq, cscale(cexpi(ku[ax] * (node<L, R>(k) - xh)), S[k]));
         }
         __syncthreads();
 #pragma unroll
@@ -144,7 +220,7 @@ __global__ void __launch_bounds__(128) p2m_kernel(
             const int r = threadIdx.x + m * NT;
             if (r < L3) {
                 const int a = r / (L * L), b = (r / L) % L, cc = r % L;
-                double2 s = acc[m];
+                V s = acc[m];
                 for (int p = 0; p < cnt; ++p) s = cfma(cmul(W[0][p][a], W[1][p][b]), W[2][p][cc], s);
                 acc[m] = s;
             }
@@ -159,183 +235,253 @@ __global__ void __launch_bounds__(128) p2m_kernel(
 }
 
 // ---------------------------------------------------------------------------
-// K4/K5: M2M and L2L.  The modulated Kronecker factor of one son octant is
-// C_ax[k][j] = A_bit[k][j] e^{i kappa v_ax beta_s (2 x_k - bit - x_j)}, with
-// A_bit[k][j] = S_k((bit + x_j)/2) (interpolation.py:140-148); L2L uses
-// C'_ax[j][k] = conj(C_ax[k][j]) (interpolation.py:151-154 + the conjugate
-// modulation of traversal.py:362-391).  Three mode products in shared memory.
+// K4/K5: M2M and L2L, one WARP per output slot (8 warps per CTA), the three
+// real mode products in per-warp shared memory with __syncwarp only.
 
-template <int L>
-__device__ __forceinline__ void build_factors(double2 (*C)[L][L], int oct, const double ku[3],
-                                              bool transpose_conj) {
-    for (int t = threadIdx.x; t < 3 * L * L; t += blockDim.x) {
-        const int ax = t / (L * L), k = (t / L) % L, j = t % L;  // C[ax][k][j]
-        const int bit = (oct >> (2 - ax)) & 1;
-        double S[L];
-        // A_bit[k][j] = S_k((bit + x_j)/2) ; for the transpose use (k <-> j)
-        const int kk = transpose_conj ? j : k;  // father node index
-        const int jj = transpose_conj ? k : j;  // son node index
-        lagrange<L>(((double)bit + node<L>(jj)) / 2.0, S);
-        const double ph = ku[ax] * (2.0 * node<L>(kk) - (double)bit - node<L>(jj));
-        double2 w = cscale(cexpi(ph), S[kk]);
-        if (transpose_conj) w = cconj(w);
-        C[ax][k][j] = w;
-    }
-}
+constexpr int NODAL_WARPS = 8;
 
-// y = (C0 (x) C1 (x) C2) x for one L^3 tile; x and tmp in shared memory; the
-// result for entry r = threadIdx.x (< L^3) is returned.
-template <int L>
-__device__ __forceinline__ double2 kron3_apply(const double2 (*C)[L][L], double2* x, double2* tmp) {
-    constexpr int L3 = cube<L>();
-    const int r = threadIdx.x;
-    const int a = r / (L * L), b = (r / L) % L, c = r % L;
-    double2 v = make_double2(0.0, 0.0);
-    if (r < L3) {
+// One mode product along `axis` of an L^3 tile (C order) with the real factor
+// A_bit: TRANSPOSE=false -> out k, in j, coefficient A[bit][k][j] (M2M);
+// TRANSPOSE=true -> out j, in k, coefficient A[bit][k][j] (L2L).
+template <int L, typename R, bool TRANSPOSE>
+__device__ __forceinline__ cx<R> mode_product(const R* A, int bit, int axis, const cx<R>* x, int r) {
+    using V = cx<R>;
+    const int i0 = r / (L * L), i1 = (r / L) % L, i2 = r % L;
+    const int o = axis == 0 ? i0 : (axis == 1 ? i1 : i2);
+    const int stride = axis == 0 ? L * L : (axis == 1 ? L : 1);
+    const int base = r - o * stride;
+    const R* Ab = A + bit * L * L;
+    V v = cz<V>();
 #pragma unroll
-        for (int j = 0; j < L; ++j) v = cfma(C[0][a][j], x[(j * L + b) * L + c], v);
-    }
-    __syncthreads();
-    if (r < L3) tmp[r] = v;
-    __syncthreads();
-    v = make_double2(0.0, 0.0);
-    if (r < L3) {
-#pragma unroll
-        for (int j = 0; j < L; ++j) v = cfma(C[1][b][j], tmp[(a * L + j) * L + c], v);
-    }
-    __syncthreads();
-    if (r < L3) x[r] = v;
-    __syncthreads();
-    v = make_double2(0.0, 0.0);
-    if (r < L3) {
-#pragma unroll
-        for (int j = 0; j < L; ++j) v = cfma(C[2][c][j], x[(a * L + b) * L + j], v);
+    for (int t = 0; t < L; ++t) {
+        const R a = TRANSPOSE ? Ab[t * L + o] : Ab[o * L + t];
+        v = crfma(a, x[base + t * stride], v);
     }
     return v;
 }
 
-template <int L>
-__global__ void __launch_bounds__(nodal_threads<L>()) m2m_kernel(
+// the nodal buffers of one warp: 2 L^3 complex (dynamic shared memory)
+template <typename R, int L>
+__host__ __device__ constexpr int nodal_smem_bytes() {
+    return NODAL_WARPS * 2 * cube<L>() * (int)sizeof(cx<R>) + 2 * L * L * (int)sizeof(R);
+}
+
+template <typename R, int L>
+__global__ void __launch_bounds__(32 * NODAL_WARPS) m2m_kernel(
     int64_t n, const int64_t* __restrict__ out_slot, const int32_t* __restrict__ dir,
-    const int64_t* __restrict__ son_slot, double son_beta, const double* __restrict__ dirs,
-    double kappa, double2* __restrict__ mult) {
-    constexpr int L3 = cube<L>();
-    __shared__ double2 C[3][L][L];
-    __shared__ double2 X[L3], T[L3];
-    const int64_t i = blockIdx.x;
+    const int64_t* __restrict__ son_slot, double son_beta, const double* __restrict__ dirs, double kappa,
+    cx<R>* __restrict__ mult) {
+    using V = cx<R>;
+    constexpr int L3 = cube<L>(), E = per_lane<L>();
+    extern __shared__ unsigned char smraw[];
+    V* bufs = reinterpret_cast<V*>(smraw);
+    R* A = reinterpret_cast<R*>(bufs + NODAL_WARPS * 2 * L3);
+    make_factor_tables<L, R>(A);
+    __syncthreads();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * NODAL_WARPS + w;
+    if (i >= n) return;
     const int d = dir[i];
-    double ku[3];
+    R ku[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) ku[k] = d >= 0 ? kappa * son_beta * dirs[3 * d + k] : 0.0;
-    double2 acc = make_double2(0.0, 0.0);
+    for (int k = 0; k < 3; ++k) ku[k] = (R)(d >= 0 ? kappa * son_beta * dirs[3 * d + k] : 0.0);
+    V* X = bufs + w * 2 * L3;
+    V* T = X + L3;
+    V acc[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] = cz<V>();
     for (int o = 0; o < 8; ++o) {
         const int64_t ss = son_slot[8 * i + o];
         if (ss < 0) continue;
-        __syncthreads();
-        if (threadIdx.x < L3) X[threadIdx.x] = mult[ss * L3 + threadIdx.x];
-        build_factors<L>(C, o, ku, false);
-        __syncthreads();
-        acc = cadd(acc, kron3_apply<L>(C, X, T));
+        const int b0 = (o >> 2) & 1, b1 = (o >> 1) & 1, b2 = o & 1;
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int r = lane + 32 * e;
+            if (r < L3) {
+                const int j0 = r / (L * L), j1 = (r / L) % L, j2 = r % L;
+                // son-side phase e^{-i th (bit + x_j)} (conj plane wave on the son grid)
+                const R ph = -(ku[0] * (b0 + node<L, R>(j0)) + ku[1] * (b1 + node<L, R>(j1)) +
+                               ku[2] * (b2 + node<L, R>(j2)));
+                X[r] = d >= 0 ? cmul(mult[ss * L3 + r], cexpi(ph)) : mult[ss * L3 + r];
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int r = lane + 32 * e;
+            if (r < L3) T[r] = mode_product<L, R, false>(A, b0, 0, X, r);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int r = lane + 32 * e;
+            if (r < L3) X[r] = mode_product<L, R, false>(A, b1, 1, T, r);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int r = lane + 32 * e;
+            if (r < L3) acc[e] = cadd(acc[e], mode_product<L, R, false>(A, b2, 2, X, r));
+        }
     }
-    if (threadIdx.x < L3) mult[out_slot[i] * L3 + threadIdx.x] = acc;
+    const int64_t ob = out_slot[i] * L3;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int r = lane + 32 * e;
+        if (r < L3) {
+            const int k0 = r / (L * L), k1 = (r / L) % L, k2 = r % L;
+            // father-side phase e^{i th 2 x_k}
+            const R ph = 2 * (ku[0] * node<L, R>(k0) + ku[1] * node<L, R>(k1) + ku[2] * node<L, R>(k2));
+            mult[ob + r] = d >= 0 ? cmul(acc[e], cexpi(ph)) : acc[e];
+        }
+    }
 }
 
-template <int L>
-__global__ void __launch_bounds__(nodal_threads<L>()) l2l_kernel(
+template <typename R, int L>
+__global__ void __launch_bounds__(32 * NODAL_WARPS) l2l_kernel(
     int64_t n, const int64_t* __restrict__ out_slot, const int8_t* __restrict__ octant,
     const int64_t* __restrict__ ptr, const int64_t* __restrict__ src_slot,
-    const int32_t* __restrict__ src_dir, double son_beta, const double* __restrict__ dirs,
-    double kappa, double2* __restrict__ local) {
-    constexpr int L3 = cube<L>();
-    __shared__ double2 C[3][L][L];
-    __shared__ double2 X[L3], T[L3];
-    const int64_t i = blockIdx.x;
-    const int oct = octant[i];
-    const int64_t o = out_slot[i] * L3;
-    double2 acc = make_double2(0.0, 0.0);
-    if (threadIdx.x < L3) acc = local[o + threadIdx.x];
-    for (int64_t e = ptr[i]; e < ptr[i + 1]; ++e) {
-        const int d = src_dir[e];
-        double ku[3];
+    const int32_t* __restrict__ src_dir, double son_beta, const double* __restrict__ dirs, double kappa,
+    cx<R>* __restrict__ local) {
+    using V = cx<R>;
+    constexpr int L3 = cube<L>(), E = per_lane<L>();
+    extern __shared__ unsigned char smraw[];
+    V* bufs = reinterpret_cast<V*>(smraw);
+    R* A = reinterpret_cast<R*>(bufs + NODAL_WARPS * 2 * L3);
+    make_factor_tables<L, R>(A);
+    __syncthreads();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * NODAL_WARPS + w;
+    if (i >= n) return;
+    const int o = octant[i];
+    const int b0 = (o >> 2) & 1, b1 = (o >> 1) & 1, b2 = o & 1;
+    V* X = bufs + w * 2 * L3;
+    V* T = X + L3;
+    const int64_t ob = out_slot[i] * L3;
+    V acc[E];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) ku[k] = d >= 0 ? kappa * son_beta * dirs[3 * d + k] : 0.0;
-        __syncthreads();
-        if (threadIdx.x < L3) X[threadIdx.x] = local[src_slot[e] * L3 + threadIdx.x];
-        build_factors<L>(C, oct, ku, true);
-        __syncthreads();
-        acc = cadd(acc, kron3_apply<L>(C, X, T));
+    for (int e = 0; e < E; ++e) {
+        const int r = lane + 32 * e;
+        acc[e] = r < L3 ? local[ob + r] : cz<V>();
     }
-    if (threadIdx.x < L3) local[o + threadIdx.x] = acc;
+    for (int64_t s = ptr[i]; s < ptr[i + 1]; ++s) {
+        const int d = src_dir[s];
+        const int64_t sb = src_slot[s] * L3;
+        R ku[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) ku[k] = (R)(d >= 0 ? kappa * son_beta * dirs[3 * d + k] : 0.0);
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int r = lane + 32 * e;
+            if (r < L3) {
+                const int k0 = r / (L * L), k1 = (r / L) % L, k2 = r % L;
+                // father-side phase e^{-i th 2 x_k} (conj plane wave on the father grid)
+                const R ph = -2 * (ku[0] * node<L, R>(k0) + ku[1] * node<L, R>(k1) + ku[2] * node<L, R>(k2));
+                X[r] = d >= 0 ? cmul(local[sb + r], cexpi(ph)) : local[sb + r];
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int r = lane + 32 * e;
+            if (r < L3) T[r] = mode_product<L, R, true>(A, b0, 0, X, r);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int r = lane + 32 * e;
+            if (r < L3) X[r] = mode_product<L, R, true>(A, b1, 1, T, r);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int r = lane + 32 * e;
+            if (r < L3) {
+                const V y = mode_product<L, R, true>(A, b2, 2, X, r);
+                const int j0 = r / (L * L), j1 = (r / L) % L, j2 = r % L;
+                // son-side phase e^{i th (bit + x_j)}
+                const R ph = ku[0] * (b0 + node<L, R>(j0)) + ku[1] * (b1 + node<L, R>(j1)) +
+                             ku[2] * (b2 + node<L, R>(j2));
+                acc[e] = cadd(acc[e], d >= 0 ? cmul(y, cexpi(ph)) : y);
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int r = lane + 32 * e;
+        if (r < L3) local[ob + r] = acc[e];
+    }
 }
 
 // ---------------------------------------------------------------------------
-// Pruned odd-size 3D DFTs.  tw[k] = e^{-2 pi i k / P}.
+// K6 M2F: L^3 corner of a zero P^3 grid -> unitary forward DFT
+// (fourier.py:67-72), pruned per axis; one WARP per expansion.
 
-template <int P>
-__device__ __forceinline__ void make_twiddles(double2* tw) {
-    for (int k = threadIdx.x; k < P; k += blockDim.x) {
-        double s, c;
-        sincospi(2.0 * (double)k / (double)P, &s, &c);
-        tw[k] = make_double2(c, -s);
-    }
-}
+constexpr int M2F_WARPS = 4;
 
-// K6 M2F: L^3 corner of a zero P^3 grid -> unitary forward DFT (fourier.py:67-72).
-template <int L>
-__global__ void __launch_bounds__(128) m2f_kernel(int64_t n, const int64_t* __restrict__ src_slot,
-                                                  const double2* __restrict__ mult,
-                                                  double2* __restrict__ hat) {
+template <typename R, int L>
+__global__ void __launch_bounds__(32 * M2F_WARPS) m2f_kernel(int64_t n, const int64_t* __restrict__ src_slot,
+                                                             const cx<R>* __restrict__ mult,
+                                                             cx<R>* __restrict__ hat) {
+    using V = cx<R>;
     constexpr int P = pad<L>(), L3 = cube<L>(), P3 = P * P * P;
-    extern __shared__ double2 sm[];
-    double2* tw = sm;                 // P
-    double2* X = tw + P;              // L^3
-    double2* Y1 = X + L3;             // L*L*P   [a][b][f2]
-    double2* Y2 = Y1 + L * L * P;     // L*P*P   [a][f1][f2]
-    const int64_t i = blockIdx.x;
-    make_twiddles<P>(tw);
-    const int64_t s = src_slot[i] * L3;
-    for (int r = threadIdx.x; r < L3; r += blockDim.x) X[r] = mult[s + r];
+    constexpr int WS = L3 + L * L * P + L * P * P;
+    extern __shared__ unsigned char smraw[];
+    V* tw = reinterpret_cast<V*>(smraw);
+    make_twiddles<P, V>(tw);
     __syncthreads();
-    for (int t = threadIdx.x; t < L * L * P; t += blockDim.x) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * M2F_WARPS + w;
+    if (i >= n) return;
+    V* X = tw + P + w * WS;  // L^3
+    V* Y1 = X + L3;          // [a][b][f2]
+    V* Y2 = Y1 + L * L * P;  // [a][f1][f2]
+    const int64_t s = src_slot[i] * L3;
+    for (int r = lane; r < L3; r += 32) X[r] = mult[s + r];
+    __syncwarp();
+    for (int t = lane; t < L * L * P; t += 32) {
         const int ab = t / P, f2 = t % P;
-        double2 v = make_double2(0.0, 0.0);
+        V v = cz<V>();
 #pragma unroll
         for (int c = 0; c < L; ++c) v = cfma(X[ab * L + c], tw[(f2 * c) % P], v);
         Y1[t] = v;
     }
-    __syncthreads();
-    for (int t = threadIdx.x; t < L * P * P; t += blockDim.x) {
+    __syncwarp();
+    for (int t = lane; t < L * P * P; t += 32) {
         const int a = t / (P * P), f1 = (t / P) % P, f2 = t % P;
-        double2 v = make_double2(0.0, 0.0);
+        V v = cz<V>();
 #pragma unroll
         for (int b = 0; b < L; ++b) v = cfma(Y1[(a * L + b) * P + f2], tw[(f1 * b) % P], v);
         Y2[t] = v;
     }
-    __syncthreads();
-    const double scale = 1.0 / (P * sqrt((double)P));
-    double2* out = hat + i * (int64_t)P3;
-    for (int t = threadIdx.x; t < P3; t += blockDim.x) {
+    __syncwarp();
+    const R scale = (R)(1.0 / (P * sqrt((double)P)));
+    V* out = hat + i * (int64_t)P3;
+    for (int t = lane; t < P3; t += 32) {
         const int f0 = t / (P * P), f12 = t % (P * P);
-        double2 v = make_double2(0.0, 0.0);
+        V v = cz<V>();
 #pragma unroll
         for (int a = 0; a < L; ++a) v = cfma(Y2[a * P * P + f12], tw[(f0 * a) % P], v);
         out[t] = cscale(v, scale);
     }
 }
 
-// K9 symbols: kernel column on the difference grid (wrap order) and its
-// unnormalised forward DFT (fourier.py:156-183).
-template <int L>
+// K9 symbols: kernel column G(beta (t + z)) on the difference grid (wrap
+// order) and its unnormalised forward DFT (fourier.py:156-183), in FP64,
+// stored as R.
+template <typename R, int L>
 __global__ void __launch_bounds__(256) symbols_kernel(int64_t n, const int32_t* __restrict__ tvec,
                                                       const double* __restrict__ beta, double kappa,
-                                                      double2* __restrict__ sym) {
+                                                      cx<R>* __restrict__ sym) {
     constexpr int P = pad<L>(), P3 = P * P * P;
-    extern __shared__ double2 sm[];
-    double2* tw = sm;
+    extern __shared__ unsigned char smraw[];
+    double2* tw = reinterpret_cast<double2*>(smraw);
     double2* A = tw + P;
     double2* B = A + P3;
     const int64_t i = blockIdx.x;
-    make_twiddles<P>(tw);
+    make_twiddles<P, double2>(tw);
     const double h = 1.0 / (L - 1);
     const double b = beta[i];
     const double inv4pi = 1.0 / (4.0 * 3.141592653589793);
@@ -348,7 +494,6 @@ __global__ void __launch_bounds__(256) symbols_kernel(int64_t n, const int32_t* 
         A[t] = cscale(cexpi(kappa * r), inv4pi / r);
     }
     __syncthreads();
-    // axis 2, then 1, then 0 (full DFTs)
     for (int t = threadIdx.x; t < P3; t += blockDim.x) {
         const int row = t / P, f = t % P;
         double2 v = make_double2(0.0, 0.0);
@@ -363,203 +508,107 @@ __global__ void __launch_bounds__(256) symbols_kernel(int64_t n, const int32_t* 
         A[t] = v;
     }
     __syncthreads();
-    double2* out = sym + i * (int64_t)P3;
+    cx<R>* out = sym + i * (int64_t)P3;
     for (int t = threadIdx.x; t < P3; t += blockDim.x) {
         const int f = t / (P * P), bc = t % (P * P);
         double2 v = make_double2(0.0, 0.0);
         for (int k = 0; k < P; ++k) v = cfma(A[k * P * P + bc], tw[(f * k) % P], v);
-        out[t] = v;
+        out[t] = from_d<cx<R>>(v);
     }
 }
 
-// ---------------------------------------------------------------------------
-// K7+K8: Hadamard M2L over a target-major CSR row, then the pruned inverse
-// DFT (F2L) of the accumulated spectrum, written once to the local slot.
-
 // itertools.permutations(range(3)) order (fourier.py:94)
 __constant__ int8_t c_perm[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+
+// flat index of the canonical entry feeding frequency j under rotation rid:
+// mapped[perm[a]] = (sign[a] f[a]) mod P  (fourier.py:123-143)
+template <int P>
+__device__ __forceinline__ int rotated_index(int j, int rid) {
+    const int f[3] = {j / (P * P), (j / P) % P, j % P};
+    const int wt[3] = {P * P, P, 1};
+    const int pi = rid >> 3;
+    int idx = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const int ng = (rid >> (2 - a)) & 1;
+        idx += wt[c_perm[pi][a]] * (ng ? (f[a] ? P - f[a] : 0) : f[a]);
+    }
+    return idx;
+}
+
+// K9b: derived symbols D_t[j] = D_canon[rotated_index(j, rid)] (permute_symbol,
+// fourier.py:186-196), materialised once per plan so the M2L streams them with
+// coalesced loads (the in-loop gather made v1 L1-bound, profiles/r01_summary_v1.md).
+template <typename R, int L>
+__global__ void __launch_bounds__(256) expand_symbols_kernel(int64_t n, const int32_t* __restrict__ canon,
+                                                             const int8_t* __restrict__ rid,
+                                                             const cx<R>* __restrict__ symc,
+                                                             cx<R>* __restrict__ symd) {
+    constexpr int P = pad<L>(), P3 = P * P * P;
+    const int64_t i = blockIdx.x;
+    const int r = rid[i];
+    const cx<R>* src = symc + (int64_t)canon[i] * P3;
+    cx<R>* dst = symd + i * P3;
+    for (int j = threadIdx.x; j < P3; j += blockDim.x) dst[j] = src[rotated_index<P>(j, r)];
+}
+
+// ---------------------------------------------------------------------------
+// K7+K8: Hadamard M2L + fused F2L.
 
 template <int L>
 __host__ __device__ constexpr int m2l_threads() {
     return L <= 3 ? 128 : L == 4 ? 352 : L == 5 ? 256 : L == 6 ? 448 : L == 7 ? 320 : 384;
 }
 
-template <int L>
-__global__ void __launch_bounds__(m2l_threads<L>()) m2l_kernel(
-    int64_t nrows, const int64_t* __restrict__ row_slot, const int64_t* __restrict__ row_ptr,
-    const int32_t* __restrict__ e_src, const int32_t* __restrict__ e_sym,
-    const int8_t* __restrict__ e_rid, const double2* __restrict__ hat,
-    const double2* __restrict__ sym, double2* __restrict__ local) {
-    constexpr int P = pad<L>(), L3 = cube<L>(), P3 = P * P * P;
-    constexpr int NT = m2l_threads<L>();
-    constexpr int PER = (P3 + NT - 1) / NT;
-    extern __shared__ double2 sm[];
-    double2* tw = sm;             // P
-    double2* X = tw + P;          // P^3
-    double2* Z1 = X + P3;         // L*P*P
-    const int64_t row = blockIdx.x;
-    make_twiddles<P>(tw);
-    int f[PER][3];
-    double2 acc[PER];
-#pragma unroll
-    for (int m = 0; m < PER; ++m) {
-        const int j = threadIdx.x + m * NT;
-        f[m][0] = j / (P * P);
-        f[m][1] = (j / P) % P;
-        f[m][2] = j % P;
-        acc[m] = make_double2(0.0, 0.0);
-    }
-    const int64_t e0 = row_ptr[row], e1 = row_ptr[row + 1];
-    for (int64_t e = e0; e < e1; ++e) {
-        const int64_t src = e_src[e];
-        const int64_t sy = e_sym[e];
-        const int rid = e_rid[e];
-        const int pi = rid >> 3;
-        int w[3], ng[3];
-        const int wt[3] = {P * P, P, 1};
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            w[a] = wt[c_perm[pi][a]];
-            ng[a] = (rid >> (2 - a)) & 1;
-        }
-        const double2* S = hat + src * P3;
-        const double2* D = sym + sy * P3;
-#pragma unroll
-        for (int m = 0; m < PER; ++m) {
-            const int j = threadIdx.x + m * NT;
-            if (j < P3) {
-                int idx = 0;
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    const int fa = f[m][a];
-                    const int v = ng[a] ? (fa ? P - fa : 0) : fa;
-                    idx += w[a] * v;
-                }
-                acc[m] = cfma(__ldg(D + idx), __ldg(S + j), acc[m]);
-            }
-        }
-    }
-#pragma unroll
-    for (int m = 0; m < PER; ++m) {
-        const int j = threadIdx.x + m * NT;
-        if (j < P3) X[j] = acc[m];
-    }
-    __syncthreads();
-    // inverse, pruned: contract f0 -> a (L*P*P outputs) ...
-    for (int t = threadIdx.x; t < L * P * P; t += NT) {
-        const int a = t / (P * P), f12 = t % (P * P);
-        double2 v = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int f0 = 0; f0 < P; ++f0) v = cfma(X[f0 * P * P + f12], cconj(tw[(f0 * a) % P]), v);
-        Z1[t] = v;
-    }
-    __syncthreads();
-    // ... f1 -> b (L*L*P outputs, into X) ...
-    for (int t = threadIdx.x; t < L * L * P; t += NT) {
-        const int a = t / (L * P), b = (t / P) % L, f2 = t % P;
-        double2 v = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int f1 = 0; f1 < P; ++f1) v = cfma(Z1[(a * P + f1) * P + f2], cconj(tw[(f1 * b) % P]), v);
-        X[t] = v;
-    }
-    __syncthreads();
-    // ... f2 -> c (L^3 outputs), scaled by P^{-3/2}
-    const double scale = 1.0 / (P * sqrt((double)P));
-    double2* out = local + row_slot[row] * L3;
-    for (int t = threadIdx.x; t < L3; t += NT) {
-        const int ab = t / L, c = t % L;
-        double2 v = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int f2 = 0; f2 < P; ++f2) v = cfma(X[ab * P + f2], cconj(tw[(f2 * c) % P]), v);
-        out[t] = cscale(v, scale);
-    }
-}
-
-// Derived symbols: D_t[j] = D_canon[perm_rid(j)] materialised once per plan so
-// that the M2L inner loop streams them with coalesced 16-B loads (the v1
-// in-loop gather cost ~20 L1 wavefronts per warp and event, see
-// profiles/r01_summary_v1.md).
-template <int L>
-__global__ void __launch_bounds__(256) expand_symbols_kernel(int64_t n, const int32_t* __restrict__ canon,
-                                                             const int8_t* __restrict__ rid,
-                                                             const double2* __restrict__ symc,
-                                                             double2* __restrict__ symd) {
-    constexpr int P = pad<L>(), P3 = P * P * P;
-    const int64_t i = blockIdx.x;
-    const int r = rid[i];
-    const int pi = r >> 3;
-    const int wt[3] = {P * P, P, 1};
-    int w[3], ng[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        w[a] = wt[c_perm[pi][a]];
-        ng[a] = (r >> (2 - a)) & 1;
-    }
-    const double2* src = symc + (int64_t)canon[i] * P3;
-    double2* dst = symd + i * P3;
-    for (int j = threadIdx.x; j < P3; j += blockDim.x) {
-        const int f[3] = {j / (P * P), (j / P) % P, j % P};
-        int idx = 0;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) idx += w[a] * (ng[a] ? (f[a] ? P - f[a] : 0) : f[a]);
-        dst[j] = src[idx];
-    }
-}
-
-// M2L v2: one CTA per group of <= G target rows that share a parent cell and a
-// key (siblings), entries sorted by source so each source spectrum is loaded
-// once per group into registers; derived symbols streamed coalesced; G
-// register accumulators; F2L epilogue per row.  Entry = {src hat index,
-// translation id | a << 29} (a = row index inside the group).
-template <int L>
-__host__ __device__ constexpr int m2l_group_size() { return L <= 5 ? 8 : (L == 6 ? 4 : 2); }
-
-template <int L>
-__device__ __forceinline__ void f2l_row(const double2* tw, double2* X, double2* Z1, double2* out) {
+// pruned inverse DFT of one accumulated spectrum X (P^3, smem) into an L^3
+// nodal vector (fourier.py:74-80): contract f0 -> a, f1 -> b, f2 -> c.
+template <int L, typename V>
+__device__ __forceinline__ void f2l_row(const V* tw, V* X, V* Z1, V* out, int nt) {
     constexpr int P = pad<L>(), L3 = cube<L>();
-    const int NT = blockDim.x;
-    for (int t = threadIdx.x; t < L * P * P; t += NT) {
+    for (int t = threadIdx.x; t < L * P * P; t += nt) {
         const int a = t / (P * P), f12 = t % (P * P);
-        double2 v = make_double2(0.0, 0.0);
+        V v = cz<V>();
 #pragma unroll
         for (int f0 = 0; f0 < P; ++f0) v = cfma(X[f0 * P * P + f12], cconj(tw[(f0 * a) % P]), v);
         Z1[t] = v;
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < L * L * P; t += NT) {
+    for (int t = threadIdx.x; t < L * L * P; t += nt) {
         const int a = t / (L * P), b = (t / P) % L, f2 = t % P;
-        double2 v = make_double2(0.0, 0.0);
+        V v = cz<V>();
 #pragma unroll
         for (int f1 = 0; f1 < P; ++f1) v = cfma(Z1[(a * P + f1) * P + f2], cconj(tw[(f1 * b) % P]), v);
         X[t] = v;
     }
     __syncthreads();
     const double scale = 1.0 / (P * sqrt((double)P));
-    for (int t = threadIdx.x; t < L3; t += NT) {
+    for (int t = threadIdx.x; t < L3; t += nt) {
         const int ab = t / L, c = t % L;
-        double2 v = make_double2(0.0, 0.0);
+        V v = cz<V>();
 #pragma unroll
         for (int f2 = 0; f2 < P; ++f2) v = cfma(X[ab * P + f2], cconj(tw[(f2 * c) % P]), v);
         out[t] = cscale(v, scale);
     }
 }
 
-// M2L v1b: one CTA per target row (high occupancy), derived symbols streamed
-// coalesced; two entries in flight per iteration.
-template <int L>
+// Product M2L: one CTA per target row (= local slot with >= 1 M2L source),
+// entries {source spectrum, derived symbol} streamed coalesced, two entries in
+// flight per iteration, accumulation and F2L in FP64 for both storage types.
+template <typename R, int L>
 __global__ void __launch_bounds__(m2l_threads<L>()) m2l_rows_kernel(
     int64_t nrows, const int64_t* __restrict__ row_slot, const int64_t* __restrict__ row_ptr,
-    const int2* __restrict__ ent, const double2* __restrict__ hat, const double2* __restrict__ symd,
-    double2* __restrict__ local) {
+    const int2* __restrict__ ent, const cx<R>* __restrict__ hat, const cx<R>* __restrict__ symd,
+    cx<R>* __restrict__ local) {
     constexpr int P = pad<L>(), L3 = cube<L>(), P3 = P * P * P;
     constexpr int NT = m2l_threads<L>();
     constexpr int PER = (P3 + NT - 1) / NT;
-    extern __shared__ double2 sm[];
-    double2* tw = sm;
+    extern __shared__ unsigned char smraw[];
+    double2* tw = reinterpret_cast<double2*>(smraw);
     double2* X = tw + P;
     double2* Z1 = X + P3;
+    double2* O = Z1 + L * P * P;
     const int64_t row = blockIdx.x;
-    make_twiddles<P>(tw);
+    make_twiddles<P, double2>(tw);
     double2 acc[PER], acc2[PER];
 #pragma unroll
     for (int m = 0; m < PER; ++m) acc[m] = acc2[m] = make_double2(0.0, 0.0);
@@ -567,15 +616,16 @@ __global__ void __launch_bounds__(m2l_threads<L>()) m2l_rows_kernel(
     int64_t e = e0;
     for (; e + 2 <= e1; e += 2) {
         const int2 a = ent[e], b = ent[e + 1];
-        const double2* Sa = hat + (int64_t)a.x * P3;
-        const double2* Da = symd + (int64_t)a.y * P3;
-        const double2* Sb = hat + (int64_t)b.x * P3;
-        const double2* Db = symd + (int64_t)b.y * P3;
+        const cx<R>* Sa = hat + (int64_t)a.x * P3;
+        const cx<R>* Da = symd + (int64_t)a.y * P3;
+        const cx<R>* Sb = hat + (int64_t)b.x * P3;
+        const cx<R>* Db = symd + (int64_t)b.y * P3;
 #pragma unroll
         for (int m = 0; m < PER; ++m) {
             const int j = threadIdx.x + m * NT;
             if (j < P3) {
-                const double2 sa = __ldg(Sa + j), da = __ldg(Da + j), sb = __ldg(Sb + j), db = __ldg(Db + j);
+                const double2 sa = to_d(__ldg(Sa + j)), da = to_d(__ldg(Da + j));
+                const double2 sb = to_d(__ldg(Sb + j)), db = to_d(__ldg(Db + j));
                 acc[m] = cfma(da, sa, acc[m]);
                 acc2[m] = cfma(db, sb, acc2[m]);
             }
@@ -583,12 +633,12 @@ __global__ void __launch_bounds__(m2l_threads<L>()) m2l_rows_kernel(
     }
     if (e < e1) {
         const int2 a = ent[e];
-        const double2* Sa = hat + (int64_t)a.x * P3;
-        const double2* Da = symd + (int64_t)a.y * P3;
+        const cx<R>* Sa = hat + (int64_t)a.x * P3;
+        const cx<R>* Da = symd + (int64_t)a.y * P3;
 #pragma unroll
         for (int m = 0; m < PER; ++m) {
             const int j = threadIdx.x + m * NT;
-            if (j < P3) acc[m] = cfma(__ldg(Da + j), __ldg(Sa + j), acc[m]);
+            if (j < P3) acc[m] = cfma(to_d(__ldg(Da + j)), to_d(__ldg(Sa + j)), acc[m]);
         }
     }
 #pragma unroll
@@ -597,113 +647,57 @@ __global__ void __launch_bounds__(m2l_threads<L>()) m2l_rows_kernel(
         if (j < P3) X[j] = cadd(acc[m], acc2[m]);
     }
     __syncthreads();
-    f2l_row<L>(tw, X, Z1, local + row_slot[row] * L3);
+    f2l_row<L, double2>(tw, X, Z1, O, NT);
+    __syncthreads();
+    cx<R>* out = local + row_slot[row] * L3;
+    for (int t = threadIdx.x; t < L3; t += NT) out[t] = from_d<cx<R>>(O[t]);
 }
 
-// Run record of the grouped M2L: {source spectrum index, target mask, G
-// derived-symbol ids (one per row of the group; unused where the mask bit is 0)}.
+// Reference M2L (v1, c128): canonical symbols gathered in the inner loop.
+// Kept as an independent operator for the parity tests.
 template <int L>
-__host__ __device__ constexpr int m2l_run_words() { return m2l_group_size<L>() + 2; }
-
-template <int L>
-__global__ void __launch_bounds__(m2l_threads<L>()) m2l_grouped_kernel(
-    int64_t ngroups, const int64_t* __restrict__ grp_rows, const int64_t* __restrict__ grp_ptr,
-    const int32_t* __restrict__ runs, const double2* __restrict__ hat, const double2* __restrict__ symd,
-    double2* __restrict__ local) {
-    constexpr int P = pad<L>(), L3 = cube<L>(), P3 = P * P * P;
+__global__ void __launch_bounds__(m2l_threads<L>()) m2l_canon_kernel(
+    int64_t nrows, const int64_t* __restrict__ row_slot, const int64_t* __restrict__ row_ptr,
+    const int32_t* __restrict__ e_src, const int32_t* __restrict__ e_sym,
+    const int8_t* __restrict__ e_rid, const double2* __restrict__ hat,
+    const double2* __restrict__ sym, double2* __restrict__ local) {
+    constexpr int P = pad<L>(), P3 = P * P * P;
     constexpr int NT = m2l_threads<L>();
     constexpr int PER = (P3 + NT - 1) / NT;
-    constexpr int G = m2l_group_size<L>();
-    constexpr int W = m2l_run_words<L>();
-    constexpr int CHUNK = 128;  // run records staged in shared memory per pass
-    extern __shared__ double2 sm[];
-    double2* tw = sm;
+    extern __shared__ unsigned char smraw[];
+    double2* tw = reinterpret_cast<double2*>(smraw);
     double2* X = tw + P;
     double2* Z1 = X + P3;
-    int32_t* rec = reinterpret_cast<int32_t*>(Z1 + L * P * P);  // CHUNK * W ints
-    const int64_t g = blockIdx.x;
-    make_twiddles<P>(tw);
-    double2 acc[G][PER];
+    const int64_t row = blockIdx.x;
+    make_twiddles<P, double2>(tw);
+    double2 acc[PER];
 #pragma unroll
-    for (int k = 0; k < G; ++k)
-#pragma unroll
-        for (int m = 0; m < PER; ++m) acc[k][m] = make_double2(0.0, 0.0);
-    const int64_t r0 = grp_ptr[g], r1 = grp_ptr[g + 1];
-    for (int64_t cb = r0; cb < r1; cb += CHUNK) {
-        const int n = (int)((r1 - cb) < CHUNK ? (r1 - cb) : CHUNK);
-        __syncthreads();
-        for (int t = threadIdx.x; t < n * W; t += NT) rec[t] = runs[cb * W + t];
-        __syncthreads();
-        double2 S[PER], Sn[PER];
-        {
-            const double2* Sp = hat + (int64_t)rec[0] * P3;
-#pragma unroll
-            for (int m = 0; m < PER; ++m) {
-                const int j = threadIdx.x + m * NT;
-                S[m] = j < P3 ? __ldg(Sp + j) : make_double2(0.0, 0.0);
-            }
-        }
-        for (int r = 0; r < n; ++r) {
-            const int32_t* rr = rec + r * W;
-            const unsigned mask = (unsigned)rr[1];
-            // prefetch the next source spectrum
-            // all symbol loads of this run + the next source in flight together
-            double2 D[G][PER];
-#pragma unroll
-            for (int k = 0; k < G; ++k) {
-                const double2* Dp = symd + (int64_t)rr[2 + k] * P3;
-#pragma unroll
-                for (int m = 0; m < PER; ++m) {
-                    const int j = threadIdx.x + m * NT;
-                    D[k][m] = ldg_pred(Dp + j, ((mask >> k) & 1) && j < P3);
-                }
-            }
-            {
-                const bool more = r + 1 < n;
-                const double2* Sp = hat + (int64_t)(more ? rr[W] : 0) * P3;
-#pragma unroll
-                for (int m = 0; m < PER; ++m) {
-                    const int j = threadIdx.x + m * NT;
-                    Sn[m] = ldg_pred(Sp + j, more && j < P3);
-                }
-            }
-            // register fence: every D load above is issued before any FMA below
-#pragma unroll
-            for (int k = 0; k < G; ++k)
-#pragma unroll
-                for (int m = 0; m < PER; ++m) asm volatile("" : "+d"(D[k][m].x), "+d"(D[k][m].y));
-#pragma unroll
-            for (int k = 0; k < G; ++k) {
-                if ((mask >> k) & 1) {
-#pragma unroll
-                    for (int m = 0; m < PER; ++m) acc[k][m] = cfma(D[k][m], S[m], acc[k][m]);
-                }
-            }
-#pragma unroll
-            for (int m = 0; m < PER; ++m) S[m] = Sn[m];
-        }
-    }
-#pragma unroll
-    for (int k = 0; k < G; ++k) {
-        const int64_t row = grp_rows[g * G + k];
-        if (row < 0) break;
-        __syncthreads();
+    for (int m = 0; m < PER; ++m) acc[m] = make_double2(0.0, 0.0);
+    for (int64_t e = row_ptr[row]; e < row_ptr[row + 1]; ++e) {
+        const double2* S = hat + (int64_t)e_src[e] * P3;
+        const double2* D = sym + (int64_t)e_sym[e] * P3;
+        const int rid = e_rid[e];
 #pragma unroll
         for (int m = 0; m < PER; ++m) {
             const int j = threadIdx.x + m * NT;
-            if (j < P3) X[j] = acc[k][m];
+            if (j < P3) acc[m] = cfma(__ldg(D + rotated_index<P>(j, rid)), __ldg(S + j), acc[m]);
         }
-        __syncthreads();
-        f2l_row<L>(tw, X, Z1, local + row * L3);
     }
+#pragma unroll
+    for (int m = 0; m < PER; ++m) {
+        const int j = threadIdx.x + m * NT;
+        if (j < P3) X[j] = acc[m];
+    }
+    __syncthreads();
+    f2l_row<L, double2>(tw, X, Z1, local + row_slot[row] * cube<L>(), NT);
 }
 
 // ---------------------------------------------------------------------------
 // K3: L2P + near-field add + un-permute.  One CTA per target leaf, one thread
 // per particle; L2P(x) = sum_abc loc[abc] conj(W0_a W1_b W2_c) with the same
-// per-axis weights as P2M.
+// per-axis weights as P2M.  Output accumulated in FP64.
 
-template <int L>
+template <typename R, int L>
 __global__ void __launch_bounds__(64) l2p_kernel(
     int64_t n, const int32_t* __restrict__ leaf_cell, const int64_t* __restrict__ slot_lo,
     const int64_t* __restrict__ slot_hi, const int32_t* __restrict__ slot_dir,
@@ -711,11 +705,12 @@ __global__ void __launch_bounds__(64) l2p_kernel(
     const double* __restrict__ calpha, const int32_t* __restrict__ clevel,
     const double* __restrict__ lbeta, const double* __restrict__ dirs, const double* __restrict__ px,
     const double* __restrict__ py, const double* __restrict__ pz, double kappa,
-    const double2* __restrict__ local, const double2* __restrict__ near,
-    const int64_t* __restrict__ perm, double2* __restrict__ out) {
+    const cx<R>* __restrict__ local, const cx<R>* __restrict__ near, const int64_t* __restrict__ perm,
+    cx<R>* __restrict__ out) {
+    using V = cx<R>;
     constexpr int L3 = cube<L>();
     constexpr int NT = 64;
-    __shared__ double2 loc[L3];
+    __shared__ V loc[L3];
     const int64_t i = blockIdx.x;
     const int c = leaf_cell[i];
     const double beta = lbeta[clevel[c]];
@@ -725,51 +720,52 @@ __global__ void __launch_bounds__(64) l2p_kernel(
     for (int64_t base = s0; base < s1; base += NT) {
         const int64_t p = base + threadIdx.x;
         const bool valid = p < s1;
-        double xh[3] = {0.0, 0.0, 0.0};
+        R xh[3] = {0, 0, 0};
         if (valid) {
-            xh[0] = (px[p] - al[0]) / beta;
-            xh[1] = (py[p] - al[1]) / beta;
-            xh[2] = (pz[p] - al[2]) / beta;
+            xh[0] = (R)((px[p] - al[0]) / beta);
+            xh[1] = (R)((py[p] - al[1]) / beta);
+            xh[2] = (R)((pz[p] - al[2]) / beta);
         }
-        double S[3][L];
+        R S[3][L];
 #pragma unroll
-        for (int ax = 0; ax < 3; ++ax) lagrange<L>(xh[ax], S[ax]);
-        double2 acc = valid ? near[p] : make_double2(0.0, 0.0);
+        for (int ax = 0; ax < 3; ++ax) lagrange<L, R>(xh[ax], S[ax]);
+        double2 acc = valid ? to_d(near[p]) : make_double2(0.0, 0.0);
         for (int64_t s = k0; s < k1; ++s) {
             const int d = slot_dir[s];
             __syncthreads();
             for (int r = threadIdx.x; r < L3; r += NT) loc[r] = local[s * L3 + r];
             __syncthreads();
-            double2 W[3][L];
+            V W[3][L];
 #pragma unroll
             for (int ax = 0; ax < 3; ++ax) {
-                const double ku = d >= 0 ? kappa * beta * dirs[3 * d + ax] : 0.0;
+                const R ku = (R)(d >= 0 ? kappa * beta * dirs[3 * d + ax] : 0.0);
 #pragma unroll
-                for (int k = 0; k < L; ++k)
-                    W[ax][k] = cscale(cexpi(ku * (xh[ax] - node<L>(k))), S[ax][k]);
+                for (int k = 0; k < L; ++k) W[ax][k] = cscale(cexpi(ku * (xh[ax] - node<L, R>(k))), S[ax][k]);
             }
-            double2 va = make_double2(0.0, 0.0);
+            V va = cz<V>();
 #pragma unroll
             for (int a = 0; a < L; ++a) {
-                double2 vb = make_double2(0.0, 0.0);
+                V vb = cz<V>();
 #pragma unroll
                 for (int b = 0; b < L; ++b) {
-                    double2 vc = make_double2(0.0, 0.0);
+                    V vc = cz<V>();
 #pragma unroll
                     for (int cc = 0; cc < L; ++cc) vc = cfma(loc[(a * L + b) * L + cc], W[2][cc], vc);
                     vb = cfma(vc, W[1][b], vb);
                 }
                 va = cfma(vb, W[0][a], va);
             }
-            acc = cadd(acc, va);
+            acc = cadd(acc, to_d(va));
         }
-        if (valid) out[perm[p]] = acc;
+        if (valid) out[perm[p]] = from_d<V>(acc);
     }
 }
 
 // ---------------------------------------------------------------------------
 // K1: P2P.  One CTA per target leaf; `split` threads per target share the
-// sources (fixed-order shuffle reduction); source runs staged in shared memory.
+// sources (fixed-order shuffle reduction); source runs staged in shared
+// memory.  Coordinate differences in FP64 (cell-relative accuracy for the
+// FP32 path, SURVEY §7 hard part 6), kernel arithmetic in R, sums in FP64.
 
 constexpr int P2P_NT = 128;
 constexpr int P2P_TILE = 256;
@@ -779,7 +775,7 @@ __device__ __forceinline__ double2 helm_pair(double dx, double dy, double dz, do
     const double r2 = dx * dx + dy * dy + dz * dz;
     const double rinv = rsqrt(r2);  // r2 = 0 -> inf -> r = NaN -> masked below
     const double r = r2 * rinv;
-    const bool ok = r >= tol;     // kernel.py:40-43 singularity suppression
+    const bool ok = r >= tol;       // kernel.py:40-43 singularity suppression
     double s, c;
     sincospi(kpi * (ok ? r : 0.0), &s, &c);
     const double g = ok ? rinv * (1.0 / (4.0 * 3.141592653589793)) : 0.0;
@@ -787,15 +783,31 @@ __device__ __forceinline__ double2 helm_pair(double dx, double dy, double dz, do
     return make_double2(gr * qs.x - gi * qs.y, gr * qs.y + gi * qs.x);
 }
 
+__device__ __forceinline__ double2 helm_pair(double dxd, double dyd, double dzd, float2 qs, double kpid,
+                                             double told) {
+    const float dx = (float)dxd, dy = (float)dyd, dz = (float)dzd;
+    const float r2 = dx * dx + dy * dy + dz * dz;
+    const float rinv = rsqrtf(r2);
+    const float r = r2 * rinv;
+    const bool ok = r >= (float)told;
+    float s, c;
+    sincospif((float)kpid * (ok ? r : 0.0f), &s, &c);  // full range reduction
+    const float g = ok ? rinv * (float)(1.0 / (4.0 * 3.141592653589793)) : 0.0f;
+    const float gr = g * c, gi = g * s;
+    return make_double2((double)(gr * qs.x - gi * qs.y), (double)(gr * qs.y + gi * qs.x));
+}
+
+template <typename R>
 __global__ void __launch_bounds__(P2P_NT) p2p_kernel(
     int64_t n, const int64_t* __restrict__ tgt_lo, const int64_t* __restrict__ tgt_hi,
     const int64_t* __restrict__ ptr, const int64_t* __restrict__ src_lo,
     const int64_t* __restrict__ src_hi, const double* __restrict__ tx,
     const double* __restrict__ ty, const double* __restrict__ tz, const double* __restrict__ px,
-    const double* __restrict__ py, const double* __restrict__ pz, const double2* __restrict__ q,
-    double kappa, double tol, double2* __restrict__ near) {
+    const double* __restrict__ py, const double* __restrict__ pz, const cx<R>* __restrict__ q,
+    double kappa, double tol, cx<R>* __restrict__ near) {
+    using V = cx<R>;
     __shared__ double sx[P2P_TILE], sy[P2P_TILE], sz[P2P_TILE];
-    __shared__ double2 sq[P2P_TILE];
+    __shared__ V sq[P2P_TILE];
     const int64_t i = blockIdx.x;
     const int64_t t0 = tgt_lo[i], t1 = tgt_hi[i];
     const int64_t nt = t1 - t0;
@@ -812,7 +824,7 @@ __global__ void __launch_bounds__(P2P_NT) p2p_kernel(
         for (int64_t e = e0; e < e1; ++e) {
             const int64_t a = src_lo[e], b = src_hi[e];
             for (int64_t sb = a; sb < b; sb += P2P_TILE) {
-                const int cnt = (int)((b - sb) < (int64_t)(P2P_TILE) ? (b - sb) : (int64_t)(P2P_TILE));
+                const int cnt = (int)((b - sb) < P2P_TILE ? (b - sb) : P2P_TILE);
                 __syncthreads();
                 for (int k = threadIdx.x; k < cnt; k += P2P_NT) {
                     sx[k] = px[sb + k];
@@ -834,25 +846,31 @@ __global__ void __launch_bounds__(P2P_NT) p2p_kernel(
             acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
             acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
         }
-        if (valid && part == 0) near[t] = acc;
+        if (valid && part == 0) near[t] = from_d<V>(acc);
     }
 }
 
-// K10: direct sum, one thread per target, all sources tiled through smem.
+// K10: direct sum (FP64).  Sources are split over blockIdx.y so that a few
+// thousand check targets still fill the GPU; partial sums land in
+// part[blockIdx.y][target] and are reduced in a fixed order by direct_reduce.
+constexpr int DIRECT_SPLIT = 64;
+
 __global__ void __launch_bounds__(128) direct_kernel(
     int64_t nt, const double* __restrict__ tx, const double* __restrict__ ty,
     const double* __restrict__ tz, int64_t ns, const double* __restrict__ sx,
     const double* __restrict__ sy, const double* __restrict__ sz, const double2* __restrict__ q,
-    double kappa, double tol, double2* __restrict__ out) {
+    double kappa, double tol, double2* __restrict__ part) {
     __shared__ double ax[256], ay[256], az[256];
     __shared__ double2 aq[256];
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool valid = t < nt;
     const double x = valid ? tx[t] : 0.0, y = valid ? ty[t] : 0.0, z = valid ? tz[t] : 0.0;
     const double kpi = kappa / 3.141592653589793;
+    const int64_t chunk = (ns + gridDim.y - 1) / gridDim.y;
+    const int64_t lo = blockIdx.y * chunk, hi = (lo + chunk) < ns ? lo + chunk : ns;
     double2 acc = make_double2(0.0, 0.0);
-    for (int64_t sb = 0; sb < ns; sb += 256) {
-        const int cnt = (int)((ns - sb) < (int64_t)(256) ? (ns - sb) : (int64_t)(256));
+    for (int64_t sb = lo; sb < hi; sb += 256) {
+        const int cnt = (int)((hi - sb) < 256 ? (hi - sb) : 256);
         __syncthreads();
         for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
             ax[k] = sx[sb + k];
@@ -868,7 +886,16 @@ __global__ void __launch_bounds__(128) direct_kernel(
                 acc.y += g.y;
             }
     }
-    if (valid) out[t] = acc;
+    if (valid) part[blockIdx.y * nt + t] = acc;
+}
+
+__global__ void direct_reduce(int64_t nt, int nsplit, const double2* __restrict__ part,
+                              double2* __restrict__ out) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int k = 0; k < nsplit; ++k) acc = cadd(acc, part[k * nt + t]);
+    out[t] = acc;
 }
 
 // ---------------------------------------------------------------------------
@@ -881,10 +908,11 @@ int set_smem(K kernel, size_t bytes) {
                   "cudaFuncSetAttribute");
 }
 
-inline int grid_ok(int64_t n) { return n > 0 && n < (int64_t)1 << 31; }
+inline bool grid_ok(int64_t n) { return n > 0 && n < ((int64_t)1 << 31); }
+inline unsigned blocks_of(int64_t n, int per) { return (unsigned)((n + per - 1) / per); }
 
-#define DEFMM_DISPATCH_L(L, ...)           \
-    switch (L) {                           \
+#define DEFMM_DISPATCH_L(L, ...)                              \
+    switch (L) {                                              \
         case 2: { constexpr int LL = 2; __VA_ARGS__; } break; \
         case 3: { constexpr int LL = 3; __VA_ARGS__; } break; \
         case 4: { constexpr int LL = 4; __VA_ARGS__; } break; \
@@ -892,8 +920,145 @@ inline int grid_ok(int64_t n) { return n > 0 && n < (int64_t)1 << 31; }
         case 6: { constexpr int LL = 6; __VA_ARGS__; } break; \
         case 7: { constexpr int LL = 7; __VA_ARGS__; } break; \
         case 8: { constexpr int LL = 8; __VA_ARGS__; } break; \
-        default: return -3;                \
+        default: return -3;                                   \
     }
+
+template <typename R>
+int launch_p2m(int32_t L, int64_t n, const int32_t* cell, const int32_t* dir, const int64_t* out_slot,
+               const int64_t* cell_start, const int64_t* cell_stop, const double* cell_alpha,
+               const int32_t* cell_level, const double* level_beta, const double* dirs, const double* px,
+               const double* py, const double* pz, const void* q, double kappa, void* mult, void* stream) {
+    if (n == 0) return 0;
+    if (!grid_ok(n)) return -1;
+    cudaStream_t s = (cudaStream_t)stream;
+    DEFMM_DISPATCH_L(L, (p2m_kernel<R, LL><<<(unsigned)n, 128, 0, s>>>(
+                            n, cell, dir, out_slot, cell_start, cell_stop, cell_alpha, cell_level, level_beta,
+                            dirs, px, py, pz, (const cx<R>*)q, kappa, (cx<R>*)mult)));
+    return report(cudaGetLastError(), "p2m");
+}
+
+template <typename R>
+int launch_m2m(int32_t L, int64_t n, const int64_t* out_slot, const int32_t* dir, const int64_t* son_slot,
+               double son_beta, const double* dirs, double kappa, void* mult, void* stream) {
+    if (n == 0) return 0;
+    if (!grid_ok(n)) return -1;
+    cudaStream_t s = (cudaStream_t)stream;
+    DEFMM_DISPATCH_L(L, {
+        const size_t bytes = nodal_smem_bytes<R, LL>();
+        int rc = set_smem(m2m_kernel<R, LL>, bytes);
+        if (rc) return rc;
+        m2m_kernel<R, LL><<<blocks_of(n, NODAL_WARPS), 32 * NODAL_WARPS, bytes, s>>>(
+            n, out_slot, dir, son_slot, son_beta, dirs, kappa, (cx<R>*)mult);
+    });
+    return report(cudaGetLastError(), "m2m");
+}
+
+template <typename R>
+int launch_l2l(int32_t L, int64_t n, const int64_t* out_slot, const int8_t* octant, const int64_t* ptr,
+               const int64_t* src_slot, const int32_t* src_dir, double son_beta, const double* dirs,
+               double kappa, void* local, void* stream) {
+    if (n == 0) return 0;
+    if (!grid_ok(n)) return -1;
+    cudaStream_t s = (cudaStream_t)stream;
+    DEFMM_DISPATCH_L(L, {
+        const size_t bytes = nodal_smem_bytes<R, LL>();
+        int rc = set_smem(l2l_kernel<R, LL>, bytes);
+        if (rc) return rc;
+        l2l_kernel<R, LL><<<blocks_of(n, NODAL_WARPS), 32 * NODAL_WARPS, bytes, s>>>(
+            n, out_slot, octant, ptr, src_slot, src_dir, son_beta, dirs, kappa, (cx<R>*)local);
+    });
+    return report(cudaGetLastError(), "l2l");
+}
+
+template <typename R>
+int launch_m2f(int32_t L, int64_t n, const int64_t* src_slot, const void* mult, void* hat, void* stream) {
+    if (n == 0) return 0;
+    if (!grid_ok(n)) return -1;
+    cudaStream_t s = (cudaStream_t)stream;
+    DEFMM_DISPATCH_L(L, {
+        constexpr int P = 2 * LL - 1;
+        const size_t bytes = sizeof(cx<R>) * (P + M2F_WARPS * (LL * LL * LL + LL * LL * P + LL * P * P));
+        int rc = set_smem(m2f_kernel<R, LL>, bytes);
+        if (rc) return rc;
+        m2f_kernel<R, LL><<<blocks_of(n, M2F_WARPS), 32 * M2F_WARPS, bytes, s>>>(n, src_slot, (const cx<R>*)mult,
+                                                                                (cx<R>*)hat);
+    });
+    return report(cudaGetLastError(), "m2f");
+}
+
+template <typename R>
+int launch_symbols(int32_t L, int64_t n, const int32_t* tvec, const double* beta, double kappa, void* sym,
+                   void* stream) {
+    if (n == 0) return 0;
+    if (!grid_ok(n)) return -1;
+    cudaStream_t s = (cudaStream_t)stream;
+    DEFMM_DISPATCH_L(L, {
+        constexpr int P = 2 * LL - 1;
+        const size_t bytes = sizeof(double2) * (P + 2 * P * P * P);
+        int rc = set_smem(symbols_kernel<R, LL>, bytes);
+        if (rc) return rc;
+        symbols_kernel<R, LL><<<(unsigned)n, 256, bytes, s>>>(n, tvec, beta, kappa, (cx<R>*)sym);
+    });
+    return report(cudaGetLastError(), "symbols");
+}
+
+template <typename R>
+int launch_expand(int32_t L, int64_t n, const int32_t* canon, const int8_t* rid, const void* symc, void* symd,
+                  void* stream) {
+    if (n == 0) return 0;
+    if (!grid_ok(n)) return -1;
+    cudaStream_t s = (cudaStream_t)stream;
+    DEFMM_DISPATCH_L(L, (expand_symbols_kernel<R, LL><<<(unsigned)n, 256, 0, s>>>(
+                            n, canon, rid, (const cx<R>*)symc, (cx<R>*)symd)));
+    return report(cudaGetLastError(), "expand_symbols");
+}
+
+template <typename R>
+int launch_m2l_rows(int32_t L, int64_t nrows, const int64_t* row_slot, const int64_t* row_ptr,
+                    const int32_t* entries, const void* hat, const void* symd, void* local, void* stream) {
+    if (nrows == 0) return 0;
+    if (!grid_ok(nrows)) return -1;
+    cudaStream_t s = (cudaStream_t)stream;
+    DEFMM_DISPATCH_L(L, {
+        constexpr int P = 2 * LL - 1;
+        const size_t bytes = sizeof(double2) * (P + P * P * P + LL * P * P + LL * LL * LL);
+        int rc = set_smem(m2l_rows_kernel<R, LL>, bytes);
+        if (rc) return rc;
+        m2l_rows_kernel<R, LL><<<(unsigned)nrows, m2l_threads<LL>(), bytes, s>>>(
+            nrows, row_slot, row_ptr, (const int2*)entries, (const cx<R>*)hat, (const cx<R>*)symd,
+            (cx<R>*)local);
+    });
+    return report(cudaGetLastError(), "m2l_rows");
+}
+
+template <typename R>
+int launch_l2p(int32_t L, int64_t n, const int32_t* leaf_cell, const int64_t* slot_lo, const int64_t* slot_hi,
+               const int32_t* slot_dir, const int64_t* cell_start, const int64_t* cell_stop,
+               const double* cell_alpha, const int32_t* cell_level, const double* level_beta, const double* dirs,
+               const double* px, const double* py, const double* pz, double kappa, const void* local,
+               const void* near, const int64_t* perm, void* out, void* stream) {
+    if (n == 0) return 0;
+    if (!grid_ok(n)) return -1;
+    cudaStream_t s = (cudaStream_t)stream;
+    DEFMM_DISPATCH_L(L, (l2p_kernel<R, LL><<<(unsigned)n, 64, 0, s>>>(
+                            n, leaf_cell, slot_lo, slot_hi, slot_dir, cell_start, cell_stop, cell_alpha,
+                            cell_level, level_beta, dirs, px, py, pz, kappa, (const cx<R>*)local,
+                            (const cx<R>*)near, perm, (cx<R>*)out)));
+    return report(cudaGetLastError(), "l2p");
+}
+
+template <typename R>
+int launch_p2p(int64_t n, const int64_t* tgt_lo, const int64_t* tgt_hi, const int64_t* ptr,
+               const int64_t* src_lo, const int64_t* src_hi, const double* tx, const double* ty,
+               const double* tz, const double* sx, const double* sy, const double* sz, const void* q,
+               double kappa, double tol, void* near, void* stream) {
+    if (n == 0) return 0;
+    if (!grid_ok(n)) return -1;
+    p2p_kernel<R><<<(unsigned)n, P2P_NT, 0, (cudaStream_t)stream>>>(n, tgt_lo, tgt_hi, ptr, src_lo, src_hi, tx,
+                                                                    ty, tz, sx, sy, sz, (const cx<R>*)q, kappa,
+                                                                    tol, (cx<R>*)near);
+    return report(cudaGetLastError(), "p2p");
+}
 
 }  // namespace
 
@@ -902,176 +1067,95 @@ extern "C" {
 int defmm_abi_version(void) { return DEFMM_ABI_VERSION; }
 const char* defmm_last_error(void) { return g_last_error; }
 
-int defmm_p2m_c128(int32_t L, int64_t n, const int32_t* cell, const int32_t* dir, const int64_t* out_slot,
-                   const int64_t* cell_start, const int64_t* cell_stop, const double* cell_alpha,
-                   const int32_t* cell_level, const double* level_beta, const double* dirs,
-                   const double* px, const double* py, const double* pz, const void* q, double kappa,
-                   void* mult, void* stream) {
-    if (n == 0) return 0;
-    if (!grid_ok(n)) return -1;
-    cudaStream_t s = (cudaStream_t)stream;
-    DEFMM_DISPATCH_L(L, (p2m_kernel<LL><<<(unsigned)n, 128, 0, s>>>(
-                            n, cell, dir, out_slot, cell_start, cell_stop, cell_alpha, cell_level,
-                            level_beta, dirs, px, py, pz, (const double2*)q, kappa, (double2*)mult)));
-    return report(cudaGetLastError(), "p2m");
-}
+#define DEFMM_EXPORT_TYPED(SUFFIX, R)                                                                               \
+    int defmm_p2m_##SUFFIX(int32_t L, int64_t n, const int32_t* cell, const int32_t* dir, const int64_t* out_slot,  \
+                           const int64_t* cell_start, const int64_t* cell_stop, const double* cell_alpha,          \
+                           const int32_t* cell_level, const double* level_beta, const double* dirs,                \
+                           const double* px, const double* py, const double* pz, const void* q, double kappa,      \
+                           void* mult, void* stream) {                                                             \
+        return launch_p2m<R>(L, n, cell, dir, out_slot, cell_start, cell_stop, cell_alpha, cell_level,             \
+                             level_beta, dirs, px, py, pz, q, kappa, mult, stream);                                \
+    }                                                                                                               \
+    int defmm_m2m_##SUFFIX(int32_t L, int64_t n, const int64_t* out_slot, const int32_t* dir,                       \
+                           const int64_t* son_slot, double son_beta, const double* dirs, double kappa, void* mult,  \
+                           void* stream) {                                                                         \
+        return launch_m2m<R>(L, n, out_slot, dir, son_slot, son_beta, dirs, kappa, mult, stream);                  \
+    }                                                                                                               \
+    int defmm_m2f_##SUFFIX(int32_t L, int64_t n, const int64_t* src_slot, const void* mult, void* hat,              \
+                           void* stream) {                                                                         \
+        return launch_m2f<R>(L, n, src_slot, mult, hat, stream);                                                   \
+    }                                                                                                               \
+    int defmm_symbols_##SUFFIX(int32_t L, int64_t n, const int32_t* tvec, const double* beta, double kappa,         \
+                               void* sym, void* stream) {                                                          \
+        return launch_symbols<R>(L, n, tvec, beta, kappa, sym, stream);                                            \
+    }                                                                                                               \
+    int defmm_expand_symbols_##SUFFIX(int32_t L, int64_t n, const int32_t* canon, const int8_t* rid,                \
+                                      const void* sym_canon, void* sym_derived, void* stream) {                    \
+        return launch_expand<R>(L, n, canon, rid, sym_canon, sym_derived, stream);                                 \
+    }                                                                                                               \
+    int defmm_m2l_rows_##SUFFIX(int32_t L, int64_t nrows, const int64_t* row_slot, const int64_t* row_ptr,          \
+                                const int32_t* entries, const void* hat, const void* sym_derived, void* local,     \
+                                void* stream) {                                                                    \
+        return launch_m2l_rows<R>(L, nrows, row_slot, row_ptr, entries, hat, sym_derived, local, stream);          \
+    }                                                                                                               \
+    int defmm_l2l_##SUFFIX(int32_t L, int64_t n, const int64_t* out_slot, const int8_t* octant,                     \
+                           const int64_t* ptr, const int64_t* src_slot, const int32_t* src_dir, double son_beta,   \
+                           const double* dirs, double kappa, void* local, void* stream) {                          \
+        return launch_l2l<R>(L, n, out_slot, octant, ptr, src_slot, src_dir, son_beta, dirs, kappa, local,         \
+                             stream);                                                                              \
+    }                                                                                                               \
+    int defmm_l2p_##SUFFIX(int32_t L, int64_t n, const int32_t* leaf_cell, const int64_t* slot_lo,                  \
+                           const int64_t* slot_hi, const int32_t* slot_dir, const int64_t* cell_start,             \
+                           const int64_t* cell_stop, const double* cell_alpha, const int32_t* cell_level,          \
+                           const double* level_beta, const double* dirs, const double* px, const double* py,       \
+                           const double* pz, double kappa, const void* local, const void* near,                    \
+                           const int64_t* perm, void* out, void* stream) {                                         \
+        return launch_l2p<R>(L, n, leaf_cell, slot_lo, slot_hi, slot_dir, cell_start, cell_stop, cell_alpha,       \
+                             cell_level, level_beta, dirs, px, py, pz, kappa, local, near, perm, out, stream);     \
+    }                                                                                                               \
+    int defmm_p2p_##SUFFIX(int64_t n, const int64_t* tgt_lo, const int64_t* tgt_hi, const int64_t* ptr,             \
+                           const int64_t* src_lo, const int64_t* src_hi, const double* tx, const double* ty,       \
+                           const double* tz, const double* sx, const double* sy, const double* sz, const void* q,  \
+                           double kappa, double tol, void* near, void* stream) {                                   \
+        return launch_p2p<R>(n, tgt_lo, tgt_hi, ptr, src_lo, src_hi, tx, ty, tz, sx, sy, sz, q, kappa, tol, near,   \
+                             stream);                                                                              \
+    }
 
-int defmm_m2m_c128(int32_t L, int64_t n, const int64_t* out_slot, const int32_t* dir, const int64_t* son_slot,
-                   double son_beta, const double* dirs, double kappa, void* mult, void* stream) {
-    if (n == 0) return 0;
-    if (!grid_ok(n)) return -1;
-    cudaStream_t s = (cudaStream_t)stream;
-    DEFMM_DISPATCH_L(L, (m2m_kernel<LL><<<(unsigned)n, nodal_threads<LL>(), 0, s>>>(
-                            n, out_slot, dir, son_slot, son_beta, dirs, kappa, (double2*)mult)));
-    return report(cudaGetLastError(), "m2m");
-}
+DEFMM_EXPORT_TYPED(c128, double)
+DEFMM_EXPORT_TYPED(c64, float)
 
-int defmm_l2l_c128(int32_t L, int64_t n, const int64_t* out_slot, const int8_t* octant, const int64_t* ptr,
-                   const int64_t* src_slot, const int32_t* src_dir, double son_beta, const double* dirs,
-                   double kappa, void* local, void* stream) {
-    if (n == 0) return 0;
-    if (!grid_ok(n)) return -1;
-    cudaStream_t s = (cudaStream_t)stream;
-    DEFMM_DISPATCH_L(L, (l2l_kernel<LL><<<(unsigned)n, nodal_threads<LL>(), 0, s>>>(
-                            n, out_slot, octant, ptr, src_slot, src_dir, son_beta, dirs, kappa,
-                            (double2*)local)));
-    return report(cudaGetLastError(), "l2l");
-}
-
-int defmm_m2f_c128(int32_t L, int64_t n, const int64_t* src_slot, const void* mult, void* hat, void* stream) {
-    if (n == 0) return 0;
-    if (!grid_ok(n)) return -1;
-    cudaStream_t s = (cudaStream_t)stream;
-    DEFMM_DISPATCH_L(L, {
-        constexpr int P = 2 * LL - 1;
-        const size_t bytes = sizeof(double2) * (P + LL * LL * LL + LL * LL * P + LL * P * P);
-        int rc = set_smem(m2f_kernel<LL>, bytes);
-        if (rc) return rc;
-        m2f_kernel<LL><<<(unsigned)n, 128, bytes, s>>>(n, src_slot, (const double2*)mult, (double2*)hat);
-    });
-    return report(cudaGetLastError(), "m2f");
-}
-
-int defmm_symbols_c128(int32_t L, int64_t n, const int32_t* tvec, const double* beta, double kappa, void* sym,
-                       void* stream) {
-    if (n == 0) return 0;
-    if (!grid_ok(n)) return -1;
-    cudaStream_t s = (cudaStream_t)stream;
-    DEFMM_DISPATCH_L(L, {
-        constexpr int P = 2 * LL - 1;
-        const size_t bytes = sizeof(double2) * (P + 2 * P * P * P);
-        int rc = set_smem(symbols_kernel<LL>, bytes);
-        if (rc) return rc;
-        symbols_kernel<LL><<<(unsigned)n, 256, bytes, s>>>(n, tvec, beta, kappa, (double2*)sym);
-    });
-    return report(cudaGetLastError(), "symbols");
-}
-
-int defmm_m2l_c128(int32_t L, int64_t nrows, const int64_t* row_slot, const int64_t* row_ptr,
-                   const int32_t* e_src, const int32_t* e_sym, const int8_t* e_rid, const void* hat,
-                   const void* sym, void* local, void* stream) {
+int defmm_m2l_canon_c128(int32_t L, int64_t nrows, const int64_t* row_slot, const int64_t* row_ptr,
+                         const int32_t* e_src, const int32_t* e_sym, const int8_t* e_rid, const void* hat,
+                         const void* sym, void* local, void* stream) {
     if (nrows == 0) return 0;
     if (!grid_ok(nrows)) return -1;
     cudaStream_t s = (cudaStream_t)stream;
     DEFMM_DISPATCH_L(L, {
         constexpr int P = 2 * LL - 1;
         const size_t bytes = sizeof(double2) * (P + P * P * P + LL * P * P);
-        int rc = set_smem(m2l_kernel<LL>, bytes);
+        int rc = set_smem(m2l_canon_kernel<LL>, bytes);
         if (rc) return rc;
-        m2l_kernel<LL><<<(unsigned)nrows, m2l_threads<LL>(), bytes, s>>>(
+        m2l_canon_kernel<LL><<<(unsigned)nrows, m2l_threads<LL>(), bytes, s>>>(
             nrows, row_slot, row_ptr, e_src, e_sym, e_rid, (const double2*)hat, (const double2*)sym,
             (double2*)local);
     });
-    return report(cudaGetLastError(), "m2l");
+    return report(cudaGetLastError(), "m2l_canon");
 }
 
-int defmm_expand_symbols_c128(int32_t L, int64_t n, const int32_t* canon, const int8_t* rid, const void* sym_canon,
-                               void* sym_derived, void* stream) {
-    if (n == 0) return 0;
-    if (!grid_ok(n)) return -1;
-    cudaStream_t s = (cudaStream_t)stream;
-    DEFMM_DISPATCH_L(L, (expand_symbols_kernel<LL><<<(unsigned)n, 256, 0, s>>>(
-                            n, canon, rid, (const double2*)sym_canon, (double2*)sym_derived)));
-    return report(cudaGetLastError(), "expand_symbols");
-}
-
-int defmm_m2l_group_size(int32_t L) {
-    int g = -3;
-    DEFMM_DISPATCH_L(L, g = m2l_group_size<LL>());
-    return g;
-}
-
-int defmm_m2l_grouped_c128(int32_t L, int64_t ngroups, const int64_t* grp_rows, const int64_t* grp_ptr,
-                           const int32_t* runs, const void* hat, const void* sym_derived, void* local,
-                           void* stream) {
-    if (ngroups == 0) return 0;
-    if (!grid_ok(ngroups)) return -1;
-    cudaStream_t s = (cudaStream_t)stream;
-    DEFMM_DISPATCH_L(L, {
-        constexpr int P = 2 * LL - 1;
-        const size_t bytes = sizeof(double2) * (P + P * P * P + LL * P * P) + sizeof(int32_t) * 128 * m2l_run_words<LL>();
-        int rc = set_smem(m2l_grouped_kernel<LL>, bytes);
-        if (rc) return rc;
-        m2l_grouped_kernel<LL><<<(unsigned)ngroups, m2l_threads<LL>(), bytes, s>>>(
-            ngroups, grp_rows, grp_ptr, runs, (const double2*)hat, (const double2*)sym_derived, (double2*)local);
-    });
-    return report(cudaGetLastError(), "m2l_grouped");
-}
-
-int defmm_m2l_rows_c128(int32_t L, int64_t nrows, const int64_t* row_slot, const int64_t* row_ptr,
-                        const int32_t* entries, const void* hat, const void* sym_derived, void* local,
-                        void* stream) {
-    if (nrows == 0) return 0;
-    if (!grid_ok(nrows)) return -1;
-    cudaStream_t s = (cudaStream_t)stream;
-    DEFMM_DISPATCH_L(L, {
-        constexpr int P = 2 * LL - 1;
-        const size_t bytes = sizeof(double2) * (P + P * P * P + LL * P * P);
-        int rc = set_smem(m2l_rows_kernel<LL>, bytes);
-        if (rc) return rc;
-        m2l_rows_kernel<LL><<<(unsigned)nrows, m2l_threads<LL>(), bytes, s>>>(
-            nrows, row_slot, row_ptr, (const int2*)entries, (const double2*)hat, (const double2*)sym_derived,
-            (double2*)local);
-    });
-    return report(cudaGetLastError(), "m2l_rows");
-}
-
-int defmm_l2p_c128(int32_t L, int64_t n, const int32_t* leaf_cell, const int64_t* slot_lo, const int64_t* slot_hi,
-                   const int32_t* slot_dir, const int64_t* cell_start, const int64_t* cell_stop,
-                   const double* cell_alpha, const int32_t* cell_level, const double* level_beta,
-                   const double* dirs, const double* px, const double* py, const double* pz, double kappa,
-                   const void* local, const void* near, const int64_t* perm, void* out, void* stream) {
-    if (n == 0) return 0;
-    if (!grid_ok(n)) return -1;
-    cudaStream_t s = (cudaStream_t)stream;
-    DEFMM_DISPATCH_L(L, (l2p_kernel<LL><<<(unsigned)n, 64, 0, s>>>(
-                            n, leaf_cell, slot_lo, slot_hi, slot_dir, cell_start, cell_stop, cell_alpha,
-                            cell_level, level_beta, dirs, px, py, pz, kappa, (const double2*)local,
-                            (const double2*)near, perm, (double2*)out)));
-    return report(cudaGetLastError(), "l2p");
-}
-
-int defmm_p2p_c128(int64_t n, const int64_t* tgt_lo, const int64_t* tgt_hi, const int64_t* ptr,
-                   const int64_t* src_lo, const int64_t* src_hi, const double* tx, const double* ty,
-                   const double* tz, const double* sx, const double* sy, const double* sz, const void* q,
-                   double kappa, double tol, void* near, void* stream) {
-    if (n == 0) return 0;
-    if (!grid_ok(n)) return -1;
-    p2p_kernel<<<(unsigned)n, P2P_NT, 0, (cudaStream_t)stream>>>(n, tgt_lo, tgt_hi, ptr, src_lo, src_hi, tx, ty,
-                                                                 tz, sx, sy, sz, (const double2*)q, kappa,
-                                                                 tol, (double2*)near);
-    return report(cudaGetLastError(), "p2p");
-}
+int64_t defmm_direct_workspace_bytes(int64_t nt) { return (int64_t)DIRECT_SPLIT * nt * (int64_t)sizeof(double2); }
 
 int defmm_direct_c128(int64_t nt, const double* tx, const double* ty, const double* tz, int64_t ns,
                       const double* sx, const double* sy, const double* sz, const void* q, double kappa,
-                      double tol, void* out, void* stream) {
+                      double tol, void* workspace, void* out, void* stream) {
     if (nt == 0) return 0;
     const int64_t blocks = (nt + 127) / 128;
     if (!grid_ok(blocks)) return -1;
-    direct_kernel<<<(unsigned)blocks, 128, 0, (cudaStream_t)stream>>>(nt, tx, ty, tz, ns, sx, sy, sz,
-                                                                      (const double2*)q, kappa, tol,
-                                                                      (double2*)out);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int split = ns >= (int64_t)DIRECT_SPLIT * 256 ? DIRECT_SPLIT : 1;
+    double2* part = (double2*)workspace;
+    direct_kernel<<<dim3((unsigned)blocks, split), 128, 0, s>>>(nt, tx, ty, tz, ns, sx, sy, sz,
+                                                                (const double2*)q, kappa, tol, part);
+    direct_reduce<<<(unsigned)blocks, 128, 0, s>>>(nt, split, part, (double2*)out);
     return report(cudaGetLastError(), "direct");
 }
 

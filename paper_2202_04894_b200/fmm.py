@@ -70,6 +70,7 @@ class FmmPlan:
     # ------------------------------------------------------------------
     def _upload(self):
         p, d = self.plan, self.device
+        self.cdtype = torch.complex128 if self.config.dtype == "c128" else torch.complex64
         L = self.config.order
         i64, i32, f64 = torch.int64, torch.int32, torch.float64
         tt, st = self.tt, self.st
@@ -99,15 +100,7 @@ class FmmPlan:
             self.m2m.append((float(st.side_at(lev + 1)), _dev(slots, i64, d), _dev(p.m_dir[slots], i32, d),
                              _dev(son_slot, i64, d), int(slots.shape[0])))
         self.hat_slot = _dev(p.hat_slot, i64, d)
-        # M2L (v2: sibling groups over derived symbols)
-        G = int(_lib.load().defmm_m2l_group_size(L))
-        if G != p.group_size:
-            raise _lib.DefmmLibraryError(f"library M2L group size {G} != plan {p.group_size}")
-        self.grp_rows = _dev(p.grp_rows.reshape(-1), i64, d)
-        self.grp_ptr = _dev(p.grp_ptr, i64, d)
-        self.grp_runs = _dev(p.grp_runs.reshape(-1), i32, d)
-        self.n_groups = int(p.grp_rows.shape[0])
-        # v1 row CSR (kept for the operator tests)
+        # M2L rows (target-major CSR)
         self.row_slot = _dev(p.m2l_row_slot, i64, d)
         self.row_ptr = _dev(p.m2l_row_ptr, i64, d)
         self.e_src = _dev(p.m2l_src, i32, d)
@@ -128,37 +121,39 @@ class FmmPlan:
         self.p2p_ptr = _dev(p.p2p_ptr, i64, d)
         self.p2p_lo = _dev(p.p2p_lo, i64, d)
         self.p2p_hi = _dev(p.p2p_hi, i64, d)
-        # workspaces
-        c128 = torch.complex128
-        self.mult = torch.empty((max(p.n_mult, 1), self.L3), dtype=c128, device=d)
-        self.hat = torch.empty((max(p.n_hat, 1), self.P3), dtype=c128, device=d)
-        self.local = torch.empty((max(p.n_local, 1), self.L3), dtype=c128, device=d)
-        self.near = torch.empty(self.n_tgt, dtype=c128, device=d)
-        self.q = torch.zeros(self.n_src, dtype=c128, device=d)
-        self.out = torch.empty(self.n_tgt, dtype=c128, device=d)
+        # workspaces (storage precision per FmmConfig.dtype)
+        cd = self.cdtype
+        self.mult = torch.empty((max(p.n_mult, 1), self.L3), dtype=cd, device=d)
+        self.hat = torch.empty((max(p.n_hat, 1), self.P3), dtype=cd, device=d)
+        self.local = torch.empty((max(p.n_local, 1), self.L3), dtype=cd, device=d)
+        self.near = torch.empty(self.n_tgt, dtype=cd, device=d)
+        self.q = torch.zeros(self.n_src, dtype=cd, device=d)
+        self.out = torch.empty(self.n_tgt, dtype=cd, device=d)
         self.side_stream = torch.cuda.Stream(device=d)
-        self.m2l_variant = "rows_derived"
+        self.m2l_variant = "derived"
 
     def _symbols(self):
         p = self.plan
-        self.sym = torch.empty((max(p.n_sym, 1), self.P3), dtype=torch.complex128, device=self.device)
+        self.sym = torch.empty((max(p.n_sym, 1), self.P3), dtype=self.cdtype, device=self.device)
+        st = torch.cuda.current_stream(self.device).cuda_stream
         if p.n_sym:
             tv = _dev(p.sym_tvec.reshape(-1), torch.int32, self.device)
             beta = _dev(p.sym_beta, torch.float64, self.device)
-            st = torch.cuda.current_stream(self.device).cuda_stream
-            _lib.call("defmm_symbols_c128", self.L, p.n_sym, tv, beta, float(p.kappa), self.sym, st)
+            _lib.call(self._op("symbols"), self.L, p.n_sym, tv, beta, float(p.kappa), self.sym, st)
         n_tr = int(p.trans_canon.shape[0])
-        self.sym_derived = torch.empty((max(n_tr, 1), self.P3), dtype=torch.complex128, device=self.device)
+        self.sym_derived = torch.empty((max(n_tr, 1), self.P3), dtype=self.cdtype, device=self.device)
         if n_tr:
-            _lib.call("defmm_expand_symbols_c128", self.L, n_tr, _dev(p.trans_canon, torch.int32, self.device),
-                      _dev(p.trans_rid, torch.int8, self.device), self.sym, self.sym_derived,
-                      torch.cuda.current_stream(self.device).cuda_stream)
+            _lib.call(self._op("expand_symbols"), self.L, n_tr, _dev(p.trans_canon, torch.int32, self.device),
+                      _dev(p.trans_rid, torch.int8, self.device), self.sym, self.sym_derived, st)
+
+    def _op(self, name: str) -> str:
+        return f"defmm_{name}_{self.config.dtype}"
 
     # ------------------------------------------------------------------
     def set_charges(self, charges):
         """Load charges (caller order) into the sorted device buffer."""
         q = torch.as_tensor(np.asarray(charges, dtype=complex)) if not torch.is_tensor(charges) else charges
-        q = q.to(device=self.device, dtype=torch.complex128)
+        q = q.to(device=self.device, dtype=self.cdtype)
         self.q.copy_(q[self.s_perm])
 
     def set_charges_sorted(self, q_sorted):
@@ -180,12 +175,12 @@ class FmmPlan:
             a = ev()
             a.record(stream)
         # upward: P2M at every leaf key, M2M per level bottom-up, M2F
-        _lib.call("defmm_p2m_c128", L, self.p2m_slot.shape[0], self.p2m_cell, self.p2m_dir, self.p2m_slot,
+        _lib.call(self._op("p2m"), L, self.p2m_slot.shape[0], self.p2m_cell, self.p2m_dir, self.p2m_slot,
                   sg["start"], sg["stop"], sg["alpha"], sg["level"], sg["beta"], self.dirs, *self.s_xyz, self.q,
                   kappa, self.mult, sh)
         for son_beta, slots, mdir, son_slot, n in self.m2m:
-            _lib.call("defmm_m2m_c128", L, n, slots, mdir, son_slot, son_beta, self.dirs, kappa, self.mult, sh)
-        _lib.call("defmm_m2f_c128", L, p.n_hat, self.hat_slot, self.mult, self.hat, sh)
+            _lib.call(self._op("m2m"), L, n, slots, mdir, son_slot, son_beta, self.dirs, kappa, self.mult, sh)
+        _lib.call(self._op("m2f"), L, p.n_hat, self.hat_slot, self.mult, self.hat, sh)
         if stage_events is not None:
             b = ev()
             b.record(stream)
@@ -198,7 +193,7 @@ class FmmPlan:
             if stage_events is not None:
                 e0 = ev()
                 e0.record(side)
-            _lib.call("defmm_p2p_c128", p.leaf_cells.shape[0], self.tgt_lo, self.tgt_hi, self.p2p_ptr,
+            _lib.call(self._op("p2p"), p.leaf_cells.shape[0], self.tgt_lo, self.tgt_hi, self.p2p_ptr,
                       self.p2p_lo, self.p2p_hi, *self.t_xyz, *self.s_xyz, self.q, kappa, float(p.tol),
                       self.near, side.cuda_stream)
             if stage_events is not None:
@@ -207,25 +202,24 @@ class FmmPlan:
                 stage_events.append(("p2p", e0, e1))
         # M2L (+ fused F2L) into the local slots
         self.local.zero_()
-        if self.m2l_variant == "rows_derived":
-            _lib.call("defmm_m2l_rows_c128", L, self.row_slot.shape[0], self.row_slot, self.row_ptr,
+        if self.m2l_variant == "derived":
+            _lib.call(self._op("m2l_rows"), L, self.row_slot.shape[0], self.row_slot, self.row_ptr,
                       self.row_entries, self.hat, self.sym_derived, self.local, sh)
-        elif self.m2l_variant == "rows":
-            _lib.call("defmm_m2l_c128", L, self.row_slot.shape[0], self.row_slot, self.row_ptr, self.e_src,
+        elif self.m2l_variant == "canonical" and self.config.dtype == "c128":
+            _lib.call("defmm_m2l_canon_c128", L, self.row_slot.shape[0], self.row_slot, self.row_ptr, self.e_src,
                       self.e_sym, self.e_rid, self.hat, self.sym, self.local, sh)
         else:
-            _lib.call("defmm_m2l_grouped_c128", L, self.n_groups, self.grp_rows, self.grp_ptr, self.grp_runs,
-                      self.hat, self.sym_derived, self.local, sh)
+            raise ValueError(f"unknown M2L variant {self.m2l_variant!r} for dtype {self.config.dtype}")
         if stage_events is not None:
             c = ev()
             c.record(stream)
             stage_events.append(("m2l", b, c))
         # downward: L2L per level top-down, then L2P + near + un-permute
         for son_beta, outs, octant, ptr, src, sdir, n in self.l2l:
-            _lib.call("defmm_l2l_c128", L, n, outs, octant, ptr, src, sdir, son_beta, self.dirs, kappa,
+            _lib.call(self._op("l2l"), L, n, outs, octant, ptr, src, sdir, son_beta, self.dirs, kappa,
                       self.local, sh)
         stream.wait_stream(side)
-        _lib.call("defmm_l2p_c128", L, self.leaf_cell.shape[0], self.leaf_cell, self.leaf_lo, self.leaf_hi,
+        _lib.call(self._op("l2p"), L, self.leaf_cell.shape[0], self.leaf_cell, self.leaf_lo, self.leaf_hi,
                   self.slot_dir, tg["start"], tg["stop"], tg["alpha"], tg["level"], tg["beta"], self.dirs,
                   *self.t_xyz, kappa, self.local, self.near, self.t_perm, out, sh)
         if stage_events is not None:
@@ -269,7 +263,7 @@ def run_fmm_full(targets, sources, charges, config: FmmConfig = FmmConfig(), eve
     info.hf_max_level = plan.plan.hf_max
     stages = []
     out = plan.apply(stage_events=stages)
-    pot = out.cpu().numpy()
+    pot = out.cpu().numpy().astype(np.complex128)  # fresh complex128 array (tree.py:224-228)
     for k, v in plan.timings.items():
         info.timings[k] = v
     el = {name: a.elapsed_time(b) / 1e3 for name, a, b in stages}

@@ -146,13 +146,9 @@ class Plan:
     p2p_ptr: np.ndarray = None
     p2p_lo: np.ndarray = None
     p2p_hi: np.ndarray = None
-    # derived symbols + grouped M2L (v2 kernel)
-    trans_canon: np.ndarray = None  # per distinct (level, t): canonical symbol id
-    trans_rid: np.ndarray = None
-    group_size: int = 8
-    grp_rows: np.ndarray = None  # (ngroups, G) local slots, -1 padded
-    grp_ptr: np.ndarray = None
-    grp_runs: np.ndarray = None  # (nruns, G+2) int32 {hat, row mask, trans per row}
+    # derived symbols (one per distinct (level, translation))
+    trans_canon: np.ndarray = None  # canonical symbol id
+    trans_rid: np.ndarray = None  # cube-group rotation id
     # event logs (optional, for the events= API)
     m2l_events: tuple = None
     p2p_events: tuple = None
@@ -366,11 +362,9 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
     ent[:, 1] = inv[order_ev]
     plan.m2l_rows_entries = ent
     plan.m2l_level = tt.level[l_cell[rows]]
-    # derived-symbol table (one per distinct (level, t)) and sibling groups
+    # derived-symbol table: one per distinct (level, t)
     plan.trans_canon = cinv.astype(np.int32)
     plan.trans_rid = rid
-    plan.group_size = group_size(order)
-    _group_rows(plan, tt, l_cell, l_loc, tslot, src_hat, inv)
 
     # L2L gather lists per son level
     l2l_levels = []
@@ -437,57 +431,6 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
         plan.m2l_events = (mt, ms, ev_dir)
         plan.p2p_events = (pt, ps)
     return plan
-
-
-def group_size(order: int) -> int:
-    """Rows per M2L group (must equal defmm_m2l_group_size in the library)."""
-    return 8 if order <= 5 else (4 if order == 6 else 2)
-
-
-def _group_rows(plan, tt, l_cell, l_loc, tslot, src_hat, trans):
-    """Sibling groups for the v2 M2L kernel: rows sharing (level, key, parent)
-    ordered key-major (derived symbols of one key stay L2-resident) and then
-    in Morton order; entries of a group sorted by source spectrum."""
-    G = plan.group_size
-    rows = plan.m2l_row_slot
-    rc = l_cell[rows]
-    key = l_loc[rows]
-    lev = tt.level[rc]
-    par = tt.parent[rc]
-    o = np.lexsort((rc, par, key, lev))
-    rows_o = rows[o]
-    brk = np.ones(rows_o.shape[0], bool)
-    brk[1:] = (lev[o][1:] != lev[o][:-1]) | (key[o][1:] != key[o][:-1]) | (par[o][1:] != par[o][:-1])
-    gstart = np.nonzero(brk)[0]
-    # position inside the sibling set, then chunk into groups of <= G rows
-    sib = np.arange(rows_o.shape[0]) - np.repeat(gstart, np.diff(np.append(gstart, rows_o.shape[0])))
-    new_group = brk | (sib % G == 0)
-    gid = np.cumsum(new_group) - 1
-    ngroups = int(gid[-1]) + 1 if gid.size else 0
-    pos = sib % G
-    grp_rows = np.full((ngroups, G), -1, np.int64)
-    grp_rows[gid, pos] = rows_o
-    # event -> (group, position): rows are slot ids; map through a slot-indexed table
-    slot_g = np.full(plan.n_local if plan.l_cell is not None else int(rows.max()) + 1, -1, np.int64)
-    slot_p = np.zeros_like(slot_g)
-    slot_g[rows_o] = gid
-    slot_p[rows_o] = pos
-    eg = slot_g[tslot]
-    ea = slot_p[tslot]
-    eo = np.lexsort((ea, src_hat, eg))
-    eg, ea, es, et = eg[eo], ea[eo], src_hat[eo], trans[eo]
-    # one run per (group, source): mask of rows + derived symbol per row
-    brk = np.ones(eg.shape[0], bool)
-    brk[1:] = (eg[1:] != eg[:-1]) | (es[1:] != es[:-1])
-    rid_ = np.cumsum(brk) - 1
-    nruns = int(rid_[-1]) + 1 if rid_.size else 0
-    runs = np.zeros((nruns, G + 2), np.int64)
-    runs[:, 0] = es[brk]
-    np.bitwise_or.at(runs[:, 1], rid_, (1 << ea).astype(np.int64))
-    runs[rid_, 2 + ea] = et
-    plan.grp_rows = grp_rows
-    plan.grp_ptr = np.searchsorted(eg[brk], np.arange(ngroups + 1)).astype(np.int64)
-    plan.grp_runs = runs.astype(np.int32)
 
 
 def _check_stencils(sym_t, sym_lev, tree, order, tol):

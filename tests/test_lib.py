@@ -10,8 +10,14 @@ from paper_2202_04894_b200 import _lib
 
 
 def _declared():
+    """Every entry point the header declares (typed families expanded)."""
     src = open(os.path.join(ROOT, "include", "defmm_b200.h")).read()
-    return sorted(set(re.findall(r"\b(defmm_[a-z0-9_]+)\s*\(", src)))
+    names = set(re.findall(r"\b(defmm_[a-z0-9_]+)\s*\(", src))
+    typed = {n for n in names if n.endswith("##SUFFIX")} | set(re.findall(r"\b(defmm_[a-z0-9_]+)_##SUFFIX", src))
+    names = {n for n in names if "##" not in n and n != "defmm_tree"}
+    for suffix in re.findall(r"^DEFMM_DECLARE_TYPED\((\w+)\)", src, re.M):
+        names |= {f"{t}_{suffix}" for t in typed if "##" not in t}
+    return sorted(names)
 
 
 def test_header_and_binding_agree():
