@@ -43,6 +43,7 @@ def _args():
     ap.add_argument("--cpu-sample", type=int, default=20000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dtype", default=None, choices=[None, "c128", "c64"], help="override the workload dtype")
+    ap.add_argument("--p2p-overlap", default=None, choices=[None, "upward", "m2l"])
     ap.add_argument("--m2l", default=None, help="M2L kernel variant (derived | canonical)")
     return ap.parse_args()
 
@@ -196,6 +197,8 @@ def run_b200(args):
     setup_s = time.perf_counter() - t0
     if args.m2l:
         plan.m2l_variant = args.m2l
+    if args.p2p_overlap:
+        plan.p2p_overlap = args.p2p_overlap
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
 

@@ -135,6 +135,11 @@ int defmm_m2l_canon_c128(int32_t L, int64_t nrows, const int64_t* row_slot, cons
                          const int32_t* e_src, const int32_t* e_sym, const int8_t* e_rid,
                          const void* hat, const void* sym, void* local, void* stream);
 
+/* Entries between consecutive P^3 spectra (hat, sym, sym_derived): P^3 for
+ * c128, P^3 rounded up to even for c64 (aligned 16-B vector loads; the pad
+ * entry is written as 0). */
+int defmm_spectrum_stride(int32_t L, int32_t c64);
+
 /* K10 direct sum -- kernel.py:58-75: out[i] = sum_s G(|t_i - y_s|) q_s (FP64).
  * workspace: defmm_direct_workspace_bytes(nt) bytes of device memory. */
 int64_t defmm_direct_workspace_bytes(int64_t nt);

@@ -25,6 +25,7 @@ _SIGS = {
     "defmm_tree_free": [_vp],
     "defmm_m2l_canon_c128": [_i32, _i64] + [_vp] * 9,
     "defmm_direct_workspace_bytes": [_i64],
+    "defmm_spectrum_stride": [_i32, _i32],
     "defmm_direct_c128": [_i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _f64, _f64, _vp, _vp, _vp],
 }
 for _t in ("c128", "c64"):

@@ -144,6 +144,12 @@ template <int L>
 __host__ __device__ constexpr int pad() { return 2 * L - 1; }
 template <int L>
 __host__ __device__ constexpr int per_lane() { return (cube<L>() + 31) / 32; }
+// stride (in complex entries) of one P^3 spectrum in HBM: padded to an even
+// count for complex64 so two entries form one aligned 16-B vector load
+template <typename R, int L>
+__host__ __device__ constexpr int spec_stride() {
+    return sizeof(R) == 4 ? (pad<L>() * pad<L>() * pad<L>() + 1) / 2 * 2 : pad<L>() * pad<L>() * pad<L>();
+}
 
 // M2M/L2L factor tables A_bit[k][j] = S_k((bit + x_j)/2), bit in {0,1}
 // (interpolation.py:140-148), computed once per CTA in shared memory.
@@ -458,13 +464,16 @@ __global__ void __launch_bounds__(32 * M2F_WARPS) m2f_kernel(int64_t n, const in
     }
     __syncwarp();
     const R scale = (R)(1.0 / (P * sqrt((double)P)));
-    V* out = hat + i * (int64_t)P3;
-    for (int t = lane; t < P3; t += 32) {
+    constexpr int SS = spec_stride<R, L>();
+    V* out = hat + i * (int64_t)SS;
+    for (int t = lane; t < SS; t += 32) {
         const int f0 = t / (P * P), f12 = t % (P * P);
         V v = cz<V>();
+        if (t < P3) {
 #pragma unroll
-        for (int a = 0; a < L; ++a) v = cfma(Y2[a * P * P + f12], tw[(f0 * a) % P], v);
-        out[t] = cscale(v, scale);
+            for (int a = 0; a < L; ++a) v = cfma(Y2[a * P * P + f12], tw[(f0 * a) % P], v);
+        }
+        out[t] = cscale(v, scale);  // the pad entry (c64) is written as 0
     }
 }
 
@@ -508,11 +517,13 @@ __global__ void __launch_bounds__(256) symbols_kernel(int64_t n, const int32_t* 
         A[t] = v;
     }
     __syncthreads();
-    cx<R>* out = sym + i * (int64_t)P3;
-    for (int t = threadIdx.x; t < P3; t += blockDim.x) {
+    constexpr int SS = spec_stride<R, L>();
+    cx<R>* out = sym + i * (int64_t)SS;
+    for (int t = threadIdx.x; t < SS; t += blockDim.x) {
         const int f = t / (P * P), bc = t % (P * P);
         double2 v = make_double2(0.0, 0.0);
-        for (int k = 0; k < P; ++k) v = cfma(A[k * P * P + bc], tw[(f * k) % P], v);
+        if (t < P3)
+            for (int k = 0; k < P; ++k) v = cfma(A[k * P * P + bc], tw[(f * k) % P], v);
         out[t] = from_d<cx<R>>(v);
     }
 }
@@ -547,9 +558,10 @@ __global__ void __launch_bounds__(256) expand_symbols_kernel(int64_t n, const in
     constexpr int P = pad<L>(), P3 = P * P * P;
     const int64_t i = blockIdx.x;
     const int r = rid[i];
-    const cx<R>* src = symc + (int64_t)canon[i] * P3;
-    cx<R>* dst = symd + i * P3;
-    for (int j = threadIdx.x; j < P3; j += blockDim.x) dst[j] = src[rotated_index<P>(j, r)];
+    constexpr int SS = spec_stride<R, L>();
+    const cx<R>* src = symc + (int64_t)canon[i] * SS;
+    cx<R>* dst = symd + i * SS;
+    for (int j = threadIdx.x; j < SS; j += blockDim.x) dst[j] = j < P3 ? src[rotated_index<P>(j, r)] : cz<cx<R>>();
 }
 
 // ---------------------------------------------------------------------------
@@ -558,6 +570,15 @@ __global__ void __launch_bounds__(256) expand_symbols_kernel(int64_t n, const in
 template <int L>
 __host__ __device__ constexpr int m2l_threads() {
     return L <= 3 ? 128 : L == 4 ? 352 : L == 5 ? 256 : L == 6 ? 448 : L == 7 ? 320 : 384;
+}
+// complex64: one thread per PAIR of frequencies (16-B loads)
+template <int L>
+__host__ __device__ constexpr int m2l_threads_c64() {
+    return L <= 2 ? 32 : L == 3 ? 64 : L == 4 ? 192 : L == 5 ? 384 : L == 6 ? 352 : L == 7 ? 384 : 576;
+}
+template <typename R, int L>
+__host__ __device__ constexpr int m2l_block() {
+    return sizeof(R) == 4 ? m2l_threads_c64<L>() : m2l_threads<L>();
 }
 
 // pruned inverse DFT of one accumulated spectrum X (P^3, smem) into an L^3
@@ -592,59 +613,74 @@ __device__ __forceinline__ void f2l_row(const V* tw, V* X, V* Z1, V* out, int nt
 }
 
 // Product M2L: one CTA per target row (= local slot with >= 1 M2L source),
-// entries {source spectrum, derived symbol} streamed coalesced, two entries in
-// flight per iteration, accumulation and F2L in FP64 for both storage types.
+// entries {source spectrum, derived symbol} streamed coalesced, two entries
+// in flight per iteration, accumulation and F2L in FP64 for both storage types.
 template <typename R, int L>
-__global__ void __launch_bounds__(m2l_threads<L>()) m2l_rows_kernel(
+__global__ void __launch_bounds__(m2l_block<R, L>()) m2l_rows_kernel(
     int64_t nrows, const int64_t* __restrict__ row_slot, const int64_t* __restrict__ row_ptr,
     const int2* __restrict__ ent, const cx<R>* __restrict__ hat, const cx<R>* __restrict__ symd,
     cx<R>* __restrict__ local) {
     constexpr int P = pad<L>(), L3 = cube<L>(), P3 = P * P * P;
-    constexpr int NT = m2l_threads<L>();
-    constexpr int PER = (P3 + NT - 1) / NT;
+    constexpr int SS = spec_stride<R, L>();
+    constexpr int NT = m2l_block<R, L>();
+    constexpr bool VEC = sizeof(R) == 4;     // complex64: two frequencies per thread
+    constexpr int W = VEC ? 2 : 1;           // complex entries per load
+    constexpr int PER = (SS / W + NT - 1) / NT;
     extern __shared__ unsigned char smraw[];
     double2* tw = reinterpret_cast<double2*>(smraw);
     double2* X = tw + P;
-    double2* Z1 = X + P3;
+    double2* Z1 = X + P3 + 1;
     double2* O = Z1 + L * P * P;
     const int64_t row = blockIdx.x;
     make_twiddles<P, double2>(tw);
-    double2 acc[PER], acc2[PER];
+    // two independent entries in flight per iteration (4 was measured slower:
+    // registers -> occupancy); accumulation in FP64
+    double2 acc[2][PER][W];
 #pragma unroll
-    for (int m = 0; m < PER; ++m) acc[m] = acc2[m] = make_double2(0.0, 0.0);
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int m = 0; m < PER; ++m)
+#pragma unroll
+            for (int w = 0; w < W; ++w) acc[u][m][w] = make_double2(0.0, 0.0);
     const int64_t e0 = row_ptr[row], e1 = row_ptr[row + 1];
-    int64_t e = e0;
-    for (; e + 2 <= e1; e += 2) {
-        const int2 a = ent[e], b = ent[e + 1];
-        const cx<R>* Sa = hat + (int64_t)a.x * P3;
-        const cx<R>* Da = symd + (int64_t)a.y * P3;
-        const cx<R>* Sb = hat + (int64_t)b.x * P3;
-        const cx<R>* Db = symd + (int64_t)b.y * P3;
-#pragma unroll
-        for (int m = 0; m < PER; ++m) {
-            const int j = threadIdx.x + m * NT;
-            if (j < P3) {
-                const double2 sa = to_d(__ldg(Sa + j)), da = to_d(__ldg(Da + j));
-                const double2 sb = to_d(__ldg(Sb + j)), db = to_d(__ldg(Db + j));
-                acc[m] = cfma(da, sa, acc[m]);
-                acc2[m] = cfma(db, sb, acc2[m]);
-            }
-        }
-    }
-    if (e < e1) {
+    for (int64_t e = e0; e < e1; e += 2) {
+        const bool two = e + 1 < e1;
         const int2 a = ent[e];
-        const cx<R>* Sa = hat + (int64_t)a.x * P3;
-        const cx<R>* Da = symd + (int64_t)a.y * P3;
+        const int2 b = two ? ent[e + 1] : a;
 #pragma unroll
         for (int m = 0; m < PER; ++m) {
-            const int j = threadIdx.x + m * NT;
-            if (j < P3) acc[m] = cfma(to_d(__ldg(Da + j)), to_d(__ldg(Sa + j)), acc[m]);
+            const int jv = threadIdx.x + m * NT;  // vector index
+            if (jv * W < SS) {
+                if constexpr (VEC) {
+                    const float4 sa = __ldg(reinterpret_cast<const float4*>(hat + (int64_t)a.x * SS) + jv);
+                    const float4 da = __ldg(reinterpret_cast<const float4*>(symd + (int64_t)a.y * SS) + jv);
+                    const float4 sb = __ldg(reinterpret_cast<const float4*>(hat + (int64_t)b.x * SS) + jv);
+                    const float4 db = __ldg(reinterpret_cast<const float4*>(symd + (int64_t)b.y * SS) + jv);
+                    acc[0][m][0] = cfma(make_double2(da.x, da.y), make_double2(sa.x, sa.y), acc[0][m][0]);
+                    acc[0][m][1] = cfma(make_double2(da.z, da.w), make_double2(sa.z, sa.w), acc[0][m][1]);
+                    if (two) {
+                        acc[1][m][0] = cfma(make_double2(db.x, db.y), make_double2(sb.x, sb.y), acc[1][m][0]);
+                        acc[1][m][1] = cfma(make_double2(db.z, db.w), make_double2(sb.z, sb.w), acc[1][m][1]);
+                    }
+                } else {
+                    const double2 sa = to_d(__ldg(hat + (int64_t)a.x * SS + jv));
+                    const double2 da = to_d(__ldg(symd + (int64_t)a.y * SS + jv));
+                    const double2 sb = to_d(__ldg(hat + (int64_t)b.x * SS + jv));
+                    const double2 db = to_d(__ldg(symd + (int64_t)b.y * SS + jv));
+                    acc[0][m][0] = cfma(da, sa, acc[0][m][0]);
+                    if (two) acc[1][m][0] = cfma(db, sb, acc[1][m][0]);
+                }
+            }
         }
     }
 #pragma unroll
     for (int m = 0; m < PER; ++m) {
-        const int j = threadIdx.x + m * NT;
-        if (j < P3) X[j] = cadd(acc[m], acc2[m]);
+        const int jv = threadIdx.x + m * NT;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            const int j = jv * W + w;
+            if (j < P3) X[j] = cadd(acc[0][m][w], acc[1][m][w]);
+        }
     }
     __syncthreads();
     f2l_row<L, double2>(tw, X, Z1, O, NT);
@@ -1021,10 +1057,10 @@ int launch_m2l_rows(int32_t L, int64_t nrows, const int64_t* row_slot, const int
     cudaStream_t s = (cudaStream_t)stream;
     DEFMM_DISPATCH_L(L, {
         constexpr int P = 2 * LL - 1;
-        const size_t bytes = sizeof(double2) * (P + P * P * P + LL * P * P + LL * LL * LL);
+        const size_t bytes = sizeof(double2) * (P + P * P * P + 1 + LL * P * P + LL * LL * LL);
         int rc = set_smem(m2l_rows_kernel<R, LL>, bytes);
         if (rc) return rc;
-        m2l_rows_kernel<R, LL><<<(unsigned)nrows, m2l_threads<LL>(), bytes, s>>>(
+        m2l_rows_kernel<R, LL><<<(unsigned)nrows, m2l_block<R, LL>(), bytes, s>>>(
             nrows, row_slot, row_ptr, (const int2*)entries, (const cx<R>*)hat, (const cx<R>*)symd,
             (cx<R>*)local);
     });
@@ -1140,6 +1176,16 @@ int defmm_m2l_canon_c128(int32_t L, int64_t nrows, const int64_t* row_slot, cons
             (double2*)local);
     });
     return report(cudaGetLastError(), "m2l_canon");
+}
+
+int defmm_spectrum_stride(int32_t L, int32_t c64) {
+    int v = -3;
+    if (c64) {
+        DEFMM_DISPATCH_L(L, v = spec_stride<float, LL>());
+    } else {
+        DEFMM_DISPATCH_L(L, v = spec_stride<double, LL>());
+    }
+    return v;
 }
 
 int64_t defmm_direct_workspace_bytes(int64_t nt) { return (int64_t)DIRECT_SPLIT * nt * (int64_t)sizeof(double2); }

@@ -75,6 +75,8 @@ class FmmPlan:
         i64, i32, f64 = torch.int64, torch.int32, torch.float64
         tt, st = self.tt, self.st
         self.L, self.L3, self.P3 = L, L**3, (2 * L - 1) ** 3
+        # HBM stride of one spectrum (even-padded for complex64 vector loads)
+        self.SS = int(_lib.load().defmm_spectrum_stride(L, int(self.config.dtype == "c64")))
         # particles (sorted order), SoA
         self.s_xyz = [_dev(self.sp.positions[:, k], f64, d) for k in range(3)]
         self.t_xyz = self.s_xyz if self.same else [_dev(self.tp.positions[:, k], f64, d) for k in range(3)]
@@ -124,24 +126,25 @@ class FmmPlan:
         # workspaces (storage precision per FmmConfig.dtype)
         cd = self.cdtype
         self.mult = torch.empty((max(p.n_mult, 1), self.L3), dtype=cd, device=d)
-        self.hat = torch.empty((max(p.n_hat, 1), self.P3), dtype=cd, device=d)
+        self.hat = torch.empty((max(p.n_hat, 1), self.SS), dtype=cd, device=d)
         self.local = torch.empty((max(p.n_local, 1), self.L3), dtype=cd, device=d)
         self.near = torch.empty(self.n_tgt, dtype=cd, device=d)
         self.q = torch.zeros(self.n_src, dtype=cd, device=d)
         self.out = torch.empty(self.n_tgt, dtype=cd, device=d)
         self.side_stream = torch.cuda.Stream(device=d)
         self.m2l_variant = "derived"
+        self.p2p_overlap = "upward"  # or "m2l"
 
     def _symbols(self):
         p = self.plan
-        self.sym = torch.empty((max(p.n_sym, 1), self.P3), dtype=self.cdtype, device=self.device)
+        self.sym = torch.empty((max(p.n_sym, 1), self.SS), dtype=self.cdtype, device=self.device)
         st = torch.cuda.current_stream(self.device).cuda_stream
         if p.n_sym:
             tv = _dev(p.sym_tvec.reshape(-1), torch.int32, self.device)
             beta = _dev(p.sym_beta, torch.float64, self.device)
             _lib.call(self._op("symbols"), self.L, p.n_sym, tv, beta, float(p.kappa), self.sym, st)
         n_tr = int(p.trans_canon.shape[0])
-        self.sym_derived = torch.empty((max(n_tr, 1), self.P3), dtype=self.cdtype, device=self.device)
+        self.sym_derived = torch.empty((max(n_tr, 1), self.SS), dtype=self.cdtype, device=self.device)
         if n_tr:
             _lib.call(self._op("expand_symbols"), self.L, n_tr, _dev(p.trans_canon, torch.int32, self.device),
                       _dev(p.trans_rid, torch.int8, self.device), self.sym, self.sym_derived, st)
@@ -171,6 +174,26 @@ class FmmPlan:
         out = self.out if out is None else out
         ev = (lambda: torch.cuda.Event(enable_timing=True)) if stage_events is not None else None
         sg, tg = self.sg, self.tg
+
+        def near_field():
+            # near field on the side stream (FP-pipe bound), concurrent with the
+            # far field; `p2p_overlap` picks the far-field stage it overlaps
+            side = self.side_stream
+            side.wait_stream(stream)
+            with torch.cuda.stream(side):
+                if stage_events is not None:
+                    e0 = ev()
+                    e0.record(side)
+                _lib.call(self._op("p2p"), p.leaf_cells.shape[0], self.tgt_lo, self.tgt_hi, self.p2p_ptr,
+                          self.p2p_lo, self.p2p_hi, *self.t_xyz, *self.s_xyz, self.q, kappa, float(p.tol),
+                          self.near, side.cuda_stream)
+                if stage_events is not None:
+                    e1 = ev()
+                    e1.record(side)
+                    stage_events.append(("p2p", e0, e1))
+
+        if self.p2p_overlap == "upward":
+            near_field()
         if stage_events is not None:
             a = ev()
             a.record(stream)
@@ -185,21 +208,10 @@ class FmmPlan:
             b = ev()
             b.record(stream)
             stage_events.append(("upward", a, b))
-        # near field on the side stream, concurrent with the (L2-bound) M2L:
-        # P2P is FP64-pipe bound, so the two overlap on the SMs
-        side = self.side_stream
-        side.wait_stream(stream)
-        with torch.cuda.stream(side):
-            if stage_events is not None:
-                e0 = ev()
-                e0.record(side)
-            _lib.call(self._op("p2p"), p.leaf_cells.shape[0], self.tgt_lo, self.tgt_hi, self.p2p_ptr,
-                      self.p2p_lo, self.p2p_hi, *self.t_xyz, *self.s_xyz, self.q, kappa, float(p.tol),
-                      self.near, side.cuda_stream)
-            if stage_events is not None:
-                e1 = ev()
-                e1.record(side)
-                stage_events.append(("p2p", e0, e1))
+        if self.p2p_overlap != "upward":
+            near_field()
+        else:
+            stream.wait_stream(self.side_stream)  # M2L runs alone (clean roofline timing)
         # M2L (+ fused F2L) into the local slots
         self.local.zero_()
         if self.m2l_variant == "derived":
@@ -218,7 +230,7 @@ class FmmPlan:
         for son_beta, outs, octant, ptr, src, sdir, n in self.l2l:
             _lib.call(self._op("l2l"), L, n, outs, octant, ptr, src, sdir, son_beta, self.dirs, kappa,
                       self.local, sh)
-        stream.wait_stream(side)
+        stream.wait_stream(self.side_stream)
         _lib.call(self._op("l2p"), L, self.leaf_cell.shape[0], self.leaf_cell, self.leaf_lo, self.leaf_hi,
                   self.slot_dir, tg["start"], tg["stop"], tg["alpha"], tg["level"], tg["beta"], self.dirs,
                   *self.t_xyz, kappa, self.local, self.near, self.t_perm, out, sh)
