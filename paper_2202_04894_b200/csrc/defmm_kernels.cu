@@ -634,14 +634,18 @@ __global__ void __launch_bounds__(m2l_block<R, L>()) m2l_rows_kernel(
     const int64_t row = blockIdx.x;
     make_twiddles<P, double2>(tw);
     // two independent entries in flight per iteration (4 was measured slower:
-    // registers -> occupancy); accumulation in FP64
-    double2 acc[2][PER][W];
+    // registers -> occupancy).  Products and the two partial sums are formed in
+    // the storage precision (c64: FP32 -- converting every operand to FP64 made
+    // the F2F unit the bottleneck, profiles/r01_summary_v2.md); the partial
+    // sums are combined and transformed (F2L) in FP64.
+    using V = cx<R>;
+    V acc[2][PER][W];
 #pragma unroll
     for (int u = 0; u < 2; ++u)
 #pragma unroll
         for (int m = 0; m < PER; ++m)
 #pragma unroll
-            for (int w = 0; w < W; ++w) acc[u][m][w] = make_double2(0.0, 0.0);
+            for (int w = 0; w < W; ++w) acc[u][m][w] = cz<V>();
     const int64_t e0 = row_ptr[row], e1 = row_ptr[row + 1];
     for (int64_t e = e0; e < e1; e += 2) {
         const bool two = e + 1 < e1;
@@ -656,17 +660,17 @@ __global__ void __launch_bounds__(m2l_block<R, L>()) m2l_rows_kernel(
                     const float4 da = __ldg(reinterpret_cast<const float4*>(symd + (int64_t)a.y * SS) + jv);
                     const float4 sb = __ldg(reinterpret_cast<const float4*>(hat + (int64_t)b.x * SS) + jv);
                     const float4 db = __ldg(reinterpret_cast<const float4*>(symd + (int64_t)b.y * SS) + jv);
-                    acc[0][m][0] = cfma(make_double2(da.x, da.y), make_double2(sa.x, sa.y), acc[0][m][0]);
-                    acc[0][m][1] = cfma(make_double2(da.z, da.w), make_double2(sa.z, sa.w), acc[0][m][1]);
+                    acc[0][m][0] = cfma(make_float2(da.x, da.y), make_float2(sa.x, sa.y), acc[0][m][0]);
+                    acc[0][m][1] = cfma(make_float2(da.z, da.w), make_float2(sa.z, sa.w), acc[0][m][1]);
                     if (two) {
-                        acc[1][m][0] = cfma(make_double2(db.x, db.y), make_double2(sb.x, sb.y), acc[1][m][0]);
-                        acc[1][m][1] = cfma(make_double2(db.z, db.w), make_double2(sb.z, sb.w), acc[1][m][1]);
+                        acc[1][m][0] = cfma(make_float2(db.x, db.y), make_float2(sb.x, sb.y), acc[1][m][0]);
+                        acc[1][m][1] = cfma(make_float2(db.z, db.w), make_float2(sb.z, sb.w), acc[1][m][1]);
                     }
                 } else {
-                    const double2 sa = to_d(__ldg(hat + (int64_t)a.x * SS + jv));
-                    const double2 da = to_d(__ldg(symd + (int64_t)a.y * SS + jv));
-                    const double2 sb = to_d(__ldg(hat + (int64_t)b.x * SS + jv));
-                    const double2 db = to_d(__ldg(symd + (int64_t)b.y * SS + jv));
+                    const V sa = __ldg(hat + (int64_t)a.x * SS + jv);
+                    const V da = __ldg(symd + (int64_t)a.y * SS + jv);
+                    const V sb = __ldg(hat + (int64_t)b.x * SS + jv);
+                    const V db = __ldg(symd + (int64_t)b.y * SS + jv);
                     acc[0][m][0] = cfma(da, sa, acc[0][m][0]);
                     if (two) acc[1][m][0] = cfma(db, sb, acc[1][m][0]);
                 }
@@ -679,7 +683,7 @@ __global__ void __launch_bounds__(m2l_block<R, L>()) m2l_rows_kernel(
 #pragma unroll
         for (int w = 0; w < W; ++w) {
             const int j = jv * W + w;
-            if (j < P3) X[j] = cadd(acc[0][m][w], acc[1][m][w]);
+            if (j < P3) X[j] = cadd(to_d(acc[0][m][w]), to_d(acc[1][m][w]));
         }
     }
     __syncthreads();
