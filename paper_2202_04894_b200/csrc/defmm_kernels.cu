@@ -890,6 +890,94 @@ __global__ void __launch_bounds__(P2P_NT) p2p_kernel(
     }
 }
 
+// complex64 near field: sources staged in shared memory as hi/lo float
+// splits of the FP64 coordinates, so dx = (xt_hi - xs_hi) + (xt_lo - xs_lo)
+// keeps near-field differences accurate without FP64 (SURVEY §7 hard part 6);
+// e^{i kappa r} via an explicit reduction of kappa r / pi to [-1, 1] and the
+// hardware sin/cos (abs. error < 4e-7 on [-pi, pi]); FP32 partial sums per
+// thread, combined with a fixed-order shuffle.
+__device__ __forceinline__ void split_f32(double x, float& hi, float& lo) {
+    hi = __double2float_rn(x);
+    lo = __double2float_rn(x - (double)hi);
+}
+
+__global__ void __launch_bounds__(P2P_NT) p2p_f32_kernel(
+    int64_t n, const int64_t* __restrict__ tgt_lo, const int64_t* __restrict__ tgt_hi,
+    const int64_t* __restrict__ ptr, const int64_t* __restrict__ src_lo,
+    const int64_t* __restrict__ src_hi, const double* __restrict__ tx,
+    const double* __restrict__ ty, const double* __restrict__ tz, const double* __restrict__ px,
+    const double* __restrict__ py, const double* __restrict__ pz, const float2* __restrict__ q,
+    double kappa, double tol, float2* __restrict__ near) {
+    __shared__ float4 sh[P2P_TILE];  // (x_hi, y_hi, z_hi, q.re)
+    __shared__ float4 sl[P2P_TILE];  // (x_lo, y_lo, z_lo, q.im)
+    const int64_t i = blockIdx.x;
+    const int64_t t0 = tgt_lo[i], t1 = tgt_hi[i];
+    const int64_t nt = t1 - t0;
+    const int split = nt <= 16 ? 8 : nt <= 32 ? 4 : nt <= 64 ? 2 : 1;
+    const int per_pass = P2P_NT / split;
+    const float kpi = (float)(kappa / 3.141592653589793);
+    const float ftol = (float)tol;
+    const float inv4pi = (float)(1.0 / (4.0 * 3.141592653589793));
+    const int64_t e0 = ptr[i], e1 = ptr[i + 1];
+    for (int64_t tb = t0; tb < t1; tb += per_pass) {
+        const int64_t t = tb + threadIdx.x / split;
+        const int part = threadIdx.x % split;
+        const bool valid = t < t1;
+        float xh = 0.f, xl = 0.f, yh = 0.f, yl = 0.f, zh = 0.f, zl = 0.f;
+        if (valid) {
+            split_f32(tx[t], xh, xl);
+            split_f32(ty[t], yh, yl);
+            split_f32(tz[t], zh, zl);
+        }
+        float ar = 0.f, ai = 0.f;
+        for (int64_t e = e0; e < e1; ++e) {
+            const int64_t a = src_lo[e], b = src_hi[e];
+            for (int64_t sb = a; sb < b; sb += P2P_TILE) {
+                const int cnt = (int)((b - sb) < P2P_TILE ? (b - sb) : P2P_TILE);
+                __syncthreads();
+                for (int k = threadIdx.x; k < cnt; k += P2P_NT) {
+                    float4 hh, ll;
+                    split_f32(px[sb + k], hh.x, ll.x);
+                    split_f32(py[sb + k], hh.y, ll.y);
+                    split_f32(pz[sb + k], hh.z, ll.z);
+                    const float2 qq = q[sb + k];
+                    hh.w = qq.x;
+                    ll.w = qq.y;
+                    sh[k] = hh;
+                    sl[k] = ll;
+                }
+                __syncthreads();
+                if (valid) {
+#pragma unroll 4
+                    for (int k = part; k < cnt; k += split) {
+                        const float4 h = sh[k], l = sl[k];
+                        const float dx = (xh - h.x) + (xl - l.x);
+                        const float dy = (yh - h.y) + (yl - l.y);
+                        const float dz = (zh - h.z) + (zl - l.z);
+                        const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                        const float rinv = rsqrtf(r2);
+                        const float r = r2 * rinv;
+                        const bool ok = r >= ftol;  // r2 = 0 -> NaN -> masked
+                        float xr = kpi * (ok ? r : 0.0f);
+                        xr = fmaf(-2.0f, rintf(0.5f * xr), xr);  // kappa r / pi reduced to [-1, 1]
+                        float sn, cs;
+                        __sincosf(3.14159265358979f * xr, &sn, &cs);
+                        const float g = ok ? rinv * inv4pi : 0.0f;
+                        const float gr = g * cs, gi = g * sn;
+                        ar = fmaf(gr, h.w, fmaf(-gi, l.w, ar));
+                        ai = fmaf(gr, l.w, fmaf(gi, h.w, ai));
+                    }
+                }
+            }
+        }
+        for (int off = 1; off < split; off <<= 1) {
+            ar += __shfl_xor_sync(0xffffffffu, ar, off);
+            ai += __shfl_xor_sync(0xffffffffu, ai, off);
+        }
+        if (valid && part == 0) near[t] = make_float2(ar, ai);
+    }
+}
+
 // K10: direct sum (FP64).  Sources are split over blockIdx.y so that a few
 // thousand check targets still fill the GPU; partial sums land in
 // part[blockIdx.y][target] and are reduced in a fixed order by direct_reduce.
@@ -1094,9 +1182,15 @@ int launch_p2p(int64_t n, const int64_t* tgt_lo, const int64_t* tgt_hi, const in
                double kappa, double tol, void* near, void* stream) {
     if (n == 0) return 0;
     if (!grid_ok(n)) return -1;
-    p2p_kernel<R><<<(unsigned)n, P2P_NT, 0, (cudaStream_t)stream>>>(n, tgt_lo, tgt_hi, ptr, src_lo, src_hi, tx,
-                                                                    ty, tz, sx, sy, sz, (const cx<R>*)q, kappa,
-                                                                    tol, (cx<R>*)near);
+    if constexpr (sizeof(R) == 4) {
+        p2p_f32_kernel<<<(unsigned)n, P2P_NT, 0, (cudaStream_t)stream>>>(
+            n, tgt_lo, tgt_hi, ptr, src_lo, src_hi, tx, ty, tz, sx, sy, sz, (const float2*)q, kappa, tol,
+            (float2*)near);
+    } else {
+        p2p_kernel<R><<<(unsigned)n, P2P_NT, 0, (cudaStream_t)stream>>>(n, tgt_lo, tgt_hi, ptr, src_lo, src_hi,
+                                                                        tx, ty, tz, sx, sy, sz, (const cx<R>*)q,
+                                                                        kappa, tol, (cx<R>*)near);
+    }
     return report(cudaGetLastError(), "p2p");
 }
 
