@@ -36,12 +36,13 @@ UNIT = "particles/s"
 def _args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="cfg2")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=20000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the other-precision run of the same lists")
     ap.add_argument("--dtype", default=None, choices=[None, "c128", "c64"], help="override the workload dtype")
     ap.add_argument("--p2p-overlap", default=None, choices=[None, "upward", "m2l"])
     ap.add_argument("--m2l", default=None, help="M2L kernel variant (derived | canonical)")
@@ -88,7 +89,7 @@ class _Clocks:
         self.proc = None
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200"],
+                ["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -134,23 +135,29 @@ def _measured_peak_hbm():
 
 
 def run_reference(args):
+    """The reference's CPU path on this host: the numpy restatement of helmfmm's
+    matvec (oracle/defmm_oracle.py; the Python reference itself cannot travel
+    to the GPU box).  Each step = one oracle matvec on a bounded sample of the
+    workload (the first n points, same kappa/L/ncrit), n sized so the whole run
+    takes about two minutes.  Single-threaded by design like the reference
+    (SPEC.md:467)."""
     from paper_2202_04894_b200.workloads import WORKLOADS
 
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     w = WORKLOADS[args.workload]
-    vals = []
-    for _ in range(max(args.warmup, 0)):
-        pass  # the oracle has no warm state worth priming; warm-up steps are not repeated
-    t0 = time.perf_counter()
+    n_sample = int(min(max(120.0 / max(args.steps, 1) * 1000.0, 2000), args.cpu_sample))
+    vals, walls = [], []
     for _ in range(args.steps):
-        v, tm, counts = _cpu_oracle_sample(args.workload, args.cpu_sample)
+        t0 = time.perf_counter()
+        v, tm, counts = _cpu_oracle_sample(args.workload, n_sample)
+        walls.append(time.perf_counter() - t0)
         vals.append(v)
-    wall = time.perf_counter() - t0
     value = float(np.median(vals))
     cfg = _workload_desc(w, w.n)
-    sample = f"first {args.cpu_sample} points of the {w.name} distribution, same kappa/L/ncrit; matvec stages only"
+    sample = (f"oracle matvec (upward + M2L/P2P + downward, complex128) on the first {n_sample} points of the "
+              f"{w.name} distribution, same kappa/L/ncrit")
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -159,7 +166,7 @@ def run_reference(args):
         "n_gpus": args.gpus,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": 1e3 * wall / max(args.steps, 1),
+        "ms_per_step": 1e3 * float(np.median(walls)),
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
@@ -170,6 +177,60 @@ def run_reference(args):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _measure(plan, steps, warmup, flush, barrier, dist_max):
+    """Device-resident matvecs: per-step and per-stage CUDA-event times (ms)."""
+    import torch
+
+    dev = plan.device
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(warmup):
+        plan.apply()
+    barrier()
+    tot = {"step": 0.0, "upward": 0.0, "m2l": 0.0, "p2p": 0.0, "downward": 0.0}
+    for _ in range(steps):
+        flush.zero_()  # evict L2 between iterations (outside the timed events)
+        stages = []
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        plan.apply(stage_events=stages)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        tot["step"] += a.elapsed_time(b)
+        for nm, x, y in stages:
+            tot[nm] += x.elapsed_time(y)
+    barrier()
+    out = {k: v / max(steps, 1) for k, v in tot.items()}
+    out["step"] = dist_max(out["step"])
+    return out
+
+
+def _measure_e2e(plan, q, steps, warmup, flush, barrier, dist_max):
+    """Public-API matvec with HOST buffers: pinned H2D charges + D2H potentials."""
+    import torch
+
+    dev = plan.device
+    stream = torch.cuda.current_stream(dev)
+    q_host = torch.as_tensor(q).to(plan.cdtype).pin_memory()
+    out_host = torch.empty(q_host.shape[0], dtype=plan.cdtype).pin_memory()
+    for _ in range(max(1, warmup)):
+        plan.set_charges(q_host.to(dev, non_blocking=True))
+        out_host.copy_(plan.apply(), non_blocking=True)
+    barrier()
+    e_ms = 0.0
+    for _ in range(steps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        plan.set_charges(q_host.to(dev, non_blocking=True))
+        out_host.copy_(plan.apply(), non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        e_ms += a.elapsed_time(b)
+    return dist_max(e_ms / max(steps, 1)), out_host.numpy(), q_host.element_size() * q_host.shape[0]
 
 
 def run_b200(args):
@@ -188,9 +249,22 @@ def run_b200(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def dist_max(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     pts, q, kappa, w = make_workload(args.workload)
     n = pts.shape[0]
     dtype = args.dtype or w.dtype
+    other = "c128" if dtype == "c64" else "c64"
     cfg = FmmConfig(order=w.order, ncrit=w.ncrit, kappa=kappa, dtype=dtype)
     t0 = time.perf_counter()
     plan = FmmPlan(pts, None, cfg, device=dev, charges=q)
@@ -199,71 +273,21 @@ def run_b200(args):
         plan.m2l_variant = args.m2l
     if args.p2p_overlap:
         plan.p2p_overlap = args.p2p_overlap
-    stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
-
-    # --- device-resident matvec (value) --------------------------------
-    for _ in range(args.warmup):
-        plan.apply()
-    barrier()
     clocks = _Clocks(local)
-    tot_ms, m2l_ms, p2p_ms, up_ms, down_ms = 0.0, 0.0, 0.0, 0.0, 0.0
-    for _ in range(args.steps):
-        flush.zero_()  # evict L2 between iterations (outside the timed events)
-        stages = []
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        plan.apply(stage_events=stages)
-        b.record(stream)
-        torch.cuda.synchronize(dev)
-        tot_ms += a.elapsed_time(b)
-        el = {nm: x.elapsed_time(y) for nm, x, y in stages}
-        m2l_ms += el["m2l"]
-        p2p_ms += el["p2p"]
-        up_ms += el["upward"]
-        down_ms += el["downward"]
-    barrier()
+    st = _measure(plan, args.steps, args.warmup, flush, barrier, dist_max)
+    e_step, pot, qbytes = _measure_e2e(plan, q, args.steps, args.warmup, flush, barrier, dist_max)
+    st2 = None
+    if not args.no_secondary:
+        plan2 = FmmPlan(pts, None, FmmConfig(order=w.order, ncrit=w.ncrit, kappa=kappa, dtype=other),
+                        device=dev, charges=q, reuse=plan)
+        st2 = _measure(plan2, args.steps, args.warmup, flush, barrier, dist_max)
+        del plan2
     clk = clocks.stop()
-    K = max(args.steps, 1)
-    t_step = tot_ms / K
-    if world > 1:
-        tt = torch.tensor([t_step], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_step = float(tt.item())
-    value = world * n / (t_step / 1e3)  # replicas: every rank runs the full matvec
+    value = world * n / (st["step"] / 1e3)  # replicas: every rank runs the full matvec
 
-    # --- end to end through the public plan API with host buffers -------
-    q_host = torch.as_tensor(q).to(plan.cdtype).pin_memory()
-    out_host = torch.empty(n, dtype=plan.cdtype).pin_memory()
-    for _ in range(max(1, args.warmup)):
-        plan.set_charges(q_host.to(dev, non_blocking=True))
-        out_host.copy_(plan.apply(), non_blocking=True)
-    barrier()
-    e_ms = 0.0
-    for _ in range(args.steps):
-        flush.zero_()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        plan.set_charges(q_host.to(dev, non_blocking=True))
-        out_host.copy_(plan.apply(), non_blocking=True)
-        b.record(stream)
-        torch.cuda.synchronize(dev)
-        e_ms += a.elapsed_time(b)
-    e_step = e_ms / K
-    if world > 1:
-        tt = torch.tensor([e_step], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e_step = float(tt.item())
-
-    # --- accuracy on the 1000 sampled check targets ------------------------
-    pot = out_host.numpy()
+    # accuracy on the 1000 sampled check targets (BASELINE: "at fixed rel. L2 error")
     s = sample_targets(n)
     side = plan.st.root_box.side
     d = direct_sum(HelmholtzKernel(kappa=kappa, singularity_tol=1e-12 * side), pts[s], pts, q, device=dev)
@@ -274,7 +298,7 @@ def run_b200(args):
             dist.destroy_process_group()
         return
 
-    # --- roofline of the dominant kernel (M2L + fused F2L) -----------------
+    # roofline of the dominant kernel (M2L + fused F2L), timed alone on the main stream
     p = plan.plan
     L = w.order
     P3 = (2 * L - 1) ** 3
@@ -282,7 +306,7 @@ def run_b200(args):
     n_m2l = p.counts["m2l_events"]
     rows = p.m2l_row_slot.shape[0]
     alg_bytes = n_m2l * 2 * P3 * c + rows * L**3 * c  # symbol + source spectrum per event, local write
-    m2l_s = (m2l_ms / K) / 1e3
+    m2l_s = st["m2l"] / 1e3
     peak, peak_kind = _measured_peak_hbm()
     achieved = alg_bytes / m2l_s / 1e9
     line = {
@@ -292,27 +316,32 @@ def run_b200(args):
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": t_step,
+        "ms_per_step": st["step"],
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f64" if dtype == "c128" else "f32 (FP64 sums)",
+        "dtype": "f32 storage, f64 sums" if dtype == "c64" else "f64",
         "data": "synthetic",
         "config": dict(_workload_desc(w, n, dtype), l2_flush="256 MiB memset between timed iterations",
                        parallelism=f"replicas{world}" if world > 1 else "single"),
-        "stages_ms": {"upward": up_ms / K, "m2l": m2l_ms / K, "p2p_concurrent": p2p_ms / K,
-                      "downward": down_ms / K},
-        "roofline": {"bound": "hbm", "kernel": "defmm m2l_kernel (Hadamard M2L + fused F2L)",
+        "stages_ms": {"upward_with_concurrent_p2p": st["upward"], "m2l": st["m2l"], "p2p": st["p2p"],
+                      "downward": st["downward"]},
+        "roofline": {"bound": "hbm", "kernel": f"m2l_rows_kernel<{'float' if dtype == 'c64' else 'double'}, {L}>",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
-                     "alg_bytes_per_launch": alg_bytes, "kernel_ms": m2l_s * 1e3},
-        "e2e": {"value": world * n / (e_step / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(n * c),
-                "d2h_bytes_per_step": int(n * c), "ms_per_step": e_step},
-        "accuracy": {"rel_l2_vs_direct_1000": eps},
+                     "frac": achieved / peak, "traffic": None, "alg_bytes_per_launch": alg_bytes,
+                     "kernel_ms": st["m2l"],
+                     "note": "algorithmic bytes = 2 spectra per M2L event + local write; frac > 1 = L2 reuse"},
+        "e2e": {"value": world * n / (e_step / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(qbytes),
+                "d2h_bytes_per_step": int(qbytes), "ms_per_step": e_step},
+        "accuracy": {"rel_l2_vs_direct_1000": eps, "eps_ref_reference": 1.0386568720063353e-2
+                     if args.workload == "cfg2" else None},
         "gpu_launches": int(args.steps * plan.launches_per_apply),
         "clocks": clk,
         "setup_s": setup_s,
     }
+    if st2 is not None:
+        line[f"{other}_same_lists"] = {"value": world * n / (st2["step"] / 1e3), "ms_per_step": st2["step"],
+                                       "m2l_ms": st2["m2l"], "p2p_ms": st2["p2p"]}
     if not args.no_cpu_baseline:
         v, tm, counts = _cpu_oracle_sample(args.workload, args.cpu_sample)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "port",

@@ -33,12 +33,32 @@ class FmmPlan:
     a target/source pair sharing one root box, traversal.py:449-461)."""
 
     def __init__(self, targets, sources=None, config: FmmConfig = FmmConfig(), device="cuda",
-                 keep_events: bool = False, charges=None):
+                 keep_events: bool = False, charges=None, reuse: "FmmPlan | None" = None):
+        """``reuse``: share the host tree + lists of an existing plan built for
+        the same geometry and (order, ncrit, eta, kappa) -- e.g. to run the same
+        lists at another storage precision."""
         if not torch.cuda.is_available():
             raise RuntimeError("the defmm B200 path needs a CUDA device (no CPU fallback)")
         _lib.load()
         self.config = config
         self.device = torch.device(device)
+        if reuse is not None:
+            rc = reuse.config
+            if (rc.order, rc.ncrit, rc.eta, rc.kappa, rc.hf_switch, rc.hard_depth_cap) != (
+                    config.order, config.ncrit, config.eta, config.kappa, config.hf_switch, config.hard_depth_cap):
+                raise ValueError("reuse= needs a plan built with the same list parameters")
+            self.same = reuse.same
+            self.tt, self.st, self.tp, self.sp = reuse.tt, reuse.st, reuse.tp, reuse.sp
+            self.plan = reuse.plan
+            self.timings = dict(reuse.timings)
+            t2 = time.perf_counter()
+            self._upload()
+            self._symbols()
+            torch.cuda.synchronize(self.device)
+            self.timings["precompute"] = time.perf_counter() - t2
+            if charges is not None:
+                self.set_charges(charges)
+            return
         t0 = time.perf_counter()
         tree_cfg = TreeConfig(ncrit=config.ncrit, hard_depth_cap=config.hard_depth_cap)
         same = sources is None or targets is sources
