@@ -47,3 +47,22 @@ def load_ref(name):
 @pytest.fixture(scope="session")
 def operators():
     return np.load(os.path.join(GOLDEN, "operators.npz"))
+
+
+def two_tree_cases():
+    return sorted(os.path.basename(p)[4:-4] for p in glob.glob(os.path.join(GOLDEN, "two_*.npz")))
+
+
+def load_two_tree(name):
+    d = np.load(os.path.join(GOLDEN, f"two_{name}.npz"))
+    return {
+        "targets": d["targets"],
+        "sources": d["sources"],
+        "charges": d["charges"],
+        "config": json.loads(str(d["config"])),
+        "pot": d["pot"],
+        "counts": json.loads(str(d["counts"])),
+        "hf_max": int(d["hf_max"]),
+        "m2l": d["m2l"],
+        "p2p": d["p2p"],
+    }

@@ -85,6 +85,51 @@ def _event_arrays(events):
     return np.array(m2l, np.int64).reshape(-1, 5), np.array(p2p, np.int64).reshape(-1, 4)
 
 
+def _two_tree_cases():
+    """(name, targets, sources, charges, FmmConfig kwargs) -- traversal.py:453-461."""
+    out = []
+    rng = np.random.default_rng(3)
+    sources = rng.uniform(size=(400, 3))
+    targets = rng.uniform(size=(150, 3)) * [1.0, 1.0, 0.2] + [0.0, 0.0, 1.5]
+    q = rng.uniform(size=400) + 1j * rng.uniform(size=400)
+    out.append(("tt_distinct400", targets, sources, q, dict(order=5, ncrit=32, kappa=0.0)))
+    src = make_points("sphere", 2500, 0)
+    tgt = make_points("cube-surface", 1200, 5) * 0.7
+    qq = make_charges(2500, 1)
+    box = compute_root_box(np.vstack([tgt, src]))
+    out.append(("tt_hf_sphere", tgt, src, qq, dict(order=4, ncrit=32, kappa=24.0 / box.side)))
+    return out
+
+
+def two_tree_cases():
+    for name, tgt, src, q, kw in _two_tree_cases():
+        cfg = FmmConfig(**kw)
+        events = []
+        pot, info = run_fmm_full(tgt, src, q, cfg, events=events)
+        m2l = []
+        p2p = []
+        for ev in events:
+            t, s_ = ev.target, ev.source
+            if ev.kind == "M2L":
+                e, i = ev.direction if ev.direction is not None else (-1, -1)
+                m2l.append((t.level, t.key.code, s_.key.code, e, i))
+            else:
+                p2p.append((t.level, t.key.code, s_.level, s_.key.code))
+        np.savez_compressed(
+            os.path.join(HERE, f"two_{name}.npz"),
+            targets=tgt,
+            sources=src,
+            charges=q,
+            config=json.dumps(kw),
+            pot=pot,
+            counts=json.dumps(info.counts),
+            hf_max=info.hf_max_level,
+            m2l=np.array(m2l, np.int64).reshape(-1, 5),
+            p2p=np.array(p2p, np.int64).reshape(-1, 4),
+        )
+        print(name, info.counts, "hf_max", info.hf_max_level)
+
+
 def fmm_cases():
     for name, pts, q, kw in _cases():
         cfg = FmmConfig(**kw)
@@ -159,5 +204,11 @@ def operators():
 
 
 if __name__ == "__main__":
-    operators()
-    fmm_cases()
+    import sys as _sys
+
+    if "--two-tree-only" in _sys.argv:
+        two_tree_cases()
+    else:
+        operators()
+        fmm_cases()
+        two_tree_cases()

@@ -198,3 +198,37 @@ def test_cfg2_full_size_sampled_parity(name, dtype):
     d = direct_sum(HelmholtzKernel(kappa=k, singularity_tol=1e-12 * side), pts[s], pts, q)
     assert _rel(d, ref["direct_sample"]) <= 1e-12
     assert _rel(pot[s], d) <= (1 + 1e-2) * eps_ref
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("case", __import__("conftest").two_tree_cases())
+def test_two_tree_run_fmm_matches_reference(case, dtype):
+    """test_traversal.py:173-181 analogue against the reference's own output."""
+    from conftest import load_two_tree
+    from paper_2202_04894_b200 import FmmConfig, run_fmm_full
+
+    g = load_two_tree(case)
+    pot, info = run_fmm_full(g["targets"], g["sources"], g["charges"], FmmConfig(dtype=dtype, **g["config"]))
+    assert info.counts == g["counts"]
+    assert pot.shape == (len(g["targets"]),)
+    assert _rel(pot, g["pot"]) <= (FP64_TOL if dtype == "c128" else C64_TOL)
+
+
+def test_event_log_partitions_all_pairs():
+    """test_traversal.py:190-201: events= receives every M2L/P2P event; their
+    particle blocks cover every (target, source) pair exactly once."""
+    from paper_2202_04894_b200 import FmmConfig, run_fmm_full
+
+    g = load_case("volume3000")
+    events = []
+    pot, info = run_fmm_full(g["points"], g["points"], g["charges"], FmmConfig(**g["config"]), events=events)
+    n = len(g["points"])
+    cov = np.zeros((n, n), np.int8)
+    for ev in events:
+        cov[ev.target.start : ev.target.stop, ev.source.start : ev.source.stop] += 1
+    assert np.all(cov == 1)
+    assert info.counts["m2l_events"] == sum(1 for e in events if e.kind == "M2L")
+    ref = sorted(map(tuple, g["m2l"].tolist()))
+    mine = sorted((e.target.level, e.target.key.code, e.source.key.code, *(e.direction or (-1, -1)))
+                  for e in events if e.kind == "M2L")
+    assert mine == ref

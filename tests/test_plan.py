@@ -142,3 +142,31 @@ def test_mac_violation_raises():
     _check_stencils(np.array([[2, 0, 0]]), np.array([2]), tr, 4, 1e-12)
     with pytest.raises(ValueError):
         _check_stencils(np.array([[1, 0, 0]]), np.array([2]), tr, 4, 1e-12)
+
+
+@pytest.mark.parametrize("case", __import__("conftest").two_tree_cases())
+def test_two_tree_plan_matches_reference(case):
+    """targets is not sources: two trees on one root box (traversal.py:453-461);
+    counts and both event lists equal the reference's."""
+    from conftest import load_two_tree
+    from paper_2202_04894_b200.geometry import compute_root_box
+
+    g = load_two_tree(case)
+    kw = g["config"]
+    box = compute_root_box(np.vstack([g["targets"], g["sources"]]))
+    cfg = TreeConfig(ncrit=kw["ncrit"])
+    st, sp = build_tree(g["sources"], g["charges"], cfg, root_box=box)
+    tt, tp = build_tree(g["targets"], np.zeros(len(g["targets"])), cfg, root_box=box)
+    pl = build_plan(tt, st, kw["order"], kw["kappa"], 1.0, 2.0, keep_events=True)
+    assert pl.hf_max == g["hf_max"]
+    assert {k: pl.counts[k] for k in g["counts"]} == g["counts"]
+    tc = tt.morton_code(np.arange(tt.n_cells)).astype(np.int64)
+    sc = st.morton_code(np.arange(st.n_cells)).astype(np.int64)
+    mt, ms, ed = pl.m2l_events
+    e = np.where(ed >= 0, pl.hf_max - tt.level[mt], -1)
+    i = np.where(ed >= 0, ed - pl.dir_off[np.maximum(e, 0)], -1)
+    mine = sorted(zip(tt.level[mt].tolist(), tc[mt].tolist(), sc[ms].tolist(), e.tolist(), i.tolist()))
+    assert mine == sorted(map(tuple, g["m2l"].tolist()))
+    pt, pss = pl.p2p_events
+    mp = sorted(zip(tt.level[pt].tolist(), tc[pt].tolist(), st.level[pss].tolist(), sc[pss].tolist()))
+    assert mp == sorted(map(tuple, g["p2p"].tolist()))
