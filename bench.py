@@ -126,6 +126,17 @@ class _Clocks:
         }
 
 
+def _ncu_traffic(key):
+    """dram read+write bytes of one launch from the committed ncu --set full
+    capture (profiles/r01_ncu_full_v2_metrics.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_full_v2_metrics.json")) as fh:
+            rec = json.load(fh)[key]
+        return rec["dram__bytes_read.sum"] + rec["dram__bytes_write.sum"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def _measured_peak_hbm():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -307,6 +318,8 @@ def run_b200(args):
     rows = p.m2l_row_slot.shape[0]
     alg_bytes = n_m2l * 2 * P3 * c + rows * L**3 * c  # symbol + source spectrum per event, local write
     m2l_s = st["m2l"] / 1e3
+    kname = f"m2l_rows_kernel<{'float' if dtype == 'c64' else 'double'}, {L}>"
+    traffic = _ncu_traffic(f"{dtype}:{kname}") if args.workload in ("cfg2",) else None
     peak, peak_kind = _measured_peak_hbm()
     achieved = alg_bytes / m2l_s / 1e9
     line = {
@@ -326,11 +339,12 @@ def run_b200(args):
                        parallelism=f"replicas{world}" if world > 1 else "single"),
         "stages_ms": {"upward_with_concurrent_p2p": st["upward"], "m2l": st["m2l"], "p2p": st["p2p"],
                       "downward": st["downward"]},
-        "roofline": {"bound": "hbm", "kernel": f"m2l_rows_kernel<{'float' if dtype == 'c64' else 'double'}, {L}>",
+        "roofline": {"bound": "hbm", "kernel": kname,
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "alg_bytes_per_launch": alg_bytes,
+                     "frac": achieved / peak, "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
                      "kernel_ms": st["m2l"],
-                     "note": "algorithmic bytes = 2 spectra per M2L event + local write; frac > 1 = L2 reuse"},
+                     "note": "algorithmic bytes = 2 spectra per M2L event + local write; frac > 1 = L2 reuse; "
+                             "traffic = ncu dram bytes of one launch (profiles/r01_ncu_full_v2_metrics.json)"},
         "e2e": {"value": world * n / (e_step / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(qbytes),
                 "d2h_bytes_per_step": int(qbytes), "ms_per_step": e_step},
         "accuracy": {"rel_l2_vs_direct_1000": eps, "eps_ref_reference": 1.0386568720063353e-2
