@@ -28,20 +28,38 @@ def _dev(a, dtype, device):
     return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype).to(device)
 
 
+def _sub_csr(ptr, keep):
+    """Rows ``keep`` of a CSR: (row ids, new row pointer, selected entry ids)."""
+    ptr = np.asarray(ptr)
+    starts = ptr[:-1][keep]
+    lens = (ptr[1:] - ptr[:-1])[keep]
+    new_ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    sel = np.repeat(starts - new_ptr[:-1], lens) + np.arange(int(new_ptr[-1]))
+    return np.nonzero(keep)[0], new_ptr, sel.astype(np.int64)
+
+
 class FmmPlan:
     """Reusable device plan for one particle geometry (targets is sources, or
     a target/source pair sharing one root box, traversal.py:449-461)."""
 
     def __init__(self, targets, sources=None, config: FmmConfig = FmmConfig(), device="cuda",
-                 keep_events: bool = False, charges=None, reuse: "FmmPlan | None" = None):
+                 keep_events: bool = False, charges=None, reuse: "FmmPlan | None" = None,
+                 shard=None, allreduce=None):
         """``reuse``: share the host tree + lists of an existing plan built for
         the same geometry and (order, ncrit, eta, kappa) -- e.g. to run the same
-        lists at another storage precision."""
+        lists at another storage precision.
+
+        ``shard``: (rank, world) or a ``parallel.Shard`` -- this process then
+        computes only its Morton chunk (parallel.py); ``allreduce(tensor)``
+        must sum a device tensor over the ranks in place (NCCL
+        ``torch.distributed.all_reduce``), it completes the multipoles."""
         if not torch.cuda.is_available():
             raise RuntimeError("the defmm B200 path needs a CUDA device (no CPU fallback)")
         _lib.load()
         self.config = config
         self.device = torch.device(device)
+        self._shard_arg = shard
+        self.allreduce = allreduce
         if reuse is not None:
             rc = reuse.config
             if (rc.order, rc.ncrit, rc.eta, rc.kappa, rc.hf_switch, rc.hard_depth_cap) != (
@@ -52,6 +70,7 @@ class FmmPlan:
             self.plan = reuse.plan
             self.timings = dict(reuse.timings)
             t2 = time.perf_counter()
+            self._make_shard()
             self._upload()
             self._symbols()
             torch.cuda.synchronize(self.device)
@@ -80,6 +99,7 @@ class FmmPlan:
                                keep_events=keep_events)
         t2 = time.perf_counter()
         self.timings = {"tree": t1 - t0, "blank": t2 - t1}
+        self._make_shard()
         self._upload()
         self._symbols()
         torch.cuda.synchronize(self.device)
@@ -113,40 +133,44 @@ class FmmPlan:
         self.sg = geom(st)
         self.tg = self.sg if self.same else geom(tt)
         self.dirs = _dev(p.dirs if p.dirs.size else np.zeros((1, 3)), f64, d)
+        h = self._host_lists()
         # upward lists
-        self.p2m_cell = _dev(p.m_cell[p.p2m_idx], i32, d)
-        self.p2m_dir = _dev(p.m_dir[p.p2m_idx], i32, d)
-        self.p2m_slot = _dev(p.p2m_idx, i64, d)
+        self.p2m_cell = _dev(p.m_cell[h["p2m_idx"]], i32, d)
+        self.p2m_dir = _dev(p.m_dir[h["p2m_idx"]], i32, d)
+        self.p2m_slot = _dev(h["p2m_idx"], i64, d)
         self.m2m = []
-        for lev, slots, son_slot in p.m2m_levels:
+        for lev, slots, son_slot in h["m2m"]:
             self.m2m.append((float(st.side_at(lev + 1)), _dev(slots, i64, d), _dev(p.m_dir[slots], i32, d),
                              _dev(son_slot, i64, d), int(slots.shape[0])))
-        self.hat_slot = _dev(p.hat_slot, i64, d)
+        self.hat_slot = _dev(h["hat_slot"], i64, d)
+        self.n_hat = int(h["hat_slot"].shape[0])
         # M2L rows (target-major CSR)
-        self.row_slot = _dev(p.m2l_row_slot, i64, d)
-        self.row_ptr = _dev(p.m2l_row_ptr, i64, d)
-        self.e_src = _dev(p.m2l_src, i32, d)
-        self.e_sym = _dev(p.m2l_sym, i32, d)
-        self.e_rid = _dev(p.m2l_rid, torch.int8, d)
-        self.row_entries = _dev(p.m2l_rows_entries.reshape(-1), i32, d)
+        self.row_slot = _dev(h["rows"], i64, d)
+        self.row_ptr = _dev(h["row_ptr"], i64, d)
+        self.e_src = _dev(h["ent"][:, 0], i32, d)
+        self.e_sym = _dev(p.m2l_sym[h["ent_sel"]], i32, d)
+        self.e_rid = _dev(p.m2l_rid[h["ent_sel"]], torch.int8, d)
+        self.row_entries = _dev(h["ent"].reshape(-1), i32, d)
         # downward
         self.l2l = []
-        for lev, outs, octant, ptr, src, sdir in p.l2l_levels:
+        for lev, outs, octant, ptr, src, sdir in h["l2l"]:
             self.l2l.append((float(tt.side_at(lev)), _dev(outs, i64, d), _dev(octant, torch.int8, d),
                              _dev(ptr, i64, d), _dev(src, i64, d), _dev(sdir, i32, d), int(outs.shape[0])))
-        self.leaf_cell = _dev(p.leaf_cells, i32, d)
-        self.leaf_lo = _dev(p.leaf_slot_lo, i64, d)
-        self.leaf_hi = _dev(p.leaf_slot_hi, i64, d)
+        lv = h["leaves"]
+        self.n_leaves = int(lv.sum())
+        self.leaf_cell = _dev(p.leaf_cells[lv], i32, d)
+        self.leaf_lo = _dev(p.leaf_slot_lo[lv], i64, d)
+        self.leaf_hi = _dev(p.leaf_slot_hi[lv], i64, d)
         self.slot_dir = _dev(p.l_dir, i32, d)
-        self.tgt_lo = _dev(tt.start[p.leaf_cells], i64, d)
-        self.tgt_hi = _dev(tt.stop[p.leaf_cells], i64, d)
-        self.p2p_ptr = _dev(p.p2p_ptr, i64, d)
-        self.p2p_lo = _dev(p.p2p_lo, i64, d)
-        self.p2p_hi = _dev(p.p2p_hi, i64, d)
+        self.tgt_lo = _dev(tt.start[p.leaf_cells[lv]], i64, d)
+        self.tgt_hi = _dev(tt.stop[p.leaf_cells[lv]], i64, d)
+        self.p2p_ptr = _dev(h["p2p_ptr"], i64, d)
+        self.p2p_lo = _dev(p.p2p_lo[h["p2p_sel"]], i64, d)
+        self.p2p_hi = _dev(p.p2p_hi[h["p2p_sel"]], i64, d)
         # workspaces (storage precision per FmmConfig.dtype)
         cd = self.cdtype
         self.mult = torch.empty((max(p.n_mult, 1), self.L3), dtype=cd, device=d)
-        self.hat = torch.empty((max(p.n_hat, 1), self.SS), dtype=cd, device=d)
+        self.hat = torch.empty((max(self.n_hat, 1), self.SS), dtype=cd, device=d)
         self.local = torch.empty((max(p.n_local, 1), self.L3), dtype=cd, device=d)
         self.near = torch.empty(self.n_tgt, dtype=cd, device=d)
         self.q = torch.zeros(self.n_src, dtype=cd, device=d)
@@ -154,6 +178,59 @@ class FmmPlan:
         self.side_stream = torch.cuda.Stream(device=d)
         self.m2l_variant = "derived"
         self.p2p_overlap = "upward"  # or "m2l"
+
+    def _make_shard(self):
+        from .parallel import Shard, make_shard
+
+        sa = self._shard_arg
+        if sa is None or isinstance(sa, Shard):
+            self.shard = sa
+        else:
+            rank, world = sa
+            self.shard = make_shard(self.plan, self.tt, self.st, int(rank), int(world)) if int(world) > 1 else None
+        if self.shard is not None and self.shard.world > 1 and self.allreduce is None:
+            raise ValueError("a sharded plan needs allreduce= to complete the multipoles")
+
+    def _host_lists(self) -> dict:
+        """The plan's lists, restricted to this rank's chunk when sharded
+        (parallel.py); spectra are renumbered compactly."""
+        p, sh = self.plan, self.shard
+        n_ent = p.m2l_rows_entries.shape[0]
+        h = {
+            "p2m_idx": p.p2m_idx,
+            "m2m": [(lev, sl, ss) for lev, sl, ss in p.m2m_levels],
+            "hat_slot": p.hat_slot,
+            "rows": p.m2l_row_slot,
+            "row_ptr": p.m2l_row_ptr,
+            "ent": p.m2l_rows_entries,
+            "ent_sel": np.arange(n_ent),
+            "l2l": list(p.l2l_levels),
+            "leaves": np.ones(p.leaf_cells.shape[0], bool),
+            "p2p_ptr": p.p2p_ptr,
+            "p2p_sel": np.arange(p.p2p_lo.shape[0]),
+        }
+        if sh is None:
+            return h
+        h["p2m_idx"] = sh.p2m_idx
+        h["m2m"] = [(lev, sl[k], ss[k]) for (lev, sl, ss), k in zip(p.m2m_levels, sh.m2m_keep) if k.any()]
+        rows, ptr, sel = _sub_csr(p.m2l_row_ptr, sh.row_keep)
+        h["rows"], h["row_ptr"], h["ent_sel"] = p.m2l_row_slot[sh.row_keep], ptr, sel
+        hat_ids = np.nonzero(sh.hat_keep)[0]
+        remap = np.full(p.n_hat, -1, np.int64)
+        remap[hat_ids] = np.arange(hat_ids.shape[0])
+        ent = p.m2l_rows_entries[sel].copy()
+        ent[:, 0] = remap[ent[:, 0]]
+        h["ent"], h["hat_slot"] = ent, p.hat_slot[hat_ids]
+        l2l = []
+        for (lev, outs, octant, lptr, src, sdir), k in zip(p.l2l_levels, sh.l2l_keep):
+            if not k.any():
+                continue
+            _, nptr, lsel = _sub_csr(lptr, k)
+            l2l.append((lev, outs[k], octant[k], nptr, src[lsel], sdir[lsel]))
+        h["l2l"] = l2l
+        h["leaves"] = sh.leaf_keep
+        _, h["p2p_ptr"], h["p2p_sel"] = _sub_csr(p.p2p_ptr, sh.leaf_keep)
+        return h
 
     def _symbols(self):
         p = self.plan
@@ -184,52 +261,67 @@ class FmmPlan:
 
     def apply(self, out=None, stage_events=None):
         """One matvec with the charges currently loaded; returns potentials in
-        the caller's target order (device tensor).  ``stage_events`` (list)
-        receives (name, start_event, end_event) for the stage timers."""
+        the caller's target order (device tensor; when sharded only this
+        rank's targets are non-zero).  ``stage_events`` (list) receives
+        (name, start_event, end_event) for the stage timers."""
+        self.apply_upward(stage_events)
+        if self.shard is not None:
+            # M2M is linear: summing the partial multipoles over the ranks
+            # completes every multipole (the one data-path collective)
+            self.allreduce(self.mult)
+        return self.apply_rest(out, stage_events)
+
+    def _near_field(self, stage_events):
+        """P2P on the side stream (FP-pipe bound), concurrent with the far field."""
         p = self.plan
-        L = self.L
-        kappa = float(p.kappa)
+        stream = torch.cuda.current_stream(self.device)
+        side = self.side_stream
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            if stage_events is not None:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record(side)
+            _lib.call(self._op("p2p"), self.n_leaves, self.tgt_lo, self.tgt_hi, self.p2p_ptr, self.p2p_lo,
+                      self.p2p_hi, *self.t_xyz, *self.s_xyz, self.q, float(p.kappa), float(p.tol), self.near,
+                      side.cuda_stream)
+            if stage_events is not None:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(side)
+                stage_events.append(("p2p", e0, e1))
+
+    def apply_upward(self, stage_events=None):
+        """Phase 1: (P2P launch on the side stream,) P2M and M2M -- partial
+        multipoles of the active cells when sharded."""
+        L, kappa, sg = self.L, float(self.plan.kappa), self.sg
         stream = torch.cuda.current_stream(self.device)
         sh = stream.cuda_stream
-        out = self.out if out is None else out
-        ev = (lambda: torch.cuda.Event(enable_timing=True)) if stage_events is not None else None
-        sg, tg = self.sg, self.tg
-
-        def near_field():
-            # near field on the side stream (FP-pipe bound), concurrent with the
-            # far field; `p2p_overlap` picks the far-field stage it overlaps
-            side = self.side_stream
-            side.wait_stream(stream)
-            with torch.cuda.stream(side):
-                if stage_events is not None:
-                    e0 = ev()
-                    e0.record(side)
-                _lib.call(self._op("p2p"), p.leaf_cells.shape[0], self.tgt_lo, self.tgt_hi, self.p2p_ptr,
-                          self.p2p_lo, self.p2p_hi, *self.t_xyz, *self.s_xyz, self.q, kappa, float(p.tol),
-                          self.near, side.cuda_stream)
-                if stage_events is not None:
-                    e1 = ev()
-                    e1.record(side)
-                    stage_events.append(("p2p", e0, e1))
-
         if self.p2p_overlap == "upward":
-            near_field()
+            self._near_field(stage_events)
         if stage_events is not None:
-            a = ev()
-            a.record(stream)
-        # upward: P2M at every leaf key, M2M per level bottom-up, M2F
+            self._ev_a = torch.cuda.Event(enable_timing=True)
+            self._ev_a.record(stream)
+        if self.shard is not None:
+            self.mult.zero_()  # multipoles of other ranks' cells stay 0 -> partial sums
         _lib.call(self._op("p2m"), L, self.p2m_slot.shape[0], self.p2m_cell, self.p2m_dir, self.p2m_slot,
                   sg["start"], sg["stop"], sg["alpha"], sg["level"], sg["beta"], self.dirs, *self.s_xyz, self.q,
                   kappa, self.mult, sh)
         for son_beta, slots, mdir, son_slot, n in self.m2m:
             _lib.call(self._op("m2m"), L, n, slots, mdir, son_slot, son_beta, self.dirs, kappa, self.mult, sh)
-        _lib.call(self._op("m2f"), L, p.n_hat, self.hat_slot, self.mult, self.hat, sh)
+
+    def apply_rest(self, out=None, stage_events=None):
+        """Phase 2 (multipoles complete): M2F, M2L + F2L, L2L, L2P (+ near, un-permute)."""
+        L, kappa, tg = self.L, float(self.plan.kappa), self.tg
+        stream = torch.cuda.current_stream(self.device)
+        sh = stream.cuda_stream
+        out = self.out if out is None else out
+        ev = (lambda: torch.cuda.Event(enable_timing=True)) if stage_events is not None else None
+        _lib.call(self._op("m2f"), L, self.n_hat, self.hat_slot, self.mult, self.hat, sh)
         if stage_events is not None:
             b = ev()
             b.record(stream)
-            stage_events.append(("upward", a, b))
+            stage_events.append(("upward", self._ev_a, b))
         if self.p2p_overlap != "upward":
-            near_field()
+            self._near_field(stage_events)
         else:
             stream.wait_stream(self.side_stream)  # M2L runs alone (clean roofline timing)
         # M2L (+ fused F2L) into the local slots
@@ -251,9 +343,11 @@ class FmmPlan:
             _lib.call(self._op("l2l"), L, n, outs, octant, ptr, src, sdir, son_beta, self.dirs, kappa,
                       self.local, sh)
         stream.wait_stream(self.side_stream)
-        _lib.call(self._op("l2p"), L, self.leaf_cell.shape[0], self.leaf_cell, self.leaf_lo, self.leaf_hi,
-                  self.slot_dir, tg["start"], tg["stop"], tg["alpha"], tg["level"], tg["beta"], self.dirs,
-                  *self.t_xyz, kappa, self.local, self.near, self.t_perm, out, sh)
+        if self.shard is not None:
+            out.zero_()  # this rank writes only its own targets
+        _lib.call(self._op("l2p"), L, self.n_leaves, self.leaf_cell, self.leaf_lo, self.leaf_hi, self.slot_dir,
+                  tg["start"], tg["stop"], tg["alpha"], tg["level"], tg["beta"], self.dirs, *self.t_xyz, kappa,
+                  self.local, self.near, self.t_perm, out, sh)
         if stage_events is not None:
             e = ev()
             e.record(stream)

@@ -1,0 +1,113 @@
+"""Morton-order sharding of one FMM plan over the ranks of one node.
+
+SURVEY.md §8(e): the target leaves, already in Morton (= particle) order, are
+cut into ``world`` contiguous chunks balanced by an estimate of their work
+(24 flop per P2P pair + 8 P^3 flop per M2L event, weighted by the measured
+per-unit costs), with cuts on leaf boundaries so no leaf straddles two ranks.
+
+Rank r then owns the particle range [cut[r], cut[r+1]) and works only on the
+cells whose particle range intersects it ("active" cells):
+
+* upward: P2M on its own leaves, M2M on its active cells.  A cell spanning
+  several chunks gets a PARTIAL multipole on each rank (its other sons are
+  zero there); because M2M is linear, one ``all_reduce(sum)`` of the nodal
+  multipole array over NCCL/NVLink completes every multipole on every rank --
+  the only data-path collective;
+* M2F only for the spectra its own M2L rows read;
+* M2L rows, L2L slots and L2P/P2P leaves of its active target cells (shared
+  top cells are computed redundantly by every rank that needs them), so the
+  far field needs no halo exchange of locals and the near field reads the
+  (replicated, read-only) source particles directly.
+
+Single-tree mode (targets is sources) only; the two-tree mode runs replicas.
+Everything here is host-side index bookkeeping (numpy); it is exercised with
+world_size-2 gloo process groups on CPU in tests/test_parallel.py.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+__all__ = ["Shard", "leaf_costs", "partition_leaves", "make_shard"]
+
+# relative unit costs measured on the B200 (profiles/r01_summary_v2.md, c64):
+# M2L ~2.9 ms / 10.8 M events; P2P ~0.77 ms / 3.83e8 pairs
+_COST_M2L_EVENT = 2.9e-3 / 10.84e6
+_COST_P2P_PAIR = 0.77e-3 / 3.83e8
+
+
+def leaf_costs(plan, tt) -> np.ndarray:
+    """Estimated work per target leaf (in plan.leaf_cells order)."""
+    leaves = plan.leaf_cells
+    n_t = (tt.stop[leaves] - tt.start[leaves]).astype(np.float64)
+    n_src = np.zeros(leaves.shape[0], np.float64)
+    run_len = (plan.p2p_hi - plan.p2p_lo).astype(np.float64)
+    cs = np.concatenate([[0.0], np.cumsum(run_len)])
+    n_src = cs[plan.p2p_ptr[1:]] - cs[plan.p2p_ptr[:-1]]
+    cost = n_t * n_src * _COST_P2P_PAIR
+    # M2L events of every row whose target cell contains the leaf, spread over
+    # the leaves by particle count
+    rows = plan.m2l_row_slot
+    rc = plan.l_cell[rows]
+    ev = np.diff(plan.m2l_row_ptr).astype(np.float64)
+    lstart = tt.start[leaves]
+    a = np.searchsorted(lstart, tt.start[rc])
+    b = np.searchsorted(lstart, tt.stop[rc])
+    per_particle = ev * _COST_M2L_EVENT / (tt.stop[rc] - tt.start[rc])
+    # difference array over leaf indices, weighted by the leaf's particle count
+    acc = np.zeros(leaves.shape[0] + 1, np.float64)
+    np.add.at(acc, a, per_particle)
+    np.add.at(acc, b, -per_particle)
+    cost += np.cumsum(acc)[:-1] * n_t
+    return cost
+
+
+def partition_leaves(plan, tt, world: int) -> np.ndarray:
+    """Particle-index cuts (world+1) on leaf boundaries, balanced by cost."""
+    leaves = plan.leaf_cells
+    if world <= 1 or leaves.shape[0] < world:
+        return np.array([0, int(tt.stop[0])] if world <= 1 else [0] + [int(tt.stop[0])] * world, np.int64)
+    c = np.cumsum(leaf_costs(plan, tt))
+    targets = c[-1] * np.arange(1, world) / world
+    k = np.searchsorted(c, targets)  # leaf index where each chunk ends
+    k = np.clip(k, 0, leaves.shape[0] - 1)
+    cuts = [0] + [int(tt.stop[leaves[i]]) for i in k] + [int(tt.stop[0])]
+    return np.maximum.accumulate(np.array(cuts, np.int64))
+
+
+@dataclass
+class Shard:
+    rank: int
+    world: int
+    lo: int  # owned particle range [lo, hi)
+    hi: int
+    p2m_idx: np.ndarray  # subset of plan.p2m_idx
+    m2m_keep: list  # per plan.m2m_levels entry: row mask
+    hat_keep: np.ndarray  # spectra this rank transforms
+    row_keep: np.ndarray  # M2L rows this rank computes
+    l2l_keep: list  # per plan.l2l_levels entry: out mask
+    leaf_keep: np.ndarray  # target leaves (plan.leaf_cells order)
+
+
+def make_shard(plan, tt, st, rank: int, world: int, cuts=None) -> Shard:
+    if tt is not st:
+        raise ValueError("sharding is implemented for single-tree plans (targets is sources)")
+    cuts = partition_leaves(plan, tt, world) if cuts is None else np.asarray(cuts)
+    lo, hi = int(cuts[rank]), int(cuts[rank + 1])
+
+    def active(cells):
+        return (tt.start[cells] < hi) & (tt.stop[cells] > lo)
+
+    p2m_idx = plan.p2m_idx[active(plan.m_cell[plan.p2m_idx])]
+    m2m_keep = [active(plan.m_cell[slots]) for _, slots, _ in plan.m2m_levels]
+    rows = plan.m2l_row_slot
+    row_keep = active(plan.l_cell[rows])
+    # spectra read by the kept rows
+    e = np.repeat(row_keep, np.diff(plan.m2l_row_ptr))
+    hat_keep = np.zeros(plan.n_hat, bool)
+    hat_keep[plan.m2l_rows_entries[e, 0]] = True
+    l2l_keep = [active(plan.l_cell[outs]) for _, outs, *_ in plan.l2l_levels]
+    leaf_keep = active(plan.leaf_cells)
+    return Shard(rank, world, lo, hi, p2m_idx, m2m_keep, hat_keep, row_keep, l2l_keep, leaf_keep)

@@ -232,3 +232,27 @@ def test_event_log_partitions_all_pairs():
     mine = sorted((e.target.level, e.target.key.code, e.source.key.code, *(e.direction or (-1, -1)))
                   for e in events if e.kind == "M2L")
     assert mine == ref
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("case", ["cubesurf4000", "sphere3000"])
+def test_virtual_ranks_match_single_gpu(case, world):
+    """§8(e): the Morton-sharded path, emulated as `world` virtual ranks on one
+    GPU (phase 1 on every rank, the multipole all-reduce as a device sum,
+    phase 2 on every rank), reproduces the single-plan potentials."""
+    from paper_2202_04894_b200 import FmmConfig, FmmPlan
+
+    g = load_case(case)
+    cfg = FmmConfig(**g["config"])
+    base = FmmPlan(g["points"], None, cfg, charges=g["charges"])
+    ref = base.apply().clone()
+    ranks = [FmmPlan(g["points"], None, cfg, charges=g["charges"], reuse=base, shard=(r, world),
+                     allreduce=lambda t: None) for r in range(world)]
+    for r in ranks:
+        r.apply_upward()
+    total = sum(r.mult for r in ranks)
+    for r in ranks:
+        r.mult.copy_(total)
+    out = sum(r.apply_rest().clone() for r in ranks)
+    assert _rel(out.cpu().numpy(), ref.cpu().numpy()) <= 1e-13
+    assert _rel(out.cpu().numpy(), g["pot"]) <= FP64_TOL
