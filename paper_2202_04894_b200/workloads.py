@@ -49,6 +49,8 @@ WORKLOADS = {
     "cfg3": Workload("cfg3", "ellipsoid", 4_000_000, 256.0, 5, 64, "c64"),
     "cfg4": Workload("cfg4", "refined-cube", 16_000_000, 512.0, 6, 128, "c64"),
     "cfg5": Workload("cfg5", "volume", 2_000_000, 64.0, 4, 64, "c128"),
+    "cfg5_l6": Workload("cfg5_l6", "volume", 2_000_000, 64.0, 6, 64, "c128"),
+    "cfg5_l8": Workload("cfg5_l8", "volume", 2_000_000, 64.0, 8, 64, "c128"),
 }
 
 
