@@ -75,9 +75,14 @@ void defmm_tree_free(defmm_tree* t);
  * K3 L2P + un-permute -- interpolation.py:127-137 via traversal.py:394-402,
  *   tree.py:224-228.  For leaf i < n, p in [cell_start, cell_stop):
  *   out[perm[p]] = near[p] + sum_{s in [slot_lo[i], slot_hi[i])} L2P(local[s], slot_dir[s]).
- * K1 P2P -- traversal.py:303-317 + kernel.py:37-55.  For target leaf i < n:
- *   near[p] = sum over source ranges [src_lo[e], src_hi[e]), e in [ptr[i], ptr[i+1]),
- *   of G(|x_p - y_s|) q_s for p in [tgt_lo[i], tgt_hi[i]); G = 0 for r < tol.
+ * K1 P2P -- traversal.py:303-317 + kernel.py:37-55.  Target leaf l owns the merged
+ *   source runs [src_lo[e], src_hi[e]), e in [ptr[l], ptr[l+1]); their concatenation
+ *   is cut into work items i < n_items = (item_leaf[i], flattened range
+ *   [item_f0[i], item_f1[i])).  For p in [tgt_lo[l], tgt_hi[l]) an item computes
+ *   sum_s G(|x_p - y_s|) q_s (G = 0 for r < tol) into near[p] when
+ *   item_out[i] < 0 (the leaf's only item), else into
+ *   partial[item_out[i] + p - tgt_lo[l]]; the n_split split leaves are then
+ *   reduced in item order: near[p] = sum_{m < split_n} partial[split_base + m*nt + ...].
  *   Targets t*, sources s* (the same arrays in single-tree mode).
  */
 #define DEFMM_DECLARE_TYPED(SUFFIX)                                                              \
@@ -114,11 +119,15 @@ void defmm_tree_free(defmm_tree* t);
                            const double* dirs, const double* px, const double* py,              \
                            const double* pz, double kappa, const void* local, const void* near, \
                            const int64_t* perm, void* out, void* stream);                       \
-    int defmm_p2p_##SUFFIX(int64_t n, const int64_t* tgt_lo, const int64_t* tgt_hi,              \
-                           const int64_t* ptr, const int64_t* src_lo, const int64_t* src_hi,    \
-                           const double* tx, const double* ty, const double* tz,                \
-                           const double* sx, const double* sy, const double* sz, const void* q, \
-                           double kappa, double tol, void* near, void* stream);
+    int defmm_p2p_##SUFFIX(int64_t n_items, const int32_t* item_leaf, const int64_t* item_f0,    \
+                           const int64_t* item_f1, const int64_t* item_out,                     \
+                           const int64_t* tgt_lo, const int64_t* tgt_hi, const int64_t* ptr,    \
+                           const int64_t* src_lo, const int64_t* src_hi, const double* tx,      \
+                           const double* ty, const double* tz, const double* sx,                \
+                           const double* sy, const double* sz, const void* q, double kappa,     \
+                           double tol, void* near, void* partial, int64_t n_split,              \
+                           const int32_t* split_leaf, const int64_t* split_base,                \
+                           const int32_t* split_n, void* stream);
 
 /* expands to: defmm_p2m_c128 defmm_m2m_c128 defmm_m2f_c128 defmm_symbols_c128
  * defmm_expand_symbols_c128 defmm_m2l_rows_c128 defmm_l2l_c128 defmm_l2p_c128

@@ -837,56 +837,109 @@ __device__ __forceinline__ double2 helm_pair(double dxd, double dyd, double dzd,
     return make_double2((double)(gr * qs.x - gi * qs.y), (double)(gr * qs.y + gi * qs.x));
 }
 
+// Work items: a target leaf's flattened source list (its merged runs) is cut
+// into pieces [f0, f1) of bounded size so that the few coarse leaves next to
+// huge source cells (cfg3: up to 1.6 M sources) do not serialise the kernel.
+// item_out < 0: the item is the leaf's only one and writes near[] directly;
+// otherwise it writes nt partial sums at partial[item_out + (t - t0)],
+// combined in fixed order by p2p_reduce_kernel.
+struct P2PItems {
+    const int32_t* leaf;
+    const int64_t* f0;
+    const int64_t* f1;
+    const int64_t* out;
+};
+
+// visit the sources [f0, f1) of the flattened run list of one leaf
+template <typename F>
+__device__ __forceinline__ void for_source_tiles(const int64_t* src_lo, const int64_t* src_hi, int64_t e0,
+                                                 int64_t e1, int64_t f0, int64_t f1, F&& tile) {
+    int64_t base = 0;  // flattened offset of run e
+    for (int64_t e = e0; e < e1 && base < f1; ++e) {
+        const int64_t a = src_lo[e], len = src_hi[e] - a;
+        const int64_t lo = f0 > base ? f0 - base : 0;
+        const int64_t hi = (f1 - base) < len ? (f1 - base) : len;
+        for (int64_t sb = lo; sb < hi; sb += P2P_TILE) {
+            const int cnt = (int)((hi - sb) < P2P_TILE ? (hi - sb) : P2P_TILE);
+            tile(a + sb, cnt);
+        }
+        base += len;
+    }
+}
+
 template <typename R>
 __global__ void __launch_bounds__(P2P_NT) p2p_kernel(
-    int64_t n, const int64_t* __restrict__ tgt_lo, const int64_t* __restrict__ tgt_hi,
+    int64_t n, P2PItems it, const int64_t* __restrict__ tgt_lo, const int64_t* __restrict__ tgt_hi,
     const int64_t* __restrict__ ptr, const int64_t* __restrict__ src_lo,
     const int64_t* __restrict__ src_hi, const double* __restrict__ tx,
     const double* __restrict__ ty, const double* __restrict__ tz, const double* __restrict__ px,
     const double* __restrict__ py, const double* __restrict__ pz, const cx<R>* __restrict__ q,
-    double kappa, double tol, cx<R>* __restrict__ near) {
+    double kappa, double tol, cx<R>* __restrict__ near, cx<R>* __restrict__ partial) {
     using V = cx<R>;
     __shared__ double sx[P2P_TILE], sy[P2P_TILE], sz[P2P_TILE];
     __shared__ V sq[P2P_TILE];
-    const int64_t i = blockIdx.x;
-    const int64_t t0 = tgt_lo[i], t1 = tgt_hi[i];
+    const int64_t item = blockIdx.x;
+    const int leaf = it.leaf[item];
+    const int64_t f0 = it.f0[item], f1 = it.f1[item], ob = it.out[item];
+    const int64_t t0 = tgt_lo[leaf], t1 = tgt_hi[leaf];
     const int64_t nt = t1 - t0;
     const int split = nt <= 16 ? 8 : nt <= 32 ? 4 : nt <= 64 ? 2 : 1;
     const int per_pass = P2P_NT / split;
     const double kpi = kappa / 3.141592653589793;
-    const int64_t e0 = ptr[i], e1 = ptr[i + 1];
+    const int64_t e0 = ptr[leaf], e1 = ptr[leaf + 1];
     for (int64_t tb = t0; tb < t1; tb += per_pass) {
         const int64_t t = tb + threadIdx.x / split;
         const int part = threadIdx.x % split;
         const bool valid = t < t1;
         const double xt = valid ? tx[t] : 0.0, yt = valid ? ty[t] : 0.0, zt = valid ? tz[t] : 0.0;
         double2 acc = make_double2(0.0, 0.0);
-        for (int64_t e = e0; e < e1; ++e) {
-            const int64_t a = src_lo[e], b = src_hi[e];
-            for (int64_t sb = a; sb < b; sb += P2P_TILE) {
-                const int cnt = (int)((b - sb) < P2P_TILE ? (b - sb) : P2P_TILE);
-                __syncthreads();
-                for (int k = threadIdx.x; k < cnt; k += P2P_NT) {
-                    sx[k] = px[sb + k];
-                    sy[k] = py[sb + k];
-                    sz[k] = pz[sb + k];
-                    sq[k] = q[sb + k];
-                }
-                __syncthreads();
-                if (valid) {
-                    for (int k = part; k < cnt; k += split) {
-                        const double2 g = helm_pair(xt - sx[k], yt - sy[k], zt - sz[k], sq[k], kpi, tol);
-                        acc.x += g.x;
-                        acc.y += g.y;
-                    }
+        for_source_tiles(src_lo, src_hi, e0, e1, f0, f1, [&](int64_t sb, int cnt) {
+            __syncthreads();
+            for (int k = threadIdx.x; k < cnt; k += P2P_NT) {
+                sx[k] = px[sb + k];
+                sy[k] = py[sb + k];
+                sz[k] = pz[sb + k];
+                sq[k] = q[sb + k];
+            }
+            __syncthreads();
+            if (valid) {
+                for (int k = part; k < cnt; k += split) {
+                    const double2 g = helm_pair(xt - sx[k], yt - sy[k], zt - sz[k], sq[k], kpi, tol);
+                    acc.x += g.x;
+                    acc.y += g.y;
                 }
             }
-        }
+        });
         for (int off = 1; off < split; off <<= 1) {
             acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
             acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
         }
-        if (valid && part == 0) near[t] = from_d<V>(acc);
+        if (valid && part == 0) {
+            if (ob < 0)
+                near[t] = from_d<V>(acc);
+            else
+                partial[ob + (t - t0)] = from_d<V>(acc);
+        }
+    }
+}
+
+// near[t] = sum_m partial[base + m * nt + (t - t0)] for the split leaves
+template <typename R>
+__global__ void __launch_bounds__(128) p2p_reduce_kernel(int64_t n, const int32_t* __restrict__ leaf,
+                                                         const int64_t* __restrict__ base,
+                                                         const int32_t* __restrict__ nitems,
+                                                         const int64_t* __restrict__ tgt_lo,
+                                                         const int64_t* __restrict__ tgt_hi,
+                                                         const cx<R>* __restrict__ partial,
+                                                         cx<R>* __restrict__ near) {
+    const int64_t i = blockIdx.x;
+    const int l = leaf[i];
+    const int64_t t0 = tgt_lo[l], nt = tgt_hi[l] - t0;
+    const int k = nitems[i];
+    for (int64_t x = threadIdx.x; x < nt; x += blockDim.x) {
+        double2 acc = make_double2(0.0, 0.0);
+        for (int m = 0; m < k; ++m) acc = cadd(acc, to_d(partial[base[i] + m * nt + x]));
+        near[t0 + x] = from_d<cx<R>>(acc);
     }
 }
 
@@ -902,23 +955,25 @@ __device__ __forceinline__ void split_f32(double x, float& hi, float& lo) {
 }
 
 __global__ void __launch_bounds__(P2P_NT) p2p_f32_kernel(
-    int64_t n, const int64_t* __restrict__ tgt_lo, const int64_t* __restrict__ tgt_hi,
+    int64_t n, P2PItems it, const int64_t* __restrict__ tgt_lo, const int64_t* __restrict__ tgt_hi,
     const int64_t* __restrict__ ptr, const int64_t* __restrict__ src_lo,
     const int64_t* __restrict__ src_hi, const double* __restrict__ tx,
     const double* __restrict__ ty, const double* __restrict__ tz, const double* __restrict__ px,
     const double* __restrict__ py, const double* __restrict__ pz, const float2* __restrict__ q,
-    double kappa, double tol, float2* __restrict__ near) {
+    double kappa, double tol, float2* __restrict__ near, float2* __restrict__ partial) {
     __shared__ float4 sh[P2P_TILE];  // (x_hi, y_hi, z_hi, q.re)
     __shared__ float4 sl[P2P_TILE];  // (x_lo, y_lo, z_lo, q.im)
-    const int64_t i = blockIdx.x;
-    const int64_t t0 = tgt_lo[i], t1 = tgt_hi[i];
+    const int64_t item = blockIdx.x;
+    const int leaf = it.leaf[item];
+    const int64_t f0 = it.f0[item], f1 = it.f1[item], ob = it.out[item];
+    const int64_t t0 = tgt_lo[leaf], t1 = tgt_hi[leaf];
     const int64_t nt = t1 - t0;
     const int split = nt <= 16 ? 8 : nt <= 32 ? 4 : nt <= 64 ? 2 : 1;
     const int per_pass = P2P_NT / split;
     const float kpi = (float)(kappa / 3.141592653589793);
     const float ftol = (float)tol;
     const float inv4pi = (float)(1.0 / (4.0 * 3.141592653589793));
-    const int64_t e0 = ptr[i], e1 = ptr[i + 1];
+    const int64_t e0 = ptr[leaf], e1 = ptr[leaf + 1];
     for (int64_t tb = t0; tb < t1; tb += per_pass) {
         const int64_t t = tb + threadIdx.x / split;
         const int part = threadIdx.x % split;
@@ -930,51 +985,52 @@ __global__ void __launch_bounds__(P2P_NT) p2p_f32_kernel(
             split_f32(tz[t], zh, zl);
         }
         float ar = 0.f, ai = 0.f;
-        for (int64_t e = e0; e < e1; ++e) {
-            const int64_t a = src_lo[e], b = src_hi[e];
-            for (int64_t sb = a; sb < b; sb += P2P_TILE) {
-                const int cnt = (int)((b - sb) < P2P_TILE ? (b - sb) : P2P_TILE);
-                __syncthreads();
-                for (int k = threadIdx.x; k < cnt; k += P2P_NT) {
-                    float4 hh, ll;
-                    split_f32(px[sb + k], hh.x, ll.x);
-                    split_f32(py[sb + k], hh.y, ll.y);
-                    split_f32(pz[sb + k], hh.z, ll.z);
-                    const float2 qq = q[sb + k];
-                    hh.w = qq.x;
-                    ll.w = qq.y;
-                    sh[k] = hh;
-                    sl[k] = ll;
-                }
-                __syncthreads();
-                if (valid) {
+        for_source_tiles(src_lo, src_hi, e0, e1, f0, f1, [&](int64_t sb, int cnt) {
+            __syncthreads();
+            for (int k = threadIdx.x; k < cnt; k += P2P_NT) {
+                float4 hh, ll;
+                split_f32(px[sb + k], hh.x, ll.x);
+                split_f32(py[sb + k], hh.y, ll.y);
+                split_f32(pz[sb + k], hh.z, ll.z);
+                const float2 qq = q[sb + k];
+                hh.w = qq.x;
+                ll.w = qq.y;
+                sh[k] = hh;
+                sl[k] = ll;
+            }
+            __syncthreads();
+            if (valid) {
 #pragma unroll 4
-                    for (int k = part; k < cnt; k += split) {
-                        const float4 h = sh[k], l = sl[k];
-                        const float dx = (xh - h.x) + (xl - l.x);
-                        const float dy = (yh - h.y) + (yl - l.y);
-                        const float dz = (zh - h.z) + (zl - l.z);
-                        const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                        const float rinv = rsqrtf(r2);
-                        const float r = r2 * rinv;
-                        const bool ok = r >= ftol;  // r2 = 0 -> NaN -> masked
-                        float xr = kpi * (ok ? r : 0.0f);
-                        xr = fmaf(-2.0f, rintf(0.5f * xr), xr);  // kappa r / pi reduced to [-1, 1]
-                        float sn, cs;
-                        __sincosf(3.14159265358979f * xr, &sn, &cs);
-                        const float g = ok ? rinv * inv4pi : 0.0f;
-                        const float gr = g * cs, gi = g * sn;
-                        ar = fmaf(gr, h.w, fmaf(-gi, l.w, ar));
-                        ai = fmaf(gr, l.w, fmaf(gi, h.w, ai));
-                    }
+                for (int k = part; k < cnt; k += split) {
+                    const float4 h = sh[k], l = sl[k];
+                    const float dx = (xh - h.x) + (xl - l.x);
+                    const float dy = (yh - h.y) + (yl - l.y);
+                    const float dz = (zh - h.z) + (zl - l.z);
+                    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                    const float rinv = rsqrtf(r2);
+                    const float r = r2 * rinv;
+                    const bool ok = r >= ftol;  // r2 = 0 -> NaN -> masked
+                    float xr = kpi * (ok ? r : 0.0f);
+                    xr = fmaf(-2.0f, rintf(0.5f * xr), xr);  // kappa r / pi reduced to [-1, 1]
+                    float sn, cs;
+                    __sincosf(3.14159265358979f * xr, &sn, &cs);
+                    const float g = ok ? rinv * inv4pi : 0.0f;
+                    const float gr = g * cs, gi = g * sn;
+                    ar = fmaf(gr, h.w, fmaf(-gi, l.w, ar));
+                    ai = fmaf(gr, l.w, fmaf(gi, h.w, ai));
                 }
             }
-        }
+        });
         for (int off = 1; off < split; off <<= 1) {
             ar += __shfl_xor_sync(0xffffffffu, ar, off);
             ai += __shfl_xor_sync(0xffffffffu, ai, off);
         }
-        if (valid && part == 0) near[t] = make_float2(ar, ai);
+        if (valid && part == 0) {
+            if (ob < 0)
+                near[t] = make_float2(ar, ai);
+            else
+                partial[ob + (t - t0)] = make_float2(ar, ai);
+        }
     }
 }
 
@@ -1176,20 +1232,29 @@ int launch_l2p(int32_t L, int64_t n, const int32_t* leaf_cell, const int64_t* sl
 }
 
 template <typename R>
-int launch_p2p(int64_t n, const int64_t* tgt_lo, const int64_t* tgt_hi, const int64_t* ptr,
-               const int64_t* src_lo, const int64_t* src_hi, const double* tx, const double* ty,
-               const double* tz, const double* sx, const double* sy, const double* sz, const void* q,
-               double kappa, double tol, void* near, void* stream) {
-    if (n == 0) return 0;
-    if (!grid_ok(n)) return -1;
+int launch_p2p(int64_t n_items, const int32_t* item_leaf, const int64_t* item_f0, const int64_t* item_f1,
+               const int64_t* item_out, const int64_t* tgt_lo, const int64_t* tgt_hi, const int64_t* ptr,
+               const int64_t* src_lo, const int64_t* src_hi, const double* tx, const double* ty, const double* tz,
+               const double* sx, const double* sy, const double* sz, const void* q, double kappa, double tol,
+               void* near, void* partial, int64_t n_split, const int32_t* split_leaf, const int64_t* split_base,
+               const int32_t* split_n, void* stream) {
+    if (n_items == 0) return 0;
+    if (!grid_ok(n_items)) return -1;
+    cudaStream_t s = (cudaStream_t)stream;
+    const P2PItems it{item_leaf, item_f0, item_f1, item_out};
     if constexpr (sizeof(R) == 4) {
-        p2p_f32_kernel<<<(unsigned)n, P2P_NT, 0, (cudaStream_t)stream>>>(
-            n, tgt_lo, tgt_hi, ptr, src_lo, src_hi, tx, ty, tz, sx, sy, sz, (const float2*)q, kappa, tol,
-            (float2*)near);
+        p2p_f32_kernel<<<(unsigned)n_items, P2P_NT, 0, s>>>(n_items, it, tgt_lo, tgt_hi, ptr, src_lo, src_hi, tx,
+                                                            ty, tz, sx, sy, sz, (const float2*)q, kappa, tol,
+                                                            (float2*)near, (float2*)partial);
     } else {
-        p2p_kernel<R><<<(unsigned)n, P2P_NT, 0, (cudaStream_t)stream>>>(n, tgt_lo, tgt_hi, ptr, src_lo, src_hi,
-                                                                        tx, ty, tz, sx, sy, sz, (const cx<R>*)q,
-                                                                        kappa, tol, (cx<R>*)near);
+        p2p_kernel<R><<<(unsigned)n_items, P2P_NT, 0, s>>>(n_items, it, tgt_lo, tgt_hi, ptr, src_lo, src_hi, tx,
+                                                           ty, tz, sx, sy, sz, (const cx<R>*)q, kappa, tol,
+                                                           (cx<R>*)near, (cx<R>*)partial);
+    }
+    if (n_split > 0) {
+        if (!grid_ok(n_split)) return -1;
+        p2p_reduce_kernel<R><<<(unsigned)n_split, 128, 0, s>>>(n_split, split_leaf, split_base, split_n, tgt_lo,
+                                                                tgt_hi, (const cx<R>*)partial, (cx<R>*)near);
     }
     return report(cudaGetLastError(), "p2p");
 }
@@ -1247,12 +1312,16 @@ const char* defmm_last_error(void) { return g_last_error; }
         return launch_l2p<R>(L, n, leaf_cell, slot_lo, slot_hi, slot_dir, cell_start, cell_stop, cell_alpha,       \
                              cell_level, level_beta, dirs, px, py, pz, kappa, local, near, perm, out, stream);     \
     }                                                                                                               \
-    int defmm_p2p_##SUFFIX(int64_t n, const int64_t* tgt_lo, const int64_t* tgt_hi, const int64_t* ptr,             \
-                           const int64_t* src_lo, const int64_t* src_hi, const double* tx, const double* ty,       \
-                           const double* tz, const double* sx, const double* sy, const double* sz, const void* q,  \
-                           double kappa, double tol, void* near, void* stream) {                                   \
-        return launch_p2p<R>(n, tgt_lo, tgt_hi, ptr, src_lo, src_hi, tx, ty, tz, sx, sy, sz, q, kappa, tol, near,   \
-                             stream);                                                                              \
+    int defmm_p2p_##SUFFIX(int64_t n_items, const int32_t* item_leaf, const int64_t* item_f0,                    \
+                           const int64_t* item_f1, const int64_t* item_out, const int64_t* tgt_lo,                \
+                           const int64_t* tgt_hi, const int64_t* ptr, const int64_t* src_lo,                      \
+                           const int64_t* src_hi, const double* tx, const double* ty, const double* tz,           \
+                           const double* sx, const double* sy, const double* sz, const void* q, double kappa,     \
+                           double tol, void* near, void* partial, int64_t n_split, const int32_t* split_leaf,     \
+                           const int64_t* split_base, const int32_t* split_n, void* stream) {                     \
+        return launch_p2p<R>(n_items, item_leaf, item_f0, item_f1, item_out, tgt_lo, tgt_hi, ptr, src_lo, src_hi,  \
+                             tx, ty, tz, sx, sy, sz, q, kappa, tol, near, partial, n_split, split_leaf,           \
+                             split_base, split_n, stream);                                                        \
     }
 
 DEFMM_EXPORT_TYPED(c128, double)

@@ -18,7 +18,7 @@ import torch
 from . import _lib
 from .config import FmmConfig, FmmInfo, InteractionEvent, TreeConfig
 from .geometry import compute_root_box
-from .plan import build_plan
+from .plan import build_plan, p2p_work_items
 from .tree import build_tree
 
 __all__ = ["FmmPlan", "run_fmm", "run_fmm_full"]
@@ -165,14 +165,23 @@ class FmmPlan:
         self.tgt_lo = _dev(tt.start[p.leaf_cells[lv]], i64, d)
         self.tgt_hi = _dev(tt.stop[p.leaf_cells[lv]], i64, d)
         self.p2p_ptr = _dev(h["p2p_ptr"], i64, d)
-        self.p2p_lo = _dev(p.p2p_lo[h["p2p_sel"]], i64, d)
-        self.p2p_hi = _dev(p.p2p_hi[h["p2p_sel"]], i64, d)
+        p2p_lo, p2p_hi = p.p2p_lo[h["p2p_sel"]], p.p2p_hi[h["p2p_sel"]]
+        self.p2p_lo = _dev(p2p_lo, i64, d)
+        self.p2p_hi = _dev(p2p_hi, i64, d)
+        wi = p2p_work_items(h["p2p_ptr"], p2p_hi - p2p_lo, tt.stop[p.leaf_cells[lv]] - tt.start[p.leaf_cells[lv]])
+        self.n_items = int(wi["item_leaf"].shape[0])
+        self.p2p_items = [_dev(wi[k], torch.int32 if k == "item_leaf" else i64, d)
+                          for k in ("item_leaf", "item_f0", "item_f1", "item_out")]
+        self.n_split = int(wi["split_leaf"].shape[0])
+        self.p2p_split = [_dev(wi["split_leaf"], i32, d), _dev(wi["split_base"], i64, d), _dev(wi["split_n"], i32, d)]
+        self._partial_size = wi["partial_size"]
         # workspaces (storage precision per FmmConfig.dtype)
         cd = self.cdtype
         self.mult = torch.empty((max(p.n_mult, 1), self.L3), dtype=cd, device=d)
         self.hat = torch.empty((max(self.n_hat, 1), self.SS), dtype=cd, device=d)
         self.local = torch.empty((max(p.n_local, 1), self.L3), dtype=cd, device=d)
         self.near = torch.empty(self.n_tgt, dtype=cd, device=d)
+        self.p2p_partial = torch.empty(max(self._partial_size, 1), dtype=cd, device=d)
         self.q = torch.zeros(self.n_src, dtype=cd, device=d)
         self.out = torch.empty(self.n_tgt, dtype=cd, device=d)
         self.side_stream = torch.cuda.Stream(device=d)
@@ -281,9 +290,9 @@ class FmmPlan:
             if stage_events is not None:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e0.record(side)
-            _lib.call(self._op("p2p"), self.n_leaves, self.tgt_lo, self.tgt_hi, self.p2p_ptr, self.p2p_lo,
-                      self.p2p_hi, *self.t_xyz, *self.s_xyz, self.q, float(p.kappa), float(p.tol), self.near,
-                      side.cuda_stream)
+            _lib.call(self._op("p2p"), self.n_items, *self.p2p_items, self.tgt_lo, self.tgt_hi, self.p2p_ptr,
+                      self.p2p_lo, self.p2p_hi, *self.t_xyz, *self.s_xyz, self.q, float(p.kappa), float(p.tol),
+                      self.near, self.p2p_partial, self.n_split, *self.p2p_split, side.cuda_stream)
             if stage_events is not None:
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record(side)
@@ -316,14 +325,14 @@ class FmmPlan:
         out = self.out if out is None else out
         ev = (lambda: torch.cuda.Event(enable_timing=True)) if stage_events is not None else None
         _lib.call(self._op("m2f"), L, self.n_hat, self.hat_slot, self.mult, self.hat, sh)
-        if stage_events is not None:
-            b = ev()
-            b.record(stream)
-            stage_events.append(("upward", self._ev_a, b))
         if self.p2p_overlap != "upward":
             self._near_field(stage_events)
         else:
             stream.wait_stream(self.side_stream)  # M2L runs alone (clean roofline timing)
+        if stage_events is not None:
+            b = ev()
+            b.record(stream)
+            stage_events.append(("upward", self._ev_a, b))
         # M2L (+ fused F2L) into the local slots
         self.local.zero_()
         if self.m2l_variant == "derived":
@@ -356,7 +365,7 @@ class FmmPlan:
 
     @property
     def launches_per_apply(self) -> int:
-        return 5 + len(self.m2m) + len(self.l2l)
+        return 5 + len(self.m2m) + len(self.l2l) + (1 if self.n_split else 0)
 
     def events(self):
         """InteractionEvent list (traversal.py:80-85) with Cell views."""

@@ -36,7 +36,11 @@ import numpy as np
 from .directions import generate_direction_tree, nearest_directions
 from .tree import SQRT3, ClusterTree
 
-__all__ = ["Plan", "build_plan", "hf_max_level", "canonicalize_many", "GROUP48"]
+__all__ = ["Plan", "build_plan", "hf_max_level", "canonicalize_many", "GROUP48", "p2p_work_items"]
+
+# upper bound of target x source pairs per P2P work item (cfg2's largest leaf
+# has 4e4 pairs; cfg3's coarse leaves next to huge source cells up to 1.6e7)
+P2P_ITEM_PAIRS = 1 << 16
 
 
 def _group48() -> np.ndarray:
@@ -431,6 +435,40 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
         plan.m2l_events = (mt, ms, ev_dir)
         plan.p2p_events = (pt, ps)
     return plan
+
+
+def p2p_work_items(ptr, run_len, nt, max_pairs: int = P2P_ITEM_PAIRS) -> dict:
+    """Cut every target leaf's flattened source list into work items of at
+    most ~max_pairs pairs (defmm_p2p_*: item_leaf/f0/f1/out + split lists).
+    Items are ordered by decreasing work so the heavy ones start first."""
+    ptr = np.asarray(ptr, np.int64)
+    cs = np.concatenate([[0], np.cumsum(np.asarray(run_len, np.int64))])
+    ns = cs[ptr[1:]] - cs[ptr[:-1]]
+    nt = np.asarray(nt, np.int64)
+    work = nt * ns
+    k = np.maximum(1, -(-work // max_pairs))
+    k = np.minimum(k, np.maximum(ns, 1))
+    chunk = -(-ns // k)
+    k = np.where(ns > 0, -(-ns // np.maximum(chunk, 1)), 1)  # drop empty tail items
+    leaf = np.repeat(np.arange(ns.shape[0]), k)
+    m = np.arange(leaf.shape[0]) - np.repeat(np.cumsum(k) - k, k)
+    f0 = m * chunk[leaf]
+    f1 = np.minimum(ns[leaf], f0 + chunk[leaf])
+    split = k > 1
+    base = np.zeros(ns.shape[0], np.int64)
+    base[split] = np.concatenate([[0], np.cumsum((k * nt)[split])[:-1]]) if split.any() else []
+    out = np.where(split[leaf], base[leaf] + m * nt[leaf], -1)
+    order = np.argsort(-(nt[leaf] * (f1 - f0)), kind="stable")
+    return {
+        "item_leaf": leaf[order].astype(np.int32),
+        "item_f0": f0[order].astype(np.int64),
+        "item_f1": f1[order].astype(np.int64),
+        "item_out": out[order].astype(np.int64),
+        "split_leaf": np.nonzero(split)[0].astype(np.int32),
+        "split_base": base[split].astype(np.int64),
+        "split_n": k[split].astype(np.int32),
+        "partial_size": int((k * nt)[split].sum()),
+    }
 
 
 def _check_stencils(sym_t, sym_lev, tree, order, tol):

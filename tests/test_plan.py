@@ -170,3 +170,32 @@ def test_two_tree_plan_matches_reference(case):
     pt, pss = pl.p2p_events
     mp = sorted(zip(tt.level[pt].tolist(), tc[pt].tolist(), st.level[pss].tolist(), sc[pss].tolist()))
     assert mp == sorted(map(tuple, g["p2p"].tolist()))
+
+
+def test_p2p_work_items_cover_each_leaf_source_list_once():
+    from paper_2202_04894_b200.plan import p2p_work_items
+
+    rng = np.random.default_rng(0)
+    nleaf = 200
+    runs = rng.integers(1, 6, nleaf)
+    ptr = np.concatenate([[0], np.cumsum(runs)])
+    run_len = rng.integers(1, 5000, ptr[-1])
+    nt = rng.integers(1, 65, nleaf)
+    wi = p2p_work_items(ptr, run_len, nt, max_pairs=20000)
+    cs = np.concatenate([[0], np.cumsum(run_len)])
+    ns = cs[ptr[1:]] - cs[ptr[:-1]]
+    covered = np.zeros(nleaf, np.int64)
+    for l, a, b in zip(wi["item_leaf"], wi["item_f0"], wi["item_f1"]):
+        assert 0 <= a < b <= ns[l]
+        assert nt[l] * (b - a) <= 20000 + nt[l] * 5000  # bounded (one chunk of rounding)
+        covered[l] += b - a
+    assert np.array_equal(covered, ns)
+    # split leaves: partial blocks are disjoint and exactly k * nt long
+    seen = set()
+    for l, base, k in zip(wi["split_leaf"], wi["split_base"], wi["split_n"]):
+        outs = sorted(o for ll, o in zip(wi["item_leaf"], wi["item_out"]) if ll == l)
+        assert outs == [base + m * nt[l] for m in range(k)]
+        assert not (set(range(base, base + k * nt[l])) & seen)
+        seen |= set(range(base, base + k * nt[l]))
+    single = set(range(nleaf)) - set(wi["split_leaf"].tolist())
+    assert all(o == -1 for l, o in zip(wi["item_leaf"], wi["item_out"]) if l in single)
