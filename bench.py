@@ -50,7 +50,8 @@ def _args():
     ap.add_argument("--no-secondary", action="store_true", help="skip the other-precision run of the same lists")
     ap.add_argument("--dtype", default=None, choices=[None, "c128", "c64"], help="override the workload dtype")
     ap.add_argument("--p2p-overlap", default=None, choices=[None, "upward", "m2l"])
-    ap.add_argument("--m2l", default=None, help="M2L kernel variant (derived | canonical)")
+    ap.add_argument("--m2l-levels", default="hybrid", choices=["hybrid", "blocked_all", "rows"])
+    ap.add_argument("--m2l", default=None, help="M2L kernel variant (hybrid | derived | canonical)")
     return ap.parse_args()
 
 
@@ -288,7 +289,8 @@ def run_b200(args):
 
     shard = (rank, world) if world > 1 else None
     t0 = time.perf_counter()
-    plan = FmmPlan(pts, None, cfg, device=dev, charges=q, shard=shard, allreduce=allreduce if shard else None)
+    plan = FmmPlan(pts, None, cfg, device=dev, charges=q, shard=shard, allreduce=allreduce if shard else None,
+                   m2l=args.m2l_levels)
     setup_s = time.perf_counter() - t0
     if args.m2l:
         plan.m2l_variant = args.m2l
@@ -334,7 +336,10 @@ def run_b200(args):
     alg_bytes = n_m2l * 2 * P3 * c + rows * L**3 * c  # symbol + source spectrum per event, local write
     m2l_s = st["m2l"] / 1e3
     kname = f"m2l_rows_kernel<{'float' if dtype == 'c64' else 'double'}, {L}>"
-    traffic = _ncu_traffic(f"{dtype}:{kname}") if args.workload in ("cfg2",) else None
+    if plan.dense_levels:  # hybrid: some levels run the blocked kernel + F2L
+        kname = (f"M2L stage: {kname} (levels {sorted(set(range(plan.tt.depth + 1)) - set(plan.dense_levels))}) + "
+                 f"m2l_blocked_kernel + f2l_rows_kernel (levels {plan.dense_levels})")
+    traffic = _ncu_traffic(f"{dtype}:{kname}") if args.workload in ("cfg2",) and not plan.dense_levels else None
     peak, peak_kind = _measured_peak_hbm()
     achieved = alg_bytes / m2l_s / 1e9
     line = {

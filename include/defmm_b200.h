@@ -68,6 +68,13 @@ void defmm_tree_free(defmm_tree* t);
  *   Row r (target slot row_slot[r]) owns entries [row_ptr[r], row_ptr[r+1]),
  *   int32 pairs {source spectrum index, derived-symbol index}:
  *   local[row_slot[r]] = F2L(sum_e sym_derived[e.sym] (*) hat[e.src])
+ * K7 v3 blocked M2L (product path) -- the same sums grouped in parent-pair blocks:
+ *   group g = (target parent, key) owns rows grp_rows[8g+a] (row index into lhat,
+ *   -1 absent) and blocks [grp_ptr[g], grp_ptr[g+1]); block k = (source parent)
+ *   holds spectra blk_src[8k+b] (-1 absent), derived symbols blk_trans[27k+d]
+ *   for child offset d = (a-b)+(1,1,1) in base 3, and blk_mask[k] with bit 8a+b
+ *   set for every M2L event (a, b).  lhat[row] = sum D (*) hat  (stride
+ *   defmm_spectrum_stride);  then K8 f2l_rows: local[row_slot[r]] = F2L(lhat[r]).
  * K5 L2L -- traversal.py:355-391 in gather form.
  *   for i < n: local[out_slot[i]] += sum_{e in [ptr[i], ptr[i+1])}
  *   (C'0 (x) C'1 (x) C'2) local[src_slot[e]], C' the transposed/conjugate-
@@ -107,6 +114,13 @@ void defmm_tree_free(defmm_tree* t);
                                 const int64_t* row_ptr, const int32_t* entries,                 \
                                 const void* hat, const void* sym_derived, void* local,          \
                                 void* stream);                                                  \
+    int defmm_m2l_blocked_##SUFFIX(int32_t L, int64_t ngroups, const int64_t* grp_ptr,           \
+                                   const int64_t* grp_rows, const int32_t* blk_src,             \
+                                   const int32_t* blk_trans, const int64_t* blk_mask,           \
+                                   const void* hat, const void* sym_derived, void* lhat,        \
+                                   void* stream);                                               \
+    int defmm_f2l_rows_##SUFFIX(int32_t L, int64_t nrows, const int64_t* row_slot,               \
+                                const void* lhat, void* local, void* stream);                   \
     int defmm_l2l_##SUFFIX(int32_t L, int64_t n, const int64_t* out_slot, const int8_t* octant,  \
                            const int64_t* ptr, const int64_t* src_slot, const int32_t* src_dir, \
                            double son_beta, const double* dirs, double kappa, void* local,      \
@@ -130,12 +144,12 @@ void defmm_tree_free(defmm_tree* t);
                            const int32_t* split_n, void* stream);
 
 /* expands to: defmm_p2m_c128 defmm_m2m_c128 defmm_m2f_c128 defmm_symbols_c128
- * defmm_expand_symbols_c128 defmm_m2l_rows_c128 defmm_l2l_c128 defmm_l2p_c128
- * defmm_p2p_c128 */
+ * defmm_expand_symbols_c128 defmm_m2l_rows_c128 defmm_m2l_blocked_c128
+ * defmm_f2l_rows_c128 defmm_l2l_c128 defmm_l2p_c128 defmm_p2p_c128 */
 DEFMM_DECLARE_TYPED(c128)
 /* expands to: defmm_p2m_c64 defmm_m2m_c64 defmm_m2f_c64 defmm_symbols_c64
- * defmm_expand_symbols_c64 defmm_m2l_rows_c64 defmm_l2l_c64 defmm_l2p_c64
- * defmm_p2p_c64 */
+ * defmm_expand_symbols_c64 defmm_m2l_rows_c64 defmm_m2l_blocked_c64
+ * defmm_f2l_rows_c64 defmm_l2l_c64 defmm_l2p_c64 defmm_p2p_c64 */
 DEFMM_DECLARE_TYPED(c64)
 
 /* K7 reference variant (c128): canonical symbols gathered through the closed-

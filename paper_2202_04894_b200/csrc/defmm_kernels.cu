@@ -693,6 +693,151 @@ __global__ void __launch_bounds__(m2l_block<R, L>()) m2l_rows_kernel(
     for (int t = threadIdx.x; t < L3; t += NT) out[t] = from_d<cx<R>>(O[t]);
 }
 
+// ---------------------------------------------------------------------------
+// K7 v3: parent-pair blocked M2L.  A CTA owns a group = (target parent P,
+// key) with up to 8 target rows (its children a); a block = (group, source
+// parent Q) holds up to 8 source spectra (children b) and, per child offset
+// delta = a - b in [-1,1]^3, the derived symbol of translation
+// 2 (P - Q) + delta.  Every (a, b) pair with its bit in the block mask is one
+// M2L event.  The pair -> (symbol, spectrum, accumulator) indices are
+// compile-time constants after unrolling over delta and b, so each loaded
+// spectrum/symbol is reused for all pairs of the block from registers.
+// Accumulated spectra go to lhat (row-major, stride SS); f2l_rows_kernel
+// then applies the pruned inverse DFT.
+
+// bit 8a+b of every (a, b) pair with a - b = delta(d)
+__host__ __device__ constexpr uint64_t pairs_of(int d) {
+    uint64_t m = 0;
+    for (int b = 0; b < 8; ++b) {
+        const int a0 = ((b >> 2) & 1) + d / 9 - 1, a1 = ((b >> 1) & 1) + (d / 3) % 3 - 1, a2 = (b & 1) + d % 3 - 1;
+        if (a0 >= 0 && a0 <= 1 && a1 >= 0 && a1 <= 1 && a2 >= 0 && a2 <= 1)
+            m |= (uint64_t)1 << (8 * (a0 * 4 + a1 * 2 + a2) + b);
+    }
+    return m;
+}
+__host__ __device__ constexpr int pair_a(int d, int b) {
+    const int a0 = ((b >> 2) & 1) + d / 9 - 1, a1 = ((b >> 1) & 1) + (d / 3) % 3 - 1, a2 = (b & 1) + d % 3 - 1;
+    return (a0 >= 0 && a0 <= 1 && a1 >= 0 && a1 <= 1 && a2 >= 0 && a2 <= 1) ? a0 * 4 + a1 * 2 + a2 : -1;
+}
+
+template <typename R, int L>
+__host__ __device__ constexpr int m2lb_threads() {
+    return m2l_threads<L>();  // one complex entry per thread and load
+}
+
+template <typename R>
+struct Vec2;  // two complex entries (c64) / one (c128) per thread-load
+template <>
+struct Vec2<float> {  // one complex64 per load: 2-wide float4 needed 200 registers
+    using t = float2;
+    static constexpr int W = 1;
+};
+template <>
+struct Vec2<double> {
+    using t = double2;
+    static constexpr int W = 1;
+};
+
+__device__ __forceinline__ void vfma(float2 (&acc)[2], const float4& d, const float4& s) {
+    acc[0] = cfma(make_float2(d.x, d.y), make_float2(s.x, s.y), acc[0]);
+    acc[1] = cfma(make_float2(d.z, d.w), make_float2(s.z, s.w), acc[1]);
+}
+__device__ __forceinline__ void vfma(double2 (&acc)[1], const double2& d, const double2& s) {
+    acc[0] = cfma(d, s, acc[0]);
+}
+__device__ __forceinline__ void vfma(float2 (&acc)[1], const float2& d, const float2& s) {
+    acc[0] = cfma(d, s, acc[0]);
+}
+
+template <typename R, int L>
+__global__ void __launch_bounds__(m2lb_threads<R, L>()) m2l_blocked_kernel(
+    int64_t ngroups, const int64_t* __restrict__ grp_ptr, const int64_t* __restrict__ grp_rows,
+    const int32_t* __restrict__ blk_src, const int32_t* __restrict__ blk_trans,
+    const int64_t* __restrict__ blk_mask, const cx<R>* __restrict__ hat, const cx<R>* __restrict__ symd,
+    cx<R>* __restrict__ lhat) {
+    using VT = typename Vec2<R>::t;
+    using V = cx<R>;
+    constexpr int W = Vec2<R>::W;
+    constexpr int SS = spec_stride<R, L>();
+    constexpr int NV = SS / W;
+    constexpr int NT = m2lb_threads<R, L>();
+    constexpr int PER = (NV + NT - 1) / NT;
+    const int64_t g = blockIdx.x;
+    const int64_t b0 = grp_ptr[g], b1 = grp_ptr[g + 1];
+    const VT* hv = reinterpret_cast<const VT*>(hat);
+    const VT* dv = reinterpret_cast<const VT*>(symd);
+    for (int m = 0; m < PER; ++m) {
+        const int jv = threadIdx.x + m * NT;
+        const bool act = jv < NV;
+        V acc[8][W];
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int w = 0; w < W; ++w) acc[a][w] = cz<V>();
+        for (int64_t blk = b0; blk < b1; ++blk) {
+            const uint64_t mask = (uint64_t)__ldg(blk_mask + blk);
+            const int32_t* bs = blk_src + 8 * blk;
+            const int32_t* bt = blk_trans + 27 * blk;
+            VT S[8];
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const int sidx = __ldg(bs + b);
+                S[b] = (sidx >= 0 && act) ? __ldg(hv + (int64_t)sidx * NV + jv) : VT{};
+            }
+            // branch-free body (one basic block): the scheduler can then issue
+            // every symbol load of the block before the FMAs that consume them
+            // (a per-delta `continue` serialised their latencies)
+            VT D[27];
+#pragma unroll
+            for (int d = 0; d < 27; ++d) {
+                const int tidx = __ldg(bt + d);
+                D[d] = ((mask & pairs_of(d)) != 0 && act) ? __ldg(dv + (int64_t)max(tidx, 0) * NV + jv) : VT{};
+            }
+#pragma unroll
+            for (int d = 0; d < 27; ++d) {
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    const int a = pair_a(d, b);  // compile-time after unrolling
+                    if (a >= 0 && ((mask >> (8 * a + b)) & 1)) vfma(acc[a], D[d], S[b]);
+                }
+            }
+        }
+        if (act) {
+#pragma unroll
+            for (int a = 0; a < 8; ++a) {
+                const int64_t row = grp_rows[8 * g + a];
+                if (row >= 0) {
+#pragma unroll
+                    for (int w = 0; w < W; ++w) lhat[row * SS + (int64_t)jv * W + w] = acc[a][w];
+                }
+            }
+        }
+    }
+}
+
+// pruned inverse DFT of accumulated spectra (fourier.py:74-80), one CTA per row:
+// local[row_slot[r]] = F2L(lhat[r]); FP64 transform for both storage types
+template <typename R, int L>
+__global__ void __launch_bounds__(128) f2l_rows_kernel(int64_t nrows, const int64_t* __restrict__ row_slot,
+                                                       const cx<R>* __restrict__ lhat, cx<R>* __restrict__ local) {
+    constexpr int P = pad<L>(), L3 = cube<L>(), P3 = P * P * P;
+    constexpr int SS = spec_stride<R, L>();
+    extern __shared__ unsigned char smraw[];
+    double2* tw = reinterpret_cast<double2*>(smraw);
+    double2* X = tw + P;
+    double2* Z1 = X + P3 + 1;
+    double2* O = Z1 + L * P * P;
+    const int64_t r = blockIdx.x;
+    make_twiddles<P, double2>(tw);
+    const cx<R>* src = lhat + r * SS;
+    for (int j = threadIdx.x; j < P3; j += blockDim.x) X[j] = to_d(src[j]);
+    __syncthreads();
+    f2l_row<L, double2>(tw, X, Z1, O, blockDim.x);
+    __syncthreads();
+    cx<R>* out = local + row_slot[r] * L3;
+    for (int t = threadIdx.x; t < L3; t += blockDim.x) out[t] = from_d<cx<R>>(O[t]);
+}
+
 // Reference M2L (v1, c128): canonical symbols gathered in the inner loop.
 // Kept as an independent operator for the parity tests.
 template <int L>
@@ -823,19 +968,6 @@ __device__ __forceinline__ double2 helm_pair(double dx, double dy, double dz, do
     return make_double2(gr * qs.x - gi * qs.y, gr * qs.y + gi * qs.x);
 }
 
-__device__ __forceinline__ double2 helm_pair(double dxd, double dyd, double dzd, float2 qs, double kpid,
-                                             double told) {
-    const float dx = (float)dxd, dy = (float)dyd, dz = (float)dzd;
-    const float r2 = dx * dx + dy * dy + dz * dz;
-    const float rinv = rsqrtf(r2);
-    const float r = r2 * rinv;
-    const bool ok = r >= (float)told;
-    float s, c;
-    sincospif((float)kpid * (ok ? r : 0.0f), &s, &c);  // full range reduction
-    const float g = ok ? rinv * (float)(1.0 / (4.0 * 3.141592653589793)) : 0.0f;
-    const float gr = g * c, gi = g * s;
-    return make_double2((double)(gr * qs.x - gi * qs.y), (double)(gr * qs.y + gi * qs.x));
-}
 
 // Work items: a target leaf's flattened source list (its merged runs) is cut
 // into pieces [f0, f1) of bounded size so that the few coarse leaves next to
@@ -1216,6 +1348,36 @@ int launch_m2l_rows(int32_t L, int64_t nrows, const int64_t* row_slot, const int
 }
 
 template <typename R>
+int launch_m2l_blocked(int32_t L, int64_t ngroups, const int64_t* grp_ptr, const int64_t* grp_rows,
+                       const int32_t* blk_src, const int32_t* blk_trans, const int64_t* blk_mask, const void* hat,
+                       const void* symd, void* lhat, void* stream) {
+    if (ngroups == 0) return 0;
+    if (!grid_ok(ngroups)) return -1;
+    cudaStream_t s = (cudaStream_t)stream;
+    DEFMM_DISPATCH_L(L, (m2l_blocked_kernel<R, LL><<<(unsigned)ngroups, m2lb_threads<R, LL>(), 0, s>>>(
+                            ngroups, grp_ptr, grp_rows, blk_src, blk_trans, blk_mask, (const cx<R>*)hat,
+                            (const cx<R>*)symd, (cx<R>*)lhat)));
+    return report(cudaGetLastError(), "m2l_blocked");
+}
+
+template <typename R>
+int launch_f2l_rows(int32_t L, int64_t nrows, const int64_t* row_slot, const void* lhat, void* local,
+                    void* stream) {
+    if (nrows == 0) return 0;
+    if (!grid_ok(nrows)) return -1;
+    cudaStream_t s = (cudaStream_t)stream;
+    DEFMM_DISPATCH_L(L, {
+        constexpr int P = 2 * LL - 1;
+        const size_t bytes = sizeof(double2) * (P + P * P * P + 1 + LL * P * P + LL * LL * LL);
+        int rc = set_smem(f2l_rows_kernel<R, LL>, bytes);
+        if (rc) return rc;
+        f2l_rows_kernel<R, LL><<<(unsigned)nrows, 128, bytes, s>>>(nrows, row_slot, (const cx<R>*)lhat,
+                                                                   (cx<R>*)local);
+    });
+    return report(cudaGetLastError(), "f2l_rows");
+}
+
+template <typename R>
 int launch_l2p(int32_t L, int64_t n, const int32_t* leaf_cell, const int64_t* slot_lo, const int64_t* slot_hi,
                const int32_t* slot_dir, const int64_t* cell_start, const int64_t* cell_stop,
                const double* cell_alpha, const int32_t* cell_level, const double* level_beta, const double* dirs,
@@ -1296,6 +1458,16 @@ const char* defmm_last_error(void) { return g_last_error; }
                                 const int32_t* entries, const void* hat, const void* sym_derived, void* local,     \
                                 void* stream) {                                                                    \
         return launch_m2l_rows<R>(L, nrows, row_slot, row_ptr, entries, hat, sym_derived, local, stream);          \
+    }                                                                                                               \
+    int defmm_m2l_blocked_##SUFFIX(int32_t L, int64_t ngroups, const int64_t* grp_ptr, const int64_t* grp_rows,     \
+                                   const int32_t* blk_src, const int32_t* blk_trans, const int64_t* blk_mask,     \
+                                   const void* hat, const void* sym_derived, void* lhat, void* stream) {          \
+        return launch_m2l_blocked<R>(L, ngroups, grp_ptr, grp_rows, blk_src, blk_trans, blk_mask, hat,             \
+                                     sym_derived, lhat, stream);                                                  \
+    }                                                                                                               \
+    int defmm_f2l_rows_##SUFFIX(int32_t L, int64_t nrows, const int64_t* row_slot, const void* lhat, void* local,   \
+                                void* stream) {                                                                    \
+        return launch_f2l_rows<R>(L, nrows, row_slot, lhat, local, stream);                                        \
     }                                                                                                               \
     int defmm_l2l_##SUFFIX(int32_t L, int64_t n, const int64_t* out_slot, const int8_t* octant,                     \
                            const int64_t* ptr, const int64_t* src_slot, const int32_t* src_dir, double son_beta,   \

@@ -28,6 +28,17 @@ def _dev(a, dtype, device):
     return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype).to(device)
 
 
+def _rows_to_ids(slots, rows):
+    """Local slots -> index into the sorted row-slot list ``rows`` (-1 if absent)."""
+    slots = np.asarray(slots)
+    j = np.searchsorted(rows, np.maximum(slots, 0))
+    j = np.minimum(j, max(rows.shape[0] - 1, 0))
+    ok = (slots >= 0) & (rows.shape[0] > 0)
+    if rows.shape[0]:
+        ok &= rows[j] == slots
+    return np.where(ok, j, -1).astype(np.int64)
+
+
 def _sub_csr(ptr, keep):
     """Rows ``keep`` of a CSR: (row ids, new row pointer, selected entry ids)."""
     ptr = np.asarray(ptr)
@@ -44,7 +55,7 @@ class FmmPlan:
 
     def __init__(self, targets, sources=None, config: FmmConfig = FmmConfig(), device="cuda",
                  keep_events: bool = False, charges=None, reuse: "FmmPlan | None" = None,
-                 shard=None, allreduce=None):
+                 shard=None, allreduce=None, m2l: str = "hybrid"):
         """``reuse``: share the host tree + lists of an existing plan built for
         the same geometry and (order, ncrit, eta, kappa) -- e.g. to run the same
         lists at another storage precision.
@@ -60,6 +71,9 @@ class FmmPlan:
         self.device = torch.device(device)
         self._shard_arg = shard
         self.allreduce = allreduce
+        # "hybrid" (per-level choice), "blocked_all" (every level blocked) or
+        # "rows" (no level blocked) -- decides the lists built for the hybrid path
+        self.m2l_variant_default = m2l
         if reuse is not None:
             rc = reuse.config
             if (rc.order, rc.ncrit, rc.eta, rc.kappa, rc.hf_switch, rc.hard_depth_cap) != (
@@ -144,13 +158,24 @@ class FmmPlan:
                              _dev(son_slot, i64, d), int(slots.shape[0])))
         self.hat_slot = _dev(h["hat_slot"], i64, d)
         self.n_hat = int(h["hat_slot"].shape[0])
-        # M2L rows (target-major CSR)
+        # M2L, all rows (target-major CSR): reference variants "derived" / "canonical"
         self.row_slot = _dev(h["rows"], i64, d)
         self.row_ptr = _dev(h["row_ptr"], i64, d)
         self.e_src = _dev(h["ent"][:, 0], i32, d)
         self.e_sym = _dev(p.m2l_sym[h["ent_sel"]], i32, d)
         self.e_rid = _dev(p.m2l_rid[h["ent_sel"]], torch.int8, d)
         self.row_entries = _dev(h["ent"].reshape(-1), i32, d)
+        # M2L product path ("hybrid"): sparse levels -> row kernel, dense -> blocked
+        self.rk_rows = _dev(h["rk_rows"], i64, d)
+        self.rk_ptr = _dev(h["rk_ptr"], i64, d)
+        self.rk_ent = _dev(h["rk_ent"].reshape(-1), i32, d)
+        self.bk_rows = _dev(h["bk_rows"], i64, d)
+        self.n_groups = int(h["grp_rows"].shape[0])
+        self.grp_ptr = _dev(h["grp_ptr"], i64, d)
+        self.grp_rows = _dev(h["grp_rows"].reshape(-1), i64, d)
+        self.blk_src = _dev(h["blk_src"].reshape(-1), i32, d)
+        self.blk_trans = _dev(h["blk_trans"].reshape(-1), i32, d)
+        self.blk_mask = _dev(h["blk_mask"], i64, d)
         # downward
         self.l2l = []
         for lev, outs, octant, ptr, src, sdir in h["l2l"]:
@@ -180,12 +205,13 @@ class FmmPlan:
         self.mult = torch.empty((max(p.n_mult, 1), self.L3), dtype=cd, device=d)
         self.hat = torch.empty((max(self.n_hat, 1), self.SS), dtype=cd, device=d)
         self.local = torch.empty((max(p.n_local, 1), self.L3), dtype=cd, device=d)
+        self.lhat = torch.empty((max(int(self.bk_rows.shape[0]), 1), self.SS), dtype=cd, device=d)
         self.near = torch.empty(self.n_tgt, dtype=cd, device=d)
         self.p2p_partial = torch.empty(max(self._partial_size, 1), dtype=cd, device=d)
         self.q = torch.zeros(self.n_src, dtype=cd, device=d)
         self.out = torch.empty(self.n_tgt, dtype=cd, device=d)
         self.side_stream = torch.cuda.Stream(device=d)
-        self.m2l_variant = "derived"
+        self.m2l_variant = "hybrid"
         self.p2p_overlap = "upward"  # or "m2l"
 
     def _make_shard(self):
@@ -200,7 +226,51 @@ class FmmPlan:
         if self.shard is not None and self.shard.world > 1 and self.allreduce is None:
             raise ValueError("a sharded plan needs allreduce= to complete the multipoles")
 
+    # events per parent-pair block above which a level's M2L runs blocked
+    BLOCKED_MIN_EVENTS_PER_BLOCK = 32.0
+
     def _host_lists(self) -> dict:
+        """Per-level hybrid M2L: levels whose parent-pair blocks are dense
+        (volume-like, >= BLOCKED_MIN_EVENTS_PER_BLOCK events per block) run
+        the blocked kernel (K7 v3, operand reuse in registers), sparse
+        (surface-like) levels the row kernel (its blocks would be mostly
+        predicated-off pairs) -- profiles/r01_summary_v3.md."""
+        h = self._host_lists_all()
+        p, tt = self.plan, self.tt
+        rows = h["rows"]
+        rlev = tt.level[p.l_cell[rows]] if rows.size else np.zeros(0, np.int64)
+        # density per level from the full plan (identical on every rank)
+        g_rows = p.blk_group_rows
+        first = np.where(g_rows >= 0, g_rows, np.iinfo(np.int64).max).min(axis=1)
+        glev_full = tt.level[p.l_cell[first]] if first.size else np.zeros(0, np.int64)
+        nblk = np.diff(p.blk_group_ptr)
+        ev = np.bitwise_count(p.blk_mask.view(np.uint64)).astype(np.int64) if p.blk_mask.size else np.zeros(0, np.int64)
+        blev = np.repeat(glev_full, nblk)
+        dense = set()
+        for lev in np.unique(blev):
+            sel = blev == lev
+            if ev[sel].mean() >= self.BLOCKED_MIN_EVENTS_PER_BLOCK:
+                dense.add(int(lev))
+        if self.m2l_variant_default != "blocked":
+            dense = set() if self.m2l_variant_default != "blocked_all" else set(int(x) for x in np.unique(blev))
+        is_dense = np.isin(rlev, list(dense)) if dense else np.zeros(rows.shape[0], bool)
+        # rows of sparse levels -> row kernel
+        keep_rows, rptr, rsel = _sub_csr(h["row_ptr"], ~is_dense)
+        h["rk_rows"], h["rk_ptr"], h["rk_ent"] = rows[~is_dense], rptr, h["ent"][rsel]
+        # groups of dense levels -> blocked kernel, rows renumbered into lhat
+        dense_rows = rows[is_dense]
+        gr = h["grp_rows"]
+        gr_slots = np.where(gr >= 0, rows[np.maximum(gr, 0)] if rows.size else -1, -1)
+        gid = _rows_to_ids(gr_slots, dense_rows)
+        gkeep = np.any(gid >= 0, axis=1)
+        _, gptr, bsel = _sub_csr(h["grp_ptr"], gkeep)
+        h["bk_rows"] = dense_rows
+        h["grp_ptr"], h["grp_rows"] = gptr, gid[gkeep]
+        h["blk_src"], h["blk_trans"], h["blk_mask"] = h["blk_src"][bsel], h["blk_trans"][bsel], h["blk_mask"][bsel]
+        self.dense_levels = sorted(dense)
+        return h
+
+    def _host_lists_all(self) -> dict:
         """The plan's lists, restricted to this rank's chunk when sharded
         (parallel.py); spectra are renumbered compactly."""
         p, sh = self.plan, self.shard
@@ -218,7 +288,12 @@ class FmmPlan:
             "p2p_ptr": p.p2p_ptr,
             "p2p_sel": np.arange(p.p2p_lo.shape[0]),
         }
+        # blocked M2L: group rows as indices into h["rows"] (lhat rows)
+        blk = {"grp_ptr": p.blk_group_ptr, "grp_rows": p.blk_group_rows, "blk_src": p.blk_src,
+               "blk_trans": p.blk_trans, "blk_mask": p.blk_mask}
         if sh is None:
+            h.update(blk)
+            h["grp_rows"] = _rows_to_ids(blk["grp_rows"], h["rows"])
             return h
         h["p2m_idx"] = sh.p2m_idx
         h["m2m"] = [(lev, sl[k], ss[k]) for (lev, sl, ss), k in zip(p.m2m_levels, sh.m2m_keep) if k.any()]
@@ -230,6 +305,13 @@ class FmmPlan:
         ent = p.m2l_rows_entries[sel].copy()
         ent[:, 0] = remap[ent[:, 0]]
         h["ent"], h["hat_slot"] = ent, p.hat_slot[hat_ids]
+        gr = _rows_to_ids(p.blk_group_rows, h["rows"])  # -1 for rows of other ranks
+        gkeep = np.any(gr >= 0, axis=1)
+        _, gptr, bsel = _sub_csr(p.blk_group_ptr, gkeep)
+        bsrc = p.blk_src[bsel]
+        h.update({"grp_ptr": gptr, "grp_rows": gr[gkeep], "blk_trans": p.blk_trans[bsel],
+                  "blk_mask": p.blk_mask[bsel],
+                  "blk_src": np.where(bsrc >= 0, remap[np.maximum(bsrc, 0)], -1).astype(np.int32)})
         l2l = []
         for (lev, outs, octant, lptr, src, sdir), k in zip(p.l2l_levels, sh.l2l_keep):
             if not k.any():
@@ -335,7 +417,13 @@ class FmmPlan:
             stage_events.append(("upward", self._ev_a, b))
         # M2L (+ fused F2L) into the local slots
         self.local.zero_()
-        if self.m2l_variant == "derived":
+        if self.m2l_variant == "hybrid":
+            _lib.call(self._op("m2l_rows"), L, self.rk_rows.shape[0], self.rk_rows, self.rk_ptr, self.rk_ent,
+                      self.hat, self.sym_derived, self.local, sh)
+            _lib.call(self._op("m2l_blocked"), L, self.n_groups, self.grp_ptr, self.grp_rows, self.blk_src,
+                      self.blk_trans, self.blk_mask, self.hat, self.sym_derived, self.lhat, sh)
+            _lib.call(self._op("f2l_rows"), L, self.bk_rows.shape[0], self.bk_rows, self.lhat, self.local, sh)
+        elif self.m2l_variant == "derived":
             _lib.call(self._op("m2l_rows"), L, self.row_slot.shape[0], self.row_slot, self.row_ptr,
                       self.row_entries, self.hat, self.sym_derived, self.local, sh)
         elif self.m2l_variant == "canonical" and self.config.dtype == "c128":
@@ -365,7 +453,7 @@ class FmmPlan:
 
     @property
     def launches_per_apply(self) -> int:
-        return 5 + len(self.m2m) + len(self.l2l) + (1 if self.n_split else 0)
+        return 5 + len(self.m2m) + len(self.l2l) + (1 if self.n_split else 0) + 2 * (self.m2l_variant == "hybrid")
 
     def events(self):
         """InteractionEvent list (traversal.py:80-85) with Cell views."""

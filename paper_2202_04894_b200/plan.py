@@ -153,6 +153,12 @@ class Plan:
     # derived symbols (one per distinct (level, translation))
     trans_canon: np.ndarray = None  # canonical symbol id
     trans_rid: np.ndarray = None  # cube-group rotation id
+    # parent-pair blocks of the blocked M2L (K7 v3)
+    blk_group_rows: np.ndarray = None  # (ngroups, 8) local slots of the group's rows, -1 absent
+    blk_group_ptr: np.ndarray = None  # block range per group
+    blk_src: np.ndarray = None  # (nblocks, 8) spectrum index per source child, -1 absent
+    blk_trans: np.ndarray = None  # (nblocks, 27) derived symbol per child offset, -1 unused
+    blk_mask: np.ndarray = None  # (nblocks,) int64: bit 8a+b = (a, b) is an M2L event
     # event logs (optional, for the events= API)
     m2l_events: tuple = None
     p2p_events: tuple = None
@@ -369,6 +375,7 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
     # derived-symbol table: one per distinct (level, t)
     plan.trans_canon = cinv.astype(np.int32)
     plan.trans_rid = rid
+    _m2l_blocks(plan, tt, st, mt, ms, mlev, src_loc, src_hat, inv, tslot)
 
     # L2L gather lists per son level
     l2l_levels = []
@@ -435,6 +442,65 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
         plan.m2l_events = (mt, ms, ev_dir)
         plan.p2p_events = (pt, ps)
     return plan
+
+
+def _octant(tree, cells):
+    par = tree.parent[cells]
+    o = tree.coords[cells] - 2 * tree.coords[par]
+    return par, o[:, 0] * 4 + o[:, 1] * 2 + o[:, 2]
+
+
+def _m2l_blocks(plan, tt, st, mt, ms, mlev, key, src_hat, trans, tslot):
+    """Parent-pair blocks for the blocked M2L kernel (K7 v3).
+
+    Group g = (target parent P, key): up to 8 target rows (t_a, key), a = the
+    octant of t in P.  Block = (g, source parent Q): up to 8 source spectra
+    (s_b, key) and, for every child offset delta = a_vec - b_vec in [-1,1]^3,
+    the derived symbol of translation 2 (P - Q) + delta; bit 8a+b of the
+    block mask marks the (a, b) pairs that are M2L events.  Every event lives
+    in exactly one block, so the kernel reuses each loaded spectrum/symbol for
+    all pairs of its block from registers."""
+    n = mt.shape[0]
+    if n == 0:
+        plan.blk_group_rows = np.zeros((0, 8), np.int64)
+        plan.blk_group_ptr = np.zeros(1, np.int64)
+        plan.blk_src = np.zeros((0, 8), np.int32)
+        plan.blk_trans = np.zeros((0, 27), np.int32)
+        plan.blk_mask = np.zeros(0, np.int64)
+        return
+    P, a = _octant(tt, mt)
+    Q, b = _octant(st, ms)
+    dv = (tt.coords[mt] - 2 * tt.coords[P]) - (st.coords[ms] - 2 * st.coords[Q])
+    d = (dv[:, 0] + 1) * 9 + (dv[:, 1] + 1) * 3 + (dv[:, 2] + 1)
+    kk = key + 1
+    # groups ordered (level, key, P): symbols of one key stay L2-resident
+    go = np.lexsort((P, kk, mlev))
+    gk = np.stack([mlev[go], kk[go], P[go]], 1)
+    gbrk = np.ones(n, bool)
+    gbrk[1:] = np.any(gk[1:] != gk[:-1], axis=1)
+    gid = np.empty(n, np.int64)
+    gid[go] = np.cumsum(gbrk) - 1
+    ng = int(gid.max()) + 1
+    bo = np.lexsort((Q, gid))
+    bk = np.stack([gid[bo], Q[bo]], 1)
+    bbrk = np.ones(n, bool)
+    bbrk[1:] = np.any(bk[1:] != bk[:-1], axis=1)
+    bid = np.empty(n, np.int64)
+    bid[bo] = np.cumsum(bbrk) - 1
+    nb = int(bid.max()) + 1
+    rows = np.full((ng, 8), -1, np.int64)
+    rows[gid, a] = tslot
+    src = np.full((nb, 8), -1, np.int32)
+    src[bid, b] = src_hat
+    tr = np.full((nb, 27), -1, np.int32)
+    tr[bid, d] = trans
+    mask = np.zeros(nb, np.int64)
+    np.bitwise_or.at(mask, bid, np.left_shift(np.int64(1), (8 * a + b).astype(np.int64)))
+    blk_g = np.empty(nb, np.int64)
+    blk_g[bid] = gid
+    plan.blk_group_rows = rows
+    plan.blk_group_ptr = np.searchsorted(blk_g, np.arange(ng + 1)).astype(np.int64)
+    plan.blk_src, plan.blk_trans, plan.blk_mask = src, tr, mask
 
 
 def p2p_work_items(ptr, run_len, nt, max_pairs: int = P2P_ITEM_PAIRS) -> dict:

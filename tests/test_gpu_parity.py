@@ -130,8 +130,8 @@ def test_symbol_and_m2f_kernels(L):
 
 @pytest.mark.parametrize("case", ["cubesurf4000", "c1_kd8", "volume3000"])
 def test_m2l_canonical_gather_and_derived_symbols_agree(case):
-    """The canonical-gather M2L (in-loop rotation) and the derived-symbol M2L
-    (product path) give the same potentials."""
+    """The canonical-gather M2L (in-loop rotation), the row-wise derived-symbol
+    M2L and the parent-pair blocked M2L (product path) agree."""
     from paper_2202_04894_b200 import FmmConfig, FmmPlan
 
     g = load_case(case)
@@ -141,6 +141,12 @@ def test_m2l_canonical_gather_and_derived_symbols_agree(case):
     plan.m2l_variant = "derived"
     b = plan.apply().cpu().numpy()
     assert _rel(b, a) <= 1e-13
+    plan.m2l_variant = "hybrid"
+    c = plan.apply().cpu().numpy()
+    assert _rel(c, a) <= 1e-13
+    for mode in ("blocked_all", "rows"):
+        p2 = FmmPlan(g["points"], None, FmmConfig(**g["config"]), charges=g["charges"], reuse=plan, m2l=mode)
+        assert _rel(p2.apply().cpu().numpy(), a) <= 1e-13
     assert _rel(b, g["pot"]) <= FP64_TOL
 
 

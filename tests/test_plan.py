@@ -199,3 +199,33 @@ def test_p2p_work_items_cover_each_leaf_source_list_once():
         seen |= set(range(base, base + k * nt[l]))
     single = set(range(nleaf)) - set(wi["split_leaf"].tolist())
     assert all(o == -1 for l, o in zip(wi["item_leaf"], wi["item_out"]) if l in single)
+
+
+@pytest.mark.parametrize("case", ["cubesurf4000", "volume3000", "c1_kd16"])
+def test_m2l_blocks_reconstruct_the_event_list(case):
+    """Every M2L event appears in exactly one parent-pair block with its row,
+    source spectrum and derived symbol (K7 v3 input)."""
+    g = load_case(case)
+    tr, ps, pl = _plan(g)
+    rows_ev = []
+    for gi in range(pl.blk_group_rows.shape[0]):
+        for bi in range(pl.blk_group_ptr[gi], pl.blk_group_ptr[gi + 1]):
+            m = int(pl.blk_mask[bi])
+            for bit in range(64):
+                if (m >> bit) & 1:
+                    a, b = divmod(bit, 8)
+                    row = pl.blk_group_rows[gi, a]
+                    src = pl.blk_src[bi, b]
+                    # child offset index from the octants
+                    av = np.array([(a >> 2) & 1, (a >> 1) & 1, a & 1])
+                    bv = np.array([(b >> 2) & 1, (b >> 1) & 1, b & 1])
+                    dv = av - bv
+                    d = (dv[0] + 1) * 9 + (dv[1] + 1) * 3 + (dv[2] + 1)
+                    tr_id = pl.blk_trans[bi, d]
+                    assert row >= 0 and src >= 0 and tr_id >= 0
+                    rows_ev.append((int(row), int(src), int(tr_id)))
+    ref = []
+    for r in range(len(pl.m2l_row_slot)):
+        for e in range(pl.m2l_row_ptr[r], pl.m2l_row_ptr[r + 1]):
+            ref.append((int(pl.m2l_row_slot[r]), int(pl.m2l_rows_entries[e, 0]), int(pl.m2l_rows_entries[e, 1])))
+    assert sorted(rows_ev) == sorted(ref)
