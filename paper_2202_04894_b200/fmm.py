@@ -251,8 +251,10 @@ class FmmPlan:
             sel = blev == lev
             if ev[sel].mean() >= self.BLOCKED_MIN_EVENTS_PER_BLOCK:
                 dense.add(int(lev))
-        if self.m2l_variant_default != "blocked":
-            dense = set() if self.m2l_variant_default != "blocked_all" else set(int(x) for x in np.unique(blev))
+        if self.m2l_variant_default == "rows":
+            dense = set()
+        elif self.m2l_variant_default == "blocked_all":
+            dense = set(int(x) for x in np.unique(blev))
         is_dense = np.isin(rlev, list(dense)) if dense else np.zeros(rows.shape[0], bool)
         # rows of sparse levels -> row kernel
         keep_rows, rptr, rsel = _sub_csr(h["row_ptr"], ~is_dense)
