@@ -982,21 +982,61 @@ struct P2PItems {
     const int64_t* out;
 };
 
-// visit the sources [f0, f1) of the flattened run list of one leaf
-template <typename F>
-__device__ __forceinline__ void for_source_tiles(const int64_t* src_lo, const int64_t* src_hi, int64_t e0,
-                                                 int64_t e1, int64_t f0, int64_t f1, F&& tile) {
-    int64_t base = 0;  // flattened offset of run e
-    for (int64_t e = e0; e < e1 && base < f1; ++e) {
-        const int64_t a = src_lo[e], len = src_hi[e] - a;
-        const int64_t lo = f0 > base ? f0 - base : 0;
-        const int64_t hi = (f1 - base) < len ? (f1 - base) : len;
-        for (int64_t sb = lo; sb < hi; sb += P2P_TILE) {
-            const int cnt = (int)((hi - sb) < P2P_TILE ? (hi - sb) : P2P_TILE);
-            tile(a + sb, cnt);
+// Visit the sources [f0, f1) of one leaf's flattened run list in PACKED tiles
+// of up to P2P_TILE sources (a tile may span several runs: leaves in cfg3/cfg5
+// have 14-18 short runs).  The run table of the item is staged in shared
+// memory (windows of P2P_MAXRUNS runs); `load(slot, src)` stages source src in
+// tile slot `slot`, then `compute(cnt)` consumes the tile.
+constexpr int P2P_MAXRUNS = 128;
+
+template <typename LOAD, typename COMPUTE>
+__device__ __forceinline__ void for_packed_tiles(const int64_t* src_lo, const int64_t* src_hi, int64_t e0,
+                                                 int64_t e1, int64_t f0, int64_t f1, int64_t* rlo,
+                                                 int64_t* rpre, LOAD&& load, COMPUTE&& compute) {
+    int64_t base = 0;  // flattened offset of the first run of the window
+    for (int64_t w0 = e0; w0 < e1 && base < f1; w0 += P2P_MAXRUNS) {
+        const int nr = (int)((e1 - w0) < P2P_MAXRUNS ? (e1 - w0) : P2P_MAXRUNS);
+        __syncthreads();
+        for (int k = threadIdx.x; k < nr; k += blockDim.x) {
+            rlo[k] = src_lo[w0 + k];
+            rpre[k + 1] = src_hi[w0 + k] - src_lo[w0 + k];
         }
-        base += len;
+        __syncthreads();
+        if (threadIdx.x == 0) {  // inclusive prefix of the run lengths (<= 128 adds)
+            int64_t acc = base;
+            rpre[0] = base;
+            for (int k = 1; k <= nr; ++k) {
+                acc += rpre[k];
+                rpre[k] = acc;
+            }
+        }
+        __syncthreads();
+        const int64_t wend = rpre[nr];
+        const int64_t lo = f0 > base ? f0 : base, hi = f1 < wend ? f1 : wend;
+        for (int64_t fb = lo; fb < hi; fb += P2P_TILE) {
+            const int cnt = (int)((hi - fb) < P2P_TILE ? (hi - fb) : P2P_TILE);
+            __syncthreads();
+            for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
+                const int64_t g = fb + k;
+                int r = 0, top = nr;  // last run with rpre[r] <= g
+                while (top - r > 1) {
+                    const int mid = (r + top) >> 1;
+                    if (rpre[mid] <= g) r = mid; else top = mid;
+                }
+                load(k, rlo[r] + (g - rpre[r]));
+            }
+            __syncthreads();
+            compute(cnt);
+        }
+        base = wend;
     }
+}
+
+// `split` threads share the sources of a PAIR of targets (each staged source
+// feeds two pair evaluations from registers); fixed-order shuffle reduction.
+__device__ __forceinline__ int p2p_split(int64_t nt) {
+    const int64_t pairs = (nt + 1) / 2;
+    return pairs <= 16 ? 8 : pairs <= 32 ? 4 : pairs <= 64 ? 2 : 1;
 }
 
 template <typename R>
@@ -1010,47 +1050,59 @@ __global__ void __launch_bounds__(P2P_NT) p2p_kernel(
     using V = cx<R>;
     __shared__ double sx[P2P_TILE], sy[P2P_TILE], sz[P2P_TILE];
     __shared__ V sq[P2P_TILE];
+    __shared__ int64_t rlo[P2P_MAXRUNS], rpre[P2P_MAXRUNS + 1];
     const int64_t item = blockIdx.x;
     const int leaf = it.leaf[item];
     const int64_t f0 = it.f0[item], f1 = it.f1[item], ob = it.out[item];
     const int64_t t0 = tgt_lo[leaf], t1 = tgt_hi[leaf];
-    const int64_t nt = t1 - t0;
-    const int split = nt <= 16 ? 8 : nt <= 32 ? 4 : nt <= 64 ? 2 : 1;
-    const int per_pass = P2P_NT / split;
+    const int split = p2p_split(t1 - t0);
+    const int per_pass = 2 * (P2P_NT / split);
     const double kpi = kappa / 3.141592653589793;
     const int64_t e0 = ptr[leaf], e1 = ptr[leaf + 1];
     for (int64_t tb = t0; tb < t1; tb += per_pass) {
-        const int64_t t = tb + threadIdx.x / split;
+        const int64_t ta = tb + 2 * (threadIdx.x / split), tb2 = ta + 1;
         const int part = threadIdx.x % split;
-        const bool valid = t < t1;
-        const double xt = valid ? tx[t] : 0.0, yt = valid ? ty[t] : 0.0, zt = valid ? tz[t] : 0.0;
-        double2 acc = make_double2(0.0, 0.0);
-        for_source_tiles(src_lo, src_hi, e0, e1, f0, f1, [&](int64_t sb, int cnt) {
-            __syncthreads();
-            for (int k = threadIdx.x; k < cnt; k += P2P_NT) {
-                sx[k] = px[sb + k];
-                sy[k] = py[sb + k];
-                sz[k] = pz[sb + k];
-                sq[k] = q[sb + k];
-            }
-            __syncthreads();
-            if (valid) {
-                for (int k = part; k < cnt; k += split) {
-                    const double2 g = helm_pair(xt - sx[k], yt - sy[k], zt - sz[k], sq[k], kpi, tol);
-                    acc.x += g.x;
-                    acc.y += g.y;
+        const bool va = ta < t1, vb = tb2 < t1;
+        const double xa = va ? tx[ta] : 0.0, ya = va ? ty[ta] : 0.0, za = va ? tz[ta] : 0.0;
+        const double xb = vb ? tx[tb2] : xa, yb = vb ? ty[tb2] : ya, zb = vb ? tz[tb2] : za;
+        double2 acca = make_double2(0.0, 0.0), accb = make_double2(0.0, 0.0);
+        for_packed_tiles(
+            src_lo, src_hi, e0, e1, f0, f1, rlo, rpre,
+            [&](int k, int64_t g) {
+                sx[k] = px[g];
+                sy[k] = py[g];
+                sz[k] = pz[g];
+                sq[k] = q[g];
+            },
+            [&](int cnt) {
+                if (va) {
+                    for (int k = part; k < cnt; k += split) {
+                        const double x = sx[k], y = sy[k], z = sz[k];
+                        const double2 qs = to_d(sq[k]);
+                        const double2 ga = helm_pair(xa - x, ya - y, za - z, qs, kpi, tol);
+                        const double2 gb = helm_pair(xb - x, yb - y, zb - z, qs, kpi, tol);
+                        acca.x += ga.x;
+                        acca.y += ga.y;
+                        accb.x += gb.x;
+                        accb.y += gb.y;
+                    }
                 }
-            }
-        });
+            });
         for (int off = 1; off < split; off <<= 1) {
-            acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
-            acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+            acca.x += __shfl_xor_sync(0xffffffffu, acca.x, off);
+            acca.y += __shfl_xor_sync(0xffffffffu, acca.y, off);
+            accb.x += __shfl_xor_sync(0xffffffffu, accb.x, off);
+            accb.y += __shfl_xor_sync(0xffffffffu, accb.y, off);
         }
-        if (valid && part == 0) {
-            if (ob < 0)
-                near[t] = from_d<V>(acc);
-            else
-                partial[ob + (t - t0)] = from_d<V>(acc);
+        if (part == 0) {
+            if (va) {
+                if (ob < 0) near[ta] = from_d<V>(acca);
+                else partial[ob + (ta - t0)] = from_d<V>(acca);
+            }
+            if (vb) {
+                if (ob < 0) near[tb2] = from_d<V>(accb);
+                else partial[ob + (tb2 - t0)] = from_d<V>(accb);
+            }
         }
     }
 }
@@ -1086,6 +1138,34 @@ __device__ __forceinline__ void split_f32(double x, float& hi, float& lo) {
     lo = __double2float_rn(x - (double)hi);
 }
 
+__device__ __forceinline__ float rsqrt_approx(float x) {  // MUFU.RSQ without denormal fix-ups
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// one complex64 pair: near-field differences from hi/lo splits, phase
+// u = kappa r / (2 pi) reduced to [-1/2, 1/2] for the hardware sin/cos
+__device__ __forceinline__ void pair_f32(float xh, float xl, float yh, float yl, float zh, float zl,
+                                         const float4& h, const float4& l, float k2pi, float ftol,
+                                         float inv4pi, float& ar, float& ai) {
+    const float dx = (xh - h.x) + (xl - l.x);
+    const float dy = (yh - h.y) + (yl - l.y);
+    const float dz = (zh - h.z) + (zl - l.z);
+    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    const float rinv = rsqrt_approx(r2);  // r2 = 0 -> inf -> r = NaN -> masked
+    const float r = r2 * rinv;
+    const bool ok = r >= ftol;
+    float u = k2pi * (ok ? r : 0.0f);
+    u -= rintf(u);
+    float sn, cs;
+    __sincosf(6.283185307179586f * u, &sn, &cs);
+    const float g = ok ? rinv * inv4pi : 0.0f;
+    const float gr = g * cs, gi = g * sn;
+    ar = fmaf(gr, h.w, fmaf(-gi, l.w, ar));
+    ai = fmaf(gr, l.w, fmaf(gi, h.w, ai));
+}
+
 __global__ void __launch_bounds__(P2P_NT) p2p_f32_kernel(
     int64_t n, P2PItems it, const int64_t* __restrict__ tgt_lo, const int64_t* __restrict__ tgt_hi,
     const int64_t* __restrict__ ptr, const int64_t* __restrict__ src_lo,
@@ -1095,73 +1175,72 @@ __global__ void __launch_bounds__(P2P_NT) p2p_f32_kernel(
     double kappa, double tol, float2* __restrict__ near, float2* __restrict__ partial) {
     __shared__ float4 sh[P2P_TILE];  // (x_hi, y_hi, z_hi, q.re)
     __shared__ float4 sl[P2P_TILE];  // (x_lo, y_lo, z_lo, q.im)
+    __shared__ int64_t rlo[P2P_MAXRUNS], rpre[P2P_MAXRUNS + 1];
     const int64_t item = blockIdx.x;
     const int leaf = it.leaf[item];
     const int64_t f0 = it.f0[item], f1 = it.f1[item], ob = it.out[item];
     const int64_t t0 = tgt_lo[leaf], t1 = tgt_hi[leaf];
-    const int64_t nt = t1 - t0;
-    const int split = nt <= 16 ? 8 : nt <= 32 ? 4 : nt <= 64 ? 2 : 1;
-    const int per_pass = P2P_NT / split;
-    const float kpi = (float)(kappa / 3.141592653589793);
+    const int split = p2p_split(t1 - t0);
+    const int per_pass = 2 * (P2P_NT / split);
+    const float k2pi = (float)(kappa / (2.0 * 3.141592653589793));
     const float ftol = (float)tol;
     const float inv4pi = (float)(1.0 / (4.0 * 3.141592653589793));
     const int64_t e0 = ptr[leaf], e1 = ptr[leaf + 1];
     for (int64_t tb = t0; tb < t1; tb += per_pass) {
-        const int64_t t = tb + threadIdx.x / split;
+        const int64_t ta = tb + 2 * (threadIdx.x / split), tb2 = ta + 1;
         const int part = threadIdx.x % split;
-        const bool valid = t < t1;
-        float xh = 0.f, xl = 0.f, yh = 0.f, yl = 0.f, zh = 0.f, zl = 0.f;
-        if (valid) {
-            split_f32(tx[t], xh, xl);
-            split_f32(ty[t], yh, yl);
-            split_f32(tz[t], zh, zl);
+        const bool va = ta < t1, vb = tb2 < t1;
+        float axh = 0.f, axl = 0.f, ayh = 0.f, ayl = 0.f, azh = 0.f, azl = 0.f;
+        if (va) {
+            split_f32(tx[ta], axh, axl);
+            split_f32(ty[ta], ayh, ayl);
+            split_f32(tz[ta], azh, azl);
         }
-        float ar = 0.f, ai = 0.f;
-        for_source_tiles(src_lo, src_hi, e0, e1, f0, f1, [&](int64_t sb, int cnt) {
-            __syncthreads();
-            for (int k = threadIdx.x; k < cnt; k += P2P_NT) {
+        float bxh = axh, bxl = axl, byh = ayh, byl = ayl, bzh = azh, bzl = azl;
+        if (vb) {
+            split_f32(tx[tb2], bxh, bxl);
+            split_f32(ty[tb2], byh, byl);
+            split_f32(tz[tb2], bzh, bzl);
+        }
+        float aar = 0.f, aai = 0.f, bar = 0.f, bai = 0.f;
+        for_packed_tiles(
+            src_lo, src_hi, e0, e1, f0, f1, rlo, rpre,
+            [&](int k, int64_t g) {
                 float4 hh, ll;
-                split_f32(px[sb + k], hh.x, ll.x);
-                split_f32(py[sb + k], hh.y, ll.y);
-                split_f32(pz[sb + k], hh.z, ll.z);
-                const float2 qq = q[sb + k];
+                split_f32(px[g], hh.x, ll.x);
+                split_f32(py[g], hh.y, ll.y);
+                split_f32(pz[g], hh.z, ll.z);
+                const float2 qq = q[g];
                 hh.w = qq.x;
                 ll.w = qq.y;
                 sh[k] = hh;
                 sl[k] = ll;
-            }
-            __syncthreads();
-            if (valid) {
-#pragma unroll 4
-                for (int k = part; k < cnt; k += split) {
-                    const float4 h = sh[k], l = sl[k];
-                    const float dx = (xh - h.x) + (xl - l.x);
-                    const float dy = (yh - h.y) + (yl - l.y);
-                    const float dz = (zh - h.z) + (zl - l.z);
-                    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                    const float rinv = rsqrtf(r2);
-                    const float r = r2 * rinv;
-                    const bool ok = r >= ftol;  // r2 = 0 -> NaN -> masked
-                    float xr = kpi * (ok ? r : 0.0f);
-                    xr = fmaf(-2.0f, rintf(0.5f * xr), xr);  // kappa r / pi reduced to [-1, 1]
-                    float sn, cs;
-                    __sincosf(3.14159265358979f * xr, &sn, &cs);
-                    const float g = ok ? rinv * inv4pi : 0.0f;
-                    const float gr = g * cs, gi = g * sn;
-                    ar = fmaf(gr, h.w, fmaf(-gi, l.w, ar));
-                    ai = fmaf(gr, l.w, fmaf(gi, h.w, ai));
+            },
+            [&](int cnt) {
+                if (va) {
+#pragma unroll 2
+                    for (int k = part; k < cnt; k += split) {
+                        const float4 h = sh[k], l = sl[k];
+                        pair_f32(axh, axl, ayh, ayl, azh, azl, h, l, k2pi, ftol, inv4pi, aar, aai);
+                        pair_f32(bxh, bxl, byh, byl, bzh, bzl, h, l, k2pi, ftol, inv4pi, bar, bai);
+                    }
                 }
-            }
-        });
+            });
         for (int off = 1; off < split; off <<= 1) {
-            ar += __shfl_xor_sync(0xffffffffu, ar, off);
-            ai += __shfl_xor_sync(0xffffffffu, ai, off);
+            aar += __shfl_xor_sync(0xffffffffu, aar, off);
+            aai += __shfl_xor_sync(0xffffffffu, aai, off);
+            bar += __shfl_xor_sync(0xffffffffu, bar, off);
+            bai += __shfl_xor_sync(0xffffffffu, bai, off);
         }
-        if (valid && part == 0) {
-            if (ob < 0)
-                near[t] = make_float2(ar, ai);
-            else
-                partial[ob + (t - t0)] = make_float2(ar, ai);
+        if (part == 0) {
+            if (va) {
+                if (ob < 0) near[ta] = make_float2(aar, aai);
+                else partial[ob + (ta - t0)] = make_float2(aar, aai);
+            }
+            if (vb) {
+                if (ob < 0) near[tb2] = make_float2(bar, bai);
+                else partial[ob + (tb2 - t0)] = make_float2(bar, bai);
+            }
         }
     }
 }
