@@ -73,7 +73,9 @@ void defmm_tree_free(defmm_tree* t);
  *   -1 absent) and blocks [grp_ptr[g], grp_ptr[g+1]); block k = (source parent)
  *   holds spectra blk_src[8k+b] (-1 absent), derived symbols blk_trans[27k+d]
  *   for child offset d = (a-b)+(1,1,1) in base 3, and blk_mask[k] with bit 8a+b
- *   set for every M2L event (a, b).  lhat[row] = sum D (*) hat  (stride
+ *   set for every M2L event (a, b); blk_kind[k] (or NULL = all general) = -1 for a
+ *   general block, 2p+v for a PLANAR block whose pairs all have a_p = b_p = v
+ *   (surface data: 4x4 in-plane pairs, no predicated-off pair).  lhat[row] = sum D (*) hat  (stride
  *   defmm_spectrum_stride);  then K8 f2l_rows: local[row_slot[r]] = F2L(lhat[r]).
  * K5 L2L -- traversal.py:355-391 in gather form.
  *   for i < n: local[out_slot[i]] += sum_{e in [ptr[i], ptr[i+1])}
@@ -117,8 +119,8 @@ void defmm_tree_free(defmm_tree* t);
     int defmm_m2l_blocked_##SUFFIX(int32_t L, int64_t ngroups, const int64_t* grp_ptr,           \
                                    const int64_t* grp_rows, const int32_t* blk_src,             \
                                    const int32_t* blk_trans, const int64_t* blk_mask,           \
-                                   const void* hat, const void* sym_derived, void* lhat,        \
-                                   void* stream);                                               \
+                                   const int8_t* blk_kind, const void* hat,                     \
+                                   const void* sym_derived, void* lhat, void* stream);          \
     int defmm_f2l_rows_##SUFFIX(int32_t L, int64_t nrows, const int64_t* row_slot,               \
                                 const void* lhat, void* local, void* stream);                   \
     int defmm_l2l_##SUFFIX(int32_t L, int64_t n, const int64_t* out_slot, const int8_t* octant,  \

@@ -738,10 +738,6 @@ struct Vec2<double> {
     static constexpr int W = 1;
 };
 
-__device__ __forceinline__ void vfma(float2 (&acc)[2], const float4& d, const float4& s) {
-    acc[0] = cfma(make_float2(d.x, d.y), make_float2(s.x, s.y), acc[0]);
-    acc[1] = cfma(make_float2(d.z, d.w), make_float2(s.z, s.w), acc[1]);
-}
 __device__ __forceinline__ void vfma(double2 (&acc)[1], const double2& d, const double2& s) {
     acc[0] = cfma(d, s, acc[0]);
 }
@@ -749,12 +745,58 @@ __device__ __forceinline__ void vfma(float2 (&acc)[1], const float2& d, const fl
     acc[0] = cfma(d, s, acc[0]);
 }
 
+// Planar block (surface data): every pair (a, b) has a_p == b_p == v for one
+// axis p -- 4 x 4 in-plane pairs, 9 in-plane offsets: 4 spectra + 9 symbols
+// serve up to 16 events with no predicated-off pair.  i, j = in-plane child
+// index (2 bits), octant = embed(i, p, v).
+__host__ __device__ constexpr int embed2(int i, int p, int v) {
+    // in-plane bits (hi, lo) go to the two remaining axes in increasing order
+    return p == 0 ? (v << 2) | i : p == 1 ? (((i >> 1) & 1) << 2) | (v << 1) | (i & 1) : (i << 1) | v;
+}
+__host__ __device__ constexpr int delta_index3(int a, int b) {
+    return ((((a >> 2) & 1) - ((b >> 2) & 1)) + 1) * 9 + ((((a >> 1) & 1) - ((b >> 1) & 1)) + 1) * 3 +
+           (((a & 1) - (b & 1)) + 1);
+}
+
+template <int PP, int PV, typename VT, typename V, int W>
+__device__ __forceinline__ void planar_block(uint64_t mask, const int32_t* bs, const int32_t* bt, const VT* hv,
+                                             const VT* dv, int64_t NV, int jv, bool act, V (&acc)[8][W]) {
+    VT S[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int sidx = __ldg(bs + embed2(i, PP, PV));
+        S[i] = (sidx >= 0 && act) ? __ldg(hv + (int64_t)sidx * NV + jv) : VT{};
+    }
+    // in-plane offsets (du, dv) in [-1,1]^2 -> 9 symbols
+    VT D[9];
+#pragma unroll
+    for (int e = 0; e < 9; ++e) {
+        // representative pair with this in-plane offset
+        const int du = e / 3 - 1, dw = e % 3 - 1;
+        const int ia = ((du > 0) << 1) | (dw > 0), ib = ((du < 0) << 1) | (dw < 0);
+        const int d = delta_index3(embed2(ia, PP, PV), embed2(ib, PP, PV));
+        const int tidx = __ldg(bt + d);
+        D[e] = (tidx >= 0 && act) ? __ldg(dv + (int64_t)tidx * NV + jv) : VT{};
+    }
+#pragma unroll
+    for (int ia = 0; ia < 4; ++ia)
+#pragma unroll
+        for (int ib = 0; ib < 4; ++ib) {
+            const int a = embed2(ia, PP, PV), b = embed2(ib, PP, PV);
+            const int e = (((ia >> 1) & 1) - ((ib >> 1) & 1) + 1) * 3 + ((ia & 1) - (ib & 1) + 1);
+            if ((mask >> (8 * a + b)) & 1) vfma(acc[a], D[e], S[ib]);
+        }
+}
+
+#ifndef DEFMM_M2LB_MINBLOCKS
+#define DEFMM_M2LB_MINBLOCKS 2
+#endif
 template <typename R, int L>
-__global__ void __launch_bounds__(m2lb_threads<R, L>()) m2l_blocked_kernel(
+__global__ void __launch_bounds__(m2lb_threads<R, L>(), DEFMM_M2LB_MINBLOCKS) m2l_blocked_kernel(
     int64_t ngroups, const int64_t* __restrict__ grp_ptr, const int64_t* __restrict__ grp_rows,
     const int32_t* __restrict__ blk_src, const int32_t* __restrict__ blk_trans,
-    const int64_t* __restrict__ blk_mask, const cx<R>* __restrict__ hat, const cx<R>* __restrict__ symd,
-    cx<R>* __restrict__ lhat) {
+    const int64_t* __restrict__ blk_mask, const int8_t* __restrict__ blk_kind, const cx<R>* __restrict__ hat,
+    const cx<R>* __restrict__ symd, cx<R>* __restrict__ lhat) {
     using VT = typename Vec2<R>::t;
     using V = cx<R>;
     constexpr int W = Vec2<R>::W;
@@ -778,6 +820,18 @@ __global__ void __launch_bounds__(m2lb_threads<R, L>()) m2l_blocked_kernel(
             const uint64_t mask = (uint64_t)__ldg(blk_mask + blk);
             const int32_t* bs = blk_src + 8 * blk;
             const int32_t* bt = blk_trans + 27 * blk;
+            const int kind = blk_kind ? __ldg(blk_kind + blk) : -1;  // warp-uniform
+            if (kind >= 0) {
+                switch (kind) {
+                    case 0: planar_block<0, 0>(mask, bs, bt, hv, dv, NV, jv, act, acc); break;
+                    case 1: planar_block<0, 1>(mask, bs, bt, hv, dv, NV, jv, act, acc); break;
+                    case 2: planar_block<1, 0>(mask, bs, bt, hv, dv, NV, jv, act, acc); break;
+                    case 3: planar_block<1, 1>(mask, bs, bt, hv, dv, NV, jv, act, acc); break;
+                    case 4: planar_block<2, 0>(mask, bs, bt, hv, dv, NV, jv, act, acc); break;
+                    default: planar_block<2, 1>(mask, bs, bt, hv, dv, NV, jv, act, acc); break;
+                }
+                continue;
+            }
             VT S[8];
 #pragma unroll
             for (int b = 0; b < 8; ++b) {
@@ -1428,14 +1482,14 @@ int launch_m2l_rows(int32_t L, int64_t nrows, const int64_t* row_slot, const int
 
 template <typename R>
 int launch_m2l_blocked(int32_t L, int64_t ngroups, const int64_t* grp_ptr, const int64_t* grp_rows,
-                       const int32_t* blk_src, const int32_t* blk_trans, const int64_t* blk_mask, const void* hat,
-                       const void* symd, void* lhat, void* stream) {
+                       const int32_t* blk_src, const int32_t* blk_trans, const int64_t* blk_mask,
+                       const int8_t* blk_kind, const void* hat, const void* symd, void* lhat, void* stream) {
     if (ngroups == 0) return 0;
     if (!grid_ok(ngroups)) return -1;
     cudaStream_t s = (cudaStream_t)stream;
     DEFMM_DISPATCH_L(L, (m2l_blocked_kernel<R, LL><<<(unsigned)ngroups, m2lb_threads<R, LL>(), 0, s>>>(
-                            ngroups, grp_ptr, grp_rows, blk_src, blk_trans, blk_mask, (const cx<R>*)hat,
-                            (const cx<R>*)symd, (cx<R>*)lhat)));
+                            ngroups, grp_ptr, grp_rows, blk_src, blk_trans, blk_mask, blk_kind,
+                            (const cx<R>*)hat, (const cx<R>*)symd, (cx<R>*)lhat)));
     return report(cudaGetLastError(), "m2l_blocked");
 }
 
@@ -1540,8 +1594,9 @@ const char* defmm_last_error(void) { return g_last_error; }
     }                                                                                                               \
     int defmm_m2l_blocked_##SUFFIX(int32_t L, int64_t ngroups, const int64_t* grp_ptr, const int64_t* grp_rows,     \
                                    const int32_t* blk_src, const int32_t* blk_trans, const int64_t* blk_mask,     \
-                                   const void* hat, const void* sym_derived, void* lhat, void* stream) {          \
-        return launch_m2l_blocked<R>(L, ngroups, grp_ptr, grp_rows, blk_src, blk_trans, blk_mask, hat,             \
+                                   const int8_t* blk_kind, const void* hat, const void* sym_derived, void* lhat,  \
+                                   void* stream) {                                                                \
+        return launch_m2l_blocked<R>(L, ngroups, grp_ptr, grp_rows, blk_src, blk_trans, blk_mask, blk_kind, hat,   \
                                      sym_derived, lhat, stream);                                                  \
     }                                                                                                               \
     int defmm_f2l_rows_##SUFFIX(int32_t L, int64_t nrows, const int64_t* row_slot, const void* lhat, void* local,   \

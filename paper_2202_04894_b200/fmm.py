@@ -176,6 +176,7 @@ class FmmPlan:
         self.blk_src = _dev(h["blk_src"].reshape(-1), i32, d)
         self.blk_trans = _dev(h["blk_trans"].reshape(-1), i32, d)
         self.blk_mask = _dev(h["blk_mask"], i64, d)
+        self.blk_kind = _dev(h["blk_kind"], torch.int8, d)
         # downward
         self.l2l = []
         for lev, outs, octant, ptr, src, sdir in h["l2l"]:
@@ -269,6 +270,7 @@ class FmmPlan:
         h["bk_rows"] = dense_rows
         h["grp_ptr"], h["grp_rows"] = gptr, gid[gkeep]
         h["blk_src"], h["blk_trans"], h["blk_mask"] = h["blk_src"][bsel], h["blk_trans"][bsel], h["blk_mask"][bsel]
+        h["blk_kind"] = h["blk_kind"][bsel]
         self.dense_levels = sorted(dense)
         return h
 
@@ -292,7 +294,7 @@ class FmmPlan:
         }
         # blocked M2L: group rows as indices into h["rows"] (lhat rows)
         blk = {"grp_ptr": p.blk_group_ptr, "grp_rows": p.blk_group_rows, "blk_src": p.blk_src,
-               "blk_trans": p.blk_trans, "blk_mask": p.blk_mask}
+               "blk_trans": p.blk_trans, "blk_mask": p.blk_mask, "blk_kind": p.blk_kind}
         if sh is None:
             h.update(blk)
             h["grp_rows"] = _rows_to_ids(blk["grp_rows"], h["rows"])
@@ -312,7 +314,7 @@ class FmmPlan:
         _, gptr, bsel = _sub_csr(p.blk_group_ptr, gkeep)
         bsrc = p.blk_src[bsel]
         h.update({"grp_ptr": gptr, "grp_rows": gr[gkeep], "blk_trans": p.blk_trans[bsel],
-                  "blk_mask": p.blk_mask[bsel],
+                  "blk_mask": p.blk_mask[bsel], "blk_kind": p.blk_kind[bsel],
                   "blk_src": np.where(bsrc >= 0, remap[np.maximum(bsrc, 0)], -1).astype(np.int32)})
         l2l = []
         for (lev, outs, octant, lptr, src, sdir), k in zip(p.l2l_levels, sh.l2l_keep):
@@ -423,7 +425,7 @@ class FmmPlan:
             _lib.call(self._op("m2l_rows"), L, self.rk_rows.shape[0], self.rk_rows, self.rk_ptr, self.rk_ent,
                       self.hat, self.sym_derived, self.local, sh)
             _lib.call(self._op("m2l_blocked"), L, self.n_groups, self.grp_ptr, self.grp_rows, self.blk_src,
-                      self.blk_trans, self.blk_mask, self.hat, self.sym_derived, self.lhat, sh)
+                      self.blk_trans, self.blk_mask, self.blk_kind, self.hat, self.sym_derived, self.lhat, sh)
             _lib.call(self._op("f2l_rows"), L, self.bk_rows.shape[0], self.bk_rows, self.lhat, self.local, sh)
         elif self.m2l_variant == "derived":
             _lib.call(self._op("m2l_rows"), L, self.row_slot.shape[0], self.row_slot, self.row_ptr,

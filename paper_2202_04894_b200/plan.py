@@ -159,6 +159,7 @@ class Plan:
     blk_src: np.ndarray = None  # (nblocks, 8) spectrum index per source child, -1 absent
     blk_trans: np.ndarray = None  # (nblocks, 27) derived symbol per child offset, -1 unused
     blk_mask: np.ndarray = None  # (nblocks,) int64: bit 8a+b = (a, b) is an M2L event
+    blk_kind: np.ndarray = None  # (nblocks,) int8: -1 general, 2p+v planar
     # event logs (optional, for the events= API)
     m2l_events: tuple = None
     p2p_events: tuple = None
@@ -467,6 +468,7 @@ def _m2l_blocks(plan, tt, st, mt, ms, mlev, key, src_hat, trans, tslot):
         plan.blk_src = np.zeros((0, 8), np.int32)
         plan.blk_trans = np.zeros((0, 27), np.int32)
         plan.blk_mask = np.zeros(0, np.int64)
+        plan.blk_kind = np.zeros(0, np.int8)
         return
     P, a = _octant(tt, mt)
     Q, b = _octant(st, ms)
@@ -501,6 +503,33 @@ def _m2l_blocks(plan, tt, st, mt, ms, mlev, key, src_hat, trans, tslot):
     plan.blk_group_rows = rows
     plan.blk_group_ptr = np.searchsorted(blk_g, np.arange(ng + 1)).astype(np.int64)
     plan.blk_src, plan.blk_trans, plan.blk_mask = src, tr, mask
+    plan.blk_kind = planar_kind(mask)
+
+
+def _planar_masks():
+    """allowed[2p+v]: pair bits 8a+b with a_p == b_p == v."""
+    out = []
+    for p in range(3):
+        for v in range(2):
+            m = 0
+            for a in range(8):
+                for b in range(8):
+                    if ((a >> (2 - p)) & 1) == v and ((b >> (2 - p)) & 1) == v:
+                        m |= 1 << (8 * a + b)
+            out.append(np.uint64(m))
+    return out
+
+
+_PLANAR = _planar_masks()
+
+
+def planar_kind(mask: np.ndarray) -> np.ndarray:
+    """-1 for a general block, 2p+v when every pair lies in the plane a_p = b_p = v."""
+    m = np.asarray(mask).view(np.uint64)
+    kind = np.full(m.shape[0], -1, np.int8)
+    for k in range(5, -1, -1):
+        kind[(m & ~_PLANAR[k]) == 0] = k
+    return kind
 
 
 def p2p_work_items(ptr, run_len, nt, max_pairs: int = P2P_ITEM_PAIRS) -> dict:

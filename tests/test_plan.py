@@ -229,3 +229,13 @@ def test_m2l_blocks_reconstruct_the_event_list(case):
         for e in range(pl.m2l_row_ptr[r], pl.m2l_row_ptr[r + 1]):
             ref.append((int(pl.m2l_row_slot[r]), int(pl.m2l_rows_entries[e, 0]), int(pl.m2l_rows_entries[e, 1])))
     assert sorted(rows_ev) == sorted(ref)
+    # planar classification: every pair of a planar block lies in its plane
+    for bi, k in enumerate(pl.blk_kind):
+        if k < 0:
+            continue
+        p_, v = divmod(int(k), 2)
+        m = int(pl.blk_mask[bi]) & ((1 << 64) - 1)
+        for bit in range(64):
+            if (m >> bit) & 1:
+                a, b = divmod(bit, 8)
+                assert ((a >> (2 - p_)) & 1) == v and ((b >> (2 - p_)) & 1) == v
