@@ -130,6 +130,23 @@ def two_tree_cases():
         print(name, info.counts, "hf_max", info.hf_max_level)
 
 
+def harness_cases():
+    """Reference generators (distributions.py) and one harness record."""
+    from helmfmm.harness import ExperimentConfig, run_experiment
+
+    out = {}
+    for kind in ("uniform-cube", "sphere", "refined-cube", "ellipse"):
+        out[f"dist_{kind}"] = generate_distribution(Distribution(kind, 257, 3))
+    out["charges_257_4"] = random_charges(257, 4)
+    cfg = ExperimentConfig(distribution="refined-cube", n=1500, kappa_d=12.0, order=4, ncrit=32,
+                           check_error=60, seed=1)
+    rec = run_experiment(cfg)
+    out["record"] = json.dumps(rec.to_json_dict())
+    out["record_pot"] = rec.potentials
+    np.savez_compressed(os.path.join(HERE, "harness.npz"), **out)
+    print("harness", rec.counts, rec.errors)
+
+
 def fmm_cases():
     for name, pts, q, kw in _cases():
         cfg = FmmConfig(**kw)
@@ -208,7 +225,10 @@ if __name__ == "__main__":
 
     if "--two-tree-only" in _sys.argv:
         two_tree_cases()
+    elif "--harness-only" in _sys.argv:
+        harness_cases()
     else:
         operators()
         fmm_cases()
         two_tree_cases()
+        harness_cases()
