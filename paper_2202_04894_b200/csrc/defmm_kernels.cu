@@ -157,9 +157,11 @@ template <int L, typename R>
 __device__ __forceinline__ void make_factor_tables(R* A) {
     for (int t = threadIdx.x; t < 2 * L * L; t += blockDim.x) {
         const int bit = t / (L * L), k = (t / L) % L, j = t % L;
-        double S[L];
-        lagrange<L, double>(((double)bit + node<L, double>(j)) / 2.0, S);
-        A[t] = (R)S[k];
+        const double x = ((double)bit + node<L, double>(j)) / 2.0;
+        double v = 1.0;  // S_k(x), evaluated directly (no runtime-indexed local array)
+        for (int m = 0; m < L; ++m)
+            if (m != k) v = v * (x - node<L, double>(m)) / (node<L, double>(k) - node<L, double>(m));
+        A[t] = (R)v;
     }
 }
 
@@ -170,6 +172,21 @@ __device__ __forceinline__ void make_twiddles(V* tw) {
         double s, c;
         sincospi(2.0 * (double)k / (double)P, &s, &c);
         tw[k] = from_d<V>(make_double2(c, -s));
+    }
+}
+
+// twm[f * L + x] = e^{-2 pi i (f x mod P) / P}, f < P, x < L: the pruned DFT
+// factors, so the inner loops index without a modulo (M2F was ALU-bound on it)
+// e^{-2 pi i k / P} for every P = 2L-1 (L = 2..8), filled once by the
+// launchers (cudaMemcpyToSymbol); kernels build their P x L matrix from it
+__constant__ double2 c_tw[8][15];
+
+template <int L, typename V>
+__device__ __forceinline__ void make_twiddle_matrix(V* twm) {
+    constexpr int P = 2 * L - 1;
+    for (int t = threadIdx.x; t < P * L; t += blockDim.x) {
+        const int f = t / L, x = t - (t / L) * L;
+        twm[t] = from_d<V>(c_tw[L - 1][(f * x) % P]);
     }
 }
 
@@ -296,9 +313,11 @@ __global__ void __launch_bounds__(32 * NODAL_WARPS) m2m_kernel(
     V acc[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) acc[e] = cz<V>();
+    // runtime son loop (measured faster than unrolling the octants or
+    // prefetching all son expansions: code size / registers)
     for (int o = 0; o < 8; ++o) {
         const int64_t ss = son_slot[8 * i + o];
-        if (ss < 0) continue;
+        if (ss < 0) continue;  // warp-uniform
         const int b0 = (o >> 2) & 1, b1 = (o >> 1) & 1, b2 = o & 1;
         __syncwarp();
 #pragma unroll
@@ -306,10 +325,11 @@ __global__ void __launch_bounds__(32 * NODAL_WARPS) m2m_kernel(
             const int r = lane + 32 * e;
             if (r < L3) {
                 const int j0 = r / (L * L), j1 = (r / L) % L, j2 = r % L;
+                const V m = mult[ss * L3 + r];
                 // son-side phase e^{-i th (bit + x_j)} (conj plane wave on the son grid)
                 const R ph = -(ku[0] * (b0 + node<L, R>(j0)) + ku[1] * (b1 + node<L, R>(j1)) +
                                ku[2] * (b2 + node<L, R>(j2)));
-                X[r] = d >= 0 ? cmul(mult[ss * L3 + r], cexpi(ph)) : mult[ss * L3 + r];
+                X[r] = d >= 0 ? cmul(m, cexpi(ph)) : m;
             }
         }
         __syncwarp();
@@ -371,9 +391,26 @@ __global__ void __launch_bounds__(32 * NODAL_WARPS) l2l_kernel(
         const int r = lane + 32 * e;
         acc[e] = r < L3 ? local[ob + r] : cz<V>();
     }
-    for (int64_t s = ptr[i]; s < ptr[i + 1]; ++s) {
+    const int64_t s0 = ptr[i], s1 = ptr[i + 1];
+    V nxt[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int r = lane + 32 * e;
+        nxt[e] = (s0 < s1 && r < L3) ? local[src_slot[s0] * L3 + r] : cz<V>();
+    }
+    for (int64_t s = s0; s < s1; ++s) {
         const int d = src_dir[s];
-        const int64_t sb = src_slot[s] * L3;
+        V cur[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) cur[e] = nxt[e];
+        if (s + 1 < s1) {  // next source in flight during this one's transform
+            const int64_t nb = src_slot[s + 1] * L3;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int r = lane + 32 * e;
+                if (r < L3) nxt[e] = local[nb + r];
+            }
+        }
         R ku[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) ku[k] = (R)(d >= 0 ? kappa * son_beta * dirs[3 * d + k] : 0.0);
@@ -385,7 +422,7 @@ __global__ void __launch_bounds__(32 * NODAL_WARPS) l2l_kernel(
                 const int k0 = r / (L * L), k1 = (r / L) % L, k2 = r % L;
                 // father-side phase e^{-i th 2 x_k} (conj plane wave on the father grid)
                 const R ph = -2 * (ku[0] * node<L, R>(k0) + ku[1] * node<L, R>(k1) + ku[2] * node<L, R>(k2));
-                X[r] = d >= 0 ? cmul(local[sb + r], cexpi(ph)) : local[sb + r];
+                X[r] = d >= 0 ? cmul(cur[e], cexpi(ph)) : cur[e];
             }
         }
         __syncwarp();
@@ -435,13 +472,13 @@ __global__ void __launch_bounds__(32 * M2F_WARPS) m2f_kernel(int64_t n, const in
     constexpr int P = pad<L>(), L3 = cube<L>(), P3 = P * P * P;
     constexpr int WS = L3 + L * L * P + L * P * P;
     extern __shared__ unsigned char smraw[];
-    V* tw = reinterpret_cast<V*>(smraw);
-    make_twiddles<P, V>(tw);
+    V* tw = reinterpret_cast<V*>(smraw);  // twiddle matrix P x L
+    make_twiddle_matrix<L, V>(tw);
     __syncthreads();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t i = (int64_t)blockIdx.x * M2F_WARPS + w;
     if (i >= n) return;
-    V* X = tw + P + w * WS;  // L^3
+    V* X = tw + P * L + w * WS;  // L^3
     V* Y1 = X + L3;          // [a][b][f2]
     V* Y2 = Y1 + L * L * P;  // [a][f1][f2]
     const int64_t s = src_slot[i] * L3;
@@ -451,7 +488,7 @@ __global__ void __launch_bounds__(32 * M2F_WARPS) m2f_kernel(int64_t n, const in
         const int ab = t / P, f2 = t % P;
         V v = cz<V>();
 #pragma unroll
-        for (int c = 0; c < L; ++c) v = cfma(X[ab * L + c], tw[(f2 * c) % P], v);
+        for (int c = 0; c < L; ++c) v = cfma(X[ab * L + c], tw[f2 * L + c], v);
         Y1[t] = v;
     }
     __syncwarp();
@@ -459,7 +496,7 @@ __global__ void __launch_bounds__(32 * M2F_WARPS) m2f_kernel(int64_t n, const in
         const int a = t / (P * P), f1 = (t / P) % P, f2 = t % P;
         V v = cz<V>();
 #pragma unroll
-        for (int b = 0; b < L; ++b) v = cfma(Y1[(a * L + b) * P + f2], tw[(f1 * b) % P], v);
+        for (int b = 0; b < L; ++b) v = cfma(Y1[(a * L + b) * P + f2], tw[f1 * L + b], v);
         Y2[t] = v;
     }
     __syncwarp();
@@ -471,7 +508,7 @@ __global__ void __launch_bounds__(32 * M2F_WARPS) m2f_kernel(int64_t n, const in
         V v = cz<V>();
         if (t < P3) {
 #pragma unroll
-            for (int a = 0; a < L; ++a) v = cfma(Y2[a * P * P + f12], tw[(f0 * a) % P], v);
+            for (int a = 0; a < L; ++a) v = cfma(Y2[a * P * P + f12], tw[f0 * L + a], v);
         }
         out[t] = cscale(v, scale);  // the pad entry (c64) is written as 0
     }
@@ -582,7 +619,8 @@ __host__ __device__ constexpr int m2l_block() {
 }
 
 // pruned inverse DFT of one accumulated spectrum X (P^3, smem) into an L^3
-// nodal vector (fourier.py:74-80): contract f0 -> a, f1 -> b, f2 -> c.
+// nodal vector (fourier.py:74-80): contract f0 -> a, f1 -> b, f2 -> c;
+// tw = the P x L twiddle matrix (make_twiddle_matrix), conjugated here.
 template <int L, typename V>
 __device__ __forceinline__ void f2l_row(const V* tw, V* X, V* Z1, V* out, int nt) {
     constexpr int P = pad<L>(), L3 = cube<L>();
@@ -590,7 +628,7 @@ __device__ __forceinline__ void f2l_row(const V* tw, V* X, V* Z1, V* out, int nt
         const int a = t / (P * P), f12 = t % (P * P);
         V v = cz<V>();
 #pragma unroll
-        for (int f0 = 0; f0 < P; ++f0) v = cfma(X[f0 * P * P + f12], cconj(tw[(f0 * a) % P]), v);
+        for (int f0 = 0; f0 < P; ++f0) v = cfma(X[f0 * P * P + f12], cconj(tw[f0 * L + a]), v);
         Z1[t] = v;
     }
     __syncthreads();
@@ -598,7 +636,7 @@ __device__ __forceinline__ void f2l_row(const V* tw, V* X, V* Z1, V* out, int nt
         const int a = t / (L * P), b = (t / P) % L, f2 = t % P;
         V v = cz<V>();
 #pragma unroll
-        for (int f1 = 0; f1 < P; ++f1) v = cfma(Z1[(a * P + f1) * P + f2], cconj(tw[(f1 * b) % P]), v);
+        for (int f1 = 0; f1 < P; ++f1) v = cfma(Z1[(a * P + f1) * P + f2], cconj(tw[f1 * L + b]), v);
         X[t] = v;
     }
     __syncthreads();
@@ -607,7 +645,7 @@ __device__ __forceinline__ void f2l_row(const V* tw, V* X, V* Z1, V* out, int nt
         const int ab = t / L, c = t % L;
         V v = cz<V>();
 #pragma unroll
-        for (int f2 = 0; f2 < P; ++f2) v = cfma(X[ab * P + f2], cconj(tw[(f2 * c) % P]), v);
+        for (int f2 = 0; f2 < P; ++f2) v = cfma(X[ab * P + f2], cconj(tw[f2 * L + c]), v);
         out[t] = cscale(v, scale);
     }
 }
@@ -628,11 +666,11 @@ __global__ void __launch_bounds__(m2l_block<R, L>()) m2l_rows_kernel(
     constexpr int PER = (SS / W + NT - 1) / NT;
     extern __shared__ unsigned char smraw[];
     double2* tw = reinterpret_cast<double2*>(smraw);
-    double2* X = tw + P;
+    double2* X = tw + P * L;
     double2* Z1 = X + P3 + 1;
     double2* O = Z1 + L * P * P;
     const int64_t row = blockIdx.x;
-    make_twiddles<P, double2>(tw);
+    make_twiddle_matrix<L, double2>(tw);
     // two independent entries in flight per iteration (4 was measured slower:
     // registers -> occupancy).  Products and the two partial sums are formed in
     // the storage precision (c64: FP32 -- converting every operand to FP64 made
@@ -878,11 +916,11 @@ __global__ void __launch_bounds__(128) f2l_rows_kernel(int64_t nrows, const int6
     constexpr int SS = spec_stride<R, L>();
     extern __shared__ unsigned char smraw[];
     double2* tw = reinterpret_cast<double2*>(smraw);
-    double2* X = tw + P;
+    double2* X = tw + P * L;
     double2* Z1 = X + P3 + 1;
     double2* O = Z1 + L * P * P;
     const int64_t r = blockIdx.x;
-    make_twiddles<P, double2>(tw);
+    make_twiddle_matrix<L, double2>(tw);
     const cx<R>* src = lhat + r * SS;
     for (int j = threadIdx.x; j < P3; j += blockDim.x) X[j] = to_d(src[j]);
     __syncthreads();
@@ -905,10 +943,10 @@ __global__ void __launch_bounds__(m2l_threads<L>()) m2l_canon_kernel(
     constexpr int PER = (P3 + NT - 1) / NT;
     extern __shared__ unsigned char smraw[];
     double2* tw = reinterpret_cast<double2*>(smraw);
-    double2* X = tw + P;
+    double2* X = tw + P * L;
     double2* Z1 = X + P3;
     const int64_t row = blockIdx.x;
-    make_twiddles<P, double2>(tw);
+    make_twiddle_matrix<L, double2>(tw);
     double2 acc[PER];
 #pragma unroll
     for (int m = 0; m < PER; ++m) acc[m] = make_double2(0.0, 0.0);
@@ -1350,6 +1388,23 @@ __global__ void direct_reduce(int64_t nt, int nsplit, const double2* __restrict_
 // ---------------------------------------------------------------------------
 // launch helpers
 
+// fill c_tw once per process (before the first launch that needs it)
+int ensure_twiddles() {
+    static bool done = false;
+    if (done) return 0;
+    double2 h[8][15] = {};
+    for (int L = 2; L <= 8; ++L) {
+        const int P = 2 * L - 1;
+        for (int k = 0; k < P; ++k) {
+            const double a = 2.0 * 3.14159265358979323846 * (double)k / (double)P;
+            h[L - 1][k] = make_double2(cos(a), -sin(a));
+        }
+    }
+    const int rc = report(cudaMemcpyToSymbol(c_tw, h, sizeof(h)), "cudaMemcpyToSymbol(c_tw)");
+    if (rc == 0) done = true;
+    return rc;
+}
+
 template <typename K>
 int set_smem(K kernel, size_t bytes) {
     if (bytes <= 48 * 1024) return 0;
@@ -1423,10 +1478,11 @@ template <typename R>
 int launch_m2f(int32_t L, int64_t n, const int64_t* src_slot, const void* mult, void* hat, void* stream) {
     if (n == 0) return 0;
     if (!grid_ok(n)) return -1;
+    if (int rc0 = ensure_twiddles()) return rc0;
     cudaStream_t s = (cudaStream_t)stream;
     DEFMM_DISPATCH_L(L, {
         constexpr int P = 2 * LL - 1;
-        const size_t bytes = sizeof(cx<R>) * (P + M2F_WARPS * (LL * LL * LL + LL * LL * P + LL * P * P));
+        const size_t bytes = sizeof(cx<R>) * (P * LL + M2F_WARPS * (LL * LL * LL + LL * LL * P + LL * P * P));
         int rc = set_smem(m2f_kernel<R, LL>, bytes);
         if (rc) return rc;
         m2f_kernel<R, LL><<<blocks_of(n, M2F_WARPS), 32 * M2F_WARPS, bytes, s>>>(n, src_slot, (const cx<R>*)mult,
@@ -1467,10 +1523,11 @@ int launch_m2l_rows(int32_t L, int64_t nrows, const int64_t* row_slot, const int
                     const int32_t* entries, const void* hat, const void* symd, void* local, void* stream) {
     if (nrows == 0) return 0;
     if (!grid_ok(nrows)) return -1;
+    if (int rc0 = ensure_twiddles()) return rc0;
     cudaStream_t s = (cudaStream_t)stream;
     DEFMM_DISPATCH_L(L, {
         constexpr int P = 2 * LL - 1;
-        const size_t bytes = sizeof(double2) * (P + P * P * P + 1 + LL * P * P + LL * LL * LL);
+        const size_t bytes = sizeof(double2) * (P * LL + P * P * P + 1 + LL * P * P + LL * LL * LL);
         int rc = set_smem(m2l_rows_kernel<R, LL>, bytes);
         if (rc) return rc;
         m2l_rows_kernel<R, LL><<<(unsigned)nrows, m2l_block<R, LL>(), bytes, s>>>(
@@ -1498,10 +1555,11 @@ int launch_f2l_rows(int32_t L, int64_t nrows, const int64_t* row_slot, const voi
                     void* stream) {
     if (nrows == 0) return 0;
     if (!grid_ok(nrows)) return -1;
+    if (int rc0 = ensure_twiddles()) return rc0;
     cudaStream_t s = (cudaStream_t)stream;
     DEFMM_DISPATCH_L(L, {
         constexpr int P = 2 * LL - 1;
-        const size_t bytes = sizeof(double2) * (P + P * P * P + 1 + LL * P * P + LL * LL * LL);
+        const size_t bytes = sizeof(double2) * (P * LL + P * P * P + 1 + LL * P * P + LL * LL * LL);
         int rc = set_smem(f2l_rows_kernel<R, LL>, bytes);
         if (rc) return rc;
         f2l_rows_kernel<R, LL><<<(unsigned)nrows, 128, bytes, s>>>(nrows, row_slot, (const cx<R>*)lhat,
@@ -1638,10 +1696,11 @@ int defmm_m2l_canon_c128(int32_t L, int64_t nrows, const int64_t* row_slot, cons
                          const void* sym, void* local, void* stream) {
     if (nrows == 0) return 0;
     if (!grid_ok(nrows)) return -1;
+    if (int rc0 = ensure_twiddles()) return rc0;
     cudaStream_t s = (cudaStream_t)stream;
     DEFMM_DISPATCH_L(L, {
         constexpr int P = 2 * LL - 1;
-        const size_t bytes = sizeof(double2) * (P + P * P * P + LL * P * P);
+        const size_t bytes = sizeof(double2) * (P * LL + P * P * P + LL * P * P);
         int rc = set_smem(m2l_canon_kernel<LL>, bytes);
         if (rc) return rc;
         m2l_canon_kernel<LL><<<(unsigned)nrows, m2l_threads<LL>(), bytes, s>>>(
