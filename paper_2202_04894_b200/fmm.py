@@ -455,6 +455,30 @@ class FmmPlan:
             stage_events.append(("downward", c, e))
         return out
 
+    def capture_graph(self):
+        """Record one matvec (all launches on both streams, the memsets) into a
+        CUDA graph; ``replay()`` then re-executes it with whatever charges are
+        in ``self.q``.  Not for sharded plans (the NCCL all-reduce stays eager)."""
+        if self.shard is not None:
+            raise ValueError("CUDA-graph replay is for single-GPU plans")
+        torch.cuda.synchronize(self.device)
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            self.apply()  # warm-up on the capture stream
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        torch.cuda.synchronize(self.device)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.apply()
+        torch.cuda.synchronize(self.device)
+        return self.graph
+
+    def replay(self):
+        """Matvec via the captured CUDA graph; returns ``self.out``."""
+        self.graph.replay()
+        return self.out
+
     @property
     def launches_per_apply(self) -> int:
         return 5 + len(self.m2m) + len(self.l2l) + (1 if self.n_split else 0) + 2 * (self.m2l_variant == "hybrid")

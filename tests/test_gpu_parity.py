@@ -262,3 +262,17 @@ def test_virtual_ranks_match_single_gpu(case, world):
     out = sum(r.apply_rest().clone() for r in ranks)
     assert _rel(out.cpu().numpy(), ref.cpu().numpy()) <= 1e-13
     assert _rel(out.cpu().numpy(), g["pot"]) <= FP64_TOL
+
+
+def test_cuda_graph_replay_matches_eager():
+    from paper_2202_04894_b200 import FmmConfig, FmmPlan
+
+    g = load_case("cubesurf4000")
+    plan = FmmPlan(g["points"], None, FmmConfig(**g["config"]), charges=g["charges"])
+    a = plan.apply().clone()
+    plan.capture_graph()
+    b = plan.replay().clone()
+    assert torch.equal(a, b)
+    plan.set_charges(2 * g["charges"])  # replay picks up new charges
+    c = plan.replay().clone()
+    assert _rel(c.cpu().numpy(), 2 * a.cpu().numpy()) <= 1e-14
