@@ -42,6 +42,51 @@ int defmm_tree_fetch(const defmm_tree* t, int64_t* perm, double* sorted_pts, int
                      int64_t* coords, int64_t* start, int64_t* stop, int64_t* parent);
 void defmm_tree_free(defmm_tree* t);
 
+/* ---- host: dual tree traversal (plan lists) ------------------------------
+ * Replaces the reference's recursive DTT (traversal.py:320-348, whose HF pair
+ * set equals blank_dtt traversal.py:182-200) for one (target, source) tree
+ * pair on a common grid.  Trees are level-major arrays (HOST memory):
+ * level_off[depth+2], coords[ncell*3], first_son, n_sons, parent.  Per level l:
+ * M2L iff gap^2 >= g2min[l] (the reference MAC, traversal.py:100-113, as an
+ * exact integer threshold); key = key_tab[tab_off[l] + dense(t_vec)] with
+ * dense(t) = ((t0+R)(2R+1) + t1+R)(2R+1) + t2+R over |t|_inf <= R[l]
+ * (nearest direction, directions.py:78-89; -1 at LF levels); P2P iff either
+ * cell is a leaf (traversal.py:336-343); else recurse into sons x sons.
+ * Returns -4 when a translation falls outside its level's key table. */
+typedef struct defmm_dtt defmm_dtt;
+int defmm_dtt_build(const int64_t* t_level_off, int32_t t_depth, const int64_t* t_coords,
+                    const int64_t* t_first_son, const int64_t* t_nsons, const int64_t* t_parent,
+                    const int64_t* s_level_off, int32_t s_depth, const int64_t* s_coords,
+                    const int64_t* s_first_son, const int64_t* s_nsons, const int64_t* s_parent,
+                    int32_t depth, const int64_t* g2min, const int32_t* R, const int64_t* tab_off,
+                    const int32_t* key_tab, defmm_dtt** out);
+/* sizes[6] = {M2L events, rows, groups, blocks, P2P events, translations} */
+int defmm_dtt_sizes(const defmm_dtt* d, int64_t* sizes);
+/* rows = distinct (target, key) in (level, target, key) order, row_ptr[rows+1]
+ * over the events (ev_s source cell, ev_trans translation id); groups =
+ * (level, key, target parent) with grp_rows[8*g + octant] = row id or -1 and
+ * grp_ptr[groups+1] over the blocks; block = (group, source parent) with
+ * blk_src[8*b + octant] = event id or -1, blk_trans[27*b + child offset] =
+ * translation id or -1, blk_mask bit 8a+b = pair (a, b) is an event.
+ * Translation ids (ev_trans, blk_trans) rank the distinct (level, t_vec) in
+ * dense-table order; defmm_dtt_translations lists their dense indices.
+ * P2P events (p_t, p_s).  Any pointer may be NULL (not copied). */
+int defmm_dtt_fetch(const defmm_dtt* d, int32_t* ev_s, int32_t* ev_trans, int64_t* row_ptr,
+                    int32_t* row_t, int32_t* row_key, int32_t* row_lev, int64_t* grp_rows,
+                    int32_t* grp_p, int32_t* grp_key, int32_t* grp_lev, int64_t* grp_ptr,
+                    int64_t* blk_src, int32_t* blk_trans, int64_t* blk_mask, int32_t* p_t,
+                    int32_t* p_s);
+int defmm_dtt_translations(const defmm_dtt* d, int64_t* dense_ids);
+/* Spectrum index of every M2L event's source expansion (the M2F list,
+ * fourier.py:67-72 applied once per used multipole): slot = m_dense[base[l] +
+ * (ev_s - s_level_off[l]) * nd[l] + loc], loc = row key - key_base[l] (0 at LF
+ * levels); hat_slot[0..*n_hat) = the used slots ascending (capacity n_mult),
+ * src_hat[event] = rank of its slot.  -6 if an event has no source expansion. */
+int defmm_dtt_source_hats(const defmm_dtt* d, const int64_t* m_dense, const int64_t* base, const int64_t* nd,
+                          const int64_t* s_level_off, const int32_t* key_base, int64_t n_mult,
+                          int32_t* src_hat, int64_t* hat_slot, int64_t* n_hat);
+void defmm_dtt_free(defmm_dtt* d);
+
 /* ---- device operators ------------------------------------------------------
  * Every operator exists as *_c128 (complex arrays are double2 = interleaved
  * FP64 re/im, exactly the reference's complex128) and *_c64 (float2; phases,

@@ -23,6 +23,12 @@ _SIGS = {
     "defmm_tree_ncells": [_vp],
     "defmm_tree_fetch": [_vp] + [_vp] * 7,
     "defmm_tree_free": [_vp],
+    "defmm_dtt_build": [_vp, _i32] + [_vp] * 4 + [_vp, _i32] + [_vp] * 4 + [_i32] + [_vp] * 5,
+    "defmm_dtt_sizes": [_vp, _vp],
+    "defmm_dtt_fetch": [_vp] * 17,
+    "defmm_dtt_translations": [_vp, _vp],
+    "defmm_dtt_source_hats": [_vp] * 6 + [_i64, _vp, _vp, _vp],
+    "defmm_dtt_free": [_vp],
     "defmm_m2l_canon_c128": [_i32, _i64] + [_vp] * 9,
     "defmm_direct_workspace_bytes": [_i64],
     "defmm_spectrum_stride": [_i32, _i32],
@@ -70,6 +76,7 @@ def load():
     lib.defmm_tree_ncells.restype = _i64
     lib.defmm_direct_workspace_bytes.restype = _i64
     lib.defmm_tree_free.restype = None
+    lib.defmm_dtt_free.restype = None
     lib.defmm_last_error.restype = C.c_char_p
     _lib = lib
     return lib

@@ -21,7 +21,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CU_SOURCES = ["defmm_kernels.cu"]
-CPP_SOURCES = ["tree_build.cpp"]
+CPP_SOURCES = ["tree_build.cpp", "dtt_build.cpp"]
 
 
 def _run(cmd):
@@ -54,10 +54,10 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
         if force or _stale(o, [s, header]):
-            _run(["g++", "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-c", s, "-o", o])
+            _run(["g++", "-O2", "-std=c++17", "-fPIC", "-pthread", "-ffp-contract=off", "-c", s, "-o", o])
         objs.append(o)
     if force or _stale(LIB, objs):
-        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"])
+        _run([NVCC, *ARCH, "-shared", "-Xcompiler", "-pthread", "-o", LIB, *objs, "-lcudart"])
     return LIB
 
 

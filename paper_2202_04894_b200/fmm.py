@@ -161,9 +161,7 @@ class FmmPlan:
         # M2L, all rows (target-major CSR): reference variants "derived" / "canonical"
         self.row_slot = _dev(h["rows"], i64, d)
         self.row_ptr = _dev(h["row_ptr"], i64, d)
-        self.e_src = _dev(h["ent"][:, 0], i32, d)
-        self.e_sym = _dev(p.m2l_sym[h["ent_sel"]], i32, d)
-        self.e_rid = _dev(p.m2l_rid[h["ent_sel"]], torch.int8, d)
+        self._ent_canon = None  # per-event (src, sym, rid) of the canonical variant, on first use
         self.row_entries = _dev(h["ent"].reshape(-1), i32, d)
         # M2L product path ("hybrid"): sparse levels -> row kernel, dense -> blocked
         self.rk_rows = _dev(h["rk_rows"], i64, d)
@@ -286,7 +284,6 @@ class FmmPlan:
             "rows": p.m2l_row_slot,
             "row_ptr": p.m2l_row_ptr,
             "ent": p.m2l_rows_entries,
-            "ent_sel": np.arange(n_ent),
             "l2l": list(p.l2l_levels),
             "leaves": np.ones(p.leaf_cells.shape[0], bool),
             "p2p_ptr": p.p2p_ptr,
@@ -302,7 +299,7 @@ class FmmPlan:
         h["p2m_idx"] = sh.p2m_idx
         h["m2m"] = [(lev, sl[k], ss[k]) for (lev, sl, ss), k in zip(p.m2m_levels, sh.m2m_keep) if k.any()]
         rows, ptr, sel = _sub_csr(p.m2l_row_ptr, sh.row_keep)
-        h["rows"], h["row_ptr"], h["ent_sel"] = p.m2l_row_slot[sh.row_keep], ptr, sel
+        h["rows"], h["row_ptr"] = p.m2l_row_slot[sh.row_keep], ptr
         hat_ids = np.nonzero(sh.hat_keep)[0]
         remap = np.full(p.n_hat, -1, np.int64)
         remap[hat_ids] = np.arange(hat_ids.shape[0])
@@ -431,8 +428,15 @@ class FmmPlan:
             _lib.call(self._op("m2l_rows"), L, self.row_slot.shape[0], self.row_slot, self.row_ptr,
                       self.row_entries, self.hat, self.sym_derived, self.local, sh)
         elif self.m2l_variant == "canonical" and self.config.dtype == "c128":
-            _lib.call("defmm_m2l_canon_c128", L, self.row_slot.shape[0], self.row_slot, self.row_ptr, self.e_src,
-                      self.e_sym, self.e_rid, self.hat, self.sym, self.local, sh)
+            if self._ent_canon is None:
+                ent = self.row_entries.view(-1, 2)
+                tid = ent[:, 1].long()
+                self._ent_canon = (ent[:, 0].contiguous(),
+                                   torch.as_tensor(self.plan.trans_canon, device=ent.device)[tid].to(torch.int32),
+                                   torch.as_tensor(self.plan.trans_rid, device=ent.device)[tid].to(torch.int8))
+            e_src, e_sym, e_rid = self._ent_canon
+            _lib.call("defmm_m2l_canon_c128", L, self.row_slot.shape[0], self.row_slot, self.row_ptr, e_src,
+                      e_sym, e_rid, self.hat, self.sym, self.local, sh)
         else:
             raise ValueError(f"unknown M2L variant {self.m2l_variant!r} for dtype {self.config.dtype}")
         if stage_events is not None:

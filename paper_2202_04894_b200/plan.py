@@ -28,11 +28,14 @@ Integer counts reproduce FmmInfo.counts exactly (traversal.py:495-505).
 
 from __future__ import annotations
 
+import ctypes as C
 import itertools
+import math
 from dataclasses import dataclass, field
 
 import numpy as np
 
+from . import _lib
 from .directions import generate_direction_tree, nearest_directions
 from .tree import SQRT3, ClusterTree
 
@@ -137,9 +140,6 @@ class Plan:
     l_dir: np.ndarray = None
     m2l_row_slot: np.ndarray = None
     m2l_row_ptr: np.ndarray = None
-    m2l_src: np.ndarray = None  # hat index
-    m2l_sym: np.ndarray = None
-    m2l_rid: np.ndarray = None
     m2l_level: np.ndarray = None  # per row
     m2l_rows_entries: np.ndarray = None  # (n_m2l, 2) int32 {hat, derived symbol} in row order
     l2l_levels: list = None  # [(son level, out_slot, octant, ptr, src_slot, src_dir)]
@@ -180,6 +180,19 @@ class Plan:
     def n_sym(self):
         return int(self.sym_tvec.shape[0])
 
+    # per-event views in row order (derived from the entries table)
+    @property
+    def m2l_src(self):  # spectrum index
+        return self.m2l_rows_entries[:, 0]
+
+    @property
+    def m2l_sym(self):  # canonical symbol id
+        return self.trans_canon[self.m2l_rows_entries[:, 1]]
+
+    @property
+    def m2l_rid(self):  # cube-group rotation id
+        return self.trans_rid[self.m2l_rows_entries[:, 1]]
+
 
 def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: float, hf_switch: float,
                keep_events: bool = False) -> Plan:
@@ -196,63 +209,34 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
     tol = 1e-12 * st.root_box.side  # traversal.py:465-467
     plan = Plan(order=order, kappa=kappa, tol=tol, hf_max=hf, same=same, dirs=dirs, dir_off=dir_off)
 
-    # ---- level-synchronous DTT (traversal.py:320-348) ----------------------
-    m2l_t, m2l_s, m2l_lev = [], [], []
-    p2p_t, p2p_s = [], []
-    T = np.zeros(1, np.int64)
-    S = np.zeros(1, np.int64)
-    for lev in range(depth + 1):
-        if T.size == 0:
-            break
-        d = tt.coords[T] - st.coords[S]
-        g = np.maximum(np.abs(d) - 1, 0)
-        g2 = (g * g).sum(axis=1)
-        mac = _mac_lut(g2, lev, lev <= hf, tt.side_at(lev), kappa, eta)
-        m2l_t.append(T[mac])
-        m2l_s.append(S[mac])
-        m2l_lev.append(np.full(int(mac.sum()), lev, np.int64))
-        rest = ~mac
-        leafy = tt.is_leaf[T] | st.is_leaf[S]
-        sel = rest & leafy
-        p2p_t.append(T[sel])
-        p2p_s.append(S[sel])
-        sel = rest & ~leafy
-        rt, rs = T[sel], S[sel]
-        T, S = _expand_pairs(tt.first_son[rt], tt.n_sons[rt], st.first_son[rs], st.n_sons[rs])
-    mt = np.concatenate(m2l_t) if m2l_t else np.zeros(0, np.int64)
-    ms = np.concatenate(m2l_s) if m2l_s else np.zeros(0, np.int64)
-    mlev = np.concatenate(m2l_lev) if m2l_lev else np.zeros(0, np.int64)
-    pt = np.concatenate(p2p_t)
-    ps = np.concatenate(p2p_s)
-    n_m2l = mt.shape[0]
+    # ---- dual tree traversal (native, traversal.py:320-348) ----------------
+    g2min, R, tab_off, key_tab = _traversal_tables(tt, depth, hf, dt, dir_off, kappa, eta)
+    nat = NativeDtt(tt, st, depth, g2min, R, tab_off, key_tab)
+    row_ptr, row_t, row_key, row_lev = nat["row_ptr"], nat["row_t"], nat["row_key"], nat["row_lev"]
+    ev_s, ev_trans = nat["ev_s"], nat["ev_trans"]
+    pt, ps = nat["p_t"].astype(np.int64), nat["p_s"].astype(np.int64)
+    n_m2l = int(ev_s.shape[0])
+    n_rows = int(row_t.shape[0])
+    row_cnt = np.diff(row_ptr)
+    # events are level-contiguous (rows are ordered (level, target, key))
+    lev_rows = np.searchsorted(row_lev, np.arange(depth + 2)).astype(np.int64)
+    lev_ev = row_ptr[lev_rows]
+    row_loc = np.where(row_key >= 0, row_key - dir_off[np.maximum(hf - row_lev, 0)], -1).astype(np.int64)
 
-    # ---- per-event translation, key, symbol --------------------------------
-    tv = tt.coords[mt] - st.coords[ms]
-    # distinct (level, t): key on a packed integer (translations are short:
-    # |t|_inf <= 3 at LF levels, bounded by the HF near field above)
-    off = int(np.abs(tv).max()) if n_m2l else 0
-    R = 2 * off + 1
-    if (depth + 1) * R**3 >= 2**62:
-        raise ValueError("translation range too large for the packed plan keys")
-    packed = ((mlev * R + (tv[:, 0] + off)) * R + (tv[:, 1] + off)) * R + (tv[:, 2] + off)
-    uniq, inv = np.unique(packed, return_inverse=True)
-    u_lev = np.empty(uniq.shape[0], np.int64)
-    u_lev[inv] = mlev
-    u_tv = np.empty((uniq.shape[0], 3), np.int64)
-    u_tv[inv] = tv
-    # key: global direction id at HF levels (traversal.py:187-190, 326-331)
-    u_dir = np.full(uniq.shape[0], -1, np.int64)
-    for lev in np.unique(u_lev):
-        if lev <= hf:
-            e = hf - int(lev)
-            sel = np.nonzero(u_lev == lev)[0]
-            u_dir[sel] = dir_off[e] + nearest_directions(dt.levels[e], u_tv[sel])
+    # ---- distinct (level, t): the used entries of the dense tables ---------
+    uniq = nat["trans_dense"]  # used dense-table entries == (level, t) lexicographic order
+    inv = ev_trans  # translation id per event
+    u_lev = np.searchsorted(tab_off, uniq, side="right") - 1
+    rel = uniq - tab_off[u_lev]
+    w = 2 * R[u_lev].astype(np.int64) + 1
+    u_tv = np.stack([rel // (w * w), (rel // w) % w, rel % w], 1) - R[u_lev].astype(np.int64)[:, None]
     # canonical symbol classes (fourier.py:233-247)
     if uniq.shape[0]:
         canon, rid = canonicalize_many(u_tv)
     else:
         canon, rid = np.zeros((0, 3), np.int64), np.zeros(0, np.int8)
-    cpack = ((u_lev * R + canon[:, 0]) * R + canon[:, 1]) * R + canon[:, 2]
+    Rc = int(canon.max()) + 1 if canon.size else 1
+    cpack = ((u_lev * Rc + canon[:, 0]) * Rc + canon[:, 1]) * Rc + canon[:, 2]
     cuniq, cinv = np.unique(cpack, return_inverse=True)
     sym_lev = np.empty(cuniq.shape[0], np.int64)
     sym_lev[cinv] = u_lev
@@ -261,21 +245,20 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
     plan.sym_tvec = sym_t.astype(np.int32)
     plan.sym_beta = np.array([tt.side_at(int(l)) for l in sym_lev], dtype=np.float64)
     _check_stencils(sym_t, sym_lev, tt, order, tol)
-    ev_dir = u_dir[inv]
-    ev_sym = cinv[inv].astype(np.int32)
-    ev_rid = rid[inv]
 
     # ---- marks (traversal.py:190-192) + downward propagation (:203-213) ---
     # mark key = cell * KD + local direction index (refinement e = hf - level)
     KD = int(dirs.shape[0]) + 1
-    hf_ev = ev_dir >= 0
-    loc_i = np.where(hf_ev, ev_dir - dir_off[np.maximum(hf - mlev, 0)], -1)
     t_marks = [[] for _ in range(depth + 1)]
     s_marks = [[] for _ in range(depth + 1)] if not same else t_marks
     for lev in range(min(hf, depth) + 1):
-        sel = hf_ev & (mlev == lev)
-        t_marks[lev].append(mt[sel] * KD + loc_i[sel])
-        s_marks[lev].append(ms[sel] * KD + loc_i[sel])
+        r0, r1 = lev_rows[lev], lev_rows[lev + 1]
+        if r1 == r0:
+            continue
+        t_marks[lev].append(row_t[r0:r1].astype(np.int64) * KD + row_loc[r0:r1])
+        loc_ev = np.repeat(row_loc[r0:r1], row_cnt[r0:r1])
+        s_marks[lev].append(_unique_cell_keys(ev_s[lev_ev[lev] : lev_ev[lev + 1]], loc_ev, st, lev,
+                                              dt.levels[hf - lev].shape[0], KD))
     marks_t = _propagate_marks(tt, t_marks, hf, dt, KD)
     marks_s = marks_t if same else _propagate_marks(st, s_marks, hf, dt, KD)
 
@@ -338,17 +321,19 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
     plan.m2m_levels = m2m_levels
 
     # ---- M2L sources -> spectra (M2F only for used multipoles) -------------
-    src_loc = np.where(hf_ev, loc_i, -1)
-    src_slot = mslot(ms, src_loc)
-    if np.any(src_slot < 0):
-        raise RuntimeError("missing source expansion: blank-pass bug")
-    hat_slot, src_hat = np.unique(src_slot, return_inverse=True)
+    nd_s, base_s = _dense_space(st, hf, dt)
+    m_dense = np.full(int(base_s[-1]), -1, np.int64)
+    m_dense[_dense_index(st, nd_s, base_s, m_cell, m_loc)] = np.arange(m_cell.shape[0])
+    key_base = np.zeros(depth + 1, np.int32)
+    for lev in range(min(hf, depth) + 1):
+        key_base[lev] = dir_off[hf - lev]
+    src_hat, hat_slot = nat.source_hats(m_dense, base_s, nd_s, st.level_offsets, key_base, m_cell.shape[0])
+    nat.close()
     plan.hat_slot = hat_slot
 
     # ---- local slots on the target tree -------------------------------------
-    tgt_key_cell = mt
-    tgt_key_loc = src_loc  # same key
-    l_cell, l_loc, l2l = _local_slots(tt, tgt_key_cell, tgt_key_loc, hf, dt, dir_off, KD)
+    rt64 = row_t.astype(np.int64)
+    l_cell, l_loc, l2l = _local_slots(tt, rt64, row_loc, hf, dt, dir_off, KD)
     plan.l_cell = l_cell
     plan.l_dir = np.where(l_loc >= 0, dir_off[np.maximum(hf - tt.level[l_cell], 0)] + l_loc, -1)
     lkey = l_cell * (KD + 1) + (l_loc + 1)
@@ -360,23 +345,27 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
         assert np.all(lkey[j] == k)
         return j
 
-    tslot = lslot(tgt_key_cell, tgt_key_loc)
-    order_ev = np.argsort(tslot, kind="stable")
-    rows, row_start = np.unique(tslot[order_ev], return_index=True)
-    plan.m2l_row_slot = rows.astype(np.int64)
-    plan.m2l_row_ptr = np.concatenate([row_start, [n_m2l]]).astype(np.int64)
-    plan.m2l_src = src_hat[order_ev].astype(np.int32)
-    plan.m2l_sym = ev_sym[order_ev]
-    plan.m2l_rid = ev_rid[order_ev]
+    tslot = lslot(rt64, row_loc)  # rows are (level, cell, key)-ordered: increasing
+    plan.m2l_row_slot = tslot.astype(np.int64)
+    plan.m2l_row_ptr = row_ptr
     ent = np.empty((n_m2l, 2), np.int32)
-    ent[:, 0] = src_hat[order_ev]
-    ent[:, 1] = inv[order_ev]
+    ent[:, 0] = src_hat
+    ent[:, 1] = inv
     plan.m2l_rows_entries = ent
-    plan.m2l_level = tt.level[l_cell[rows]]
+    plan.m2l_level = row_lev.astype(np.int64)
     # derived-symbol table: one per distinct (level, t)
     plan.trans_canon = cinv.astype(np.int32)
     plan.trans_rid = rid
-    _m2l_blocks(plan, tt, st, mt, ms, mlev, src_loc, src_hat, inv, tslot)
+    # parent-pair blocks of the blocked M2L (K7 v3), from the traversal
+    gr = nat["grp_rows"]
+    plan.blk_group_rows = np.where(gr >= 0, tslot[np.maximum(gr, 0)], -1) if n_rows else gr
+    plan.blk_group_ptr = nat["grp_ptr"]
+    bs = nat["blk_src"]
+    plan.blk_src = np.where(bs >= 0, src_hat[np.maximum(bs, 0)] if n_m2l else 0, -1).astype(np.int32)
+    bt = nat["blk_trans"]
+    plan.blk_trans = bt
+    plan.blk_mask = nat["blk_mask"]
+    plan.blk_kind = planar_kind(plan.blk_mask)
 
     # L2L gather lists per son level
     l2l_levels = []
@@ -440,70 +429,207 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
         "translations": int(uniq.shape[0]),
     }
     if keep_events:
-        plan.m2l_events = (mt, ms, ev_dir)
+        plan.m2l_events = (np.repeat(rt64, row_cnt), ev_s.astype(np.int64), np.repeat(row_key.astype(np.int64), row_cnt))
         plan.p2p_events = (pt, ps)
     return plan
 
 
-def _octant(tree, cells):
-    par = tree.parent[cells]
-    o = tree.coords[cells] - 2 * tree.coords[par]
-    return par, o[:, 0] * 4 + o[:, 1] * 2 + o[:, 2]
+def mac_threshold(level: int, hf: bool, beta: float, kappa: float, eta: float, gmax: int) -> int:
+    """Smallest integer gap^2 in [0, gmax] satisfying the reference MAC at this
+    level (gmax + 1 if none): ``gap2 >= 1`` at LF levels (traversal.py:100-104),
+    ``max(kappa*w*w, 2.0*w) <= eta*(beta*sqrt(gap2))`` at HF levels (:107-113),
+    evaluated with the same FP64 expression.  The HF test is an up-set in gap2
+    (sqrt and multiplication by positive constants are monotone under
+    round-to-nearest), so the threshold reproduces the per-pair test exactly."""
+    if not hf:
+        return 1 if gmax >= 1 else gmax + 1
+    w = SQRT3 * beta / 2.0
+    lhs = max(kappa * w * w, 2.0 * w)
+
+    def ok(g):
+        return bool(lhs <= eta * (beta * np.sqrt(float(g))))
+
+    if not ok(gmax):
+        return gmax + 1
+    lo, hi = 0, gmax
+    while lo < hi:
+        mid = (lo + hi) // 2
+        if ok(mid):
+            hi = mid
+        else:
+            lo = mid + 1
+    return lo
 
 
-def _m2l_blocks(plan, tt, st, mt, ms, mlev, key, src_hat, trans, tslot):
-    """Parent-pair blocks for the blocked M2L kernel (K7 v3).
+def _traversal_tables(tt, depth, hf, dt, dir_off, kappa, eta):
+    """Per-level MAC thresholds and dense HF key tables for defmm_dtt_build.
 
-    Group g = (target parent P, key): up to 8 target rows (t_a, key), a = the
-    octant of t in P.  Block = (g, source parent Q): up to 8 source spectra
-    (s_b, key) and, for every child offset delta = a_vec - b_vec in [-1,1]^3,
-    the derived symbol of translation 2 (P - Q) + delta; bit 8a+b of the
-    block mask marks the (a, b) pairs that are M2L events.  Every event lives
-    in exactly one block, so the kernel reuses each loaded spectrum/symbol for
-    all pairs of its block from registers."""
-    n = mt.shape[0]
-    if n == 0:
-        plan.blk_group_rows = np.zeros((0, 8), np.int64)
-        plan.blk_group_ptr = np.zeros(1, np.int64)
-        plan.blk_src = np.zeros((0, 8), np.int32)
-        plan.blk_trans = np.zeros((0, 27), np.int32)
-        plan.blk_mask = np.zeros(0, np.int64)
-        plan.blk_kind = np.zeros(0, np.int8)
-        return
-    P, a = _octant(tt, mt)
-    Q, b = _octant(st, ms)
-    dv = (tt.coords[mt] - 2 * tt.coords[P]) - (st.coords[ms] - 2 * st.coords[Q])
-    d = (dv[:, 0] + 1) * 9 + (dv[:, 1] + 1) * 3 + (dv[:, 2] + 1)
-    kk = key + 1
-    # groups ordered (level, key, P): symbols of one key stay L2-resident
-    go = np.lexsort((P, kk, mlev))
-    gk = np.stack([mlev[go], kk[go], P[go]], 1)
-    gbrk = np.ones(n, bool)
-    gbrk[1:] = np.any(gk[1:] != gk[:-1], axis=1)
-    gid = np.empty(n, np.int64)
-    gid[go] = np.cumsum(gbrk) - 1
-    ng = int(gid.max()) + 1
-    bo = np.lexsort((Q, gid))
-    bk = np.stack([gid[bo], Q[bo]], 1)
-    bbrk = np.ones(n, bool)
-    bbrk[1:] = np.any(bk[1:] != bk[:-1], axis=1)
-    bid = np.empty(n, np.int64)
-    bid[bo] = np.cumsum(bbrk) - 1
-    nb = int(bid.max()) + 1
-    rows = np.full((ng, 8), -1, np.int64)
-    rows[gid, a] = tslot
-    src = np.full((nb, 8), -1, np.int32)
-    src[bid, b] = src_hat
-    tr = np.full((nb, 27), -1, np.int32)
-    tr[bid, d] = trans
-    mask = np.zeros(nb, np.int64)
-    np.bitwise_or.at(mask, bid, np.left_shift(np.int64(1), (8 * a + b).astype(np.int64)))
-    blk_g = np.empty(nb, np.int64)
-    blk_g[bid] = gid
-    plan.blk_group_rows = rows
-    plan.blk_group_ptr = np.searchsorted(blk_g, np.arange(ng + 1)).astype(np.int64)
-    plan.blk_src, plan.blk_trans, plan.blk_mask = src, tr, mask
-    plan.blk_kind = planar_kind(mask)
+    Level l's candidate translations are bounded by R_l = min(2^l - 1,
+    2 D_{l-1} + 1), D_{l-1} the largest |t|_inf of a non-admissible pair one
+    level up.  key_tab holds the global nearest-direction id of every
+    admissible translation of an HF level (directions.nearest_directions,
+    bit-exact with directions.py:78-89), -1 elsewhere."""
+    g2min = np.zeros(depth + 1, np.int64)
+    R = np.zeros(depth + 1, np.int32)
+    tabs = []
+    for lev in range(depth + 1):
+        span = (1 << lev) - 1
+        gmax = 3 * max(span - 1, 0) ** 2
+        g2min[lev] = mac_threshold(lev, lev <= hf, tt.side_at(lev), kappa, eta, gmax)
+        if lev == 0:
+            r = 0
+        else:
+            pspan = (1 << (lev - 1)) - 1
+            gp = int(g2min[lev - 1])
+            dp = pspan if gp > 3 * max(pspan - 1, 0) ** 2 else min(pspan, math.isqrt(max(gp - 1, 0)) + 1)
+            r = min(span, 2 * dp + 1)
+        R[lev] = r
+        w = 2 * r + 1
+        tab = np.full(w**3, -1, np.int32)
+        if lev <= hf and g2min[lev] <= gmax:
+            ax = np.arange(-r, r + 1, dtype=np.int64)
+            tv = np.stack(np.meshgrid(ax, ax, ax, indexing="ij"), -1).reshape(-1, 3)
+            g = np.maximum(np.abs(tv) - 1, 0)
+            adm = np.nonzero((g * g).sum(1) >= g2min[lev])[0]
+            e = hf - lev
+            tab[adm] = dir_off[e] + nearest_directions(dt.levels[e], tv[adm])
+        tabs.append(tab)
+    tab_off = np.concatenate([[0], np.cumsum([t.shape[0] for t in tabs])]).astype(np.int64)
+    if tab_off[-1] >= 2**31:
+        raise ValueError("translation tables exceed the int32 index range")
+    return g2min, R, tab_off, np.concatenate(tabs)
+
+
+class NativeDtt:
+    """Lists of defmm_dtt_build (csrc/dtt_build.cpp); the handle stays open
+    for the source-spectrum pass (defmm_dtt_source_hats) until close()."""
+
+    _NAMES = ["ev_s", "ev_trans", "row_ptr", "row_t", "row_key", "row_lev", "grp_rows", "grp_p", "grp_key",
+              "grp_lev", "grp_ptr", "blk_src", "blk_trans", "blk_mask", "p_t", "p_s"]
+
+    def __init__(self, tt: ClusterTree, st: ClusterTree, depth, g2min, R, tab_off, key_tab):
+        self.lib = lib = _lib.load()
+
+        def arrs(tree):
+            return [np.ascontiguousarray(tree.level_offsets, np.int64), np.ascontiguousarray(tree.coords, np.int64),
+                    np.ascontiguousarray(tree.first_son, np.int64), np.ascontiguousarray(tree.n_sons, np.int64),
+                    np.ascontiguousarray(tree.parent, np.int64)]
+
+        ta = arrs(tt)
+        sa = ta if st is tt else arrs(st)
+        g2min = np.ascontiguousarray(g2min, np.int64)
+        R = np.ascontiguousarray(R, np.int32)
+        tab_off = np.ascontiguousarray(tab_off, np.int64)
+        key_tab = np.ascontiguousarray(key_tab, np.int32)
+        self.h = C.c_void_p()
+        rc = lib.defmm_dtt_build(ta[0].ctypes.data, tt.depth, *[a.ctypes.data for a in ta[1:]],
+                                 sa[0].ctypes.data, st.depth, *[a.ctypes.data for a in sa[1:]],
+                                 int(depth), g2min.ctypes.data, R.ctypes.data, tab_off.ctypes.data,
+                                 key_tab.ctypes.data, C.byref(self.h))
+        if rc == -4:
+            raise RuntimeError("defmm_dtt_build: a translation fell outside its level's key table")
+        if rc != 0:
+            raise RuntimeError(f"defmm_dtt_build failed ({rc})")
+        sz = np.zeros(6, np.int64)
+        _lib.check(lib.defmm_dtt_sizes(self.h, sz.ctypes.data), "defmm_dtt_sizes")
+        ne, nr, ng, nb, npp, ntr = (int(x) for x in sz)
+        self.n_events = ne
+        shapes = {
+            "ev_s": (ne, np.int32), "ev_trans": (ne, np.int32), "row_ptr": (nr + 1, np.int64),
+            "row_t": (nr, np.int32), "row_key": (nr, np.int32), "row_lev": (nr, np.int32),
+            "grp_rows": ((ng, 8), np.int64), "grp_p": (ng, np.int32), "grp_key": (ng, np.int32),
+            "grp_lev": (ng, np.int32), "grp_ptr": (ng + 1, np.int64), "blk_src": ((nb, 8), np.int64),
+            "blk_trans": ((nb, 27), np.int32), "blk_mask": (nb, np.int64), "p_t": (npp, np.int32),
+            "p_s": (npp, np.int32),
+        }
+        self.a = {k: np.empty(*shapes[k]) for k in self._NAMES}
+        _lib.check(lib.defmm_dtt_fetch(self.h, *[self.a[k].ctypes.data for k in self._NAMES]), "defmm_dtt_fetch")
+        self.a["trans_dense"] = np.empty(ntr, np.int64)
+        _lib.check(lib.defmm_dtt_translations(self.h, self.a["trans_dense"].ctypes.data), "defmm_dtt_translations")
+
+    def __getitem__(self, k):
+        return self.a[k]
+
+    def source_hats(self, m_dense, base, nd, level_off, key_base, n_mult):
+        """(src_hat per event int32, hat_slot) -- see defmm_dtt_source_hats."""
+        args = [np.ascontiguousarray(x, np.int64) for x in (m_dense, base, nd, level_off)]
+        kb = np.ascontiguousarray(key_base, np.int32)
+        src_hat = np.empty(self.n_events, np.int32)
+        hat = np.empty(max(int(n_mult), 1), np.int64)
+        nh = C.c_int64(0)
+        rc = self.lib.defmm_dtt_source_hats(self.h, *[x.ctypes.data for x in args], kb.ctypes.data, int(n_mult),
+                                            src_hat.ctypes.data, hat.ctypes.data, C.byref(nh))
+        if rc == -6:
+            raise RuntimeError("missing source expansion: blank-pass bug")
+        _lib.check(rc, "defmm_dtt_source_hats")
+        return src_hat, hat[: nh.value].copy()
+
+    def close(self):
+        if self.h:
+            self.lib.defmm_dtt_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def dtt_numpy(tt: ClusterTree, st: ClusterTree, kappa: float, eta: float, hf_switch: float):
+    """Vectorised level-synchronous restatement of traversal.py:320-348 with
+    the per-pair MAC (cross-check of dtt_native in tests/test_plan.py).
+    Returns (m2l_t, m2l_s, m2l_level, p2p_t, p2p_s)."""
+    depth = max(tt.depth, st.depth)
+    hf = hf_max_level(tt, depth, kappa, hf_switch)
+    m2l_t, m2l_s, m2l_lev, p2p_t, p2p_s = [], [], [], [], []
+    T = np.zeros(1, np.int64)
+    S = np.zeros(1, np.int64)
+    for lev in range(depth + 1):
+        if T.size == 0:
+            break
+        d = tt.coords[T] - st.coords[S]
+        g = np.maximum(np.abs(d) - 1, 0)
+        g2 = (g * g).sum(axis=1)
+        mac = _mac_lut(g2, lev, lev <= hf, tt.side_at(lev), kappa, eta)
+        m2l_t.append(T[mac])
+        m2l_s.append(S[mac])
+        m2l_lev.append(np.full(int(mac.sum()), lev, np.int64))
+        rest = ~mac
+        leafy = tt.is_leaf[T] | st.is_leaf[S]
+        sel = rest & leafy
+        p2p_t.append(T[sel])
+        p2p_s.append(S[sel])
+        sel = rest & ~leafy
+        rt, rs = T[sel], S[sel]
+        T, S = _expand_pairs(tt.first_son[rt], tt.n_sons[rt], st.first_son[rs], st.n_sons[rs])
+    cat = lambda xs: np.concatenate(xs) if xs else np.zeros(0, np.int64)  # noqa: E731
+    return cat(m2l_t), cat(m2l_s), cat(m2l_lev), cat(p2p_t), cat(p2p_s)
+
+
+def _dense_space(tree, hf, dt):
+    """Per-level dense index space over (cell, local direction): nd[l] slots
+    per cell (directions of refinement hf - l at HF levels, 1 at LF levels)."""
+    nd = np.ones(tree.depth + 1, np.int64)
+    for lev in range(min(hf, tree.depth) + 1):
+        nd[lev] = dt.levels[hf - lev].shape[0]
+    ncell = np.diff(tree.level_offsets)[: tree.depth + 1]
+    base = np.concatenate([[0], np.cumsum(ncell * nd)]).astype(np.int64)
+    return nd, base
+
+
+def _dense_index(tree, nd, base, cells, loc):
+    lev = tree.level[cells]
+    return base[lev] + (cells - tree.level_offsets[lev]) * nd[lev] + np.maximum(loc, 0)
+
+
+def _unique_cell_keys(cells, loc, tree, lev, nd, KD):
+    """Sorted distinct cell*KD + loc of one level's (cell, loc) list (bitmap)."""
+    off = int(tree.level_offsets[lev])
+    bm = np.zeros(int(tree.level_offsets[lev + 1] - off) * nd, bool)
+    bm[(cells.astype(np.int64) - off) * nd + loc] = True
+    nz = np.nonzero(bm)[0]
+    return (off + nz // nd) * KD + nz % nd
 
 
 def _planar_masks():

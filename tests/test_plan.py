@@ -239,3 +239,93 @@ def test_m2l_blocks_reconstruct_the_event_list(case):
             if (m >> bit) & 1:
                 a, b = divmod(bit, 8)
                 assert ((a >> (2 - p_)) & 1) == v and ((b >> (2 - p_)) & 1) == v
+
+
+# ---- native traversal (csrc/dtt_build.cpp) against the numpy restatement ----
+
+def _event_sets(mt, ms, pt, ps):
+    return sorted(zip(mt.tolist(), ms.tolist())), sorted(zip(pt.tolist(), ps.tolist()))
+
+
+@pytest.mark.parametrize(
+    "kind,n,kd,ncrit",
+    [("sphere", 3000, 32.0, 32), ("cube-surface", 5000, 96.0, 24), ("volume", 4000, 16.0, 16),
+     ("refined-cube", 4000, 128.0, 20), ("ellipsoid", 3000, 0.0, 32)],
+)
+def test_native_traversal_equals_numpy_dtt(kind, n, kd, ncrit):
+    """defmm_dtt_build (threshold MAC, dense key tables, target-major sweep)
+    visits exactly the pairs of the per-pair numpy traversal, with the same keys."""
+    from paper_2202_04894_b200.plan import dtt_numpy
+    from paper_2202_04894_b200.workloads import kappa_for, make_points
+
+    pts = make_points(kind, n, 3)
+    kappa = kappa_for(pts, kd) if kd else 0.0
+    tr, _ = build_tree(pts, np.ones(n), TreeConfig(ncrit=ncrit))
+    pl = build_plan(tr, tr, 4, kappa, 1.0, 2.0, keep_events=True)
+    mt, ms, mlev, pt, ps = dtt_numpy(tr, tr, kappa, 1.0, 2.0)
+    nm, npp = _event_sets(*pl.m2l_events[:2], *pl.p2p_events)
+    rm, rp = _event_sets(mt, ms, pt, ps)
+    assert nm == rm and npp == rp
+    # keys: nearest direction of each event's translation (directions.py:78-89)
+    hf = pl.hf_max
+    if hf >= 0:
+        dt = generate_direction_tree(hf)
+        m_t, m_s, key = pl.m2l_events
+        lev = tr.level[m_t]
+        for l in np.unique(lev[lev <= hf]):
+            sel = lev == l
+            e = hf - int(l)
+            ref = pl.dir_off[e] + nearest_directions(dt.levels[e], tr.coords[m_t[sel]] - tr.coords[m_s[sel]])
+            assert np.array_equal(key[sel], ref)
+        assert np.all(key[lev > hf] == -1)
+
+
+def test_native_traversal_two_trees_equals_numpy_dtt():
+    from paper_2202_04894_b200.geometry import compute_root_box
+    from paper_2202_04894_b200.plan import dtt_numpy
+
+    rng = np.random.default_rng(5)
+    src = rng.random((3000, 3))
+    tgt = rng.random((2000, 3)) * 0.5 + 0.25
+    box = compute_root_box(np.vstack([tgt, src]))
+    cfg = TreeConfig(ncrit=20)
+    st, _ = build_tree(src, np.ones(3000), cfg, root_box=box)
+    tt, _ = build_tree(tgt, np.zeros(2000), cfg, root_box=box)
+    kappa = 40.0
+    pl = build_plan(tt, st, 4, kappa, 1.0, 2.0, keep_events=True)
+    mt, ms, mlev, pt, ps = dtt_numpy(tt, st, kappa, 1.0, 2.0)
+    assert _event_sets(*pl.m2l_events[:2], *pl.p2p_events) == _event_sets(mt, ms, pt, ps)
+
+
+@pytest.mark.parametrize("kappa", [0.0, 3.0, 25.0, 80.0, 300.0])
+@pytest.mark.parametrize("eta", [0.5, 1.0, 2.0])
+def test_mac_threshold_equals_per_gap_mac(kappa, eta):
+    """The integer threshold reproduces the reference MAC (traversal.py:100-113)
+    for every gap^2 of every level (the HF test is an up-set in gap^2)."""
+    from paper_2202_04894_b200.plan import _mac_lut, mac_threshold
+
+    for level in range(0, 7):
+        span = (1 << level) - 1
+        gmax = 3 * max(span - 1, 0) ** 2
+        g = np.arange(gmax + 1)
+        beta = 2.0 / (1 << level)
+        for hf in (False, True):
+            if hf and kappa == 0.0:
+                continue
+            thr = mac_threshold(level, hf, beta, kappa, eta, gmax)
+            assert np.array_equal(g >= thr, _mac_lut(g, level, hf, beta, kappa, eta))
+
+
+def test_native_traversal_is_independent_of_thread_count(monkeypatch):
+    g = load_case("cubesurf4000")
+    kw = g["config"]
+    tr, _ = build_tree(g["points"], g["charges"], TreeConfig(ncrit=kw["ncrit"]))
+    outs = []
+    for nthr in ("1", "3", "8"):
+        monkeypatch.setenv("DEFMM_PLAN_THREADS", nthr)
+        pl = build_plan(tr, tr, kw["order"], kw["kappa"], 1.0, 2.0)
+        outs.append(pl)
+    for pl in outs[1:]:
+        for name in ("m2l_row_slot", "m2l_row_ptr", "m2l_rows_entries", "blk_group_rows", "blk_group_ptr",
+                     "blk_src", "blk_trans", "blk_mask", "p2p_ptr", "p2p_lo", "p2p_hi", "hat_slot"):
+            assert np.array_equal(getattr(pl, name), getattr(outs[0], name)), name
