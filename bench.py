@@ -51,7 +51,8 @@ def _args():
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of the CUDA graph")
     ap.add_argument("--dtype", default=None, choices=[None, "c128", "c64"], help="override the workload dtype")
     ap.add_argument("--p2p-overlap", default=None, choices=[None, "upward", "m2l"])
-    ap.add_argument("--m2l-levels", default="hybrid", choices=["hybrid", "blocked_all", "rows"])
+    ap.add_argument("--m2l-levels", default="hybrid",
+                    choices=["hybrid", "hybrid_rows", "blocked_all", "rows", "slice_all"])
     ap.add_argument("--m2l", default=None, help="M2L kernel variant (hybrid | derived | canonical)")
     return ap.parse_args()
 

@@ -122,6 +122,14 @@ void defmm_dtt_free(defmm_dtt* d);
  *   general block, 2p+v for a PLANAR block whose pairs all have a_p = b_p = v
  *   (surface data: 4x4 in-plane pairs, no predicated-off pair).  lhat[row] = sum D (*) hat  (stride
  *   defmm_spectrum_stride);  then K8 f2l_rows: local[row_slot[r]] = F2L(lhat[r]).
+ *   K7 v4 slice variant (m2l_slice): grid = nbatch row batches x spectral slices
+ *   (defmm_spectral_layout).  batch[4k..4k+3] = {row0, row1, first canonical
+ *   symbol of the batch's level, that level's canonical count}; rows r in
+ *   [row0, row1) are lhat rows whose events are sorted by symbol group
+ *   (G = 192 symbols for c64, 96 for c128): group g's events are
+ *   entries[seg[(r - row_base)(ngs+1) + g] .. seg[... + g + 1]), each {spectrum,
+ *   (canonical index within the group << 6) | rotation id}.  lhat[r] = sum over
+ *   events of rot(sym_canon) (*) hat -- the same sum as the row kernel.
  * K5 L2L -- traversal.py:355-391 in gather form.
  *   for i < n: local[out_slot[i]] += sum_{e in [ptr[i], ptr[i+1])}
  *   (C'0 (x) C'1 (x) C'2) local[src_slot[e]], C' the transposed/conjugate-
@@ -166,6 +174,10 @@ void defmm_dtt_free(defmm_dtt* d);
                                    const int32_t* blk_trans, const int64_t* blk_mask,           \
                                    const int8_t* blk_kind, const void* hat,                     \
                                    const void* sym_derived, void* lhat, void* stream);          \
+    int defmm_m2l_slice_##SUFFIX(int32_t L, int64_t nbatch, const int32_t* batch,                \
+                                 int64_t row_base, const int64_t* seg, int32_t ngs,             \
+                                 const int32_t* entries, const void* hat,                       \
+                                 const void* sym_canon, void* lhat, void* stream);              \
     int defmm_f2l_rows_##SUFFIX(int32_t L, int64_t nrows, const int64_t* row_slot,               \
                                 const void* lhat, void* local, void* stream);                   \
     int defmm_l2l_##SUFFIX(int32_t L, int64_t n, const int64_t* out_slot, const int8_t* octant,  \
@@ -192,12 +204,20 @@ void defmm_dtt_free(defmm_dtt* d);
 
 /* expands to: defmm_p2m_c128 defmm_m2m_c128 defmm_m2f_c128 defmm_symbols_c128
  * defmm_expand_symbols_c128 defmm_m2l_rows_c128 defmm_m2l_blocked_c128
- * defmm_f2l_rows_c128 defmm_l2l_c128 defmm_l2p_c128 defmm_p2p_c128 */
+ * defmm_m2l_slice_c128 defmm_f2l_rows_c128 defmm_l2l_c128 defmm_l2p_c128 defmm_p2p_c128 */
 DEFMM_DECLARE_TYPED(c128)
 /* expands to: defmm_p2m_c64 defmm_m2m_c64 defmm_m2f_c64 defmm_symbols_c64
  * defmm_expand_symbols_c64 defmm_m2l_rows_c64 defmm_m2l_blocked_c64
- * defmm_f2l_rows_c64 defmm_l2l_c64 defmm_l2p_c64 defmm_p2p_c64 */
+ * defmm_m2l_slice_c64 defmm_f2l_rows_c64 defmm_l2l_c64 defmm_l2p_c64 defmm_p2p_c64 */
 DEFMM_DECLARE_TYPED(c64)
+
+/* Spectral layout of order L (HOST call, no device needed): every spectrum is
+ * stored in orbit order, forder[pos] = natural frequency f0 P^2 + f1 P + f2 at
+ * storage position pos < P^3; slices [slice_start[k], slice_start[k+1]),
+ * k < *nslices, are unions of cube-group orbits of <= 64 positions. */
+int defmm_spectral_layout(int32_t L, int32_t* forder, int32_t* slice_start, int32_t* nslices);
+/* canonical symbols per shared-memory group G of the slice M2L (c64 != 0: complex64) */
+int defmm_slice_group(int32_t c64);
 
 /* K7 reference variant (c128): canonical symbols gathered through the closed-
  * form rotation inside the loop (e_sym canonical id, e_rid rotation id). */

@@ -20,8 +20,10 @@
 //    closed form of the cube-group frequency permutation (fourier.py:123-196).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <vector>
 
 #include "../../include/defmm_b200.h"
 
@@ -180,6 +182,36 @@ __device__ __forceinline__ void make_twiddles(V* tw) {
 // e^{-2 pi i k / P} for every P = 2L-1 (L = 2..8), filled once by the
 // launchers (cudaMemcpyToSymbol); kernels build their P x L matrix from it
 __constant__ double2 c_tw[8][15];
+
+// ---------------------------------------------------------------------------
+// Spectral layout.  Every P^3 spectrum (multipole spectra, symbols, local
+// accumulators) is stored in ORBIT ORDER: the natural frequency indices
+// j = f0 P^2 + f1 P + f2 grouped by their orbit under the 48-element cube group
+// acting on (f0, f1, f2) mod P (fourier.py:90-101 / rotated_index below), the
+// orbits packed first-fit-decreasing into SLICES of <= SLICE_W positions.  A
+// slice is closed under every rotation, so the slice M2L can hold the
+// canonical symbols of one slice in shared memory.  g_forder[L-1][pos] =
+// natural index at a position, g_finv the inverse; the Hadamard product is
+// order-agnostic, the kernels that touch natural indices (M2F, symbols, F2L,
+// rotations) go through these tables.
+constexpr int SLICE_W = 64;
+constexpr int MAX_SLICES = 72;
+constexpr int MAX_P3 = 15 * 15 * 15;
+__device__ int16_t g_forder[8][MAX_P3];
+__device__ int16_t g_finv[8][MAX_P3];
+__device__ int32_t g_slice_start[8][MAX_SLICES + 1];
+// rotation table per slice: g_rot[L-1][slice][rid][k] = slice-local position
+// of the canonical entry feeding position start + k under rotation rid
+__device__ int8_t g_rot[8][MAX_SLICES][48][SLICE_W];
+
+template <int L>
+__device__ __forceinline__ int forder(int pos) {
+    return g_forder[L - 1][pos];
+}
+template <int L>
+__device__ __forceinline__ int finv(int j) {
+    return g_finv[L - 1][j];
+}
 
 template <int L, typename V>
 __device__ __forceinline__ void make_twiddle_matrix(V* twm) {
@@ -504,9 +536,10 @@ __global__ void __launch_bounds__(32 * M2F_WARPS) m2f_kernel(int64_t n, const in
     constexpr int SS = spec_stride<R, L>();
     V* out = hat + i * (int64_t)SS;
     for (int t = lane; t < SS; t += 32) {
-        const int f0 = t / (P * P), f12 = t % (P * P);
         V v = cz<V>();
         if (t < P3) {
+            const int j = forder<L>(t);  // orbit-ordered position -> natural frequency
+            const int f0 = j / (P * P), f12 = j % (P * P);
 #pragma unroll
             for (int a = 0; a < L; ++a) v = cfma(Y2[a * P * P + f12], tw[f0 * L + a], v);
         }
@@ -557,10 +590,12 @@ __global__ void __launch_bounds__(256) symbols_kernel(int64_t n, const int32_t* 
     constexpr int SS = spec_stride<R, L>();
     cx<R>* out = sym + i * (int64_t)SS;
     for (int t = threadIdx.x; t < SS; t += blockDim.x) {
-        const int f = t / (P * P), bc = t % (P * P);
         double2 v = make_double2(0.0, 0.0);
-        if (t < P3)
+        if (t < P3) {
+            const int j = forder<L>(t);
+            const int f = j / (P * P), bc = j % (P * P);
             for (int k = 0; k < P; ++k) v = cfma(A[k * P * P + bc], tw[(f * k) % P], v);
+        }
         out[t] = from_d<cx<R>>(v);
     }
 }
@@ -598,7 +633,8 @@ __global__ void __launch_bounds__(256) expand_symbols_kernel(int64_t n, const in
     constexpr int SS = spec_stride<R, L>();
     const cx<R>* src = symc + (int64_t)canon[i] * SS;
     cx<R>* dst = symd + i * SS;
-    for (int j = threadIdx.x; j < SS; j += blockDim.x) dst[j] = j < P3 ? src[rotated_index<P>(j, r)] : cz<cx<R>>();
+    for (int t = threadIdx.x; t < SS; t += blockDim.x)
+        dst[t] = t < P3 ? src[finv<L>(rotated_index<P>(forder<L>(t), r))] : cz<cx<R>>();
 }
 
 // ---------------------------------------------------------------------------
@@ -721,7 +757,7 @@ __global__ void __launch_bounds__(m2l_block<R, L>()) m2l_rows_kernel(
 #pragma unroll
         for (int w = 0; w < W; ++w) {
             const int j = jv * W + w;
-            if (j < P3) X[j] = cadd(to_d(acc[0][m][w]), to_d(acc[1][m][w]));
+            if (j < P3) X[forder<L>(j)] = cadd(to_d(acc[0][m][w]), to_d(acc[1][m][w]));
         }
     }
     __syncthreads();
@@ -907,6 +943,94 @@ __global__ void __launch_bounds__(m2lb_threads<R, L>(), DEFMM_M2LB_MINBLOCKS) m2
     }
 }
 
+// ---------------------------------------------------------------------------
+// K7 v4: slice M2L.  Grid = (row batch, spectral slice).  The Hadamard M2L is
+// independent per frequency, and a slice is closed under the cube group, so a
+// CTA keeps the CANONICAL symbols of its level restricted to its slice in
+// shared memory (in groups of G symbols) together with the slice's 48
+// rotation maps, and streams only the source spectra (one slice = <= 64
+// contiguous entries per event, one warp per row): half the L2->SM bytes of
+// the row kernel, whose derived symbols double the per-event traffic.
+// Events of a row are sorted by symbol group; the accumulated slice is kept in
+// lhat between groups (read back by the same thread).  Per event the warp
+// reads one {spectrum, canonical-in-group << 6 | rotation} entry.
+constexpr int SLICE_WARPS = 16;
+template <typename R>
+__host__ __device__ constexpr int slice_group() {
+    return sizeof(R) == 4 ? 192 : 96;  // symbols per group: G * 64 * sizeof(cx<R>) = 96 KB
+}
+template <typename R>
+__host__ __device__ constexpr size_t slice_smem_bytes() {
+    return sizeof(cx<R>) * slice_group<R>() * SLICE_W + 48 * SLICE_W;
+}
+
+template <typename R, int L>
+__global__ void __launch_bounds__(32 * SLICE_WARPS, 2) m2l_slice_kernel(
+    const int4* __restrict__ batch, int64_t row_base, const int64_t* __restrict__ seg, int ngs,
+    const int2* __restrict__ ent, const cx<R>* __restrict__ hat, const cx<R>* __restrict__ symc,
+    cx<R>* __restrict__ lhat) {
+    using V = cx<R>;
+    constexpr int SS = spec_stride<R, L>();
+    constexpr int G = slice_group<R>();
+    constexpr int U = sizeof(R) == 4 ? 4 : 2;  // events in flight per warp (c128: 64-register cap)
+    extern __shared__ unsigned char smraw[];
+    V* sym = reinterpret_cast<V*>(smraw);                          // [G][SLICE_W]
+    int8_t* rot = reinterpret_cast<int8_t*>(sym + G * SLICE_W);    // [48][SLICE_W]
+    const int sl = blockIdx.y;
+    const int start = g_slice_start[L - 1][sl];
+    const int size = g_slice_start[L - 1][sl + 1] - start;
+    const int4 bt = batch[blockIdx.x];  // {row0, row1, first canonical symbol, count}
+    const int8_t* rsrc = &g_rot[L - 1][sl][0][0];
+    for (int t = threadIdx.x; t < 48 * SLICE_W; t += blockDim.x) rot[t] = rsrc[t];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int k0 = lane, k1 = lane + 32;
+    const bool on0 = k0 < size, on1 = k1 < size;
+    const int ng = (bt.w + G - 1) / G;
+    for (int g = 0; g < ng; ++g) {
+        __syncthreads();  // the previous group's symbols are consumed
+        const int nc = min(G, bt.w - g * G);
+        const V* src = symc + (int64_t)(bt.z + g * G) * SS + start;
+        for (int t = threadIdx.x; t < nc * SLICE_W; t += blockDim.x) {
+            const int c = t / SLICE_W, k = t % SLICE_W;
+            sym[t] = k < size ? __ldg(src + (int64_t)c * SS + k) : cz<V>();
+        }
+        __syncthreads();
+        for (int row = bt.x + warp; row < bt.y; row += SLICE_WARPS) {
+            const int64_t* sg = seg + (row - row_base) * (int64_t)(ngs + 1);
+            const int64_t e0 = sg[g], e1 = sg[g + 1];
+            if (g > 0 && e0 == e1) continue;
+            V* out = lhat + (int64_t)row * SS + start;
+            V acc[2][2];
+            acc[0][0] = (g > 0 && on0) ? out[k0] : cz<V>();
+            acc[0][1] = (g > 0 && on1) ? out[k1] : cz<V>();
+            acc[1][0] = acc[1][1] = cz<V>();
+            for (int64_t e = e0; e < e1; e += U) {
+                int2 m[U];
+                V s0[U], s1[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) m[u] = __ldg(ent + min(e + u, e1 - 1));
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const V* S = hat + (int64_t)m[u].x * SS + start;
+                    s0[u] = on0 ? __ldg(S + k0) : cz<V>();
+                    s1[u] = on1 ? __ldg(S + k1) : cz<V>();
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (e + u < e1) {
+                        const V* D = sym + (m[u].y >> 6) * SLICE_W;
+                        const int8_t* rr = rot + (m[u].y & 63) * SLICE_W;
+                        if (on0) acc[u & 1][0] = cfma(D[rr[k0]], s0[u], acc[u & 1][0]);
+                        if (on1) acc[u & 1][1] = cfma(D[rr[k1]], s1[u], acc[u & 1][1]);
+                    }
+                }
+            }
+            if (on0) out[k0] = from_d<V>(cadd(to_d(acc[0][0]), to_d(acc[1][0])));
+            if (on1) out[k1] = from_d<V>(cadd(to_d(acc[0][1]), to_d(acc[1][1])));
+        }
+    }
+}
+
 // pruned inverse DFT of accumulated spectra (fourier.py:74-80), one CTA per row:
 // local[row_slot[r]] = F2L(lhat[r]); FP64 transform for both storage types
 template <typename R, int L>
@@ -922,7 +1046,7 @@ __global__ void __launch_bounds__(128) f2l_rows_kernel(int64_t nrows, const int6
     const int64_t r = blockIdx.x;
     make_twiddle_matrix<L, double2>(tw);
     const cx<R>* src = lhat + r * SS;
-    for (int j = threadIdx.x; j < P3; j += blockDim.x) X[j] = to_d(src[j]);
+    for (int j = threadIdx.x; j < P3; j += blockDim.x) X[forder<L>(j)] = to_d(src[j]);
     __syncthreads();
     f2l_row<L, double2>(tw, X, Z1, O, blockDim.x);
     __syncthreads();
@@ -957,13 +1081,13 @@ __global__ void __launch_bounds__(m2l_threads<L>()) m2l_canon_kernel(
 #pragma unroll
         for (int m = 0; m < PER; ++m) {
             const int j = threadIdx.x + m * NT;
-            if (j < P3) acc[m] = cfma(__ldg(D + rotated_index<P>(j, rid)), __ldg(S + j), acc[m]);
+            if (j < P3) acc[m] = cfma(__ldg(D + finv<L>(rotated_index<P>(forder<L>(j), rid))), __ldg(S + j), acc[m]);
         }
     }
 #pragma unroll
     for (int m = 0; m < PER; ++m) {
         const int j = threadIdx.x + m * NT;
-        if (j < P3) X[j] = acc[m];
+        if (j < P3) X[forder<L>(j)] = acc[m];
     }
     __syncthreads();
     f2l_row<L, double2>(tw, X, Z1, local + row_slot[row] * cube<L>(), NT);
@@ -1389,9 +1513,121 @@ __global__ void direct_reduce(int64_t nt, int nsplit, const double2* __restrict_
 // launch helpers
 
 // fill c_tw once per process (before the first launch that needs it)
+// host restatement of rotated_index (same closed form)
+int host_rotated_index(int P, int j, int rid) {
+    static const int perm[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+    const int f[3] = {j / (P * P), (j / P) % P, j % P};
+    const int wt[3] = {P * P, P, 1};
+    int idx = 0;
+    for (int a = 0; a < 3; ++a) {
+        const int ng = (rid >> (2 - a)) & 1;
+        idx += wt[perm[rid >> 3][a]] * (ng ? (f[a] ? P - f[a] : 0) : f[a]);
+    }
+    return idx;
+}
+
+struct HostLayout {
+    int P3 = 0, nslices = 0;
+    std::vector<int16_t> forder, finv;
+    std::vector<int32_t> start;
+    std::vector<int8_t> rot;  // [slice][48][SLICE_W]
+};
+
+// orbit-ordered spectral layout of order L (see g_forder): orbits keyed by the
+// sorted per-axis |frequency| (min(f, P - f)), enumerated in key order,
+// packed first-fit-decreasing into slices of <= SLICE_W positions
+HostLayout make_layout(int L) {
+    HostLayout H;
+    const int P = 2 * L - 1, P3 = P * P * P;
+    H.P3 = P3;
+    std::vector<std::vector<int>> orbits;
+    std::vector<int> key_of(P3);
+    const int A = P / 2 + 1;
+    std::vector<int> orbit_of_key(A * A * A, -1);
+    for (int j = 0; j < P3; ++j) {
+        int a[3] = {j / (P * P), (j / P) % P, j % P};
+        for (int& x : a) x = std::min(x, P - x);
+        std::sort(a, a + 3);
+        key_of[j] = (a[0] * A + a[1]) * A + a[2];
+    }
+    for (int k = 0; k < A * A * A; ++k)
+        for (int j = 0; j < P3; ++j)
+            if (key_of[j] == k) {
+                if (orbit_of_key[k] < 0) {
+                    orbit_of_key[k] = (int)orbits.size();
+                    orbits.emplace_back();
+                }
+                orbits[orbit_of_key[k]].push_back(j);
+            }
+    std::vector<int> order(orbits.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int x, int y) { return orbits[x].size() > orbits[y].size(); });
+    std::vector<std::vector<int>> bins;
+    std::vector<int> fill;
+    for (int o : order) {
+        const int sz = (int)orbits[o].size();
+        size_t b = 0;
+        while (b < bins.size() && fill[b] + sz > SLICE_W) ++b;
+        if (b == bins.size()) {
+            bins.emplace_back();
+            fill.push_back(0);
+        }
+        bins[b].push_back(o);
+        fill[b] += sz;
+    }
+    H.nslices = (int)bins.size();
+    H.forder.resize(P3);
+    H.finv.resize(P3);
+    H.start.assign(1, 0);
+    int pos = 0;
+    for (const auto& b : bins) {
+        for (int o : b)
+            for (int j : orbits[o]) H.forder[pos++] = (int16_t)j;
+        H.start.push_back(pos);
+    }
+    for (int t = 0; t < P3; ++t) H.finv[H.forder[t]] = (int16_t)t;
+    H.rot.assign((size_t)H.nslices * 48 * SLICE_W, 0);
+    for (int sl = 0; sl < H.nslices; ++sl)
+        for (int rid = 0; rid < 48; ++rid)
+            for (int k = 0; k < H.start[sl + 1] - H.start[sl]; ++k) {
+                const int p = H.finv[host_rotated_index(P, H.forder[H.start[sl] + k], rid)];
+                H.rot[((size_t)sl * 48 + rid) * SLICE_W + k] = (int8_t)(p - H.start[sl]);
+            }
+    return H;
+}
+
+const HostLayout& layout_of(int L) {
+    static HostLayout cache[9];
+    static bool made[9] = {};
+    if (!made[L]) {
+        cache[L] = make_layout(L);
+        made[L] = true;
+    }
+    return cache[L];
+}
+
 int ensure_twiddles() {
     static bool done = false;
     if (done) return 0;
+    for (int L = 2; L <= 8; ++L) {
+        const HostLayout& H = layout_of(L);
+        if (H.nslices > MAX_SLICES) return report(cudaErrorInvalidValue, "spectral layout: too many slices");
+        const size_t o = (size_t)(L - 1);
+        int rc = report(cudaMemcpyToSymbol(g_forder, H.forder.data(), H.P3 * sizeof(int16_t),
+                                           o * MAX_P3 * sizeof(int16_t)), "cudaMemcpyToSymbol(g_forder)");
+        if (!rc)
+            rc = report(cudaMemcpyToSymbol(g_finv, H.finv.data(), H.P3 * sizeof(int16_t),
+                                           o * MAX_P3 * sizeof(int16_t)), "cudaMemcpyToSymbol(g_finv)");
+        if (!rc)
+            rc = report(cudaMemcpyToSymbol(g_slice_start, H.start.data(), H.start.size() * sizeof(int32_t),
+                                           o * (MAX_SLICES + 1) * sizeof(int32_t)),
+                        "cudaMemcpyToSymbol(g_slice_start)");
+        if (!rc)
+            rc = report(cudaMemcpyToSymbol(g_rot, H.rot.data(), H.rot.size(), o * MAX_SLICES * 48 * SLICE_W),
+                        "cudaMemcpyToSymbol(g_rot)");
+        if (rc) return rc;
+    }
     double2 h[8][15] = {};
     for (int L = 2; L <= 8; ++L) {
         const int P = 2 * L - 1;
@@ -1496,6 +1732,7 @@ int launch_symbols(int32_t L, int64_t n, const int32_t* tvec, const double* beta
                    void* stream) {
     if (n == 0) return 0;
     if (!grid_ok(n)) return -1;
+    if (int rc0 = ensure_twiddles()) return rc0;
     cudaStream_t s = (cudaStream_t)stream;
     DEFMM_DISPATCH_L(L, {
         constexpr int P = 2 * LL - 1;
@@ -1512,6 +1749,7 @@ int launch_expand(int32_t L, int64_t n, const int32_t* canon, const int8_t* rid,
                   void* stream) {
     if (n == 0) return 0;
     if (!grid_ok(n)) return -1;
+    if (int rc0 = ensure_twiddles()) return rc0;
     cudaStream_t s = (cudaStream_t)stream;
     DEFMM_DISPATCH_L(L, (expand_symbols_kernel<R, LL><<<(unsigned)n, 256, 0, s>>>(
                             n, canon, rid, (const cx<R>*)symc, (cx<R>*)symd)));
@@ -1548,6 +1786,26 @@ int launch_m2l_blocked(int32_t L, int64_t ngroups, const int64_t* grp_ptr, const
                             ngroups, grp_ptr, grp_rows, blk_src, blk_trans, blk_mask, blk_kind,
                             (const cx<R>*)hat, (const cx<R>*)symd, (cx<R>*)lhat)));
     return report(cudaGetLastError(), "m2l_blocked");
+}
+
+template <typename R>
+int launch_m2l_slice(int32_t L, int64_t nbatch, const int32_t* batch, int64_t row_base, const int64_t* seg,
+                     int32_t ngs, const int32_t* entries, const void* hat, const void* symc, void* lhat,
+                     void* stream) {
+    if (nbatch == 0) return 0;
+    if (!grid_ok(nbatch) || ngs < 1) return -1;
+    if (int rc0 = ensure_twiddles()) return rc0;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t bytes = slice_smem_bytes<R>();
+    DEFMM_DISPATCH_L(L, {
+        int rc = set_smem(m2l_slice_kernel<R, LL>, bytes);
+        if (rc) return rc;
+        const dim3 grid((unsigned)nbatch, (unsigned)layout_of(LL).nslices);
+        m2l_slice_kernel<R, LL><<<grid, 32 * SLICE_WARPS, bytes, s>>>(
+            (const int4*)batch, row_base, seg, ngs, (const int2*)entries, (const cx<R>*)hat, (const cx<R>*)symc,
+            (cx<R>*)lhat);
+    });
+    return report(cudaGetLastError(), "m2l_slice");
 }
 
 template <typename R>
@@ -1617,6 +1875,19 @@ int launch_p2p(int64_t n_items, const int32_t* item_leaf, const int64_t* item_f0
 extern "C" {
 
 int defmm_abi_version(void) { return DEFMM_ABI_VERSION; }
+
+int defmm_slice_group(int32_t c64) { return c64 ? slice_group<float>() : slice_group<double>(); }
+
+int defmm_spectral_layout(int32_t L, int32_t* forder, int32_t* slice_start, int32_t* nslices) {
+    if (L < 2 || L > 8) return -1;
+    const HostLayout& H = layout_of(L);
+    if (nslices) *nslices = H.nslices;
+    if (forder)
+        for (int t = 0; t < H.P3; ++t) forder[t] = H.forder[t];
+    if (slice_start)
+        for (int t = 0; t <= H.nslices; ++t) slice_start[t] = H.start[t];
+    return 0;
+}
 const char* defmm_last_error(void) { return g_last_error; }
 
 #define DEFMM_EXPORT_TYPED(SUFFIX, R)                                                                               \
@@ -1656,6 +1927,11 @@ const char* defmm_last_error(void) { return g_last_error; }
                                    void* stream) {                                                                \
         return launch_m2l_blocked<R>(L, ngroups, grp_ptr, grp_rows, blk_src, blk_trans, blk_mask, blk_kind, hat,   \
                                      sym_derived, lhat, stream);                                                  \
+    }                                                                                                               \
+    int defmm_m2l_slice_##SUFFIX(int32_t L, int64_t nbatch, const int32_t* batch, int64_t row_base,               \
+                                 const int64_t* seg, int32_t ngs, const int32_t* entries, const void* hat,         \
+                                 const void* sym_canon, void* lhat, void* stream) {                               \
+        return launch_m2l_slice<R>(L, nbatch, batch, row_base, seg, ngs, entries, hat, sym_canon, lhat, stream);   \
     }                                                                                                               \
     int defmm_f2l_rows_##SUFFIX(int32_t L, int64_t nrows, const int64_t* row_slot, const void* lhat, void* local,   \
                                 void* stream) {                                                                    \

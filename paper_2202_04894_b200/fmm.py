@@ -175,6 +175,12 @@ class FmmPlan:
         self.blk_trans = _dev(h["blk_trans"].reshape(-1), i32, d)
         self.blk_mask = _dev(h["blk_mask"], i64, d)
         self.blk_kind = _dev(h["blk_kind"], torch.int8, d)
+        sl = h["slice"]
+        self.n_slice_batch = int(sl["n_batch"])
+        self.sl_batch = _dev(sl["batch"].reshape(-1), i32, d)
+        self.sl_seg = _dev(sl["seg"], i64, d)
+        self.sl_ent = _dev(sl["ent"].reshape(-1), i32, d)
+        self.sl_ngs, self.sl_row_base = int(sl["ngs"]), int(sl["row_base"])
         # downward
         self.l2l = []
         for lev, outs, octant, ptr, src, sdir in h["l2l"]:
@@ -250,27 +256,85 @@ class FmmPlan:
             sel = blev == lev
             if ev[sel].mean() >= self.BLOCKED_MIN_EVENTS_PER_BLOCK:
                 dense.add(int(lev))
-        if self.m2l_variant_default == "rows":
+        mode = self.m2l_variant_default
+        if mode in ("rows", "slice_all"):
             dense = set()
-        elif self.m2l_variant_default == "blocked_all":
+        elif mode == "blocked_all":
             dense = set(int(x) for x in np.unique(blev))
         is_dense = np.isin(rlev, list(dense)) if dense else np.zeros(rows.shape[0], bool)
-        # rows of sparse levels -> row kernel
-        keep_rows, rptr, rsel = _sub_csr(h["row_ptr"], ~is_dense)
-        h["rk_rows"], h["rk_ptr"], h["rk_ent"] = rows[~is_dense], rptr, h["ent"][rsel]
-        # groups of dense levels -> blocked kernel, rows renumbered into lhat
         dense_rows = rows[is_dense]
+        # rows of sparse levels -> slice kernel (default) or row kernel
+        keep_rows, rptr, rsel = _sub_csr(h["row_ptr"], ~is_dense)
+        sparse_rows = rows[~is_dense]
+        z = np.zeros(0, np.int64)
+        if mode in ("rows", "hybrid_rows"):
+            h["rk_rows"], h["rk_ptr"], h["rk_ent"] = sparse_rows, rptr, h["ent"][rsel]
+            h["slice"] = self._slice_lists(np.zeros(1, np.int64), np.zeros((0, 2), np.int32), z, 0)
+        else:
+            h["rk_rows"], h["rk_ptr"], h["rk_ent"] = z, np.zeros(1, np.int64), np.zeros((0, 2), np.int32)
+            h["slice"] = self._slice_lists(rptr, h["ent"][rsel], rlev[~is_dense], int(dense_rows.shape[0]))
+        # groups of dense levels -> blocked kernel, rows renumbered into lhat
         gr = h["grp_rows"]
         gr_slots = np.where(gr >= 0, rows[np.maximum(gr, 0)] if rows.size else -1, -1)
         gid = _rows_to_ids(gr_slots, dense_rows)
         gkeep = np.any(gid >= 0, axis=1)
         _, gptr, bsel = _sub_csr(h["grp_ptr"], gkeep)
-        h["bk_rows"] = dense_rows
+        # lhat rows: blocked rows, then slice rows (one F2L launch for both)
+        h["bk_rows"] = np.concatenate([dense_rows, sparse_rows if h["slice"]["n_batch"] else z])
         h["grp_ptr"], h["grp_rows"] = gptr, gid[gkeep]
         h["blk_src"], h["blk_trans"], h["blk_mask"] = h["blk_src"][bsel], h["blk_trans"][bsel], h["blk_mask"][bsel]
         h["blk_kind"] = h["blk_kind"][bsel]
         self.dense_levels = sorted(dense)
         return h
+
+    # rows per slice-kernel batch: enough events per batch to amortise the
+    # shared-memory symbol loads (G symbols per group), one row per warp at least
+    SLICE_MIN_BATCH_ROWS = 16
+    SLICE_MAX_BATCH_ROWS = 512
+
+    def _slice_lists(self, rptr, ent, rlev, lhat_base) -> dict:
+        """Lists of the slice M2L (K7 v4, defmm_m2l_slice_*): per row, events
+        sorted by canonical-symbol group (G per group, the level's canonical
+        symbols are contiguous in the symbol table); entries {spectrum,
+        (canonical-in-group << 6) | rotation}; seg[r, g] = first event of group
+        g; batches of rows of one level {row0, row1, first symbol, count}."""
+        p = self.plan
+        n = int(rlev.shape[0])
+        G = int(_lib.load().defmm_slice_group(int(self.config.dtype == "c64")))
+        if n == 0:
+            return {"n_batch": 0, "batch": np.zeros((0, 4), np.int32), "seg": np.zeros(1, np.int64),
+                    "ent": np.zeros((0, 2), np.int32), "ngs": 1, "row_base": lhat_base}
+        cnt = np.diff(rptr)
+        lev_lo = np.searchsorted(p.sym_level, rlev, side="left")
+        lev_nc = np.searchsorted(p.sym_level, rlev, side="right") - lev_lo
+        ngs = int(max(1, (-(-lev_nc // G)).max()))
+        tid = ent[:, 1].astype(np.int64)
+        clocal = p.trans_canon[tid].astype(np.int64) - np.repeat(lev_lo, cnt)
+        grp = clocal // G
+        meta = ((clocal % G) << 6) | p.trans_rid[tid].astype(np.int64)
+        key = np.repeat(np.arange(n, dtype=np.int64), cnt) * ngs + grp
+        if ngs > 1:
+            order = np.argsort(key, kind="stable")
+            key, meta, src = key[order], meta[order], ent[order, 0]
+        else:
+            src = ent[:, 0]
+        sent = np.empty((key.shape[0], 2), np.int32)
+        sent[:, 0] = src
+        sent[:, 1] = meta
+        probe = (np.arange(n, dtype=np.int64)[:, None] * ngs + np.arange(ngs + 1)[None, :]).reshape(-1)
+        seg = np.searchsorted(key, probe, side="left").astype(np.int64)
+        # batches: rows of one level (contiguous: rows are slot-sorted, level-major)
+        batches = []
+        brk = np.nonzero(np.diff(rlev))[0] + 1
+        for a, b in zip(np.concatenate([[0], brk]), np.concatenate([brk, [n]])):
+            ev_row = max(float(cnt[a:b].mean()), 1.0)
+            ngl = -(-int(lev_nc[a]) // G)
+            br = int(np.clip(16 * G * ngl / ev_row, self.SLICE_MIN_BATCH_ROWS, self.SLICE_MAX_BATCH_ROWS))
+            br = -(-br // 16) * 16
+            for r0 in range(int(a), int(b), br):
+                batches.append((lhat_base + r0, lhat_base + min(int(b), r0 + br), int(lev_lo[a]), int(lev_nc[a])))
+        return {"n_batch": len(batches), "batch": np.asarray(batches, np.int32).reshape(-1, 4), "seg": seg,
+                "ent": sent, "ngs": ngs, "row_base": lhat_base}
 
     def _host_lists_all(self) -> dict:
         """The plan's lists, restricted to this rank's chunk when sharded
@@ -423,6 +487,8 @@ class FmmPlan:
                       self.hat, self.sym_derived, self.local, sh)
             _lib.call(self._op("m2l_blocked"), L, self.n_groups, self.grp_ptr, self.grp_rows, self.blk_src,
                       self.blk_trans, self.blk_mask, self.blk_kind, self.hat, self.sym_derived, self.lhat, sh)
+            _lib.call(self._op("m2l_slice"), L, self.n_slice_batch, self.sl_batch, self.sl_row_base, self.sl_seg,
+                      self.sl_ngs, self.sl_ent, self.hat, self.sym, self.lhat, sh)
             _lib.call(self._op("f2l_rows"), L, self.bk_rows.shape[0], self.bk_rows, self.lhat, self.local, sh)
         elif self.m2l_variant == "derived":
             _lib.call(self._op("m2l_rows"), L, self.row_slot.shape[0], self.row_slot, self.row_ptr,
@@ -485,7 +551,14 @@ class FmmPlan:
 
     @property
     def launches_per_apply(self) -> int:
-        return 5 + len(self.m2m) + len(self.l2l) + (1 if self.n_split else 0) + 2 * (self.m2l_variant == "hybrid")
+        """Kernels of one matvec: p2p (+ split reduce), p2m, m2m per level, m2f,
+        the M2L kernels with work, l2l per level, l2p."""
+        if self.m2l_variant == "hybrid":
+            m2l = sum(int(n > 0) for n in (self.rk_rows.shape[0], self.n_groups, self.n_slice_batch,
+                                           self.bk_rows.shape[0]))
+        else:
+            m2l = 1
+        return 4 + (1 if self.n_split else 0) + len(self.m2m) + len(self.l2l) + m2l
 
     def events(self):
         """InteractionEvent list (traversal.py:80-85) with Cell views."""
@@ -506,6 +579,21 @@ class FmmPlan:
         for t, s in zip(pt.tolist(), ps.tolist()):
             out.append(InteractionEvent("P2P", tl[t], sl[s]))
         return out
+
+
+def spectral_layout(L: int):
+    """(forder, slice_start): storage position -> natural frequency index
+    f0 P^2 + f1 P + f2 of every device spectrum, and the orbit-closed slices
+    (defmm_spectral_layout, host call)."""
+    import ctypes as C
+
+    P3 = (2 * L - 1) ** 3
+    forder = np.empty(P3, np.int32)
+    starts = np.empty(P3 + 1, np.int32)
+    ns = C.c_int32(0)
+    _lib.check(_lib.load().defmm_spectral_layout(int(L), forder.ctypes.data, starts.ctypes.data, C.byref(ns)),
+               "defmm_spectral_layout")
+    return forder, starts[: ns.value + 1].copy()
 
 
 def run_fmm_full(targets, sources, charges, config: FmmConfig = FmmConfig(), events: list | None = None):

@@ -129,6 +129,7 @@ class Plan:
     # symbols
     sym_tvec: np.ndarray = None  # (nsym, 3) int32 canonical translations
     sym_beta: np.ndarray = None  # (nsym,)
+    sym_level: np.ndarray = None  # (nsym,) level; symbols are sorted by (level, canonical t)
     # multipole slots (source tree)
     m_cell: np.ndarray = None
     m_dir: np.ndarray = None  # global dir id or -1
@@ -244,6 +245,7 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
     sym_t[cinv] = canon
     plan.sym_tvec = sym_t.astype(np.int32)
     plan.sym_beta = np.array([tt.side_at(int(l)) for l in sym_lev], dtype=np.float64)
+    plan.sym_level = sym_lev
     _check_stencils(sym_t, sym_lev, tt, order, tol)
 
     # ---- marks (traversal.py:190-192) + downward propagation (:203-213) ---

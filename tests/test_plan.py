@@ -9,7 +9,7 @@ from conftest import golden_cases, load_case, load_ref
 from oracle import defmm_oracle as O
 from paper_2202_04894_b200.config import FmmConfig, TreeConfig
 from paper_2202_04894_b200.directions import generate_direction_tree, nearest_directions
-from paper_2202_04894_b200.plan import build_plan, canonicalize_many
+from paper_2202_04894_b200.plan import GROUP48, build_plan, canonicalize_many
 from paper_2202_04894_b200.tree import build_tree
 from paper_2202_04894_b200.workloads import make_workload
 
@@ -329,3 +329,24 @@ def test_native_traversal_is_independent_of_thread_count(monkeypatch):
         for name in ("m2l_row_slot", "m2l_row_ptr", "m2l_rows_entries", "blk_group_rows", "blk_group_ptr",
                      "blk_src", "blk_trans", "blk_mask", "p2p_ptr", "p2p_lo", "p2p_hi", "hat_slot"):
             assert np.array_equal(getattr(pl, name), getattr(outs[0], name)), name
+
+
+@pytest.mark.parametrize("L", [2, 3, 4, 5, 6, 7, 8])
+def test_spectral_layout_slices_are_closed_under_the_cube_group(L):
+    """Device spectra are stored in orbit order (defmm_spectral_layout); every
+    slice of <= 64 positions is a union of orbits of the 48 rotations
+    (fourier.py:90-143), so the slice M2L's canonical symbols stay in-slice."""
+    from paper_2202_04894_b200.fmm import spectral_layout
+
+    P = 2 * L - 1
+    forder, starts = spectral_layout(L)
+    assert np.array_equal(np.sort(forder), np.arange(P**3))
+    assert starts[0] == 0 and starts[-1] == P**3 and np.all(np.diff(starts) > 0) and np.diff(starts).max() <= 64
+    f = np.stack([forder // (P * P), (forder // P) % P, forder % P], 1)
+    pos_of = np.empty(P**3, np.int64)
+    pos_of[forder] = np.arange(P**3)
+    slice_of = np.searchsorted(starts, np.arange(P**3), side="right") - 1
+    for g in GROUP48:
+        img = (f @ g.T) % P  # signed permutation of the frequency vector mod P
+        j = img[:, 0] * P * P + img[:, 1] * P + img[:, 2]
+        assert np.array_equal(slice_of[pos_of[j]], slice_of)
