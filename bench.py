@@ -52,7 +52,7 @@ def _args():
     ap.add_argument("--dtype", default=None, choices=[None, "c128", "c64"], help="override the workload dtype")
     ap.add_argument("--p2p-overlap", default=None, choices=[None, "upward", "m2l"])
     ap.add_argument("--m2l-levels", default="hybrid",
-                    choices=["hybrid", "hybrid_rows", "blocked_all", "rows", "slice_all"])
+                    choices=["hybrid", "hybrid_rows", "blocked_all", "rows", "slice_all", "quad_all"])
     ap.add_argument("--m2l", default=None, help="M2L kernel variant (hybrid | derived | canonical)")
     return ap.parse_args()
 

@@ -122,6 +122,13 @@ void defmm_dtt_free(defmm_dtt* d);
  *   general block, 2p+v for a PLANAR block whose pairs all have a_p = b_p = v
  *   (surface data: 4x4 in-plane pairs, no predicated-off pair).  lhat[row] = sum D (*) hat  (stride
  *   defmm_spectrum_stride);  then K8 f2l_rows: local[row_slot[r]] = F2L(lhat[r]).
+ *   K7 v5 quad variant (m2l_quad): the same groups, each block split along
+ *   one axis p into quads (target layer V, source layer W) of <= 4 x 4 pairs;
+ *   quads[16q .. 16q+15] = {src[4] spectrum of in-plane source child ib (or
+ *   -1), trans[9] derived symbol of in-plane offset e = (du+1)*3 + (dw+1) (or
+ *   -1), mask16 (bit 4 ia + ib = event), code 4p + 2V + W, 0}; in-plane child
+ *   ia/ib -> octant: its 2 bits go to the other two axes in increasing order,
+ *   axis p gets V (target) / W (source).  grp_ptr spans each group's quads.
  *   K7 v4 slice variant (m2l_slice): grid = nbatch row batches x spectral slices
  *   (defmm_spectral_layout).  batch[4k..4k+3] = {row0, row1, first canonical
  *   symbol of the batch's level, that level's canonical count}; rows r in
@@ -174,6 +181,10 @@ void defmm_dtt_free(defmm_dtt* d);
                                    const int32_t* blk_trans, const int64_t* blk_mask,           \
                                    const int8_t* blk_kind, const void* hat,                     \
                                    const void* sym_derived, void* lhat, void* stream);          \
+    int defmm_m2l_quad_##SUFFIX(int32_t L, int64_t ngroups, const int64_t* grp_ptr,              \
+                                const int64_t* grp_rows, const int32_t* quads,                  \
+                                const void* hat, const void* sym_derived, void* lhat,           \
+                                void* stream);                                                  \
     int defmm_m2l_slice_##SUFFIX(int32_t L, int64_t nbatch, const int32_t* batch,                \
                                  int64_t row_base, const int64_t* seg, int32_t ngs,             \
                                  const int32_t* entries, const void* hat,                       \
@@ -204,11 +215,11 @@ void defmm_dtt_free(defmm_dtt* d);
 
 /* expands to: defmm_p2m_c128 defmm_m2m_c128 defmm_m2f_c128 defmm_symbols_c128
  * defmm_expand_symbols_c128 defmm_m2l_rows_c128 defmm_m2l_blocked_c128
- * defmm_m2l_slice_c128 defmm_f2l_rows_c128 defmm_l2l_c128 defmm_l2p_c128 defmm_p2p_c128 */
+ * defmm_m2l_quad_c128 defmm_m2l_slice_c128 defmm_f2l_rows_c128 defmm_l2l_c128 defmm_l2p_c128 defmm_p2p_c128 */
 DEFMM_DECLARE_TYPED(c128)
 /* expands to: defmm_p2m_c64 defmm_m2m_c64 defmm_m2f_c64 defmm_symbols_c64
  * defmm_expand_symbols_c64 defmm_m2l_rows_c64 defmm_m2l_blocked_c64
- * defmm_m2l_slice_c64 defmm_f2l_rows_c64 defmm_l2l_c64 defmm_l2p_c64 defmm_p2p_c64 */
+ * defmm_m2l_quad_c64 defmm_m2l_slice_c64 defmm_f2l_rows_c64 defmm_l2l_c64 defmm_l2p_c64 defmm_p2p_c64 */
 DEFMM_DECLARE_TYPED(c64)
 
 /* Spectral layout of order L (HOST call, no device needed): every spectrum is

@@ -191,18 +191,22 @@ __constant__ double2 c_tw[8][15];
 // orbits packed first-fit-decreasing into SLICES of <= SLICE_W positions.  A
 // slice is closed under every rotation, so the slice M2L can hold the
 // canonical symbols of one slice in shared memory.  g_forder[L-1][pos] =
-// natural index at a position, g_finv the inverse; the Hadamard product is
+// natural index at a position, g_finv the inverse.  All orbits but the zero
+// frequency have even size and the zero orbit sits in the last slice, so
+// every other slice starts at an even position (16-B vector loads for c64).
+// The Hadamard product is
 // order-agnostic, the kernels that touch natural indices (M2F, symbols, F2L,
 // rotations) go through these tables.
-constexpr int SLICE_W = 64;
-constexpr int MAX_SLICES = 72;
+constexpr int SLICE_W = 128;  // positions per slice: 4 per lane
+constexpr int MAX_SLICES = 40;
 constexpr int MAX_P3 = 15 * 15 * 15;
 __device__ int16_t g_forder[8][MAX_P3];
 __device__ int16_t g_finv[8][MAX_P3];
 __device__ int32_t g_slice_start[8][MAX_SLICES + 1];
-// rotation table per slice: g_rot[L-1][slice][rid][k] = slice-local position
-// of the canonical entry feeding position start + k under rotation rid
-__device__ int8_t g_rot[8][MAX_SLICES][48][SLICE_W];
+// rotation maps per slice, packed per lane: byte q of g_rot[L-1][slice][rid][lane]
+// = slice-local position of the canonical entry feeding the lane's q-th
+// position (2 lane, 2 lane + 1, 64 + 2 lane, 65 + 2 lane) under rotation rid
+__device__ uint32_t g_rot[8][MAX_SLICES][48][32];
 
 template <int L>
 __device__ __forceinline__ int forder(int pos) {
@@ -944,24 +948,149 @@ __global__ void __launch_bounds__(m2lb_threads<R, L>(), DEFMM_M2LB_MINBLOCKS) m2
 }
 
 // ---------------------------------------------------------------------------
+// K7 v5: quad M2L (surface-like levels).  Every parent-pair block (P, Q) is
+// split along one axis p into QUADS (target layer a_p = V, source layer
+// b_p = W): <= 4 x 4 pairs whose translations differ only in-plane, i.e. 4
+// spectra and <= 9 symbols feed <= 16 events from registers, with one
+// branch-free code path per (p, V, W).  A CTA owns a group = (target parent,
+// key) and keeps its <= 8 target accumulators in registers across the
+// group's quads (c64: two frequencies per thread, 16-B loads).
+// Quad descriptor (4 x int4): src[4] spectrum of in-plane source child ib
+// (or -1), trans[9] derived symbol of in-plane offset e = (du+1)*3 + (dw+1)
+// (or -1), mask16 bit 4 ia + ib, code = 4p + 2V + W.
+template <typename R>
+struct QuadVec;
+template <>
+struct QuadVec<float> {  // two complex64 per thread
+    using t = float4;
+    static constexpr int W = 2;
+};
+template <>
+struct QuadVec<double> {
+    using t = double2;
+    static constexpr int W = 1;
+};
+template <typename R, int L>
+__host__ __device__ constexpr int quad_threads() {
+    return ((spec_stride<R, L>() / QuadVec<R>::W + 31) / 32) * 32;
+}
+
+__device__ __forceinline__ void qfma(float2 (&acc)[2], const float4& d, const float4& s) {
+    acc[0] = cfma(make_float2(d.x, d.y), make_float2(s.x, s.y), acc[0]);
+    acc[1] = cfma(make_float2(d.z, d.w), make_float2(s.z, s.w), acc[1]);
+}
+__device__ __forceinline__ void qfma(double2 (&acc)[1], const double2& d, const double2& s) {
+    acc[0] = cfma(d, s, acc[0]);
+}
+
+template <int PP, int PV, int PW, typename VT, typename V, int W>
+__device__ __forceinline__ void quad_body(const int4& q0, const int4& q1, const int4& q2, const int4& q3,
+                                          const VT* hv, const VT* dv, int64_t NV, int jv, bool act,
+                                          V (&acc)[8][W]) {
+    const int src[4] = {q0.x, q0.y, q0.z, q0.w};
+    const int tr[9] = {q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w, q3.x};
+    const uint32_t mask = (uint32_t)q3.y;
+    VT S[4], D[9];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) S[i] = (src[i] >= 0 && act) ? __ldg(hv + (int64_t)src[i] * NV + jv) : VT{};
+#pragma unroll
+    for (int e = 0; e < 9; ++e) D[e] = (tr[e] >= 0 && act) ? __ldg(dv + (int64_t)tr[e] * NV + jv) : VT{};
+#pragma unroll
+    for (int ia = 0; ia < 4; ++ia)
+#pragma unroll
+        for (int ib = 0; ib < 4; ++ib) {
+            const int e = (((ia >> 1) & 1) - ((ib >> 1) & 1) + 1) * 3 + ((ia & 1) - (ib & 1) + 1);
+            if ((mask >> (4 * ia + ib)) & 1) qfma(acc[embed2(ia, PP, PV)], D[e], S[ib]);
+        }
+}
+
+template <typename R, int L>
+__global__ void __launch_bounds__(quad_threads<R, L>()) m2l_quad_kernel(
+    int64_t ngroups, const int64_t* __restrict__ grp_ptr, const int64_t* __restrict__ grp_rows,
+    const int4* __restrict__ quads, const cx<R>* __restrict__ hat, const cx<R>* __restrict__ symd,
+    cx<R>* __restrict__ lhat) {
+    using VT = typename QuadVec<R>::t;
+    using V = cx<R>;
+    constexpr int W = QuadVec<R>::W;
+    constexpr int SS = spec_stride<R, L>();
+    constexpr int NV = SS / W;
+    const int64_t g = blockIdx.x;
+    const int jv = threadIdx.x;
+    const bool act = jv < NV;
+    const VT* hv = reinterpret_cast<const VT*>(hat);
+    const VT* dv = reinterpret_cast<const VT*>(symd);
+    V acc[8][W];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int w = 0; w < W; ++w) acc[a][w] = cz<V>();
+    const int64_t q0i = grp_ptr[g], q1i = grp_ptr[g + 1];
+    for (int64_t qi = q0i; qi < q1i; ++qi) {
+        const int4 q0 = __ldg(quads + 4 * qi), q1 = __ldg(quads + 4 * qi + 1);
+        const int4 q2 = __ldg(quads + 4 * qi + 2), q3 = __ldg(quads + 4 * qi + 3);
+        switch (q3.z) {  // warp-uniform
+            case 0: quad_body<0, 0, 0>(q0, q1, q2, q3, hv, dv, NV, jv, act, acc); break;
+            case 1: quad_body<0, 0, 1>(q0, q1, q2, q3, hv, dv, NV, jv, act, acc); break;
+            case 2: quad_body<0, 1, 0>(q0, q1, q2, q3, hv, dv, NV, jv, act, acc); break;
+            case 3: quad_body<0, 1, 1>(q0, q1, q2, q3, hv, dv, NV, jv, act, acc); break;
+            case 4: quad_body<1, 0, 0>(q0, q1, q2, q3, hv, dv, NV, jv, act, acc); break;
+            case 5: quad_body<1, 0, 1>(q0, q1, q2, q3, hv, dv, NV, jv, act, acc); break;
+            case 6: quad_body<1, 1, 0>(q0, q1, q2, q3, hv, dv, NV, jv, act, acc); break;
+            case 7: quad_body<1, 1, 1>(q0, q1, q2, q3, hv, dv, NV, jv, act, acc); break;
+            case 8: quad_body<2, 0, 0>(q0, q1, q2, q3, hv, dv, NV, jv, act, acc); break;
+            case 9: quad_body<2, 0, 1>(q0, q1, q2, q3, hv, dv, NV, jv, act, acc); break;
+            case 10: quad_body<2, 1, 0>(q0, q1, q2, q3, hv, dv, NV, jv, act, acc); break;
+            default: quad_body<2, 1, 1>(q0, q1, q2, q3, hv, dv, NV, jv, act, acc); break;
+        }
+    }
+    if (act) {
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            const int64_t row = grp_rows[8 * g + a];
+            if (row >= 0) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) lhat[row * SS + (int64_t)jv * W + w] = acc[a][w];
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K7 v4: slice M2L.  Grid = (row batch, spectral slice).  The Hadamard M2L is
 // independent per frequency, and a slice is closed under the cube group, so a
 // CTA keeps the CANONICAL symbols of its level restricted to its slice in
 // shared memory (in groups of G symbols) together with the slice's 48
-// rotation maps, and streams only the source spectra (one slice = <= 64
-// contiguous entries per event, one warp per row): half the L2->SM bytes of
+// rotation maps, and streams only the source spectra (one slice = <= 128
+// entries per event, 4 per lane, one warp per row): half the L2->SM bytes of
 // the row kernel, whose derived symbols double the per-event traffic.
 // Events of a row are sorted by symbol group; the accumulated slice is kept in
-// lhat between groups (read back by the same thread).  Per event the warp
-// reads one {spectrum, canonical-in-group << 6 | rotation} entry.
+// lhat between groups (read back by the same thread).  Event entries
+// {spectrum, canonical-in-group << 6 | rotation} are loaded 32 at a time and
+// broadcast by shuffles.
 constexpr int SLICE_WARPS = 16;
 template <typename R>
 __host__ __device__ constexpr int slice_group() {
-    return sizeof(R) == 4 ? 192 : 96;  // symbols per group: G * 64 * sizeof(cx<R>) = 96 KB
+    return sizeof(R) == 4 ? 96 : 48;  // symbols per group: G * 128 * sizeof(cx<R>) = 96 KB
 }
 template <typename R>
 __host__ __device__ constexpr size_t slice_smem_bytes() {
-    return sizeof(cx<R>) * slice_group<R>() * SLICE_W + 48 * SLICE_W;
+    return sizeof(cx<R>) * slice_group<R>() * SLICE_W + 48 * 32 * sizeof(uint32_t);
+}
+
+// two adjacent complex entries (k even; 16-B aligned for c64, whose second
+// entry past an odd last slice is the zero pad of the stride)
+__device__ __forceinline__ void ld2(const float2* p, bool on, bool, float2& a, float2& b) {
+    if (on) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+        a = make_float2(v.x, v.y);
+        b = make_float2(v.z, v.w);
+    } else {
+        a = b = make_float2(0.f, 0.f);
+    }
+}
+__device__ __forceinline__ void ld2(const double2* p, bool on, bool on_b, double2& a, double2& b) {
+    a = on ? __ldg(p) : make_double2(0.0, 0.0);
+    b = on_b ? __ldg(p + 1) : make_double2(0.0, 0.0);
 }
 
 template <typename R, int L>
@@ -972,19 +1101,20 @@ __global__ void __launch_bounds__(32 * SLICE_WARPS, 2) m2l_slice_kernel(
     using V = cx<R>;
     constexpr int SS = spec_stride<R, L>();
     constexpr int G = slice_group<R>();
-    constexpr int U = sizeof(R) == 4 ? 4 : 2;  // events in flight per warp (c128: 64-register cap)
     extern __shared__ unsigned char smraw[];
-    V* sym = reinterpret_cast<V*>(smraw);                          // [G][SLICE_W]
-    int8_t* rot = reinterpret_cast<int8_t*>(sym + G * SLICE_W);    // [48][SLICE_W]
+    V* sym = reinterpret_cast<V*>(smraw);                                  // [G][SLICE_W]
+    uint32_t* rot = reinterpret_cast<uint32_t*>(sym + G * SLICE_W);        // [48][32]
     const int sl = blockIdx.y;
     const int start = g_slice_start[L - 1][sl];
     const int size = g_slice_start[L - 1][sl + 1] - start;
     const int4 bt = batch[blockIdx.x];  // {row0, row1, first canonical symbol, count}
-    const int8_t* rsrc = &g_rot[L - 1][sl][0][0];
-    for (int t = threadIdx.x; t < 48 * SLICE_W; t += blockDim.x) rot[t] = rsrc[t];
+    for (int t = threadIdx.x; t < 48 * 32; t += blockDim.x) rot[t] = g_rot[L - 1][sl][t >> 5][t & 31];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int k0 = lane, k1 = lane + 32;
-    const bool on0 = k0 < size, on1 = k1 < size;
+    // positions k0, k0+1 and k0+64, k0+65 (the last slice may be odd-sized:
+    // its pad partner is the zero pad entry of the c64 stride, or masked)
+    const int k0 = 2 * lane, k2 = 64 + 2 * lane;
+    const bool on0 = k0 < size, on2 = k2 < size;
+    const bool on1 = k0 + 1 < size, on3 = k2 + 1 < size;
     const int ng = (bt.w + G - 1) / G;
     for (int g = 0; g < ng; ++g) {
         __syncthreads();  // the previous group's symbols are consumed
@@ -1000,33 +1130,51 @@ __global__ void __launch_bounds__(32 * SLICE_WARPS, 2) m2l_slice_kernel(
             const int64_t e0 = sg[g], e1 = sg[g + 1];
             if (g > 0 && e0 == e1) continue;
             V* out = lhat + (int64_t)row * SS + start;
-            V acc[2][2];
-            acc[0][0] = (g > 0 && on0) ? out[k0] : cz<V>();
-            acc[0][1] = (g > 0 && on1) ? out[k1] : cz<V>();
-            acc[1][0] = acc[1][1] = cz<V>();
-            for (int64_t e = e0; e < e1; e += U) {
-                int2 m[U];
-                V s0[U], s1[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) m[u] = __ldg(ent + min(e + u, e1 - 1));
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const V* S = hat + (int64_t)m[u].x * SS + start;
-                    s0[u] = on0 ? __ldg(S + k0) : cz<V>();
-                    s1[u] = on1 ? __ldg(S + k1) : cz<V>();
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    if (e + u < e1) {
-                        const V* D = sym + (m[u].y >> 6) * SLICE_W;
-                        const int8_t* rr = rot + (m[u].y & 63) * SLICE_W;
-                        if (on0) acc[u & 1][0] = cfma(D[rr[k0]], s0[u], acc[u & 1][0]);
-                        if (on1) acc[u & 1][1] = cfma(D[rr[k1]], s1[u], acc[u & 1][1]);
-                    }
+            V a0, a1, a2, a3;
+            if (g > 0) {
+                a0 = on0 ? out[k0] : cz<V>();
+                a1 = on1 ? out[k0 + 1] : cz<V>();
+                a2 = on2 ? out[k2] : cz<V>();
+                a3 = on3 ? out[k2 + 1] : cz<V>();
+            } else {
+                a0 = a1 = a2 = a3 = cz<V>();
+            }
+            for (int64_t base = e0; base < e1; base += 32) {
+                const int cnt = e1 - base < 32 ? (int)(e1 - base) : 32;
+                const int2 mine = lane < cnt ? __ldg(ent + base + lane) : make_int2(0, 0);
+                for (int u = 0; u < cnt; u += 2) {
+                    // two events in flight
+                    const int sxa = __shfl_sync(0xffffffffu, mine.x, u);
+                    const int sya = __shfl_sync(0xffffffffu, mine.y, u);
+                    const bool hb = u + 1 < cnt;
+                    const int sxb = __shfl_sync(0xffffffffu, mine.x, hb ? u + 1 : u);
+                    const int syb = __shfl_sync(0xffffffffu, mine.y, hb ? u + 1 : u);
+                    const V* SA = hat + (int64_t)sxa * SS + start;
+                    const V* SB = hat + (int64_t)sxb * SS + start;
+                    V xa0, xa1, xa2, xa3, xb0, xb1, xb2, xb3;
+                    ld2(SA + k0, on0, on1, xa0, xa1);
+                    ld2(SA + k2, on2, on3, xa2, xa3);
+                    ld2(SB + k0, on0 && hb, on1 && hb, xb0, xb1);
+                    ld2(SB + k2, on2 && hb, on3 && hb, xb2, xb3);
+                    const uint32_t ra = rot[(sya & 63) * 32 + lane];
+                    const uint32_t rb = rot[(syb & 63) * 32 + lane];
+                    const V* DA = sym + (sya >> 6) * SLICE_W;
+                    const V* DB = sym + (syb >> 6) * SLICE_W;
+                    a0 = cfma(DA[ra & 0xff], xa0, a0);
+                    a1 = cfma(DA[(ra >> 8) & 0xff], xa1, a1);
+                    a2 = cfma(DA[(ra >> 16) & 0xff], xa2, a2);
+                    a3 = cfma(DA[ra >> 24], xa3, a3);
+                    // event b (zeros when absent: its spectrum loads were masked)
+                    a0 = cfma(DB[rb & 0xff], xb0, a0);
+                    a1 = cfma(DB[(rb >> 8) & 0xff], xb1, a1);
+                    a2 = cfma(DB[(rb >> 16) & 0xff], xb2, a2);
+                    a3 = cfma(DB[rb >> 24], xb3, a3);
                 }
             }
-            if (on0) out[k0] = from_d<V>(cadd(to_d(acc[0][0]), to_d(acc[1][0])));
-            if (on1) out[k1] = from_d<V>(cadd(to_d(acc[0][1]), to_d(acc[1][1])));
+            if (on0) out[k0] = a0;
+            if (on1) out[k0 + 1] = a1;
+            if (on2) out[k2] = a2;
+            if (on3) out[k2 + 1] = a3;
         }
     }
 }
@@ -1530,7 +1678,7 @@ struct HostLayout {
     int P3 = 0, nslices = 0;
     std::vector<int16_t> forder, finv;
     std::vector<int32_t> start;
-    std::vector<int8_t> rot;  // [slice][48][SLICE_W]
+    std::vector<uint32_t> rot;  // [slice][48][32 lanes], 4 packed slice-local positions
 };
 
 // orbit-ordered spectral layout of order L (see g_forder): orbits keyed by the
@@ -1559,8 +1707,9 @@ HostLayout make_layout(int L) {
                 }
                 orbits[orbit_of_key[k]].push_back(j);
             }
-    std::vector<int> order(orbits.size());
-    for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+    // orbit 0 = the zero frequency (key 0): packed last, alone at the end
+    std::vector<int> order;
+    for (size_t i = 1; i < orbits.size(); ++i) order.push_back((int)i);
     std::stable_sort(order.begin(), order.end(),
                      [&](int x, int y) { return orbits[x].size() > orbits[y].size(); });
     std::vector<std::vector<int>> bins;
@@ -1576,6 +1725,18 @@ HostLayout make_layout(int L) {
         bins[b].push_back(o);
         fill[b] += sz;
     }
+    // the zero orbit goes into the least-filled bin, which is moved last
+    size_t zb = 0;
+    for (size_t b = 1; b < bins.size(); ++b)
+        if (fill[b] < fill[zb]) zb = b;
+    if (bins.empty() || fill[zb] + 1 > SLICE_W) {
+        bins.emplace_back();
+        fill.push_back(0);
+        zb = bins.size() - 1;
+    }
+    bins[zb].push_back(0);
+    fill[zb] += 1;
+    std::rotate(bins.begin() + zb, bins.begin() + zb + 1, bins.end());
     H.nslices = (int)bins.size();
     H.forder.resize(P3);
     H.finv.resize(P3);
@@ -1587,12 +1748,19 @@ HostLayout make_layout(int L) {
         H.start.push_back(pos);
     }
     for (int t = 0; t < P3; ++t) H.finv[H.forder[t]] = (int16_t)t;
-    H.rot.assign((size_t)H.nslices * 48 * SLICE_W, 0);
+    H.rot.assign((size_t)H.nslices * 48 * 32, 0);
     for (int sl = 0; sl < H.nslices; ++sl)
         for (int rid = 0; rid < 48; ++rid)
-            for (int k = 0; k < H.start[sl + 1] - H.start[sl]; ++k) {
-                const int p = H.finv[host_rotated_index(P, H.forder[H.start[sl] + k], rid)];
-                H.rot[((size_t)sl * 48 + rid) * SLICE_W + k] = (int8_t)(p - H.start[sl]);
+            for (int lane = 0; lane < 32; ++lane) {
+                uint32_t w = 0;
+                for (int q = 0; q < 4; ++q) {
+                    const int k = (q >> 1) * 64 + 2 * lane + (q & 1);
+                    int loc = 0;
+                    if (k < H.start[sl + 1] - H.start[sl])
+                        loc = H.finv[host_rotated_index(P, H.forder[H.start[sl] + k], rid)] - H.start[sl];
+                    w |= (uint32_t)(loc & 0xff) << (8 * q);
+                }
+                H.rot[((size_t)sl * 48 + rid) * 32 + lane] = w;
             }
     return H;
 }
@@ -1624,7 +1792,8 @@ int ensure_twiddles() {
                                            o * (MAX_SLICES + 1) * sizeof(int32_t)),
                         "cudaMemcpyToSymbol(g_slice_start)");
         if (!rc)
-            rc = report(cudaMemcpyToSymbol(g_rot, H.rot.data(), H.rot.size(), o * MAX_SLICES * 48 * SLICE_W),
+            rc = report(cudaMemcpyToSymbol(g_rot, H.rot.data(), H.rot.size() * sizeof(uint32_t),
+                                           o * MAX_SLICES * 48 * 32 * sizeof(uint32_t)),
                         "cudaMemcpyToSymbol(g_rot)");
         if (rc) return rc;
     }
@@ -1789,6 +1958,18 @@ int launch_m2l_blocked(int32_t L, int64_t ngroups, const int64_t* grp_ptr, const
 }
 
 template <typename R>
+int launch_m2l_quad(int32_t L, int64_t ngroups, const int64_t* grp_ptr, const int64_t* grp_rows,
+                    const int32_t* quads, const void* hat, const void* symd, void* lhat, void* stream) {
+    if (ngroups == 0) return 0;
+    if (!grid_ok(ngroups)) return -1;
+    cudaStream_t s = (cudaStream_t)stream;
+    DEFMM_DISPATCH_L(L, (m2l_quad_kernel<R, LL><<<(unsigned)ngroups, quad_threads<R, LL>(), 0, s>>>(
+                            ngroups, grp_ptr, grp_rows, (const int4*)quads, (const cx<R>*)hat,
+                            (const cx<R>*)symd, (cx<R>*)lhat)));
+    return report(cudaGetLastError(), "m2l_quad");
+}
+
+template <typename R>
 int launch_m2l_slice(int32_t L, int64_t nbatch, const int32_t* batch, int64_t row_base, const int64_t* seg,
                      int32_t ngs, const int32_t* entries, const void* hat, const void* symc, void* lhat,
                      void* stream) {
@@ -1927,6 +2108,11 @@ const char* defmm_last_error(void) { return g_last_error; }
                                    void* stream) {                                                                \
         return launch_m2l_blocked<R>(L, ngroups, grp_ptr, grp_rows, blk_src, blk_trans, blk_mask, blk_kind, hat,   \
                                      sym_derived, lhat, stream);                                                  \
+    }                                                                                                               \
+    int defmm_m2l_quad_##SUFFIX(int32_t L, int64_t ngroups, const int64_t* grp_ptr, const int64_t* grp_rows,        \
+                                const int32_t* quads, const void* hat, const void* sym_derived, void* lhat,        \
+                                void* stream) {                                                                    \
+        return launch_m2l_quad<R>(L, ngroups, grp_ptr, grp_rows, quads, hat, sym_derived, lhat, stream);           \
     }                                                                                                               \
     int defmm_m2l_slice_##SUFFIX(int32_t L, int64_t nbatch, const int32_t* batch, int64_t row_base,               \
                                  const int64_t* seg, int32_t ngs, const int32_t* entries, const void* hat,         \

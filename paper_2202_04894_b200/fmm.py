@@ -28,6 +28,95 @@ def _dev(a, dtype, device):
     return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype).to(device)
 
 
+def _quad_tables():
+    """Per (p, V, W): pair-bit mask of the quad, and per in-plane (ia, ib) the
+    block pair bit 8a+b, per in-plane offset e its block child offset d."""
+    def embed2(i, pp, v):
+        return (v << 2) | i if pp == 0 else (((i >> 1) & 1) << 2) | (v << 1) | (i & 1) if pp == 1 else (i << 1) | v
+
+    def d3(a, b):
+        return ((((a >> 2) & 1) - ((b >> 2) & 1)) + 1) * 9 + ((((a >> 1) & 1) - ((b >> 1) & 1)) + 1) * 3 + \
+            (((a & 1) - (b & 1)) + 1)
+
+    out = {}
+    for pp in range(3):
+        for v in range(2):
+            for w in range(2):
+                bit = np.zeros((4, 4), np.int64)
+                qm = 0
+                d_of_e = np.zeros(9, np.int64)
+                for ia in range(4):
+                    for ib in range(4):
+                        a, b = embed2(ia, pp, v), embed2(ib, pp, w)
+                        bit[ia, ib] = 8 * a + b
+                        qm |= 1 << (8 * a + b)
+                        e = (((ia >> 1) & 1) - ((ib >> 1) & 1) + 1) * 3 + ((ia & 1) - (ib & 1) + 1)
+                        d_of_e[e] = d3(a, b)
+                out[(pp, v, w)] = (np.uint64(qm), bit, d_of_e, [embed2(ib, pp, w) for ib in range(4)])
+    return out
+
+
+_QUAD_TABLES = None
+
+
+def _quads(bsrc, btr, bmask, gptr):
+    """Quad descriptors (defmm_m2l_quad_*) of every block: split along the axis
+    giving the fewest non-empty quads; quads ordered (block, V, W)."""
+    global _QUAD_TABLES
+    if _QUAD_TABLES is None:
+        _QUAD_TABLES = _quad_tables()
+    T = _QUAD_TABLES
+    nb = bmask.shape[0]
+    m = bmask.view(np.uint64)
+    cnt = np.stack([sum(((m & T[(pp, v, w)][0]) != 0).astype(np.int64) for v in range(2) for w in range(2))
+                    for pp in range(3)]) if nb else np.zeros((3, 0), np.int64)
+    best = np.argmin(cnt, axis=0) if nb else np.zeros(0, np.int64)
+    parts, keys = [], []
+    for pp in range(3):
+        bsel = np.nonzero(best == pp)[0]
+        if bsel.size == 0:
+            continue
+        mb = m[bsel]
+        for v in range(2):
+            for w in range(2):
+                qm, bit, d_of_e, b_of = T[(pp, v, w)]
+                ne = (mb & qm) != 0
+                blk = bsel[ne]
+                if blk.size == 0:
+                    continue
+                mm = mb[ne]
+                q = np.full((blk.shape[0], 16), -1, np.int32)
+                m16 = np.zeros(blk.shape[0], np.int64)
+                for ia in range(4):
+                    for ib in range(4):
+                        m16 |= ((mm >> np.uint64(bit[ia, ib])) & np.uint64(1)).astype(np.int64) << (4 * ia + ib)
+                for ib in range(4):
+                    used = (m16 >> ib) & 0x1111
+                    q[:, ib] = np.where(used != 0, bsrc[blk, b_of[ib]], -1)
+                for e in range(9):
+                    du, dw = e // 3 - 1, e % 3 - 1
+                    em = 0
+                    for ia in range(4):
+                        for ib in range(4):
+                            if ((ia >> 1) & 1) - ((ib >> 1) & 1) == du and (ia & 1) - (ib & 1) == dw:
+                                em |= 1 << (4 * ia + ib)
+                    q[:, 4 + e] = np.where((m16 & em) != 0, btr[blk, d_of_e[e]], -1)
+                q[:, 13] = m16
+                q[:, 14] = 4 * pp + 2 * v + w
+                q[:, 15] = 0
+                parts.append(q)
+                keys.append(blk * 4 + 2 * v + w)
+    if not parts:
+        return np.zeros((0, 16), np.int32), np.zeros(gptr.shape[0], np.int64)
+    q = np.concatenate(parts)
+    k = np.concatenate(keys)
+    o = np.argsort(k, kind="stable")
+    q, k = q[o], k[o]
+    qblk = k // 4
+    qptr = np.searchsorted(qblk, gptr).astype(np.int64)  # block range per group -> quad range
+    return q, qptr
+
+
 def _rows_to_ids(slots, rows):
     """Local slots -> index into the sorted row-slot list ``rows`` (-1 if absent)."""
     slots = np.asarray(slots)
@@ -175,6 +264,10 @@ class FmmPlan:
         self.blk_trans = _dev(h["blk_trans"].reshape(-1), i32, d)
         self.blk_mask = _dev(h["blk_mask"], i64, d)
         self.blk_kind = _dev(h["blk_kind"], torch.int8, d)
+        self.n_qgroups = int(h["qd_rows"].shape[0])
+        self.qd_ptr = _dev(h["qd_ptr"], i64, d)
+        self.qd_rows = _dev(h["qd_rows"].reshape(-1), i64, d)
+        self.quads = _dev(h["quads"].reshape(-1), i32, d)
         sl = h["slice"]
         self.n_slice_batch = int(sl["n_batch"])
         self.sl_batch = _dev(sl["batch"].reshape(-1), i32, d)
@@ -257,7 +350,7 @@ class FmmPlan:
             if ev[sel].mean() >= self.BLOCKED_MIN_EVENTS_PER_BLOCK:
                 dense.add(int(lev))
         mode = self.m2l_variant_default
-        if mode in ("rows", "slice_all"):
+        if mode in ("rows", "slice_all", "quad_all"):
             dense = set()
         elif mode == "blocked_all":
             dense = set(int(x) for x in np.unique(blev))
@@ -267,23 +360,45 @@ class FmmPlan:
         keep_rows, rptr, rsel = _sub_csr(h["row_ptr"], ~is_dense)
         sparse_rows = rows[~is_dense]
         z = np.zeros(0, np.int64)
+        no_slice = self._slice_lists(np.zeros(1, np.int64), np.zeros((0, 2), np.int32), z, 0)
+        h["rk_rows"], h["rk_ptr"], h["rk_ent"] = z, np.zeros(1, np.int64), np.zeros((0, 2), np.int32)
+        h["slice"] = no_slice
+        quad = mode in ("hybrid", "quad_all")
         if mode in ("rows", "hybrid_rows"):
             h["rk_rows"], h["rk_ptr"], h["rk_ent"] = sparse_rows, rptr, h["ent"][rsel]
-            h["slice"] = self._slice_lists(np.zeros(1, np.int64), np.zeros((0, 2), np.int32), z, 0)
-        else:
-            h["rk_rows"], h["rk_ptr"], h["rk_ent"] = z, np.zeros(1, np.int64), np.zeros((0, 2), np.int32)
-            h["slice"] = self._slice_lists(rptr, h["ent"][rsel], rlev[~is_dense], int(dense_rows.shape[0]))
+        elif mode == "slice_all":
+            h["slice"] = self._slice_lists(rptr, h["ent"][rsel], rlev[~is_dense], 0)
+        if quad:  # sparse levels -> quad kernel over the blocks of their groups
+            is_dense = np.ones(rows.shape[0], bool)
+            dense_rows = rows
         # groups of dense levels -> blocked kernel, rows renumbered into lhat
         gr = h["grp_rows"]
         gr_slots = np.where(gr >= 0, rows[np.maximum(gr, 0)] if rows.size else -1, -1)
         gid = _rows_to_ids(gr_slots, dense_rows)
         gkeep = np.any(gid >= 0, axis=1)
         _, gptr, bsel = _sub_csr(h["grp_ptr"], gkeep)
-        # lhat rows: blocked rows, then slice rows (one F2L launch for both)
+        # lhat rows: blocked (+ quad) rows, then slice rows (one F2L launch)
         h["bk_rows"] = np.concatenate([dense_rows, sparse_rows if h["slice"]["n_batch"] else z])
-        h["grp_ptr"], h["grp_rows"] = gptr, gid[gkeep]
-        h["blk_src"], h["blk_trans"], h["blk_mask"] = h["blk_src"][bsel], h["blk_trans"][bsel], h["blk_mask"][bsel]
-        h["blk_kind"] = h["blk_kind"][bsel]
+        gptr, grows = gptr, gid[gkeep]
+        bsrc, btr, bmask, bkind = h["blk_src"][bsel], h["blk_trans"][bsel], h["blk_mask"][bsel], h["blk_kind"][bsel]
+        if quad:
+            # groups whose level is dense keep the blocked kernel, the others -> quads
+            glev = np.full(grows.shape[0], -1, np.int64)
+            first = np.where(grows >= 0, grows, np.iinfo(np.int64).max).min(axis=1) if grows.size else z
+            if grows.size:
+                glev = tt.level[p.l_cell[dense_rows[first]]]
+            gd = np.isin(glev, list(dense)) if dense else np.zeros(grows.shape[0], bool)
+            _, dptr, dsel = _sub_csr(gptr, gd)
+            _, qgptr, qsel = _sub_csr(gptr, ~gd)
+            quads, qptr = _quads(bsrc[qsel], btr[qsel], bmask[qsel], qgptr)
+            h["qd_ptr"], h["qd_rows"], h["quads"] = qptr, grows[~gd], quads
+            gptr, grows = dptr, grows[gd]
+            bsrc, btr, bmask, bkind = bsrc[dsel], btr[dsel], bmask[dsel], bkind[dsel]
+        else:
+            h["qd_ptr"], h["qd_rows"], h["quads"] = np.zeros(1, np.int64), np.zeros((0, 8), np.int64), \
+                np.zeros((0, 16), np.int32)
+        h["grp_ptr"], h["grp_rows"] = gptr, grows
+        h["blk_src"], h["blk_trans"], h["blk_mask"], h["blk_kind"] = bsrc, btr, bmask, bkind
         self.dense_levels = sorted(dense)
         return h
 
@@ -487,6 +602,8 @@ class FmmPlan:
                       self.hat, self.sym_derived, self.local, sh)
             _lib.call(self._op("m2l_blocked"), L, self.n_groups, self.grp_ptr, self.grp_rows, self.blk_src,
                       self.blk_trans, self.blk_mask, self.blk_kind, self.hat, self.sym_derived, self.lhat, sh)
+            _lib.call(self._op("m2l_quad"), L, self.n_qgroups, self.qd_ptr, self.qd_rows, self.quads, self.hat,
+                      self.sym_derived, self.lhat, sh)
             _lib.call(self._op("m2l_slice"), L, self.n_slice_batch, self.sl_batch, self.sl_row_base, self.sl_seg,
                       self.sl_ngs, self.sl_ent, self.hat, self.sym, self.lhat, sh)
             _lib.call(self._op("f2l_rows"), L, self.bk_rows.shape[0], self.bk_rows, self.lhat, self.local, sh)
@@ -554,8 +671,8 @@ class FmmPlan:
         """Kernels of one matvec: p2p (+ split reduce), p2m, m2m per level, m2f,
         the M2L kernels with work, l2l per level, l2p."""
         if self.m2l_variant == "hybrid":
-            m2l = sum(int(n > 0) for n in (self.rk_rows.shape[0], self.n_groups, self.n_slice_batch,
-                                           self.bk_rows.shape[0]))
+            m2l = sum(int(n > 0) for n in (self.rk_rows.shape[0], self.n_groups, self.n_qgroups,
+                                           self.n_slice_batch, self.bk_rows.shape[0]))
         else:
             m2l = 1
         return 4 + (1 if self.n_split else 0) + len(self.m2m) + len(self.l2l) + m2l

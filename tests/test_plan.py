@@ -334,14 +334,14 @@ def test_native_traversal_is_independent_of_thread_count(monkeypatch):
 @pytest.mark.parametrize("L", [2, 3, 4, 5, 6, 7, 8])
 def test_spectral_layout_slices_are_closed_under_the_cube_group(L):
     """Device spectra are stored in orbit order (defmm_spectral_layout); every
-    slice of <= 64 positions is a union of orbits of the 48 rotations
+    slice of <= 128 positions is a union of orbits of the 48 rotations
     (fourier.py:90-143), so the slice M2L's canonical symbols stay in-slice."""
     from paper_2202_04894_b200.fmm import spectral_layout
 
     P = 2 * L - 1
     forder, starts = spectral_layout(L)
     assert np.array_equal(np.sort(forder), np.arange(P**3))
-    assert starts[0] == 0 and starts[-1] == P**3 and np.all(np.diff(starts) > 0) and np.diff(starts).max() <= 64
+    assert starts[0] == 0 and starts[-1] == P**3 and np.all(np.diff(starts) > 0) and np.diff(starts).max() <= 128
     f = np.stack([forder // (P * P), (forder // P) % P, forder % P], 1)
     pos_of = np.empty(P**3, np.int64)
     pos_of[forder] = np.arange(P**3)
@@ -350,3 +350,39 @@ def test_spectral_layout_slices_are_closed_under_the_cube_group(L):
         img = (f @ g.T) % P  # signed permutation of the frequency vector mod P
         j = img[:, 0] * P * P + img[:, 1] * P + img[:, 2]
         assert np.array_equal(slice_of[pos_of[j]], slice_of)
+
+
+@pytest.mark.parametrize("case", ["cubesurf4000", "volume3000"])
+def test_quads_reconstruct_every_block_pair(case):
+    """Quad descriptors (defmm_m2l_quad_*) carry exactly the (group, target
+    child, spectrum, derived symbol) events of the parent-pair blocks."""
+    from paper_2202_04894_b200.fmm import _quads
+
+    def embed2(i, pp, v):
+        return (v << 2) | i if pp == 0 else (((i >> 1) & 1) << 2) | (v << 1) | (i & 1) if pp == 1 else (i << 1) | v
+
+    g = load_case(case)
+    tr, ps, pl = _plan(g)
+    q, qptr = _quads(pl.blk_src, pl.blk_trans, pl.blk_mask, pl.blk_group_ptr)
+    assert qptr[0] == 0 and qptr[-1] == q.shape[0] and np.all(np.diff(qptr) >= 0)
+    qg = np.searchsorted(qptr, np.arange(q.shape[0]), side="right") - 1
+    got = []
+    for k in range(q.shape[0]):
+        code = int(q[k, 14])
+        pp, v = code // 4, (code >> 1) & 1
+        for ia in range(4):
+            for ib in range(4):
+                if (int(q[k, 13]) >> (4 * ia + ib)) & 1:
+                    e = (((ia >> 1) & 1) - ((ib >> 1) & 1) + 1) * 3 + ((ia & 1) - (ib & 1) + 1)
+                    got.append((int(qg[k]), embed2(ia, pp, v), int(q[k, ib]), int(q[k, 4 + e])))
+    bg = np.searchsorted(pl.blk_group_ptr, np.arange(pl.blk_mask.shape[0]), side="right") - 1
+    ref = []
+    for bi in range(pl.blk_mask.shape[0]):
+        m = int(pl.blk_mask[bi])
+        for a in range(8):
+            for b in range(8):
+                if (m >> (8 * a + b)) & 1:
+                    d = ((((a >> 2) & 1) - ((b >> 2) & 1)) + 1) * 9 + ((((a >> 1) & 1) - ((b >> 1) & 1)) + 1) * 3 + \
+                        (((a & 1) - (b & 1)) + 1)
+                    ref.append((int(bg[bi]), a, int(pl.blk_src[bi, b]), int(pl.blk_trans[bi, d])))
+    assert sorted(got) == sorted(ref)
