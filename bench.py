@@ -50,8 +50,8 @@ def _args():
     ap.add_argument("--no-secondary", action="store_true", help="skip the other-precision run of the same lists")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of the CUDA graph")
     ap.add_argument("--dtype", default=None, choices=[None, "c128", "c64"], help="override the workload dtype")
-    ap.add_argument("--p2p-overlap", default=None, choices=[None, "upward", "m2l"])
-    ap.add_argument("--m2l-levels", default="hybrid",
+    ap.add_argument("--p2p-overlap", default=None, choices=[None, "upward", "m2l", "full"])
+    ap.add_argument("--m2l-levels", default="hybrid_rows",
                     choices=["hybrid", "hybrid_rows", "blocked_all", "rows", "slice_all", "quad_all"])
     ap.add_argument("--m2l", default=None, help="M2L kernel variant (hybrid | derived | canonical)")
     return ap.parse_args()
@@ -135,13 +135,13 @@ class _Clocks:
 
 
 def _ncu_traffic(key):
-    """dram read+write bytes of one launch from the committed ncu --set full
-    capture (profiles/r01_ncu_full_v2_metrics.json), or None."""
+    """DRAM read+write bytes of the M2L stage kernels of one matvec, from the
+    committed ncu launch list of the same workload (profiles/r01_m2l_traffic.json,
+    written by tools/ncu_to_json.py from tools/profile_gpu.sh), or None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_full_v2_metrics.json")) as fh:
-            rec = json.load(fh)[key]
-        return rec["dram__bytes_read.sum"] + rec["dram__bytes_write.sum"]
-    except (OSError, KeyError, ValueError):
+        with open(os.path.join(ROOT, "profiles", "r01_m2l_traffic.json")) as fh:
+            return float(json.load(fh)[key]["dram_bytes"])
+    except (OSError, KeyError, ValueError, TypeError):
         return None
 
 
@@ -333,7 +333,10 @@ def run_b200(args):
     st2 = None
     if not args.no_secondary:
         plan2 = FmmPlan(pts, None, FmmConfig(order=w.order, ncrit=w.ncrit, kappa=kappa, dtype=other),
-                        device=dev, charges=q, reuse=plan, shard=shard, allreduce=allreduce if shard else None)
+                        device=dev, charges=q, reuse=plan, shard=shard, allreduce=allreduce if shard else None,
+                        m2l=args.m2l_levels)
+        if args.p2p_overlap:
+            plan2.p2p_overlap = args.p2p_overlap
         st2 = _measure(plan2, args.steps, args.warmup, flush, barrier, dist_max)
         del plan2
     clk = clocks.stop()
@@ -367,11 +370,8 @@ def run_b200(args):
     rows = p.m2l_row_slot.shape[0]
     alg_bytes = n_m2l * 2 * P3 * c + rows * L**3 * c  # symbol + source spectrum per event, local write
     m2l_s = st["m2l"] / 1e3
-    kname = f"m2l_rows_kernel<{'float' if dtype == 'c64' else 'double'}, {L}>"
-    if plan.dense_levels:  # hybrid: some levels run the blocked kernel + F2L
-        kname = (f"M2L stage: {kname} (levels {sorted(set(range(plan.tt.depth + 1)) - set(plan.dense_levels))}) + "
-                 f"m2l_blocked_kernel + f2l_rows_kernel (levels {plan.dense_levels})")
-    traffic = _ncu_traffic(f"{dtype}:{kname}") if args.workload in ("cfg2",) and not plan.dense_levels else None
+    kname = "M2L stage: " + " + ".join(plan.m2l_kernels())
+    traffic = _ncu_traffic(f"{args.workload}:{dtype}:m2l")
     peak, peak_kind = _measured_peak_hbm()
     achieved = alg_bytes / m2l_s / 1e9
     line = {
@@ -399,7 +399,7 @@ def run_b200(args):
                      "frac": achieved / peak, "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
                      "kernel_ms": st["m2l"],
                      "note": "algorithmic bytes = 2 spectra per M2L event + local write; frac > 1 = L2 reuse; "
-                             "traffic = ncu dram bytes of one launch (profiles/r01_ncu_full_v2_metrics.json)"},
+                             "traffic = ncu dram bytes of the M2L-stage launches of one matvec (profiles/r01_m2l_traffic.json)"},
         "e2e": {"value": n / (e_step / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(qbytes),
                 "d2h_bytes_per_step": int(qbytes), "ms_per_step": e_step},
         "accuracy": {"rel_l2_vs_direct_1000": eps, "eps_ref_reference": _EPS_REF.get(args.workload)},

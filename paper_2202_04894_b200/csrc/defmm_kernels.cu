@@ -970,9 +970,15 @@ struct QuadVec<double> {
     using t = double2;
     static constexpr int W = 1;
 };
+// the spectrum is split over gridDim.y chunks of <= 384 vector lanes (L >= 5
+// c128 spectra exceed one CTA's 1024 threads)
+template <typename R, int L>
+__host__ __device__ constexpr int quad_chunks() {
+    return (spec_stride<R, L>() / QuadVec<R>::W + 383) / 384;
+}
 template <typename R, int L>
 __host__ __device__ constexpr int quad_threads() {
-    return ((spec_stride<R, L>() / QuadVec<R>::W + 31) / 32) * 32;
+    return ((spec_stride<R, L>() / QuadVec<R>::W + quad_chunks<R, L>() - 1) / quad_chunks<R, L>() + 31) / 32 * 32;
 }
 
 __device__ __forceinline__ void qfma(float2 (&acc)[2], const float4& d, const float4& s) {
@@ -1015,7 +1021,7 @@ __global__ void __launch_bounds__(quad_threads<R, L>()) m2l_quad_kernel(
     constexpr int SS = spec_stride<R, L>();
     constexpr int NV = SS / W;
     const int64_t g = blockIdx.x;
-    const int jv = threadIdx.x;
+    const int jv = blockIdx.y * quad_threads<R, L>() + threadIdx.x;
     const bool act = jv < NV;
     const VT* hv = reinterpret_cast<const VT*>(hat);
     const VT* dv = reinterpret_cast<const VT*>(symd);
@@ -1963,7 +1969,7 @@ int launch_m2l_quad(int32_t L, int64_t ngroups, const int64_t* grp_ptr, const in
     if (ngroups == 0) return 0;
     if (!grid_ok(ngroups)) return -1;
     cudaStream_t s = (cudaStream_t)stream;
-    DEFMM_DISPATCH_L(L, (m2l_quad_kernel<R, LL><<<(unsigned)ngroups, quad_threads<R, LL>(), 0, s>>>(
+    DEFMM_DISPATCH_L(L, (m2l_quad_kernel<R, LL><<<dim3((unsigned)ngroups, quad_chunks<R, LL>()), quad_threads<R, LL>(), 0, s>>>(
                             ngroups, grp_ptr, grp_rows, (const int4*)quads, (const cx<R>*)hat,
                             (const cx<R>*)symd, (cx<R>*)lhat)));
     return report(cudaGetLastError(), "m2l_quad");

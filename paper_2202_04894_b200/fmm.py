@@ -144,7 +144,7 @@ class FmmPlan:
 
     def __init__(self, targets, sources=None, config: FmmConfig = FmmConfig(), device="cuda",
                  keep_events: bool = False, charges=None, reuse: "FmmPlan | None" = None,
-                 shard=None, allreduce=None, m2l: str = "hybrid"):
+                 shard=None, allreduce=None, m2l: str = "hybrid_rows"):
         """``reuse``: share the host tree + lists of an existing plan built for
         the same geometry and (order, ncrit, eta, kappa) -- e.g. to run the same
         lists at another storage precision.
@@ -566,7 +566,7 @@ class FmmPlan:
         L, kappa, sg = self.L, float(self.plan.kappa), self.sg
         stream = torch.cuda.current_stream(self.device)
         sh = stream.cuda_stream
-        if self.p2p_overlap == "upward":
+        if self.p2p_overlap in ("upward", "full"):
             self._near_field(stage_events)
         if stage_events is not None:
             self._ev_a = torch.cuda.Event(enable_timing=True)
@@ -587,10 +587,11 @@ class FmmPlan:
         out = self.out if out is None else out
         ev = (lambda: torch.cuda.Event(enable_timing=True)) if stage_events is not None else None
         _lib.call(self._op("m2f"), L, self.n_hat, self.hat_slot, self.mult, self.hat, sh)
-        if self.p2p_overlap != "upward":
+        if self.p2p_overlap == "m2l":
             self._near_field(stage_events)
-        else:
+        elif self.p2p_overlap == "upward":
             stream.wait_stream(self.side_stream)  # M2L runs alone (clean roofline timing)
+        # "full": P2P spans the upward pass and the M2L, joined before L2P
         if stage_events is not None:
             b = ev()
             b.record(stream)
@@ -665,6 +666,21 @@ class FmmPlan:
         """Matvec via the captured CUDA graph; returns ``self.out``."""
         self.graph.replay()
         return self.out
+
+    def m2l_kernels(self) -> list:
+        """Names of the M2L-stage kernels one matvec launches (with their levels)."""
+        R = "float" if self.config.dtype == "c64" else "double"
+        if self.m2l_variant != "hybrid":
+            return [f"m2l_rows_kernel<{R}, {self.L}> (all levels, {self.m2l_variant})"]
+        dense = list(self.dense_levels)
+        sparse = sorted(set(range(self.tt.depth + 1)) - set(dense))
+        out = []
+        for n, name, lev in ((self.rk_rows.shape[0], "m2l_rows_kernel", sparse), (self.n_groups, "m2l_blocked_kernel", dense),
+                             (self.n_qgroups, "m2l_quad_kernel", sparse), (self.n_slice_batch, "m2l_slice_kernel", sparse),
+                             (self.bk_rows.shape[0], "f2l_rows_kernel", None)):
+            if n:
+                out.append(f"{name}<{R}, {self.L}>" + (f" (levels {lev})" if lev is not None else ""))
+        return out
 
     @property
     def launches_per_apply(self) -> int:
