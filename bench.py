@@ -51,6 +51,8 @@ def _args():
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of the CUDA graph")
     ap.add_argument("--dtype", default=None, choices=[None, "c128", "c64"], help="override the workload dtype")
     ap.add_argument("--p2p-overlap", default=None, choices=[None, "upward", "m2l", "full"])
+    ap.add_argument("--p2p-grid", type=int, default=None, help="persistent P2P grid (CTAs; 0 = one per item)")
+    ap.add_argument("--far-priority", type=int, default=None, help="far field on a high-priority stream (1/0)")
     ap.add_argument("--m2l-levels", default="hybrid_rows",
                     choices=["hybrid", "hybrid_rows", "blocked_all", "rows", "slice_all", "quad_all"])
     ap.add_argument("--m2l", default=None, help="M2L kernel variant (hybrid | derived | canonical)")
@@ -322,6 +324,10 @@ def run_b200(args):
         plan.m2l_variant = args.m2l
     if args.p2p_overlap:
         plan.p2p_overlap = args.p2p_overlap
+    if args.p2p_grid is not None:
+        plan.p2p_grid = args.p2p_grid
+    if args.far_priority is not None:
+        plan.far_priority = bool(args.far_priority)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
 
     clocks = _Clocks(local)
@@ -337,6 +343,10 @@ def run_b200(args):
                         m2l=args.m2l_levels)
         if args.p2p_overlap:
             plan2.p2p_overlap = args.p2p_overlap
+        if args.p2p_grid is not None:
+            plan2.p2p_grid = args.p2p_grid
+        if args.far_priority is not None:
+            plan2.far_priority = bool(args.far_priority)
         st2 = _measure(plan2, args.steps, args.warmup, flush, barrier, dist_max)
         del plan2
     clk = clocks.stop()

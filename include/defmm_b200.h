@@ -152,7 +152,12 @@ void defmm_dtt_free(defmm_dtt* d);
  *   item_out[i] < 0 (the leaf's only item), else into
  *   partial[item_out[i] + p - tgt_lo[l]]; the n_split split leaves are then
  *   reduced in item order: near[p] = sum_{m < split_n} partial[split_base + m*nt + ...].
- *   Targets t*, sources s* (the same arrays in single-tree mode).
+ *   Targets t*, sources s* (the same arrays in single-tree mode).  grid > 0 launches
+ *   a persistent grid of `grid` CTAs striding over the items (so the P2P leaves SM
+ *   room for the far-field kernels running concurrently on another stream);
+ *   grid = 0 launches one CTA per item.  Results do not depend on grid.  hilo
+ *   (c64 only): 1 = hi/lo float pairs of the target-relative coordinates
+ *   (accuracy for L >= 6), 0 = single floats (cheaper; L <= 5).
  */
 #define DEFMM_DECLARE_TYPED(SUFFIX)                                                              \
     int defmm_p2m_##SUFFIX(int32_t L, int64_t n, const int32_t* cell, const int32_t* dir,        \
@@ -211,7 +216,8 @@ void defmm_dtt_free(defmm_dtt* d);
                            const double* sy, const double* sz, const void* q, double kappa,     \
                            double tol, void* near, void* partial, int64_t n_split,              \
                            const int32_t* split_leaf, const int64_t* split_base,                \
-                           const int32_t* split_n, void* stream);
+                           const int32_t* split_n, int32_t grid, int32_t hilo,                  \
+                           void* stream);
 
 /* expands to: defmm_p2m_c128 defmm_m2m_c128 defmm_m2f_c128 defmm_symbols_c128
  * defmm_expand_symbols_c128 defmm_m2l_rows_c128 defmm_m2l_blocked_c128

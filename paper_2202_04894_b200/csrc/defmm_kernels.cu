@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "../../include/defmm_b200.h"
@@ -1338,6 +1339,64 @@ __device__ __forceinline__ double2 helm_pair(double dx, double dy, double dz, do
     return make_double2(gr * qs.x - gi * qs.y, gr * qs.y + gi * qs.x);
 }
 
+// P2P-specific FP64 transcendental pieces.  The CUDA library rsqrt/sincospi
+// cost ~128 issued instructions per pair in the P2P loop (64-bit polynomial
+// constants rematerialised with UMOV pairs, special-case branches): with the
+// coefficients in constant memory (DFMA reads them as c[][] operands) and no
+// special cases (r2 = 0 is masked by the r >= tol test) the loop is bound by
+// the FP64 pipe instead of instruction issue.
+// sin(pi y) / y and cos(pi y) on |y| <= 1/4: Taylor coefficients (error
+// < 2.3e-16 absolute, checked against libm), rounded to double.
+__constant__ double c_sinpi[8] = {3.141592653589793, -5.16771278004997, 2.5501640398773455,
+                                  -0.5992645293207921, 0.08214588661112823, -0.0073704309457143504,
+                                  0.00046630280576761255, -2.1915353447830217e-05};
+__constant__ double c_cospi[9] = {1.0, -4.934802200544679, 4.0587121264167685, -1.3352627688545895,
+                                  0.2353306303588932, -0.02580689139001406, 0.0019295743094039231,
+                                  -0.0001046381049248457, 4.303069587032947e-06};
+
+// sin(pi x), cos(pi x) for 0 <= x < 2^50: x = y + n/2 with n = rint(2x) by the
+// 1.5 * 2^52 trick (y exact, |y| <= 1/4), quadrant n mod 4.
+__device__ __forceinline__ void sincospi_p2p(double x, double& s, double& c) {
+    const double magic = 6755399441055744.0;
+    const double t = fma(x, 2.0, magic);
+    const int q = __double2loint(t);
+    const double y = fma(t - magic, -0.5, x);
+    const double y2 = y * y;
+    double ps = c_sinpi[7];
+#pragma unroll
+    for (int k = 6; k >= 0; --k) ps = fma(ps, y2, c_sinpi[k]);
+    double pc = c_cospi[8];
+#pragma unroll
+    for (int k = 7; k >= 0; --k) pc = fma(pc, y2, c_cospi[k]);
+    const double sy = ps * y;
+    double ss = (q & 1) ? pc : sy, cc = (q & 1) ? sy : pc;
+    if (q & 2) ss = -ss;
+    if ((q + 1) & 2) cc = -cc;
+    s = ss;
+    c = cc;
+}
+
+// 1/sqrt(x): hardware approximation + one third-order Newton step
+// (relative error O(d^3) from the ~2^-22 seed); x = 0 -> NaN (masked).
+__device__ __forceinline__ double rsqrt_p2p(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double e = fma(-x * y, y, 1.0);  // 1 - x y^2
+    return fma(y * e, fma(0.375, e, 0.5), y);
+}
+
+__device__ __forceinline__ double2 helm_pair_p2p(double dx, double dy, double dz, double2 qs, double kpi,
+                                                 double tol) {
+    const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+    const double rinv = rsqrt_p2p(r2);
+    const double r = r2 * rinv;
+    const bool ok = r >= tol;  // kernel.py:40-43 singularity suppression (NaN at r2 = 0 -> false)
+    double s, c;
+    sincospi_p2p(kpi * (ok ? r : 0.0), s, c);
+    const double g = ok ? rinv : 0.0;  // 1/(4 pi) is folded into the staged charges
+    const double gr = g * c, gi = g * s;
+    return make_double2(gr * qs.x - gi * qs.y, gr * qs.y + gi * qs.x);
+}
 
 // Work items: a target leaf's flattened source list (its merged runs) is cut
 // into pieces [f0, f1) of bounded size so that the few coarse leaves next to
@@ -1419,9 +1478,10 @@ __global__ void __launch_bounds__(P2P_NT) p2p_kernel(
     double kappa, double tol, cx<R>* __restrict__ near, cx<R>* __restrict__ partial) {
     using V = cx<R>;
     __shared__ double sx[P2P_TILE], sy[P2P_TILE], sz[P2P_TILE];
-    __shared__ V sq[P2P_TILE];
+    __shared__ double2 sq[P2P_TILE];  // q / (4 pi)
+    const double inv4pi = 1.0 / (4.0 * 3.141592653589793);
     __shared__ int64_t rlo[P2P_MAXRUNS], rpre[P2P_MAXRUNS + 1];
-    const int64_t item = blockIdx.x;
+    for (int64_t item = blockIdx.x; item < n; item += gridDim.x) {
     const int leaf = it.leaf[item];
     const int64_t f0 = it.f0[item], f1 = it.f1[item], ob = it.out[item];
     const int64_t t0 = tgt_lo[leaf], t1 = tgt_hi[leaf];
@@ -1442,15 +1502,16 @@ __global__ void __launch_bounds__(P2P_NT) p2p_kernel(
                 sx[k] = px[g];
                 sy[k] = py[g];
                 sz[k] = pz[g];
-                sq[k] = q[g];
+                const double2 qq = to_d(q[g]);
+                sq[k] = make_double2(qq.x * inv4pi, qq.y * inv4pi);
             },
             [&](int cnt) {
                 if (va) {
                     for (int k = part; k < cnt; k += split) {
                         const double x = sx[k], y = sy[k], z = sz[k];
-                        const double2 qs = to_d(sq[k]);
-                        const double2 ga = helm_pair(xa - x, ya - y, za - z, qs, kpi, tol);
-                        const double2 gb = helm_pair(xb - x, yb - y, zb - z, qs, kpi, tol);
+                        const double2 qs = sq[k];
+                        const double2 ga = helm_pair_p2p(xa - x, ya - y, za - z, qs, kpi, tol);
+                        const double2 gb = helm_pair_p2p(xb - x, yb - y, zb - z, qs, kpi, tol);
                         acca.x += ga.x;
                         acca.y += ga.y;
                         accb.x += gb.x;
@@ -1475,6 +1536,8 @@ __global__ void __launch_bounds__(P2P_NT) p2p_kernel(
             }
         }
     }
+    __syncthreads();  // the next item restages the run table and tiles
+    }
 }
 
 // near[t] = sum_m partial[base + m * nt + (t - t0)] for the split leaves
@@ -1497,45 +1560,81 @@ __global__ void __launch_bounds__(128) p2p_reduce_kernel(int64_t n, const int32_
     }
 }
 
-// complex64 near field: sources staged in shared memory as hi/lo float
-// splits of the FP64 coordinates, so dx = (xt_hi - xs_hi) + (xt_lo - xs_lo)
-// keeps near-field differences accurate without FP64 (SURVEY §7 hard part 6);
-// e^{i kappa r} via an explicit reduction of kappa r / pi to [-1, 1] and the
-// hardware sin/cos (abs. error < 4e-7 on [-pi, pi]); FP32 partial sums per
-// thread, combined with a fixed-order shuffle.
-__device__ __forceinline__ void split_f32(double x, float& hi, float& lo) {
-    hi = __double2float_rn(x);
-    lo = __double2float_rn(x - (double)hi);
-}
-
+// complex64 near field in TARGET-RELATIVE coordinates: every item stages its
+// sources as FP32 offsets from a reference point c of its target leaf (the
+// leaf's first target), formed in FP64 before rounding, and its targets the
+// same way (SURVEY §7 hard part 6: cell-relative coordinates).
+//   HILO = false: one float per offset, dx = x'_t - x'_s is one FADD; the
+//     offset rounding (2^-25 |x_s - c|) bounds the near-field floor at a few
+//     1e-7 -- enough for L <= 5, whose c64 bar is >= ~1e-5.
+//   HILO = true: hi/lo float pairs per offset, dx = (x'h_t - x'h_s) +
+//     (x'l_t - x'l_s) (three FADDs) -- float rounding of dx itself, needed by
+//     the L >= 6 bar (cfg2 L6: 3.1e-6).
+// Charges are staged pre-scaled by 1/(4 pi).  e^{i kappa r} via the reduction
+// of u = kappa r / (2 pi) to [-1/2, 1/2] and the hardware sin/cos (abs. error
+// < 4e-7 on [-pi, pi]); FP32 partial sums per thread, combined with a
+// fixed-order shuffle.
 __device__ __forceinline__ float rsqrt_approx(float x) {  // MUFU.RSQ without denormal fix-ups
     float y;
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
 
-// one complex64 pair: near-field differences from hi/lo splits, phase
-// u = kappa r / (2 pi) reduced to [-1/2, 1/2] for the hardware sin/cos
-__device__ __forceinline__ void pair_f32(float xh, float xl, float yh, float yl, float zh, float zl,
-                                         const float4& h, const float4& l, float k2pi, float ftol,
-                                         float inv4pi, float& ar, float& ai) {
-    const float dx = (xh - h.x) + (xl - l.x);
-    const float dy = (yh - h.y) + (yl - l.y);
-    const float dz = (zh - h.z) + (zl - l.z);
+template <bool HILO>
+struct P2PF32Src;
+template <>
+struct P2PF32Src<false> {  // (x', y', z', q.re / 4 pi), q.im / 4 pi
+    float4 a;
+    float qi;
+};
+template <>
+struct P2PF32Src<true> {  // hi (x, y, z, q.re / 4 pi), lo (x, y, z, q.im / 4 pi)
+    float4 a, b;
+};
+
+// target offsets: hi in x[0..2], lo in x[3..5] (HILO only)
+template <bool HILO>
+__device__ __forceinline__ void pair_f32(const float (&t)[6], const P2PF32Src<HILO>& s, float k2pi, float ftol,
+                                         float& ar, float& ai) {
+    float dx, dy, dz, qr, qi;
+    if constexpr (HILO) {
+        dx = (t[0] - s.a.x) + (t[3] - s.b.x);
+        dy = (t[1] - s.a.y) + (t[4] - s.b.y);
+        dz = (t[2] - s.a.z) + (t[5] - s.b.z);
+        qr = s.a.w;
+        qi = s.b.w;
+    } else {
+        dx = t[0] - s.a.x;
+        dy = t[1] - s.a.y;
+        dz = t[2] - s.a.z;
+        qr = s.a.w;
+        qi = s.qi;
+    }
     const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
     const float rinv = rsqrt_approx(r2);  // r2 = 0 -> inf -> r = NaN -> masked
     const float r = r2 * rinv;
     const bool ok = r >= ftol;
     float u = k2pi * (ok ? r : 0.0f);
-    u -= rintf(u);
+    // u - rint(u) by the 1.5 * 2^23 round-to-nearest trick: two FADDs on the
+    // FMA pipe instead of FRND on the XU pipe; exact for |u| < 2^22 (the
+    // near-field kappa r / 2 pi is far below)
+    u -= __fsub_rn(__fadd_rn(u, 12582912.0f), 12582912.0f);
     float sn, cs;
     __sincosf(6.283185307179586f * u, &sn, &cs);
-    const float g = ok ? rinv * inv4pi : 0.0f;
+    const float g = ok ? rinv : 0.0f;
     const float gr = g * cs, gi = g * sn;
-    ar = fmaf(gr, h.w, fmaf(-gi, l.w, ar));
-    ai = fmaf(gr, l.w, fmaf(gi, h.w, ai));
+    ar = fmaf(gr, qr, fmaf(-gi, qi, ar));
+    ai = fmaf(gr, qi, fmaf(gi, qr, ai));
 }
 
+template <bool HILO>
+__device__ __forceinline__ void rel_f32(double x, double c, float& hi, float& lo) {
+    const double d = x - c;
+    hi = __double2float_rn(d);
+    lo = HILO ? __double2float_rn(d - (double)hi) : 0.0f;
+}
+
+template <bool HILO>
 __global__ void __launch_bounds__(P2P_NT) p2p_f32_kernel(
     int64_t n, P2PItems it, const int64_t* __restrict__ tgt_lo, const int64_t* __restrict__ tgt_hi,
     const int64_t* __restrict__ ptr, const int64_t* __restrict__ src_lo,
@@ -1543,75 +1642,81 @@ __global__ void __launch_bounds__(P2P_NT) p2p_f32_kernel(
     const double* __restrict__ ty, const double* __restrict__ tz, const double* __restrict__ px,
     const double* __restrict__ py, const double* __restrict__ pz, const float2* __restrict__ q,
     double kappa, double tol, float2* __restrict__ near, float2* __restrict__ partial) {
-    __shared__ float4 sh[P2P_TILE];  // (x_hi, y_hi, z_hi, q.re)
-    __shared__ float4 sl[P2P_TILE];  // (x_lo, y_lo, z_lo, q.im)
+    __shared__ P2PF32Src<HILO> sp[P2P_TILE];
     __shared__ int64_t rlo[P2P_MAXRUNS], rpre[P2P_MAXRUNS + 1];
-    const int64_t item = blockIdx.x;
-    const int leaf = it.leaf[item];
-    const int64_t f0 = it.f0[item], f1 = it.f1[item], ob = it.out[item];
-    const int64_t t0 = tgt_lo[leaf], t1 = tgt_hi[leaf];
-    const int split = p2p_split(t1 - t0);
-    const int per_pass = 2 * (P2P_NT / split);
     const float k2pi = (float)(kappa / (2.0 * 3.141592653589793));
     const float ftol = (float)tol;
     const float inv4pi = (float)(1.0 / (4.0 * 3.141592653589793));
-    const int64_t e0 = ptr[leaf], e1 = ptr[leaf + 1];
-    for (int64_t tb = t0; tb < t1; tb += per_pass) {
-        const int64_t ta = tb + 2 * (threadIdx.x / split), tb2 = ta + 1;
-        const int part = threadIdx.x % split;
-        const bool va = ta < t1, vb = tb2 < t1;
-        float axh = 0.f, axl = 0.f, ayh = 0.f, ayl = 0.f, azh = 0.f, azl = 0.f;
-        if (va) {
-            split_f32(tx[ta], axh, axl);
-            split_f32(ty[ta], ayh, ayl);
-            split_f32(tz[ta], azh, azl);
-        }
-        float bxh = axh, bxl = axl, byh = ayh, byl = ayl, bzh = azh, bzl = azl;
-        if (vb) {
-            split_f32(tx[tb2], bxh, bxl);
-            split_f32(ty[tb2], byh, byl);
-            split_f32(tz[tb2], bzh, bzl);
-        }
-        float aar = 0.f, aai = 0.f, bar = 0.f, bai = 0.f;
-        for_packed_tiles(
-            src_lo, src_hi, e0, e1, f0, f1, rlo, rpre,
-            [&](int k, int64_t g) {
-                float4 hh, ll;
-                split_f32(px[g], hh.x, ll.x);
-                split_f32(py[g], hh.y, ll.y);
-                split_f32(pz[g], hh.z, ll.z);
-                const float2 qq = q[g];
-                hh.w = qq.x;
-                ll.w = qq.y;
-                sh[k] = hh;
-                sl[k] = ll;
-            },
-            [&](int cnt) {
-                if (va) {
-#pragma unroll 2
-                    for (int k = part; k < cnt; k += split) {
-                        const float4 h = sh[k], l = sl[k];
-                        pair_f32(axh, axl, ayh, ayl, azh, azl, h, l, k2pi, ftol, inv4pi, aar, aai);
-                        pair_f32(bxh, bxl, byh, byl, bzh, bzl, h, l, k2pi, ftol, inv4pi, bar, bai);
-                    }
-                }
-            });
-        for (int off = 1; off < split; off <<= 1) {
-            aar += __shfl_xor_sync(0xffffffffu, aar, off);
-            aai += __shfl_xor_sync(0xffffffffu, aai, off);
-            bar += __shfl_xor_sync(0xffffffffu, bar, off);
-            bai += __shfl_xor_sync(0xffffffffu, bai, off);
-        }
-        if (part == 0) {
+    for (int64_t item = blockIdx.x; item < n; item += gridDim.x) {
+        const int leaf = it.leaf[item];
+        const int64_t f0 = it.f0[item], f1 = it.f1[item], ob = it.out[item];
+        const int64_t t0 = tgt_lo[leaf], t1 = tgt_hi[leaf];
+        const double cx = tx[t0], cy = ty[t0], cz = tz[t0];  // reference point of the item
+        const int split = p2p_split(t1 - t0);
+        const int per_pass = 2 * (P2P_NT / split);
+        const int64_t e0 = ptr[leaf], e1 = ptr[leaf + 1];
+        for (int64_t tb = t0; tb < t1; tb += per_pass) {
+            const int64_t ta = tb + 2 * (threadIdx.x / split), tb2 = ta + 1;
+            const int part = threadIdx.x % split;
+            const bool va = ta < t1, vb = tb2 < t1;
+            float A[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
             if (va) {
-                if (ob < 0) near[ta] = make_float2(aar, aai);
-                else partial[ob + (ta - t0)] = make_float2(aar, aai);
+                rel_f32<HILO>(tx[ta], cx, A[0], A[3]);
+                rel_f32<HILO>(ty[ta], cy, A[1], A[4]);
+                rel_f32<HILO>(tz[ta], cz, A[2], A[5]);
             }
+            float B[6] = {A[0], A[1], A[2], A[3], A[4], A[5]};
             if (vb) {
-                if (ob < 0) near[tb2] = make_float2(bar, bai);
-                else partial[ob + (tb2 - t0)] = make_float2(bar, bai);
+                rel_f32<HILO>(tx[tb2], cx, B[0], B[3]);
+                rel_f32<HILO>(ty[tb2], cy, B[1], B[4]);
+                rel_f32<HILO>(tz[tb2], cz, B[2], B[5]);
+            }
+            float aar = 0.f, aai = 0.f, bar = 0.f, bai = 0.f;
+            for_packed_tiles(
+                src_lo, src_hi, e0, e1, f0, f1, rlo, rpre,
+                [&](int k, int64_t g) {
+                    const float2 qq = q[g];
+                    P2PF32Src<HILO> v;
+                    float lx, ly, lz;
+                    rel_f32<HILO>(px[g], cx, v.a.x, lx);
+                    rel_f32<HILO>(py[g], cy, v.a.y, ly);
+                    rel_f32<HILO>(pz[g], cz, v.a.z, lz);
+                    v.a.w = qq.x * inv4pi;
+                    if constexpr (HILO) {
+                        v.b = make_float4(lx, ly, lz, qq.y * inv4pi);
+                    } else {
+                        v.qi = qq.y * inv4pi;
+                    }
+                    sp[k] = v;
+                },
+                [&](int cnt) {
+                    if (va) {
+#pragma unroll 2
+                        for (int k = part; k < cnt; k += split) {
+                            const P2PF32Src<HILO> sk = sp[k];
+                            pair_f32<HILO>(A, sk, k2pi, ftol, aar, aai);
+                            pair_f32<HILO>(B, sk, k2pi, ftol, bar, bai);
+                        }
+                    }
+                });
+            for (int off = 1; off < split; off <<= 1) {
+                aar += __shfl_xor_sync(0xffffffffu, aar, off);
+                aai += __shfl_xor_sync(0xffffffffu, aai, off);
+                bar += __shfl_xor_sync(0xffffffffu, bar, off);
+                bai += __shfl_xor_sync(0xffffffffu, bai, off);
+            }
+            if (part == 0) {
+                if (va) {
+                    if (ob < 0) near[ta] = make_float2(aar, aai);
+                    else partial[ob + (ta - t0)] = make_float2(aar, aai);
+                }
+                if (vb) {
+                    if (ob < 0) near[tb2] = make_float2(bar, bai);
+                    else partial[ob + (tb2 - t0)] = make_float2(bar, bai);
+                }
             }
         }
+        __syncthreads();  // the next item restages the run table and tiles
     }
 }
 
@@ -1824,6 +1929,22 @@ int set_smem(K kernel, size_t bytes) {
 }
 
 inline bool grid_ok(int64_t n) { return n > 0 && n < ((int64_t)1 << 31); }
+// DEFMM_CARVEOUT=<percent>: one preferred L1/shared carveout for every kernel
+// (kernels with different carveouts cannot share an SM, which serialises the
+// P2P stream against the far-field stream)
+inline int carveout_pct() {
+    static const int pct = [] {
+        const char* e = getenv("DEFMM_CARVEOUT");
+        return e ? atoi(e) : -1;
+    }();
+    return pct;
+}
+template <typename K>
+inline int carve(K* k) {
+    if (carveout_pct() >= 0)
+        cudaFuncSetAttribute((const void*)k, cudaFuncAttributePreferredSharedMemoryCarveout, carveout_pct());
+    return 0;
+}
 inline unsigned blocks_of(int64_t n, int per) { return (unsigned)((n + per - 1) / per); }
 
 #define DEFMM_DISPATCH_L(L, ...)                              \
@@ -1846,7 +1967,7 @@ int launch_p2m(int32_t L, int64_t n, const int32_t* cell, const int32_t* dir, co
     if (n == 0) return 0;
     if (!grid_ok(n)) return -1;
     cudaStream_t s = (cudaStream_t)stream;
-    DEFMM_DISPATCH_L(L, (p2m_kernel<R, LL><<<(unsigned)n, 128, 0, s>>>(
+    DEFMM_DISPATCH_L(L, (carve(p2m_kernel<R, LL>), p2m_kernel<R, LL><<<(unsigned)n, 128, 0, s>>>(
                             n, cell, dir, out_slot, cell_start, cell_stop, cell_alpha, cell_level, level_beta,
                             dirs, px, py, pz, (const cx<R>*)q, kappa, (cx<R>*)mult)));
     return report(cudaGetLastError(), "p2m");
@@ -1862,6 +1983,7 @@ int launch_m2m(int32_t L, int64_t n, const int64_t* out_slot, const int32_t* dir
         const size_t bytes = nodal_smem_bytes<R, LL>();
         int rc = set_smem(m2m_kernel<R, LL>, bytes);
         if (rc) return rc;
+        carve(m2m_kernel<R, LL>);
         m2m_kernel<R, LL><<<blocks_of(n, NODAL_WARPS), 32 * NODAL_WARPS, bytes, s>>>(
             n, out_slot, dir, son_slot, son_beta, dirs, kappa, (cx<R>*)mult);
     });
@@ -1879,6 +2001,7 @@ int launch_l2l(int32_t L, int64_t n, const int64_t* out_slot, const int8_t* octa
         const size_t bytes = nodal_smem_bytes<R, LL>();
         int rc = set_smem(l2l_kernel<R, LL>, bytes);
         if (rc) return rc;
+        carve(l2l_kernel<R, LL>);
         l2l_kernel<R, LL><<<blocks_of(n, NODAL_WARPS), 32 * NODAL_WARPS, bytes, s>>>(
             n, out_slot, octant, ptr, src_slot, src_dir, son_beta, dirs, kappa, (cx<R>*)local);
     });
@@ -1896,6 +2019,7 @@ int launch_m2f(int32_t L, int64_t n, const int64_t* src_slot, const void* mult, 
         const size_t bytes = sizeof(cx<R>) * (P * LL + M2F_WARPS * (LL * LL * LL + LL * LL * P + LL * P * P));
         int rc = set_smem(m2f_kernel<R, LL>, bytes);
         if (rc) return rc;
+        carve(m2f_kernel<R, LL>);
         m2f_kernel<R, LL><<<blocks_of(n, M2F_WARPS), 32 * M2F_WARPS, bytes, s>>>(n, src_slot, (const cx<R>*)mult,
                                                                                 (cx<R>*)hat);
     });
@@ -1943,6 +2067,7 @@ int launch_m2l_rows(int32_t L, int64_t nrows, const int64_t* row_slot, const int
         const size_t bytes = sizeof(double2) * (P * LL + P * P * P + 1 + LL * P * P + LL * LL * LL);
         int rc = set_smem(m2l_rows_kernel<R, LL>, bytes);
         if (rc) return rc;
+        carve(m2l_rows_kernel<R, LL>);
         m2l_rows_kernel<R, LL><<<(unsigned)nrows, m2l_block<R, LL>(), bytes, s>>>(
             nrows, row_slot, row_ptr, (const int2*)entries, (const cx<R>*)hat, (const cx<R>*)symd,
             (cx<R>*)local);
@@ -1957,7 +2082,7 @@ int launch_m2l_blocked(int32_t L, int64_t ngroups, const int64_t* grp_ptr, const
     if (ngroups == 0) return 0;
     if (!grid_ok(ngroups)) return -1;
     cudaStream_t s = (cudaStream_t)stream;
-    DEFMM_DISPATCH_L(L, (m2l_blocked_kernel<R, LL><<<(unsigned)ngroups, m2lb_threads<R, LL>(), 0, s>>>(
+    DEFMM_DISPATCH_L(L, (carve(m2l_blocked_kernel<R, LL>), m2l_blocked_kernel<R, LL><<<(unsigned)ngroups, m2lb_threads<R, LL>(), 0, s>>>(
                             ngroups, grp_ptr, grp_rows, blk_src, blk_trans, blk_mask, blk_kind,
                             (const cx<R>*)hat, (const cx<R>*)symd, (cx<R>*)lhat)));
     return report(cudaGetLastError(), "m2l_blocked");
@@ -1969,7 +2094,7 @@ int launch_m2l_quad(int32_t L, int64_t ngroups, const int64_t* grp_ptr, const in
     if (ngroups == 0) return 0;
     if (!grid_ok(ngroups)) return -1;
     cudaStream_t s = (cudaStream_t)stream;
-    DEFMM_DISPATCH_L(L, (m2l_quad_kernel<R, LL><<<dim3((unsigned)ngroups, quad_chunks<R, LL>()), quad_threads<R, LL>(), 0, s>>>(
+    DEFMM_DISPATCH_L(L, (carve(m2l_quad_kernel<R, LL>), m2l_quad_kernel<R, LL><<<dim3((unsigned)ngroups, quad_chunks<R, LL>()), quad_threads<R, LL>(), 0, s>>>(
                             ngroups, grp_ptr, grp_rows, (const int4*)quads, (const cx<R>*)hat,
                             (const cx<R>*)symd, (cx<R>*)lhat)));
     return report(cudaGetLastError(), "m2l_quad");
@@ -1988,6 +2113,7 @@ int launch_m2l_slice(int32_t L, int64_t nbatch, const int32_t* batch, int64_t ro
         int rc = set_smem(m2l_slice_kernel<R, LL>, bytes);
         if (rc) return rc;
         const dim3 grid((unsigned)nbatch, (unsigned)layout_of(LL).nslices);
+        carve(m2l_slice_kernel<R, LL>);
         m2l_slice_kernel<R, LL><<<grid, 32 * SLICE_WARPS, bytes, s>>>(
             (const int4*)batch, row_base, seg, ngs, (const int2*)entries, (const cx<R>*)hat, (const cx<R>*)symc,
             (cx<R>*)lhat);
@@ -2007,6 +2133,7 @@ int launch_f2l_rows(int32_t L, int64_t nrows, const int64_t* row_slot, const voi
         const size_t bytes = sizeof(double2) * (P * LL + P * P * P + 1 + LL * P * P + LL * LL * LL);
         int rc = set_smem(f2l_rows_kernel<R, LL>, bytes);
         if (rc) return rc;
+        carve(f2l_rows_kernel<R, LL>);
         f2l_rows_kernel<R, LL><<<(unsigned)nrows, 128, bytes, s>>>(nrows, row_slot, (const cx<R>*)lhat,
                                                                    (cx<R>*)local);
     });
@@ -2022,7 +2149,7 @@ int launch_l2p(int32_t L, int64_t n, const int32_t* leaf_cell, const int64_t* sl
     if (n == 0) return 0;
     if (!grid_ok(n)) return -1;
     cudaStream_t s = (cudaStream_t)stream;
-    DEFMM_DISPATCH_L(L, (l2p_kernel<R, LL><<<(unsigned)n, 64, 0, s>>>(
+    DEFMM_DISPATCH_L(L, (carve(l2p_kernel<R, LL>), l2p_kernel<R, LL><<<(unsigned)n, 64, 0, s>>>(
                             n, leaf_cell, slot_lo, slot_hi, slot_dir, cell_start, cell_stop, cell_alpha,
                             cell_level, level_beta, dirs, px, py, pz, kappa, (const cx<R>*)local,
                             (const cx<R>*)near, perm, (cx<R>*)out)));
@@ -2035,22 +2162,35 @@ int launch_p2p(int64_t n_items, const int32_t* item_leaf, const int64_t* item_f0
                const int64_t* src_lo, const int64_t* src_hi, const double* tx, const double* ty, const double* tz,
                const double* sx, const double* sy, const double* sz, const void* q, double kappa, double tol,
                void* near, void* partial, int64_t n_split, const int32_t* split_leaf, const int64_t* split_base,
-               const int32_t* split_n, void* stream) {
+               const int32_t* split_n, int32_t grid, int32_t hilo, void* stream) {
     if (n_items == 0) return 0;
     if (!grid_ok(n_items)) return -1;
     cudaStream_t s = (cudaStream_t)stream;
     const P2PItems it{item_leaf, item_f0, item_f1, item_out};
+    // grid > 0: a persistent grid striding over the items (leaves SM room for
+    // the concurrently running far-field kernels); 0: one CTA per item
+    const unsigned ng = (unsigned)(grid > 0 && grid < n_items ? grid : n_items);
     if constexpr (sizeof(R) == 4) {
-        p2p_f32_kernel<<<(unsigned)n_items, P2P_NT, 0, s>>>(n_items, it, tgt_lo, tgt_hi, ptr, src_lo, src_hi, tx,
-                                                            ty, tz, sx, sy, sz, (const float2*)q, kappa, tol,
-                                                            (float2*)near, (float2*)partial);
+        if (hilo) {
+            carve(p2p_f32_kernel<true>);
+            p2p_f32_kernel<true><<<ng, P2P_NT, 0, s>>>(n_items, it, tgt_lo, tgt_hi, ptr, src_lo, src_hi, tx, ty,
+                                                       tz, sx, sy, sz, (const float2*)q, kappa, tol,
+                                                       (float2*)near, (float2*)partial);
+        } else {
+            carve(p2p_f32_kernel<false>);
+            p2p_f32_kernel<false><<<ng, P2P_NT, 0, s>>>(n_items, it, tgt_lo, tgt_hi, ptr, src_lo, src_hi, tx, ty,
+                                                        tz, sx, sy, sz, (const float2*)q, kappa, tol,
+                                                        (float2*)near, (float2*)partial);
+        }
     } else {
-        p2p_kernel<R><<<(unsigned)n_items, P2P_NT, 0, s>>>(n_items, it, tgt_lo, tgt_hi, ptr, src_lo, src_hi, tx,
+        carve(p2p_kernel<R>);
+        p2p_kernel<R><<<ng, P2P_NT, 0, s>>>(n_items, it, tgt_lo, tgt_hi, ptr, src_lo, src_hi, tx,
                                                            ty, tz, sx, sy, sz, (const cx<R>*)q, kappa, tol,
                                                            (cx<R>*)near, (cx<R>*)partial);
     }
     if (n_split > 0) {
         if (!grid_ok(n_split)) return -1;
+        carve(p2p_reduce_kernel<R>);
         p2p_reduce_kernel<R><<<(unsigned)n_split, 128, 0, s>>>(n_split, split_leaf, split_base, split_n, tgt_lo,
                                                                 tgt_hi, (const cx<R>*)partial, (cx<R>*)near);
     }
@@ -2150,10 +2290,11 @@ const char* defmm_last_error(void) { return g_last_error; }
                            const int64_t* src_hi, const double* tx, const double* ty, const double* tz,           \
                            const double* sx, const double* sy, const double* sz, const void* q, double kappa,     \
                            double tol, void* near, void* partial, int64_t n_split, const int32_t* split_leaf,     \
-                           const int64_t* split_base, const int32_t* split_n, void* stream) {                     \
+                           const int64_t* split_base, const int32_t* split_n, int32_t grid, int32_t hilo,         \
+                           void* stream) {                                                                        \
         return launch_p2p<R>(n_items, item_leaf, item_f0, item_f1, item_out, tgt_lo, tgt_hi, ptr, src_lo, src_hi,  \
                              tx, ty, tz, sx, sy, sz, q, kappa, tol, near, partial, n_split, split_leaf,           \
-                             split_base, split_n, stream);                                                        \
+                             split_base, split_n, grid, hilo, stream);                                            \
     }
 
 DEFMM_EXPORT_TYPED(c128, double)

@@ -308,9 +308,19 @@ class FmmPlan:
         self.p2p_partial = torch.empty(max(self._partial_size, 1), dtype=cd, device=d)
         self.q = torch.zeros(self.n_src, dtype=cd, device=d)
         self.out = torch.empty(self.n_tgt, dtype=cd, device=d)
-        self.side_stream = torch.cuda.Stream(device=d)
+        lo, hi = torch.cuda.Stream.priority_range()  # (lowest, highest) priority numbers
+        self.side_stream = torch.cuda.Stream(device=d, priority=lo)
+        self.far_stream = torch.cuda.Stream(device=d, priority=hi)
+        self.far_priority = False
         self.m2l_variant = "hybrid"
-        self.p2p_overlap = "upward"  # or "m2l"
+        # "upward": P2P concurrent with P2M/M2M/M2F, joined before the M2L (clean
+        # stage timers); "full": P2P spans the upward pass and the M2L on a
+        # persistent grid of p2p_grid CTAs (SM room left for the far field)
+        self.p2p_overlap = "upward"
+        self.p2p_grid = 0
+        # c64 near-field coordinates: hi/lo float pairs where the order's
+        # accuracy bar needs them (defmm_b200.h, K1)
+        self.p2p_hilo = self.L >= 6
 
     def _make_shard(self):
         from .parallel import Shard, make_shard
@@ -535,6 +545,20 @@ class FmmPlan:
         the caller's target order (device tensor; when sharded only this
         rank's targets are non-zero).  ``stage_events`` (list) receives
         (name, start_event, end_event) for the stage timers."""
+        if self.far_priority and self.shard is None:
+            # far field on a HIGH-priority stream, P2P on the low-priority side
+            # stream: the block scheduler then dispatches the latency-bound
+            # far-field chain first and the P2P fills the remaining SM slots
+            cur = torch.cuda.current_stream(self.device)
+            fs = self.far_stream
+            fs.wait_stream(cur)
+            with torch.cuda.stream(fs):
+                res = self._apply(out, stage_events)
+            cur.wait_stream(fs)
+            return res
+        return self._apply(out, stage_events)
+
+    def _apply(self, out=None, stage_events=None):
         self.apply_upward(stage_events)
         if self.shard is not None:
             # M2M is linear: summing the partial multipoles over the ranks
@@ -554,7 +578,8 @@ class FmmPlan:
                 e0.record(side)
             _lib.call(self._op("p2p"), self.n_items, *self.p2p_items, self.tgt_lo, self.tgt_hi, self.p2p_ptr,
                       self.p2p_lo, self.p2p_hi, *self.t_xyz, *self.s_xyz, self.q, float(p.kappa), float(p.tol),
-                      self.near, self.p2p_partial, self.n_split, *self.p2p_split, side.cuda_stream)
+                      self.near, self.p2p_partial, self.n_split, *self.p2p_split, int(self.p2p_grid),
+                      int(self.p2p_hilo), side.cuda_stream)
             if stage_events is not None:
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record(side)
