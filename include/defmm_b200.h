@@ -87,6 +87,27 @@ int defmm_dtt_source_hats(const defmm_dtt* d, const int64_t* m_dense, const int6
                           int32_t* src_hat, int64_t* hat_slot, int64_t* n_hat);
 void defmm_dtt_free(defmm_dtt* d);
 
+/* ---- host: M2L row tiles for the shared-memory tile kernel (K7 v6) --------
+ * The rows order[0..n_order) (row r = events [row_ptr[r], row_ptr[r+1]) of
+ * ent = {source spectrum, derived symbol} int32 pairs; the same lists the
+ * reference's dtt produces, traversal.py:320-348) are cut greedily into tiles
+ * of consecutive rows whose operand UNION (distinct spectra + symbols) has at
+ * most u_max (<= 65535) entries, at most k_max rows and at most e_max events.  Outputs (caller
+ * allocates upper bounds: n_order+1 tiles/rows, 2*events ops, events ev):
+ *   tile t = tiled rows [tile_ptr[t], tile_ptr[t+1]) of tile_rows (row ids),
+ *            operands ops[op_ptr[t] .. op_ptr[t+1]) (v >= 0: spectrum v,
+ *            v < 0: derived symbol -1-v), local index = position in the tile;
+ *   tiled row k = events ev[ev_ptr[k] .. ev_ptr[k+1]) packed
+ *            local spectrum | local symbol << 16, in the row's event order.
+ * counts = {tiles, tiled rows, ops, events, untiled rows (own union > u_max or
+ * own events > e_max)}.
+ * Returns 0, or -1 for invalid u_max / k_max. */
+int defmm_m2l_tiles(int64_t n_order, const int64_t* order, const int64_t* row_ptr, const int32_t* ent,
+                    int64_t n_hat, int64_t n_trans, int32_t u_max, int32_t k_max, int32_t e_max,
+                    int64_t* tile_ptr,
+                    int64_t* tile_rows, int64_t* op_ptr, int32_t* ops, int64_t* ev_ptr, uint32_t* ev,
+                    int64_t* counts);
+
 /* ---- device operators ------------------------------------------------------
  * Every operator exists as *_c128 (complex arrays are double2 = interleaved
  * FP64 re/im, exactly the reference's complex128) and *_c64 (float2; phases,
@@ -137,6 +158,12 @@ void defmm_dtt_free(defmm_dtt* d);
  *   entries[seg[(r - row_base)(ngs+1) + g] .. seg[... + g + 1]), each {spectrum,
  *   (canonical index within the group << 6) | rotation id}.  lhat[r] = sum over
  *   events of rot(sym_canon) (*) hat -- the same sum as the row kernel.
+ *   K7 v6 tile variant (m2l_tile): one CTA (256 threads) per tile, walking
+ *   the spectrum in slices of F = 16 (c64) / 8 (c128) entries; dynamic shared
+ *   memory 2 u_max F complex + ids + e_max events (the u_max / e_max the
+ *   tiles were built with).  Tiles, operands and packed events as produced by
+ *   defmm_m2l_tiles; lhat[lhat_base + k] = sum over tiled row k's events of
+ *   sym_derived[t] (*) hat[s] -- the same sum as the row kernel.
  * K5 L2L -- traversal.py:355-391 in gather form.
  *   for i < n: local[out_slot[i]] += sum_{e in [ptr[i], ptr[i+1])}
  *   (C'0 (x) C'1 (x) C'2) local[src_slot[e]], C' the transposed/conjugate-
@@ -194,6 +221,11 @@ void defmm_dtt_free(defmm_dtt* d);
                                  int64_t row_base, const int64_t* seg, int32_t ngs,             \
                                  const int32_t* entries, const void* hat,                       \
                                  const void* sym_canon, void* lhat, void* stream);              \
+    int defmm_m2l_tile_##SUFFIX(int32_t L, int64_t ntiles, const int64_t* tile_ptr,               \
+                                const int64_t* op_ptr, const int32_t* ops, const int64_t* ev_ptr,  \
+                                const uint32_t* ev, int64_t lhat_base, int32_t u_max,              \
+                                int32_t e_max, const void* hat, const void* sym_derived,           \
+                                void* lhat, void* stream);                                         \
     int defmm_f2l_rows_##SUFFIX(int32_t L, int64_t nrows, const int64_t* row_slot,               \
                                 const void* lhat, void* local, void* stream);                   \
     int defmm_l2l_##SUFFIX(int32_t L, int64_t n, const int64_t* out_slot, const int8_t* octant,  \
@@ -221,11 +253,11 @@ void defmm_dtt_free(defmm_dtt* d);
 
 /* expands to: defmm_p2m_c128 defmm_m2m_c128 defmm_m2f_c128 defmm_symbols_c128
  * defmm_expand_symbols_c128 defmm_m2l_rows_c128 defmm_m2l_blocked_c128
- * defmm_m2l_quad_c128 defmm_m2l_slice_c128 defmm_f2l_rows_c128 defmm_l2l_c128 defmm_l2p_c128 defmm_p2p_c128 */
+ * defmm_m2l_quad_c128 defmm_m2l_tile_c128 defmm_m2l_slice_c128 defmm_f2l_rows_c128 defmm_l2l_c128 defmm_l2p_c128 defmm_p2p_c128 */
 DEFMM_DECLARE_TYPED(c128)
 /* expands to: defmm_p2m_c64 defmm_m2m_c64 defmm_m2f_c64 defmm_symbols_c64
  * defmm_expand_symbols_c64 defmm_m2l_rows_c64 defmm_m2l_blocked_c64
- * defmm_m2l_quad_c64 defmm_m2l_slice_c64 defmm_f2l_rows_c64 defmm_l2l_c64 defmm_l2p_c64 defmm_p2p_c64 */
+ * defmm_m2l_quad_c64 defmm_m2l_tile_c64 defmm_m2l_slice_c64 defmm_f2l_rows_c64 defmm_l2l_c64 defmm_l2p_c64 defmm_p2p_c64 */
 DEFMM_DECLARE_TYPED(c64)
 
 /* Spectral layout of order L (HOST call, no device needed): every spectrum is

@@ -1063,6 +1063,131 @@ __global__ void __launch_bounds__(quad_threads<R, L>()) m2l_quad_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// K7 v6: tile M2L.  One CTA per tile = a run of Morton-consecutive rows with
+// one key (host: defmm_m2l_tiles) whose source spectra and derived symbols,
+// as a union, fit shared memory.  The CTA stages the tile's operand ids and
+// packed events once, then walks the spectrum in slices of F entries with a
+// cp.async double buffer: while slice s is consumed from shared memory, the
+// union's slice s+1 streams in.  Each operand is read from L2 once per tile
+// instead of once per event (4-8x fewer L2->SM bytes than the row kernel on
+// surface data).  Threads = KS row slots x F frequencies; with nr < KS rows a
+// row is split over KS / nr slots (every (KS/nr)-th event), reduced in fixed
+// slot order.  Accumulated spectra go to lhat; f2l_rows_kernel applies the
+// inverse DFT.
+template <typename R>
+struct TileCfg;
+template <>
+struct TileCfg<float> {  // 16 x complex64 = 128 B per operand slice
+    static constexpr int F = 16, KS = 16;
+};
+template <>
+struct TileCfg<double> {  // 8 x complex128 = 128 B per operand slice
+    static constexpr int F = 8, KS = 32;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(smem_u32(dst)), "l"(src), "n"(BYTES));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <typename R>
+__host__ __device__ constexpr size_t tile_smem_bytes(int u_max, int e_max) {
+    return 2 * (size_t)u_max * TileCfg<R>::F * sizeof(cx<R>)                 // operand slices, double buffer
+           + (size_t)TileCfg<R>::KS * TileCfg<R>::F * sizeof(cx<R>)          // part sums
+           + (size_t)u_max * sizeof(int32_t) + (size_t)e_max * sizeof(uint32_t);  // operand ids, events
+}
+
+template <typename R, int L>
+__global__ void __launch_bounds__(256) m2l_tile_kernel(
+    const int64_t* __restrict__ tile_ptr, const int64_t* __restrict__ op_ptr, const int32_t* __restrict__ ops,
+    const int64_t* __restrict__ ev_ptr, const uint32_t* __restrict__ ev, int64_t lhat_base, int u_max,
+    const cx<R>* __restrict__ hat, const cx<R>* __restrict__ symd, cx<R>* __restrict__ lhat) {
+    using V = cx<R>;
+    constexpr int F = TileCfg<R>::F, KS = TileCfg<R>::KS, NT = F * KS;
+    constexpr int SS = spec_stride<R, L>();
+    constexpr int NS = (SS + F - 1) / F;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    V* buf = reinterpret_cast<V*>(smraw);         // [2][u_max][F]
+    V* red = buf + 2 * (size_t)u_max * F;         // [KS][F]
+    int32_t* sops = reinterpret_cast<int32_t*>(red + KS * F);
+    uint32_t* sev = reinterpret_cast<uint32_t*>(sops + u_max);
+    const int64_t tile = blockIdx.x;
+    const int64_t r0 = tile_ptr[tile];
+    const int nr = (int)(tile_ptr[tile + 1] - r0);
+    const int64_t o0 = op_ptr[tile];
+    const int nu = (int)(op_ptr[tile + 1] - o0);
+    const int64_t eb = ev_ptr[r0];
+    const int ne = (int)(ev_ptr[r0 + nr] - eb);
+    const int f = threadIdx.x % F, slot = threadIdx.x / F;
+    for (int i = threadIdx.x; i < nu; i += NT) cp_async<4>(sops + i, ops + o0 + i);
+    for (int i = threadIdx.x; i < ne; i += NT) cp_async<4>(sev + i, ev + eb + i);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    auto issue = [&](int sl) {
+        V* dst = buf + (size_t)(sl & 1) * u_max * F;
+        const int j = sl * F + f;
+        for (int u = slot; u < nu; u += KS) {
+            const int32_t g = sops[u];
+            if (j < SS) {
+                const V* src = g >= 0 ? hat + (int64_t)g * SS : symd + (int64_t)(-1 - g) * SS;
+                cp_async<sizeof(V)>(dst + u * F + f, src + j);
+            } else {
+                dst[u * F + f] = cz<V>();
+            }
+        }
+        cp_async_commit();
+    };
+    const int parts = KS / nr;  // nr <= KS (host k_max)
+    const int row = slot % nr, part = slot / nr;
+    const bool active = part < parts;
+    // part p of a row: a contiguous event range (vector loads of 4 packed events)
+    int c0 = 0, c1 = 0;
+    if (active) {
+        const int e0 = (int)(ev_ptr[r0 + row] - eb), len = (int)(ev_ptr[r0 + row + 1] - eb) - e0;
+        c0 = e0 + (len * part) / parts;
+        c1 = e0 + (len * (part + 1)) / parts;
+    }
+    issue(0);
+    for (int sl = 0; sl < NS; ++sl) {
+        if (sl + 1 < NS) {
+            issue(sl + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const V* bs = buf + (size_t)(sl & 1) * u_max * F + f;
+        auto ev1 = [&](uint32_t pk, V& a) { a = cfma(bs[(pk >> 16) * F], bs[(pk & 0xffffu) * F], a); };
+        V acc0 = cz<V>(), acc1 = cz<V>(), acc2 = cz<V>(), acc3 = cz<V>();
+        int e = c0;
+        for (; e < c1 && (e & 3); ++e) ev1(sev[e], acc0);
+        for (; e + 4 <= c1; e += 4) {
+            const uint4 p4 = *reinterpret_cast<const uint4*>(sev + e);
+            ev1(p4.x, acc0);
+            ev1(p4.y, acc1);
+            ev1(p4.z, acc2);
+            ev1(p4.w, acc3);
+        }
+        for (; e < c1; ++e) ev1(sev[e], acc1);
+        red[slot * F + f] = cadd(cadd(acc0, acc1), cadd(acc2, acc3));
+        __syncthreads();  // part sums visible; buffer (sl & 1) consumed
+        const int j = sl * F + f;
+        if (part == 0 && j < SS) {
+            V a = red[row * F + f];
+            for (int q = 1; q < parts; ++q) a = cadd(a, red[(row + q * nr) * F + f]);
+            lhat[(lhat_base + r0 + row) * SS + j] = a;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K7 v4: slice M2L.  Grid = (row batch, spectral slice).  The Hadamard M2L is
 // independent per frequency, and a slice is closed under the cube group, so a
 // CTA keeps the CANONICAL symbols of its level restricted to its slice in
@@ -2101,6 +2226,25 @@ int launch_m2l_quad(int32_t L, int64_t ngroups, const int64_t* grp_ptr, const in
 }
 
 template <typename R>
+int launch_m2l_tile(int32_t L, int64_t ntiles, const int64_t* tile_ptr, const int64_t* op_ptr, const int32_t* ops,
+                    const int64_t* ev_ptr, const uint32_t* ev, int64_t lhat_base, int32_t u_max, int32_t e_max,
+                    const void* hat, const void* symd, void* lhat, void* stream) {
+    if (ntiles == 0) return 0;
+    if (!grid_ok(ntiles) || u_max < 1 || e_max < 1) return -1;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t bytes = tile_smem_bytes<R>(u_max, e_max);
+    DEFMM_DISPATCH_L(L, {
+        int rc = set_smem(m2l_tile_kernel<R, LL>, bytes);
+        if (rc) return rc;
+        carve(m2l_tile_kernel<R, LL>);
+        m2l_tile_kernel<R, LL><<<(unsigned)ntiles, 256, bytes, s>>>(tile_ptr, op_ptr, ops, ev_ptr, ev, lhat_base,
+                                                                   u_max, (const cx<R>*)hat, (const cx<R>*)symd,
+                                                                   (cx<R>*)lhat);
+    });
+    return report(cudaGetLastError(), "m2l_tile");
+}
+
+template <typename R>
 int launch_m2l_slice(int32_t L, int64_t nbatch, const int32_t* batch, int64_t row_base, const int64_t* seg,
                      int32_t ngs, const int32_t* entries, const void* hat, const void* symc, void* lhat,
                      void* stream) {
@@ -2264,6 +2408,13 @@ const char* defmm_last_error(void) { return g_last_error; }
                                  const int64_t* seg, int32_t ngs, const int32_t* entries, const void* hat,         \
                                  const void* sym_canon, void* lhat, void* stream) {                               \
         return launch_m2l_slice<R>(L, nbatch, batch, row_base, seg, ngs, entries, hat, sym_canon, lhat, stream);   \
+    }                                                                                                               \
+    int defmm_m2l_tile_##SUFFIX(int32_t L, int64_t ntiles, const int64_t* tile_ptr, const int64_t* op_ptr,          \
+                                const int32_t* ops, const int64_t* ev_ptr, const uint32_t* ev, int64_t lhat_base,  \
+                                int32_t u_max, int32_t e_max, const void* hat, const void* sym_derived,            \
+                                void* lhat, void* stream) {                                                        \
+        return launch_m2l_tile<R>(L, ntiles, tile_ptr, op_ptr, ops, ev_ptr, ev, lhat_base, u_max, e_max, hat,      \
+                                  sym_derived, lhat, stream);                                                      \
     }                                                                                                               \
     int defmm_f2l_rows_##SUFFIX(int32_t L, int64_t nrows, const int64_t* row_slot, const void* lhat, void* local,   \
                                 void* stream) {                                                                    \

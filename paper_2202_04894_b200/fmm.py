@@ -117,6 +117,37 @@ def _quads(bsrc, btr, bmask, gptr):
     return q, qptr
 
 
+def m2l_tiles(order, row_ptr, ent, n_hat: int, n_trans: int, u_max: int, k_max: int, e_max: int = 1 << 30) -> dict:
+    """Host tiling of M2L rows for the tile kernel (defmm_m2l_tiles, native):
+    tiles of consecutive rows of ``order`` whose operand union (spectra +
+    derived symbols) has <= u_max entries and <= k_max rows."""
+    import ctypes as C
+
+    lib = _lib.load()
+    ptr = np.ascontiguousarray(row_ptr, np.int64)
+    ent = np.ascontiguousarray(ent, np.int32)
+    order = np.ascontiguousarray(order, np.int64)
+    n = order.shape[0]
+    n_ev = int((ptr[order + 1] - ptr[order]).sum()) if n else 0
+    tile_ptr = np.zeros(n + 1, np.int64)
+    tile_rows = np.zeros(max(n, 1), np.int64)
+    op_ptr = np.zeros(n + 1, np.int64)
+    ops = np.zeros(max(2 * n_ev, 1), np.int32)
+    ev_ptr = np.zeros(n + 1, np.int64)
+    ev = np.zeros(max(n_ev, 1), np.uint32)
+    counts = np.zeros(5, np.int64)
+
+    def a(x):
+        return x.ctypes.data_as(C.c_void_p)
+
+    _lib.check(lib.defmm_m2l_tiles(n, a(order), a(ptr), a(ent), int(n_hat), int(n_trans), int(u_max), int(k_max),
+                                   int(e_max), a(tile_ptr), a(tile_rows), a(op_ptr), a(ops), a(ev_ptr), a(ev), a(counts)),
+               "defmm_m2l_tiles")
+    nt, nr, no, ne = (int(x) for x in counts[:4])
+    return {"n_tiles": nt, "tile_ptr": tile_ptr[: nt + 1], "rows": tile_rows[:nr], "op_ptr": op_ptr[: nt + 1],
+            "ops": ops[:no], "ev_ptr": ev_ptr[: nr + 1], "ev": ev[:ne], "untiled": int(counts[4])}
+
+
 def _rows_to_ids(slots, rows):
     """Local slots -> index into the sorted row-slot list ``rows`` (-1 if absent)."""
     slots = np.asarray(slots)
@@ -268,6 +299,15 @@ class FmmPlan:
         self.qd_ptr = _dev(h["qd_ptr"], i64, d)
         self.qd_rows = _dev(h["qd_rows"].reshape(-1), i64, d)
         self.quads = _dev(h["quads"].reshape(-1), i32, d)
+        tl = h["tl"]
+        self.n_tiles = int(tl["n_tiles"]) if tl is not None else 0
+        if self.n_tiles:
+            self.tl_ptr = _dev(tl["tile_ptr"], i64, d)
+            self.tl_op_ptr = _dev(tl["op_ptr"], i64, d)
+            self.tl_ops = _dev(tl["ops"], i32, d)
+            self.tl_ev_ptr = _dev(tl["ev_ptr"], i64, d)
+            self.tl_ev = _dev(tl["ev"].view(np.int32), i32, d)
+            self.tl_base = int(tl["lhat_base"])
         sl = h["slice"]
         self.n_slice_batch = int(sl["n_batch"])
         self.sl_batch = _dev(sl["batch"].reshape(-1), i32, d)
@@ -360,7 +400,7 @@ class FmmPlan:
             if ev[sel].mean() >= self.BLOCKED_MIN_EVENTS_PER_BLOCK:
                 dense.add(int(lev))
         mode = self.m2l_variant_default
-        if mode in ("rows", "slice_all", "quad_all"):
+        if mode in ("rows", "slice_all", "quad_all", "tiles_all"):
             dense = set()
         elif mode == "blocked_all":
             dense = set(int(x) for x in np.unique(blev))
@@ -378,6 +418,20 @@ class FmmPlan:
             h["rk_rows"], h["rk_ptr"], h["rk_ent"] = sparse_rows, rptr, h["ent"][rsel]
         elif mode == "slice_all":
             h["slice"] = self._slice_lists(rptr, h["ent"][rsel], rlev[~is_dense], 0)
+        h["tl"] = None
+        if mode in ("tiles", "tiles_all"):
+            # sparse-level rows -> shared-memory tiles (K7 v6); rows whose own
+            # operands exceed a tile -> row kernel
+            sp_ids = np.nonzero(~is_dense)[0]
+            slot = rows[sp_ids]
+            order = sp_ids[np.lexsort((p.l_cell[slot], p.l_dir[slot], rlev[sp_ids]))]
+            tl = self._tile_lists(order, h)
+            h["tl"] = tl
+            untiled = np.setdiff1d(sp_ids, tl["rows"])
+            sel_mask = np.zeros(rows.shape[0], bool)
+            sel_mask[untiled] = True
+            _, uptr, usel = _sub_csr(h["row_ptr"], sel_mask)
+            h["rk_rows"], h["rk_ptr"], h["rk_ent"] = rows[untiled], uptr, h["ent"][usel]
         if quad:  # sparse levels -> quad kernel over the blocks of their groups
             is_dense = np.ones(rows.shape[0], bool)
             dense_rows = rows
@@ -387,8 +441,11 @@ class FmmPlan:
         gid = _rows_to_ids(gr_slots, dense_rows)
         gkeep = np.any(gid >= 0, axis=1)
         _, gptr, bsel = _sub_csr(h["grp_ptr"], gkeep)
-        # lhat rows: blocked (+ quad) rows, then slice rows (one F2L launch)
+        # lhat rows: blocked (+ quad) rows, then slice or tile rows (one F2L launch)
         h["bk_rows"] = np.concatenate([dense_rows, sparse_rows if h["slice"]["n_batch"] else z])
+        if h["tl"] is not None:
+            h["tl"]["lhat_base"] = int(dense_rows.shape[0])
+            h["bk_rows"] = np.concatenate([dense_rows, rows[h["tl"]["rows"]]])
         gptr, grows = gptr, gid[gkeep]
         bsrc, btr, bmask, bkind = h["blk_src"][bsel], h["blk_trans"][bsel], h["blk_mask"][bsel], h["blk_kind"][bsel]
         if quad:
@@ -411,6 +468,19 @@ class FmmPlan:
         h["blk_src"], h["blk_trans"], h["blk_mask"], h["blk_kind"] = bsrc, btr, bmask, bkind
         self.dense_levels = sorted(dense)
         return h
+
+    # tile kernel (K7 v6): operand slices of 128 B (c64: 16 x 8 B, c128:
+    # 8 x 16 B), double-buffered: 2 x 352 x 128 B + 4096 events ~ 107 KB of
+    # shared memory -> 2 CTAs per SM
+    TILE_U_MAX = 352
+    TILE_E_MAX = 4096
+
+    def _tile_lists(self, order, h) -> dict:
+        """Greedy operand-union tiles over the rows ``order`` (indices into
+        h["rows"], sorted (level, key, Morton target)): defmm_m2l_tiles."""
+        return m2l_tiles(order, h["row_ptr"], h["ent"], int(h["hat_slot"].shape[0]),
+                         int(self.plan.trans_canon.shape[0]), int(self.TILE_U_MAX),
+                         16 if self.config.dtype == "c64" else 32, int(self.TILE_E_MAX))
 
     # rows per slice-kernel batch: enough events per batch to amortise the
     # shared-memory symbol loads (G symbols per group), one row per warp at least
@@ -630,6 +700,11 @@ class FmmPlan:
                       self.blk_trans, self.blk_mask, self.blk_kind, self.hat, self.sym_derived, self.lhat, sh)
             _lib.call(self._op("m2l_quad"), L, self.n_qgroups, self.qd_ptr, self.qd_rows, self.quads, self.hat,
                       self.sym_derived, self.lhat, sh)
+            if self.n_tiles:
+                _lib.call(self._op("m2l_tile"), L, self.n_tiles, self.tl_ptr, self.tl_op_ptr, self.tl_ops,
+                          self.tl_ev_ptr, self.tl_ev, self.tl_base, int(self.TILE_U_MAX),
+                          int(self.TILE_E_MAX), self.hat,
+                          self.sym_derived, self.lhat, sh)
             _lib.call(self._op("m2l_slice"), L, self.n_slice_batch, self.sl_batch, self.sl_row_base, self.sl_seg,
                       self.sl_ngs, self.sl_ent, self.hat, self.sym, self.lhat, sh)
             _lib.call(self._op("f2l_rows"), L, self.bk_rows.shape[0], self.bk_rows, self.lhat, self.local, sh)
@@ -701,7 +776,8 @@ class FmmPlan:
         sparse = sorted(set(range(self.tt.depth + 1)) - set(dense))
         out = []
         for n, name, lev in ((self.rk_rows.shape[0], "m2l_rows_kernel", sparse), (self.n_groups, "m2l_blocked_kernel", dense),
-                             (self.n_qgroups, "m2l_quad_kernel", sparse), (self.n_slice_batch, "m2l_slice_kernel", sparse),
+                             (self.n_qgroups, "m2l_quad_kernel", sparse), (self.n_tiles, "m2l_tile_kernel", sparse),
+                             (self.n_slice_batch, "m2l_slice_kernel", sparse),
                              (self.bk_rows.shape[0], "f2l_rows_kernel", None)):
             if n:
                 out.append(f"{name}<{R}, {self.L}>" + (f" (levels {lev})" if lev is not None else ""))
@@ -712,7 +788,7 @@ class FmmPlan:
         """Kernels of one matvec: p2p (+ split reduce), p2m, m2m per level, m2f,
         the M2L kernels with work, l2l per level, l2p."""
         if self.m2l_variant == "hybrid":
-            m2l = sum(int(n > 0) for n in (self.rk_rows.shape[0], self.n_groups, self.n_qgroups,
+            m2l = sum(int(n > 0) for n in (self.rk_rows.shape[0], self.n_groups, self.n_qgroups, self.n_tiles,
                                            self.n_slice_batch, self.bk_rows.shape[0]))
         else:
             m2l = 1

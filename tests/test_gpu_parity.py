@@ -148,7 +148,7 @@ def test_m2l_canonical_gather_and_derived_symbols_agree(case):
     plan.m2l_variant = "hybrid"
     c = plan.apply().cpu().numpy()
     assert _rel(c, a) <= 1e-13
-    for mode in ("blocked_all", "rows", "slice_all", "hybrid_rows", "quad_all"):
+    for mode in ("blocked_all", "rows", "slice_all", "hybrid_rows", "quad_all", "tiles", "tiles_all"):
         p2 = FmmPlan(g["points"], None, FmmConfig(**g["config"]), charges=g["charges"], reuse=plan, m2l=mode)
         assert _rel(p2.apply().cpu().numpy(), a) <= 1e-13
     assert _rel(b, g["pot"]) <= FP64_TOL

@@ -386,3 +386,42 @@ def test_quads_reconstruct_every_block_pair(case):
                         (((a & 1) - (b & 1)) + 1)
                     ref.append((int(bg[bi]), a, int(pl.blk_src[bi, b]), int(pl.blk_trans[bi, d])))
     assert sorted(got) == sorted(ref)
+
+
+@pytest.mark.parametrize("case", ["cubesurf4000", "volume3000", "c1_kd16"])
+@pytest.mark.parametrize("u_max,k_max,e_max", [(768, 16, 1 << 20), (96, 32, 4096), (40, 4, 25)])
+def test_m2l_tiles_reconstruct_every_row(case, u_max, k_max, e_max):
+    """defmm_m2l_tiles (tile kernel lists): every tiled row's packed local
+    events map back to its (spectrum, symbol) entries in order, tile unions
+    hold each operand once within u_max / k_max, and exactly the rows whose
+    own operands exceed u_max are left to the row kernel."""
+    from paper_2202_04894_b200.fmm import m2l_tiles
+
+    _, _, p = _plan(load_case(case))
+    ptr, ent = p.m2l_row_ptr, p.m2l_rows_entries
+    nrows = ptr.shape[0] - 1
+    order = np.lexsort((p.l_cell[p.m2l_row_slot], p.l_dir[p.m2l_row_slot], p.m2l_level))
+    n_hat = int(ent[:, 0].max()) + 1
+    n_trans = int(p.trans_canon.shape[0])
+    t = m2l_tiles(order, ptr, ent, n_hat, n_trans, u_max, k_max, e_max)
+    own = np.array([len(np.unique(ent[ptr[r]:ptr[r + 1], 0])) + len(np.unique(ent[ptr[r]:ptr[r + 1], 1]))
+                    for r in range(nrows)])
+    tiled = set(t["rows"].tolist())
+    assert tiled == {int(r) for r in order if own[r] <= u_max and ptr[r + 1] - ptr[r] <= e_max}
+    assert t["untiled"] == nrows - len(tiled)
+    # tiled rows keep the caller's order
+    pos = {int(r): i for i, r in enumerate(order)}
+    assert all(pos[int(a)] < pos[int(b)] for a, b in zip(t["rows"][:-1], t["rows"][1:]))
+    for k in range(t["n_tiles"]):
+        r0, r1 = t["tile_ptr"][k], t["tile_ptr"][k + 1]
+        ops = t["ops"][t["op_ptr"][k]:t["op_ptr"][k + 1]]
+        assert 1 <= r1 - r0 <= k_max and len(ops) <= u_max
+        assert t["ev_ptr"][r1] - t["ev_ptr"][r0] <= e_max
+        assert len(np.unique(ops)) == len(ops)
+        for j in range(r0, r1):
+            r = t["rows"][j]
+            e = t["ev"][t["ev_ptr"][j]:t["ev_ptr"][j + 1]].astype(np.int64)
+            s_op, t_op = ops[e & 0xFFFF], ops[e >> 16]
+            assert np.all(s_op >= 0) and np.all(t_op < 0)
+            np.testing.assert_array_equal(s_op, ent[ptr[r]:ptr[r + 1], 0])
+            np.testing.assert_array_equal(-1 - t_op, ent[ptr[r]:ptr[r + 1], 1])
