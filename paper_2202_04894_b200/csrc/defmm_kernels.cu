@@ -1536,65 +1536,149 @@ struct P2PItems {
     const int64_t* out;
 };
 
-// Visit the sources [f0, f1) of one leaf's flattened run list in PACKED tiles
-// of up to P2P_TILE sources (a tile may span several runs: leaves in cfg3/cfg5
-// have 14-18 short runs).  The run table of the item is staged in shared
-// memory (windows of P2P_MAXRUNS runs); `load(slot, src)` stages source src in
-// tile slot `slot`, then `compute(cnt)` consumes the tile.
+// One work item = targets [t0, t1) of a leaf against the sources [f0, f1) of
+// its flattened run list (runs e in [e0, e1)).  Threads take a PAIR of
+// targets each (every staged source feeds two pair evaluations from
+// registers); when the leaf has fewer than P2P_NT pairs, `parts` =
+// P2P_NT / pairs threads share a pair's sources (every parts-th source) and
+// are reduced through shared memory in fixed part order (deterministic).
+// Sources are staged in PACKED tiles of up to P2P_TILE (a tile may span
+// several runs: cfg3/cfg5 leaves have 14-18 short runs), double-buffered: the
+// next tile's global loads are issued before the current tile is consumed
+// and stored after it, one barrier per tile.  The run table is staged in
+// windows of P2P_MAXRUNS runs.
+//   tgt(t) -> TS        target state (coordinates) of target t
+//   load(g) -> Src      staged form of source g
+//   pair(TS, Src, A&)   accumulate one pair
+//   store(t, A)         write the item's result for target t
 constexpr int P2P_MAXRUNS = 128;
+constexpr int P2P_PER = P2P_TILE / P2P_NT;  // staged sources per thread and tile
 
-template <typename LOAD, typename COMPUTE>
-__device__ __forceinline__ void for_packed_tiles(const int64_t* src_lo, const int64_t* src_hi, int64_t e0,
-                                                 int64_t e1, int64_t f0, int64_t f1, int64_t* rlo,
-                                                 int64_t* rpre, LOAD&& load, COMPUTE&& compute) {
-    int64_t base = 0;  // flattened offset of the first run of the window
-    for (int64_t w0 = e0; w0 < e1 && base < f1; w0 += P2P_MAXRUNS) {
-        const int nr = (int)((e1 - w0) < P2P_MAXRUNS ? (e1 - w0) : P2P_MAXRUNS);
-        __syncthreads();
-        for (int k = threadIdx.x; k < nr; k += blockDim.x) {
-            rlo[k] = src_lo[w0 + k];
-            rpre[k + 1] = src_hi[w0 + k] - src_lo[w0 + k];
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {  // inclusive prefix of the run lengths (<= 128 adds)
-            int64_t acc = base;
-            rpre[0] = base;
-            for (int k = 1; k <= nr; ++k) {
-                acc += rpre[k];
-                rpre[k] = acc;
-            }
-        }
-        __syncthreads();
-        const int64_t wend = rpre[nr];
-        const int64_t lo = f0 > base ? f0 : base, hi = f1 < wend ? f1 : wend;
-        for (int64_t fb = lo; fb < hi; fb += P2P_TILE) {
-            const int cnt = (int)((hi - fb) < P2P_TILE ? (hi - fb) : P2P_TILE);
+template <typename Src, typename A, typename TGT, typename LOAD, typename PAIR, typename STORE>
+__device__ __forceinline__ void p2p_item(int64_t t0, int64_t t1, int64_t e0, int64_t e1, int64_t f0, int64_t f1,
+                                         const int64_t* __restrict__ src_lo, const int64_t* __restrict__ src_hi,
+                                         Src (*tiles)[P2P_TILE], A (*red)[P2P_NT], int64_t* rlo, int64_t* rpre,
+                                         TGT&& tgt, LOAD&& load, PAIR&& pair, STORE&& store) {
+    const int64_t np_all = (t1 - t0 + 1) / 2;
+    const int np = (int)(np_all < P2P_NT ? np_all : P2P_NT);
+    const int parts = P2P_NT / np;
+    const int pi = threadIdx.x % np, part = threadIdx.x / np;
+    for (int64_t pb = 0; pb < np_all; pb += np) {
+        const int64_t ta = t0 + 2 * (pb + pi), tb = ta + 1;
+        const bool va = part < parts && ta < t1, vb = va && tb < t1;
+        const auto TA = tgt(va ? ta : t0);
+        const auto TB = tgt(vb ? tb : (va ? ta : t0));
+        A acca{}, accb{};
+        int64_t base = 0;  // flattened offset of the first run of the window
+        for (int64_t w0 = e0; w0 < e1 && base < f1; w0 += P2P_MAXRUNS) {
+            const int nr = (int)((e1 - w0) < P2P_MAXRUNS ? (e1 - w0) : P2P_MAXRUNS);
             __syncthreads();
-            for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
-                const int64_t g = fb + k;
-                int r = 0, top = nr;  // last run with rpre[r] <= g
-                while (top - r > 1) {
-                    const int mid = (r + top) >> 1;
-                    if (rpre[mid] <= g) r = mid; else top = mid;
+            for (int k = threadIdx.x; k < nr; k += P2P_NT) {
+                rlo[k] = src_lo[w0 + k];
+                rpre[k + 1] = src_hi[w0 + k] - src_lo[w0 + k];
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {  // inclusive prefix of the run lengths (<= 128 adds)
+                int64_t acc = base;
+                rpre[0] = base;
+                for (int k = 1; k <= nr; ++k) {
+                    acc += rpre[k];
+                    rpre[k] = acc;
                 }
-                load(k, rlo[r] + (g - rpre[r]));
             }
             __syncthreads();
-            compute(cnt);
+            const int64_t wend = rpre[nr];
+            const int64_t lo = f0 > base ? f0 : base, hi = f1 < wend ? f1 : wend;
+            auto fetch = [&](int64_t fb, int cnt, Src (&v)[P2P_PER]) {
+#pragma unroll
+                for (int j = 0; j < P2P_PER; ++j) {
+                    const int k = threadIdx.x + j * P2P_NT;
+                    if (k < cnt) {
+                        const int64_t g = fb + k;
+                        int r = 0, top = nr;  // last run with rpre[r] <= g
+                        while (top - r > 1) {
+                            const int mid = (r + top) >> 1;
+                            if (rpre[mid] <= g) r = mid; else top = mid;
+                        }
+                        v[j] = load(rlo[r] + (g - rpre[r]));
+                    }
+                }
+            };
+            auto put = [&](int buf, int cnt, const Src (&v)[P2P_PER]) {
+#pragma unroll
+                for (int j = 0; j < P2P_PER; ++j) {
+                    const int k = threadIdx.x + j * P2P_NT;
+                    if (k < cnt) tiles[buf][k] = v[j];
+                }
+            };
+            if (lo < hi) {
+                Src v[P2P_PER];
+                int cnt = (int)((hi - lo) < P2P_TILE ? (hi - lo) : P2P_TILE);
+                fetch(lo, cnt, v);
+                put(0, cnt, v);
+                __syncthreads();
+                int buf = 0;
+                for (int64_t fb = lo; fb < hi; fb += P2P_TILE) {
+                    const int64_t fn = fb + P2P_TILE;
+                    const int cn = fn < hi ? (int)((hi - fn) < P2P_TILE ? (hi - fn) : P2P_TILE) : 0;
+                    if (cn) fetch(fn, cn, v);  // in flight while the current tile is consumed
+                    if (va) {
+                        const Src* tl = tiles[buf];
+#pragma unroll 2
+                        for (int k = part; k < cnt; k += parts) {
+                            const Src sk = tl[k];
+                            pair(TA, sk, acca);
+                            pair(TB, sk, accb);
+                        }
+                    }
+                    if (cn) put(buf ^ 1, cn, v);
+                    __syncthreads();
+                    buf ^= 1;
+                    cnt = cn;
+                }
+            }
+            base = wend;
         }
-        base = wend;
+        red[0][threadIdx.x] = acca;
+        red[1][threadIdx.x] = accb;
+        __syncthreads();
+        if (part == 0 && va) {
+            A a = red[0][pi], b = red[1][pi];
+            for (int q = 1; q < parts; ++q) {
+                a = a + red[0][pi + q * np];
+                b = b + red[1][pi + q * np];
+            }
+            store(ta, a);
+            if (vb) store(tb, b);
+        }
+        __syncthreads();
     }
 }
 
-// `split` threads share the sources of a PAIR of targets (each staged source
-// feeds two pair evaluations from registers); fixed-order shuffle reduction.
-__device__ __forceinline__ int p2p_split(int64_t nt) {
-    const int64_t pairs = (nt + 1) / 2;
-    return pairs <= 16 ? 8 : pairs <= 32 ? 4 : pairs <= 64 ? 2 : 1;
-}
+struct P2PAcc64 {  // FP64 complex partial sum
+    double re, im;
+    __device__ P2PAcc64 operator+(const P2PAcc64& o) const { return {re + o.re, im + o.im}; }
+};
+struct P2PAcc32 {
+    float re, im;
+    __device__ P2PAcc32 operator+(const P2PAcc32& o) const { return {re + o.re, im + o.im}; }
+};
+struct P2PSrc64 {  // source position + charge / (4 pi)
+    double x, y, z;
+    double2 q;
+};
+struct P2PTgt64 {
+    double x, y, z;
+};
 
+#ifndef DEFMM_P2P_MINB64
+#define DEFMM_P2P_MINB64 1
+#endif
+#ifndef DEFMM_P2P_MINB32
+#define DEFMM_P2P_MINB32 8
+#endif
 template <typename R>
-__global__ void __launch_bounds__(P2P_NT) p2p_kernel(
+__global__ void __launch_bounds__(P2P_NT, DEFMM_P2P_MINB64) p2p_kernel(
     int64_t n, P2PItems it, const int64_t* __restrict__ tgt_lo, const int64_t* __restrict__ tgt_hi,
     const int64_t* __restrict__ ptr, const int64_t* __restrict__ src_lo,
     const int64_t* __restrict__ src_hi, const double* __restrict__ tx,
@@ -1602,66 +1686,32 @@ __global__ void __launch_bounds__(P2P_NT) p2p_kernel(
     const double* __restrict__ py, const double* __restrict__ pz, const cx<R>* __restrict__ q,
     double kappa, double tol, cx<R>* __restrict__ near, cx<R>* __restrict__ partial) {
     using V = cx<R>;
-    __shared__ double sx[P2P_TILE], sy[P2P_TILE], sz[P2P_TILE];
-    __shared__ double2 sq[P2P_TILE];  // q / (4 pi)
-    const double inv4pi = 1.0 / (4.0 * 3.141592653589793);
+    __shared__ P2PSrc64 tiles[2][P2P_TILE];
+    __shared__ P2PAcc64 red[2][P2P_NT];
     __shared__ int64_t rlo[P2P_MAXRUNS], rpre[P2P_MAXRUNS + 1];
-    for (int64_t item = blockIdx.x; item < n; item += gridDim.x) {
-    const int leaf = it.leaf[item];
-    const int64_t f0 = it.f0[item], f1 = it.f1[item], ob = it.out[item];
-    const int64_t t0 = tgt_lo[leaf], t1 = tgt_hi[leaf];
-    const int split = p2p_split(t1 - t0);
-    const int per_pass = 2 * (P2P_NT / split);
+    const double inv4pi = 1.0 / (4.0 * 3.141592653589793);
     const double kpi = kappa / 3.141592653589793;
-    const int64_t e0 = ptr[leaf], e1 = ptr[leaf + 1];
-    for (int64_t tb = t0; tb < t1; tb += per_pass) {
-        const int64_t ta = tb + 2 * (threadIdx.x / split), tb2 = ta + 1;
-        const int part = threadIdx.x % split;
-        const bool va = ta < t1, vb = tb2 < t1;
-        const double xa = va ? tx[ta] : 0.0, ya = va ? ty[ta] : 0.0, za = va ? tz[ta] : 0.0;
-        const double xb = vb ? tx[tb2] : xa, yb = vb ? ty[tb2] : ya, zb = vb ? tz[tb2] : za;
-        double2 acca = make_double2(0.0, 0.0), accb = make_double2(0.0, 0.0);
-        for_packed_tiles(
-            src_lo, src_hi, e0, e1, f0, f1, rlo, rpre,
-            [&](int k, int64_t g) {
-                sx[k] = px[g];
-                sy[k] = py[g];
-                sz[k] = pz[g];
+    for (int64_t item = blockIdx.x; item < n; item += gridDim.x) {
+        const int leaf = it.leaf[item];
+        const int64_t f0 = it.f0[item], f1 = it.f1[item], ob = it.out[item];
+        const int64_t t0 = tgt_lo[leaf], t1 = tgt_hi[leaf];
+        p2p_item(
+            t0, t1, ptr[leaf], ptr[leaf + 1], f0, f1, src_lo, src_hi, tiles, red, rlo, rpre,
+            [&](int64_t t) { return P2PTgt64{tx[t], ty[t], tz[t]}; },
+            [&](int64_t g) {
                 const double2 qq = to_d(q[g]);
-                sq[k] = make_double2(qq.x * inv4pi, qq.y * inv4pi);
+                return P2PSrc64{px[g], py[g], pz[g], make_double2(qq.x * inv4pi, qq.y * inv4pi)};
             },
-            [&](int cnt) {
-                if (va) {
-                    for (int k = part; k < cnt; k += split) {
-                        const double x = sx[k], y = sy[k], z = sz[k];
-                        const double2 qs = sq[k];
-                        const double2 ga = helm_pair_p2p(xa - x, ya - y, za - z, qs, kpi, tol);
-                        const double2 gb = helm_pair_p2p(xb - x, yb - y, zb - z, qs, kpi, tol);
-                        acca.x += ga.x;
-                        acca.y += ga.y;
-                        accb.x += gb.x;
-                        accb.y += gb.y;
-                    }
-                }
+            [&](const P2PTgt64& t, const P2PSrc64& s, P2PAcc64& a) {
+                const double2 g = helm_pair_p2p(t.x - s.x, t.y - s.y, t.z - s.z, s.q, kpi, tol);
+                a.re += g.x;
+                a.im += g.y;
+            },
+            [&](int64_t t, const P2PAcc64& a) {
+                const V v = from_d<V>(make_double2(a.re, a.im));
+                if (ob < 0) near[t] = v;
+                else partial[ob + (t - t0)] = v;
             });
-        for (int off = 1; off < split; off <<= 1) {
-            acca.x += __shfl_xor_sync(0xffffffffu, acca.x, off);
-            acca.y += __shfl_xor_sync(0xffffffffu, acca.y, off);
-            accb.x += __shfl_xor_sync(0xffffffffu, accb.x, off);
-            accb.y += __shfl_xor_sync(0xffffffffu, accb.y, off);
-        }
-        if (part == 0) {
-            if (va) {
-                if (ob < 0) near[ta] = from_d<V>(acca);
-                else partial[ob + (ta - t0)] = from_d<V>(acca);
-            }
-            if (vb) {
-                if (ob < 0) near[tb2] = from_d<V>(accb);
-                else partial[ob + (tb2 - t0)] = from_d<V>(accb);
-            }
-        }
-    }
-    __syncthreads();  // the next item restages the run table and tiles
     }
 }
 
@@ -1760,14 +1810,20 @@ __device__ __forceinline__ void rel_f32(double x, double c, float& hi, float& lo
 }
 
 template <bool HILO>
-__global__ void __launch_bounds__(P2P_NT) p2p_f32_kernel(
+struct P2PTgt32 {
+    float t[6];  // offsets: hi x, y, z, then lo x, y, z (HILO)
+};
+
+template <bool HILO>
+__global__ void __launch_bounds__(P2P_NT, DEFMM_P2P_MINB32) p2p_f32_kernel(
     int64_t n, P2PItems it, const int64_t* __restrict__ tgt_lo, const int64_t* __restrict__ tgt_hi,
     const int64_t* __restrict__ ptr, const int64_t* __restrict__ src_lo,
     const int64_t* __restrict__ src_hi, const double* __restrict__ tx,
     const double* __restrict__ ty, const double* __restrict__ tz, const double* __restrict__ px,
     const double* __restrict__ py, const double* __restrict__ pz, const float2* __restrict__ q,
     double kappa, double tol, float2* __restrict__ near, float2* __restrict__ partial) {
-    __shared__ P2PF32Src<HILO> sp[P2P_TILE];
+    __shared__ P2PF32Src<HILO> tiles[2][P2P_TILE];
+    __shared__ P2PAcc32 red[2][P2P_NT];
     __shared__ int64_t rlo[P2P_MAXRUNS], rpre[P2P_MAXRUNS + 1];
     const float k2pi = (float)(kappa / (2.0 * 3.141592653589793));
     const float ftol = (float)tol;
@@ -1777,71 +1833,38 @@ __global__ void __launch_bounds__(P2P_NT) p2p_f32_kernel(
         const int64_t f0 = it.f0[item], f1 = it.f1[item], ob = it.out[item];
         const int64_t t0 = tgt_lo[leaf], t1 = tgt_hi[leaf];
         const double cx = tx[t0], cy = ty[t0], cz = tz[t0];  // reference point of the item
-        const int split = p2p_split(t1 - t0);
-        const int per_pass = 2 * (P2P_NT / split);
-        const int64_t e0 = ptr[leaf], e1 = ptr[leaf + 1];
-        for (int64_t tb = t0; tb < t1; tb += per_pass) {
-            const int64_t ta = tb + 2 * (threadIdx.x / split), tb2 = ta + 1;
-            const int part = threadIdx.x % split;
-            const bool va = ta < t1, vb = tb2 < t1;
-            float A[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            if (va) {
-                rel_f32<HILO>(tx[ta], cx, A[0], A[3]);
-                rel_f32<HILO>(ty[ta], cy, A[1], A[4]);
-                rel_f32<HILO>(tz[ta], cz, A[2], A[5]);
-            }
-            float B[6] = {A[0], A[1], A[2], A[3], A[4], A[5]};
-            if (vb) {
-                rel_f32<HILO>(tx[tb2], cx, B[0], B[3]);
-                rel_f32<HILO>(ty[tb2], cy, B[1], B[4]);
-                rel_f32<HILO>(tz[tb2], cz, B[2], B[5]);
-            }
-            float aar = 0.f, aai = 0.f, bar = 0.f, bai = 0.f;
-            for_packed_tiles(
-                src_lo, src_hi, e0, e1, f0, f1, rlo, rpre,
-                [&](int k, int64_t g) {
-                    const float2 qq = q[g];
-                    P2PF32Src<HILO> v;
-                    float lx, ly, lz;
-                    rel_f32<HILO>(px[g], cx, v.a.x, lx);
-                    rel_f32<HILO>(py[g], cy, v.a.y, ly);
-                    rel_f32<HILO>(pz[g], cz, v.a.z, lz);
-                    v.a.w = qq.x * inv4pi;
-                    if constexpr (HILO) {
-                        v.b = make_float4(lx, ly, lz, qq.y * inv4pi);
-                    } else {
-                        v.qi = qq.y * inv4pi;
-                    }
-                    sp[k] = v;
-                },
-                [&](int cnt) {
-                    if (va) {
-#pragma unroll 2
-                        for (int k = part; k < cnt; k += split) {
-                            const P2PF32Src<HILO> sk = sp[k];
-                            pair_f32<HILO>(A, sk, k2pi, ftol, aar, aai);
-                            pair_f32<HILO>(B, sk, k2pi, ftol, bar, bai);
-                        }
-                    }
-                });
-            for (int off = 1; off < split; off <<= 1) {
-                aar += __shfl_xor_sync(0xffffffffu, aar, off);
-                aai += __shfl_xor_sync(0xffffffffu, aai, off);
-                bar += __shfl_xor_sync(0xffffffffu, bar, off);
-                bai += __shfl_xor_sync(0xffffffffu, bai, off);
-            }
-            if (part == 0) {
-                if (va) {
-                    if (ob < 0) near[ta] = make_float2(aar, aai);
-                    else partial[ob + (ta - t0)] = make_float2(aar, aai);
+        p2p_item(
+            t0, t1, ptr[leaf], ptr[leaf + 1], f0, f1, src_lo, src_hi, tiles, red, rlo, rpre,
+            [&](int64_t t) {
+                P2PTgt32<HILO> T;
+                rel_f32<HILO>(tx[t], cx, T.t[0], T.t[3]);
+                rel_f32<HILO>(ty[t], cy, T.t[1], T.t[4]);
+                rel_f32<HILO>(tz[t], cz, T.t[2], T.t[5]);
+                return T;
+            },
+            [&](int64_t g) {
+                const float2 qq = q[g];
+                P2PF32Src<HILO> v;
+                float lx, ly, lz;
+                rel_f32<HILO>(px[g], cx, v.a.x, lx);
+                rel_f32<HILO>(py[g], cy, v.a.y, ly);
+                rel_f32<HILO>(pz[g], cz, v.a.z, lz);
+                v.a.w = qq.x * inv4pi;
+                if constexpr (HILO) {
+                    v.b = make_float4(lx, ly, lz, qq.y * inv4pi);
+                } else {
+                    v.qi = qq.y * inv4pi;
                 }
-                if (vb) {
-                    if (ob < 0) near[tb2] = make_float2(bar, bai);
-                    else partial[ob + (tb2 - t0)] = make_float2(bar, bai);
-                }
-            }
-        }
-        __syncthreads();  // the next item restages the run table and tiles
+                return v;
+            },
+            [&](const P2PTgt32<HILO>& T, const P2PF32Src<HILO>& s, P2PAcc32& a) {
+                pair_f32<HILO>(T.t, s, k2pi, ftol, a.re, a.im);
+            },
+            [&](int64_t t, const P2PAcc32& a) {
+                const float2 v = make_float2(a.re, a.im);
+                if (ob < 0) near[t] = v;
+                else partial[ob + (t - t0)] = v;
+            });
     }
 }
 
