@@ -53,8 +53,8 @@ def _args():
     ap.add_argument("--p2p-overlap", default=None, choices=[None, "upward", "m2l", "full"])
     ap.add_argument("--p2p-grid", type=int, default=None, help="persistent P2P grid (CTAs; 0 = one per item)")
     ap.add_argument("--far-priority", type=int, default=None, help="far field on a high-priority stream (1/0)")
-    ap.add_argument("--m2l-levels", default="hybrid_rows",
-                    choices=["hybrid", "hybrid_rows", "blocked_all", "rows", "slice_all", "quad_all", "tiles",
+    ap.add_argument("--m2l-levels", default="auto",
+                    choices=["auto", "hybrid", "hybrid_rows", "blocked_all", "rows", "slice_all", "quad_all", "tiles",
                              "tiles_all"])
     ap.add_argument("--m2l", default=None, help="M2L kernel variant (hybrid | derived | canonical)")
     return ap.parse_args()

@@ -10,6 +10,7 @@ libdefmm_b200 kernel called through the C-ABI; there is no CPU path.
 
 from __future__ import annotations
 
+import os
 import time
 
 import numpy as np
@@ -175,7 +176,7 @@ class FmmPlan:
 
     def __init__(self, targets, sources=None, config: FmmConfig = FmmConfig(), device="cuda",
                  keep_events: bool = False, charges=None, reuse: "FmmPlan | None" = None,
-                 shard=None, allreduce=None, m2l: str = "hybrid_rows"):
+                 shard=None, allreduce=None, m2l: str = "auto", m2l_levels: dict | None = None):
         """``reuse``: share the host tree + lists of an existing plan built for
         the same geometry and (order, ncrit, eta, kappa) -- e.g. to run the same
         lists at another storage precision.
@@ -194,6 +195,7 @@ class FmmPlan:
         # "hybrid" (per-level choice), "blocked_all" (every level blocked) or
         # "rows" (no level blocked) -- decides the lists built for the hybrid path
         self.m2l_variant_default = m2l
+        self.m2l_level_override = m2l_levels
         if reuse is not None:
             rc = reuse.config
             if (rc.order, rc.ncrit, rc.eta, rc.kappa, rc.hf_switch, rc.hard_depth_cap) != (
@@ -377,12 +379,67 @@ class FmmPlan:
     # events per parent-pair block above which a level's M2L runs blocked
     BLOCKED_MIN_EVENTS_PER_BLOCK = 32.0
 
+    # M2L kernel per level for each mode: (dense level, sparse level)
+    _MODE_KINDS = {
+        "auto": ("blocked", "rows"), "hybrid_rows": ("blocked", "rows"), "hybrid": ("blocked", "quad"), "rows": ("rows", "rows"),
+        "blocked_all": ("blocked", "blocked"), "quad_all": ("quad", "quad"), "tiles": ("blocked", "tile"),
+        "tiles_all": ("tile", "tile"), "slice_all": ("slice", "slice"),
+    }
+
+    # "auto": a sparse level runs the quad kernel when its quads are this full
+    # (complex64 only): cfg2 L6 (cube faces, 13.3 events/quad) wins 6% of the
+    # M2L; 7-9 events/quad (cfg2 L4-5, cfg3) and every complex128 level lose
+    # (profiles/r01_summary_v5.md)
+    QUAD_MIN_EVENTS_PER_QUAD = 12.0
+
+    def _quad_fill(self, levels, blev, glev_full, nblk) -> dict:
+        """level -> mean M2L events per quad of its parent-pair blocks."""
+        p = self.plan
+        out = {}
+        for lv in levels:
+            gsel = np.nonzero(glev_full == lv)[0]
+            if gsel.size == 0:
+                continue
+            bsel = np.nonzero(blev == lv)[0]
+            bptr = np.concatenate([[0], np.cumsum(nblk[gsel])]).astype(np.int64)
+            qd, _ = _quads(p.blk_src[bsel], p.blk_trans[bsel], p.blk_mask[bsel], bptr)
+            if qd.shape[0]:
+                out[int(lv)] = float(np.bitwise_count(qd[:, 13].astype(np.uint64)).mean())
+        return out
+
+    def _level_kinds(self, levels, dense, quad_fill=None) -> dict:
+        """level -> M2L kernel ("rows", "blocked", "quad", "tile", "slice")
+        from the mode, then per-level overrides (``m2l_levels=`` dict or
+        DEFMM_M2L_LEVELS="4:quad,6:rows")."""
+        mode = self.m2l_variant_default
+        if mode not in self._MODE_KINDS:
+            raise ValueError(f"unknown M2L mode {mode!r}")
+        kd, ks = self._MODE_KINDS[mode]
+        kinds = {int(lv): (kd if int(lv) in dense else ks) for lv in levels}
+        if mode == "auto" and self.config.dtype == "c64":
+            for lv, fill in (quad_fill or {}).items():
+                if kinds.get(lv) == "rows" and fill >= self.QUAD_MIN_EVENTS_PER_QUAD:
+                    kinds[lv] = "quad"
+        over = dict(self.m2l_level_override or {})
+        env = os.environ.get("DEFMM_M2L_LEVELS", "")
+        for tok in filter(None, env.split(",")):
+            lv, k = tok.split(":")
+            over[int(lv)] = k
+        for lv, k in over.items():
+            if k not in ("rows", "blocked", "quad", "tile", "slice"):
+                raise ValueError(f"unknown M2L kernel {k!r} for level {lv}")
+            if int(lv) in kinds:
+                kinds[int(lv)] = k
+        return kinds
+
     def _host_lists(self) -> dict:
-        """Per-level hybrid M2L: levels whose parent-pair blocks are dense
-        (volume-like, >= BLOCKED_MIN_EVENTS_PER_BLOCK events per block) run
-        the blocked kernel (K7 v3, operand reuse in registers), sparse
-        (surface-like) levels the row kernel (its blocks would be mostly
-        predicated-off pairs) -- profiles/r01_summary_v3.md."""
+        """Per-level M2L kernel choice: levels whose parent-pair blocks are
+        dense (volume-like, >= BLOCKED_MIN_EVENTS_PER_BLOCK events per block)
+        run the blocked kernel (K7 v3, operand reuse in registers), sparse
+        (surface-like) levels the row kernel by default (their blocks would be
+        mostly predicated-off pairs) -- profiles/r01_summary_v3.md, v4.md.
+        lhat rows: grouped (blocked + quad) rows, then slice rows, then tile
+        rows (one F2L launch over all of them)."""
         h = self._host_lists_all()
         p, tt = self.plan, self.tt
         rows = h["rows"]
@@ -399,74 +456,75 @@ class FmmPlan:
             sel = blev == lev
             if ev[sel].mean() >= self.BLOCKED_MIN_EVENTS_PER_BLOCK:
                 dense.add(int(lev))
-        mode = self.m2l_variant_default
-        if mode in ("rows", "slice_all", "quad_all", "tiles_all"):
-            dense = set()
-        elif mode == "blocked_all":
-            dense = set(int(x) for x in np.unique(blev))
-        is_dense = np.isin(rlev, list(dense)) if dense else np.zeros(rows.shape[0], bool)
-        dense_rows = rows[is_dense]
-        # rows of sparse levels -> slice kernel (default) or row kernel
-        keep_rows, rptr, rsel = _sub_csr(h["row_ptr"], ~is_dense)
-        sparse_rows = rows[~is_dense]
+        fill = None
+        if self.m2l_variant_default == "auto" and self.config.dtype == "c64":
+            fill = self._quad_fill([lv for lv in np.unique(rlev) if int(lv) not in dense], blev, glev_full, nblk)
+        self.quad_fill = fill
+        kinds = self._level_kinds(np.unique(rlev), dense, fill)
+        self.level_kinds = kinds
+        rkind = np.array([kinds[int(lv)] for lv in rlev], dtype=object) if rows.size else np.zeros(0, object)
         z = np.zeros(0, np.int64)
-        no_slice = self._slice_lists(np.zeros(1, np.int64), np.zeros((0, 2), np.int32), z, 0)
-        h["rk_rows"], h["rk_ptr"], h["rk_ent"] = z, np.zeros(1, np.int64), np.zeros((0, 2), np.int32)
-        h["slice"] = no_slice
-        quad = mode in ("hybrid", "quad_all")
-        if mode in ("rows", "hybrid_rows"):
-            h["rk_rows"], h["rk_ptr"], h["rk_ent"] = sparse_rows, rptr, h["ent"][rsel]
-        elif mode == "slice_all":
-            h["slice"] = self._slice_lists(rptr, h["ent"][rsel], rlev[~is_dense], 0)
+
+        def pick(*ks):
+            return np.isin(rkind, list(ks)) if rows.size else np.zeros(0, bool)
+
+        # row kernel
+        is_rows = pick("rows")
+        # tiles (rows whose own operands exceed a tile fall back to the row kernel)
         h["tl"] = None
-        if mode in ("tiles", "tiles_all"):
-            # sparse-level rows -> shared-memory tiles (K7 v6); rows whose own
-            # operands exceed a tile -> row kernel
-            sp_ids = np.nonzero(~is_dense)[0]
-            slot = rows[sp_ids]
-            order = sp_ids[np.lexsort((p.l_cell[slot], p.l_dir[slot], rlev[sp_ids]))]
+        is_tile = pick("tile")
+        if is_tile.any():
+            t_ids = np.nonzero(is_tile)[0]
+            slot = rows[t_ids]
+            order = t_ids[np.lexsort((p.l_cell[slot], p.l_dir[slot], rlev[t_ids]))]
             tl = self._tile_lists(order, h)
             h["tl"] = tl
-            untiled = np.setdiff1d(sp_ids, tl["rows"])
-            sel_mask = np.zeros(rows.shape[0], bool)
-            sel_mask[untiled] = True
-            _, uptr, usel = _sub_csr(h["row_ptr"], sel_mask)
-            h["rk_rows"], h["rk_ptr"], h["rk_ent"] = rows[untiled], uptr, h["ent"][usel]
-        if quad:  # sparse levels -> quad kernel over the blocks of their groups
-            is_dense = np.ones(rows.shape[0], bool)
-            dense_rows = rows
-        # groups of dense levels -> blocked kernel, rows renumbered into lhat
+            is_rows = is_rows.copy()
+            is_rows[np.setdiff1d(t_ids, tl["rows"])] = True
+        _, rptr, rsel = _sub_csr(h["row_ptr"], is_rows)
+        h["rk_rows"], h["rk_ptr"], h["rk_ent"] = rows[is_rows], rptr, h["ent"][rsel]
+        # grouped rows (blocked + quad)
+        is_grp = pick("blocked", "quad")
+        grp_rows = rows[is_grp]
+        # slice rows
+        is_slice = pick("slice")
+        n_grp = int(grp_rows.shape[0])
+        if is_slice.any():
+            _, sptr, ssel = _sub_csr(h["row_ptr"], is_slice)
+            h["slice"] = self._slice_lists(sptr, h["ent"][ssel], rlev[is_slice], n_grp)
+        else:
+            h["slice"] = self._slice_lists(np.zeros(1, np.int64), np.zeros((0, 2), np.int32), z, 0)
+        # lhat rows: grouped, slice, tile
+        parts = [grp_rows, rows[is_slice]]
+        if h["tl"] is not None:
+            h["tl"]["lhat_base"] = n_grp + int(is_slice.sum())
+            parts.append(rows[h["tl"]["rows"]])
+        h["bk_rows"] = np.concatenate(parts) if parts else z
+        # groups of grouped levels, rows renumbered into lhat
         gr = h["grp_rows"]
         gr_slots = np.where(gr >= 0, rows[np.maximum(gr, 0)] if rows.size else -1, -1)
-        gid = _rows_to_ids(gr_slots, dense_rows)
+        gid = _rows_to_ids(gr_slots, grp_rows)
         gkeep = np.any(gid >= 0, axis=1)
         _, gptr, bsel = _sub_csr(h["grp_ptr"], gkeep)
-        # lhat rows: blocked (+ quad) rows, then slice or tile rows (one F2L launch)
-        h["bk_rows"] = np.concatenate([dense_rows, sparse_rows if h["slice"]["n_batch"] else z])
-        if h["tl"] is not None:
-            h["tl"]["lhat_base"] = int(dense_rows.shape[0])
-            h["bk_rows"] = np.concatenate([dense_rows, rows[h["tl"]["rows"]]])
-        gptr, grows = gptr, gid[gkeep]
+        grows = gid[gkeep]
         bsrc, btr, bmask, bkind = h["blk_src"][bsel], h["blk_trans"][bsel], h["blk_mask"][bsel], h["blk_kind"][bsel]
-        if quad:
-            # groups whose level is dense keep the blocked kernel, the others -> quads
-            glev = np.full(grows.shape[0], -1, np.int64)
-            first = np.where(grows >= 0, grows, np.iinfo(np.int64).max).min(axis=1) if grows.size else z
-            if grows.size:
-                glev = tt.level[p.l_cell[dense_rows[first]]]
-            gd = np.isin(glev, list(dense)) if dense else np.zeros(grows.shape[0], bool)
-            _, dptr, dsel = _sub_csr(gptr, gd)
-            _, qgptr, qsel = _sub_csr(gptr, ~gd)
+        # groups of quad levels -> quad kernel, the others -> blocked kernel
+        first = np.where(grows >= 0, grows, np.iinfo(np.int64).max).min(axis=1) if grows.size else z
+        glev = tt.level[p.l_cell[grp_rows[first]]] if grows.size else z
+        gq = np.array([kinds[int(lv)] == "quad" for lv in glev], bool) if grows.size else np.zeros(0, bool)
+        if gq.any():
+            _, dptr, dsel = _sub_csr(gptr, ~gq)
+            _, qgptr, qsel = _sub_csr(gptr, gq)
             quads, qptr = _quads(bsrc[qsel], btr[qsel], bmask[qsel], qgptr)
-            h["qd_ptr"], h["qd_rows"], h["quads"] = qptr, grows[~gd], quads
-            gptr, grows = dptr, grows[gd]
+            h["qd_ptr"], h["qd_rows"], h["quads"] = qptr, grows[gq], quads
+            gptr, grows = dptr, grows[~gq]
             bsrc, btr, bmask, bkind = bsrc[dsel], btr[dsel], bmask[dsel], bkind[dsel]
         else:
             h["qd_ptr"], h["qd_rows"], h["quads"] = np.zeros(1, np.int64), np.zeros((0, 8), np.int64), \
                 np.zeros((0, 16), np.int32)
         h["grp_ptr"], h["grp_rows"] = gptr, grows
         h["blk_src"], h["blk_trans"], h["blk_mask"], h["blk_kind"] = bsrc, btr, bmask, bkind
-        self.dense_levels = sorted(dense)
+        self.dense_levels = sorted(lv for lv, k in kinds.items() if k == "blocked")
         return h
 
     # tile kernel (K7 v6): operand slices of 128 B (c64: 16 x 8 B, c128:
@@ -772,15 +830,17 @@ class FmmPlan:
         R = "float" if self.config.dtype == "c64" else "double"
         if self.m2l_variant != "hybrid":
             return [f"m2l_rows_kernel<{R}, {self.L}> (all levels, {self.m2l_variant})"]
-        dense = list(self.dense_levels)
-        sparse = sorted(set(range(self.tt.depth + 1)) - set(dense))
+        kinds = getattr(self, "level_kinds", {})
+
+        def lv(k):
+            return sorted(l for l, x in kinds.items() if x == k)
+
         out = []
-        for n, name, lev in ((self.rk_rows.shape[0], "m2l_rows_kernel", sparse), (self.n_groups, "m2l_blocked_kernel", dense),
-                             (self.n_qgroups, "m2l_quad_kernel", sparse), (self.n_tiles, "m2l_tile_kernel", sparse),
-                             (self.n_slice_batch, "m2l_slice_kernel", sparse),
-                             (self.bk_rows.shape[0], "f2l_rows_kernel", None)):
+        for n, name, k in ((self.rk_rows.shape[0], "m2l_rows_kernel", "rows"), (self.n_groups, "m2l_blocked_kernel", "blocked"),
+                           (self.n_qgroups, "m2l_quad_kernel", "quad"), (self.n_tiles, "m2l_tile_kernel", "tile"),
+                           (self.n_slice_batch, "m2l_slice_kernel", "slice"), (self.bk_rows.shape[0], "f2l_rows_kernel", None)):
             if n:
-                out.append(f"{name}<{R}, {self.L}>" + (f" (levels {lev})" if lev is not None else ""))
+                out.append(f"{name}<{R}, {self.L}>" + (f" (levels {lv(k)})" if k is not None else ""))
         return out
 
     @property
