@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Summarise an ncu capture (``ncu -i X.ncu-rep --page raw --csv`` output, or a
 ``--csv --log-file`` metrics list) into JSON: per kernel name, the mean of each
-numeric metric over its launches and the launch count.
+numeric metric over its launches (bytes, nanoseconds; raw-page units are
+converted) and the launch count.
 
   python tools/ncu_to_json.py capture.csv [--prefix cfg2:c64:] > out.json
 """
@@ -12,6 +13,11 @@ import csv
 import json
 import sys
 from collections import defaultdict
+
+
+# raw-page units -> bytes / nanoseconds / Hz (launch lists are already in base units)
+_SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+          "ns": 1.0, "nsecond": 1.0, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6, "s": 1e9, "second": 1e9}
 
 
 def _num(x):
@@ -47,13 +53,14 @@ def parse(path):
             if len(r) > vi and _num(r[vi]) is not None:
                 out[short(r[ki])][r[mi]].append(_num(r[vi]))
     else:  # raw page: one row per launch, one column per metric (row 2 = units)
+        units = rows[hdr + 1]
         for r in rows[hdr + 2:]:
             if len(r) != len(h):
                 continue
             for j, name in enumerate(h):
                 v = _num(r[j])
                 if v is not None and "__" in name:
-                    out[short(r[ki])][name].append(v)
+                    out[short(r[ki])][name].append(v * _SCALE.get(units[j].strip(), 1.0))
     res = {}
     for k, d in out.items():
         res[k] = {m: sum(v) / len(v) for m, v in d.items()}
