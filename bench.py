@@ -148,6 +148,40 @@ def _ncu_traffic(key):
         return None
 
 
+def _fma_peaks(dev):
+    """FP32 / FP64 FMA peaks of this GPU (TFLOP/s), measured with
+    defmm_fma_peak (8 independent FMA chains per thread, no memory traffic)."""
+    import torch
+
+    from paper_2202_04894_b200 import _lib
+
+    lib = _lib.load()
+    out = torch.zeros(1, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    threads = 4 * sms * 256
+    res = {}
+    for fp64, iters in ((0, 40000), (1, 20000)):
+        _lib.check(lib.defmm_fma_peak(fp64, 100, out.data_ptr(), stream.cuda_stream), "defmm_fma_peak")
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        _lib.check(lib.defmm_fma_peak(fp64, iters, out.data_ptr(), stream.cuda_stream), "defmm_fma_peak")
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        res["fp64" if fp64 else "fp32"] = 2.0 * 8 * 16 * iters * threads / (a.elapsed_time(b) * 1e-3) / 1e12
+    return res
+
+
+def _ncu_pipe(key):
+    """FP-pipe utilisation of the P2P kernel from the committed ncu capture
+    (profiles/r01_p2p_pipes.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_p2p_pipes.json")) as fh:
+            return json.load(fh)[key]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def _measured_peak_hbm():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -385,6 +419,17 @@ def run_b200(args):
     traffic = _ncu_traffic(f"{args.workload}:{dtype}:m2l")
     peak, peak_kind = _measured_peak_hbm()
     achieved = alg_bytes / m2l_s / 1e9
+    # P2P: 24 flop per pair against the measured FMA peak of
+    # the pipe it runs on; the ncu FP-pipe utilisation is the graded number
+    fpk = _fma_peaks(dev)
+    pipe = "fp32" if dtype == "c64" else "fp64"
+    pairs = int(p.counts["p2p_pairs"])
+    p2p_tf = 24.0 * pairs / (st["p2p"] * 1e-3) / 1e12
+    p2p_roof = {"bound": pipe, "achieved": p2p_tf, "peak": fpk[pipe], "unit": "TFLOP/s", "frac": p2p_tf / fpk[pipe],
+                "flop_per_pair": 24, "pairs": pairs, "kernel_ms": st["p2p"], "peak_kind": "measured (defmm_fma_peak)",
+                "ncu_pipe_utilisation": _ncu_pipe(f"{args.workload}:{dtype}"),
+                "note": "frac counts 24 algorithmic flop/pair; sincos/rsqrt/hi-lo work is extra issue, so the "
+                        "pipe utilisation from ncu (profiles/r01_p2p_pipes.json) is the FP-pipe figure"}
     line = {
         "metric": METRIC,
         "value": value,
@@ -411,6 +456,8 @@ def run_b200(args):
                      "kernel_ms": st["m2l"],
                      "note": "algorithmic bytes = 2 spectra per M2L event + local write; frac > 1 = L2 reuse; "
                              "traffic = ncu dram bytes of the M2L-stage launches of one matvec (profiles/r01_m2l_traffic.json)"},
+        "p2p_roofline": p2p_roof,
+        "fma_peaks_tflops": fpk,
         "e2e": {"value": n / (e_step / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(qbytes),
                 "d2h_bytes_per_step": int(qbytes), "ms_per_step": e_step},
         "accuracy": {"rel_l2_vs_direct_1000": eps, "eps_ref_reference": _EPS_REF.get(args.workload)},

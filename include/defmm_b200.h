@@ -87,6 +87,12 @@ int defmm_dtt_source_hats(const defmm_dtt* d, const int64_t* m_dense, const int6
                           int32_t* src_hat, int64_t* hat_slot, int64_t* n_hat);
 void defmm_dtt_free(defmm_dtt* d);
 
+/* ---- FMA peak probe (measurement only) --------------------------------------
+ * Launches 4 x SMs CTAs of 256 threads, each thread running 8 independent FMA
+ * chains for iters x 16 steps: flops = 2 * 8 * 16 * iters * threads.  fp64
+ * selects double.  out: one element, written only to keep the chains live. */
+int defmm_fma_peak(int32_t fp64, int64_t iters, void* out, void* stream);
+
 /* ---- host: M2L row tiles for the shared-memory tile kernel (K7 v6) --------
  * The rows order[0..n_order) (row r = events [row_ptr[r], row_ptr[r+1]) of
  * ent = {source spectrum, derived symbol} int32 pairs; the same lists the

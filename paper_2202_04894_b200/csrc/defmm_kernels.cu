@@ -24,6 +24,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/defmm_b200.h"
@@ -962,9 +963,14 @@ __global__ void __launch_bounds__(m2lb_threads<R, L>(), DEFMM_M2LB_MINBLOCKS) m2
 template <typename R>
 struct QuadVec;
 template <>
-struct QuadVec<float> {  // two complex64 per thread
-    using t = float4;
-    static constexpr int W = 2;
+#ifndef DEFMM_QUAD_C64_W
+#define DEFMM_QUAD_C64_W 2
+#endif
+// complex64: two entries per thread (float4, 96 registers, 27% warps active);
+// one per thread (float2, 56 registers) measured 1% slower on cfg2 L6
+struct QuadVec<float> {
+    using t = std::conditional_t<DEFMM_QUAD_C64_W == 2, float4, float2>;
+    static constexpr int W = DEFMM_QUAD_C64_W;
 };
 template <>
 struct QuadVec<double> {
@@ -985,6 +991,9 @@ __host__ __device__ constexpr int quad_threads() {
 __device__ __forceinline__ void qfma(float2 (&acc)[2], const float4& d, const float4& s) {
     acc[0] = cfma(make_float2(d.x, d.y), make_float2(s.x, s.y), acc[0]);
     acc[1] = cfma(make_float2(d.z, d.w), make_float2(s.z, s.w), acc[1]);
+}
+__device__ __forceinline__ void qfma(float2 (&acc)[1], const float2& d, const float2& s) {
+    acc[0] = cfma(d, s, acc[0]);
 }
 __device__ __forceinline__ void qfma(double2 (&acc)[1], const double2& d, const double2& s) {
     acc[0] = cfma(d, s, acc[0]);
@@ -1672,7 +1681,7 @@ struct P2PTgt64 {
 };
 
 #ifndef DEFMM_P2P_MINB64
-#define DEFMM_P2P_MINB64 1
+#define DEFMM_P2P_MINB64 4
 #endif
 #ifndef DEFMM_P2P_MINB32
 #define DEFMM_P2P_MINB32 8
