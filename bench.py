@@ -53,6 +53,8 @@ def _args():
     ap.add_argument("--p2p-overlap", default=None, choices=[None, "upward", "m2l", "full"])
     ap.add_argument("--p2p-grid", type=int, default=None, help="persistent P2P grid (CTAs; 0 = one per item)")
     ap.add_argument("--far-priority", type=int, default=None, help="far field on a high-priority stream (1/0)")
+    ap.add_argument("--exchange", default="halo", choices=["halo", "allreduce"],
+                    help="N > 1 multipole exchange: halo (span all-reduce + all_to_all) or a full all-reduce")
     ap.add_argument("--m2l-levels", default="auto",
                     choices=["auto", "hybrid", "hybrid_rows", "blocked_all", "rows", "slice_all", "quad_all", "tiles",
                              "tiles_all"])
@@ -347,13 +349,14 @@ def run_b200(args):
     other = "c128" if dtype == "c64" else "c64"
     cfg = FmmConfig(order=w.order, ncrit=w.ncrit, kappa=kappa, dtype=dtype)
 
-    def allreduce(t):  # NCCL sum of the partial multipoles (parallel.py)
+    def allreduce(t):  # NCCL sum of the whole multipole array (--exchange allreduce)
         dist.all_reduce(torch.view_as_real(t))
 
     shard = (rank, world) if world > 1 else None
+    # N > 1: halo exchange (span all-reduce + all_to_all of the read multipoles, parallel.py)
+    ar = allreduce if (shard and args.exchange == "allreduce") else None
     t0 = time.perf_counter()
-    plan = FmmPlan(pts, None, cfg, device=dev, charges=q, shard=shard, allreduce=allreduce if shard else None,
-                   m2l=args.m2l_levels)
+    plan = FmmPlan(pts, None, cfg, device=dev, charges=q, shard=shard, allreduce=ar, m2l=args.m2l_levels)
     setup_s = time.perf_counter() - t0
     if args.m2l:
         plan.m2l_variant = args.m2l
@@ -374,7 +377,7 @@ def run_b200(args):
     st2 = None
     if not args.no_secondary:
         plan2 = FmmPlan(pts, None, FmmConfig(order=w.order, ncrit=w.ncrit, kappa=kappa, dtype=other),
-                        device=dev, charges=q, reuse=plan, shard=shard, allreduce=allreduce if shard else None,
+                        device=dev, charges=q, reuse=plan, shard=shard, allreduce=ar,
                         m2l=args.m2l_levels)
         if args.p2p_overlap:
             plan2.p2p_overlap = args.p2p_overlap
@@ -446,7 +449,7 @@ def run_b200(args):
         "dtype": "f32 storage, f64 sums" if dtype == "c64" else "f64",
         "data": "synthetic",
         "config": dict(_workload_desc(w, n, dtype), l2_flush="256 MiB memset between timed iterations",
-                       parallelism=(f"morton-sharded x{world} (NCCL all-reduce of multipoles)"
+                       parallelism=(f"morton-sharded x{world} (NCCL {args.exchange} of multipoles)"
                                     if world > 1 else "single")),
         "stages_ms": {"upward_with_concurrent_p2p": st["upward"], "m2l": st["m2l"], "p2p": st["p2p"],
                       "downward": st["downward"]},

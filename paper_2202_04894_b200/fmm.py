@@ -373,8 +373,16 @@ class FmmPlan:
         else:
             rank, world = sa
             self.shard = make_shard(self.plan, self.tt, self.st, int(rank), int(world)) if int(world) > 1 else None
+        self.halo = None
         if self.shard is not None and self.shard.world > 1 and self.allreduce is None:
-            raise ValueError("a sharded plan needs allreduce= to complete the multipoles")
+            # halo exchange over torch.distributed (NCCL between GPUs)
+            import torch.distributed as dist
+
+            from .parallel import make_halo
+
+            if not (dist.is_available() and dist.is_initialized()):
+                raise ValueError("a sharded plan needs torch.distributed initialised (or allreduce=)")
+            self.halo = make_halo(self.plan, self.tt, self.shard.cuts, self.shard.rank, self.shard.world)
 
     # events per parent-pair block above which a level's M2L runs blocked
     BLOCKED_MIN_EVENTS_PER_BLOCK = 32.0
@@ -689,10 +697,23 @@ class FmmPlan:
     def _apply(self, out=None, stage_events=None):
         self.apply_upward(stage_events)
         if self.shard is not None:
-            # M2M is linear: summing the partial multipoles over the ranks
-            # completes every multipole (the one data-path collective)
-            self.allreduce(self.mult)
+            if self.allreduce is not None:
+                # M2M is linear: summing the partial multipoles over the ranks
+                # completes every multipole
+                self.allreduce(self.mult)
+            else:
+                from .parallel import halo_exchange
+
+                halo_exchange(self.mult, self._halo_dev())
         return self.apply_rest(out, stage_events)
+
+    def _halo_dev(self):
+        if getattr(self, "_halo_t", None) is None:
+            h = self.halo
+            dev = self.mult.device
+            idx = lambda a: torch.as_tensor(a, dtype=torch.int64, device=dev)  # noqa: E731
+            self._halo_t = (idx(h.span), idx(h.send), list(h.send_counts), idx(h.recv), list(h.recv_counts))
+        return self._halo_t
 
     def _near_field(self, stage_events):
         """P2P on the side stream (FP-pipe bound), concurrent with the far field."""

@@ -10,9 +10,14 @@ cells whose particle range intersects it ("active" cells):
 
 * upward: P2M on its own leaves, M2M on its active cells.  A cell spanning
   several chunks gets a PARTIAL multipole on each rank (its other sons are
-  zero there); because M2M is linear, one ``all_reduce(sum)`` of the nodal
-  multipole array over NCCL/NVLink completes every multipole on every rank --
-  the only data-path collective;
+  zero there); a cell inside one chunk is complete on its owner only;
+* halo exchange (the only data-path communication): one
+  ``all_reduce(sum)`` over the few spanning (top-of-tree) multipoles -- M2M is
+  linear, so the partial sums complete them -- and one ``all_to_all`` that
+  sends each rank exactly the complete nodal multipoles (L^3 each, 5-7x fewer
+  bytes than spectra) its M2L rows read from other ranks' chunks.  Index sets
+  are static per plan (``Halo``); ``allreduce=`` (sum of the whole multipole
+  array) remains for the virtual-rank tests;
 * M2F only for the spectra its own M2L rows read;
 * M2L rows, L2L slots and L2P/P2P leaves of its active target cells (shared
   top cells are computed redundantly by every rank that needs them), so the
@@ -30,7 +35,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["Shard", "leaf_costs", "partition_leaves", "make_shard"]
+__all__ = ["Shard", "Halo", "leaf_costs", "partition_leaves", "make_shard", "make_halo", "halo_exchange"]
 
 # relative unit costs measured on the B200 (profiles/r01_summary_v2.md, c64):
 # M2L ~2.9 ms / 10.8 M events; P2P ~0.77 ms / 3.83e8 pairs
@@ -89,6 +94,7 @@ class Shard:
     row_keep: np.ndarray  # M2L rows this rank computes
     l2l_keep: list  # per plan.l2l_levels entry: out mask
     leaf_keep: np.ndarray  # target leaves (plan.leaf_cells order)
+    cuts: np.ndarray = None  # particle cuts of all ranks (world + 1)
 
 
 def make_shard(plan, tt, st, rank: int, world: int, cuts=None) -> Shard:
@@ -110,4 +116,77 @@ def make_shard(plan, tt, st, rank: int, world: int, cuts=None) -> Shard:
     hat_keep[plan.m2l_rows_entries[e, 0]] = True
     l2l_keep = [active(plan.l_cell[outs]) for _, outs, *_ in plan.l2l_levels]
     leaf_keep = active(plan.leaf_cells)
-    return Shard(rank, world, lo, hi, p2m_idx, m2m_keep, hat_keep, row_keep, l2l_keep, leaf_keep)
+    return Shard(rank, world, lo, hi, p2m_idx, m2m_keep, hat_keep, row_keep, l2l_keep, leaf_keep, np.asarray(cuts))
+
+
+@dataclass
+class Halo:
+    """Static index sets of one rank's multipole exchange (slots into the
+    plan's multipole array; counts per peer rank, in rank order)."""
+    span: np.ndarray  # spanning multipoles (same list on every rank), all-reduced
+    send: np.ndarray  # complete multipoles this rank owns and others read, by destination
+    send_counts: list
+    recv: np.ndarray  # multipoles this rank reads from others, by source
+    recv_counts: list
+
+
+def _rank_span(plan, tt, cuts):
+    """First and last rank whose chunk intersects each multipole's cell."""
+    cells = plan.m_cell
+    a = np.searchsorted(cuts, tt.start[cells], side="right") - 1
+    b = np.searchsorted(cuts, tt.stop[cells] - 1, side="right") - 1
+    return a, b
+
+
+def _needed(plan, tt, cuts, r) -> np.ndarray:
+    """Multipole slots whose spectra rank r's M2L rows read (sorted)."""
+    lo, hi = int(cuts[r]), int(cuts[r + 1])
+    rc = plan.l_cell[plan.m2l_row_slot]
+    keep = (tt.start[rc] < hi) & (tt.stop[rc] > lo)
+    e = np.repeat(keep, np.diff(plan.m2l_row_ptr))
+    hats = np.unique(plan.m2l_rows_entries[e, 0])
+    return np.unique(plan.hat_slot[hats])
+
+
+def make_halo(plan, tt, cuts, rank: int, world: int) -> Halo:
+    cuts = np.asarray(cuts)
+    a, b = _rank_span(plan, tt, cuts)
+    span = np.nonzero(a != b)[0]
+    owner = np.where(a == b, a, -1)
+    need = [_needed(plan, tt, cuts, r) for r in range(world)]
+    send, send_counts, recv, recv_counts = [], [], [], []
+    for r in range(world):
+        if r == rank:
+            send_counts.append(0)
+            recv_counts.append(0)
+            continue
+        s_r = need[r][owner[need[r]] == rank]  # mine, read by r
+        v_r = need[rank][owner[need[rank]] == r]  # r's, read by me
+        send.append(s_r)
+        recv.append(v_r)
+        send_counts.append(int(s_r.shape[0]))
+        recv_counts.append(int(v_r.shape[0]))
+    cat = lambda xs: np.concatenate(xs).astype(np.int64) if xs else np.zeros(0, np.int64)  # noqa: E731
+    return Halo(span.astype(np.int64), cat(send), send_counts, cat(recv), recv_counts)
+
+
+def halo_exchange(mult, halo_dev, group=None):
+    """Complete the multipoles this rank's M2F reads.  ``mult``: (n_mult, L^3)
+    complex tensor; ``halo_dev`` = (span, send, send_counts, recv, recv_counts)
+    with the index tensors on mult's device.  Complex data travels as its real
+    view (NCCL / gloo have no complex types)."""
+    import torch
+    import torch.distributed as dist
+
+    span, send, send_counts, recv, recv_counts = halo_dev
+    if span.numel():
+        buf = mult.index_select(0, span)
+        dist.all_reduce(torch.view_as_real(buf), group=group)
+        mult.index_copy_(0, span, buf)
+    if sum(send_counts) + sum(recv_counts):
+        per = 2 * mult.shape[1]  # reals per multipole
+        sbuf = torch.view_as_real(mult.index_select(0, send)).contiguous()
+        rbuf = torch.empty((recv.shape[0], mult.shape[1], 2), dtype=sbuf.dtype, device=mult.device)
+        dist.all_to_all_single(rbuf.view(-1), sbuf.view(-1), [c * per for c in recv_counts],
+                               [c * per for c in send_counts], group=group)
+        mult.index_copy_(0, recv, torch.view_as_complex(rbuf))

@@ -274,6 +274,46 @@ def test_virtual_ranks_match_single_gpu(case, world):
     assert _rel(out.cpu().numpy(), g["pot"]) <= FP64_TOL
 
 
+@pytest.mark.parametrize("case,world", [("cubesurf4000", 2), ("volume3000", 3)])
+def test_virtual_ranks_halo_exchange_matches_single_gpu(case, world):
+    """The halo exchange of the N > 1 path (parallel.make_halo: span all-reduce
+    + owner -> reader copies of complete multipoles), emulated between virtual
+    ranks on one GPU with the same index sets: every rank's potentials, summed,
+    reproduce the single-plan matvec -- only the halo is exchanged."""
+    from paper_2202_04894_b200 import FmmConfig, FmmPlan
+    from paper_2202_04894_b200.parallel import make_halo
+
+    g = load_case(case)
+    cfg = FmmConfig(**g["config"])
+    base = FmmPlan(g["points"], None, cfg, charges=g["charges"])
+    ref = base.apply().clone()
+    ranks = [FmmPlan(g["points"], None, cfg, charges=g["charges"], reuse=base, shard=(r, world),
+                     allreduce=lambda t: None) for r in range(world)]
+    halos = [make_halo(base.plan, base.tt, r.shard.cuts, k, world) for k, r in enumerate(ranks)]
+    for r in ranks:
+        r.apply_upward()
+    dev = ranks[0].mult.device
+    idx = lambda a: torch.as_tensor(a, dtype=torch.int64, device=dev)  # noqa: E731
+    span = idx(halos[0].span)
+    tot = sum(r.mult.index_select(0, span) for r in ranks)
+    sent = {}
+    for k, h in enumerate(halos):  # owner k -> reader j, in rank order
+        off = 0
+        for j, c in enumerate(h.send_counts):
+            sent[(k, j)] = ranks[k].mult.index_select(0, idx(h.send[off:off + c]))
+            off += c
+    for j, (r, h) in enumerate(zip(ranks, halos)):
+        r.mult.index_copy_(0, span, tot)
+        off = 0
+        for k, c in enumerate(h.recv_counts):
+            if c:
+                r.mult.index_copy_(0, idx(h.recv[off:off + c]), sent[(k, j)])
+            off += c
+    out = sum(r.apply_rest().clone() for r in ranks)
+    assert _rel(out.cpu().numpy(), ref.cpu().numpy()) <= 1e-13
+    assert _rel(out.cpu().numpy(), g["pot"]) <= FP64_TOL
+
+
 def test_cuda_graph_replay_matches_eager():
     from paper_2202_04894_b200 import FmmConfig, FmmPlan
 

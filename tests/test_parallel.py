@@ -119,3 +119,48 @@ def test_sharding_rejects_two_tree_plans():
     pl = build_plan(tr2, tr, 5, 0.0, 1.0, 2.0)
     with pytest.raises(ValueError):
         make_shard(pl, tr2, tr, 0, 2)
+
+
+def _halo_worker(rank, world, port, case, q):
+    """Halo exchange (span all-reduce + all_to_all of owned complete multipoles)
+    over a real gloo group, on the exactly-additive emulation: afterwards every
+    multipole this rank's M2F reads equals the full particle count below it."""
+    from paper_2202_04894_b200.parallel import _needed, halo_exchange, make_halo
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        tr, pl = _plan(case)
+        sh = make_shard(pl, tr, tr, rank, world)
+        h = make_halo(pl, tr, sh.cuts, rank, world)
+        cnt = _partial_counts(tr, pl, sh).astype(np.float64)
+        mult = torch.from_numpy(np.stack([cnt, 2.0 * cnt], 1)).to(torch.complex128)
+        mult[:, 1] *= 1j
+        idx = lambda a: torch.as_tensor(a, dtype=torch.int64)  # noqa: E731
+        halo_exchange(mult, (idx(h.span), idx(h.send), h.send_counts, idx(h.recv), h.recv_counts))
+        need = _needed(pl, tr, sh.cuts, rank)
+        full = np.array([tr.stop[c] - tr.start[c] for c in pl.m_cell], np.float64)
+        got = mult.numpy()
+        ok = bool(np.array_equal(got[need, 0].real, full[need]) and np.array_equal(got[need, 1].imag, 2 * full[need]))
+        # the exchange moves far fewer multipoles than an all-reduce of all of them
+        q.put((rank, ok, int(h.span.shape[0]), int(h.send.shape[0]), int(h.recv.shape[0]), pl.n_mult))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case,world", [("cubesurf4000", 2), ("cubesurf4000", 3), ("volume3000", 4)])
+def test_halo_exchange_completes_every_needed_multipole(case, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    res = [q.get() for _ in range(world)]
+    assert all(p.exitcode == 0 for p in procs)
+    for rank, ok, n_span, n_send, n_recv, n_mult in res:
+        assert ok, rank
+        assert n_span + n_recv < n_mult  # a halo, not the whole multipole array
