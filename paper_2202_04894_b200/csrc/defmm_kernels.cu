@@ -259,6 +259,13 @@ __global__ void __launch_bounds__(128) p2m_kernel(
         ku[k] = (R)(d >= 0 ? kappa * beta * dirs[3 * d + k] : 0.0);
     }
     const int64_t s0 = cstart[c], s1 = cstop[c];
+    // e^{i ku (x_k - xh)} = e^{i ku x_k} e^{-i ku xh}: the node factors once per
+    // CTA, one sincos per particle and axis (HF keys only; LF: ku = 0)
+    __shared__ V T[3][L];
+    if (threadIdx.x < 3 * L) {
+        const int ax = threadIdx.x / L, k = threadIdx.x % L;
+        T[ax][k] = d >= 0 ? cexpi(ku[ax] * node<L, R>(k)) : cmk<V>((R)1, (R)0);
+    }
     V acc[PER];
 #pragma unroll
     for (int m = 0; m < PER; ++m) acc[m] = cz<V>();
@@ -271,9 +278,10 @@ __global__ void __launch_bounds__(128) p2m_kernel(
             const R xh = (R)((pp[base + p] - al[ax]) / beta);
             R S[L];
             lagrange<L, R>(xh, S);
-            const V qq = ax == 0 ? q[base + p] : cmk<V>((R)1, (R)0);
+            V qq = ax == 0 ? q[base + p] : cmk<V>((R)1, (R)0);
+            if (d >= 0) qq = cmul(qq, cexpi(-ku[ax] * xh));
 #pragma unroll
-            for (int k = 0; k < L; ++k) W[ax][p][k] = cmul(qq, cscale(cexpi(ku[ax] * (node<L, R>(k) - xh)), S[k]));
+            for (int k = 0; k < L; ++k) W[ax][p][k] = cmul(qq, cscale(T[ax][k], S[k]));
         }
         __syncthreads();
 #pragma unroll
@@ -1401,6 +1409,7 @@ __global__ void __launch_bounds__(64) l2p_kernel(
     constexpr int L3 = cube<L>();
     constexpr int NT = 64;
     __shared__ V loc[L3];
+    __shared__ V T[3][L];
     const int64_t i = blockIdx.x;
     const int c = leaf_cell[i];
     const double beta = lbeta[clevel[c]];
@@ -1424,13 +1433,21 @@ __global__ void __launch_bounds__(64) l2p_kernel(
             const int d = slot_dir[s];
             __syncthreads();
             for (int r = threadIdx.x; r < L3; r += NT) loc[r] = local[s * L3 + r];
+            // e^{i ku (xh - x_k)} = e^{i ku xh} e^{-i ku x_k}: node factors once
+            // per slot, one sincos per particle and axis (HF keys only)
+            if (threadIdx.x < 3 * L) {
+                const int ax = threadIdx.x / L, k = threadIdx.x % L;
+                const R ku = (R)(d >= 0 ? kappa * beta * dirs[3 * d + ax] : 0.0);
+                T[ax][k] = d >= 0 ? cexpi(-ku * node<L, R>(k)) : cmk<V>((R)1, (R)0);
+            }
             __syncthreads();
             V W[3][L];
 #pragma unroll
             for (int ax = 0; ax < 3; ++ax) {
-                const R ku = (R)(d >= 0 ? kappa * beta * dirs[3 * d + ax] : 0.0);
+                V e = cmk<V>((R)1, (R)0);
+                if (d >= 0) e = cexpi((R)(kappa * beta * dirs[3 * d + ax]) * xh[ax]);  // uniform branch
 #pragma unroll
-                for (int k = 0; k < L; ++k) W[ax][k] = cscale(cexpi(ku * (xh[ax] - node<L, R>(k))), S[ax][k]);
+                for (int k = 0; k < L; ++k) W[ax][k] = cscale(cmul(e, T[ax][k]), S[ax][k]);
             }
             V va = cz<V>();
 #pragma unroll
