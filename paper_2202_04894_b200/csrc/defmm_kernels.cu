@@ -329,10 +329,11 @@ __device__ __forceinline__ cx<R> mode_product(const R* A, int bit, int axis, con
     return v;
 }
 
-// the nodal buffers of one warp: 2 L^3 complex (dynamic shared memory)
+// the nodal buffers of one warp: 2 L^3 complex + 9 L complex of separable
+// plane-wave phase tables (dynamic shared memory), then the factor tables
 template <typename R, int L>
 __host__ __device__ constexpr int nodal_smem_bytes() {
-    return NODAL_WARPS * 2 * cube<L>() * (int)sizeof(cx<R>) + 2 * L * L * (int)sizeof(R);
+    return NODAL_WARPS * (2 * cube<L>() + 9 * L) * (int)sizeof(cx<R>) + 2 * L * L * (int)sizeof(R);
 }
 
 template <typename R, int L>
@@ -344,7 +345,8 @@ __global__ void __launch_bounds__(32 * NODAL_WARPS) m2m_kernel(
     constexpr int L3 = cube<L>(), E = per_lane<L>();
     extern __shared__ unsigned char smraw[];
     V* bufs = reinterpret_cast<V*>(smraw);
-    R* A = reinterpret_cast<R*>(bufs + NODAL_WARPS * 2 * L3);
+    V* tabs = bufs + NODAL_WARPS * 2 * L3;
+    R* A = reinterpret_cast<R*>(tabs + NODAL_WARPS * 9 * L);
     make_factor_tables<L, R>(A);
     __syncthreads();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -356,6 +358,22 @@ __global__ void __launch_bounds__(32 * NODAL_WARPS) m2m_kernel(
     for (int k = 0; k < 3; ++k) ku[k] = (R)(d >= 0 ? kappa * son_beta * dirs[3 * d + k] : 0.0);
     V* X = bufs + w * 2 * L3;
     V* T = X + L3;
+    // separable phases (HF keys): son side Q[ax][bit][j] = e^{-i ku_ax (bit + x_j)},
+    // father side F[ax][k] = e^{i 2 ku_ax x_k} -- 9 L sincos per slot instead of
+    // 9 L^3 (one per element and son)
+    V* Q = tabs + w * 9 * L;
+    V* F = Q + 6 * L;
+    if (d >= 0) {
+        for (int t = lane; t < 9 * L; t += 32) {
+            if (t < 6 * L) {
+                const int ax = t / (2 * L), bit = (t / L) & 1, j = t % L;
+                Q[t] = cexpi(-ku[ax] * ((R)bit + node<L, R>(j)));
+            } else {
+                const int ax = (t - 6 * L) / L, k = t % L;
+                F[ax * L + k] = cexpi(2 * ku[ax] * node<L, R>(k));
+            }
+        }
+    }
     V acc[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) acc[e] = cz<V>();
@@ -373,9 +391,8 @@ __global__ void __launch_bounds__(32 * NODAL_WARPS) m2m_kernel(
                 const int j0 = r / (L * L), j1 = (r / L) % L, j2 = r % L;
                 const V m = mult[ss * L3 + r];
                 // son-side phase e^{-i th (bit + x_j)} (conj plane wave on the son grid)
-                const R ph = -(ku[0] * (b0 + node<L, R>(j0)) + ku[1] * (b1 + node<L, R>(j1)) +
-                               ku[2] * (b2 + node<L, R>(j2)));
-                X[r] = d >= 0 ? cmul(m, cexpi(ph)) : m;
+                X[r] = d >= 0 ? cmul(cmul(m, Q[(0 + b0) * L + j0]), cmul(Q[(2 + b1) * L + j1], Q[(4 + b2) * L + j2]))
+                              : m;
             }
         }
         __syncwarp();
@@ -404,8 +421,7 @@ __global__ void __launch_bounds__(32 * NODAL_WARPS) m2m_kernel(
         if (r < L3) {
             const int k0 = r / (L * L), k1 = (r / L) % L, k2 = r % L;
             // father-side phase e^{i th 2 x_k}
-            const R ph = 2 * (ku[0] * node<L, R>(k0) + ku[1] * node<L, R>(k1) + ku[2] * node<L, R>(k2));
-            mult[ob + r] = d >= 0 ? cmul(acc[e], cexpi(ph)) : acc[e];
+            mult[ob + r] = d >= 0 ? cmul(cmul(acc[e], F[k0]), cmul(F[L + k1], F[2 * L + k2])) : acc[e];
         }
     }
 }
@@ -420,12 +436,17 @@ __global__ void __launch_bounds__(32 * NODAL_WARPS) l2l_kernel(
     constexpr int L3 = cube<L>(), E = per_lane<L>();
     extern __shared__ unsigned char smraw[];
     V* bufs = reinterpret_cast<V*>(smraw);
-    R* A = reinterpret_cast<R*>(bufs + NODAL_WARPS * 2 * L3);
+    V* tabs = bufs + NODAL_WARPS * 2 * L3;
+    R* A = reinterpret_cast<R*>(tabs + NODAL_WARPS * 9 * L);
     make_factor_tables<L, R>(A);
     __syncthreads();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t i = (int64_t)blockIdx.x * NODAL_WARPS + w;
     if (i >= n) return;
+    // separable phases per source (HF keys): father side G[ax][k] =
+    // e^{-i 2 ku_ax x_k}, son side H[ax][j] = e^{i ku_ax (bit_ax + x_j)}
+    V* G = tabs + w * 9 * L;
+    V* H = G + 3 * L;
     const int o = octant[i];
     const int b0 = (o >> 2) & 1, b1 = (o >> 1) & 1, b2 = o & 1;
     V* X = bufs + w * 2 * L3;
@@ -461,14 +482,22 @@ __global__ void __launch_bounds__(32 * NODAL_WARPS) l2l_kernel(
 #pragma unroll
         for (int k = 0; k < 3; ++k) ku[k] = (R)(d >= 0 ? kappa * son_beta * dirs[3 * d + k] : 0.0);
         __syncwarp();
+        if (d >= 0) {
+            for (int t = lane; t < 6 * L; t += 32) {
+                const int ax = (t % (3 * L)) / L, k = t % L;
+                const int bit = ax == 0 ? b0 : (ax == 1 ? b1 : b2);
+                if (t < 3 * L) G[t] = cexpi(-2 * ku[ax] * node<L, R>(k));
+                else H[t - 3 * L] = cexpi(ku[ax] * ((R)bit + node<L, R>(k)));
+            }
+            __syncwarp();
+        }
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const int r = lane + 32 * e;
             if (r < L3) {
                 const int k0 = r / (L * L), k1 = (r / L) % L, k2 = r % L;
                 // father-side phase e^{-i th 2 x_k} (conj plane wave on the father grid)
-                const R ph = -2 * (ku[0] * node<L, R>(k0) + ku[1] * node<L, R>(k1) + ku[2] * node<L, R>(k2));
-                X[r] = d >= 0 ? cmul(cur[e], cexpi(ph)) : cur[e];
+                X[r] = d >= 0 ? cmul(cmul(cur[e], G[k0]), cmul(G[L + k1], G[2 * L + k2])) : cur[e];
             }
         }
         __syncwarp();
@@ -491,9 +520,7 @@ __global__ void __launch_bounds__(32 * NODAL_WARPS) l2l_kernel(
                 const V y = mode_product<L, R, true>(A, b2, 2, X, r);
                 const int j0 = r / (L * L), j1 = (r / L) % L, j2 = r % L;
                 // son-side phase e^{i th (bit + x_j)}
-                const R ph = ku[0] * (b0 + node<L, R>(j0)) + ku[1] * (b1 + node<L, R>(j1)) +
-                             ku[2] * (b2 + node<L, R>(j2));
-                acc[e] = cadd(acc[e], d >= 0 ? cmul(y, cexpi(ph)) : y);
+                acc[e] = cadd(acc[e], d >= 0 ? cmul(cmul(y, H[j0]), cmul(H[L + j1], H[2 * L + j2])) : y);
             }
         }
     }
