@@ -170,6 +170,82 @@ def _sub_csr(ptr, keep):
     return np.nonzero(keep)[0], new_ptr, sel.astype(np.int64)
 
 
+# ---- per-level M2L kernel policy (host; pure functions, CPU-tested) --------
+
+# M2L kernel per level for each mode: (dense level, sparse level)
+M2L_MODE_KINDS = {
+    "auto": ("blocked", "rows"), "hybrid_rows": ("blocked", "rows"), "hybrid": ("blocked", "quad"),
+    "rows": ("rows", "rows"), "blocked_all": ("blocked", "blocked"), "quad_all": ("quad", "quad"),
+    "tiles": ("blocked", "tile"), "tiles_all": ("tile", "tile"), "slice_all": ("slice", "slice"),
+}
+M2L_KERNELS = ("rows", "blocked", "quad", "tile", "slice")
+# events per parent-pair block above which a level counts as dense (blocked kernel)
+BLOCKED_MIN_EVENTS_PER_BLOCK = 32.0
+# "auto": a complex64 sparse level runs the quad kernel when its quads are this
+# full: cfg2 L6 (cube faces, 13.3 events/quad) wins 6% of the M2L; 7-9
+# events/quad (cfg2 L4-5, cfg3) and every complex128 level lose
+# (profiles/r01_summary_v5.md)
+QUAD_MIN_EVENTS_PER_QUAD = 12.0
+
+
+def block_levels(plan, tt):
+    """(level of each parent-pair block, events per block, level of each group,
+    blocks per group) of the plan's blocked-M2L lists."""
+    g_rows = plan.blk_group_rows
+    first = np.where(g_rows >= 0, g_rows, np.iinfo(np.int64).max).min(axis=1)
+    glev = tt.level[plan.l_cell[first]] if first.size else np.zeros(0, np.int64)
+    nblk = np.diff(plan.blk_group_ptr)
+    ev = np.bitwise_count(plan.blk_mask.view(np.uint64)).astype(np.int64) if plan.blk_mask.size else \
+        np.zeros(0, np.int64)
+    return np.repeat(glev, nblk), ev, glev, nblk
+
+
+def dense_levels(plan, tt, threshold: float = BLOCKED_MIN_EVENTS_PER_BLOCK) -> set:
+    """Levels whose parent-pair blocks hold >= threshold events on average."""
+    blev, ev, _, _ = block_levels(plan, tt)
+    return {int(lv) for lv in np.unique(blev) if ev[blev == lv].mean() >= threshold}
+
+
+def quad_fill(plan, tt, levels) -> dict:
+    """level -> mean M2L events per in-plane quad of its parent-pair blocks."""
+    blev, _, glev, nblk = block_levels(plan, tt)
+    out = {}
+    for lv in levels:
+        gsel = np.nonzero(glev == lv)[0]
+        if gsel.size == 0:
+            continue
+        bsel = np.nonzero(blev == lv)[0]
+        bptr = np.concatenate([[0], np.cumsum(nblk[gsel])]).astype(np.int64)
+        qd, _ = _quads(plan.blk_src[bsel], plan.blk_trans[bsel], plan.blk_mask[bsel], bptr)
+        if qd.shape[0]:
+            out[int(lv)] = float(np.bitwise_count(qd[:, 13].astype(np.uint64)).mean())
+    return out
+
+
+def m2l_level_kinds(mode: str, dtype: str, levels, dense, fill=None, override=None, env: str = "") -> dict:
+    """level -> M2L kernel: the mode's (dense, sparse) choice; in "auto" a
+    complex64 sparse level with quad fill >= QUAD_MIN_EVENTS_PER_QUAD runs
+    quads; then the per-level overrides (dict, or "4:quad,6:rows")."""
+    if mode not in M2L_MODE_KINDS:
+        raise ValueError(f"unknown M2L mode {mode!r}")
+    kd, ks = M2L_MODE_KINDS[mode]
+    kinds = {int(lv): (kd if int(lv) in dense else ks) for lv in levels}
+    if mode == "auto" and dtype == "c64":
+        for lv, f in (fill or {}).items():
+            if kinds.get(lv) == "rows" and f >= QUAD_MIN_EVENTS_PER_QUAD:
+                kinds[lv] = "quad"
+    over = dict(override or {})
+    for tok in filter(None, env.split(",")):
+        lv, k = tok.split(":")
+        over[int(lv)] = k
+    for lv, k in over.items():
+        if k not in M2L_KERNELS:
+            raise ValueError(f"unknown M2L kernel {k!r} for level {lv}")
+        if int(lv) in kinds:
+            kinds[int(lv)] = k
+    return kinds
+
+
 class FmmPlan:
     """Reusable device plan for one particle geometry (targets is sources, or
     a target/source pair sharing one root box, traversal.py:449-461)."""
@@ -385,60 +461,7 @@ class FmmPlan:
             self.halo = make_halo(self.plan, self.tt, self.shard.cuts, self.shard.rank, self.shard.world)
 
     # events per parent-pair block above which a level's M2L runs blocked
-    BLOCKED_MIN_EVENTS_PER_BLOCK = 32.0
-
-    # M2L kernel per level for each mode: (dense level, sparse level)
-    _MODE_KINDS = {
-        "auto": ("blocked", "rows"), "hybrid_rows": ("blocked", "rows"), "hybrid": ("blocked", "quad"), "rows": ("rows", "rows"),
-        "blocked_all": ("blocked", "blocked"), "quad_all": ("quad", "quad"), "tiles": ("blocked", "tile"),
-        "tiles_all": ("tile", "tile"), "slice_all": ("slice", "slice"),
-    }
-
-    # "auto": a sparse level runs the quad kernel when its quads are this full
-    # (complex64 only): cfg2 L6 (cube faces, 13.3 events/quad) wins 6% of the
-    # M2L; 7-9 events/quad (cfg2 L4-5, cfg3) and every complex128 level lose
-    # (profiles/r01_summary_v5.md)
-    QUAD_MIN_EVENTS_PER_QUAD = 12.0
-
-    def _quad_fill(self, levels, blev, glev_full, nblk) -> dict:
-        """level -> mean M2L events per quad of its parent-pair blocks."""
-        p = self.plan
-        out = {}
-        for lv in levels:
-            gsel = np.nonzero(glev_full == lv)[0]
-            if gsel.size == 0:
-                continue
-            bsel = np.nonzero(blev == lv)[0]
-            bptr = np.concatenate([[0], np.cumsum(nblk[gsel])]).astype(np.int64)
-            qd, _ = _quads(p.blk_src[bsel], p.blk_trans[bsel], p.blk_mask[bsel], bptr)
-            if qd.shape[0]:
-                out[int(lv)] = float(np.bitwise_count(qd[:, 13].astype(np.uint64)).mean())
-        return out
-
-    def _level_kinds(self, levels, dense, quad_fill=None) -> dict:
-        """level -> M2L kernel ("rows", "blocked", "quad", "tile", "slice")
-        from the mode, then per-level overrides (``m2l_levels=`` dict or
-        DEFMM_M2L_LEVELS="4:quad,6:rows")."""
-        mode = self.m2l_variant_default
-        if mode not in self._MODE_KINDS:
-            raise ValueError(f"unknown M2L mode {mode!r}")
-        kd, ks = self._MODE_KINDS[mode]
-        kinds = {int(lv): (kd if int(lv) in dense else ks) for lv in levels}
-        if mode == "auto" and self.config.dtype == "c64":
-            for lv, fill in (quad_fill or {}).items():
-                if kinds.get(lv) == "rows" and fill >= self.QUAD_MIN_EVENTS_PER_QUAD:
-                    kinds[lv] = "quad"
-        over = dict(self.m2l_level_override or {})
-        env = os.environ.get("DEFMM_M2L_LEVELS", "")
-        for tok in filter(None, env.split(",")):
-            lv, k = tok.split(":")
-            over[int(lv)] = k
-        for lv, k in over.items():
-            if k not in ("rows", "blocked", "quad", "tile", "slice"):
-                raise ValueError(f"unknown M2L kernel {k!r} for level {lv}")
-            if int(lv) in kinds:
-                kinds[int(lv)] = k
-        return kinds
+    BLOCKED_MIN_EVENTS_PER_BLOCK = BLOCKED_MIN_EVENTS_PER_BLOCK
 
     def _host_lists(self) -> dict:
         """Per-level M2L kernel choice: levels whose parent-pair blocks are
@@ -453,22 +476,14 @@ class FmmPlan:
         rows = h["rows"]
         rlev = tt.level[p.l_cell[rows]] if rows.size else np.zeros(0, np.int64)
         # density per level from the full plan (identical on every rank)
-        g_rows = p.blk_group_rows
-        first = np.where(g_rows >= 0, g_rows, np.iinfo(np.int64).max).min(axis=1)
-        glev_full = tt.level[p.l_cell[first]] if first.size else np.zeros(0, np.int64)
-        nblk = np.diff(p.blk_group_ptr)
-        ev = np.bitwise_count(p.blk_mask.view(np.uint64)).astype(np.int64) if p.blk_mask.size else np.zeros(0, np.int64)
-        blev = np.repeat(glev_full, nblk)
-        dense = set()
-        for lev in np.unique(blev):
-            sel = blev == lev
-            if ev[sel].mean() >= self.BLOCKED_MIN_EVENTS_PER_BLOCK:
-                dense.add(int(lev))
+        dense = dense_levels(p, tt, self.BLOCKED_MIN_EVENTS_PER_BLOCK)
+        levels = np.unique(rlev)
         fill = None
         if self.m2l_variant_default == "auto" and self.config.dtype == "c64":
-            fill = self._quad_fill([lv for lv in np.unique(rlev) if int(lv) not in dense], blev, glev_full, nblk)
+            fill = quad_fill(p, tt, [lv for lv in levels if int(lv) not in dense])
         self.quad_fill = fill
-        kinds = self._level_kinds(np.unique(rlev), dense, fill)
+        kinds = m2l_level_kinds(self.m2l_variant_default, self.config.dtype, levels, dense, fill,
+                                self.m2l_level_override, os.environ.get("DEFMM_M2L_LEVELS", ""))
         self.level_kinds = kinds
         rkind = np.array([kinds[int(lv)] for lv in rlev], dtype=object) if rows.size else np.zeros(0, object)
         z = np.zeros(0, np.int64)

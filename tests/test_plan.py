@@ -425,3 +425,39 @@ def test_m2l_tiles_reconstruct_every_row(case, u_max, k_max, e_max):
             assert np.all(s_op >= 0) and np.all(t_op < 0)
             np.testing.assert_array_equal(s_op, ent[ptr[r]:ptr[r + 1], 0])
             np.testing.assert_array_equal(-1 - t_op, ent[ptr[r]:ptr[r + 1], 1])
+
+
+@pytest.mark.parametrize("case", ["cubesurf4000", "volume3000", "refined3000"])
+def test_m2l_level_policy(case):
+    """Per-level M2L kernel choice (fmm.m2l_level_kinds): dense levels ->
+    blocked, sparse -> rows; "auto" moves complex64 sparse levels with full
+    quads (>= QUAD_MIN_EVENTS_PER_QUAD events/quad) to the quad kernel and
+    never complex128 ones; overrides (dict or env string) win; bad names raise."""
+    from paper_2202_04894_b200.fmm import (QUAD_MIN_EVENTS_PER_QUAD, block_levels, dense_levels,
+                                           m2l_level_kinds, quad_fill)
+
+    tr, _, p = _plan(load_case(case))
+    levels = np.unique(p.m2l_level)
+    dense = dense_levels(p, tr)
+    blev, ev, _, _ = block_levels(p, tr)
+    for lv in np.unique(blev):
+        assert (int(lv) in dense) == (ev[blev == lv].mean() >= 32.0)
+    fill = quad_fill(p, tr, [lv for lv in levels if int(lv) not in dense])
+    assert all(1.0 <= f <= 16.0 for f in fill.values())
+    k64 = m2l_level_kinds("auto", "c64", levels, dense, fill)
+    k128 = m2l_level_kinds("auto", "c128", levels, dense, fill)
+    for lv in levels:
+        lv = int(lv)
+        if lv in dense:
+            assert k64[lv] == k128[lv] == "blocked"
+        else:
+            assert k128[lv] == "rows"
+            assert k64[lv] == ("quad" if fill.get(lv, 0.0) >= QUAD_MIN_EVENTS_PER_QUAD else "rows")
+    assert set(m2l_level_kinds("hybrid_rows", "c64", levels, dense).values()) <= {"blocked", "rows"}
+    lv0 = int(levels[0])
+    assert m2l_level_kinds("auto", "c64", levels, dense, fill, {lv0: "tile"})[lv0] == "tile"
+    assert m2l_level_kinds("rows", "c64", levels, dense, env=f"{lv0}:slice")[lv0] == "slice"
+    with pytest.raises(ValueError):
+        m2l_level_kinds("auto", "c64", levels, dense, override={lv0: "nope"})
+    with pytest.raises(ValueError):
+        m2l_level_kinds("nope", "c64", levels, dense)
