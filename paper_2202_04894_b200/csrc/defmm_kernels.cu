@@ -184,6 +184,7 @@ __device__ __forceinline__ void make_twiddles(V* tw) {
 // e^{-2 pi i k / P} for every P = 2L-1 (L = 2..8), filled once by the
 // launchers (cudaMemcpyToSymbol); kernels build their P x L matrix from it
 __constant__ double2 c_tw[8][15];
+__constant__ float2 c_twf[8][15];  // the same, rounded to float (complex64 M2F v2)
 
 // ---------------------------------------------------------------------------
 // Spectral layout.  Every P^3 spectrum (multipole spectra, symbols, local
@@ -586,6 +587,96 @@ __global__ void __launch_bounds__(32 * M2F_WARPS) m2f_kernel(int64_t n, const in
         }
         out[t] = cscale(v, scale);  // the pad entry (c64) is written as 0
     }
+}
+
+// K6 v2 M2F (small orders): the same pruned transform with one 1D DFT ROW per
+// lane -- a lane loads its row's L inputs once and produces its P outputs with
+// the twiddles as compile-time constant-bank operands (c_tw), instead of one
+// output per lane re-reading L inputs and L twiddles from shared memory (v1 was
+// L1/shared-throughput bound at 94%, 25% of the HBM roofline, r01_summary_v6).
+// The natural-order spectrum is assembled in shared memory and written out
+// coalesced in orbit order.
+template <typename R, int L>
+__host__ __device__ constexpr int m2f2_warp_elems() {
+    constexpr int P = 2 * L - 1;
+    return L * L * L + L * L * P + L * P * P + P * P * P;
+}
+template <typename R, int L>
+__host__ __device__ constexpr bool m2f2_fits() {
+    return m2f2_warp_elems<R, L>() * (int)sizeof(cx<R>) <= 24 * 1024;
+}
+
+template <int L, typename V>
+__device__ __forceinline__ V twc(int f, int c) {  // e^{-2 pi i f c / P} (compile-time f, c)
+    constexpr int P = 2 * L - 1;
+    if constexpr (sizeof(V) == 8) {
+        return c_twf[L - 1][(f * c) % P];
+    } else {
+        return c_tw[L - 1][(f * c) % P];
+    }
+}
+
+template <typename R, int L>
+__global__ void __launch_bounds__(32 * M2F_WARPS) m2f2_kernel(int64_t n, const int64_t* __restrict__ src_slot,
+                                                              const cx<R>* __restrict__ mult,
+                                                              cx<R>* __restrict__ hat) {
+    using V = cx<R>;
+    constexpr int P = pad<L>(), L3 = cube<L>(), P3 = P * P * P, PP = P * P;
+    extern __shared__ unsigned char smraw[];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * M2F_WARPS + w;
+    if (i >= n) return;
+    V* X = reinterpret_cast<V*>(smraw) + w * m2f2_warp_elems<R, L>();
+    V* Y1 = X + L3;          // [a][b][f2]
+    V* Y2 = Y1 + L * L * P;  // [a][f1][f2]
+    V* Z = Y2 + L * PP;      // [f0][f1][f2] natural order
+    const int64_t s = src_slot[i] * L3;
+    for (int r = lane; r < L3; r += 32) X[r] = mult[s + r];
+    __syncwarp();
+    for (int row = lane; row < L * L; row += 32) {  // axis 2: c -> f2
+        V x[L];
+#pragma unroll
+        for (int c = 0; c < L; ++c) x[c] = X[row * L + c];
+#pragma unroll
+        for (int f = 0; f < P; ++f) {
+            V v = cz<V>();
+#pragma unroll
+            for (int c = 0; c < L; ++c) v = cfma(x[c], twc<L, V>(f, c), v);
+            Y1[row * P + f] = v;
+        }
+    }
+    __syncwarp();
+    for (int row = lane; row < L * P; row += 32) {  // axis 1: b -> f1; row = (a, f2)
+        const int a = row / P, f2 = row % P;
+        V y[L];
+#pragma unroll
+        for (int b = 0; b < L; ++b) y[b] = Y1[(a * L + b) * P + f2];
+#pragma unroll
+        for (int f = 0; f < P; ++f) {
+            V v = cz<V>();
+#pragma unroll
+            for (int b = 0; b < L; ++b) v = cfma(y[b], twc<L, V>(f, b), v);
+            Y2[(a * P + f) * P + f2] = v;
+        }
+    }
+    __syncwarp();
+    const R scale = (R)(1.0 / (P * sqrt((double)P)));
+    for (int row = lane; row < PP; row += 32) {  // axis 0: a -> f0; row = (f1, f2)
+        V z[L];
+#pragma unroll
+        for (int a = 0; a < L; ++a) z[a] = Y2[a * PP + row];
+#pragma unroll
+        for (int f = 0; f < P; ++f) {
+            V v = cz<V>();
+#pragma unroll
+            for (int a = 0; a < L; ++a) v = cfma(z[a], twc<L, V>(f, a), v);
+            Z[f * PP + row] = cscale(v, scale);
+        }
+    }
+    __syncwarp();
+    constexpr int SS = spec_stride<R, L>();
+    V* out = hat + i * (int64_t)SS;
+    for (int t = lane; t < SS; t += 32) out[t] = t < P3 ? Z[forder<L>(t)] : cz<V>();  // pad entry (c64) = 0
 }
 
 // K9 symbols: kernel column G(beta (t + z)) on the difference grid (wrap
@@ -2117,7 +2208,13 @@ int ensure_twiddles() {
             h[L - 1][k] = make_double2(cos(a), -sin(a));
         }
     }
-    const int rc = report(cudaMemcpyToSymbol(c_tw, h, sizeof(h)), "cudaMemcpyToSymbol(c_tw)");
+    int rc = report(cudaMemcpyToSymbol(c_tw, h, sizeof(h)), "cudaMemcpyToSymbol(c_tw)");
+    if (rc == 0) {
+        float2 hf[8][15] = {};
+        for (int l = 0; l < 8; ++l)
+            for (int k = 0; k < 15; ++k) hf[l][k] = make_float2((float)h[l][k].x, (float)h[l][k].y);
+        rc = report(cudaMemcpyToSymbol(c_twf, hf, sizeof(hf)), "cudaMemcpyToSymbol(c_twf)");
+    }
     if (rc == 0) done = true;
     return rc;
 }
@@ -2217,12 +2314,22 @@ int launch_m2f(int32_t L, int64_t n, const int64_t* src_slot, const void* mult, 
     cudaStream_t s = (cudaStream_t)stream;
     DEFMM_DISPATCH_L(L, {
         constexpr int P = 2 * LL - 1;
-        const size_t bytes = sizeof(cx<R>) * (P * LL + M2F_WARPS * (LL * LL * LL + LL * LL * P + LL * P * P));
-        int rc = set_smem(m2f_kernel<R, LL>, bytes);
-        if (rc) return rc;
-        carve(m2f_kernel<R, LL>);
-        m2f_kernel<R, LL><<<blocks_of(n, M2F_WARPS), 32 * M2F_WARPS, bytes, s>>>(n, src_slot, (const cx<R>*)mult,
-                                                                                (cx<R>*)hat);
+        if constexpr (m2f2_fits<R, LL>()) {
+            if (int rc1 = ensure_twiddles()) return rc1;
+            const size_t bytes = sizeof(cx<R>) * M2F_WARPS * m2f2_warp_elems<R, LL>();
+            int rc = set_smem(m2f2_kernel<R, LL>, bytes);
+            if (rc) return rc;
+            carve(m2f2_kernel<R, LL>);
+            m2f2_kernel<R, LL><<<blocks_of(n, M2F_WARPS), 32 * M2F_WARPS, bytes, s>>>(
+                n, src_slot, (const cx<R>*)mult, (cx<R>*)hat);
+        } else {
+            const size_t bytes = sizeof(cx<R>) * (P * LL + M2F_WARPS * (LL * LL * LL + LL * LL * P + LL * P * P));
+            int rc = set_smem(m2f_kernel<R, LL>, bytes);
+            if (rc) return rc;
+            carve(m2f_kernel<R, LL>);
+            m2f_kernel<R, LL><<<blocks_of(n, M2F_WARPS), 32 * M2F_WARPS, bytes, s>>>(
+                n, src_slot, (const cx<R>*)mult, (cx<R>*)hat);
+        }
     });
     return report(cudaGetLastError(), "m2f");
 }
