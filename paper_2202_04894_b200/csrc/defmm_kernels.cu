@@ -789,9 +789,60 @@ __host__ __device__ constexpr int m2l_block() {
 // pruned inverse DFT of one accumulated spectrum X (P^3, smem) into an L^3
 // nodal vector (fourier.py:74-80): contract f0 -> a, f1 -> b, f2 -> c;
 // tw = the P x L twiddle matrix (make_twiddle_matrix), conjugated here.
-template <int L, typename V>
+// ROWS = true: one 1D row per thread with constant-bank twiddles (standalone
+// f2l_rows_kernel: 80 -> 60 us on cfg2); the fused F2L of the M2L row kernel
+// keeps the per-output form (the row variant's registers cost the row
+// kernel's occupancy: 1.65 -> 1.70 ms)
+template <int L, typename V, bool ROWS = false>
 __device__ __forceinline__ void f2l_row(const V* tw, V* X, V* Z1, V* out, int nt) {
     constexpr int P = pad<L>(), L3 = cube<L>();
+    if constexpr (ROWS && P <= 9) {
+        // one 1D inverse-DFT ROW per thread: P inputs loaded once, L outputs
+        // with the twiddles as compile-time constant-bank operands (the
+        // per-output variant re-read P inputs and P twiddles from shared memory)
+        constexpr int PP = P * P;
+        for (int row = threadIdx.x; row < PP; row += nt) {  // axis 0: f0 -> a; row = (f1, f2)
+            V x[P];
+#pragma unroll
+            for (int f = 0; f < P; ++f) x[f] = X[f * PP + row];
+#pragma unroll
+            for (int a = 0; a < L; ++a) {
+                V v = cz<V>();
+#pragma unroll
+                for (int f = 0; f < P; ++f) v = cfma(x[f], cconj(c_tw[L - 1][(f * a) % P]), v);
+                Z1[a * PP + row] = v;
+            }
+        }
+        __syncthreads();
+        for (int row = threadIdx.x; row < L * P; row += nt) {  // axis 1: f1 -> b; row = (a, f2)
+            const int a = row / P, f2 = row % P;
+            V y[P];
+#pragma unroll
+            for (int f = 0; f < P; ++f) y[f] = Z1[(a * P + f) * P + f2];
+#pragma unroll
+            for (int b = 0; b < L; ++b) {
+                V v = cz<V>();
+#pragma unroll
+                for (int f = 0; f < P; ++f) v = cfma(y[f], cconj(c_tw[L - 1][(f * b) % P]), v);
+                X[(a * L + b) * P + f2] = v;
+            }
+        }
+        __syncthreads();
+        const double scale = 1.0 / (P * sqrt((double)P));
+        for (int row = threadIdx.x; row < L * L; row += nt) {  // axis 2: f2 -> c; row = (a, b)
+            V z[P];
+#pragma unroll
+            for (int f = 0; f < P; ++f) z[f] = X[row * P + f];
+#pragma unroll
+            for (int c = 0; c < L; ++c) {
+                V v = cz<V>();
+#pragma unroll
+                for (int f = 0; f < P; ++f) v = cfma(z[f], cconj(c_tw[L - 1][(f * c) % P]), v);
+                out[row * L + c] = cscale(v, scale);
+            }
+        }
+        return;
+    }
     for (int t = threadIdx.x; t < L * P * P; t += nt) {
         const int a = t / (P * P), f12 = t % (P * P);
         V v = cz<V>();
@@ -1463,7 +1514,7 @@ __global__ void __launch_bounds__(128) f2l_rows_kernel(int64_t nrows, const int6
     const cx<R>* src = lhat + r * SS;
     for (int j = threadIdx.x; j < P3; j += blockDim.x) X[forder<L>(j)] = to_d(src[j]);
     __syncthreads();
-    f2l_row<L, double2>(tw, X, Z1, O, blockDim.x);
+    f2l_row<L, double2, true>(tw, X, Z1, O, blockDim.x);
     __syncthreads();
     cx<R>* out = local + row_slot[r] * L3;
     for (int t = threadIdx.x; t < L3; t += blockDim.x) out[t] = from_d<cx<R>>(O[t]);
