@@ -1565,7 +1565,7 @@ __global__ void __launch_bounds__(m2l_threads<L>()) m2l_canon_kernel(
 // per-axis weights as P2M.  Output accumulated in FP64.
 
 template <typename R, int L>
-__global__ void __launch_bounds__(64) l2p_kernel(
+__global__ void __launch_bounds__(64, sizeof(R) == 4 ? 16 : 8) l2p_kernel(
     int64_t n, const int32_t* __restrict__ leaf_cell, const int64_t* __restrict__ slot_lo,
     const int64_t* __restrict__ slot_hi, const int32_t* __restrict__ slot_dir,
     const int64_t* __restrict__ cstart, const int64_t* __restrict__ cstop,
