@@ -951,6 +951,101 @@ __global__ void __launch_bounds__(m2l_block<R, L>()) m2l_rows_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// K7 v8: pair M2L.  One CTA per PAIR of sibling rows (same level, key and
+// target parent; a single row when the group is odd).  The pair's events are
+// merged per source spectrum: entry {s, symbol of row a or -1, symbol of row b
+// or -1}, so a source both rows read is loaded once -- 1.6 operand loads per
+// event instead of the row kernel's 2 on surface data, with the row kernel's
+// streaming structure and register budget (the row kernel is bound by the
+// L1/shared data path: only register reuse takes bytes off it).  Two entries
+// in flight per iteration; F2L of both rows in shared memory.
+#ifndef DEFMM_PAIR_REGS
+#define DEFMM_PAIR_REGS 48
+#endif
+template <typename R, int L>
+__global__ void __launch_bounds__(m2l_block<R, L>(),
+                                  DEFMM_PAIR_REGS ? 65536 / (m2l_block<R, L>() * DEFMM_PAIR_REGS) : 1) m2l_pair_kernel(
+    int64_t npairs, const int64_t* __restrict__ pair_slot, const int64_t* __restrict__ pair_ptr,
+    const int4* __restrict__ ent, const cx<R>* __restrict__ hat, const cx<R>* __restrict__ symd,
+    cx<R>* __restrict__ local) {
+    constexpr int P = pad<L>(), L3 = cube<L>(), P3 = P * P * P;
+    constexpr int SS = spec_stride<R, L>();
+    constexpr int NT = m2l_block<R, L>();
+    constexpr bool VEC = sizeof(R) == 4;
+    constexpr int W = VEC ? 2 : 1;
+    constexpr int PER = (SS / W + NT - 1) / NT;
+    using V = cx<R>;
+    using VT = std::conditional_t<VEC, float4, double2>;
+    extern __shared__ unsigned char smraw[];
+    double2* tw = reinterpret_cast<double2*>(smraw);
+    double2* X = tw + P * L;
+    double2* Z1 = X + P3 + 1;
+    double2* O = Z1 + L * P * P;
+    const int64_t g = blockIdx.x;
+    make_twiddle_matrix<L, double2>(tw);
+    const VT* hv = reinterpret_cast<const VT*>(hat);
+    const VT* dv = reinterpret_cast<const VT*>(symd);
+    constexpr int NV = SS / W;
+    V acc[2][PER][W];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int m = 0; m < PER; ++m)
+#pragma unroll
+            for (int w = 0; w < W; ++w) acc[u][m][w] = cz<V>();
+    auto fma_v = [](V (&a)[W], const VT& d, const VT& x) {
+        if constexpr (VEC) {
+            a[0] = cfma(make_float2(d.x, d.y), make_float2(x.x, x.y), a[0]);
+            a[W - 1] = cfma(make_float2(d.z, d.w), make_float2(x.z, x.w), a[W - 1]);
+        } else {
+            a[0] = cfma(d, x, a[0]);
+        }
+    };
+    const int64_t e0 = pair_ptr[g], e1 = pair_ptr[g + 1];
+    for (int64_t e = e0; e < e1; e += 2) {
+        const bool two = e + 1 < e1;
+        const int4 p = __ldg(ent + e);
+        const int4 q = two ? __ldg(ent + e + 1) : make_int4(p.x, -1, -1, 0);
+#pragma unroll
+        for (int m = 0; m < PER; ++m) {
+            const int jv = threadIdx.x + m * NT;
+            if (jv < NV) {
+                const VT sp = __ldg(hv + (int64_t)p.x * NV + jv);
+                const VT sq = __ldg(hv + (int64_t)q.x * NV + jv);
+                const VT dpa = p.y >= 0 ? __ldg(dv + (int64_t)p.y * NV + jv) : VT{};
+                const VT dpb = p.z >= 0 ? __ldg(dv + (int64_t)p.z * NV + jv) : VT{};
+                const VT dqa = q.y >= 0 ? __ldg(dv + (int64_t)q.y * NV + jv) : VT{};
+                const VT dqb = q.z >= 0 ? __ldg(dv + (int64_t)q.z * NV + jv) : VT{};
+                fma_v(acc[0][m], dpa, sp);
+                fma_v(acc[1][m], dpb, sp);
+                fma_v(acc[0][m], dqa, sq);
+                fma_v(acc[1][m], dqb, sq);
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const int64_t slot = pair_slot[2 * g + u];
+        if (slot < 0) break;  // uniform
+#pragma unroll
+        for (int m = 0; m < PER; ++m) {
+            const int jv = threadIdx.x + m * NT;
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                const int j = jv * W + w;
+                if (jv < NV && j < P3) X[forder<L>(j)] = to_d(acc[u][m][w]);
+            }
+        }
+        __syncthreads();
+        f2l_row<L, double2>(tw, X, Z1, O, NT);
+        __syncthreads();
+        cx<R>* out = local + slot * L3;
+        for (int t = threadIdx.x; t < L3; t += NT) out[t] = from_d<cx<R>>(O[t]);
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K7 v3: parent-pair blocked M2L.  A CTA owns a group = (target parent P,
 // key) with up to 8 target rows (its children a); a block = (group, source
 // parent Q) holds up to 8 source spectra (children b) and, per child offset
@@ -2435,6 +2530,25 @@ int launch_m2l_rows(int32_t L, int64_t nrows, const int64_t* row_slot, const int
 }
 
 template <typename R>
+int launch_m2l_pair(int32_t L, int64_t npairs, const int64_t* pair_slot, const int64_t* pair_ptr, const int32_t* ent,
+                    const void* hat, const void* symd, void* local, void* stream) {
+    if (npairs == 0) return 0;
+    if (!grid_ok(npairs)) return -1;
+    if (int rc0 = ensure_twiddles()) return rc0;
+    cudaStream_t s = (cudaStream_t)stream;
+    DEFMM_DISPATCH_L(L, {
+        constexpr int P = 2 * LL - 1;
+        const size_t bytes = sizeof(double2) * (P * LL + P * P * P + 1 + LL * P * P + LL * LL * LL);
+        int rc = set_smem(m2l_pair_kernel<R, LL>, bytes);
+        if (rc) return rc;
+        carve(m2l_pair_kernel<R, LL>);
+        m2l_pair_kernel<R, LL><<<(unsigned)npairs, m2l_block<R, LL>(), bytes, s>>>(
+            npairs, pair_slot, pair_ptr, (const int4*)ent, (const cx<R>*)hat, (const cx<R>*)symd, (cx<R>*)local);
+    });
+    return report(cudaGetLastError(), "m2l_pair");
+}
+
+template <typename R>
 int launch_m2l_blocked(int32_t L, int64_t ngroups, const int64_t* grp_ptr, const int64_t* grp_rows,
                        const int32_t* blk_src, const int32_t* blk_trans, const int64_t* blk_mask,
                        const int8_t* blk_kind, const void* hat, const void* symd, void* lhat, void* stream) {
@@ -2625,6 +2739,11 @@ const char* defmm_last_error(void) { return g_last_error; }
                                 const int32_t* entries, const void* hat, const void* sym_derived, void* local,     \
                                 void* stream) {                                                                    \
         return launch_m2l_rows<R>(L, nrows, row_slot, row_ptr, entries, hat, sym_derived, local, stream);          \
+    }                                                                                                               \
+    int defmm_m2l_pair_##SUFFIX(int32_t L, int64_t npairs, const int64_t* pair_slot, const int64_t* pair_ptr,       \
+                                const int32_t* entries, const void* hat, const void* sym_derived, void* local,     \
+                                void* stream) {                                                                    \
+        return launch_m2l_pair<R>(L, npairs, pair_slot, pair_ptr, entries, hat, sym_derived, local, stream);       \
     }                                                                                                               \
     int defmm_m2l_blocked_##SUFFIX(int32_t L, int64_t ngroups, const int64_t* grp_ptr, const int64_t* grp_rows,     \
                                    const int32_t* blk_src, const int32_t* blk_trans, const int64_t* blk_mask,     \

@@ -149,6 +149,52 @@ def m2l_tiles(order, row_ptr, ent, n_hat: int, n_trans: int, u_max: int, k_max: 
             "ops": ops[:no], "ev_ptr": ev_ptr[: nr + 1], "ev": ev[:ne], "untiled": int(counts[4])}
 
 
+def m2l_pairs(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent) -> dict:
+    """Pair lists of the pair M2L (K7 v8, defmm_m2l_pair_*): the rows ``ids``
+    (indices into ``rows``, the local slots) grouped by (level, key, target
+    parent), consecutive siblings paired (an odd one alone); each pair's events
+    merged per source spectrum into {s, symbol of row a | -1, of row b | -1, 0}."""
+    z = np.zeros(0, np.int64)
+    if ids.size == 0:
+        return {"n": 0, "pair_slot": np.zeros(0, np.int64), "pair_ptr": np.zeros(1, np.int64),
+                "ent": np.zeros((0, 4), np.int32)}
+    slots = rows[ids]
+    cell = l_cell[slots]
+    key = l_dir[slots].astype(np.int64)
+    lev = level[cell].astype(np.int64)
+    par = parent[cell].astype(np.int64)
+    o = np.lexsort((cell, par, key, lev))
+    ids, slots, key, lev, par = ids[o], slots[o], key[o], lev[o], par[o]
+    n = ids.shape[0]
+    new = np.ones(n, bool)
+    new[1:] = (lev[1:] != lev[:-1]) | (key[1:] != key[:-1]) | (par[1:] != par[:-1])
+    gstart = np.nonzero(new)[0]
+    pos = np.arange(n) - gstart[np.cumsum(new) - 1]
+    side = pos % 2  # 0: row a, 1: row b of the pair
+    pid = np.cumsum(side == 0) - 1  # pair id of each row
+    npairs = int(pid[-1]) + 1
+    pair_slot = np.full((npairs, 2), -1, np.int64)
+    pair_slot[pid, side] = slots
+    cnt = row_ptr[ids + 1] - row_ptr[ids]
+    rep = np.repeat(np.arange(n), cnt)
+    sel = np.repeat(row_ptr[ids] - np.concatenate([[0], np.cumsum(cnt)[:-1]]), cnt) + np.arange(int(cnt.sum()))
+    ev = ent[sel]
+    ep, es, et, eside = pid[rep], ev[:, 0].astype(np.int64), ev[:, 1], side[rep]
+    so = np.lexsort((eside, es, ep))
+    ep, es, et, eside = ep[so], es[so], et[so], eside[so]
+    first = np.ones(ep.shape[0], bool)
+    first[1:] = (ep[1:] != ep[:-1]) | (es[1:] != es[:-1])
+    eid = np.cumsum(first) - 1
+    m = int(eid[-1]) + 1 if eid.size else 0
+    out = np.full((m, 4), -1, np.int32)
+    out[:, 3] = 0
+    out[eid, 0] = es
+    out[eid[eside == 0], 1] = et[eside == 0]
+    out[eid[eside == 1], 2] = et[eside == 1]
+    pair_ptr = np.searchsorted(ep[first], np.arange(npairs + 1)).astype(np.int64)
+    return {"n": npairs, "pair_slot": pair_slot.reshape(-1), "pair_ptr": pair_ptr, "ent": out}
+
+
 def _rows_to_ids(slots, rows):
     """Local slots -> index into the sorted row-slot list ``rows`` (-1 if absent)."""
     slots = np.asarray(slots)
@@ -177,8 +223,9 @@ M2L_MODE_KINDS = {
     "auto": ("blocked", "rows"), "hybrid_rows": ("blocked", "rows"), "hybrid": ("blocked", "quad"),
     "rows": ("rows", "rows"), "blocked_all": ("blocked", "blocked"), "quad_all": ("quad", "quad"),
     "tiles": ("blocked", "tile"), "tiles_all": ("tile", "tile"), "slice_all": ("slice", "slice"),
+    "pairs": ("blocked", "pair"), "pairs_all": ("pair", "pair"),
 }
-M2L_KERNELS = ("rows", "blocked", "quad", "tile", "slice")
+M2L_KERNELS = ("rows", "blocked", "quad", "tile", "slice", "pair")
 # events per parent-pair block above which a level counts as dense (blocked kernel)
 BLOCKED_MIN_EVENTS_PER_BLOCK = 32.0
 # "auto": a complex64 sparse level runs the quad kernel when its quads are this
@@ -186,6 +233,10 @@ BLOCKED_MIN_EVENTS_PER_BLOCK = 32.0
 # events/quad (cfg2 L4-5, cfg3) and every complex128 level lose
 # (profiles/r01_summary_v5.md)
 QUAD_MIN_EVENTS_PER_QUAD = 12.0
+# "auto": other sparse levels with at least this many rows run the pair kernel
+# (sibling rows merged per source: cfg2 M2L -9%, cfg3 -10%); small levels
+# (cfg1) keep the row kernel (profiles/r01_summary_v7.md)
+PAIR_MIN_ROWS = 2048
 
 
 def block_levels(plan, tt):
@@ -222,18 +273,24 @@ def quad_fill(plan, tt, levels) -> dict:
     return out
 
 
-def m2l_level_kinds(mode: str, dtype: str, levels, dense, fill=None, override=None, env: str = "") -> dict:
+def m2l_level_kinds(mode: str, dtype: str, levels, dense, fill=None, override=None, env: str = "",
+                    rows_per_level=None) -> dict:
     """level -> M2L kernel: the mode's (dense, sparse) choice; in "auto" a
     complex64 sparse level with quad fill >= QUAD_MIN_EVENTS_PER_QUAD runs
-    quads; then the per-level overrides (dict, or "4:quad,6:rows")."""
+    quads, another sparse level with >= PAIR_MIN_ROWS rows the pair kernel;
+    then the per-level overrides (dict, or "4:quad,6:rows")."""
     if mode not in M2L_MODE_KINDS:
         raise ValueError(f"unknown M2L mode {mode!r}")
     kd, ks = M2L_MODE_KINDS[mode]
     kinds = {int(lv): (kd if int(lv) in dense else ks) for lv in levels}
-    if mode == "auto" and dtype == "c64":
-        for lv, f in (fill or {}).items():
-            if kinds.get(lv) == "rows" and f >= QUAD_MIN_EVENTS_PER_QUAD:
+    if mode == "auto":
+        for lv in list(kinds):
+            if kinds[lv] != "rows":
+                continue
+            if dtype == "c64" and (fill or {}).get(lv, 0.0) >= QUAD_MIN_EVENTS_PER_QUAD:
                 kinds[lv] = "quad"
+            elif (rows_per_level or {}).get(lv, 0) >= PAIR_MIN_ROWS:
+                kinds[lv] = "pair"
     over = dict(override or {})
     for tok in filter(None, env.split(",")):
         lv, k = tok.split(":")
@@ -377,6 +434,11 @@ class FmmPlan:
         self.qd_ptr = _dev(h["qd_ptr"], i64, d)
         self.qd_rows = _dev(h["qd_rows"].reshape(-1), i64, d)
         self.quads = _dev(h["quads"].reshape(-1), i32, d)
+        pr = h["pair"]
+        self.n_pairs = int(pr["n"])
+        self.pr_slot = _dev(pr["pair_slot"], i64, d)
+        self.pr_ptr = _dev(pr["pair_ptr"], i64, d)
+        self.pr_ent = _dev(pr["ent"].reshape(-1), i32, d)
         tl = h["tl"]
         self.n_tiles = int(tl["n_tiles"]) if tl is not None else 0
         if self.n_tiles:
@@ -482,8 +544,11 @@ class FmmPlan:
         if self.m2l_variant_default == "auto" and self.config.dtype == "c64":
             fill = quad_fill(p, tt, [lv for lv in levels if int(lv) not in dense])
         self.quad_fill = fill
+        # rows per level from the full plan (identical on every rank)
+        flev = tt.level[p.l_cell[p.m2l_row_slot]] if p.m2l_row_slot.size else np.zeros(0, np.int64)
+        rpl = {int(lv): int(c) for lv, c in zip(*np.unique(flev, return_counts=True))}
         kinds = m2l_level_kinds(self.m2l_variant_default, self.config.dtype, levels, dense, fill,
-                                self.m2l_level_override, os.environ.get("DEFMM_M2L_LEVELS", ""))
+                                self.m2l_level_override, os.environ.get("DEFMM_M2L_LEVELS", ""), rpl)
         self.level_kinds = kinds
         rkind = np.array([kinds[int(lv)] for lv in rlev], dtype=object) if rows.size else np.zeros(0, object)
         z = np.zeros(0, np.int64)
@@ -506,6 +571,9 @@ class FmmPlan:
             is_rows[np.setdiff1d(t_ids, tl["rows"])] = True
         _, rptr, rsel = _sub_csr(h["row_ptr"], is_rows)
         h["rk_rows"], h["rk_ptr"], h["rk_ent"] = rows[is_rows], rptr, h["ent"][rsel]
+        # sibling pairs (K7 v8)
+        h["pair"] = m2l_pairs(np.nonzero(pick("pair"))[0], rows, h["row_ptr"], h["ent"], p.l_cell, p.l_dir,
+                              tt.level, tt.parent)
         # grouped rows (blocked + quad)
         is_grp = pick("blocked", "quad")
         grp_rows = rows[is_grp]
@@ -790,6 +858,8 @@ class FmmPlan:
         if self.m2l_variant == "hybrid":
             _lib.call(self._op("m2l_rows"), L, self.rk_rows.shape[0], self.rk_rows, self.rk_ptr, self.rk_ent,
                       self.hat, self.sym_derived, self.local, sh)
+            _lib.call(self._op("m2l_pair"), L, self.n_pairs, self.pr_slot, self.pr_ptr, self.pr_ent, self.hat,
+                      self.sym_derived, self.local, sh)
             _lib.call(self._op("m2l_blocked"), L, self.n_groups, self.grp_ptr, self.grp_rows, self.blk_src,
                       self.blk_trans, self.blk_mask, self.blk_kind, self.hat, self.sym_derived, self.lhat, sh)
             _lib.call(self._op("m2l_quad"), L, self.n_qgroups, self.qd_ptr, self.qd_rows, self.quads, self.hat,
@@ -872,7 +942,8 @@ class FmmPlan:
             return sorted(l for l, x in kinds.items() if x == k)
 
         out = []
-        for n, name, k in ((self.rk_rows.shape[0], "m2l_rows_kernel", "rows"), (self.n_groups, "m2l_blocked_kernel", "blocked"),
+        for n, name, k in ((self.rk_rows.shape[0], "m2l_rows_kernel", "rows"), (self.n_pairs, "m2l_pair_kernel", "pair"),
+                           (self.n_groups, "m2l_blocked_kernel", "blocked"),
                            (self.n_qgroups, "m2l_quad_kernel", "quad"), (self.n_tiles, "m2l_tile_kernel", "tile"),
                            (self.n_slice_batch, "m2l_slice_kernel", "slice"), (self.bk_rows.shape[0], "f2l_rows_kernel", None)):
             if n:
@@ -884,7 +955,7 @@ class FmmPlan:
         """Kernels of one matvec: p2p (+ split reduce), p2m, m2m per level, m2f,
         the M2L kernels with work, l2l per level, l2p."""
         if self.m2l_variant == "hybrid":
-            m2l = sum(int(n > 0) for n in (self.rk_rows.shape[0], self.n_groups, self.n_qgroups, self.n_tiles,
+            m2l = sum(int(n > 0) for n in (self.rk_rows.shape[0], self.n_pairs, self.n_groups, self.n_qgroups, self.n_tiles,
                                            self.n_slice_batch, self.bk_rows.shape[0]))
         else:
             m2l = 1

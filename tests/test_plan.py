@@ -433,7 +433,7 @@ def test_m2l_level_policy(case):
     blocked, sparse -> rows; "auto" moves complex64 sparse levels with full
     quads (>= QUAD_MIN_EVENTS_PER_QUAD events/quad) to the quad kernel and
     never complex128 ones; overrides (dict or env string) win; bad names raise."""
-    from paper_2202_04894_b200.fmm import (QUAD_MIN_EVENTS_PER_QUAD, block_levels, dense_levels,
+    from paper_2202_04894_b200.fmm import (PAIR_MIN_ROWS, QUAD_MIN_EVENTS_PER_QUAD, block_levels, dense_levels,
                                            m2l_level_kinds, quad_fill)
 
     tr, _, p = _plan(load_case(case))
@@ -444,15 +444,20 @@ def test_m2l_level_policy(case):
         assert (int(lv) in dense) == (ev[blev == lv].mean() >= 32.0)
     fill = quad_fill(p, tr, [lv for lv in levels if int(lv) not in dense])
     assert all(1.0 <= f <= 16.0 for f in fill.values())
-    k64 = m2l_level_kinds("auto", "c64", levels, dense, fill)
-    k128 = m2l_level_kinds("auto", "c128", levels, dense, fill)
+    # row counts per level scaled up so that some levels cross PAIR_MIN_ROWS
+    rpl = {int(lv): int(c) * (PAIR_MIN_ROWS // 2) for lv, c in zip(*np.unique(p.m2l_level, return_counts=True))}
+    k64 = m2l_level_kinds("auto", "c64", levels, dense, fill, rows_per_level=rpl)
+    k128 = m2l_level_kinds("auto", "c128", levels, dense, fill, rows_per_level=rpl)
     for lv in levels:
         lv = int(lv)
+        big = rpl.get(lv, 0) >= PAIR_MIN_ROWS
         if lv in dense:
             assert k64[lv] == k128[lv] == "blocked"
         else:
-            assert k128[lv] == "rows"
-            assert k64[lv] == ("quad" if fill.get(lv, 0.0) >= QUAD_MIN_EVENTS_PER_QUAD else "rows")
+            assert k128[lv] == ("pair" if big else "rows")
+            quad = fill.get(lv, 0.0) >= QUAD_MIN_EVENTS_PER_QUAD
+            assert k64[lv] == ("quad" if quad else "pair" if big else "rows")
+    assert set(m2l_level_kinds("auto", "c64", levels, dense, fill).values()) <= {"blocked", "rows", "quad"}
     assert set(m2l_level_kinds("hybrid_rows", "c64", levels, dense).values()) <= {"blocked", "rows"}
     lv0 = int(levels[0])
     assert m2l_level_kinds("auto", "c64", levels, dense, fill, {lv0: "tile"})[lv0] == "tile"
@@ -461,3 +466,34 @@ def test_m2l_level_policy(case):
         m2l_level_kinds("auto", "c64", levels, dense, override={lv0: "nope"})
     with pytest.raises(ValueError):
         m2l_level_kinds("nope", "c64", levels, dense)
+
+
+@pytest.mark.parametrize("case", ["cubesurf4000", "volume3000", "c1_kd16"])
+def test_m2l_pairs_reconstruct_every_row(case):
+    """fmm.m2l_pairs (pair M2L lists): rows are paired only with a sibling of
+    the same level and key, every row appears once, and each row's (source,
+    symbol) events are exactly its entries in the merged per-source lists."""
+    from paper_2202_04894_b200.fmm import m2l_pairs
+
+    tr, _, p = _plan(load_case(case))
+    ptr, ent, rows = p.m2l_row_ptr, p.m2l_rows_entries, p.m2l_row_slot
+    ids = np.arange(rows.shape[0])
+    pr = m2l_pairs(ids, rows, ptr, ent, p.l_cell, p.l_dir, tr.level, tr.parent)
+    ps = pr["pair_slot"].reshape(-1, 2)
+    assert sorted(ps[ps >= 0].tolist()) == sorted(rows.tolist())
+    row_of_slot = {int(s): i for i, s in enumerate(rows)}
+    for g in range(pr["n"]):
+        a, b = ps[g]
+        if b >= 0:
+            ca, cb = p.l_cell[a], p.l_cell[b]
+            assert tr.parent[ca] == tr.parent[cb] and p.l_dir[a] == p.l_dir[b]
+        e = pr["ent"][pr["pair_ptr"][g]:pr["pair_ptr"][g + 1]]
+        assert len(np.unique(e[:, 0])) == len(e)
+        for col, slot in ((1, a), (2, b)):
+            if slot < 0:
+                assert np.all(e[:, col] == -1)
+                continue
+            r = row_of_slot[int(slot)]
+            got = sorted(zip(e[e[:, col] >= 0, 0].tolist(), e[e[:, col] >= 0, col].tolist()))
+            want = sorted(zip(ent[ptr[r]:ptr[r + 1], 0].tolist(), ent[ptr[r]:ptr[r + 1], 1].tolist()))
+            assert got == want
