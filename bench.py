@@ -57,7 +57,7 @@ def _args():
                     help="N > 1 multipole exchange: halo (span all-reduce + all_to_all) or a full all-reduce")
     ap.add_argument("--m2l-levels", default="auto",
                     choices=["auto", "hybrid", "hybrid_rows", "blocked_all", "rows", "slice_all", "quad_all", "tiles",
-                             "tiles_all", "pairs", "pairs_all"])
+                             "tiles_all", "pairs", "pairs_all", "quartets", "quartets_all"])
     ap.add_argument("--m2l", default=None, help="M2L kernel variant (hybrid | derived | canonical)")
     return ap.parse_args()
 

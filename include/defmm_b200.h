@@ -164,11 +164,12 @@ int defmm_m2l_tiles(int64_t n_order, const int64_t* order, const int64_t* row_pt
  *   entries[seg[(r - row_base)(ngs+1) + g] .. seg[... + g + 1]), each {spectrum,
  *   (canonical index within the group << 6) | rotation id}.  lhat[r] = sum over
  *   events of rot(sym_canon) (*) hat -- the same sum as the row kernel.
- *   K7 v8 pair variant (m2l_pair): CTA g = rows pair_slot[2g], pair_slot[2g+1]
- *   (local slots; the second -1 for a single row); entries[4e..4e+3] for e in
- *   [pair_ptr[g], pair_ptr[g+1]) = {source spectrum, derived symbol for the
- *   first row or -1, for the second row or -1, 0}; local[slot] = F2L(sum) --
- *   the row kernel's sums, merged per source.
+ *   K7 v8 sibling-group variant (m2l_group, K = 2 or 4 rows): CTA g = rows
+ *   grp_slot[K g + k] (local slots; trailing -1 when the group is short);
+ *   entry e in [grp_ptr[g], grp_ptr[g+1]) = entries[S e .. S e + K] (S = 4 for
+ *   K = 2, 8 for K = 4) = {source spectrum, derived symbol for row k or -1
+ *   (k < K), 0 padding}; local[slot] = F2L(sum) -- the row kernel's sums,
+ *   merged per source.
  *   K7 v6 tile variant (m2l_tile): one CTA (256 threads) per tile, walking
  *   the spectrum in slices of F = 16 (c64) / 8 (c128) entries; dynamic shared
  *   memory 2 u_max F complex + ids + e_max events (the u_max / e_max the
@@ -219,9 +220,9 @@ int defmm_m2l_tiles(int64_t n_order, const int64_t* order, const int64_t* row_pt
                                 const int64_t* row_ptr, const int32_t* entries,                 \
                                 const void* hat, const void* sym_derived, void* local,          \
                                 void* stream);                                                  \
-    int defmm_m2l_pair_##SUFFIX(int32_t L, int64_t npairs, const int64_t* pair_slot,              \
-                                const int64_t* pair_ptr, const int32_t* entries, const void* hat,  \
-                                const void* sym_derived, void* local, void* stream);               \
+    int defmm_m2l_group_##SUFFIX(int32_t L, int32_t K, int64_t ngroups, const int64_t* grp_slot,  \
+                                 const int64_t* grp_ptr, const int32_t* entries, const void* hat, \
+                                 const void* sym_derived, void* local, void* stream);             \
     int defmm_m2l_blocked_##SUFFIX(int32_t L, int64_t ngroups, const int64_t* grp_ptr,           \
                                    const int64_t* grp_rows, const int32_t* blk_src,             \
                                    const int32_t* blk_trans, const int64_t* blk_mask,           \
@@ -266,11 +267,11 @@ int defmm_m2l_tiles(int64_t n_order, const int64_t* order, const int64_t* row_pt
                            void* stream);
 
 /* expands to: defmm_p2m_c128 defmm_m2m_c128 defmm_m2f_c128 defmm_symbols_c128
- * defmm_expand_symbols_c128 defmm_m2l_rows_c128 defmm_m2l_pair_c128 defmm_m2l_blocked_c128
+ * defmm_expand_symbols_c128 defmm_m2l_rows_c128 defmm_m2l_group_c128 defmm_m2l_blocked_c128
  * defmm_m2l_quad_c128 defmm_m2l_tile_c128 defmm_m2l_slice_c128 defmm_f2l_rows_c128 defmm_l2l_c128 defmm_l2p_c128 defmm_p2p_c128 */
 DEFMM_DECLARE_TYPED(c128)
 /* expands to: defmm_p2m_c64 defmm_m2m_c64 defmm_m2f_c64 defmm_symbols_c64
- * defmm_expand_symbols_c64 defmm_m2l_rows_c64 defmm_m2l_pair_c64 defmm_m2l_blocked_c64
+ * defmm_expand_symbols_c64 defmm_m2l_rows_c64 defmm_m2l_group_c64 defmm_m2l_blocked_c64
  * defmm_m2l_quad_c64 defmm_m2l_tile_c64 defmm_m2l_slice_c64 defmm_f2l_rows_c64 defmm_l2l_c64 defmm_l2p_c64 defmm_p2p_c64 */
 DEFMM_DECLARE_TYPED(c64)
 

@@ -49,7 +49,7 @@ for _t in ("c128", "c64"):
         f"defmm_m2l_blocked_{_t}": [_i32, _i64] + [_vp] * 10,
         f"defmm_m2l_quad_{_t}": [_i32, _i64] + [_vp] * 7,
         f"defmm_m2l_slice_{_t}": [_i32, _i64, _vp, _i64, _vp, _i32, _vp, _vp, _vp, _vp, _vp],
-        f"defmm_m2l_pair_{_t}": [_i32, _i64] + [_vp] * 7,
+        f"defmm_m2l_group_{_t}": [_i32, _i32, _i64] + [_vp] * 7,
         f"defmm_m2l_tile_{_t}": [_i32, _i64] + [_vp] * 5 + [_i64, _i32, _i32, _vp, _vp, _vp, _vp],
         f"defmm_f2l_rows_{_t}": [_i32, _i64, _vp, _vp, _vp, _vp],
         f"defmm_l2l_{_t}": [_i32, _i64, _vp, _vp, _vp, _vp, _vp, _f64, _vp, _f64, _vp, _vp],

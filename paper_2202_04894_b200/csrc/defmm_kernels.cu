@@ -951,29 +951,59 @@ __global__ void __launch_bounds__(m2l_block<R, L>()) m2l_rows_kernel(
 }
 
 // ---------------------------------------------------------------------------
-// K7 v8: pair M2L.  One CTA per PAIR of sibling rows (same level, key and
-// target parent; a single row when the group is odd).  The pair's events are
-// merged per source spectrum: entry {s, symbol of row a or -1, symbol of row b
-// or -1}, so a source both rows read is loaded once -- 1.6 operand loads per
-// event instead of the row kernel's 2 on surface data, with the row kernel's
-// streaming structure and register budget (the row kernel is bound by the
-// L1/shared data path: only register reuse takes bytes off it).  Two entries
-// in flight per iteration; F2L of both rows in shared memory.
+// K7 v8: sibling-group M2L (pair / quartet).  One CTA per group of K = 2 or 4
+// sibling rows (same level, key and target parent; fewer when the sibling set
+// runs out).  The group's events are merged per source spectrum: entry
+// {s, symbol of row 0 or -1, ..., symbol of row K-1 or -1} (padded to 4 / 8
+// ints), so a source several rows read is loaded once -- 1.6 (K = 2) / ~1.4
+// (K = 4) operand loads per event instead of the row kernel's 2 on surface
+// data, with the row kernel's streaming structure and register budget (the
+// row kernel is bound by the L1/shared data path: only register reuse takes
+// bytes off it).  F2L of the group's rows in shared memory, one after another.
 #ifndef DEFMM_PAIR_REGS
 #define DEFMM_PAIR_REGS 48
 #endif
-template <typename R, int L>
+template <int K>
+struct GroupEnt;
+template <>
+struct GroupEnt<2> {
+    int4 a;  // {s, t0, t1, 0}
+};
+template <>
+struct GroupEnt<4> {
+    int4 a, b;  // {s, t0, t1, t2}, {t3, 0, 0, 0}
+};
+template <int K>
+__device__ __forceinline__ GroupEnt<K> load_gent(const int* ent, int64_t e) {
+    GroupEnt<K> g;
+    g.a = __ldg(reinterpret_cast<const int4*>(ent) + (K == 2 ? e : 2 * e));
+    if constexpr (K == 4) g.b = __ldg(reinterpret_cast<const int4*>(ent) + 2 * e + 1);
+    return g;
+}
+template <int K>
+__device__ __forceinline__ int gent_src(const GroupEnt<K>& g) { return g.a.x; }
+template <int K>
+__device__ __forceinline__ int gent_sym(const GroupEnt<K>& g, int k) {
+    if constexpr (K == 2) {
+        return k == 0 ? g.a.y : g.a.z;
+    } else {
+        return k == 0 ? g.a.y : k == 1 ? g.a.z : k == 2 ? g.a.w : g.b.x;
+    }
+}
+
+template <typename R, int L, int K>
 __global__ void __launch_bounds__(m2l_block<R, L>(),
-                                  DEFMM_PAIR_REGS ? 65536 / (m2l_block<R, L>() * DEFMM_PAIR_REGS) : 1) m2l_pair_kernel(
-    int64_t npairs, const int64_t* __restrict__ pair_slot, const int64_t* __restrict__ pair_ptr,
-    const int4* __restrict__ ent, const cx<R>* __restrict__ hat, const cx<R>* __restrict__ symd,
-    cx<R>* __restrict__ local) {
+                                  DEFMM_PAIR_REGS ? 65536 / (m2l_block<R, L>() * DEFMM_PAIR_REGS) : 1)
+    m2l_group_kernel(int64_t ngroups, const int64_t* __restrict__ grp_slot, const int64_t* __restrict__ grp_ptr,
+                     const int* __restrict__ ent, const cx<R>* __restrict__ hat, const cx<R>* __restrict__ symd,
+                     cx<R>* __restrict__ local) {
     constexpr int P = pad<L>(), L3 = cube<L>(), P3 = P * P * P;
     constexpr int SS = spec_stride<R, L>();
     constexpr int NT = m2l_block<R, L>();
     constexpr bool VEC = sizeof(R) == 4;
     constexpr int W = VEC ? 2 : 1;
     constexpr int PER = (SS / W + NT - 1) / NT;
+    constexpr int UNROLL = K == 2 ? 2 : 1;  // entries in flight per iteration
     using V = cx<R>;
     using VT = std::conditional_t<VEC, float4, double2>;
     extern __shared__ unsigned char smraw[];
@@ -986,9 +1016,9 @@ __global__ void __launch_bounds__(m2l_block<R, L>(),
     const VT* hv = reinterpret_cast<const VT*>(hat);
     const VT* dv = reinterpret_cast<const VT*>(symd);
     constexpr int NV = SS / W;
-    V acc[2][PER][W];
+    V acc[K][PER][W];
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
+    for (int u = 0; u < K; ++u)
 #pragma unroll
         for (int m = 0; m < PER; ++m)
 #pragma unroll
@@ -1001,32 +1031,44 @@ __global__ void __launch_bounds__(m2l_block<R, L>(),
             a[0] = cfma(d, x, a[0]);
         }
     };
-    const int64_t e0 = pair_ptr[g], e1 = pair_ptr[g + 1];
-    for (int64_t e = e0; e < e1; e += 2) {
-        const bool two = e + 1 < e1;
-        const int4 p = __ldg(ent + e);
-        const int4 q = two ? __ldg(ent + e + 1) : make_int4(p.x, -1, -1, 0);
+    const int64_t e0 = grp_ptr[g], e1 = grp_ptr[g + 1];
+    for (int64_t e = e0; e < e1; e += UNROLL) {
+        GroupEnt<K> en[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+            if (e + u < e1) {
+                en[u] = load_gent<K>(ent, e + u);
+            } else {  // no-op entry: every symbol absent
+                en[u] = load_gent<K>(ent, e);
+                en[u].a.y = en[u].a.z = -1;
+                if constexpr (K == 4) en[u].a.w = en[u].b.x = -1;
+            }
+        }
 #pragma unroll
         for (int m = 0; m < PER; ++m) {
             const int jv = threadIdx.x + m * NT;
             if (jv < NV) {
-                const VT sp = __ldg(hv + (int64_t)p.x * NV + jv);
-                const VT sq = __ldg(hv + (int64_t)q.x * NV + jv);
-                const VT dpa = p.y >= 0 ? __ldg(dv + (int64_t)p.y * NV + jv) : VT{};
-                const VT dpb = p.z >= 0 ? __ldg(dv + (int64_t)p.z * NV + jv) : VT{};
-                const VT dqa = q.y >= 0 ? __ldg(dv + (int64_t)q.y * NV + jv) : VT{};
-                const VT dqb = q.z >= 0 ? __ldg(dv + (int64_t)q.z * NV + jv) : VT{};
-                fma_v(acc[0][m], dpa, sp);
-                fma_v(acc[1][m], dpb, sp);
-                fma_v(acc[0][m], dqa, sq);
-                fma_v(acc[1][m], dqb, sq);
+                VT sv[UNROLL], dk[UNROLL][K];
+#pragma unroll
+                for (int u = 0; u < UNROLL; ++u) {
+                    sv[u] = __ldg(hv + (int64_t)gent_src<K>(en[u]) * NV + jv);
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        const int t = gent_sym<K>(en[u], k);
+                        dk[u][k] = t >= 0 ? __ldg(dv + (int64_t)t * NV + jv) : VT{};
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < UNROLL; ++u)
+#pragma unroll
+                    for (int k = 0; k < K; ++k) fma_v(acc[k][m], dk[u][k], sv[u]);
             }
         }
     }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-        const int64_t slot = pair_slot[2 * g + u];
-        if (slot < 0) break;  // uniform
+    for (int u = 0; u < K; ++u) {
+        const int64_t slot = grp_slot[K * g + u];
+        if (slot < 0) break;  // uniform; rows fill the group from the front
 #pragma unroll
         for (int m = 0; m < PER; ++m) {
             const int jv = threadIdx.x + m * NT;
@@ -2530,22 +2572,30 @@ int launch_m2l_rows(int32_t L, int64_t nrows, const int64_t* row_slot, const int
 }
 
 template <typename R>
-int launch_m2l_pair(int32_t L, int64_t npairs, const int64_t* pair_slot, const int64_t* pair_ptr, const int32_t* ent,
-                    const void* hat, const void* symd, void* local, void* stream) {
-    if (npairs == 0) return 0;
-    if (!grid_ok(npairs)) return -1;
+int launch_m2l_group(int32_t L, int32_t K, int64_t ngroups, const int64_t* grp_slot, const int64_t* grp_ptr,
+                     const int32_t* ent, const void* hat, const void* symd, void* local, void* stream) {
+    if (ngroups == 0) return 0;
+    if (!grid_ok(ngroups) || (K != 2 && K != 4)) return -1;
     if (int rc0 = ensure_twiddles()) return rc0;
     cudaStream_t s = (cudaStream_t)stream;
     DEFMM_DISPATCH_L(L, {
         constexpr int P = 2 * LL - 1;
         const size_t bytes = sizeof(double2) * (P * LL + P * P * P + 1 + LL * P * P + LL * LL * LL);
-        int rc = set_smem(m2l_pair_kernel<R, LL>, bytes);
-        if (rc) return rc;
-        carve(m2l_pair_kernel<R, LL>);
-        m2l_pair_kernel<R, LL><<<(unsigned)npairs, m2l_block<R, LL>(), bytes, s>>>(
-            npairs, pair_slot, pair_ptr, (const int4*)ent, (const cx<R>*)hat, (const cx<R>*)symd, (cx<R>*)local);
+        if (K == 2) {
+            int rc = set_smem(m2l_group_kernel<R, LL, 2>, bytes);
+            if (rc) return rc;
+            carve(m2l_group_kernel<R, LL, 2>);
+            m2l_group_kernel<R, LL, 2><<<(unsigned)ngroups, m2l_block<R, LL>(), bytes, s>>>(
+                ngroups, grp_slot, grp_ptr, ent, (const cx<R>*)hat, (const cx<R>*)symd, (cx<R>*)local);
+        } else {
+            int rc = set_smem(m2l_group_kernel<R, LL, 4>, bytes);
+            if (rc) return rc;
+            carve(m2l_group_kernel<R, LL, 4>);
+            m2l_group_kernel<R, LL, 4><<<(unsigned)ngroups, m2l_block<R, LL>(), bytes, s>>>(
+                ngroups, grp_slot, grp_ptr, ent, (const cx<R>*)hat, (const cx<R>*)symd, (cx<R>*)local);
+        }
     });
-    return report(cudaGetLastError(), "m2l_pair");
+    return report(cudaGetLastError(), "m2l_group");
 }
 
 template <typename R>
@@ -2740,10 +2790,10 @@ const char* defmm_last_error(void) { return g_last_error; }
                                 void* stream) {                                                                    \
         return launch_m2l_rows<R>(L, nrows, row_slot, row_ptr, entries, hat, sym_derived, local, stream);          \
     }                                                                                                               \
-    int defmm_m2l_pair_##SUFFIX(int32_t L, int64_t npairs, const int64_t* pair_slot, const int64_t* pair_ptr,       \
-                                const int32_t* entries, const void* hat, const void* sym_derived, void* local,     \
-                                void* stream) {                                                                    \
-        return launch_m2l_pair<R>(L, npairs, pair_slot, pair_ptr, entries, hat, sym_derived, local, stream);       \
+    int defmm_m2l_group_##SUFFIX(int32_t L, int32_t K, int64_t ngroups, const int64_t* grp_slot,                  \
+                                 const int64_t* grp_ptr, const int32_t* entries, const void* hat,                 \
+                                 const void* sym_derived, void* local, void* stream) {                            \
+        return launch_m2l_group<R>(L, K, ngroups, grp_slot, grp_ptr, entries, hat, sym_derived, local, stream);   \
     }                                                                                                               \
     int defmm_m2l_blocked_##SUFFIX(int32_t L, int64_t ngroups, const int64_t* grp_ptr, const int64_t* grp_rows,     \
                                    const int32_t* blk_src, const int32_t* blk_trans, const int64_t* blk_mask,     \

@@ -149,15 +149,16 @@ def m2l_tiles(order, row_ptr, ent, n_hat: int, n_trans: int, u_max: int, k_max: 
             "ops": ops[:no], "ev_ptr": ev_ptr[: nr + 1], "ev": ev[:ne], "untiled": int(counts[4])}
 
 
-def m2l_pairs(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent) -> dict:
-    """Pair lists of the pair M2L (K7 v8, defmm_m2l_pair_*): the rows ``ids``
-    (indices into ``rows``, the local slots) grouped by (level, key, target
-    parent), consecutive siblings paired (an odd one alone); each pair's events
-    merged per source spectrum into {s, symbol of row a | -1, of row b | -1, 0}."""
-    z = np.zeros(0, np.int64)
+def m2l_groups(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent, K: int = 2) -> dict:
+    """Sibling-group lists of the group M2L (K7 v8, defmm_m2l_group_*, K = 2 or
+    4): the rows ``ids`` (indices into ``rows``, the local slots) grouped by
+    (level, key, target parent), consecutive siblings packed K per CTA group;
+    each group's events merged per source spectrum into {s, symbol of row k or
+    -1 (k < K)} padded to 4 (K = 2) / 8 (K = 4) ints."""
+    S = 4 if K == 2 else 8
     if ids.size == 0:
-        return {"n": 0, "pair_slot": np.zeros(0, np.int64), "pair_ptr": np.zeros(1, np.int64),
-                "ent": np.zeros((0, 4), np.int32)}
+        return {"n": 0, "K": K, "grp_slot": np.zeros(0, np.int64), "grp_ptr": np.zeros(1, np.int64),
+                "ent": np.zeros((0, S), np.int32)}
     slots = rows[ids]
     cell = l_cell[slots]
     key = l_dir[slots].astype(np.int64)
@@ -170,29 +171,33 @@ def m2l_pairs(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent) -> dict:
     new[1:] = (lev[1:] != lev[:-1]) | (key[1:] != key[:-1]) | (par[1:] != par[:-1])
     gstart = np.nonzero(new)[0]
     pos = np.arange(n) - gstart[np.cumsum(new) - 1]
-    side = pos % 2  # 0: row a, 1: row b of the pair
-    pid = np.cumsum(side == 0) - 1  # pair id of each row
-    npairs = int(pid[-1]) + 1
-    pair_slot = np.full((npairs, 2), -1, np.int64)
-    pair_slot[pid, side] = slots
+    side = pos % K  # row index within its CTA group
+    gid = np.cumsum(side == 0) - 1
+    ng = int(gid[-1]) + 1
+    grp_slot = np.full((ng, K), -1, np.int64)
+    grp_slot[gid, side] = slots
     cnt = row_ptr[ids + 1] - row_ptr[ids]
     rep = np.repeat(np.arange(n), cnt)
     sel = np.repeat(row_ptr[ids] - np.concatenate([[0], np.cumsum(cnt)[:-1]]), cnt) + np.arange(int(cnt.sum()))
     ev = ent[sel]
-    ep, es, et, eside = pid[rep], ev[:, 0].astype(np.int64), ev[:, 1], side[rep]
-    so = np.lexsort((eside, es, ep))
-    ep, es, et, eside = ep[so], es[so], et[so], eside[so]
-    first = np.ones(ep.shape[0], bool)
-    first[1:] = (ep[1:] != ep[:-1]) | (es[1:] != es[:-1])
+    eg, es, et, eside = gid[rep], ev[:, 0].astype(np.int64), ev[:, 1], side[rep]
+    so = np.lexsort((eside, es, eg))
+    eg, es, et, eside = eg[so], es[so], et[so], eside[so]
+    first = np.ones(eg.shape[0], bool)
+    first[1:] = (eg[1:] != eg[:-1]) | (es[1:] != es[:-1])
     eid = np.cumsum(first) - 1
     m = int(eid[-1]) + 1 if eid.size else 0
-    out = np.full((m, 4), -1, np.int32)
-    out[:, 3] = 0
+    out = np.full((m, S), -1, np.int32)
+    out[:, K + 1:] = 0
     out[eid, 0] = es
-    out[eid[eside == 0], 1] = et[eside == 0]
-    out[eid[eside == 1], 2] = et[eside == 1]
-    pair_ptr = np.searchsorted(ep[first], np.arange(npairs + 1)).astype(np.int64)
-    return {"n": npairs, "pair_slot": pair_slot.reshape(-1), "pair_ptr": pair_ptr, "ent": out}
+    out[eid, 1 + eside] = et
+    grp_ptr = np.searchsorted(eg[first], np.arange(ng + 1)).astype(np.int64)
+    return {"n": ng, "K": K, "grp_slot": grp_slot.reshape(-1), "grp_ptr": grp_ptr, "ent": out}
+
+
+def m2l_pairs(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent) -> dict:
+    """K = 2 sibling groups (m2l_groups)."""
+    return m2l_groups(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent, 2)
 
 
 def _rows_to_ids(slots, rows):
@@ -223,9 +228,10 @@ M2L_MODE_KINDS = {
     "auto": ("blocked", "rows"), "hybrid_rows": ("blocked", "rows"), "hybrid": ("blocked", "quad"),
     "rows": ("rows", "rows"), "blocked_all": ("blocked", "blocked"), "quad_all": ("quad", "quad"),
     "tiles": ("blocked", "tile"), "tiles_all": ("tile", "tile"), "slice_all": ("slice", "slice"),
-    "pairs": ("blocked", "pair"), "pairs_all": ("pair", "pair"),
+    "pairs": ("blocked", "pair"), "pairs_all": ("pair", "pair"), "quartets": ("blocked", "quartet"),
+    "quartets_all": ("quartet", "quartet"),
 }
-M2L_KERNELS = ("rows", "blocked", "quad", "tile", "slice", "pair")
+M2L_KERNELS = ("rows", "blocked", "quad", "tile", "slice", "pair", "quartet")
 # events per parent-pair block above which a level counts as dense (blocked kernel)
 BLOCKED_MIN_EVENTS_PER_BLOCK = 32.0
 # "auto": a complex64 sparse level runs the quad kernel when its quads are this
@@ -434,11 +440,13 @@ class FmmPlan:
         self.qd_ptr = _dev(h["qd_ptr"], i64, d)
         self.qd_rows = _dev(h["qd_rows"].reshape(-1), i64, d)
         self.quads = _dev(h["quads"].reshape(-1), i32, d)
-        pr = h["pair"]
-        self.n_pairs = int(pr["n"])
-        self.pr_slot = _dev(pr["pair_slot"], i64, d)
-        self.pr_ptr = _dev(pr["pair_ptr"], i64, d)
-        self.pr_ent = _dev(pr["ent"].reshape(-1), i32, d)
+        self.sib_groups = []  # (K, n, slots, ptr, entries) of the pair / quartet kernels
+        for kind in ("pair", "quartet"):
+            gr = h[kind]
+            if gr["n"]:
+                self.sib_groups.append((gr["K"], int(gr["n"]), _dev(gr["grp_slot"], i64, d),
+                                        _dev(gr["grp_ptr"], i64, d), _dev(gr["ent"].reshape(-1), i32, d)))
+        self.n_pairs = sum(x[1] for x in self.sib_groups)
         tl = h["tl"]
         self.n_tiles = int(tl["n_tiles"]) if tl is not None else 0
         if self.n_tiles:
@@ -572,8 +580,10 @@ class FmmPlan:
         _, rptr, rsel = _sub_csr(h["row_ptr"], is_rows)
         h["rk_rows"], h["rk_ptr"], h["rk_ent"] = rows[is_rows], rptr, h["ent"][rsel]
         # sibling pairs (K7 v8)
-        h["pair"] = m2l_pairs(np.nonzero(pick("pair"))[0], rows, h["row_ptr"], h["ent"], p.l_cell, p.l_dir,
-                              tt.level, tt.parent)
+        h["pair"] = m2l_groups(np.nonzero(pick("pair"))[0], rows, h["row_ptr"], h["ent"], p.l_cell, p.l_dir,
+                               tt.level, tt.parent, 2)
+        h["quartet"] = m2l_groups(np.nonzero(pick("quartet"))[0], rows, h["row_ptr"], h["ent"], p.l_cell, p.l_dir,
+                                  tt.level, tt.parent, 4)
         # grouped rows (blocked + quad)
         is_grp = pick("blocked", "quad")
         grp_rows = rows[is_grp]
@@ -858,8 +868,9 @@ class FmmPlan:
         if self.m2l_variant == "hybrid":
             _lib.call(self._op("m2l_rows"), L, self.rk_rows.shape[0], self.rk_rows, self.rk_ptr, self.rk_ent,
                       self.hat, self.sym_derived, self.local, sh)
-            _lib.call(self._op("m2l_pair"), L, self.n_pairs, self.pr_slot, self.pr_ptr, self.pr_ent, self.hat,
-                      self.sym_derived, self.local, sh)
+            for K, ng, gslot, gptr, gent in self.sib_groups:
+                _lib.call(self._op("m2l_group"), L, K, ng, gslot, gptr, gent, self.hat, self.sym_derived,
+                          self.local, sh)
             _lib.call(self._op("m2l_blocked"), L, self.n_groups, self.grp_ptr, self.grp_rows, self.blk_src,
                       self.blk_trans, self.blk_mask, self.blk_kind, self.hat, self.sym_derived, self.lhat, sh)
             _lib.call(self._op("m2l_quad"), L, self.n_qgroups, self.qd_ptr, self.qd_rows, self.quads, self.hat,
@@ -942,7 +953,9 @@ class FmmPlan:
             return sorted(l for l, x in kinds.items() if x == k)
 
         out = []
-        for n, name, k in ((self.rk_rows.shape[0], "m2l_rows_kernel", "rows"), (self.n_pairs, "m2l_pair_kernel", "pair"),
+        for n, name, k in ((self.rk_rows.shape[0], "m2l_rows_kernel", "rows"),
+                           (sum(x[1] for x in self.sib_groups if x[0] == 2), "m2l_group_kernel<2>", "pair"),
+                           (sum(x[1] for x in self.sib_groups if x[0] == 4), "m2l_group_kernel<4>", "quartet"),
                            (self.n_groups, "m2l_blocked_kernel", "blocked"),
                            (self.n_qgroups, "m2l_quad_kernel", "quad"), (self.n_tiles, "m2l_tile_kernel", "tile"),
                            (self.n_slice_batch, "m2l_slice_kernel", "slice"), (self.bk_rows.shape[0], "f2l_rows_kernel", None)):
@@ -955,7 +968,7 @@ class FmmPlan:
         """Kernels of one matvec: p2p (+ split reduce), p2m, m2m per level, m2f,
         the M2L kernels with work, l2l per level, l2p."""
         if self.m2l_variant == "hybrid":
-            m2l = sum(int(n > 0) for n in (self.rk_rows.shape[0], self.n_pairs, self.n_groups, self.n_qgroups, self.n_tiles,
+            m2l = len(self.sib_groups) + sum(int(n > 0) for n in (self.rk_rows.shape[0], self.n_groups, self.n_qgroups, self.n_tiles,
                                            self.n_slice_batch, self.bk_rows.shape[0]))
         else:
             m2l = 1

@@ -148,12 +148,13 @@ def test_m2l_canonical_gather_and_derived_symbols_agree(case):
     plan.m2l_variant = "hybrid"
     c = plan.apply().cpu().numpy()
     assert _rel(c, a) <= 1e-13
-    for mode in ("blocked_all", "rows", "slice_all", "hybrid_rows", "quad_all", "tiles", "tiles_all", "pairs_all"):
+    for mode in ("blocked_all", "rows", "slice_all", "hybrid_rows", "quad_all", "tiles", "tiles_all", "pairs_all",
+                 "quartets_all"):
         p2 = FmmPlan(g["points"], None, FmmConfig(**g["config"]), charges=g["charges"], reuse=plan, m2l=mode)
         assert _rel(p2.apply().cpu().numpy(), a) <= 1e-13
     # every kernel on some level at once (per-level overrides)
     levels = sorted(plan.level_kinds)
-    mix = {lv: ("rows", "blocked", "quad", "tile", "slice", "pair")[i % 6] for i, lv in enumerate(levels)}
+    mix = {lv: ("rows", "blocked", "quad", "tile", "slice", "pair", "quartet")[i % 7] for i, lv in enumerate(levels)}
     p2 = FmmPlan(g["points"], None, FmmConfig(**g["config"]), charges=g["charges"], reuse=plan, m2l_levels=mix)
     assert p2.level_kinds == mix
     assert _rel(p2.apply().cpu().numpy(), a) <= 1e-13

@@ -468,28 +468,29 @@ def test_m2l_level_policy(case):
         m2l_level_kinds("nope", "c64", levels, dense)
 
 
+@pytest.mark.parametrize("K", [2, 4])
 @pytest.mark.parametrize("case", ["cubesurf4000", "volume3000", "c1_kd16"])
-def test_m2l_pairs_reconstruct_every_row(case):
+def test_m2l_groups_reconstruct_every_row(case, K):
     """fmm.m2l_pairs (pair M2L lists): rows are paired only with a sibling of
     the same level and key, every row appears once, and each row's (source,
     symbol) events are exactly its entries in the merged per-source lists."""
-    from paper_2202_04894_b200.fmm import m2l_pairs
+    from paper_2202_04894_b200.fmm import m2l_groups
 
     tr, _, p = _plan(load_case(case))
     ptr, ent, rows = p.m2l_row_ptr, p.m2l_rows_entries, p.m2l_row_slot
     ids = np.arange(rows.shape[0])
-    pr = m2l_pairs(ids, rows, ptr, ent, p.l_cell, p.l_dir, tr.level, tr.parent)
-    ps = pr["pair_slot"].reshape(-1, 2)
+    pr = m2l_groups(ids, rows, ptr, ent, p.l_cell, p.l_dir, tr.level, tr.parent, K)
+    ps = pr["grp_slot"].reshape(-1, K)
     assert sorted(ps[ps >= 0].tolist()) == sorted(rows.tolist())
     row_of_slot = {int(s): i for i, s in enumerate(rows)}
     for g in range(pr["n"]):
-        a, b = ps[g]
-        if b >= 0:
-            ca, cb = p.l_cell[a], p.l_cell[b]
-            assert tr.parent[ca] == tr.parent[cb] and p.l_dir[a] == p.l_dir[b]
-        e = pr["ent"][pr["pair_ptr"][g]:pr["pair_ptr"][g + 1]]
+        members = [int(x) for x in ps[g] if x >= 0]
+        assert all(x < 0 for x in ps[g][len(members):])  # rows fill the group from the front
+        cells = p.l_cell[members]
+        assert len(set(tr.parent[cells].tolist())) == 1 and len(set(p.l_dir[members].tolist())) == 1
+        e = pr["ent"][pr["grp_ptr"][g]:pr["grp_ptr"][g + 1]]
         assert len(np.unique(e[:, 0])) == len(e)
-        for col, slot in ((1, a), (2, b)):
+        for col, slot in enumerate(ps[g], start=1):
             if slot < 0:
                 assert np.all(e[:, col] == -1)
                 continue
