@@ -239,6 +239,9 @@ BLOCKED_MIN_EVENTS_PER_BLOCK = 32.0
 # events/quad (cfg2 L4-5, cfg3) and every complex128 level lose
 # (profiles/r01_summary_v5.md)
 QUAD_MIN_EVENTS_PER_QUAD = 12.0
+# ... and only up to this order: at L = 6 the pair kernel beats the quads on
+# the same cfg2 level (10.2 vs 11.1 ms, profiles/r01_summary_v7.md)
+QUAD_MAX_ORDER = 4
 # "auto": other sparse levels with at least this many rows run the pair kernel
 # (sibling rows merged per source: cfg2 M2L -9%, cfg3 -10%); small levels
 # (cfg1) keep the row kernel (profiles/r01_summary_v7.md)
@@ -280,7 +283,7 @@ def quad_fill(plan, tt, levels) -> dict:
 
 
 def m2l_level_kinds(mode: str, dtype: str, levels, dense, fill=None, override=None, env: str = "",
-                    rows_per_level=None) -> dict:
+                    rows_per_level=None, order: int = 4) -> dict:
     """level -> M2L kernel: the mode's (dense, sparse) choice; in "auto" a
     complex64 sparse level with quad fill >= QUAD_MIN_EVENTS_PER_QUAD runs
     quads, another sparse level with >= PAIR_MIN_ROWS rows the pair kernel;
@@ -293,7 +296,7 @@ def m2l_level_kinds(mode: str, dtype: str, levels, dense, fill=None, override=No
         for lv in list(kinds):
             if kinds[lv] != "rows":
                 continue
-            if dtype == "c64" and (fill or {}).get(lv, 0.0) >= QUAD_MIN_EVENTS_PER_QUAD:
+            if dtype == "c64" and order <= QUAD_MAX_ORDER and (fill or {}).get(lv, 0.0) >= QUAD_MIN_EVENTS_PER_QUAD:
                 kinds[lv] = "quad"
             elif (rows_per_level or {}).get(lv, 0) >= PAIR_MIN_ROWS:
                 kinds[lv] = "pair"
@@ -549,14 +552,14 @@ class FmmPlan:
         dense = dense_levels(p, tt, self.BLOCKED_MIN_EVENTS_PER_BLOCK)
         levels = np.unique(rlev)
         fill = None
-        if self.m2l_variant_default == "auto" and self.config.dtype == "c64":
+        if self.m2l_variant_default == "auto" and self.config.dtype == "c64" and self.L <= QUAD_MAX_ORDER:
             fill = quad_fill(p, tt, [lv for lv in levels if int(lv) not in dense])
         self.quad_fill = fill
         # rows per level from the full plan (identical on every rank)
         flev = tt.level[p.l_cell[p.m2l_row_slot]] if p.m2l_row_slot.size else np.zeros(0, np.int64)
         rpl = {int(lv): int(c) for lv, c in zip(*np.unique(flev, return_counts=True))}
         kinds = m2l_level_kinds(self.m2l_variant_default, self.config.dtype, levels, dense, fill,
-                                self.m2l_level_override, os.environ.get("DEFMM_M2L_LEVELS", ""), rpl)
+                                self.m2l_level_override, os.environ.get("DEFMM_M2L_LEVELS", ""), rpl, self.L)
         self.level_kinds = kinds
         rkind = np.array([kinds[int(lv)] for lv in rlev], dtype=object) if rows.size else np.zeros(0, object)
         z = np.zeros(0, np.int64)

@@ -458,6 +458,7 @@ def test_m2l_level_policy(case):
             quad = fill.get(lv, 0.0) >= QUAD_MIN_EVENTS_PER_QUAD
             assert k64[lv] == ("quad" if quad else "pair" if big else "rows")
     assert set(m2l_level_kinds("auto", "c64", levels, dense, fill).values()) <= {"blocked", "rows", "quad"}
+    assert "quad" not in m2l_level_kinds("auto", "c64", levels, dense, fill, rows_per_level=rpl, order=6).values()
     assert set(m2l_level_kinds("hybrid_rows", "c64", levels, dense).values()) <= {"blocked", "rows"}
     lv0 = int(levels[0])
     assert m2l_level_kinds("auto", "c64", levels, dense, fill, {lv0: "tile"})[lv0] == "tile"
