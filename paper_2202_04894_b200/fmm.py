@@ -808,7 +808,8 @@ class FmmPlan:
             h = self.halo
             dev = self.mult.device
             idx = lambda a: torch.as_tensor(a, dtype=torch.int64, device=dev)  # noqa: E731
-            self._halo_t = (idx(h.span), idx(h.send), list(h.send_counts), idx(h.recv), list(h.recv_counts))
+            self._halo_t = (idx(h.span), idx(h.send), list(h.send_counts), idx(h.recv), list(h.recv_counts),
+                            bool(h.active))
         return self._halo_t
 
     def _near_field(self, stage_events):

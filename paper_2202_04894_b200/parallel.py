@@ -128,6 +128,7 @@ class Halo:
     send_counts: list
     recv: np.ndarray  # multipoles this rank reads from others, by source
     recv_counts: list
+    active: bool = True  # any rank exchanges anything (the all_to_all is collective: same on every rank)
 
 
 def _rank_span(plan, tt, cuts):
@@ -154,6 +155,8 @@ def make_halo(plan, tt, cuts, rank: int, world: int) -> Halo:
     span = np.nonzero(a != b)[0]
     owner = np.where(a == b, a, -1)
     need = [_needed(plan, tt, cuts, r) for r in range(world)]
+    # does any rank read a multipole owned by another one? (identical on every rank)
+    active = any(bool(np.any((owner[nd] >= 0) & (owner[nd] != r))) for r, nd in enumerate(need))
     send, send_counts, recv, recv_counts = [], [], [], []
     for r in range(world):
         if r == rank:
@@ -167,23 +170,23 @@ def make_halo(plan, tt, cuts, rank: int, world: int) -> Halo:
         send_counts.append(int(s_r.shape[0]))
         recv_counts.append(int(v_r.shape[0]))
     cat = lambda xs: np.concatenate(xs).astype(np.int64) if xs else np.zeros(0, np.int64)  # noqa: E731
-    return Halo(span.astype(np.int64), cat(send), send_counts, cat(recv), recv_counts)
+    return Halo(span.astype(np.int64), cat(send), send_counts, cat(recv), recv_counts, active)
 
 
 def halo_exchange(mult, halo_dev, group=None):
     """Complete the multipoles this rank's M2F reads.  ``mult``: (n_mult, L^3)
-    complex tensor; ``halo_dev`` = (span, send, send_counts, recv, recv_counts)
-    with the index tensors on mult's device.  Complex data travels as its real
+    complex tensor; ``halo_dev`` = (span, send, send_counts, recv, recv_counts,
+    active) with the index tensors on mult's device.  Complex data travels as its real
     view (NCCL / gloo have no complex types)."""
     import torch
     import torch.distributed as dist
 
-    span, send, send_counts, recv, recv_counts = halo_dev
-    if span.numel():
+    span, send, send_counts, recv, recv_counts, active = halo_dev
+    if span.numel():  # the same list on every rank
         buf = mult.index_select(0, span)
         dist.all_reduce(torch.view_as_real(buf), group=group)
         mult.index_copy_(0, span, buf)
-    if sum(send_counts) + sum(recv_counts):
+    if active:  # collective: decided identically on every rank (Halo.active)
         per = 2 * mult.shape[1]  # reals per multipole
         sbuf = torch.view_as_real(mult.index_select(0, send)).contiguous()
         rbuf = torch.empty((recv.shape[0], mult.shape[1], 2), dtype=sbuf.dtype, device=mult.device)

@@ -138,7 +138,7 @@ def _halo_worker(rank, world, port, case, q):
         mult = torch.from_numpy(np.stack([cnt, 2.0 * cnt], 1)).to(torch.complex128)
         mult[:, 1] *= 1j
         idx = lambda a: torch.as_tensor(a, dtype=torch.int64)  # noqa: E731
-        halo_exchange(mult, (idx(h.span), idx(h.send), h.send_counts, idx(h.recv), h.recv_counts))
+        halo_exchange(mult, (idx(h.span), idx(h.send), h.send_counts, idx(h.recv), h.recv_counts, h.active))
         need = _needed(pl, tr, sh.cuts, rank)
         full = np.array([tr.stop[c] - tr.start[c] for c in pl.m_cell], np.float64)
         got = mult.numpy()
