@@ -596,10 +596,21 @@ __global__ void __launch_bounds__(32 * M2F_WARPS) m2f_kernel(int64_t n, const in
 // L1/shared-throughput bound at 94%, 25% of the HBM roofline, r01_summary_v6).
 // The natural-order spectrum is assembled in shared memory and written out
 // coalesced in orbit order.
+// When the P^3 staging buffer would take a warp past 12 KB of shared memory
+// (c64 L >= 6, c128 L >= 5) the last stage writes the spectrum straight to
+// global memory in orbit order (scattered within the expansion's own
+// spectrum) instead: twice the warps per SM, shared memory being the
+// occupancy limit (c128 L5 1946 -> 1327 us, c64 L6 717 -> 666 us; c64 L5 is
+// faster staged: 897 vs 992 us)
+template <typename R, int L>
+__host__ __device__ constexpr bool m2f2_direct() {
+    constexpr int P = 2 * L - 1;
+    return (L * L * L + L * L * P + L * P * P + P * P * P) * (int)sizeof(cx<R>) > 12 * 1024;
+}
 template <typename R, int L>
 __host__ __device__ constexpr int m2f2_warp_elems() {
     constexpr int P = 2 * L - 1;
-    return L * L * L + L * L * P + L * P * P + P * P * P;
+    return L * L * L + L * L * P + L * P * P + (m2f2_direct<R, L>() ? 0 : P * P * P);
 }
 template <typename R, int L>
 __host__ __device__ constexpr bool m2f2_fits() {
@@ -670,13 +681,21 @@ __global__ void __launch_bounds__(32 * M2F_WARPS) m2f2_kernel(int64_t n, const i
             V v = cz<V>();
 #pragma unroll
             for (int a = 0; a < L; ++a) v = cfma(z[a], twc<L, V>(f, a), v);
-            Z[f * PP + row] = cscale(v, scale);
+            if constexpr (m2f2_direct<R, L>()) {
+                hat[i * (int64_t)spec_stride<R, L>() + finv<L>(f * PP + row)] = cscale(v, scale);
+            } else {
+                Z[f * PP + row] = cscale(v, scale);
+            }
         }
     }
-    __syncwarp();
     constexpr int SS = spec_stride<R, L>();
     V* out = hat + i * (int64_t)SS;
-    for (int t = lane; t < SS; t += 32) out[t] = t < P3 ? Z[forder<L>(t)] : cz<V>();  // pad entry (c64) = 0
+    if constexpr (m2f2_direct<R, L>()) {
+        if (lane == 0 && SS > P3) out[P3] = cz<V>();  // pad entry (c64)
+    } else {
+        __syncwarp();
+        for (int t = lane; t < SS; t += 32) out[t] = t < P3 ? Z[forder<L>(t)] : cz<V>();  // pad entry (c64) = 0
+    }
 }
 
 // K9 symbols: kernel column G(beta (t + z)) on the difference grid (wrap
