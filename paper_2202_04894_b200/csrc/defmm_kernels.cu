@@ -309,6 +309,9 @@ __global__ void __launch_bounds__(128) p2m_kernel(
 // real mode products in per-warp shared memory with __syncwarp only.
 
 constexpr int NODAL_WARPS = 8;
+#ifndef DEFMM_NODAL_MINB
+#define DEFMM_NODAL_MINB 4  // <= 64 registers: 4 CTAs/SM (L5: M2M -12..-32%, L2L -13..-29%)
+#endif
 
 // One mode product along `axis` of an L^3 tile (C order) with the real factor
 // A_bit: TRANSPOSE=false -> out k, in j, coefficient A[bit][k][j] (M2M);
@@ -338,7 +341,7 @@ __host__ __device__ constexpr int nodal_smem_bytes() {
 }
 
 template <typename R, int L>
-__global__ void __launch_bounds__(32 * NODAL_WARPS) m2m_kernel(
+__global__ void __launch_bounds__(32 * NODAL_WARPS, DEFMM_NODAL_MINB) m2m_kernel(
     int64_t n, const int64_t* __restrict__ out_slot, const int32_t* __restrict__ dir,
     const int64_t* __restrict__ son_slot, double son_beta, const double* __restrict__ dirs, double kappa,
     cx<R>* __restrict__ mult) {
@@ -428,7 +431,7 @@ __global__ void __launch_bounds__(32 * NODAL_WARPS) m2m_kernel(
 }
 
 template <typename R, int L>
-__global__ void __launch_bounds__(32 * NODAL_WARPS) l2l_kernel(
+__global__ void __launch_bounds__(32 * NODAL_WARPS, DEFMM_NODAL_MINB) l2l_kernel(
     int64_t n, const int64_t* __restrict__ out_slot, const int8_t* __restrict__ octant,
     const int64_t* __restrict__ ptr, const int64_t* __restrict__ src_slot,
     const int32_t* __restrict__ src_dir, double son_beta, const double* __restrict__ dirs, double kappa,
@@ -860,31 +863,31 @@ __device__ __forceinline__ void f2l_row(const V* tw, V* X, V* Z1, V* out, int nt
                 out[row * L + c] = cscale(v, scale);
             }
         }
-        return;
-    }
-    for (int t = threadIdx.x; t < L * P * P; t += nt) {
-        const int a = t / (P * P), f12 = t % (P * P);
-        V v = cz<V>();
+    } else {
+        for (int t = threadIdx.x; t < L * P * P; t += nt) {
+            const int a = t / (P * P), f12 = t % (P * P);
+            V v = cz<V>();
 #pragma unroll
-        for (int f0 = 0; f0 < P; ++f0) v = cfma(X[f0 * P * P + f12], cconj(tw[f0 * L + a]), v);
-        Z1[t] = v;
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < L * L * P; t += nt) {
-        const int a = t / (L * P), b = (t / P) % L, f2 = t % P;
-        V v = cz<V>();
+            for (int f0 = 0; f0 < P; ++f0) v = cfma(X[f0 * P * P + f12], cconj(tw[f0 * L + a]), v);
+            Z1[t] = v;
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < L * L * P; t += nt) {
+            const int a = t / (L * P), b = (t / P) % L, f2 = t % P;
+            V v = cz<V>();
 #pragma unroll
-        for (int f1 = 0; f1 < P; ++f1) v = cfma(Z1[(a * P + f1) * P + f2], cconj(tw[f1 * L + b]), v);
-        X[t] = v;
-    }
-    __syncthreads();
-    const double scale = 1.0 / (P * sqrt((double)P));
-    for (int t = threadIdx.x; t < L3; t += nt) {
-        const int ab = t / L, c = t % L;
-        V v = cz<V>();
+            for (int f1 = 0; f1 < P; ++f1) v = cfma(Z1[(a * P + f1) * P + f2], cconj(tw[f1 * L + b]), v);
+            X[t] = v;
+        }
+        __syncthreads();
+        const double scale = 1.0 / (P * sqrt((double)P));
+        for (int t = threadIdx.x; t < L3; t += nt) {
+            const int ab = t / L, c = t % L;
+            V v = cz<V>();
 #pragma unroll
-        for (int f2 = 0; f2 < P; ++f2) v = cfma(X[ab * P + f2], cconj(tw[f2 * L + c]), v);
-        out[t] = cscale(v, scale);
+            for (int f2 = 0; f2 < P; ++f2) v = cfma(X[ab * P + f2], cconj(tw[f2 * L + c]), v);
+            out[t] = cscale(v, scale);
+        }
     }
 }
 
@@ -1010,9 +1013,15 @@ __device__ __forceinline__ int gent_sym(const GroupEnt<K>& g, int k) {
     }
 }
 
+template <typename R, int L>
+__host__ __device__ constexpr int group_min_blocks() {  // register cap DEFMM_PAIR_REGS, at most 32 CTAs/SM
+    return DEFMM_PAIR_REGS ? (65536 / (m2l_block<R, L>() * DEFMM_PAIR_REGS) < 32
+                                  ? 65536 / (m2l_block<R, L>() * DEFMM_PAIR_REGS)
+                                  : 32)
+                           : 1;
+}
 template <typename R, int L, int K>
-__global__ void __launch_bounds__(m2l_block<R, L>(),
-                                  DEFMM_PAIR_REGS ? 65536 / (m2l_block<R, L>() * DEFMM_PAIR_REGS) : 1)
+__global__ void __launch_bounds__(m2l_block<R, L>(), group_min_blocks<R, L>())
     m2l_group_kernel(int64_t ngroups, const int64_t* __restrict__ grp_slot, const int64_t* __restrict__ grp_ptr,
                      const int* __restrict__ ent, const cx<R>* __restrict__ hat, const cx<R>* __restrict__ symd,
                      cx<R>* __restrict__ local) {
@@ -1325,9 +1334,11 @@ __device__ __forceinline__ void qfma(float2 (&acc)[2], const float4& d, const fl
     acc[0] = cfma(make_float2(d.x, d.y), make_float2(s.x, s.y), acc[0]);
     acc[1] = cfma(make_float2(d.z, d.w), make_float2(s.z, s.w), acc[1]);
 }
+#if DEFMM_QUAD_C64_W == 1
 __device__ __forceinline__ void qfma(float2 (&acc)[1], const float2& d, const float2& s) {
     acc[0] = cfma(d, s, acc[0]);
 }
+#endif
 __device__ __forceinline__ void qfma(double2 (&acc)[1], const double2& d, const double2& s) {
     acc[0] = cfma(d, s, acc[0]);
 }
