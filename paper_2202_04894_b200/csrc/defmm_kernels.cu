@@ -992,13 +992,17 @@ struct GroupEnt<2> {
     int4 a;  // {s, t0, t1, 0}
 };
 template <>
+struct GroupEnt<3> {
+    int4 a;  // {s, t0, t1, t2}
+};
+template <>
 struct GroupEnt<4> {
     int4 a, b;  // {s, t0, t1, t2}, {t3, 0, 0, 0}
 };
 template <int K>
 __device__ __forceinline__ GroupEnt<K> load_gent(const int* ent, int64_t e) {
     GroupEnt<K> g;
-    g.a = __ldg(reinterpret_cast<const int4*>(ent) + (K == 2 ? e : 2 * e));
+    g.a = __ldg(reinterpret_cast<const int4*>(ent) + (K <= 3 ? e : 2 * e));
     if constexpr (K == 4) g.b = __ldg(reinterpret_cast<const int4*>(ent) + 2 * e + 1);
     return g;
 }
@@ -1008,20 +1012,23 @@ template <int K>
 __device__ __forceinline__ int gent_sym(const GroupEnt<K>& g, int k) {
     if constexpr (K == 2) {
         return k == 0 ? g.a.y : g.a.z;
+    } else if constexpr (K == 3) {
+        return k == 0 ? g.a.y : k == 1 ? g.a.z : g.a.w;
     } else {
         return k == 0 ? g.a.y : k == 1 ? g.a.z : k == 2 ? g.a.w : g.b.x;
     }
 }
 
-template <typename R, int L>
-__host__ __device__ constexpr int group_min_blocks() {  // register cap DEFMM_PAIR_REGS, at most 32 CTAs/SM
-    return DEFMM_PAIR_REGS ? (65536 / (m2l_block<R, L>() * DEFMM_PAIR_REGS) < 32
-                                  ? 65536 / (m2l_block<R, L>() * DEFMM_PAIR_REGS)
-                                  : 32)
-                           : 1;
+#ifndef DEFMM_TRIPLE_REGS
+#define DEFMM_TRIPLE_REGS 56
+#endif
+template <typename R, int L, int K>
+__host__ __device__ constexpr int group_min_blocks() {  // register cap per K, at most 32 CTAs/SM
+    constexpr int regs = K == 2 ? DEFMM_PAIR_REGS : K == 3 ? DEFMM_TRIPLE_REGS : DEFMM_PAIR_REGS;
+    return 65536 / (m2l_block<R, L>() * regs) < 32 ? 65536 / (m2l_block<R, L>() * regs) : 32;
 }
 template <typename R, int L, int K>
-__global__ void __launch_bounds__(m2l_block<R, L>(), group_min_blocks<R, L>())
+__global__ void __launch_bounds__(m2l_block<R, L>(), group_min_blocks<R, L, K>())
     m2l_group_kernel(int64_t ngroups, const int64_t* __restrict__ grp_slot, const int64_t* __restrict__ grp_ptr,
                      const int* __restrict__ ent, const cx<R>* __restrict__ hat, const cx<R>* __restrict__ symd,
                      cx<R>* __restrict__ local) {
@@ -1031,7 +1038,7 @@ __global__ void __launch_bounds__(m2l_block<R, L>(), group_min_blocks<R, L>())
     constexpr bool VEC = sizeof(R) == 4;
     constexpr int W = VEC ? 2 : 1;
     constexpr int PER = (SS / W + NT - 1) / NT;
-    constexpr int UNROLL = K == 2 ? 2 : 1;  // entries in flight per iteration
+    constexpr int UNROLL = K <= 3 ? 2 : 1;  // entries in flight per iteration
     using V = cx<R>;
     using VT = std::conditional_t<VEC, float4, double2>;
     extern __shared__ unsigned char smraw[];
@@ -1069,7 +1076,8 @@ __global__ void __launch_bounds__(m2l_block<R, L>(), group_min_blocks<R, L>())
             } else {  // no-op entry: every symbol absent
                 en[u] = load_gent<K>(ent, e);
                 en[u].a.y = en[u].a.z = -1;
-                if constexpr (K == 4) en[u].a.w = en[u].b.x = -1;
+                if constexpr (K >= 3) en[u].a.w = -1;
+                if constexpr (K == 4) en[u].b.x = -1;
             }
         }
 #pragma unroll
@@ -2605,7 +2613,7 @@ template <typename R>
 int launch_m2l_group(int32_t L, int32_t K, int64_t ngroups, const int64_t* grp_slot, const int64_t* grp_ptr,
                      const int32_t* ent, const void* hat, const void* symd, void* local, void* stream) {
     if (ngroups == 0) return 0;
-    if (!grid_ok(ngroups) || (K != 2 && K != 4)) return -1;
+    if (!grid_ok(ngroups) || K < 2 || K > 4) return -1;
     if (int rc0 = ensure_twiddles()) return rc0;
     cudaStream_t s = (cudaStream_t)stream;
     DEFMM_DISPATCH_L(L, {
@@ -2616,6 +2624,12 @@ int launch_m2l_group(int32_t L, int32_t K, int64_t ngroups, const int64_t* grp_s
             if (rc) return rc;
             carve(m2l_group_kernel<R, LL, 2>);
             m2l_group_kernel<R, LL, 2><<<(unsigned)ngroups, m2l_block<R, LL>(), bytes, s>>>(
+                ngroups, grp_slot, grp_ptr, ent, (const cx<R>*)hat, (const cx<R>*)symd, (cx<R>*)local);
+        } else if (K == 3) {
+            int rc = set_smem(m2l_group_kernel<R, LL, 3>, bytes);
+            if (rc) return rc;
+            carve(m2l_group_kernel<R, LL, 3>);
+            m2l_group_kernel<R, LL, 3><<<(unsigned)ngroups, m2l_block<R, LL>(), bytes, s>>>(
                 ngroups, grp_slot, grp_ptr, ent, (const cx<R>*)hat, (const cx<R>*)symd, (cx<R>*)local);
         } else {
             int rc = set_smem(m2l_group_kernel<R, LL, 4>, bytes);

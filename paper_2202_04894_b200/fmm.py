@@ -155,7 +155,7 @@ def m2l_groups(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent, K: int = 2
     (level, key, target parent), consecutive siblings packed K per CTA group;
     each group's events merged per source spectrum into {s, symbol of row k or
     -1 (k < K)} padded to 4 (K = 2) / 8 (K = 4) ints."""
-    S = 4 if K == 2 else 8
+    S = 4 if K <= 3 else 8
     if ids.size == 0:
         return {"n": 0, "K": K, "grp_slot": np.zeros(0, np.int64), "grp_ptr": np.zeros(1, np.int64),
                 "ent": np.zeros((0, S), np.int32)}
@@ -229,9 +229,9 @@ M2L_MODE_KINDS = {
     "rows": ("rows", "rows"), "blocked_all": ("blocked", "blocked"), "quad_all": ("quad", "quad"),
     "tiles": ("blocked", "tile"), "tiles_all": ("tile", "tile"), "slice_all": ("slice", "slice"),
     "pairs": ("blocked", "pair"), "pairs_all": ("pair", "pair"), "quartets": ("blocked", "quartet"),
-    "quartets_all": ("quartet", "quartet"),
+    "quartets_all": ("quartet", "quartet"), "triples_all": ("triple", "triple"),
 }
-M2L_KERNELS = ("rows", "blocked", "quad", "tile", "slice", "pair", "quartet")
+M2L_KERNELS = ("rows", "blocked", "quad", "tile", "slice", "pair", "triple", "quartet")
 # events per parent-pair block above which a level counts as dense (blocked kernel)
 BLOCKED_MIN_EVENTS_PER_BLOCK = 32.0
 # "auto": a complex64 sparse level runs the quad kernel when its quads are this
@@ -246,6 +246,14 @@ QUAD_MAX_ORDER = 4
 # (sibling rows merged per source: cfg2 M2L -9%, cfg3 -10%); small levels
 # (cfg1) keep the row kernel (profiles/r01_summary_v7.md)
 PAIR_MIN_ROWS = 2048
+# rows per sibling group by (precision, order), measured (r01_summary_v8.md):
+# triples win at L = 5 (cfg3 c64 M2L 9.65 -> 9.26 ms) and for complex128 at
+# L >= 5 (cfg2 L6 c128 27.7 -> 19.1 ms: the pair kernel spills there), pairs
+# elsewhere (cfg2 L4: pair 2.59 vs triple 2.68 ms)
+def sibling_kind(dtype: str, order: int) -> str:
+    if order == 5 or (dtype == "c128" and order >= 5):
+        return "triple"
+    return "pair"
 
 
 def block_levels(plan, tt):
@@ -299,7 +307,7 @@ def m2l_level_kinds(mode: str, dtype: str, levels, dense, fill=None, override=No
             if dtype == "c64" and order <= QUAD_MAX_ORDER and (fill or {}).get(lv, 0.0) >= QUAD_MIN_EVENTS_PER_QUAD:
                 kinds[lv] = "quad"
             elif (rows_per_level or {}).get(lv, 0) >= PAIR_MIN_ROWS:
-                kinds[lv] = "pair"
+                kinds[lv] = sibling_kind(dtype, order)
     over = dict(override or {})
     for tok in filter(None, env.split(",")):
         lv, k = tok.split(":")
@@ -444,7 +452,7 @@ class FmmPlan:
         self.qd_rows = _dev(h["qd_rows"].reshape(-1), i64, d)
         self.quads = _dev(h["quads"].reshape(-1), i32, d)
         self.sib_groups = []  # (K, n, slots, ptr, entries) of the pair / quartet kernels
-        for kind in ("pair", "quartet"):
+        for kind in ("pair", "triple", "quartet"):
             gr = h[kind]
             if gr["n"]:
                 self.sib_groups.append((gr["K"], int(gr["n"]), _dev(gr["grp_slot"], i64, d),
@@ -585,6 +593,8 @@ class FmmPlan:
         # sibling pairs (K7 v8)
         h["pair"] = m2l_groups(np.nonzero(pick("pair"))[0], rows, h["row_ptr"], h["ent"], p.l_cell, p.l_dir,
                                tt.level, tt.parent, 2)
+        h["triple"] = m2l_groups(np.nonzero(pick("triple"))[0], rows, h["row_ptr"], h["ent"], p.l_cell, p.l_dir,
+                                 tt.level, tt.parent, 3)
         h["quartet"] = m2l_groups(np.nonzero(pick("quartet"))[0], rows, h["row_ptr"], h["ent"], p.l_cell, p.l_dir,
                                   tt.level, tt.parent, 4)
         # grouped rows (blocked + quad)
@@ -959,6 +969,7 @@ class FmmPlan:
         out = []
         for n, name, k in ((self.rk_rows.shape[0], "m2l_rows_kernel", "rows"),
                            (sum(x[1] for x in self.sib_groups if x[0] == 2), "m2l_group_kernel<2>", "pair"),
+                           (sum(x[1] for x in self.sib_groups if x[0] == 3), "m2l_group_kernel<3>", "triple"),
                            (sum(x[1] for x in self.sib_groups if x[0] == 4), "m2l_group_kernel<4>", "quartet"),
                            (self.n_groups, "m2l_blocked_kernel", "blocked"),
                            (self.n_qgroups, "m2l_quad_kernel", "quad"), (self.n_tiles, "m2l_tile_kernel", "tile"),

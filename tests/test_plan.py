@@ -434,7 +434,7 @@ def test_m2l_level_policy(case):
     quads (>= QUAD_MIN_EVENTS_PER_QUAD events/quad) to the quad kernel and
     never complex128 ones; overrides (dict or env string) win; bad names raise."""
     from paper_2202_04894_b200.fmm import (PAIR_MIN_ROWS, QUAD_MIN_EVENTS_PER_QUAD, block_levels, dense_levels,
-                                           m2l_level_kinds, quad_fill)
+                                           m2l_level_kinds, quad_fill, sibling_kind)
 
     tr, _, p = _plan(load_case(case))
     levels = np.unique(p.m2l_level)
@@ -454,9 +454,14 @@ def test_m2l_level_policy(case):
         if lv in dense:
             assert k64[lv] == k128[lv] == "blocked"
         else:
-            assert k128[lv] == ("pair" if big else "rows")
+            assert k128[lv] == ("pair" if big else "rows")  # order 4
             quad = fill.get(lv, 0.0) >= QUAD_MIN_EVENTS_PER_QUAD
             assert k64[lv] == ("quad" if quad else "pair" if big else "rows")
+    assert sibling_kind("c64", 4) == "pair" and sibling_kind("c64", 5) == "triple"
+    assert sibling_kind("c64", 6) == "pair" and sibling_kind("c128", 6) == "triple"
+    k6 = m2l_level_kinds("auto", "c128", levels, dense, fill, rows_per_level=rpl, order=6)
+    assert all(k6[int(lv)] == ("triple" if rpl.get(int(lv), 0) >= PAIR_MIN_ROWS else "rows")
+               for lv in levels if int(lv) not in dense)
     assert set(m2l_level_kinds("auto", "c64", levels, dense, fill).values()) <= {"blocked", "rows", "quad"}
     assert "quad" not in m2l_level_kinds("auto", "c64", levels, dense, fill, rows_per_level=rpl, order=6).values()
     assert set(m2l_level_kinds("hybrid_rows", "c64", levels, dense).values()) <= {"blocked", "rows"}
@@ -469,7 +474,7 @@ def test_m2l_level_policy(case):
         m2l_level_kinds("nope", "c64", levels, dense)
 
 
-@pytest.mark.parametrize("K", [2, 4])
+@pytest.mark.parametrize("K", [2, 3, 4])
 @pytest.mark.parametrize("case", ["cubesurf4000", "volume3000", "c1_kd16"])
 def test_m2l_groups_reconstruct_every_row(case, K):
     """fmm.m2l_pairs (pair M2L lists): rows are paired only with a sibling of
