@@ -177,6 +177,16 @@ def _fma_peaks(dev):
     return res
 
 
+def _ncu_m2l(key):
+    """L1/L2 throughput of the dominant M2L kernel from its committed ncu
+    capture (profiles/r01_m2l_ncu.json): the physical bound behind frac > 1."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_m2l_ncu.json")) as fh:
+            return json.load(fh)[key]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def _ncu_pipe(key):
     """FP-pipe utilisation of the P2P kernel from the committed ncu capture
     (profiles/r01_p2p_pipes.json), or None."""
@@ -489,8 +499,10 @@ def run_b200(args):
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
                      "kernel_ms": st["m2l"],
+                     "ncu_dominant_kernel": _ncu_m2l(f"{args.workload}:{dtype}"),
                      "note": "algorithmic bytes = 2 spectra per M2L event + local write; frac > 1 = L2 reuse; "
-                             "traffic = ncu dram bytes of the M2L-stage launches of one matvec (profiles/r01_m2l_traffic.json)"},
+                             "traffic = ncu dram bytes of the M2L-stage launches of one matvec (profiles/r01_m2l_traffic.json); "
+                             "the kernel's physical bound is the L1/shared data path (ncu_dominant_kernel)"},
         "p2p_roofline": p2p_roof,
         "fma_peaks_tflops": fpk,
         "e2e": {"value": n / (e_step / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(qbytes),
