@@ -240,8 +240,11 @@ BLOCKED_MIN_EVENTS_PER_BLOCK = 32.0
 # (profiles/r01_summary_v5.md)
 QUAD_MIN_EVENTS_PER_QUAD = 12.0
 # ... and only up to this order: at L = 6 the pair kernel beats the quads on
-# the same cfg2 level (10.2 vs 11.1 ms, profiles/r01_summary_v7.md)
-QUAD_MAX_ORDER = 4
+# the same cfg2 level (10.2 vs 11.1 ms, profiles/r01_summary_v7.md).  Since
+# the pair kernel keeps three entries in flight it also wins cfg2's planar
+# level 6 at L = 4 (2.445 vs 2.48 ms, r01_summary_v8.md): QUAD_MAX_ORDER = 0
+# takes the quads out of "auto" (they stay selectable per level)
+QUAD_MAX_ORDER = 0
 # "auto": other sparse levels with at least this many rows run the pair kernel
 # (sibling rows merged per source: cfg2 M2L -9%, cfg3 -10%); small levels
 # (cfg1) keep the row kernel (profiles/r01_summary_v7.md)

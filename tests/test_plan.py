@@ -433,8 +433,8 @@ def test_m2l_level_policy(case):
     blocked, sparse -> rows; "auto" moves complex64 sparse levels with full
     quads (>= QUAD_MIN_EVENTS_PER_QUAD events/quad) to the quad kernel and
     never complex128 ones; overrides (dict or env string) win; bad names raise."""
-    from paper_2202_04894_b200.fmm import (PAIR_MIN_ROWS, QUAD_MIN_EVENTS_PER_QUAD, block_levels, dense_levels,
-                                           m2l_level_kinds, quad_fill, sibling_kind)
+    from paper_2202_04894_b200.fmm import (PAIR_MIN_ROWS, QUAD_MAX_ORDER, QUAD_MIN_EVENTS_PER_QUAD, block_levels,
+                                           dense_levels, m2l_level_kinds, quad_fill, sibling_kind)
 
     tr, _, p = _plan(load_case(case))
     levels = np.unique(p.m2l_level)
@@ -446,22 +446,24 @@ def test_m2l_level_policy(case):
     assert all(1.0 <= f <= 16.0 for f in fill.values())
     # row counts per level scaled up so that some levels cross PAIR_MIN_ROWS
     rpl = {int(lv): int(c) * (PAIR_MIN_ROWS // 2) for lv, c in zip(*np.unique(p.m2l_level, return_counts=True))}
-    k64 = m2l_level_kinds("auto", "c64", levels, dense, fill, rows_per_level=rpl)
-    k128 = m2l_level_kinds("auto", "c128", levels, dense, fill, rows_per_level=rpl)
+    # the quad rule at an order it is enabled for (QUAD_MAX_ORDER may switch it off in "auto")
+    k64 = m2l_level_kinds("auto", "c64", levels, dense, fill, rows_per_level=rpl, order=QUAD_MAX_ORDER)
+    k128 = m2l_level_kinds("auto", "c128", levels, dense, fill, rows_per_level=rpl, order=QUAD_MAX_ORDER)
     for lv in levels:
         lv = int(lv)
         big = rpl.get(lv, 0) >= PAIR_MIN_ROWS
         if lv in dense:
             assert k64[lv] == k128[lv] == "blocked"
         else:
-            assert k128[lv] == ("pair" if big else "rows")  # order 4
+            assert k128[lv] == ("pair" if big else "rows")
             quad = fill.get(lv, 0.0) >= QUAD_MIN_EVENTS_PER_QUAD
             assert k64[lv] == ("quad" if quad else "pair" if big else "rows")
     k6 = m2l_level_kinds("auto", "c128", levels, dense, fill, rows_per_level=rpl, order=6)
     assert all(k6[int(lv)] == (sibling_kind("c128", 6) if rpl.get(int(lv), 0) >= PAIR_MIN_ROWS else "rows")
                for lv in levels if int(lv) not in dense)
     assert set(m2l_level_kinds("auto", "c64", levels, dense, fill).values()) <= {"blocked", "rows", "quad"}
-    assert "quad" not in m2l_level_kinds("auto", "c64", levels, dense, fill, rows_per_level=rpl, order=6).values()
+    assert "quad" not in m2l_level_kinds("auto", "c64", levels, dense, fill, rows_per_level=rpl,
+                                         order=QUAD_MAX_ORDER + 1).values()
     assert set(m2l_level_kinds("hybrid_rows", "c64", levels, dense).values()) <= {"blocked", "rows"}
     lv0 = int(levels[0])
     assert m2l_level_kinds("auto", "c64", levels, dense, fill, {lv0: "tile"})[lv0] == "tile"
