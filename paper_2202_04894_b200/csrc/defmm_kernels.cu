@@ -1022,9 +1022,12 @@ __device__ __forceinline__ int gent_sym(const GroupEnt<K>& g, int k) {
 #ifndef DEFMM_TRIPLE_REGS
 #define DEFMM_TRIPLE_REGS 56
 #endif
+#ifndef DEFMM_QUARTET_REGS
+#define DEFMM_QUARTET_REGS 56
+#endif
 template <typename R, int L, int K>
 __host__ __device__ constexpr int group_min_blocks() {  // register cap per K, at most 32 CTAs/SM
-    constexpr int regs = K == 2 ? DEFMM_PAIR_REGS : K == 3 ? DEFMM_TRIPLE_REGS : DEFMM_PAIR_REGS;
+    constexpr int regs = K == 2 ? DEFMM_PAIR_REGS : K == 3 ? DEFMM_TRIPLE_REGS : DEFMM_QUARTET_REGS;
     return 65536 / (m2l_block<R, L>() * regs) < 32 ? 65536 / (m2l_block<R, L>() * regs) : 32;
 }
 template <typename R, int L, int K>
@@ -1041,7 +1044,10 @@ __global__ void __launch_bounds__(m2l_block<R, L>(), group_min_blocks<R, L, K>()
 #ifndef DEFMM_PAIR_UNROLL
 #define DEFMM_PAIR_UNROLL 3
 #endif
-    constexpr int UNROLL = K == 2 ? DEFMM_PAIR_UNROLL : K == 3 ? 2 : 1;  // entries in flight per iteration
+#ifndef DEFMM_QUARTET_UNROLL
+#define DEFMM_QUARTET_UNROLL 1
+#endif
+    constexpr int UNROLL = K == 2 ? DEFMM_PAIR_UNROLL : K == 3 ? 2 : DEFMM_QUARTET_UNROLL;  // entries in flight
     using V = cx<R>;
     using VT = std::conditional_t<VEC, float4, double2>;
     extern __shared__ unsigned char smraw[];

@@ -249,13 +249,13 @@ QUAD_MAX_ORDER = 0
 # (sibling rows merged per source: cfg2 M2L -9%, cfg3 -10%); small levels
 # (cfg1) keep the row kernel (profiles/r01_summary_v7.md)
 PAIR_MIN_ROWS = 2048
-# rows per sibling group, measured (r01_summary_v8.md): with three entries in
-# flight and a 56-register cap the pair kernel matches or beats triples at
-# every order and precision (cfg3 c64 9.36 vs 9.30 ms, c128 14.5 vs 15.3;
-# cfg2 L6 c128 19.24 vs 19.21; cfg2 L4 2.48 vs 2.68); triples and quartets
-# stay selectable per level
+# rows per sibling group, measured (r01_summary_v8.md): at L <= 4 quartets
+# (one entry in flight, 56-register cap) beat pairs (cfg2 M2L c64 2.445 ->
+# 2.377 ms, c128 4.71 -> 4.39); from L = 5 their larger spectra make them lose
+# (cfg3 9.35 -> 9.63, cfg2 L6 8.64 -> 11.7 ms) and the pair kernel (three
+# entries in flight, 56 registers) is best; triples never win
 def sibling_kind(dtype: str, order: int) -> str:
-    return "pair"
+    return "quartet" if order <= 4 else "pair"
 
 
 def block_levels(plan, tt):

@@ -455,9 +455,11 @@ def test_m2l_level_policy(case):
         if lv in dense:
             assert k64[lv] == k128[lv] == "blocked"
         else:
-            assert k128[lv] == ("pair" if big else "rows")
+            sib = sibling_kind("c64", QUAD_MAX_ORDER)
+            assert k128[lv] == (sib if big else "rows")
             quad = fill.get(lv, 0.0) >= QUAD_MIN_EVENTS_PER_QUAD
-            assert k64[lv] == ("quad" if quad else "pair" if big else "rows")
+            assert k64[lv] == ("quad" if quad else sib if big else "rows")
+    assert sibling_kind("c64", 4) == "quartet" and sibling_kind("c128", 6) == "pair"
     k6 = m2l_level_kinds("auto", "c128", levels, dense, fill, rows_per_level=rpl, order=6)
     assert all(k6[int(lv)] == (sibling_kind("c128", 6) if rpl.get(int(lv), 0) >= PAIR_MIN_ROWS else "rows")
                for lv in levels if int(lv) not in dense)
