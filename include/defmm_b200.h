@@ -170,6 +170,13 @@ int defmm_m2l_tiles(int64_t n_order, const int64_t* order, const int64_t* row_pt
  *   K = 2, 8 for K = 4) = {source spectrum, derived symbol for row k or -1
  *   (k < K), 0 padding}; local[slot] = F2L(sum) -- the row kernel's sums,
  *   merged per source.
+ *   m2l_group_tma: the same lists and sums (same per-row order); entries are
+ *   fed through a shared-memory ring by bulk copies (one producer warp, mbarrier
+ *   full/empty pairs) instead of per-thread global loads.
+ *   m2l_group_smq: the same lists and sums; the groups are dealt to nq SMs in
+ *   chunks of `chunk` consecutive groups, round robin, and each CTA claims the
+ *   next group of its own SM (qcnt: nq device int32 counters, zeroed by the
+ *   call on the stream), so co-resident CTAs share L1; nq = the SM count.
  *   K7 v6 tile variant (m2l_tile): one CTA (256 threads) per tile, walking
  *   the spectrum in slices of F = 16 (c64) / 8 (c128) entries; dynamic shared
  *   memory 2 u_max F complex + ids + e_max events (the u_max / e_max the
@@ -223,6 +230,15 @@ int defmm_m2l_tiles(int64_t n_order, const int64_t* order, const int64_t* row_pt
     int defmm_m2l_group_##SUFFIX(int32_t L, int32_t K, int64_t ngroups, const int64_t* grp_slot,  \
                                  const int64_t* grp_ptr, const int32_t* entries, const void* hat, \
                                  const void* sym_derived, void* local, void* stream);             \
+    int defmm_m2l_group_tma_##SUFFIX(int32_t L, int32_t K, int64_t ngroups,                       \
+                                     const int64_t* grp_slot, const int64_t* grp_ptr,             \
+                                     const int32_t* entries, const void* hat,                     \
+                                     const void* sym_derived, void* local, void* stream);         \
+    int defmm_m2l_group_smq_##SUFFIX(int32_t L, int32_t K, int64_t ngroups,                       \
+                                     const int64_t* grp_slot, const int64_t* grp_ptr,             \
+                                     const int32_t* entries, const void* hat,                     \
+                                     const void* sym_derived, void* local, int32_t nq,            \
+                                     int32_t chunk, int32_t* qcnt, void* stream);                 \
     int defmm_m2l_blocked_##SUFFIX(int32_t L, int64_t ngroups, const int64_t* grp_ptr,           \
                                    const int64_t* grp_rows, const int32_t* blk_src,             \
                                    const int32_t* blk_trans, const int64_t* blk_mask,           \
@@ -267,11 +283,11 @@ int defmm_m2l_tiles(int64_t n_order, const int64_t* order, const int64_t* row_pt
                            void* stream);
 
 /* expands to: defmm_p2m_c128 defmm_m2m_c128 defmm_m2f_c128 defmm_symbols_c128
- * defmm_expand_symbols_c128 defmm_m2l_rows_c128 defmm_m2l_group_c128 defmm_m2l_blocked_c128
+ * defmm_expand_symbols_c128 defmm_m2l_rows_c128 defmm_m2l_group_c128 defmm_m2l_group_tma_c128 defmm_m2l_group_smq_c128 defmm_m2l_blocked_c128
  * defmm_m2l_quad_c128 defmm_m2l_tile_c128 defmm_m2l_slice_c128 defmm_f2l_rows_c128 defmm_l2l_c128 defmm_l2p_c128 defmm_p2p_c128 */
 DEFMM_DECLARE_TYPED(c128)
 /* expands to: defmm_p2m_c64 defmm_m2m_c64 defmm_m2f_c64 defmm_symbols_c64
- * defmm_expand_symbols_c64 defmm_m2l_rows_c64 defmm_m2l_group_c64 defmm_m2l_blocked_c64
+ * defmm_expand_symbols_c64 defmm_m2l_rows_c64 defmm_m2l_group_c64 defmm_m2l_group_tma_c64 defmm_m2l_group_smq_c64 defmm_m2l_blocked_c64
  * defmm_m2l_quad_c64 defmm_m2l_tile_c64 defmm_m2l_slice_c64 defmm_f2l_rows_c64 defmm_l2l_c64 defmm_l2p_c64 defmm_p2p_c64 */
 DEFMM_DECLARE_TYPED(c64)
 

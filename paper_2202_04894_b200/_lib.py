@@ -50,6 +50,8 @@ for _t in ("c128", "c64"):
         f"defmm_m2l_quad_{_t}": [_i32, _i64] + [_vp] * 7,
         f"defmm_m2l_slice_{_t}": [_i32, _i64, _vp, _i64, _vp, _i32, _vp, _vp, _vp, _vp, _vp],
         f"defmm_m2l_group_{_t}": [_i32, _i32, _i64] + [_vp] * 7,
+        f"defmm_m2l_group_tma_{_t}": [_i32, _i32, _i64] + [_vp] * 7,
+        f"defmm_m2l_group_smq_{_t}": [_i32, _i32, _i64] + [_vp] * 6 + [_i32, _i32, _vp, _vp],
         f"defmm_m2l_tile_{_t}": [_i32, _i64] + [_vp] * 5 + [_i64, _i32, _i32, _vp, _vp, _vp, _vp],
         f"defmm_f2l_rows_{_t}": [_i32, _i64, _vp, _vp, _vp, _vp],
         f"defmm_l2l_{_t}": [_i32, _i64, _vp, _vp, _vp, _vp, _vp, _f64, _vp, _f64, _vp, _vp],

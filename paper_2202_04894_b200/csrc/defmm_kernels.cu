@@ -1030,11 +1030,39 @@ __host__ __device__ constexpr int group_min_blocks() {  // register cap per K, a
     constexpr int regs = K == 2 ? DEFMM_PAIR_REGS : K == 3 ? DEFMM_TRIPLE_REGS : DEFMM_QUARTET_REGS;
     return 65536 / (m2l_block<R, L>() * regs) < 32 ? 65536 / (m2l_block<R, L>() * regs) : 32;
 }
-template <typename R, int L, int K>
+// SMQ = true (K7 v10, SM-local claiming): the M2L is bound by the L2 -> SM
+// fabric (ncu v10: 30 GB of L2 -> L1 sectors in 2.39 ms = ~6400 B/clk, the
+// chip's LTS throughput cap), so only L1 hits take bytes off it.  The sorted
+// groups are dealt to the nq SMs in chunks of `chunk` consecutive groups,
+// round robin (window w: SM q owns groups w nq chunk + q chunk + [0, chunk)):
+// a CTA claims the next group of ITS SM's sequence (atomic counter
+// qcnt[smid % nq]) and steals from the following SMs' sequences once its own
+// is exhausted.  CTAs resident on one SM then work on neighbouring groups,
+// which share source spectra and (same translations) symbols in that SM's
+// L1, while all SMs stay inside one window of the list (one contiguous chunk
+// per SM spread the L2 working set over the whole list: DRAM reads 0.42 ->
+// 3.9 GB).  Every group is claimed exactly once (ngroups CTAs, counters only
+// grow); per-group arithmetic is unchanged.
+__device__ __forceinline__ int64_t claim_sm_group(int64_t ngroups, int nq, int chunk, int* qcnt) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;\n" : "=r"(smid));
+    const int q0 = (int)(smid % (uint32_t)nq);
+    const int64_t span = (int64_t)nq * chunk, full = ngroups / span, rem = ngroups - full * span;
+    for (int d = 0; d < nq; ++d) {
+        const int c = q0 + d < nq ? q0 + d : q0 + d - nq;
+        const int64_t tail = rem - (int64_t)c * chunk;
+        const int64_t n = full * chunk + (tail < 0 ? 0 : tail > chunk ? chunk : tail);
+        if (n == 0 || *((volatile int*)(qcnt + c)) >= n) continue;
+        const int i = atomicAdd(qcnt + c, 1);
+        if (i < n) return (i / chunk) * span + (int64_t)c * chunk + i % chunk;
+    }
+    return -1;  // unreachable: a free slot exists while this CTA holds none
+}
+template <typename R, int L, int K, bool SMQ = false>
 __global__ void __launch_bounds__(m2l_block<R, L>(), group_min_blocks<R, L, K>())
     m2l_group_kernel(int64_t ngroups, const int64_t* __restrict__ grp_slot, const int64_t* __restrict__ grp_ptr,
                      const int* __restrict__ ent, const cx<R>* __restrict__ hat, const cx<R>* __restrict__ symd,
-                     cx<R>* __restrict__ local) {
+                     cx<R>* __restrict__ local, int nq = 0, int chunk = 1, int* qcnt = nullptr) {
     constexpr int P = pad<L>(), L3 = cube<L>(), P3 = P * P * P;
     constexpr int SS = spec_stride<R, L>();
     constexpr int NT = m2l_block<R, L>();
@@ -1055,7 +1083,14 @@ __global__ void __launch_bounds__(m2l_block<R, L>(), group_min_blocks<R, L, K>()
     double2* X = tw + P * L;
     double2* Z1 = X + P3 + 1;
     double2* O = Z1 + L * P * P;
-    const int64_t g = blockIdx.x;
+    int64_t g = blockIdx.x;
+    if constexpr (SMQ) {
+        __shared__ int64_t claimed;
+        if (threadIdx.x == 0) claimed = claim_sm_group(ngroups, nq, chunk, qcnt);
+        __syncthreads();
+        g = claimed;
+        if (g < 0) return;
+    }
     make_twiddle_matrix<L, double2>(tw);
     const VT* hv = reinterpret_cast<const VT*>(hat);
     const VT* dv = reinterpret_cast<const VT*>(symd);
@@ -1121,6 +1156,172 @@ __global__ void __launch_bounds__(m2l_block<R, L>(), group_min_blocks<R, L, K>()
             for (int w = 0; w < W; ++w) {
                 const int j = jv * W + w;
                 if (jv < NV && j < P3) X[forder<L>(j)] = to_d(acc[u][m][w]);
+            }
+        }
+        __syncthreads();
+        f2l_row<L, double2>(tw, X, Z1, O, NT);
+        __syncthreads();
+        cx<R>* out = local + slot * L3;
+        for (int t = threadIdx.x; t < L3; t += NT) out[t] = from_d<cx<R>>(O[t]);
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K7 v9: sibling-group M2L fed by bulk copies (TMA engine) into a shared-memory
+// ring.  The LDG path of m2l_group_kernel is bound by L1 LSU data-pipe
+// wavefronts (ncu v9: 91%) although its data-bank traffic is only 21-28%: L2
+// misses return sectors piecewise, ~2.5 sectors per wavefront instead of 4.
+// Here one producer lane copies each entry's source spectrum and its rows'
+// symbols (cp.async.bulk, whole spectra, complete_tx on the stage's "full"
+// mbarrier) and the consumer warps read them with full-width LDS.128 (4
+// sectors per wavefront), releasing the stage through its "empty" mbarrier.
+// Same entries, same per-row accumulation order, same F2L as m2l_group_kernel.
+__device__ __forceinline__ uint32_t sm32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(sm32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sm32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(sm32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}\n" ::"r"(sm32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     sm32(dst)),
+                 "l"(src), "r"(bytes), "r"(sm32(b))
+                 : "memory");
+}
+template <typename R, int L, int K>
+__host__ __device__ constexpr int gtma_stages() {  // ring depth: ~64 KB of stages, 2..4
+    constexpr int sb = spec_stride<R, L>() * (int)sizeof(cx<R>) * (K + 1);
+    return 65536 / sb > 4 ? 4 : 65536 / sb < 2 ? 2 : 65536 / sb;
+}
+template <typename R, int L, int K>
+__host__ __device__ constexpr size_t gtma_smem_bytes() {
+    constexpr int P = pad<L>();
+    return (size_t)gtma_stages<R, L, K>() * (K + 1) * spec_stride<R, L>() * sizeof(cx<R>) +
+           2 * gtma_stages<R, L, K>() * sizeof(uint64_t) +
+           sizeof(double2) * (P * L + P * P * P + 1 + L * P * P + L * L * L);
+}
+template <typename R, int L, int K>
+__global__ void __launch_bounds__(m2l_block<R, L>() + 32, 2)
+    m2l_group_tma_kernel(int64_t ngroups, const int64_t* __restrict__ grp_slot, const int64_t* __restrict__ grp_ptr,
+                         const int* __restrict__ ent, const cx<R>* __restrict__ hat,
+                         const cx<R>* __restrict__ symd, cx<R>* __restrict__ local) {
+    constexpr int P = pad<L>(), L3 = cube<L>(), P3 = P * P * P;
+    constexpr int SS = spec_stride<R, L>();
+    constexpr int NC = m2l_block<R, L>();  // consumer threads (multiple of 32)
+    constexpr int NT = NC + 32;            // + one producer warp
+    constexpr bool VEC = sizeof(R) == 4;
+    constexpr int W = VEC ? 2 : 1;
+    constexpr int NV = SS / W;  // 16-B vectors per spectrum
+    constexpr int PER = (NV + NC - 1) / NC;
+    constexpr int ST = gtma_stages<R, L, K>();
+    constexpr uint32_t SB = SS * sizeof(cx<R>);  // bytes per spectrum (multiple of 16)
+    using V = cx<R>;
+    using VT = std::conditional_t<VEC, float4, double2>;
+    static_assert(sizeof(VT) == 16 && SB % 16 == 0 && NC % 32 == 0, "bulk-copy layout");
+    extern __shared__ __align__(128) unsigned char smraw[];
+    VT* ring = reinterpret_cast<VT*>(smraw);  // [ST][K + 1][NV]: source, then row k's symbol
+    uint64_t* full = reinterpret_cast<uint64_t*>(smraw + (size_t)ST * (K + 1) * SB);
+    uint64_t* empty = full + ST;
+    double2* tw = reinterpret_cast<double2*>(empty + ST);
+    double2* X = tw + P * L;
+    double2* Z1 = X + P3 + 1;
+    double2* O = Z1 + L * P * P;
+    const int64_t g = blockIdx.x;
+    const int64_t e0 = grp_ptr[g], e1 = grp_ptr[g + 1];
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NC / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    make_twiddle_matrix<L, double2>(tw);
+    __syncthreads();
+    V acc[K][PER][W];
+#pragma unroll
+    for (int u = 0; u < K; ++u)
+#pragma unroll
+        for (int m = 0; m < PER; ++m)
+#pragma unroll
+            for (int w = 0; w < W; ++w) acc[u][m][w] = cz<V>();
+    if (threadIdx.x >= NC) {
+        if (threadIdx.x == NC) {  // producer lane
+            const VT* hv = reinterpret_cast<const VT*>(hat);
+            const VT* dv = reinterpret_cast<const VT*>(symd);
+            for (int64_t e = e0; e < e1; ++e) {
+                const int i = (int)(e - e0), s = i % ST;
+                if (i >= ST) mbar_wait(&empty[s], (uint32_t)((i / ST - 1) & 1));
+                const GroupEnt<K> en = load_gent<K>(ent, e);
+                uint32_t nb = 1;
+#pragma unroll
+                for (int k = 0; k < K; ++k) nb += gent_sym<K>(en, k) >= 0;
+                mbar_expect_tx(&full[s], nb * SB);
+                VT* st = ring + (size_t)s * (K + 1) * NV;
+                bulk_g2s(st, hv + (int64_t)gent_src<K>(en) * NV, SB, &full[s]);
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const int t = gent_sym<K>(en, k);
+                    if (t >= 0) bulk_g2s(st + (1 + k) * NV, dv + (int64_t)t * NV, SB, &full[s]);
+                }
+            }
+        }
+    } else {
+        for (int64_t e = e0; e < e1; ++e) {
+            const int i = (int)(e - e0), s = i % ST;
+            const GroupEnt<K> en = load_gent<K>(ent, e);
+            mbar_wait(&full[s], (uint32_t)((i / ST) & 1));
+            const VT* st = ring + (size_t)s * (K + 1) * NV;
+#pragma unroll
+            for (int m = 0; m < PER; ++m) {
+                const int jv = threadIdx.x + m * NC;
+                if (jv < NV) {
+                    const VT x = st[jv];
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        if (gent_sym<K>(en, k) >= 0) {
+                            const VT d = st[(1 + k) * NV + jv];
+                            if constexpr (VEC) {
+                                acc[k][m][0] = cfma(make_float2(d.x, d.y), make_float2(x.x, x.y), acc[k][m][0]);
+                                acc[k][m][W - 1] =
+                                    cfma(make_float2(d.z, d.w), make_float2(x.z, x.w), acc[k][m][W - 1]);
+                            } else {
+                                acc[k][m][0] = cfma(d, x, acc[k][m][0]);
+                            }
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+        const int64_t slot = grp_slot[K * g + u];
+        if (slot < 0) break;  // uniform; rows fill the group from the front
+        if (threadIdx.x < NC) {
+#pragma unroll
+            for (int m = 0; m < PER; ++m) {
+                const int jv = threadIdx.x + m * NC;
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    const int j = jv * W + w;
+                    if (jv < NV && j < P3) X[forder<L>(j)] = to_d(acc[u][m][w]);
+                }
             }
         }
         __syncthreads();
@@ -2620,35 +2821,59 @@ int launch_m2l_rows(int32_t L, int64_t nrows, const int64_t* row_slot, const int
 
 template <typename R>
 int launch_m2l_group(int32_t L, int32_t K, int64_t ngroups, const int64_t* grp_slot, const int64_t* grp_ptr,
-                     const int32_t* ent, const void* hat, const void* symd, void* local, void* stream) {
+                     const int32_t* ent, const void* hat, const void* symd, void* local, void* stream,
+                     int32_t nq = 0, int32_t chunk = 1, int32_t* qcnt = nullptr) {
+    if (ngroups == 0) return 0;
+    if (!grid_ok(ngroups) || K < 2 || K > 4 || nq < 0 || (nq > 0 && (qcnt == nullptr || chunk < 1))) return -1;
+    if (int rc0 = ensure_twiddles()) return rc0;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (nq > 0) {
+        if (int rc = report(cudaMemsetAsync(qcnt, 0, sizeof(int32_t) * nq, s), "m2l_group qcnt")) return rc;
+    }
+#define DEFMM_GROUP_LAUNCH(KK, SQ)                                                                          \
+    {                                                                                                       \
+        int rc = set_smem(m2l_group_kernel<R, LL, KK, SQ>, bytes);                                          \
+        if (rc) return rc;                                                                                  \
+        carve(m2l_group_kernel<R, LL, KK, SQ>);                                                             \
+        m2l_group_kernel<R, LL, KK, SQ><<<(unsigned)ngroups, m2l_block<R, LL>(), bytes, s>>>(               \
+            ngroups, grp_slot, grp_ptr, ent, (const cx<R>*)hat, (const cx<R>*)symd, (cx<R>*)local, nq, chunk, qcnt); \
+    }
+    DEFMM_DISPATCH_L(L, {
+        constexpr int P = 2 * LL - 1;
+        const size_t bytes = sizeof(double2) * (P * LL + P * P * P + 1 + LL * P * P + LL * LL * LL);
+        if (nq > 0) {
+            if (K == 2) DEFMM_GROUP_LAUNCH(2, true) else if (K == 3) DEFMM_GROUP_LAUNCH(3, true) else DEFMM_GROUP_LAUNCH(4, true)
+        } else {
+            if (K == 2) DEFMM_GROUP_LAUNCH(2, false) else if (K == 3) DEFMM_GROUP_LAUNCH(3, false) else DEFMM_GROUP_LAUNCH(4, false)
+        }
+    });
+#undef DEFMM_GROUP_LAUNCH
+    return report(cudaGetLastError(), "m2l_group");
+}
+
+template <typename R>
+int launch_m2l_group_tma(int32_t L, int32_t K, int64_t ngroups, const int64_t* grp_slot, const int64_t* grp_ptr,
+                         const int32_t* ent, const void* hat, const void* symd, void* local, void* stream) {
     if (ngroups == 0) return 0;
     if (!grid_ok(ngroups) || K < 2 || K > 4) return -1;
     if (int rc0 = ensure_twiddles()) return rc0;
     cudaStream_t s = (cudaStream_t)stream;
+#define DEFMM_GTMA_LAUNCH(KK)                                                                              \
+    {                                                                                                      \
+        constexpr size_t bytes = gtma_smem_bytes<R, LL, KK>();                                             \
+        if (bytes > 227 * 1024) /* ring does not fit: the LDG group kernel */                              \
+            return launch_m2l_group<R>(L, K, ngroups, grp_slot, grp_ptr, ent, hat, symd, local, stream);   \
+        int rc = set_smem(m2l_group_tma_kernel<R, LL, KK>, bytes);                                         \
+        if (rc) return rc;                                                                                 \
+        carve(m2l_group_tma_kernel<R, LL, KK>);                                                            \
+        m2l_group_tma_kernel<R, LL, KK><<<(unsigned)ngroups, m2l_block<R, LL>() + 32, bytes, s>>>(         \
+            ngroups, grp_slot, grp_ptr, ent, (const cx<R>*)hat, (const cx<R>*)symd, (cx<R>*)local);        \
+    }
     DEFMM_DISPATCH_L(L, {
-        constexpr int P = 2 * LL - 1;
-        const size_t bytes = sizeof(double2) * (P * LL + P * P * P + 1 + LL * P * P + LL * LL * LL);
-        if (K == 2) {
-            int rc = set_smem(m2l_group_kernel<R, LL, 2>, bytes);
-            if (rc) return rc;
-            carve(m2l_group_kernel<R, LL, 2>);
-            m2l_group_kernel<R, LL, 2><<<(unsigned)ngroups, m2l_block<R, LL>(), bytes, s>>>(
-                ngroups, grp_slot, grp_ptr, ent, (const cx<R>*)hat, (const cx<R>*)symd, (cx<R>*)local);
-        } else if (K == 3) {
-            int rc = set_smem(m2l_group_kernel<R, LL, 3>, bytes);
-            if (rc) return rc;
-            carve(m2l_group_kernel<R, LL, 3>);
-            m2l_group_kernel<R, LL, 3><<<(unsigned)ngroups, m2l_block<R, LL>(), bytes, s>>>(
-                ngroups, grp_slot, grp_ptr, ent, (const cx<R>*)hat, (const cx<R>*)symd, (cx<R>*)local);
-        } else {
-            int rc = set_smem(m2l_group_kernel<R, LL, 4>, bytes);
-            if (rc) return rc;
-            carve(m2l_group_kernel<R, LL, 4>);
-            m2l_group_kernel<R, LL, 4><<<(unsigned)ngroups, m2l_block<R, LL>(), bytes, s>>>(
-                ngroups, grp_slot, grp_ptr, ent, (const cx<R>*)hat, (const cx<R>*)symd, (cx<R>*)local);
-        }
+        if (K == 2) DEFMM_GTMA_LAUNCH(2) else if (K == 3) DEFMM_GTMA_LAUNCH(3) else DEFMM_GTMA_LAUNCH(4)
     });
-    return report(cudaGetLastError(), "m2l_group");
+#undef DEFMM_GTMA_LAUNCH
+    return report(cudaGetLastError(), "m2l_group_tma");
 }
 
 template <typename R>
@@ -2847,6 +3072,19 @@ const char* defmm_last_error(void) { return g_last_error; }
                                  const int64_t* grp_ptr, const int32_t* entries, const void* hat,                 \
                                  const void* sym_derived, void* local, void* stream) {                            \
         return launch_m2l_group<R>(L, K, ngroups, grp_slot, grp_ptr, entries, hat, sym_derived, local, stream);   \
+    }                                                                                                               \
+    int defmm_m2l_group_smq_##SUFFIX(int32_t L, int32_t K, int64_t ngroups, const int64_t* grp_slot,              \
+                                     const int64_t* grp_ptr, const int32_t* entries, const void* hat,             \
+                                     const void* sym_derived, void* local, int32_t nq, int32_t chunk,             \
+                                     int32_t* qcnt, void* stream) {                                               \
+        return launch_m2l_group<R>(L, K, ngroups, grp_slot, grp_ptr, entries, hat, sym_derived, local, stream, nq, \
+                                   chunk, qcnt);                                                                  \
+    }                                                                                                               \
+    int defmm_m2l_group_tma_##SUFFIX(int32_t L, int32_t K, int64_t ngroups, const int64_t* grp_slot,              \
+                                     const int64_t* grp_ptr, const int32_t* entries, const void* hat,             \
+                                     const void* sym_derived, void* local, void* stream) {                        \
+        return launch_m2l_group_tma<R>(L, K, ngroups, grp_slot, grp_ptr, entries, hat, sym_derived, local,        \
+                                       stream);                                                                   \
     }                                                                                                               \
     int defmm_m2l_blocked_##SUFFIX(int32_t L, int64_t ngroups, const int64_t* grp_ptr, const int64_t* grp_rows,     \
                                    const int32_t* blk_src, const int32_t* blk_trans, const int64_t* blk_mask,     \

@@ -518,6 +518,16 @@ class FmmPlan:
         # stage timers); "full": P2P spans the upward pass and the M2L on a
         # persistent grid of p2p_grid CTAs (SM room left for the far field)
         self.p2p_overlap = "upward"
+        # sibling-group M2L fed by bulk copies into a shared-memory ring (K7 v9)
+        # instead of per-thread global loads; DEFMM_GROUP_TMA=0/1 overrides
+        self.group_tma = os.environ.get("DEFMM_GROUP_TMA", "0") == "1"
+        # sibling groups claimed per SM from contiguous chunks (K7 v10): CTAs
+        # sharing an SM work on neighbouring groups -> L1 reuse of spectra and
+        # symbols; DEFMM_GROUP_SMQ=0/1 overrides
+        self.group_smq = os.environ.get("DEFMM_GROUP_SMQ", "0") == "1"
+        self.smq_chunk = int(os.environ.get("DEFMM_GROUP_SMQ_CHUNK", "8"))
+        self.n_sm = torch.cuda.get_device_properties(d).multi_processor_count
+        self.qcnt = torch.zeros(self.n_sm, dtype=torch.int32, device=d)
         self.p2p_grid = 0
         # c64 near-field coordinates: hi/lo float pairs where the order's
         # accuracy bar needs them (defmm_b200.h, K1)
@@ -885,8 +895,12 @@ class FmmPlan:
             _lib.call(self._op("m2l_rows"), L, self.rk_rows.shape[0], self.rk_rows, self.rk_ptr, self.rk_ent,
                       self.hat, self.sym_derived, self.local, sh)
             for K, ng, gslot, gptr, gent in self.sib_groups:
-                _lib.call(self._op("m2l_group"), L, K, ng, gslot, gptr, gent, self.hat, self.sym_derived,
-                          self.local, sh)
+                if self.group_smq:
+                    _lib.call(self._op("m2l_group_smq"), L, K, ng, gslot, gptr, gent, self.hat, self.sym_derived,
+                              self.local, self.n_sm, self.smq_chunk, self.qcnt, sh)
+                else:
+                    _lib.call(self._op("m2l_group_tma" if self.group_tma else "m2l_group"), L, K, ng, gslot, gptr,
+                              gent, self.hat, self.sym_derived, self.local, sh)
             _lib.call(self._op("m2l_blocked"), L, self.n_groups, self.grp_ptr, self.grp_rows, self.blk_src,
                       self.blk_trans, self.blk_mask, self.blk_kind, self.hat, self.sym_derived, self.lhat, sh)
             _lib.call(self._op("m2l_quad"), L, self.n_qgroups, self.qd_ptr, self.qd_rows, self.quads, self.hat,
@@ -969,10 +983,11 @@ class FmmPlan:
             return sorted(l for l, x in kinds.items() if x == k)
 
         out = []
+        gk = "m2l_group_tma_kernel" if self.group_tma and not self.group_smq else "m2l_group_kernel"
         for n, name, k in ((self.rk_rows.shape[0], "m2l_rows_kernel", "rows"),
-                           (sum(x[1] for x in self.sib_groups if x[0] == 2), "m2l_group_kernel<2>", "pair"),
-                           (sum(x[1] for x in self.sib_groups if x[0] == 3), "m2l_group_kernel<3>", "triple"),
-                           (sum(x[1] for x in self.sib_groups if x[0] == 4), "m2l_group_kernel<4>", "quartet"),
+                           (sum(x[1] for x in self.sib_groups if x[0] == 2), f"{gk}<2>", "pair"),
+                           (sum(x[1] for x in self.sib_groups if x[0] == 3), f"{gk}<3>", "triple"),
+                           (sum(x[1] for x in self.sib_groups if x[0] == 4), f"{gk}<4>", "quartet"),
                            (self.n_groups, "m2l_blocked_kernel", "blocked"),
                            (self.n_qgroups, "m2l_quad_kernel", "quad"), (self.n_tiles, "m2l_tile_kernel", "tile"),
                            (self.n_slice_batch, "m2l_slice_kernel", "slice"), (self.bk_rows.shape[0], "f2l_rows_kernel", None)):

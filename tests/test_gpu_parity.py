@@ -161,6 +161,33 @@ def test_m2l_canonical_gather_and_derived_symbols_agree(case):
     assert _rel(b, g["pot"]) <= FP64_TOL
 
 
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("case", ["cubesurf4000", "volume3000"])
+def test_group_m2l_bulk_copy_ring_and_sm_claiming_match_global_loads(case, dtype):
+    """The bulk-copy fed sibling-group M2L (m2l_group_tma) sums the same
+    entries in the same per-row order as the global-load group kernel, for
+    pairs, triples and quartets; both match the reference's potentials."""
+    from paper_2202_04894_b200 import FmmConfig, FmmPlan
+
+    g = load_case(case)
+    cfg = FmmConfig(**{**g["config"], "dtype": dtype})
+    base = FmmPlan(g["points"], None, cfg, charges=g["charges"])
+    for mode in ("pairs_all", "triples_all", "quartets_all"):
+        p2 = FmmPlan(g["points"], None, cfg, charges=g["charges"], reuse=base, m2l=mode)
+        p2.group_tma = False
+        a = p2.apply().cpu().numpy().astype(np.complex128)
+        p2.group_tma = True
+        assert any("m2l_group_tma_kernel" in k for k in p2.m2l_kernels())
+        b = p2.apply().cpu().numpy().astype(np.complex128)
+        assert _rel(b, a) <= (1e-13 if dtype == "c128" else 1e-6)
+        assert _rel(b, g["pot"]) <= (FP64_TOL if dtype == "c128" else C64_TOL)
+        # SM-local group claiming: same groups, same arithmetic -> bitwise equal
+        p2.group_tma, p2.group_smq = False, True
+        for _ in range(2):
+            c = p2.apply().cpu().numpy().astype(np.complex128)
+            assert np.array_equal(c, a)
+
+
 def test_linearity_in_the_charges():
     from paper_2202_04894_b200 import FmmConfig, FmmPlan
 
