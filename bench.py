@@ -493,8 +493,13 @@ def run_b200(args):
         "config": dict(_workload_desc(w, n, dtype), l2_flush="256 MiB memset between timed iterations",
                        parallelism=(f"morton-sharded x{world} (NCCL {args.exchange} of multipoles)"
                                     if world > 1 else "single")),
-        "stages_ms": {"upward_with_concurrent_p2p": st["upward"], "m2l": st["m2l"], "p2p": st["p2p"],
-                      "downward": st["downward"]},
+        # stage timers (eager run); the P2P runs on the side stream beside the
+        # stage named by p2p_overlap (fmm.p2p_overlap_policy)
+        "stages_ms": {("upward_with_concurrent_p2p" if plan.p2p_overlap in ("upward", "full") else "upward"): st["upward"],
+                      ("m2l_with_concurrent_p2p" if plan.p2p_overlap in ("m2l", "full") else "m2l"): st["m2l"],
+                      "p2p": st["p2p"], "downward": st["downward"]},
+        "p2p_overlap": plan.p2p_overlap,
+        "far_priority": bool(plan.far_priority),
         "roofline": {"bound": "hbm", "kernel": kname,
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
@@ -502,7 +507,7 @@ def run_b200(args):
                      "ncu_dominant_kernel": _ncu_m2l(f"{args.workload}:{dtype}"),
                      "note": "algorithmic bytes = 2 spectra per M2L event + local write; frac > 1 = L2 reuse; "
                              "traffic = ncu dram bytes of the M2L-stage launches of one matvec (profiles/r01_m2l_traffic.json); "
-                             "the kernel's physical bound is the L1/shared data path (ncu_dominant_kernel)"},
+                             "the kernel's physical bound is the L2->SM fabric: ncu_dominant_kernel.l2_to_l1_bytes_per_clk against the chip's LTS throughput cap (lts_cap_bytes_per_clk)"},
         "p2p_roofline": p2p_roof,
         "fma_peaks_tflops": fpk,
         "e2e": {"value": n / (e_step / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(qbytes),

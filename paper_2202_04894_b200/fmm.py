@@ -292,6 +292,19 @@ def quad_fill(plan, tt, levels) -> dict:
     return out
 
 
+def p2p_overlap_policy(level_kinds: dict) -> tuple:
+    """(p2p_overlap, far_priority) for a plan's M2L level kinds, measured
+    (profiles/r01_summary_v9.md): when every M2L level runs the quartet
+    kernel (L <= 4 sparse data: cfg2 c64 / c128), the M2L is bound by the
+    L2 -> SM fabric and co-runs well with the FP/XU-bound P2P under a
+    high-priority far-field stream (cfg2 c64 3.38 -> 3.28 ms, c128 6.73 ->
+    6.68); elsewhere (pairs, rows, blocked levels: cfg3, cfg5, cfg2 L6) the
+    P2P beside the upward pass is 0.6-2% faster."""
+    if level_kinds and all(k == "quartet" for k in level_kinds.values()):
+        return "m2l", True
+    return "upward", False
+
+
 def m2l_level_kinds(mode: str, dtype: str, levels, dense, fill=None, override=None, env: str = "",
                     rows_per_level=None, order: int = 4) -> dict:
     """level -> M2L kernel: the mode's (dense, sparse) choice; in "auto" a
@@ -512,12 +525,13 @@ class FmmPlan:
         lo, hi = torch.cuda.Stream.priority_range()  # (lowest, highest) priority numbers
         self.side_stream = torch.cuda.Stream(device=d, priority=lo)
         self.far_stream = torch.cuda.Stream(device=d, priority=hi)
-        self.far_priority = False
         self.m2l_variant = "hybrid"
         # "upward": P2P concurrent with P2M/M2M/M2F, joined before the M2L (clean
-        # stage timers); "full": P2P spans the upward pass and the M2L on a
-        # persistent grid of p2p_grid CTAs (SM room left for the far field)
-        self.p2p_overlap = "upward"
+        # M2L stage timer); "m2l": P2P launched after the upward pass on the
+        # low-priority side stream, concurrent with the M2L; "full": P2P spans
+        # the upward pass and the M2L (optionally on a persistent grid of
+        # p2p_grid CTAs).  far_priority: far field on the high-priority stream.
+        self.p2p_overlap, self.far_priority = p2p_overlap_policy(getattr(self, "level_kinds", {}))
         # sibling-group M2L fed by bulk copies into a shared-memory ring (K7 v9)
         # instead of per-thread global loads; DEFMM_GROUP_TMA=0/1 overrides
         self.group_tma = os.environ.get("DEFMM_GROUP_TMA", "0") == "1"

@@ -506,3 +506,15 @@ def test_m2l_groups_reconstruct_every_row(case, K):
             got = sorted(zip(e[e[:, col] >= 0, 0].tolist(), e[e[:, col] >= 0, col].tolist()))
             want = sorted(zip(ent[ptr[r]:ptr[r + 1], 0].tolist(), ent[ptr[r]:ptr[r + 1], 1].tolist()))
             assert got == want
+
+
+def test_p2p_overlap_policy():
+    """P2P beside the M2L (high-priority far field) only when every M2L level
+    runs the quartet kernel (measured, profiles/r01_summary_v9.md)."""
+    from paper_2202_04894_b200.fmm import p2p_overlap_policy
+
+    assert p2p_overlap_policy({4: "quartet", 5: "quartet", 6: "quartet", 7: "quartet"}) == ("m2l", True)
+    assert p2p_overlap_policy({4: "rows", 5: "pair"}) == ("upward", False)
+    assert p2p_overlap_policy({3: "pair", 4: "blocked"}) == ("upward", False)
+    assert p2p_overlap_policy({4: "quartet", 5: "blocked"}) == ("upward", False)
+    assert p2p_overlap_policy({}) == ("upward", False)
