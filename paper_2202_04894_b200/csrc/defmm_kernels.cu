@@ -1082,7 +1082,7 @@ __global__ void __launch_bounds__(m2l_block<R, L>(), group_min_blocks<R, L, K>()
     double2* tw = reinterpret_cast<double2*>(smraw);
     double2* X = tw + P * L;
     double2* Z1 = X + P3 + 1;
-    double2* O = Z1 + L * P * P;
+    double2* O = Z1;  // Z1 is dead after the second axis: 6 CTAs fit a 64 KB carveout
     int64_t g = blockIdx.x;
     if constexpr (SMQ) {
         __shared__ int64_t claimed;
@@ -2835,12 +2835,28 @@ int launch_m2l_group(int32_t L, int32_t K, int64_t ngroups, const int64_t* grp_s
         int rc = set_smem(m2l_group_kernel<R, LL, KK, SQ>, bytes);                                          \
         if (rc) return rc;                                                                                  \
         carve(m2l_group_kernel<R, LL, KK, SQ>);                                                             \
+        if (group_carve >= 0)                                                                               \
+            cudaFuncSetAttribute((const void*)m2l_group_kernel<R, LL, KK, SQ>,                              \
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, group_carve);               \
         m2l_group_kernel<R, LL, KK, SQ><<<(unsigned)ngroups, m2l_block<R, LL>(), bytes, s>>>(               \
             ngroups, grp_slot, grp_ptr, ent, (const cx<R>*)hat, (const cx<R>*)symd, (cx<R>*)local, nq, chunk, qcnt); \
     }
+    // DEFMM_GROUP_SMEM=<bytes>: pad the dynamic shared memory of each CTA (caps
+    // the group kernel's CTAs per SM, leaving SM room for the concurrent P2P)
+    // DEFMM_GROUP_CARVE=<percent>: preferred shared-memory carveout of the group
+    // kernel (a smaller carveout leaves more of the 256 KB to L1)
+    static const int group_carve = [] {
+        const char* e = getenv("DEFMM_GROUP_CARVE");
+        return e ? atoi(e) : -1;
+    }();
+    static const size_t smem_pad = [] {
+        const char* e = getenv("DEFMM_GROUP_SMEM");
+        return e ? (size_t)atol(e) : (size_t)0;
+    }();
     DEFMM_DISPATCH_L(L, {
         constexpr int P = 2 * LL - 1;
-        const size_t bytes = sizeof(double2) * (P * LL + P * P * P + 1 + LL * P * P + LL * LL * LL);
+        size_t bytes = sizeof(double2) * (P * LL + P * P * P + 1 + LL * P * P);  // O aliases Z1
+        if (smem_pad > bytes) bytes = smem_pad;
         if (nq > 0) {
             if (K == 2) DEFMM_GROUP_LAUNCH(2, true) else if (K == 3) DEFMM_GROUP_LAUNCH(3, true) else DEFMM_GROUP_LAUNCH(4, true)
         } else {
