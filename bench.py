@@ -50,7 +50,7 @@ def _args():
     ap.add_argument("--no-secondary", action="store_true", help="skip the other-precision run of the same lists")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of the CUDA graph")
     ap.add_argument("--dtype", default=None, choices=[None, "c128", "c64"], help="override the workload dtype")
-    ap.add_argument("--p2p-overlap", default=None, choices=[None, "upward", "m2l", "full"])
+    ap.add_argument("--p2p-overlap", default=None, choices=[None, "upward", "m2m", "m2l", "full"])
     ap.add_argument("--p2p-grid", type=int, default=None, help="persistent P2P grid (CTAs; 0 = one per item)")
     ap.add_argument("--far-priority", type=int, default=None, help="far field on a high-priority stream (1/0)")
     ap.add_argument("--exchange", default="halo", choices=["halo", "allreduce"],
@@ -495,8 +495,8 @@ def run_b200(args):
                                     if world > 1 else "single")),
         # stage timers (eager run); the P2P runs on the side stream beside the
         # stage named by p2p_overlap (fmm.p2p_overlap_policy)
-        "stages_ms": {("upward_with_concurrent_p2p" if plan.p2p_overlap in ("upward", "full") else "upward"): st["upward"],
-                      ("m2l_with_concurrent_p2p" if plan.p2p_overlap in ("m2l", "full") else "m2l"): st["m2l"],
+        "stages_ms": {("upward_with_concurrent_p2p" if plan.p2p_overlap in ("upward", "m2m", "full") else "upward"): st["upward"],
+                      ("m2l_with_concurrent_p2p" if plan.p2p_overlap in ("m2m", "m2l", "full") else "m2l"): st["m2l"],
                       "p2p": st["p2p"], "downward": st["downward"]},
         "p2p_overlap": plan.p2p_overlap,
         "far_priority": bool(plan.far_priority),

@@ -883,6 +883,8 @@ class FmmPlan:
         _lib.call(self._op("p2m"), L, self.p2m_slot.shape[0], self.p2m_cell, self.p2m_dir, self.p2m_slot,
                   sg["start"], sg["stop"], sg["alpha"], sg["level"], sg["beta"], self.dirs, *self.s_xyz, self.q,
                   kappa, self.mult, sh)
+        if self.p2p_overlap == "m2m":  # P2P queued behind the P2M (far field keeps priority)
+            self._near_field(stage_events)
         for son_beta, slots, mdir, son_slot, n in self.m2m:
             _lib.call(self._op("m2m"), L, n, slots, mdir, son_slot, son_beta, self.dirs, kappa, self.mult, sh)
 
