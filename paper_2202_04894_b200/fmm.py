@@ -803,7 +803,7 @@ class FmmPlan:
         """Load charges (caller order) into the sorted device buffer."""
         q = torch.as_tensor(np.asarray(charges, dtype=complex)) if not torch.is_tensor(charges) else charges
         q = q.to(device=self.device, dtype=self.cdtype)
-        self.q.copy_(q[self.s_perm])
+        torch.index_select(q, 0, self.s_perm, out=self.q)  # one gather into the sorted buffer
 
     def set_charges_sorted(self, q_sorted):
         self.q.copy_(q_sorted)
@@ -812,7 +812,12 @@ class FmmPlan:
         """One matvec with the charges currently loaded; returns potentials in
         the caller's target order (device tensor; when sharded only this
         rank's targets are non-zero).  ``stage_events`` (list) receives
-        (name, start_event, end_event) for the stage timers."""
+        (name, start_event, end_event) for the stage timers.  After
+        ``capture_graph()`` a plain ``apply()`` replays the captured graph."""
+        if (out is None and stage_events is None and getattr(self, "graph", None) is not None
+                and not getattr(self, "_capturing", False)):
+            self.graph.replay()
+            return self.out
         if self.far_priority and self.shard is None:
             # far field on a HIGH-priority stream, P2P on the low-priority side
             # stream: the block scheduler then dispatches the latency-bound
@@ -971,16 +976,21 @@ class FmmPlan:
         if self.shard is not None:
             raise ValueError("CUDA-graph replay is for single-GPU plans")
         torch.cuda.synchronize(self.device)
-        s = torch.cuda.Stream(device=self.device)
-        s.wait_stream(torch.cuda.current_stream(self.device))
-        with torch.cuda.stream(s):
-            self.apply()  # warm-up on the capture stream
-        torch.cuda.current_stream(self.device).wait_stream(s)
-        torch.cuda.synchronize(self.device)
-        self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
-            self.apply()
-        torch.cuda.synchronize(self.device)
+        self._capturing = True
+        try:
+            s = torch.cuda.Stream(device=self.device)
+            s.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(s):
+                self.apply()  # warm-up on the capture stream
+            torch.cuda.current_stream(self.device).wait_stream(s)
+            torch.cuda.synchronize(self.device)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.apply()
+            torch.cuda.synchronize(self.device)
+        finally:
+            self._capturing = False
+        self.graph = g
         return self.graph
 
     def replay(self):

@@ -354,3 +354,11 @@ def test_cuda_graph_replay_matches_eager():
     plan.set_charges(2 * g["charges"])  # replay picks up new charges
     c = plan.replay().clone()
     assert _rel(c.cpu().numpy(), 2 * a.cpu().numpy()) <= 1e-14
+    # after capture, the public apply() replays the graph (same buffers, same sums)
+    d = plan.apply().clone()
+    assert torch.equal(c, d)
+    plan.set_charges(g["charges"])
+    assert torch.equal(plan.apply(), a)
+    # stage timers (or an explicit out=) take the eager path
+    e = plan.apply(stage_events=[]).clone()
+    assert torch.equal(e, a)
