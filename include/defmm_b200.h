@@ -263,6 +263,8 @@ int defmm_m2l_tiles(int64_t n_order, const int64_t* order, const int64_t* row_pt
                            const int64_t* ptr, const int64_t* src_slot, const int32_t* src_dir, \
                            double son_beta, const double* dirs, double kappa, void* local,      \
                            void* stream);                                                       \
+    int defmm_add_near_##SUFFIX(int64_t n, const int64_t* perm, const void* near, void* out,     \
+                                void* stream);                                                  \
     int defmm_l2p_##SUFFIX(int32_t L, int64_t n, const int32_t* leaf_cell,                       \
                            const int64_t* slot_lo, const int64_t* slot_hi,                      \
                            const int32_t* slot_dir, const int64_t* cell_start,                  \
@@ -284,11 +286,11 @@ int defmm_m2l_tiles(int64_t n_order, const int64_t* order, const int64_t* row_pt
 
 /* expands to: defmm_p2m_c128 defmm_m2m_c128 defmm_m2f_c128 defmm_symbols_c128
  * defmm_expand_symbols_c128 defmm_m2l_rows_c128 defmm_m2l_group_c128 defmm_m2l_group_tma_c128 defmm_m2l_group_smq_c128 defmm_m2l_blocked_c128
- * defmm_m2l_quad_c128 defmm_m2l_tile_c128 defmm_m2l_slice_c128 defmm_f2l_rows_c128 defmm_l2l_c128 defmm_l2p_c128 defmm_p2p_c128 */
+ * defmm_m2l_quad_c128 defmm_m2l_tile_c128 defmm_m2l_slice_c128 defmm_f2l_rows_c128 defmm_l2l_c128 defmm_add_near_c128 defmm_l2p_c128 defmm_p2p_c128 */
 DEFMM_DECLARE_TYPED(c128)
 /* expands to: defmm_p2m_c64 defmm_m2m_c64 defmm_m2f_c64 defmm_symbols_c64
  * defmm_expand_symbols_c64 defmm_m2l_rows_c64 defmm_m2l_group_c64 defmm_m2l_group_tma_c64 defmm_m2l_group_smq_c64 defmm_m2l_blocked_c64
- * defmm_m2l_quad_c64 defmm_m2l_tile_c64 defmm_m2l_slice_c64 defmm_f2l_rows_c64 defmm_l2l_c64 defmm_l2p_c64 defmm_p2p_c64 */
+ * defmm_m2l_quad_c64 defmm_m2l_tile_c64 defmm_m2l_slice_c64 defmm_f2l_rows_c64 defmm_l2l_c64 defmm_add_near_c64 defmm_l2p_c64 defmm_p2p_c64 */
 DEFMM_DECLARE_TYPED(c64)
 
 /* Spectral layout of order L (HOST call, no device needed): every spectrum is

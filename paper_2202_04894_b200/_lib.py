@@ -55,6 +55,7 @@ for _t in ("c128", "c64"):
         f"defmm_m2l_tile_{_t}": [_i32, _i64] + [_vp] * 5 + [_i64, _i32, _i32, _vp, _vp, _vp, _vp],
         f"defmm_f2l_rows_{_t}": [_i32, _i64, _vp, _vp, _vp, _vp],
         f"defmm_l2l_{_t}": [_i32, _i64, _vp, _vp, _vp, _vp, _vp, _f64, _vp, _f64, _vp, _vp],
+        f"defmm_add_near_{_t}": [_i64, _vp, _vp, _vp, _vp],
         f"defmm_l2p_{_t}": [_i32, _i64] + [_vp] * 13 + [_f64, _vp, _vp, _vp, _vp, _vp],
         f"defmm_p2p_{_t}": [_i64] + [_vp] * 16 + [_f64, _f64, _vp, _vp, _i64, _vp, _vp, _vp, _i32, _i32, _vp],
     })

@@ -2976,6 +2976,25 @@ int launch_f2l_rows(int32_t L, int64_t nrows, const int64_t* row_slot, const voi
     return report(cudaGetLastError(), "f2l_rows");
 }
 
+// out[perm[p]] += near[p]: the near field added after an L2P that ran with a
+// zero near field (lets the L2P overlap the tail of a concurrent P2P)
+template <typename R>
+__global__ void __launch_bounds__(256) add_near_kernel(int64_t n, const int64_t* __restrict__ perm,
+                                                       const cx<R>* __restrict__ near, cx<R>* __restrict__ out) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n) {
+        const int64_t o = perm[p];
+        out[o] = cadd(out[o], near[p]);
+    }
+}
+template <typename R>
+int launch_add_near(int64_t n, const int64_t* perm, const void* near, void* out, void* stream) {
+    if (n == 0) return 0;
+    if (n < 0) return -1;
+    add_near_kernel<R><<<blocks_of(n, 256), 256, 0, (cudaStream_t)stream>>>(n, perm, (const cx<R>*)near, (cx<R>*)out);
+    return report(cudaGetLastError(), "add_near");
+}
+
 template <typename R>
 int launch_l2p(int32_t L, int64_t n, const int32_t* leaf_cell, const int64_t* slot_lo, const int64_t* slot_hi,
                const int32_t* slot_dir, const int64_t* cell_start, const int64_t* cell_stop,
@@ -3135,6 +3154,9 @@ const char* defmm_last_error(void) { return g_last_error; }
                            const double* dirs, double kappa, void* local, void* stream) {                          \
         return launch_l2l<R>(L, n, out_slot, octant, ptr, src_slot, src_dir, son_beta, dirs, kappa, local,         \
                              stream);                                                                              \
+    }                                                                                                               \
+    int defmm_add_near_##SUFFIX(int64_t n, const int64_t* perm, const void* near, void* out, void* stream) {       \
+        return launch_add_near<R>(n, perm, near, out, stream);                                                     \
     }                                                                                                               \
     int defmm_l2p_##SUFFIX(int32_t L, int64_t n, const int32_t* leaf_cell, const int64_t* slot_lo,                  \
                            const int64_t* slot_hi, const int32_t* slot_dir, const int64_t* cell_start,             \

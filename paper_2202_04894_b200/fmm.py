@@ -519,6 +519,11 @@ class FmmPlan:
         self.local = torch.empty((max(p.n_local, 1), self.L3), dtype=cd, device=d)
         self.lhat = torch.empty((max(int(self.bk_rows.shape[0]), 1), self.SS), dtype=cd, device=d)
         self.near = torch.empty(self.n_tgt, dtype=cd, device=d)
+        # late near field: with the P2P still running beside the M2L, the L2P
+        # starts from a zero near field and add_near folds the P2P in after
+        # the join (DEFMM_LATE_NEAR=1; measured slower on cfg2: 3.304 vs 3.282 ms)
+        self.late_near = os.environ.get("DEFMM_LATE_NEAR", "0") == "1"
+        self.zero_near = torch.zeros(self.n_tgt, dtype=cd, device=d)
         self.p2p_partial = torch.empty(max(self._partial_size, 1), dtype=cd, device=d)
         self.q = torch.zeros(self.n_src, dtype=cd, device=d)
         self.out = torch.empty(self.n_tgt, dtype=cd, device=d)
@@ -957,12 +962,17 @@ class FmmPlan:
         for son_beta, outs, octant, ptr, src, sdir, n in self.l2l:
             _lib.call(self._op("l2l"), L, n, outs, octant, ptr, src, sdir, son_beta, self.dirs, kappa,
                       self.local, sh)
-        stream.wait_stream(self.side_stream)
+        late = self.late_near and self.shard is None and self.p2p_overlap != "upward"
+        if not late:
+            stream.wait_stream(self.side_stream)
         if self.shard is not None:
             out.zero_()  # this rank writes only its own targets
         _lib.call(self._op("l2p"), L, self.n_leaves, self.leaf_cell, self.leaf_lo, self.leaf_hi, self.slot_dir,
                   tg["start"], tg["stop"], tg["alpha"], tg["level"], tg["beta"], self.dirs, *self.t_xyz, kappa,
-                  self.local, self.near, self.t_perm, out, sh)
+                  self.local, self.zero_near if late else self.near, self.t_perm, out, sh)
+        if late:  # P2P joined after the L2P: out[perm] += near
+            stream.wait_stream(self.side_stream)
+            _lib.call(self._op("add_near"), self.n_tgt, self.t_perm, self.near, out, sh)
         if stage_events is not None:
             e = ev()
             e.record(stream)
@@ -1030,7 +1040,8 @@ class FmmPlan:
                                            self.n_slice_batch, self.bk_rows.shape[0]))
         else:
             m2l = 1
-        return 4 + (1 if self.n_split else 0) + len(self.m2m) + len(self.l2l) + m2l
+        late = self.late_near and self.shard is None and self.p2p_overlap != "upward"
+        return 4 + (1 if self.n_split else 0) + len(self.m2m) + len(self.l2l) + m2l + int(late)
 
     def events(self):
         """InteractionEvent list (traversal.py:80-85) with Cell views."""
