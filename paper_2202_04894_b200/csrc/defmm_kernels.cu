@@ -1231,7 +1231,7 @@ __global__ void __launch_bounds__(m2l_block<R, L>() + 32, 2)
     using V = cx<R>;
     using VT = std::conditional_t<VEC, float4, double2>;
     static_assert(sizeof(VT) == 16 && SB % 16 == 0 && NC % 32 == 0, "bulk-copy layout");
-    extern __shared__ __align__(128) unsigned char smraw[];
+    extern __shared__ __align__(16) unsigned char smraw[];  // bulk copies need 16-B alignment
     VT* ring = reinterpret_cast<VT*>(smraw);  // [ST][K + 1][NV]: source, then row k's symbol
     uint64_t* full = reinterpret_cast<uint64_t*>(smraw + (size_t)ST * (K + 1) * SB);
     uint64_t* empty = full + ST;
