@@ -93,31 +93,15 @@ void defmm_dtt_free(defmm_dtt* d);
  * selects double.  out: one element, written only to keep the chains live. */
 int defmm_fma_peak(int32_t fp64, int64_t iters, void* out, void* stream);
 
-/* ---- host: M2L row tiles for the shared-memory tile kernel (K7 v6) --------
- * The rows order[0..n_order) (row r = events [row_ptr[r], row_ptr[r+1]) of
- * ent = {source spectrum, derived symbol} int32 pairs; the same lists the
- * reference's dtt produces, traversal.py:320-348) are cut greedily into tiles
- * of consecutive rows whose operand UNION (distinct spectra + symbols) has at
- * most u_max (<= 65535) entries, at most k_max rows and at most e_max events.  Outputs (caller
- * allocates upper bounds: n_order+1 tiles/rows, 2*events ops, events ev):
- *   tile t = tiled rows [tile_ptr[t], tile_ptr[t+1]) of tile_rows (row ids),
- *            operands ops[op_ptr[t] .. op_ptr[t+1]) (v >= 0: spectrum v,
- *            v < 0: derived symbol -1-v), local index = position in the tile;
- *   tiled row k = events ev[ev_ptr[k] .. ev_ptr[k+1]) packed
- *            local spectrum | local symbol << 16, in the row's event order.
- * counts = {tiles, tiled rows, ops, events, untiled rows (own union > u_max or
- * own events > e_max)}.
- * Returns 0, or -1 for invalid u_max / k_max. */
-int defmm_m2l_tiles(int64_t n_order, const int64_t* order, const int64_t* row_ptr, const int32_t* ent,
-                    int64_t n_hat, int64_t n_trans, int32_t u_max, int32_t k_max, int32_t e_max,
-                    int64_t* tile_ptr,
-                    int64_t* tile_rows, int64_t* op_ptr, int32_t* ops, int64_t* ev_ptr, uint32_t* ev,
-                    int64_t* counts);
-
 /* ---- device operators ------------------------------------------------------
  * Every operator exists as *_c128 (complex arrays are double2 = interleaved
- * FP64 re/im, exactly the reference's complex128) and *_c64 (float2; phases,
- * coordinate differences and the M2L/L2P/P2P accumulations stay FP64).
+ * FP64 re/im, exactly the reference's complex128; all arithmetic FP64) and
+ * *_c64 (float2 storage).  What the c64 operators compute in: cell-relative
+ * coordinates (x - alpha)/beta and target-relative P2P differences are formed
+ * in FP64 and rounded once (hi/lo float pairs in the P2P at L >= 6); the
+ * P2M/M2M/L2L tensor sums, the M2F, the Hadamard M2L products and per-row
+ * sums, and the P2P pair terms and per-target sums are FP32; the F2L inverse
+ * transform, the L2P sum and the near + far combine are FP64.
  * Shared geometry arrays: cell_alpha[ncell*3] lower corners, cell_level[ncell],
  * level_beta[depth+1] side lengths, cell_start/stop particle ranges (sorted
  * order), dirs[ndir*3] unit directions (global ids; -1 = low frequency),
@@ -149,40 +133,12 @@ int defmm_m2l_tiles(int64_t n_order, const int64_t* order, const int64_t* row_pt
  *   general block, 2p+v for a PLANAR block whose pairs all have a_p = b_p = v
  *   (surface data: 4x4 in-plane pairs, no predicated-off pair).  lhat[row] = sum D (*) hat  (stride
  *   defmm_spectrum_stride);  then K8 f2l_rows: local[row_slot[r]] = F2L(lhat[r]).
- *   K7 v5 quad variant (m2l_quad): the same groups, each block split along
- *   one axis p into quads (target layer V, source layer W) of <= 4 x 4 pairs;
- *   quads[16q .. 16q+15] = {src[4] spectrum of in-plane source child ib (or
- *   -1), trans[9] derived symbol of in-plane offset e = (du+1)*3 + (dw+1) (or
- *   -1), mask16 (bit 4 ia + ib = event), code 4p + 2V + W, 0}; in-plane child
- *   ia/ib -> octant: its 2 bits go to the other two axes in increasing order,
- *   axis p gets V (target) / W (source).  grp_ptr spans each group's quads.
- *   K7 v4 slice variant (m2l_slice): grid = nbatch row batches x spectral slices
- *   (defmm_spectral_layout).  batch[4k..4k+3] = {row0, row1, first canonical
- *   symbol of the batch's level, that level's canonical count}; rows r in
- *   [row0, row1) are lhat rows whose events are sorted by symbol group
- *   (G = 192 symbols for c64, 96 for c128): group g's events are
- *   entries[seg[(r - row_base)(ngs+1) + g] .. seg[... + g + 1]), each {spectrum,
- *   (canonical index within the group << 6) | rotation id}.  lhat[r] = sum over
- *   events of rot(sym_canon) (*) hat -- the same sum as the row kernel.
- *   K7 v8 sibling-group variant (m2l_group, K = 2 or 4 rows): CTA g = rows
+ *   K7 v8 sibling-group variant (m2l_group, K = 2, 3 or 4 rows): CTA g = rows
  *   grp_slot[K g + k] (local slots; trailing -1 when the group is short);
  *   entry e in [grp_ptr[g], grp_ptr[g+1]) = entries[S e .. S e + K] (S = 4 for
  *   K = 2, 8 for K = 4) = {source spectrum, derived symbol for row k or -1
  *   (k < K), 0 padding}; local[slot] = F2L(sum) -- the row kernel's sums,
  *   merged per source.
- *   m2l_group_tma: the same lists and sums (same per-row order); entries are
- *   fed through a shared-memory ring by bulk copies (one producer warp, mbarrier
- *   full/empty pairs) instead of per-thread global loads.
- *   m2l_group_smq: the same lists and sums; the groups are dealt to nq SMs in
- *   chunks of `chunk` consecutive groups, round robin, and each CTA claims the
- *   next group of its own SM (qcnt: nq device int32 counters, zeroed by the
- *   call on the stream), so co-resident CTAs share L1; nq = the SM count.
- *   K7 v6 tile variant (m2l_tile): one CTA (256 threads) per tile, walking
- *   the spectrum in slices of F = 16 (c64) / 8 (c128) entries; dynamic shared
- *   memory 2 u_max F complex + ids + e_max events (the u_max / e_max the
- *   tiles were built with).  Tiles, operands and packed events as produced by
- *   defmm_m2l_tiles; lhat[lhat_base + k] = sum over tiled row k's events of
- *   sym_derived[t] (*) hat[s] -- the same sum as the row kernel.
  * K5 L2L -- traversal.py:355-391 in gather form.
  *   for i < n: local[out_slot[i]] += sum_{e in [ptr[i], ptr[i+1])}
  *   (C'0 (x) C'1 (x) C'2) local[src_slot[e]], C' the transposed/conjugate-
@@ -230,41 +186,17 @@ int defmm_m2l_tiles(int64_t n_order, const int64_t* order, const int64_t* row_pt
     int defmm_m2l_group_##SUFFIX(int32_t L, int32_t K, int64_t ngroups, const int64_t* grp_slot,  \
                                  const int64_t* grp_ptr, const int32_t* entries, const void* hat, \
                                  const void* sym_derived, void* local, void* stream);             \
-    int defmm_m2l_group_tma_##SUFFIX(int32_t L, int32_t K, int64_t ngroups,                       \
-                                     const int64_t* grp_slot, const int64_t* grp_ptr,             \
-                                     const int32_t* entries, const void* hat,                     \
-                                     const void* sym_derived, void* local, void* stream);         \
-    int defmm_m2l_group_smq_##SUFFIX(int32_t L, int32_t K, int64_t ngroups,                       \
-                                     const int64_t* grp_slot, const int64_t* grp_ptr,             \
-                                     const int32_t* entries, const void* hat,                     \
-                                     const void* sym_derived, void* local, int32_t nq,            \
-                                     int32_t chunk, int32_t* qcnt, void* stream);                 \
     int defmm_m2l_blocked_##SUFFIX(int32_t L, int64_t ngroups, const int64_t* grp_ptr,           \
                                    const int64_t* grp_rows, const int32_t* blk_src,             \
                                    const int32_t* blk_trans, const int64_t* blk_mask,           \
                                    const int8_t* blk_kind, const void* hat,                     \
                                    const void* sym_derived, void* lhat, void* stream);          \
-    int defmm_m2l_quad_##SUFFIX(int32_t L, int64_t ngroups, const int64_t* grp_ptr,              \
-                                const int64_t* grp_rows, const int32_t* quads,                  \
-                                const void* hat, const void* sym_derived, void* lhat,           \
-                                void* stream);                                                  \
-    int defmm_m2l_slice_##SUFFIX(int32_t L, int64_t nbatch, const int32_t* batch,                \
-                                 int64_t row_base, const int64_t* seg, int32_t ngs,             \
-                                 const int32_t* entries, const void* hat,                       \
-                                 const void* sym_canon, void* lhat, void* stream);              \
-    int defmm_m2l_tile_##SUFFIX(int32_t L, int64_t ntiles, const int64_t* tile_ptr,               \
-                                const int64_t* op_ptr, const int32_t* ops, const int64_t* ev_ptr,  \
-                                const uint32_t* ev, int64_t lhat_base, int32_t u_max,              \
-                                int32_t e_max, const void* hat, const void* sym_derived,           \
-                                void* lhat, void* stream);                                         \
     int defmm_f2l_rows_##SUFFIX(int32_t L, int64_t nrows, const int64_t* row_slot,               \
                                 const void* lhat, void* local, void* stream);                   \
     int defmm_l2l_##SUFFIX(int32_t L, int64_t n, const int64_t* out_slot, const int8_t* octant,  \
                            const int64_t* ptr, const int64_t* src_slot, const int32_t* src_dir, \
                            double son_beta, const double* dirs, double kappa, void* local,      \
                            void* stream);                                                       \
-    int defmm_add_near_##SUFFIX(int64_t n, const int64_t* perm, const void* near, void* out,     \
-                                void* stream);                                                  \
     int defmm_l2p_##SUFFIX(int32_t L, int64_t n, const int32_t* leaf_cell,                       \
                            const int64_t* slot_lo, const int64_t* slot_hi,                      \
                            const int32_t* slot_dir, const int64_t* cell_start,                  \
@@ -285,21 +217,19 @@ int defmm_m2l_tiles(int64_t n_order, const int64_t* order, const int64_t* row_pt
                            void* stream);
 
 /* expands to: defmm_p2m_c128 defmm_m2m_c128 defmm_m2f_c128 defmm_symbols_c128
- * defmm_expand_symbols_c128 defmm_m2l_rows_c128 defmm_m2l_group_c128 defmm_m2l_group_tma_c128 defmm_m2l_group_smq_c128 defmm_m2l_blocked_c128
- * defmm_m2l_quad_c128 defmm_m2l_tile_c128 defmm_m2l_slice_c128 defmm_f2l_rows_c128 defmm_l2l_c128 defmm_add_near_c128 defmm_l2p_c128 defmm_p2p_c128 */
+ * defmm_expand_symbols_c128 defmm_m2l_rows_c128 defmm_m2l_group_c128 defmm_m2l_blocked_c128
+ * defmm_f2l_rows_c128 defmm_l2l_c128 defmm_l2p_c128 defmm_p2p_c128 */
 DEFMM_DECLARE_TYPED(c128)
 /* expands to: defmm_p2m_c64 defmm_m2m_c64 defmm_m2f_c64 defmm_symbols_c64
- * defmm_expand_symbols_c64 defmm_m2l_rows_c64 defmm_m2l_group_c64 defmm_m2l_group_tma_c64 defmm_m2l_group_smq_c64 defmm_m2l_blocked_c64
- * defmm_m2l_quad_c64 defmm_m2l_tile_c64 defmm_m2l_slice_c64 defmm_f2l_rows_c64 defmm_l2l_c64 defmm_add_near_c64 defmm_l2p_c64 defmm_p2p_c64 */
+ * defmm_expand_symbols_c64 defmm_m2l_rows_c64 defmm_m2l_group_c64 defmm_m2l_blocked_c64
+ * defmm_f2l_rows_c64 defmm_l2l_c64 defmm_l2p_c64 defmm_p2p_c64 */
 DEFMM_DECLARE_TYPED(c64)
 
 /* Spectral layout of order L (HOST call, no device needed): every spectrum is
  * stored in orbit order, forder[pos] = natural frequency f0 P^2 + f1 P + f2 at
  * storage position pos < P^3; slices [slice_start[k], slice_start[k+1]),
- * k < *nslices, are unions of cube-group orbits of <= 64 positions. */
+ * k < *nslices, are unions of cube-group orbits of <= 128 positions. */
 int defmm_spectral_layout(int32_t L, int32_t* forder, int32_t* slice_start, int32_t* nslices);
-/* canonical symbols per shared-memory group G of the slice M2L (c64 != 0: complex64) */
-int defmm_slice_group(int32_t c64);
 
 /* K7 reference variant (c128): canonical symbols gathered through the closed-
  * form rotation inside the loop (e_sym canonical id, e_rid rotation id). */

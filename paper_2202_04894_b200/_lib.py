@@ -30,12 +30,10 @@ _SIGS = {
     "defmm_dtt_source_hats": [_vp] * 6 + [_i64, _vp, _vp, _vp],
     "defmm_dtt_free": [_vp],
     "defmm_fma_peak": [_i32, _i64, _vp, _vp],
-    "defmm_m2l_tiles": [_i64, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _i32] + [_vp] * 7,
     "defmm_m2l_canon_c128": [_i32, _i64] + [_vp] * 9,
     "defmm_direct_workspace_bytes": [_i64],
     "defmm_spectrum_stride": [_i32, _i32],
     "defmm_spectral_layout": [_i32, _vp, _vp, _vp],
-    "defmm_slice_group": [_i32],
     "defmm_direct_c128": [_i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _f64, _f64, _vp, _vp, _vp],
 }
 for _t in ("c128", "c64"):
@@ -47,15 +45,9 @@ for _t in ("c128", "c64"):
         f"defmm_expand_symbols_{_t}": [_i32, _i64, _vp, _vp, _vp, _vp, _vp],
         f"defmm_m2l_rows_{_t}": [_i32, _i64] + [_vp] * 7,
         f"defmm_m2l_blocked_{_t}": [_i32, _i64] + [_vp] * 10,
-        f"defmm_m2l_quad_{_t}": [_i32, _i64] + [_vp] * 7,
-        f"defmm_m2l_slice_{_t}": [_i32, _i64, _vp, _i64, _vp, _i32, _vp, _vp, _vp, _vp, _vp],
         f"defmm_m2l_group_{_t}": [_i32, _i32, _i64] + [_vp] * 7,
-        f"defmm_m2l_group_tma_{_t}": [_i32, _i32, _i64] + [_vp] * 7,
-        f"defmm_m2l_group_smq_{_t}": [_i32, _i32, _i64] + [_vp] * 6 + [_i32, _i32, _vp, _vp],
-        f"defmm_m2l_tile_{_t}": [_i32, _i64] + [_vp] * 5 + [_i64, _i32, _i32, _vp, _vp, _vp, _vp],
         f"defmm_f2l_rows_{_t}": [_i32, _i64, _vp, _vp, _vp, _vp],
         f"defmm_l2l_{_t}": [_i32, _i64, _vp, _vp, _vp, _vp, _vp, _f64, _vp, _f64, _vp, _vp],
-        f"defmm_add_near_{_t}": [_i64, _vp, _vp, _vp, _vp],
         f"defmm_l2p_{_t}": [_i32, _i64] + [_vp] * 13 + [_f64, _vp, _vp, _vp, _vp, _vp],
         f"defmm_p2p_{_t}": [_i64] + [_vp] * 16 + [_f64, _f64, _vp, _vp, _i64, _vp, _vp, _vp, _i32, _i32, _vp],
     })

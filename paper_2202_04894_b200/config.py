@@ -3,9 +3,11 @@
 FmmConfig/MacParams/FmmInfo/InteractionEvent keep the fields, defaults and
 validation of traversal.py:46-85; TreeConfig those of tree.py:36-45.  The
 extra FmmConfig field ``dtype`` selects the device storage precision: "c128"
-(the reference's complex128, kernel.py:68, tree.py:147) or "c64" (complex64
-storage and streams; P2P coordinate differences and the M2L/P2P/L2P sums in
-FP64; cell-relative phases and Lagrange weights in FP32).
+(the reference's complex128, kernel.py:68, tree.py:147; all arithmetic FP64)
+or "c64" (complex64 storage and streams: coordinate differences are formed in
+FP64 and rounded once; P2M/M2M/L2L, M2F, the Hadamard M2L products and per-row
+sums and the P2P pair terms and sums run in FP32; the F2L, the L2P sum and the
+near + far combine run in FP64 -- include/defmm_b200.h).
 """
 
 from __future__ import annotations

@@ -191,9 +191,8 @@ __constant__ float2 c_twf[8][15];  // the same, rounded to float (complex64 M2F 
 // accumulators) is stored in ORBIT ORDER: the natural frequency indices
 // j = f0 P^2 + f1 P + f2 grouped by their orbit under the 48-element cube group
 // acting on (f0, f1, f2) mod P (fourier.py:90-101 / rotated_index below), the
-// orbits packed first-fit-decreasing into SLICES of <= SLICE_W positions.  A
-// slice is closed under every rotation, so the slice M2L can hold the
-// canonical symbols of one slice in shared memory.  g_forder[L-1][pos] =
+// orbits packed first-fit-decreasing into SLICES of <= SLICE_W positions (each
+// slice closed under every rotation).  g_forder[L-1][pos] =
 // natural index at a position, g_finv the inverse.  All orbits but the zero
 // frequency have even size and the zero orbit sits in the last slice, so
 // every other slice starts at an even position (16-B vector loads for c64).
@@ -205,11 +204,6 @@ constexpr int MAX_SLICES = 40;
 constexpr int MAX_P3 = 15 * 15 * 15;
 __device__ int16_t g_forder[8][MAX_P3];
 __device__ int16_t g_finv[8][MAX_P3];
-__device__ int32_t g_slice_start[8][MAX_SLICES + 1];
-// rotation maps per slice, packed per lane: byte q of g_rot[L-1][slice][rid][lane]
-// = slice-local position of the canonical entry feeding the lane's q-th
-// position (2 lane, 2 lane + 1, 64 + 2 lane, 65 + 2 lane) under rotation rid
-__device__ uint32_t g_rot[8][MAX_SLICES][48][32];
 
 template <int L>
 __device__ __forceinline__ int forder(int pos) {
@@ -1030,39 +1024,11 @@ __host__ __device__ constexpr int group_min_blocks() {  // register cap per K, a
     constexpr int regs = K == 2 ? DEFMM_PAIR_REGS : K == 3 ? DEFMM_TRIPLE_REGS : DEFMM_QUARTET_REGS;
     return 65536 / (m2l_block<R, L>() * regs) < 32 ? 65536 / (m2l_block<R, L>() * regs) : 32;
 }
-// SMQ = true (K7 v10, SM-local claiming): the M2L is bound by the L2 -> SM
-// fabric (ncu v10: 30 GB of L2 -> L1 sectors in 2.39 ms = ~6400 B/clk, the
-// chip's LTS throughput cap), so only L1 hits take bytes off it.  The sorted
-// groups are dealt to the nq SMs in chunks of `chunk` consecutive groups,
-// round robin (window w: SM q owns groups w nq chunk + q chunk + [0, chunk)):
-// a CTA claims the next group of ITS SM's sequence (atomic counter
-// qcnt[smid % nq]) and steals from the following SMs' sequences once its own
-// is exhausted.  CTAs resident on one SM then work on neighbouring groups,
-// which share source spectra and (same translations) symbols in that SM's
-// L1, while all SMs stay inside one window of the list (one contiguous chunk
-// per SM spread the L2 working set over the whole list: DRAM reads 0.42 ->
-// 3.9 GB).  Every group is claimed exactly once (ngroups CTAs, counters only
-// grow); per-group arithmetic is unchanged.
-__device__ __forceinline__ int64_t claim_sm_group(int64_t ngroups, int nq, int chunk, int* qcnt) {
-    uint32_t smid;
-    asm volatile("mov.u32 %0, %%smid;\n" : "=r"(smid));
-    const int q0 = (int)(smid % (uint32_t)nq);
-    const int64_t span = (int64_t)nq * chunk, full = ngroups / span, rem = ngroups - full * span;
-    for (int d = 0; d < nq; ++d) {
-        const int c = q0 + d < nq ? q0 + d : q0 + d - nq;
-        const int64_t tail = rem - (int64_t)c * chunk;
-        const int64_t n = full * chunk + (tail < 0 ? 0 : tail > chunk ? chunk : tail);
-        if (n == 0 || *((volatile int*)(qcnt + c)) >= n) continue;
-        const int i = atomicAdd(qcnt + c, 1);
-        if (i < n) return (i / chunk) * span + (int64_t)c * chunk + i % chunk;
-    }
-    return -1;  // unreachable: a free slot exists while this CTA holds none
-}
-template <typename R, int L, int K, bool SMQ = false>
+template <typename R, int L, int K>
 __global__ void __launch_bounds__(m2l_block<R, L>(), group_min_blocks<R, L, K>())
     m2l_group_kernel(int64_t ngroups, const int64_t* __restrict__ grp_slot, const int64_t* __restrict__ grp_ptr,
                      const int* __restrict__ ent, const cx<R>* __restrict__ hat, const cx<R>* __restrict__ symd,
-                     cx<R>* __restrict__ local, int nq = 0, int chunk = 1, int* qcnt = nullptr) {
+                     cx<R>* __restrict__ local) {
     constexpr int P = pad<L>(), L3 = cube<L>(), P3 = P * P * P;
     constexpr int SS = spec_stride<R, L>();
     constexpr int NT = m2l_block<R, L>();
@@ -1083,14 +1049,7 @@ __global__ void __launch_bounds__(m2l_block<R, L>(), group_min_blocks<R, L, K>()
     double2* X = tw + P * L;
     double2* Z1 = X + P3 + 1;
     double2* O = Z1;  // Z1 is dead after the second axis: 6 CTAs fit a 64 KB carveout
-    int64_t g = blockIdx.x;
-    if constexpr (SMQ) {
-        __shared__ int64_t claimed;
-        if (threadIdx.x == 0) claimed = claim_sm_group(ngroups, nq, chunk, qcnt);
-        __syncthreads();
-        g = claimed;
-        if (g < 0) return;
-    }
+    const int64_t g = blockIdx.x;
     make_twiddle_matrix<L, double2>(tw);
     const VT* hv = reinterpret_cast<const VT*>(hat);
     const VT* dv = reinterpret_cast<const VT*>(symd);
@@ -1156,172 +1115,6 @@ __global__ void __launch_bounds__(m2l_block<R, L>(), group_min_blocks<R, L, K>()
             for (int w = 0; w < W; ++w) {
                 const int j = jv * W + w;
                 if (jv < NV && j < P3) X[forder<L>(j)] = to_d(acc[u][m][w]);
-            }
-        }
-        __syncthreads();
-        f2l_row<L, double2>(tw, X, Z1, O, NT);
-        __syncthreads();
-        cx<R>* out = local + slot * L3;
-        for (int t = threadIdx.x; t < L3; t += NT) out[t] = from_d<cx<R>>(O[t]);
-        __syncthreads();
-    }
-}
-
-// ---------------------------------------------------------------------------
-// K7 v9: sibling-group M2L fed by bulk copies (TMA engine) into a shared-memory
-// ring.  The LDG path of m2l_group_kernel is bound by L1 LSU data-pipe
-// wavefronts (ncu v9: 91%) although its data-bank traffic is only 21-28%: L2
-// misses return sectors piecewise, ~2.5 sectors per wavefront instead of 4.
-// Here one producer lane copies each entry's source spectrum and its rows'
-// symbols (cp.async.bulk, whole spectra, complete_tx on the stage's "full"
-// mbarrier) and the consumer warps read them with full-width LDS.128 (4
-// sectors per wavefront), releasing the stage through its "empty" mbarrier.
-// Same entries, same per-row accumulation order, same F2L as m2l_group_kernel.
-__device__ __forceinline__ uint32_t sm32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(sm32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sm32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(sm32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}\n" ::"r"(sm32(b)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                     sm32(dst)),
-                 "l"(src), "r"(bytes), "r"(sm32(b))
-                 : "memory");
-}
-template <typename R, int L, int K>
-__host__ __device__ constexpr int gtma_stages() {  // ring depth: ~64 KB of stages, 2..4
-    constexpr int sb = spec_stride<R, L>() * (int)sizeof(cx<R>) * (K + 1);
-    return 65536 / sb > 4 ? 4 : 65536 / sb < 2 ? 2 : 65536 / sb;
-}
-template <typename R, int L, int K>
-__host__ __device__ constexpr size_t gtma_smem_bytes() {
-    constexpr int P = pad<L>();
-    return (size_t)gtma_stages<R, L, K>() * (K + 1) * spec_stride<R, L>() * sizeof(cx<R>) +
-           2 * gtma_stages<R, L, K>() * sizeof(uint64_t) +
-           sizeof(double2) * (P * L + P * P * P + 1 + L * P * P + L * L * L);
-}
-template <typename R, int L, int K>
-__global__ void __launch_bounds__(m2l_block<R, L>() + 32, 2)
-    m2l_group_tma_kernel(int64_t ngroups, const int64_t* __restrict__ grp_slot, const int64_t* __restrict__ grp_ptr,
-                         const int* __restrict__ ent, const cx<R>* __restrict__ hat,
-                         const cx<R>* __restrict__ symd, cx<R>* __restrict__ local) {
-    constexpr int P = pad<L>(), L3 = cube<L>(), P3 = P * P * P;
-    constexpr int SS = spec_stride<R, L>();
-    constexpr int NC = m2l_block<R, L>();  // consumer threads (multiple of 32)
-    constexpr int NT = NC + 32;            // + one producer warp
-    constexpr bool VEC = sizeof(R) == 4;
-    constexpr int W = VEC ? 2 : 1;
-    constexpr int NV = SS / W;  // 16-B vectors per spectrum
-    constexpr int PER = (NV + NC - 1) / NC;
-    constexpr int ST = gtma_stages<R, L, K>();
-    constexpr uint32_t SB = SS * sizeof(cx<R>);  // bytes per spectrum (multiple of 16)
-    using V = cx<R>;
-    using VT = std::conditional_t<VEC, float4, double2>;
-    static_assert(sizeof(VT) == 16 && SB % 16 == 0 && NC % 32 == 0, "bulk-copy layout");
-    extern __shared__ __align__(16) unsigned char smraw[];  // bulk copies need 16-B alignment
-    VT* ring = reinterpret_cast<VT*>(smraw);  // [ST][K + 1][NV]: source, then row k's symbol
-    uint64_t* full = reinterpret_cast<uint64_t*>(smraw + (size_t)ST * (K + 1) * SB);
-    uint64_t* empty = full + ST;
-    double2* tw = reinterpret_cast<double2*>(empty + ST);
-    double2* X = tw + P * L;
-    double2* Z1 = X + P3 + 1;
-    double2* O = Z1 + L * P * P;
-    const int64_t g = blockIdx.x;
-    const int64_t e0 = grp_ptr[g], e1 = grp_ptr[g + 1];
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < ST; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NC / 32);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    make_twiddle_matrix<L, double2>(tw);
-    __syncthreads();
-    V acc[K][PER][W];
-#pragma unroll
-    for (int u = 0; u < K; ++u)
-#pragma unroll
-        for (int m = 0; m < PER; ++m)
-#pragma unroll
-            for (int w = 0; w < W; ++w) acc[u][m][w] = cz<V>();
-    if (threadIdx.x >= NC) {
-        if (threadIdx.x == NC) {  // producer lane
-            const VT* hv = reinterpret_cast<const VT*>(hat);
-            const VT* dv = reinterpret_cast<const VT*>(symd);
-            for (int64_t e = e0; e < e1; ++e) {
-                const int i = (int)(e - e0), s = i % ST;
-                if (i >= ST) mbar_wait(&empty[s], (uint32_t)((i / ST - 1) & 1));
-                const GroupEnt<K> en = load_gent<K>(ent, e);
-                uint32_t nb = 1;
-#pragma unroll
-                for (int k = 0; k < K; ++k) nb += gent_sym<K>(en, k) >= 0;
-                mbar_expect_tx(&full[s], nb * SB);
-                VT* st = ring + (size_t)s * (K + 1) * NV;
-                bulk_g2s(st, hv + (int64_t)gent_src<K>(en) * NV, SB, &full[s]);
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    const int t = gent_sym<K>(en, k);
-                    if (t >= 0) bulk_g2s(st + (1 + k) * NV, dv + (int64_t)t * NV, SB, &full[s]);
-                }
-            }
-        }
-    } else {
-        for (int64_t e = e0; e < e1; ++e) {
-            const int i = (int)(e - e0), s = i % ST;
-            const GroupEnt<K> en = load_gent<K>(ent, e);
-            mbar_wait(&full[s], (uint32_t)((i / ST) & 1));
-            const VT* st = ring + (size_t)s * (K + 1) * NV;
-#pragma unroll
-            for (int m = 0; m < PER; ++m) {
-                const int jv = threadIdx.x + m * NC;
-                if (jv < NV) {
-                    const VT x = st[jv];
-#pragma unroll
-                    for (int k = 0; k < K; ++k) {
-                        if (gent_sym<K>(en, k) >= 0) {
-                            const VT d = st[(1 + k) * NV + jv];
-                            if constexpr (VEC) {
-                                acc[k][m][0] = cfma(make_float2(d.x, d.y), make_float2(x.x, x.y), acc[k][m][0]);
-                                acc[k][m][W - 1] =
-                                    cfma(make_float2(d.z, d.w), make_float2(x.z, x.w), acc[k][m][W - 1]);
-                            } else {
-                                acc[k][m][0] = cfma(d, x, acc[k][m][0]);
-                            }
-                        }
-                    }
-                }
-            }
-            __syncwarp();
-            if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < K; ++u) {
-        const int64_t slot = grp_slot[K * g + u];
-        if (slot < 0) break;  // uniform; rows fill the group from the front
-        if (threadIdx.x < NC) {
-#pragma unroll
-            for (int m = 0; m < PER; ++m) {
-                const int jv = threadIdx.x + m * NC;
-#pragma unroll
-                for (int w = 0; w < W; ++w) {
-                    const int j = jv * W + w;
-                    if (jv < NV && j < P3) X[forder<L>(j)] = to_d(acc[u][m][w]);
-                }
             }
         }
         __syncthreads();
@@ -1505,379 +1298,6 @@ __global__ void __launch_bounds__(m2lb_threads<R, L>(), DEFMM_M2LB_MINBLOCKS) m2
                     for (int w = 0; w < W; ++w) lhat[row * SS + (int64_t)jv * W + w] = acc[a][w];
                 }
             }
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// K7 v5: quad M2L (surface-like levels).  Every parent-pair block (P, Q) is
-// split along one axis p into QUADS (target layer a_p = V, source layer
-// b_p = W): <= 4 x 4 pairs whose translations differ only in-plane, i.e. 4
-// spectra and <= 9 symbols feed <= 16 events from registers, with one
-// branch-free code path per (p, V, W).  A CTA owns a group = (target parent,
-// key) and keeps its <= 8 target accumulators in registers across the
-// group's quads (c64: two frequencies per thread, 16-B loads).
-// Quad descriptor (4 x int4): src[4] spectrum of in-plane source child ib
-// (or -1), trans[9] derived symbol of in-plane offset e = (du+1)*3 + (dw+1)
-// (or -1), mask16 bit 4 ia + ib, code = 4p + 2V + W.
-template <typename R>
-struct QuadVec;
-template <>
-#ifndef DEFMM_QUAD_C64_W
-#define DEFMM_QUAD_C64_W 2
-#endif
-// complex64: two entries per thread (float4, 96 registers, 27% warps active);
-// one per thread (float2, 56 registers) measured 1% slower on cfg2 L6
-struct QuadVec<float> {
-    using t = std::conditional_t<DEFMM_QUAD_C64_W == 2, float4, float2>;
-    static constexpr int W = DEFMM_QUAD_C64_W;
-};
-template <>
-struct QuadVec<double> {
-    using t = double2;
-    static constexpr int W = 1;
-};
-// the spectrum is split over gridDim.y chunks of <= 384 vector lanes (L >= 5
-// c128 spectra exceed one CTA's 1024 threads)
-template <typename R, int L>
-__host__ __device__ constexpr int quad_chunks() {
-    return (spec_stride<R, L>() / QuadVec<R>::W + 383) / 384;
-}
-template <typename R, int L>
-__host__ __device__ constexpr int quad_threads() {
-    return ((spec_stride<R, L>() / QuadVec<R>::W + quad_chunks<R, L>() - 1) / quad_chunks<R, L>() + 31) / 32 * 32;
-}
-
-__device__ __forceinline__ void qfma(float2 (&acc)[2], const float4& d, const float4& s) {
-    acc[0] = cfma(make_float2(d.x, d.y), make_float2(s.x, s.y), acc[0]);
-    acc[1] = cfma(make_float2(d.z, d.w), make_float2(s.z, s.w), acc[1]);
-}
-#if DEFMM_QUAD_C64_W == 1
-__device__ __forceinline__ void qfma(float2 (&acc)[1], const float2& d, const float2& s) {
-    acc[0] = cfma(d, s, acc[0]);
-}
-#endif
-__device__ __forceinline__ void qfma(double2 (&acc)[1], const double2& d, const double2& s) {
-    acc[0] = cfma(d, s, acc[0]);
-}
-
-template <int PP, int PV, int PW, typename VT, typename V, int W>
-__device__ __forceinline__ void quad_body(const int4& q0, const int4& q1, const int4& q2, const int4& q3,
-                                          const VT* hv, const VT* dv, int64_t NV, int jv, bool act,
-                                          V (&acc)[8][W]) {
-    const int src[4] = {q0.x, q0.y, q0.z, q0.w};
-    const int tr[9] = {q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w, q3.x};
-    const uint32_t mask = (uint32_t)q3.y;
-    VT S[4], D[9];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) S[i] = (src[i] >= 0 && act) ? __ldg(hv + (int64_t)src[i] * NV + jv) : VT{};
-#pragma unroll
-    for (int e = 0; e < 9; ++e) D[e] = (tr[e] >= 0 && act) ? __ldg(dv + (int64_t)tr[e] * NV + jv) : VT{};
-#pragma unroll
-    for (int ia = 0; ia < 4; ++ia)
-#pragma unroll
-        for (int ib = 0; ib < 4; ++ib) {
-            const int e = (((ia >> 1) & 1) - ((ib >> 1) & 1) + 1) * 3 + ((ia & 1) - (ib & 1) + 1);
-            if ((mask >> (4 * ia + ib)) & 1) qfma(acc[embed2(ia, PP, PV)], D[e], S[ib]);
-        }
-}
-
-template <typename R, int L>
-__global__ void __launch_bounds__(quad_threads<R, L>()) m2l_quad_kernel(
-    int64_t ngroups, const int64_t* __restrict__ grp_ptr, const int64_t* __restrict__ grp_rows,
-    const int4* __restrict__ quads, const cx<R>* __restrict__ hat, const cx<R>* __restrict__ symd,
-    cx<R>* __restrict__ lhat) {
-    using VT = typename QuadVec<R>::t;
-    using V = cx<R>;
-    constexpr int W = QuadVec<R>::W;
-    constexpr int SS = spec_stride<R, L>();
-    constexpr int NV = SS / W;
-    const int64_t g = blockIdx.x;
-    const int jv = blockIdx.y * quad_threads<R, L>() + threadIdx.x;
-    const bool act = jv < NV;
-    const VT* hv = reinterpret_cast<const VT*>(hat);
-    const VT* dv = reinterpret_cast<const VT*>(symd);
-    V acc[8][W];
-#pragma unroll
-    for (int a = 0; a < 8; ++a)
-#pragma unroll
-        for (int w = 0; w < W; ++w) acc[a][w] = cz<V>();
-    const int64_t q0i = grp_ptr[g], q1i = grp_ptr[g + 1];
-    for (int64_t qi = q0i; qi < q1i; ++qi) {
-        const int4 q0 = __ldg(quads + 4 * qi), q1 = __ldg(quads + 4 * qi + 1);
-        const int4 q2 = __ldg(quads + 4 * qi + 2), q3 = __ldg(quads + 4 * qi + 3);
-        switch (q3.z) {  // warp-uniform
-            case 0: quad_body<0, 0, 0>(q0, q1, q2, q3, hv, dv, NV, jv, act, acc); break;
-            case 1: quad_body<0, 0, 1>(q0, q1, q2, q3, hv, dv, NV, jv, act, acc); break;
-            case 2: quad_body<0, 1, 0>(q0, q1, q2, q3, hv, dv, NV, jv, act, acc); break;
-            case 3: quad_body<0, 1, 1>(q0, q1, q2, q3, hv, dv, NV, jv, act, acc); break;
-            case 4: quad_body<1, 0, 0>(q0, q1, q2, q3, hv, dv, NV, jv, act, acc); break;
-            case 5: quad_body<1, 0, 1>(q0, q1, q2, q3, hv, dv, NV, jv, act, acc); break;
-            case 6: quad_body<1, 1, 0>(q0, q1, q2, q3, hv, dv, NV, jv, act, acc); break;
-            case 7: quad_body<1, 1, 1>(q0, q1, q2, q3, hv, dv, NV, jv, act, acc); break;
-            case 8: quad_body<2, 0, 0>(q0, q1, q2, q3, hv, dv, NV, jv, act, acc); break;
-            case 9: quad_body<2, 0, 1>(q0, q1, q2, q3, hv, dv, NV, jv, act, acc); break;
-            case 10: quad_body<2, 1, 0>(q0, q1, q2, q3, hv, dv, NV, jv, act, acc); break;
-            default: quad_body<2, 1, 1>(q0, q1, q2, q3, hv, dv, NV, jv, act, acc); break;
-        }
-    }
-    if (act) {
-#pragma unroll
-        for (int a = 0; a < 8; ++a) {
-            const int64_t row = grp_rows[8 * g + a];
-            if (row >= 0) {
-#pragma unroll
-                for (int w = 0; w < W; ++w) lhat[row * SS + (int64_t)jv * W + w] = acc[a][w];
-            }
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// K7 v6: tile M2L.  One CTA per tile = a run of Morton-consecutive rows with
-// one key (host: defmm_m2l_tiles) whose source spectra and derived symbols,
-// as a union, fit shared memory.  The CTA stages the tile's operand ids and
-// packed events once, then walks the spectrum in slices of F entries with a
-// cp.async double buffer: while slice s is consumed from shared memory, the
-// union's slice s+1 streams in.  Each operand is read from L2 once per tile
-// instead of once per event (4-8x fewer L2->SM bytes than the row kernel on
-// surface data).  Threads = KS row slots x F frequencies; with nr < KS rows a
-// row is split over KS / nr slots (every (KS/nr)-th event), reduced in fixed
-// slot order.  Accumulated spectra go to lhat; f2l_rows_kernel applies the
-// inverse DFT.
-template <typename R>
-struct TileCfg;
-template <>
-struct TileCfg<float> {  // 16 x complex64 = 128 B per operand slice
-    static constexpr int F = 16, KS = 16;
-};
-template <>
-struct TileCfg<double> {  // 8 x complex128 = 128 B per operand slice
-    static constexpr int F = 8, KS = 32;
-};
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-template <int BYTES>
-__device__ __forceinline__ void cp_async(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(smem_u32(dst)), "l"(src), "n"(BYTES));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-template <typename R>
-__host__ __device__ constexpr size_t tile_smem_bytes(int u_max, int e_max) {
-    return 2 * (size_t)u_max * TileCfg<R>::F * sizeof(cx<R>)                 // operand slices, double buffer
-           + (size_t)TileCfg<R>::KS * TileCfg<R>::F * sizeof(cx<R>)          // part sums
-           + (size_t)u_max * sizeof(int32_t) + (size_t)e_max * sizeof(uint32_t);  // operand ids, events
-}
-
-template <typename R, int L>
-__global__ void __launch_bounds__(256) m2l_tile_kernel(
-    const int64_t* __restrict__ tile_ptr, const int64_t* __restrict__ op_ptr, const int32_t* __restrict__ ops,
-    const int64_t* __restrict__ ev_ptr, const uint32_t* __restrict__ ev, int64_t lhat_base, int u_max,
-    const cx<R>* __restrict__ hat, const cx<R>* __restrict__ symd, cx<R>* __restrict__ lhat) {
-    using V = cx<R>;
-    constexpr int F = TileCfg<R>::F, KS = TileCfg<R>::KS, NT = F * KS;
-    constexpr int SS = spec_stride<R, L>();
-    constexpr int NS = (SS + F - 1) / F;
-    extern __shared__ __align__(16) unsigned char smraw[];
-    V* buf = reinterpret_cast<V*>(smraw);         // [2][u_max][F]
-    V* red = buf + 2 * (size_t)u_max * F;         // [KS][F]
-    int32_t* sops = reinterpret_cast<int32_t*>(red + KS * F);
-    uint32_t* sev = reinterpret_cast<uint32_t*>(sops + u_max);
-    const int64_t tile = blockIdx.x;
-    const int64_t r0 = tile_ptr[tile];
-    const int nr = (int)(tile_ptr[tile + 1] - r0);
-    const int64_t o0 = op_ptr[tile];
-    const int nu = (int)(op_ptr[tile + 1] - o0);
-    const int64_t eb = ev_ptr[r0];
-    const int ne = (int)(ev_ptr[r0 + nr] - eb);
-    const int f = threadIdx.x % F, slot = threadIdx.x / F;
-    for (int i = threadIdx.x; i < nu; i += NT) cp_async<4>(sops + i, ops + o0 + i);
-    for (int i = threadIdx.x; i < ne; i += NT) cp_async<4>(sev + i, ev + eb + i);
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
-    auto issue = [&](int sl) {
-        V* dst = buf + (size_t)(sl & 1) * u_max * F;
-        const int j = sl * F + f;
-        for (int u = slot; u < nu; u += KS) {
-            const int32_t g = sops[u];
-            if (j < SS) {
-                const V* src = g >= 0 ? hat + (int64_t)g * SS : symd + (int64_t)(-1 - g) * SS;
-                cp_async<sizeof(V)>(dst + u * F + f, src + j);
-            } else {
-                dst[u * F + f] = cz<V>();
-            }
-        }
-        cp_async_commit();
-    };
-    const int parts = KS / nr;  // nr <= KS (host k_max)
-    const int row = slot % nr, part = slot / nr;
-    const bool active = part < parts;
-    // part p of a row: a contiguous event range (vector loads of 4 packed events)
-    int c0 = 0, c1 = 0;
-    if (active) {
-        const int e0 = (int)(ev_ptr[r0 + row] - eb), len = (int)(ev_ptr[r0 + row + 1] - eb) - e0;
-        c0 = e0 + (len * part) / parts;
-        c1 = e0 + (len * (part + 1)) / parts;
-    }
-    issue(0);
-    for (int sl = 0; sl < NS; ++sl) {
-        if (sl + 1 < NS) {
-            issue(sl + 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
-        const V* bs = buf + (size_t)(sl & 1) * u_max * F + f;
-        auto ev1 = [&](uint32_t pk, V& a) { a = cfma(bs[(pk >> 16) * F], bs[(pk & 0xffffu) * F], a); };
-        V acc0 = cz<V>(), acc1 = cz<V>(), acc2 = cz<V>(), acc3 = cz<V>();
-        int e = c0;
-        for (; e < c1 && (e & 3); ++e) ev1(sev[e], acc0);
-        for (; e + 4 <= c1; e += 4) {
-            const uint4 p4 = *reinterpret_cast<const uint4*>(sev + e);
-            ev1(p4.x, acc0);
-            ev1(p4.y, acc1);
-            ev1(p4.z, acc2);
-            ev1(p4.w, acc3);
-        }
-        for (; e < c1; ++e) ev1(sev[e], acc1);
-        red[slot * F + f] = cadd(cadd(acc0, acc1), cadd(acc2, acc3));
-        __syncthreads();  // part sums visible; buffer (sl & 1) consumed
-        const int j = sl * F + f;
-        if (part == 0 && j < SS) {
-            V a = red[row * F + f];
-            for (int q = 1; q < parts; ++q) a = cadd(a, red[(row + q * nr) * F + f]);
-            lhat[(lhat_base + r0 + row) * SS + j] = a;
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// K7 v4: slice M2L.  Grid = (row batch, spectral slice).  The Hadamard M2L is
-// independent per frequency, and a slice is closed under the cube group, so a
-// CTA keeps the CANONICAL symbols of its level restricted to its slice in
-// shared memory (in groups of G symbols) together with the slice's 48
-// rotation maps, and streams only the source spectra (one slice = <= 128
-// entries per event, 4 per lane, one warp per row): half the L2->SM bytes of
-// the row kernel, whose derived symbols double the per-event traffic.
-// Events of a row are sorted by symbol group; the accumulated slice is kept in
-// lhat between groups (read back by the same thread).  Event entries
-// {spectrum, canonical-in-group << 6 | rotation} are loaded 32 at a time and
-// broadcast by shuffles.
-constexpr int SLICE_WARPS = 16;
-template <typename R>
-__host__ __device__ constexpr int slice_group() {
-    return sizeof(R) == 4 ? 96 : 48;  // symbols per group: G * 128 * sizeof(cx<R>) = 96 KB
-}
-template <typename R>
-__host__ __device__ constexpr size_t slice_smem_bytes() {
-    return sizeof(cx<R>) * slice_group<R>() * SLICE_W + 48 * 32 * sizeof(uint32_t);
-}
-
-// two adjacent complex entries (k even; 16-B aligned for c64, whose second
-// entry past an odd last slice is the zero pad of the stride)
-__device__ __forceinline__ void ld2(const float2* p, bool on, bool, float2& a, float2& b) {
-    if (on) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(p));
-        a = make_float2(v.x, v.y);
-        b = make_float2(v.z, v.w);
-    } else {
-        a = b = make_float2(0.f, 0.f);
-    }
-}
-__device__ __forceinline__ void ld2(const double2* p, bool on, bool on_b, double2& a, double2& b) {
-    a = on ? __ldg(p) : make_double2(0.0, 0.0);
-    b = on_b ? __ldg(p + 1) : make_double2(0.0, 0.0);
-}
-
-template <typename R, int L>
-__global__ void __launch_bounds__(32 * SLICE_WARPS, 2) m2l_slice_kernel(
-    const int4* __restrict__ batch, int64_t row_base, const int64_t* __restrict__ seg, int ngs,
-    const int2* __restrict__ ent, const cx<R>* __restrict__ hat, const cx<R>* __restrict__ symc,
-    cx<R>* __restrict__ lhat) {
-    using V = cx<R>;
-    constexpr int SS = spec_stride<R, L>();
-    constexpr int G = slice_group<R>();
-    extern __shared__ unsigned char smraw[];
-    V* sym = reinterpret_cast<V*>(smraw);                                  // [G][SLICE_W]
-    uint32_t* rot = reinterpret_cast<uint32_t*>(sym + G * SLICE_W);        // [48][32]
-    const int sl = blockIdx.y;
-    const int start = g_slice_start[L - 1][sl];
-    const int size = g_slice_start[L - 1][sl + 1] - start;
-    const int4 bt = batch[blockIdx.x];  // {row0, row1, first canonical symbol, count}
-    for (int t = threadIdx.x; t < 48 * 32; t += blockDim.x) rot[t] = g_rot[L - 1][sl][t >> 5][t & 31];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // positions k0, k0+1 and k0+64, k0+65 (the last slice may be odd-sized:
-    // its pad partner is the zero pad entry of the c64 stride, or masked)
-    const int k0 = 2 * lane, k2 = 64 + 2 * lane;
-    const bool on0 = k0 < size, on2 = k2 < size;
-    const bool on1 = k0 + 1 < size, on3 = k2 + 1 < size;
-    const int ng = (bt.w + G - 1) / G;
-    for (int g = 0; g < ng; ++g) {
-        __syncthreads();  // the previous group's symbols are consumed
-        const int nc = min(G, bt.w - g * G);
-        const V* src = symc + (int64_t)(bt.z + g * G) * SS + start;
-        for (int t = threadIdx.x; t < nc * SLICE_W; t += blockDim.x) {
-            const int c = t / SLICE_W, k = t % SLICE_W;
-            sym[t] = k < size ? __ldg(src + (int64_t)c * SS + k) : cz<V>();
-        }
-        __syncthreads();
-        for (int row = bt.x + warp; row < bt.y; row += SLICE_WARPS) {
-            const int64_t* sg = seg + (row - row_base) * (int64_t)(ngs + 1);
-            const int64_t e0 = sg[g], e1 = sg[g + 1];
-            if (g > 0 && e0 == e1) continue;
-            V* out = lhat + (int64_t)row * SS + start;
-            V a0, a1, a2, a3;
-            if (g > 0) {
-                a0 = on0 ? out[k0] : cz<V>();
-                a1 = on1 ? out[k0 + 1] : cz<V>();
-                a2 = on2 ? out[k2] : cz<V>();
-                a3 = on3 ? out[k2 + 1] : cz<V>();
-            } else {
-                a0 = a1 = a2 = a3 = cz<V>();
-            }
-            for (int64_t base = e0; base < e1; base += 32) {
-                const int cnt = e1 - base < 32 ? (int)(e1 - base) : 32;
-                const int2 mine = lane < cnt ? __ldg(ent + base + lane) : make_int2(0, 0);
-                for (int u = 0; u < cnt; u += 2) {
-                    // two events in flight
-                    const int sxa = __shfl_sync(0xffffffffu, mine.x, u);
-                    const int sya = __shfl_sync(0xffffffffu, mine.y, u);
-                    const bool hb = u + 1 < cnt;
-                    const int sxb = __shfl_sync(0xffffffffu, mine.x, hb ? u + 1 : u);
-                    const int syb = __shfl_sync(0xffffffffu, mine.y, hb ? u + 1 : u);
-                    const V* SA = hat + (int64_t)sxa * SS + start;
-                    const V* SB = hat + (int64_t)sxb * SS + start;
-                    V xa0, xa1, xa2, xa3, xb0, xb1, xb2, xb3;
-                    ld2(SA + k0, on0, on1, xa0, xa1);
-                    ld2(SA + k2, on2, on3, xa2, xa3);
-                    ld2(SB + k0, on0 && hb, on1 && hb, xb0, xb1);
-                    ld2(SB + k2, on2 && hb, on3 && hb, xb2, xb3);
-                    const uint32_t ra = rot[(sya & 63) * 32 + lane];
-                    const uint32_t rb = rot[(syb & 63) * 32 + lane];
-                    const V* DA = sym + (sya >> 6) * SLICE_W;
-                    const V* DB = sym + (syb >> 6) * SLICE_W;
-                    a0 = cfma(DA[ra & 0xff], xa0, a0);
-                    a1 = cfma(DA[(ra >> 8) & 0xff], xa1, a1);
-                    a2 = cfma(DA[(ra >> 16) & 0xff], xa2, a2);
-                    a3 = cfma(DA[ra >> 24], xa3, a3);
-                    // event b (zeros when absent: its spectrum loads were masked)
-                    a0 = cfma(DB[rb & 0xff], xb0, a0);
-                    a1 = cfma(DB[(rb >> 8) & 0xff], xb1, a1);
-                    a2 = cfma(DB[(rb >> 16) & 0xff], xb2, a2);
-                    a3 = cfma(DB[rb >> 24], xb3, a3);
-                }
-            }
-            if (on0) out[k0] = a0;
-            if (on1) out[k0 + 1] = a1;
-            if (on2) out[k2] = a2;
-            if (on3) out[k2 + 1] = a3;
         }
     }
 }
@@ -2517,7 +1937,6 @@ struct HostLayout {
     int P3 = 0, nslices = 0;
     std::vector<int16_t> forder, finv;
     std::vector<int32_t> start;
-    std::vector<uint32_t> rot;  // [slice][48][32 lanes], 4 packed slice-local positions
 };
 
 // orbit-ordered spectral layout of order L (see g_forder): orbits keyed by the
@@ -2587,20 +2006,6 @@ HostLayout make_layout(int L) {
         H.start.push_back(pos);
     }
     for (int t = 0; t < P3; ++t) H.finv[H.forder[t]] = (int16_t)t;
-    H.rot.assign((size_t)H.nslices * 48 * 32, 0);
-    for (int sl = 0; sl < H.nslices; ++sl)
-        for (int rid = 0; rid < 48; ++rid)
-            for (int lane = 0; lane < 32; ++lane) {
-                uint32_t w = 0;
-                for (int q = 0; q < 4; ++q) {
-                    const int k = (q >> 1) * 64 + 2 * lane + (q & 1);
-                    int loc = 0;
-                    if (k < H.start[sl + 1] - H.start[sl])
-                        loc = H.finv[host_rotated_index(P, H.forder[H.start[sl] + k], rid)] - H.start[sl];
-                    w |= (uint32_t)(loc & 0xff) << (8 * q);
-                }
-                H.rot[((size_t)sl * 48 + rid) * 32 + lane] = w;
-            }
     return H;
 }
 
@@ -2614,9 +2019,15 @@ const HostLayout& layout_of(int L) {
     return cache[L];
 }
 
+// device tables (spectral layout, twiddles) are per device: filled once per
+// device the process launches on (keyed by the current device)
 int ensure_twiddles() {
-    static bool done = false;
-    if (done) return 0;
+    constexpr int MAX_DEV = 64;
+    static bool done[MAX_DEV] = {};
+    int dev = 0;
+    if (int rc = report(cudaGetDevice(&dev), "cudaGetDevice")) return rc;
+    if (dev < 0 || dev >= MAX_DEV) return report(cudaErrorInvalidDevice, "ensure_twiddles: device index");
+    if (done[dev]) return 0;
     for (int L = 2; L <= 8; ++L) {
         const HostLayout& H = layout_of(L);
         if (H.nslices > MAX_SLICES) return report(cudaErrorInvalidValue, "spectral layout: too many slices");
@@ -2626,14 +2037,6 @@ int ensure_twiddles() {
         if (!rc)
             rc = report(cudaMemcpyToSymbol(g_finv, H.finv.data(), H.P3 * sizeof(int16_t),
                                            o * MAX_P3 * sizeof(int16_t)), "cudaMemcpyToSymbol(g_finv)");
-        if (!rc)
-            rc = report(cudaMemcpyToSymbol(g_slice_start, H.start.data(), H.start.size() * sizeof(int32_t),
-                                           o * (MAX_SLICES + 1) * sizeof(int32_t)),
-                        "cudaMemcpyToSymbol(g_slice_start)");
-        if (!rc)
-            rc = report(cudaMemcpyToSymbol(g_rot, H.rot.data(), H.rot.size() * sizeof(uint32_t),
-                                           o * MAX_SLICES * 48 * 32 * sizeof(uint32_t)),
-                        "cudaMemcpyToSymbol(g_rot)");
         if (rc) return rc;
     }
     double2 h[8][15] = {};
@@ -2651,7 +2054,7 @@ int ensure_twiddles() {
             for (int k = 0; k < 15; ++k) hf[l][k] = make_float2((float)h[l][k].x, (float)h[l][k].y);
         rc = report(cudaMemcpyToSymbol(c_twf, hf, sizeof(hf)), "cudaMemcpyToSymbol(c_twf)");
     }
-    if (rc == 0) done = true;
+    if (rc == 0) done[dev] = true;
     return rc;
 }
 
@@ -2821,75 +2224,26 @@ int launch_m2l_rows(int32_t L, int64_t nrows, const int64_t* row_slot, const int
 
 template <typename R>
 int launch_m2l_group(int32_t L, int32_t K, int64_t ngroups, const int64_t* grp_slot, const int64_t* grp_ptr,
-                     const int32_t* ent, const void* hat, const void* symd, void* local, void* stream,
-                     int32_t nq = 0, int32_t chunk = 1, int32_t* qcnt = nullptr) {
-    if (ngroups == 0) return 0;
-    if (!grid_ok(ngroups) || K < 2 || K > 4 || nq < 0 || (nq > 0 && (qcnt == nullptr || chunk < 1))) return -1;
-    if (int rc0 = ensure_twiddles()) return rc0;
-    cudaStream_t s = (cudaStream_t)stream;
-    if (nq > 0) {
-        if (int rc = report(cudaMemsetAsync(qcnt, 0, sizeof(int32_t) * nq, s), "m2l_group qcnt")) return rc;
-    }
-#define DEFMM_GROUP_LAUNCH(KK, SQ)                                                                          \
-    {                                                                                                       \
-        int rc = set_smem(m2l_group_kernel<R, LL, KK, SQ>, bytes);                                          \
-        if (rc) return rc;                                                                                  \
-        carve(m2l_group_kernel<R, LL, KK, SQ>);                                                             \
-        if (group_carve >= 0)                                                                               \
-            cudaFuncSetAttribute((const void*)m2l_group_kernel<R, LL, KK, SQ>,                              \
-                                 cudaFuncAttributePreferredSharedMemoryCarveout, group_carve);               \
-        m2l_group_kernel<R, LL, KK, SQ><<<(unsigned)ngroups, m2l_block<R, LL>(), bytes, s>>>(               \
-            ngroups, grp_slot, grp_ptr, ent, (const cx<R>*)hat, (const cx<R>*)symd, (cx<R>*)local, nq, chunk, qcnt); \
-    }
-    // DEFMM_GROUP_SMEM=<bytes>: pad the dynamic shared memory of each CTA (caps
-    // the group kernel's CTAs per SM, leaving SM room for the concurrent P2P)
-    // DEFMM_GROUP_CARVE=<percent>: preferred shared-memory carveout of the group
-    // kernel (a smaller carveout leaves more of the 256 KB to L1)
-    static const int group_carve = [] {
-        const char* e = getenv("DEFMM_GROUP_CARVE");
-        return e ? atoi(e) : -1;
-    }();
-    static const size_t smem_pad = [] {
-        const char* e = getenv("DEFMM_GROUP_SMEM");
-        return e ? (size_t)atol(e) : (size_t)0;
-    }();
-    DEFMM_DISPATCH_L(L, {
-        constexpr int P = 2 * LL - 1;
-        size_t bytes = sizeof(double2) * (P * LL + P * P * P + 1 + LL * P * P);  // O aliases Z1
-        if (smem_pad > bytes) bytes = smem_pad;
-        if (nq > 0) {
-            if (K == 2) DEFMM_GROUP_LAUNCH(2, true) else if (K == 3) DEFMM_GROUP_LAUNCH(3, true) else DEFMM_GROUP_LAUNCH(4, true)
-        } else {
-            if (K == 2) DEFMM_GROUP_LAUNCH(2, false) else if (K == 3) DEFMM_GROUP_LAUNCH(3, false) else DEFMM_GROUP_LAUNCH(4, false)
-        }
-    });
-#undef DEFMM_GROUP_LAUNCH
-    return report(cudaGetLastError(), "m2l_group");
-}
-
-template <typename R>
-int launch_m2l_group_tma(int32_t L, int32_t K, int64_t ngroups, const int64_t* grp_slot, const int64_t* grp_ptr,
-                         const int32_t* ent, const void* hat, const void* symd, void* local, void* stream) {
+                     const int32_t* ent, const void* hat, const void* symd, void* local, void* stream) {
     if (ngroups == 0) return 0;
     if (!grid_ok(ngroups) || K < 2 || K > 4) return -1;
     if (int rc0 = ensure_twiddles()) return rc0;
     cudaStream_t s = (cudaStream_t)stream;
-#define DEFMM_GTMA_LAUNCH(KK)                                                                              \
-    {                                                                                                      \
-        constexpr size_t bytes = gtma_smem_bytes<R, LL, KK>();                                             \
-        if (bytes > 227 * 1024) /* ring does not fit: the LDG group kernel */                              \
-            return launch_m2l_group<R>(L, K, ngroups, grp_slot, grp_ptr, ent, hat, symd, local, stream);   \
-        int rc = set_smem(m2l_group_tma_kernel<R, LL, KK>, bytes);                                         \
-        if (rc) return rc;                                                                                 \
-        carve(m2l_group_tma_kernel<R, LL, KK>);                                                            \
-        m2l_group_tma_kernel<R, LL, KK><<<(unsigned)ngroups, m2l_block<R, LL>() + 32, bytes, s>>>(         \
-            ngroups, grp_slot, grp_ptr, ent, (const cx<R>*)hat, (const cx<R>*)symd, (cx<R>*)local);        \
+#define DEFMM_GROUP_LAUNCH(KK)                                                                              \
+    {                                                                                                       \
+        int rc = set_smem(m2l_group_kernel<R, LL, KK>, bytes);                                              \
+        if (rc) return rc;                                                                                  \
+        carve(m2l_group_kernel<R, LL, KK>);                                                                 \
+        m2l_group_kernel<R, LL, KK><<<(unsigned)ngroups, m2l_block<R, LL>(), bytes, s>>>(                   \
+            ngroups, grp_slot, grp_ptr, ent, (const cx<R>*)hat, (const cx<R>*)symd, (cx<R>*)local);         \
     }
     DEFMM_DISPATCH_L(L, {
-        if (K == 2) DEFMM_GTMA_LAUNCH(2) else if (K == 3) DEFMM_GTMA_LAUNCH(3) else DEFMM_GTMA_LAUNCH(4)
+        constexpr int P = 2 * LL - 1;
+        const size_t bytes = sizeof(double2) * (P * LL + P * P * P + 1 + LL * P * P);  // O aliases Z1
+        if (K == 2) DEFMM_GROUP_LAUNCH(2) else if (K == 3) DEFMM_GROUP_LAUNCH(3) else DEFMM_GROUP_LAUNCH(4)
     });
-#undef DEFMM_GTMA_LAUNCH
-    return report(cudaGetLastError(), "m2l_group_tma");
+#undef DEFMM_GROUP_LAUNCH
+    return report(cudaGetLastError(), "m2l_group");
 }
 
 template <typename R>
@@ -2903,58 +2257,6 @@ int launch_m2l_blocked(int32_t L, int64_t ngroups, const int64_t* grp_ptr, const
                             ngroups, grp_ptr, grp_rows, blk_src, blk_trans, blk_mask, blk_kind,
                             (const cx<R>*)hat, (const cx<R>*)symd, (cx<R>*)lhat)));
     return report(cudaGetLastError(), "m2l_blocked");
-}
-
-template <typename R>
-int launch_m2l_quad(int32_t L, int64_t ngroups, const int64_t* grp_ptr, const int64_t* grp_rows,
-                    const int32_t* quads, const void* hat, const void* symd, void* lhat, void* stream) {
-    if (ngroups == 0) return 0;
-    if (!grid_ok(ngroups)) return -1;
-    cudaStream_t s = (cudaStream_t)stream;
-    DEFMM_DISPATCH_L(L, (carve(m2l_quad_kernel<R, LL>), m2l_quad_kernel<R, LL><<<dim3((unsigned)ngroups, quad_chunks<R, LL>()), quad_threads<R, LL>(), 0, s>>>(
-                            ngroups, grp_ptr, grp_rows, (const int4*)quads, (const cx<R>*)hat,
-                            (const cx<R>*)symd, (cx<R>*)lhat)));
-    return report(cudaGetLastError(), "m2l_quad");
-}
-
-template <typename R>
-int launch_m2l_tile(int32_t L, int64_t ntiles, const int64_t* tile_ptr, const int64_t* op_ptr, const int32_t* ops,
-                    const int64_t* ev_ptr, const uint32_t* ev, int64_t lhat_base, int32_t u_max, int32_t e_max,
-                    const void* hat, const void* symd, void* lhat, void* stream) {
-    if (ntiles == 0) return 0;
-    if (!grid_ok(ntiles) || u_max < 1 || e_max < 1) return -1;
-    cudaStream_t s = (cudaStream_t)stream;
-    const size_t bytes = tile_smem_bytes<R>(u_max, e_max);
-    DEFMM_DISPATCH_L(L, {
-        int rc = set_smem(m2l_tile_kernel<R, LL>, bytes);
-        if (rc) return rc;
-        carve(m2l_tile_kernel<R, LL>);
-        m2l_tile_kernel<R, LL><<<(unsigned)ntiles, 256, bytes, s>>>(tile_ptr, op_ptr, ops, ev_ptr, ev, lhat_base,
-                                                                   u_max, (const cx<R>*)hat, (const cx<R>*)symd,
-                                                                   (cx<R>*)lhat);
-    });
-    return report(cudaGetLastError(), "m2l_tile");
-}
-
-template <typename R>
-int launch_m2l_slice(int32_t L, int64_t nbatch, const int32_t* batch, int64_t row_base, const int64_t* seg,
-                     int32_t ngs, const int32_t* entries, const void* hat, const void* symc, void* lhat,
-                     void* stream) {
-    if (nbatch == 0) return 0;
-    if (!grid_ok(nbatch) || ngs < 1) return -1;
-    if (int rc0 = ensure_twiddles()) return rc0;
-    cudaStream_t s = (cudaStream_t)stream;
-    const size_t bytes = slice_smem_bytes<R>();
-    DEFMM_DISPATCH_L(L, {
-        int rc = set_smem(m2l_slice_kernel<R, LL>, bytes);
-        if (rc) return rc;
-        const dim3 grid((unsigned)nbatch, (unsigned)layout_of(LL).nslices);
-        carve(m2l_slice_kernel<R, LL>);
-        m2l_slice_kernel<R, LL><<<grid, 32 * SLICE_WARPS, bytes, s>>>(
-            (const int4*)batch, row_base, seg, ngs, (const int2*)entries, (const cx<R>*)hat, (const cx<R>*)symc,
-            (cx<R>*)lhat);
-    });
-    return report(cudaGetLastError(), "m2l_slice");
 }
 
 template <typename R>
@@ -2974,25 +2276,6 @@ int launch_f2l_rows(int32_t L, int64_t nrows, const int64_t* row_slot, const voi
                                                                    (cx<R>*)local);
     });
     return report(cudaGetLastError(), "f2l_rows");
-}
-
-// out[perm[p]] += near[p]: the near field added after an L2P that ran with a
-// zero near field (lets the L2P overlap the tail of a concurrent P2P)
-template <typename R>
-__global__ void __launch_bounds__(256) add_near_kernel(int64_t n, const int64_t* __restrict__ perm,
-                                                       const cx<R>* __restrict__ near, cx<R>* __restrict__ out) {
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p < n) {
-        const int64_t o = perm[p];
-        out[o] = cadd(out[o], near[p]);
-    }
-}
-template <typename R>
-int launch_add_near(int64_t n, const int64_t* perm, const void* near, void* out, void* stream) {
-    if (n == 0) return 0;
-    if (n < 0) return -1;
-    add_near_kernel<R><<<blocks_of(n, 256), 256, 0, (cudaStream_t)stream>>>(n, perm, (const cx<R>*)near, (cx<R>*)out);
-    return report(cudaGetLastError(), "add_near");
 }
 
 template <typename R>
@@ -3058,8 +2341,6 @@ extern "C" {
 
 int defmm_abi_version(void) { return DEFMM_ABI_VERSION; }
 
-int defmm_slice_group(int32_t c64) { return c64 ? slice_group<float>() : slice_group<double>(); }
-
 int defmm_spectral_layout(int32_t L, int32_t* forder, int32_t* slice_start, int32_t* nslices) {
     if (L < 2 || L > 8) return -1;
     const HostLayout& H = layout_of(L);
@@ -3108,42 +2389,12 @@ const char* defmm_last_error(void) { return g_last_error; }
                                  const void* sym_derived, void* local, void* stream) {                            \
         return launch_m2l_group<R>(L, K, ngroups, grp_slot, grp_ptr, entries, hat, sym_derived, local, stream);   \
     }                                                                                                               \
-    int defmm_m2l_group_smq_##SUFFIX(int32_t L, int32_t K, int64_t ngroups, const int64_t* grp_slot,              \
-                                     const int64_t* grp_ptr, const int32_t* entries, const void* hat,             \
-                                     const void* sym_derived, void* local, int32_t nq, int32_t chunk,             \
-                                     int32_t* qcnt, void* stream) {                                               \
-        return launch_m2l_group<R>(L, K, ngroups, grp_slot, grp_ptr, entries, hat, sym_derived, local, stream, nq, \
-                                   chunk, qcnt);                                                                  \
-    }                                                                                                               \
-    int defmm_m2l_group_tma_##SUFFIX(int32_t L, int32_t K, int64_t ngroups, const int64_t* grp_slot,              \
-                                     const int64_t* grp_ptr, const int32_t* entries, const void* hat,             \
-                                     const void* sym_derived, void* local, void* stream) {                        \
-        return launch_m2l_group_tma<R>(L, K, ngroups, grp_slot, grp_ptr, entries, hat, sym_derived, local,        \
-                                       stream);                                                                   \
-    }                                                                                                               \
     int defmm_m2l_blocked_##SUFFIX(int32_t L, int64_t ngroups, const int64_t* grp_ptr, const int64_t* grp_rows,     \
                                    const int32_t* blk_src, const int32_t* blk_trans, const int64_t* blk_mask,     \
                                    const int8_t* blk_kind, const void* hat, const void* sym_derived, void* lhat,  \
                                    void* stream) {                                                                \
         return launch_m2l_blocked<R>(L, ngroups, grp_ptr, grp_rows, blk_src, blk_trans, blk_mask, blk_kind, hat,   \
                                      sym_derived, lhat, stream);                                                  \
-    }                                                                                                               \
-    int defmm_m2l_quad_##SUFFIX(int32_t L, int64_t ngroups, const int64_t* grp_ptr, const int64_t* grp_rows,        \
-                                const int32_t* quads, const void* hat, const void* sym_derived, void* lhat,        \
-                                void* stream) {                                                                    \
-        return launch_m2l_quad<R>(L, ngroups, grp_ptr, grp_rows, quads, hat, sym_derived, lhat, stream);           \
-    }                                                                                                               \
-    int defmm_m2l_slice_##SUFFIX(int32_t L, int64_t nbatch, const int32_t* batch, int64_t row_base,               \
-                                 const int64_t* seg, int32_t ngs, const int32_t* entries, const void* hat,         \
-                                 const void* sym_canon, void* lhat, void* stream) {                               \
-        return launch_m2l_slice<R>(L, nbatch, batch, row_base, seg, ngs, entries, hat, sym_canon, lhat, stream);   \
-    }                                                                                                               \
-    int defmm_m2l_tile_##SUFFIX(int32_t L, int64_t ntiles, const int64_t* tile_ptr, const int64_t* op_ptr,          \
-                                const int32_t* ops, const int64_t* ev_ptr, const uint32_t* ev, int64_t lhat_base,  \
-                                int32_t u_max, int32_t e_max, const void* hat, const void* sym_derived,            \
-                                void* lhat, void* stream) {                                                        \
-        return launch_m2l_tile<R>(L, ntiles, tile_ptr, op_ptr, ops, ev_ptr, ev, lhat_base, u_max, e_max, hat,      \
-                                  sym_derived, lhat, stream);                                                      \
     }                                                                                                               \
     int defmm_f2l_rows_##SUFFIX(int32_t L, int64_t nrows, const int64_t* row_slot, const void* lhat, void* local,   \
                                 void* stream) {                                                                    \
@@ -3154,9 +2405,6 @@ const char* defmm_last_error(void) { return g_last_error; }
                            const double* dirs, double kappa, void* local, void* stream) {                          \
         return launch_l2l<R>(L, n, out_slot, octant, ptr, src_slot, src_dir, son_beta, dirs, kappa, local,         \
                              stream);                                                                              \
-    }                                                                                                               \
-    int defmm_add_near_##SUFFIX(int64_t n, const int64_t* perm, const void* near, void* out, void* stream) {       \
-        return launch_add_near<R>(n, perm, near, out, stream);                                                     \
     }                                                                                                               \
     int defmm_l2p_##SUFFIX(int32_t L, int64_t n, const int32_t* leaf_cell, const int64_t* slot_lo,                  \
                            const int64_t* slot_hi, const int32_t* slot_dir, const int64_t* cell_start,             \

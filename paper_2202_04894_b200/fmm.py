@@ -29,126 +29,6 @@ def _dev(a, dtype, device):
     return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype).to(device)
 
 
-def _quad_tables():
-    """Per (p, V, W): pair-bit mask of the quad, and per in-plane (ia, ib) the
-    block pair bit 8a+b, per in-plane offset e its block child offset d."""
-    def embed2(i, pp, v):
-        return (v << 2) | i if pp == 0 else (((i >> 1) & 1) << 2) | (v << 1) | (i & 1) if pp == 1 else (i << 1) | v
-
-    def d3(a, b):
-        return ((((a >> 2) & 1) - ((b >> 2) & 1)) + 1) * 9 + ((((a >> 1) & 1) - ((b >> 1) & 1)) + 1) * 3 + \
-            (((a & 1) - (b & 1)) + 1)
-
-    out = {}
-    for pp in range(3):
-        for v in range(2):
-            for w in range(2):
-                bit = np.zeros((4, 4), np.int64)
-                qm = 0
-                d_of_e = np.zeros(9, np.int64)
-                for ia in range(4):
-                    for ib in range(4):
-                        a, b = embed2(ia, pp, v), embed2(ib, pp, w)
-                        bit[ia, ib] = 8 * a + b
-                        qm |= 1 << (8 * a + b)
-                        e = (((ia >> 1) & 1) - ((ib >> 1) & 1) + 1) * 3 + ((ia & 1) - (ib & 1) + 1)
-                        d_of_e[e] = d3(a, b)
-                out[(pp, v, w)] = (np.uint64(qm), bit, d_of_e, [embed2(ib, pp, w) for ib in range(4)])
-    return out
-
-
-_QUAD_TABLES = None
-
-
-def _quads(bsrc, btr, bmask, gptr):
-    """Quad descriptors (defmm_m2l_quad_*) of every block: split along the axis
-    giving the fewest non-empty quads; quads ordered (block, V, W)."""
-    global _QUAD_TABLES
-    if _QUAD_TABLES is None:
-        _QUAD_TABLES = _quad_tables()
-    T = _QUAD_TABLES
-    nb = bmask.shape[0]
-    m = bmask.view(np.uint64)
-    cnt = np.stack([sum(((m & T[(pp, v, w)][0]) != 0).astype(np.int64) for v in range(2) for w in range(2))
-                    for pp in range(3)]) if nb else np.zeros((3, 0), np.int64)
-    best = np.argmin(cnt, axis=0) if nb else np.zeros(0, np.int64)
-    parts, keys = [], []
-    for pp in range(3):
-        bsel = np.nonzero(best == pp)[0]
-        if bsel.size == 0:
-            continue
-        mb = m[bsel]
-        for v in range(2):
-            for w in range(2):
-                qm, bit, d_of_e, b_of = T[(pp, v, w)]
-                ne = (mb & qm) != 0
-                blk = bsel[ne]
-                if blk.size == 0:
-                    continue
-                mm = mb[ne]
-                q = np.full((blk.shape[0], 16), -1, np.int32)
-                m16 = np.zeros(blk.shape[0], np.int64)
-                for ia in range(4):
-                    for ib in range(4):
-                        m16 |= ((mm >> np.uint64(bit[ia, ib])) & np.uint64(1)).astype(np.int64) << (4 * ia + ib)
-                for ib in range(4):
-                    used = (m16 >> ib) & 0x1111
-                    q[:, ib] = np.where(used != 0, bsrc[blk, b_of[ib]], -1)
-                for e in range(9):
-                    du, dw = e // 3 - 1, e % 3 - 1
-                    em = 0
-                    for ia in range(4):
-                        for ib in range(4):
-                            if ((ia >> 1) & 1) - ((ib >> 1) & 1) == du and (ia & 1) - (ib & 1) == dw:
-                                em |= 1 << (4 * ia + ib)
-                    q[:, 4 + e] = np.where((m16 & em) != 0, btr[blk, d_of_e[e]], -1)
-                q[:, 13] = m16
-                q[:, 14] = 4 * pp + 2 * v + w
-                q[:, 15] = 0
-                parts.append(q)
-                keys.append(blk * 4 + 2 * v + w)
-    if not parts:
-        return np.zeros((0, 16), np.int32), np.zeros(gptr.shape[0], np.int64)
-    q = np.concatenate(parts)
-    k = np.concatenate(keys)
-    o = np.argsort(k, kind="stable")
-    q, k = q[o], k[o]
-    qblk = k // 4
-    qptr = np.searchsorted(qblk, gptr).astype(np.int64)  # block range per group -> quad range
-    return q, qptr
-
-
-def m2l_tiles(order, row_ptr, ent, n_hat: int, n_trans: int, u_max: int, k_max: int, e_max: int = 1 << 30) -> dict:
-    """Host tiling of M2L rows for the tile kernel (defmm_m2l_tiles, native):
-    tiles of consecutive rows of ``order`` whose operand union (spectra +
-    derived symbols) has <= u_max entries and <= k_max rows."""
-    import ctypes as C
-
-    lib = _lib.load()
-    ptr = np.ascontiguousarray(row_ptr, np.int64)
-    ent = np.ascontiguousarray(ent, np.int32)
-    order = np.ascontiguousarray(order, np.int64)
-    n = order.shape[0]
-    n_ev = int((ptr[order + 1] - ptr[order]).sum()) if n else 0
-    tile_ptr = np.zeros(n + 1, np.int64)
-    tile_rows = np.zeros(max(n, 1), np.int64)
-    op_ptr = np.zeros(n + 1, np.int64)
-    ops = np.zeros(max(2 * n_ev, 1), np.int32)
-    ev_ptr = np.zeros(n + 1, np.int64)
-    ev = np.zeros(max(n_ev, 1), np.uint32)
-    counts = np.zeros(5, np.int64)
-
-    def a(x):
-        return x.ctypes.data_as(C.c_void_p)
-
-    _lib.check(lib.defmm_m2l_tiles(n, a(order), a(ptr), a(ent), int(n_hat), int(n_trans), int(u_max), int(k_max),
-                                   int(e_max), a(tile_ptr), a(tile_rows), a(op_ptr), a(ops), a(ev_ptr), a(ev), a(counts)),
-               "defmm_m2l_tiles")
-    nt, nr, no, ne = (int(x) for x in counts[:4])
-    return {"n_tiles": nt, "tile_ptr": tile_ptr[: nt + 1], "rows": tile_rows[:nr], "op_ptr": op_ptr[: nt + 1],
-            "ops": ops[:no], "ev_ptr": ev_ptr[: nr + 1], "ev": ev[:ne], "untiled": int(counts[4])}
-
-
 def m2l_groups(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent, K: int = 2) -> dict:
     """Sibling-group lists of the group M2L (K7 v8, defmm_m2l_group_*, K = 2 or
     4): the rows ``ids`` (indices into ``rows``, the local slots) grouped by
@@ -225,26 +105,14 @@ def _sub_csr(ptr, keep):
 
 # M2L kernel per level for each mode: (dense level, sparse level)
 M2L_MODE_KINDS = {
-    "auto": ("blocked", "rows"), "hybrid_rows": ("blocked", "rows"), "hybrid": ("blocked", "quad"),
-    "rows": ("rows", "rows"), "blocked_all": ("blocked", "blocked"), "quad_all": ("quad", "quad"),
-    "tiles": ("blocked", "tile"), "tiles_all": ("tile", "tile"), "slice_all": ("slice", "slice"),
+    "auto": ("blocked", "rows"), "hybrid_rows": ("blocked", "rows"),
+    "rows": ("rows", "rows"), "blocked_all": ("blocked", "blocked"),
     "pairs": ("blocked", "pair"), "pairs_all": ("pair", "pair"), "quartets": ("blocked", "quartet"),
     "quartets_all": ("quartet", "quartet"), "triples_all": ("triple", "triple"),
 }
-M2L_KERNELS = ("rows", "blocked", "quad", "tile", "slice", "pair", "triple", "quartet")
+M2L_KERNELS = ("rows", "blocked", "pair", "triple", "quartet")
 # events per parent-pair block above which a level counts as dense (blocked kernel)
 BLOCKED_MIN_EVENTS_PER_BLOCK = 32.0
-# "auto": a complex64 sparse level runs the quad kernel when its quads are this
-# full: cfg2 L6 (cube faces, 13.3 events/quad) wins 6% of the M2L; 7-9
-# events/quad (cfg2 L4-5, cfg3) and every complex128 level lose
-# (profiles/r01_summary_v5.md)
-QUAD_MIN_EVENTS_PER_QUAD = 12.0
-# ... and only up to this order: at L = 6 the pair kernel beats the quads on
-# the same cfg2 level (10.2 vs 11.1 ms, profiles/r01_summary_v7.md).  Since
-# the pair kernel keeps three entries in flight it also wins cfg2's planar
-# level 6 at L = 4 (2.445 vs 2.48 ms, r01_summary_v8.md): QUAD_MAX_ORDER = 0
-# takes the quads out of "auto" (they stay selectable per level)
-QUAD_MAX_ORDER = 0
 # "auto": other sparse levels with at least this many rows run the pair kernel
 # (sibling rows merged per source: cfg2 M2L -9%, cfg3 -10%); small levels
 # (cfg1) keep the row kernel (profiles/r01_summary_v7.md)
@@ -276,22 +144,6 @@ def dense_levels(plan, tt, threshold: float = BLOCKED_MIN_EVENTS_PER_BLOCK) -> s
     return {int(lv) for lv in np.unique(blev) if ev[blev == lv].mean() >= threshold}
 
 
-def quad_fill(plan, tt, levels) -> dict:
-    """level -> mean M2L events per in-plane quad of its parent-pair blocks."""
-    blev, _, glev, nblk = block_levels(plan, tt)
-    out = {}
-    for lv in levels:
-        gsel = np.nonzero(glev == lv)[0]
-        if gsel.size == 0:
-            continue
-        bsel = np.nonzero(blev == lv)[0]
-        bptr = np.concatenate([[0], np.cumsum(nblk[gsel])]).astype(np.int64)
-        qd, _ = _quads(plan.blk_src[bsel], plan.blk_trans[bsel], plan.blk_mask[bsel], bptr)
-        if qd.shape[0]:
-            out[int(lv)] = float(np.bitwise_count(qd[:, 13].astype(np.uint64)).mean())
-    return out
-
-
 def p2p_overlap_policy(level_kinds: dict) -> tuple:
     """(p2p_overlap, far_priority) for a plan's M2L level kinds, measured
     (profiles/r01_summary_v9.md): when every M2L level runs the quartet
@@ -305,12 +157,11 @@ def p2p_overlap_policy(level_kinds: dict) -> tuple:
     return "upward", False
 
 
-def m2l_level_kinds(mode: str, dtype: str, levels, dense, fill=None, override=None, env: str = "",
+def m2l_level_kinds(mode: str, dtype: str, levels, dense, override=None, env: str = "",
                     rows_per_level=None, order: int = 4) -> dict:
     """level -> M2L kernel: the mode's (dense, sparse) choice; in "auto" a
-    complex64 sparse level with quad fill >= QUAD_MIN_EVENTS_PER_QUAD runs
-    quads, another sparse level with >= PAIR_MIN_ROWS rows the pair kernel;
-    then the per-level overrides (dict, or "4:quad,6:rows")."""
+    sparse level with >= PAIR_MIN_ROWS rows runs the sibling-group kernel
+    (sibling_kind); then the per-level overrides (dict, or "4:pair,6:rows")."""
     if mode not in M2L_MODE_KINDS:
         raise ValueError(f"unknown M2L mode {mode!r}")
     kd, ks = M2L_MODE_KINDS[mode]
@@ -319,9 +170,7 @@ def m2l_level_kinds(mode: str, dtype: str, levels, dense, fill=None, override=No
         for lv in list(kinds):
             if kinds[lv] != "rows":
                 continue
-            if dtype == "c64" and order <= QUAD_MAX_ORDER and (fill or {}).get(lv, 0.0) >= QUAD_MIN_EVENTS_PER_QUAD:
-                kinds[lv] = "quad"
-            elif (rows_per_level or {}).get(lv, 0) >= PAIR_MIN_ROWS:
+            if (rows_per_level or {}).get(lv, 0) >= PAIR_MIN_ROWS:
                 kinds[lv] = sibling_kind(dtype, order)
     over = dict(override or {})
     for tok in filter(None, env.split(",")):
@@ -462,10 +311,6 @@ class FmmPlan:
         self.blk_trans = _dev(h["blk_trans"].reshape(-1), i32, d)
         self.blk_mask = _dev(h["blk_mask"], i64, d)
         self.blk_kind = _dev(h["blk_kind"], torch.int8, d)
-        self.n_qgroups = int(h["qd_rows"].shape[0])
-        self.qd_ptr = _dev(h["qd_ptr"], i64, d)
-        self.qd_rows = _dev(h["qd_rows"].reshape(-1), i64, d)
-        self.quads = _dev(h["quads"].reshape(-1), i32, d)
         self.sib_groups = []  # (K, n, slots, ptr, entries) of the pair / quartet kernels
         for kind in ("pair", "triple", "quartet"):
             gr = h[kind]
@@ -473,21 +318,6 @@ class FmmPlan:
                 self.sib_groups.append((gr["K"], int(gr["n"]), _dev(gr["grp_slot"], i64, d),
                                         _dev(gr["grp_ptr"], i64, d), _dev(gr["ent"].reshape(-1), i32, d)))
         self.n_pairs = sum(x[1] for x in self.sib_groups)
-        tl = h["tl"]
-        self.n_tiles = int(tl["n_tiles"]) if tl is not None else 0
-        if self.n_tiles:
-            self.tl_ptr = _dev(tl["tile_ptr"], i64, d)
-            self.tl_op_ptr = _dev(tl["op_ptr"], i64, d)
-            self.tl_ops = _dev(tl["ops"], i32, d)
-            self.tl_ev_ptr = _dev(tl["ev_ptr"], i64, d)
-            self.tl_ev = _dev(tl["ev"].view(np.int32), i32, d)
-            self.tl_base = int(tl["lhat_base"])
-        sl = h["slice"]
-        self.n_slice_batch = int(sl["n_batch"])
-        self.sl_batch = _dev(sl["batch"].reshape(-1), i32, d)
-        self.sl_seg = _dev(sl["seg"], i64, d)
-        self.sl_ent = _dev(sl["ent"].reshape(-1), i32, d)
-        self.sl_ngs, self.sl_row_base = int(sl["ngs"]), int(sl["row_base"])
         # downward
         self.l2l = []
         for lev, outs, octant, ptr, src, sdir in h["l2l"]:
@@ -519,11 +349,6 @@ class FmmPlan:
         self.local = torch.empty((max(p.n_local, 1), self.L3), dtype=cd, device=d)
         self.lhat = torch.empty((max(int(self.bk_rows.shape[0]), 1), self.SS), dtype=cd, device=d)
         self.near = torch.empty(self.n_tgt, dtype=cd, device=d)
-        # late near field: with the P2P still running beside the M2L, the L2P
-        # starts from a zero near field and add_near folds the P2P in after
-        # the join (DEFMM_LATE_NEAR=1; measured slower on cfg2: 3.304 vs 3.282 ms)
-        self.late_near = os.environ.get("DEFMM_LATE_NEAR", "0") == "1"
-        self.zero_near = torch.zeros(self.n_tgt, dtype=cd, device=d)
         self.p2p_partial = torch.empty(max(self._partial_size, 1), dtype=cd, device=d)
         self.q = torch.zeros(self.n_src, dtype=cd, device=d)
         self.out = torch.empty(self.n_tgt, dtype=cd, device=d)
@@ -537,16 +362,6 @@ class FmmPlan:
         # the upward pass and the M2L (optionally on a persistent grid of
         # p2p_grid CTAs).  far_priority: far field on the high-priority stream.
         self.p2p_overlap, self.far_priority = p2p_overlap_policy(getattr(self, "level_kinds", {}))
-        # sibling-group M2L fed by bulk copies into a shared-memory ring (K7 v9)
-        # instead of per-thread global loads; DEFMM_GROUP_TMA=0/1 overrides
-        self.group_tma = os.environ.get("DEFMM_GROUP_TMA", "0") == "1"
-        # sibling groups claimed per SM from contiguous chunks (K7 v10): CTAs
-        # sharing an SM work on neighbouring groups -> L1 reuse of spectra and
-        # symbols; DEFMM_GROUP_SMQ=0/1 overrides
-        self.group_smq = os.environ.get("DEFMM_GROUP_SMQ", "0") == "1"
-        self.smq_chunk = int(os.environ.get("DEFMM_GROUP_SMQ_CHUNK", "8"))
-        self.n_sm = torch.cuda.get_device_properties(d).multi_processor_count
-        self.qcnt = torch.zeros(self.n_sm, dtype=torch.int32, device=d)
         self.p2p_grid = 0
         # c64 near-field coordinates: hi/lo float pairs where the order's
         # accuracy bar needs them (defmm_b200.h, K1)
@@ -581,8 +396,7 @@ class FmmPlan:
         run the blocked kernel (K7 v3, operand reuse in registers), sparse
         (surface-like) levels the row kernel by default (their blocks would be
         mostly predicated-off pairs) -- profiles/r01_summary_v3.md, v4.md.
-        lhat rows: grouped (blocked + quad) rows, then slice rows, then tile
-        rows (one F2L launch over all of them)."""
+        lhat rows: the blocked rows (one F2L launch over all of them)."""
         h = self._host_lists_all()
         p, tt = self.plan, self.tt
         rows = h["rows"]
@@ -590,14 +404,10 @@ class FmmPlan:
         # density per level from the full plan (identical on every rank)
         dense = dense_levels(p, tt, self.BLOCKED_MIN_EVENTS_PER_BLOCK)
         levels = np.unique(rlev)
-        fill = None
-        if self.m2l_variant_default == "auto" and self.config.dtype == "c64" and self.L <= QUAD_MAX_ORDER:
-            fill = quad_fill(p, tt, [lv for lv in levels if int(lv) not in dense])
-        self.quad_fill = fill
         # rows per level from the full plan (identical on every rank)
         flev = tt.level[p.l_cell[p.m2l_row_slot]] if p.m2l_row_slot.size else np.zeros(0, np.int64)
         rpl = {int(lv): int(c) for lv, c in zip(*np.unique(flev, return_counts=True))}
-        kinds = m2l_level_kinds(self.m2l_variant_default, self.config.dtype, levels, dense, fill,
+        kinds = m2l_level_kinds(self.m2l_variant_default, self.config.dtype, levels, dense,
                                 self.m2l_level_override, os.environ.get("DEFMM_M2L_LEVELS", ""), rpl, self.L)
         self.level_kinds = kinds
         rkind = np.array([kinds[int(lv)] for lv in rlev], dtype=object) if rows.size else np.zeros(0, object)
@@ -608,17 +418,6 @@ class FmmPlan:
 
         # row kernel
         is_rows = pick("rows")
-        # tiles (rows whose own operands exceed a tile fall back to the row kernel)
-        h["tl"] = None
-        is_tile = pick("tile")
-        if is_tile.any():
-            t_ids = np.nonzero(is_tile)[0]
-            slot = rows[t_ids]
-            order = t_ids[np.lexsort((p.l_cell[slot], p.l_dir[slot], rlev[t_ids]))]
-            tl = self._tile_lists(order, h)
-            h["tl"] = tl
-            is_rows = is_rows.copy()
-            is_rows[np.setdiff1d(t_ids, tl["rows"])] = True
         _, rptr, rsel = _sub_csr(h["row_ptr"], is_rows)
         h["rk_rows"], h["rk_ptr"], h["rk_ent"] = rows[is_rows], rptr, h["ent"][rsel]
         # sibling pairs (K7 v8)
@@ -628,111 +427,21 @@ class FmmPlan:
                                  tt.level, tt.parent, 3)
         h["quartet"] = m2l_groups(np.nonzero(pick("quartet"))[0], rows, h["row_ptr"], h["ent"], p.l_cell, p.l_dir,
                                   tt.level, tt.parent, 4)
-        # grouped rows (blocked + quad)
-        is_grp = pick("blocked", "quad")
+        # blocked rows = the lhat rows
+        is_grp = pick("blocked")
         grp_rows = rows[is_grp]
-        # slice rows
-        is_slice = pick("slice")
-        n_grp = int(grp_rows.shape[0])
-        if is_slice.any():
-            _, sptr, ssel = _sub_csr(h["row_ptr"], is_slice)
-            h["slice"] = self._slice_lists(sptr, h["ent"][ssel], rlev[is_slice], n_grp)
-        else:
-            h["slice"] = self._slice_lists(np.zeros(1, np.int64), np.zeros((0, 2), np.int32), z, 0)
-        # lhat rows: grouped, slice, tile
-        parts = [grp_rows, rows[is_slice]]
-        if h["tl"] is not None:
-            h["tl"]["lhat_base"] = n_grp + int(is_slice.sum())
-            parts.append(rows[h["tl"]["rows"]])
-        h["bk_rows"] = np.concatenate(parts) if parts else z
-        # groups of grouped levels, rows renumbered into lhat
+        h["bk_rows"] = grp_rows
+        # groups of blocked levels, rows renumbered into lhat
         gr = h["grp_rows"]
         gr_slots = np.where(gr >= 0, rows[np.maximum(gr, 0)] if rows.size else -1, -1)
         gid = _rows_to_ids(gr_slots, grp_rows)
         gkeep = np.any(gid >= 0, axis=1)
         _, gptr, bsel = _sub_csr(h["grp_ptr"], gkeep)
-        grows = gid[gkeep]
-        bsrc, btr, bmask, bkind = h["blk_src"][bsel], h["blk_trans"][bsel], h["blk_mask"][bsel], h["blk_kind"][bsel]
-        # groups of quad levels -> quad kernel, the others -> blocked kernel
-        first = np.where(grows >= 0, grows, np.iinfo(np.int64).max).min(axis=1) if grows.size else z
-        glev = tt.level[p.l_cell[grp_rows[first]]] if grows.size else z
-        gq = np.array([kinds[int(lv)] == "quad" for lv in glev], bool) if grows.size else np.zeros(0, bool)
-        if gq.any():
-            _, dptr, dsel = _sub_csr(gptr, ~gq)
-            _, qgptr, qsel = _sub_csr(gptr, gq)
-            quads, qptr = _quads(bsrc[qsel], btr[qsel], bmask[qsel], qgptr)
-            h["qd_ptr"], h["qd_rows"], h["quads"] = qptr, grows[gq], quads
-            gptr, grows = dptr, grows[~gq]
-            bsrc, btr, bmask, bkind = bsrc[dsel], btr[dsel], bmask[dsel], bkind[dsel]
-        else:
-            h["qd_ptr"], h["qd_rows"], h["quads"] = np.zeros(1, np.int64), np.zeros((0, 8), np.int64), \
-                np.zeros((0, 16), np.int32)
-        h["grp_ptr"], h["grp_rows"] = gptr, grows
-        h["blk_src"], h["blk_trans"], h["blk_mask"], h["blk_kind"] = bsrc, btr, bmask, bkind
+        h["grp_ptr"], h["grp_rows"] = gptr, gid[gkeep]
+        h["blk_src"], h["blk_trans"], h["blk_mask"], h["blk_kind"] = (
+            h["blk_src"][bsel], h["blk_trans"][bsel], h["blk_mask"][bsel], h["blk_kind"][bsel])
         self.dense_levels = sorted(lv for lv, k in kinds.items() if k == "blocked")
         return h
-
-    # tile kernel (K7 v6): operand slices of 128 B (c64: 16 x 8 B, c128:
-    # 8 x 16 B), double-buffered: 2 x 352 x 128 B + 4096 events ~ 107 KB of
-    # shared memory -> 2 CTAs per SM
-    TILE_U_MAX = 352
-    TILE_E_MAX = 4096
-
-    def _tile_lists(self, order, h) -> dict:
-        """Greedy operand-union tiles over the rows ``order`` (indices into
-        h["rows"], sorted (level, key, Morton target)): defmm_m2l_tiles."""
-        return m2l_tiles(order, h["row_ptr"], h["ent"], int(h["hat_slot"].shape[0]),
-                         int(self.plan.trans_canon.shape[0]), int(self.TILE_U_MAX),
-                         16 if self.config.dtype == "c64" else 32, int(self.TILE_E_MAX))
-
-    # rows per slice-kernel batch: enough events per batch to amortise the
-    # shared-memory symbol loads (G symbols per group), one row per warp at least
-    SLICE_MIN_BATCH_ROWS = 16
-    SLICE_MAX_BATCH_ROWS = 512
-
-    def _slice_lists(self, rptr, ent, rlev, lhat_base) -> dict:
-        """Lists of the slice M2L (K7 v4, defmm_m2l_slice_*): per row, events
-        sorted by canonical-symbol group (G per group, the level's canonical
-        symbols are contiguous in the symbol table); entries {spectrum,
-        (canonical-in-group << 6) | rotation}; seg[r, g] = first event of group
-        g; batches of rows of one level {row0, row1, first symbol, count}."""
-        p = self.plan
-        n = int(rlev.shape[0])
-        G = int(_lib.load().defmm_slice_group(int(self.config.dtype == "c64")))
-        if n == 0:
-            return {"n_batch": 0, "batch": np.zeros((0, 4), np.int32), "seg": np.zeros(1, np.int64),
-                    "ent": np.zeros((0, 2), np.int32), "ngs": 1, "row_base": lhat_base}
-        cnt = np.diff(rptr)
-        lev_lo = np.searchsorted(p.sym_level, rlev, side="left")
-        lev_nc = np.searchsorted(p.sym_level, rlev, side="right") - lev_lo
-        ngs = int(max(1, (-(-lev_nc // G)).max()))
-        tid = ent[:, 1].astype(np.int64)
-        clocal = p.trans_canon[tid].astype(np.int64) - np.repeat(lev_lo, cnt)
-        grp = clocal // G
-        meta = ((clocal % G) << 6) | p.trans_rid[tid].astype(np.int64)
-        key = np.repeat(np.arange(n, dtype=np.int64), cnt) * ngs + grp
-        if ngs > 1:
-            order = np.argsort(key, kind="stable")
-            key, meta, src = key[order], meta[order], ent[order, 0]
-        else:
-            src = ent[:, 0]
-        sent = np.empty((key.shape[0], 2), np.int32)
-        sent[:, 0] = src
-        sent[:, 1] = meta
-        probe = (np.arange(n, dtype=np.int64)[:, None] * ngs + np.arange(ngs + 1)[None, :]).reshape(-1)
-        seg = np.searchsorted(key, probe, side="left").astype(np.int64)
-        # batches: rows of one level (contiguous: rows are slot-sorted, level-major)
-        batches = []
-        brk = np.nonzero(np.diff(rlev))[0] + 1
-        for a, b in zip(np.concatenate([[0], brk]), np.concatenate([brk, [n]])):
-            ev_row = max(float(cnt[a:b].mean()), 1.0)
-            ngl = -(-int(lev_nc[a]) // G)
-            br = int(np.clip(16 * G * ngl / ev_row, self.SLICE_MIN_BATCH_ROWS, self.SLICE_MAX_BATCH_ROWS))
-            br = -(-br // 16) * 16
-            for r0 in range(int(a), int(b), br):
-                batches.append((lhat_base + r0, lhat_base + min(int(b), r0 + br), int(lev_lo[a]), int(lev_nc[a])))
-        return {"n_batch": len(batches), "batch": np.asarray(batches, np.int32).reshape(-1, 4), "seg": seg,
-                "ent": sent, "ngs": ngs, "row_base": lhat_base}
 
     def _host_lists_all(self) -> dict:
         """The plan's lists, restricted to this rank's chunk when sharded
@@ -921,23 +630,10 @@ class FmmPlan:
             _lib.call(self._op("m2l_rows"), L, self.rk_rows.shape[0], self.rk_rows, self.rk_ptr, self.rk_ent,
                       self.hat, self.sym_derived, self.local, sh)
             for K, ng, gslot, gptr, gent in self.sib_groups:
-                if self.group_smq:
-                    _lib.call(self._op("m2l_group_smq"), L, K, ng, gslot, gptr, gent, self.hat, self.sym_derived,
-                              self.local, self.n_sm, self.smq_chunk, self.qcnt, sh)
-                else:
-                    _lib.call(self._op("m2l_group_tma" if self.group_tma else "m2l_group"), L, K, ng, gslot, gptr,
-                              gent, self.hat, self.sym_derived, self.local, sh)
+                _lib.call(self._op("m2l_group"), L, K, ng, gslot, gptr, gent, self.hat, self.sym_derived, self.local,
+                          sh)
             _lib.call(self._op("m2l_blocked"), L, self.n_groups, self.grp_ptr, self.grp_rows, self.blk_src,
                       self.blk_trans, self.blk_mask, self.blk_kind, self.hat, self.sym_derived, self.lhat, sh)
-            _lib.call(self._op("m2l_quad"), L, self.n_qgroups, self.qd_ptr, self.qd_rows, self.quads, self.hat,
-                      self.sym_derived, self.lhat, sh)
-            if self.n_tiles:
-                _lib.call(self._op("m2l_tile"), L, self.n_tiles, self.tl_ptr, self.tl_op_ptr, self.tl_ops,
-                          self.tl_ev_ptr, self.tl_ev, self.tl_base, int(self.TILE_U_MAX),
-                          int(self.TILE_E_MAX), self.hat,
-                          self.sym_derived, self.lhat, sh)
-            _lib.call(self._op("m2l_slice"), L, self.n_slice_batch, self.sl_batch, self.sl_row_base, self.sl_seg,
-                      self.sl_ngs, self.sl_ent, self.hat, self.sym, self.lhat, sh)
             _lib.call(self._op("f2l_rows"), L, self.bk_rows.shape[0], self.bk_rows, self.lhat, self.local, sh)
         elif self.m2l_variant == "derived":
             _lib.call(self._op("m2l_rows"), L, self.row_slot.shape[0], self.row_slot, self.row_ptr,
@@ -962,17 +658,12 @@ class FmmPlan:
         for son_beta, outs, octant, ptr, src, sdir, n in self.l2l:
             _lib.call(self._op("l2l"), L, n, outs, octant, ptr, src, sdir, son_beta, self.dirs, kappa,
                       self.local, sh)
-        late = self.late_near and self.shard is None and self.p2p_overlap != "upward"
-        if not late:
-            stream.wait_stream(self.side_stream)
+        stream.wait_stream(self.side_stream)
         if self.shard is not None:
             out.zero_()  # this rank writes only its own targets
         _lib.call(self._op("l2p"), L, self.n_leaves, self.leaf_cell, self.leaf_lo, self.leaf_hi, self.slot_dir,
                   tg["start"], tg["stop"], tg["alpha"], tg["level"], tg["beta"], self.dirs, *self.t_xyz, kappa,
-                  self.local, self.zero_near if late else self.near, self.t_perm, out, sh)
-        if late:  # P2P joined after the L2P: out[perm] += near
-            stream.wait_stream(self.side_stream)
-            _lib.call(self._op("add_near"), self.n_tgt, self.t_perm, self.near, out, sh)
+                  self.local, self.near, self.t_perm, out, sh)
         if stage_events is not None:
             e = ev()
             e.record(stream)
@@ -1019,14 +710,13 @@ class FmmPlan:
             return sorted(l for l, x in kinds.items() if x == k)
 
         out = []
-        gk = "m2l_group_tma_kernel" if self.group_tma and not self.group_smq else "m2l_group_kernel"
+        gk = "m2l_group_kernel"
         for n, name, k in ((self.rk_rows.shape[0], "m2l_rows_kernel", "rows"),
                            (sum(x[1] for x in self.sib_groups if x[0] == 2), f"{gk}<2>", "pair"),
                            (sum(x[1] for x in self.sib_groups if x[0] == 3), f"{gk}<3>", "triple"),
                            (sum(x[1] for x in self.sib_groups if x[0] == 4), f"{gk}<4>", "quartet"),
                            (self.n_groups, "m2l_blocked_kernel", "blocked"),
-                           (self.n_qgroups, "m2l_quad_kernel", "quad"), (self.n_tiles, "m2l_tile_kernel", "tile"),
-                           (self.n_slice_batch, "m2l_slice_kernel", "slice"), (self.bk_rows.shape[0], "f2l_rows_kernel", None)):
+                           (self.bk_rows.shape[0], "f2l_rows_kernel", None)):
             if n:
                 out.append(f"{name}<{R}, {self.L}>" + (f" (levels {lv(k)})" if k is not None else ""))
         return out
@@ -1036,12 +726,11 @@ class FmmPlan:
         """Kernels of one matvec: p2p (+ split reduce), p2m, m2m per level, m2f,
         the M2L kernels with work, l2l per level, l2p."""
         if self.m2l_variant == "hybrid":
-            m2l = len(self.sib_groups) + sum(int(n > 0) for n in (self.rk_rows.shape[0], self.n_groups, self.n_qgroups, self.n_tiles,
-                                           self.n_slice_batch, self.bk_rows.shape[0]))
+            m2l = len(self.sib_groups) + sum(int(n > 0) for n in (self.rk_rows.shape[0], self.n_groups,
+                                                                   self.bk_rows.shape[0]))
         else:
             m2l = 1
-        late = self.late_near and self.shard is None and self.p2p_overlap != "upward"
-        return 4 + (1 if self.n_split else 0) + len(self.m2m) + len(self.l2l) + m2l + int(late)
+        return 4 + (1 if self.n_split else 0) + len(self.m2m) + len(self.l2l) + m2l
 
     def events(self):
         """InteractionEvent list (traversal.py:80-85) with Cell views."""

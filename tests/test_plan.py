@@ -335,7 +335,7 @@ def test_native_traversal_is_independent_of_thread_count(monkeypatch):
 def test_spectral_layout_slices_are_closed_under_the_cube_group(L):
     """Device spectra are stored in orbit order (defmm_spectral_layout); every
     slice of <= 128 positions is a union of orbits of the 48 rotations
-    (fourier.py:90-143), so the slice M2L's canonical symbols stay in-slice."""
+    (fourier.py:90-143)."""
     from paper_2202_04894_b200.fmm import spectral_layout
 
     P = 2 * L - 1
@@ -352,89 +352,13 @@ def test_spectral_layout_slices_are_closed_under_the_cube_group(L):
         assert np.array_equal(slice_of[pos_of[j]], slice_of)
 
 
-@pytest.mark.parametrize("case", ["cubesurf4000", "volume3000"])
-def test_quads_reconstruct_every_block_pair(case):
-    """Quad descriptors (defmm_m2l_quad_*) carry exactly the (group, target
-    child, spectrum, derived symbol) events of the parent-pair blocks."""
-    from paper_2202_04894_b200.fmm import _quads
-
-    def embed2(i, pp, v):
-        return (v << 2) | i if pp == 0 else (((i >> 1) & 1) << 2) | (v << 1) | (i & 1) if pp == 1 else (i << 1) | v
-
-    g = load_case(case)
-    tr, ps, pl = _plan(g)
-    q, qptr = _quads(pl.blk_src, pl.blk_trans, pl.blk_mask, pl.blk_group_ptr)
-    assert qptr[0] == 0 and qptr[-1] == q.shape[0] and np.all(np.diff(qptr) >= 0)
-    qg = np.searchsorted(qptr, np.arange(q.shape[0]), side="right") - 1
-    got = []
-    for k in range(q.shape[0]):
-        code = int(q[k, 14])
-        pp, v = code // 4, (code >> 1) & 1
-        for ia in range(4):
-            for ib in range(4):
-                if (int(q[k, 13]) >> (4 * ia + ib)) & 1:
-                    e = (((ia >> 1) & 1) - ((ib >> 1) & 1) + 1) * 3 + ((ia & 1) - (ib & 1) + 1)
-                    got.append((int(qg[k]), embed2(ia, pp, v), int(q[k, ib]), int(q[k, 4 + e])))
-    bg = np.searchsorted(pl.blk_group_ptr, np.arange(pl.blk_mask.shape[0]), side="right") - 1
-    ref = []
-    for bi in range(pl.blk_mask.shape[0]):
-        m = int(pl.blk_mask[bi])
-        for a in range(8):
-            for b in range(8):
-                if (m >> (8 * a + b)) & 1:
-                    d = ((((a >> 2) & 1) - ((b >> 2) & 1)) + 1) * 9 + ((((a >> 1) & 1) - ((b >> 1) & 1)) + 1) * 3 + \
-                        (((a & 1) - (b & 1)) + 1)
-                    ref.append((int(bg[bi]), a, int(pl.blk_src[bi, b]), int(pl.blk_trans[bi, d])))
-    assert sorted(got) == sorted(ref)
-
-
-@pytest.mark.parametrize("case", ["cubesurf4000", "volume3000", "c1_kd16"])
-@pytest.mark.parametrize("u_max,k_max,e_max", [(768, 16, 1 << 20), (96, 32, 4096), (40, 4, 25)])
-def test_m2l_tiles_reconstruct_every_row(case, u_max, k_max, e_max):
-    """defmm_m2l_tiles (tile kernel lists): every tiled row's packed local
-    events map back to its (spectrum, symbol) entries in order, tile unions
-    hold each operand once within u_max / k_max, and exactly the rows whose
-    own operands exceed u_max are left to the row kernel."""
-    from paper_2202_04894_b200.fmm import m2l_tiles
-
-    _, _, p = _plan(load_case(case))
-    ptr, ent = p.m2l_row_ptr, p.m2l_rows_entries
-    nrows = ptr.shape[0] - 1
-    order = np.lexsort((p.l_cell[p.m2l_row_slot], p.l_dir[p.m2l_row_slot], p.m2l_level))
-    n_hat = int(ent[:, 0].max()) + 1
-    n_trans = int(p.trans_canon.shape[0])
-    t = m2l_tiles(order, ptr, ent, n_hat, n_trans, u_max, k_max, e_max)
-    own = np.array([len(np.unique(ent[ptr[r]:ptr[r + 1], 0])) + len(np.unique(ent[ptr[r]:ptr[r + 1], 1]))
-                    for r in range(nrows)])
-    tiled = set(t["rows"].tolist())
-    assert tiled == {int(r) for r in order if own[r] <= u_max and ptr[r + 1] - ptr[r] <= e_max}
-    assert t["untiled"] == nrows - len(tiled)
-    # tiled rows keep the caller's order
-    pos = {int(r): i for i, r in enumerate(order)}
-    assert all(pos[int(a)] < pos[int(b)] for a, b in zip(t["rows"][:-1], t["rows"][1:]))
-    for k in range(t["n_tiles"]):
-        r0, r1 = t["tile_ptr"][k], t["tile_ptr"][k + 1]
-        ops = t["ops"][t["op_ptr"][k]:t["op_ptr"][k + 1]]
-        assert 1 <= r1 - r0 <= k_max and len(ops) <= u_max
-        assert t["ev_ptr"][r1] - t["ev_ptr"][r0] <= e_max
-        assert len(np.unique(ops)) == len(ops)
-        for j in range(r0, r1):
-            r = t["rows"][j]
-            e = t["ev"][t["ev_ptr"][j]:t["ev_ptr"][j + 1]].astype(np.int64)
-            s_op, t_op = ops[e & 0xFFFF], ops[e >> 16]
-            assert np.all(s_op >= 0) and np.all(t_op < 0)
-            np.testing.assert_array_equal(s_op, ent[ptr[r]:ptr[r + 1], 0])
-            np.testing.assert_array_equal(-1 - t_op, ent[ptr[r]:ptr[r + 1], 1])
-
-
 @pytest.mark.parametrize("case", ["cubesurf4000", "volume3000", "refined3000"])
 def test_m2l_level_policy(case):
     """Per-level M2L kernel choice (fmm.m2l_level_kinds): dense levels ->
-    blocked, sparse -> rows; "auto" moves complex64 sparse levels with full
-    quads (>= QUAD_MIN_EVENTS_PER_QUAD events/quad) to the quad kernel and
-    never complex128 ones; overrides (dict or env string) win; bad names raise."""
-    from paper_2202_04894_b200.fmm import (PAIR_MIN_ROWS, QUAD_MAX_ORDER, QUAD_MIN_EVENTS_PER_QUAD, block_levels,
-                                           dense_levels, m2l_level_kinds, quad_fill, sibling_kind)
+    blocked; "auto" moves sparse levels with >= PAIR_MIN_ROWS rows to the
+    sibling-group kernel (quartets at L <= 4, pairs above), the rest to the
+    row kernel; overrides (dict or env string) win; bad names raise."""
+    from paper_2202_04894_b200.fmm import PAIR_MIN_ROWS, block_levels, dense_levels, m2l_level_kinds, sibling_kind
 
     tr, _, p = _plan(load_case(case))
     levels = np.unique(p.m2l_level)
@@ -442,34 +366,24 @@ def test_m2l_level_policy(case):
     blev, ev, _, _ = block_levels(p, tr)
     for lv in np.unique(blev):
         assert (int(lv) in dense) == (ev[blev == lv].mean() >= 32.0)
-    fill = quad_fill(p, tr, [lv for lv in levels if int(lv) not in dense])
-    assert all(1.0 <= f <= 16.0 for f in fill.values())
     # row counts per level scaled up so that some levels cross PAIR_MIN_ROWS
     rpl = {int(lv): int(c) * (PAIR_MIN_ROWS // 2) for lv, c in zip(*np.unique(p.m2l_level, return_counts=True))}
-    # the quad rule at an order it is enabled for (QUAD_MAX_ORDER may switch it off in "auto")
-    k64 = m2l_level_kinds("auto", "c64", levels, dense, fill, rows_per_level=rpl, order=QUAD_MAX_ORDER)
-    k128 = m2l_level_kinds("auto", "c128", levels, dense, fill, rows_per_level=rpl, order=QUAD_MAX_ORDER)
-    for lv in levels:
-        lv = int(lv)
-        big = rpl.get(lv, 0) >= PAIR_MIN_ROWS
-        if lv in dense:
-            assert k64[lv] == k128[lv] == "blocked"
-        else:
-            sib = sibling_kind("c64", QUAD_MAX_ORDER)
-            assert k128[lv] == (sib if big else "rows")
-            quad = fill.get(lv, 0.0) >= QUAD_MIN_EVENTS_PER_QUAD
-            assert k64[lv] == ("quad" if quad else sib if big else "rows")
+    for order in (4, 6):
+        for dt in ("c64", "c128"):
+            k = m2l_level_kinds("auto", dt, levels, dense, rows_per_level=rpl, order=order)
+            for lv in levels:
+                lv = int(lv)
+                big = rpl.get(lv, 0) >= PAIR_MIN_ROWS
+                assert k[lv] == ("blocked" if lv in dense else sibling_kind(dt, order) if big else "rows")
     assert sibling_kind("c64", 4) == "quartet" and sibling_kind("c128", 6) == "pair"
-    k6 = m2l_level_kinds("auto", "c128", levels, dense, fill, rows_per_level=rpl, order=6)
-    assert all(k6[int(lv)] == (sibling_kind("c128", 6) if rpl.get(int(lv), 0) >= PAIR_MIN_ROWS else "rows")
-               for lv in levels if int(lv) not in dense)
-    assert set(m2l_level_kinds("auto", "c64", levels, dense, fill).values()) <= {"blocked", "rows", "quad"}
-    assert "quad" not in m2l_level_kinds("auto", "c64", levels, dense, fill, rows_per_level=rpl,
-                                         order=QUAD_MAX_ORDER + 1).values()
+    assert set(m2l_level_kinds("auto", "c64", levels, dense).values()) <= {"blocked", "rows"}
     assert set(m2l_level_kinds("hybrid_rows", "c64", levels, dense).values()) <= {"blocked", "rows"}
     lv0 = int(levels[0])
-    assert m2l_level_kinds("auto", "c64", levels, dense, fill, {lv0: "tile"})[lv0] == "tile"
-    assert m2l_level_kinds("rows", "c64", levels, dense, env=f"{lv0}:slice")[lv0] == "slice"
+    assert m2l_level_kinds("auto", "c64", levels, dense, {lv0: "pair"})[lv0] == "pair"
+    assert m2l_level_kinds("rows", "c64", levels, dense, env=f"{lv0}:quartet")[lv0] == "quartet"
+    for gone in ("quad", "tile", "slice"):  # round-1 variants measured slower and removed
+        with pytest.raises(ValueError):
+            m2l_level_kinds("auto", "c64", levels, dense, override={lv0: gone})
     with pytest.raises(ValueError):
         m2l_level_kinds("auto", "c64", levels, dense, override={lv0: "nope"})
     with pytest.raises(ValueError):
