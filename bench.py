@@ -2,17 +2,19 @@
 """Benchmark: FMM matvec throughput (particles/s) on BASELINE config 2.
 
 Default workload = BASELINE.json configs[1] ("cfg2"): N = 1,000,000 points
-uniform on the surface of [-1,1]^3, complex128 charges U(-1,1)+iU(-1,1),
-kappa*D = 128, L = 4, ncrit = 64 (``--workload cfg2_l6`` for L = 6,
-``--workload cfg1`` for the small sphere).  A step is one matvec
-(upward + M2L || P2P + downward) with the plan (tree + lists + symbols)
-already resident, exactly the reference's "matvec" stages.
+uniform on the surface of [-1,1]^3, charges U(-1,1)+iU(-1,1), kappa*D = 128,
+L = 4, ncrit = 64, complex64 storage (the line also carries the complex128
+run of the same lists under "c128").  A step is one matvec (upward + M2L ||
+P2P + downward) with the plan (tree + lists + symbols) resident, exactly the
+reference's "matvec" stages.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2] [--impl reference]
 
-Prints ONE JSON line (rank 0).  ``--impl reference`` times the CPU oracle
-(numpy restatement of the reference, oracle/defmm_oracle.py) on a bounded
-sample of the same workload.
+``--gpus N`` (N > 1) without a torchrun environment re-launches itself under
+``torch.distributed.run`` (one rank per GPU, NCCL, 127.0.0.1).  Rank 0 prints
+ONE JSON line.  ``--impl reference`` times the reference's matvec on the host
+CPU (oracle/cpu_matvec.py: the numpy restatement of helmfmm's matvec, the
+full-size workload, complex128, all host cores).
 """
 
 from __future__ import annotations
@@ -20,6 +22,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import time
@@ -30,12 +33,15 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "particles/s per FMM matvec"
-# the reference's own rel-L2 error vs direct summation on the 1000 check targets
-# (tests/golden/ref_*.npz for cfg1/cfg2, SURVEY.md §8(d) for cfg3/cfg5 whose
-# plan counts equal the survey's reference run)
-_EPS_REF = {"cfg1": 4.1631412940687715e-3, "cfg2": 1.0386568720063353e-2, "cfg2_l6": 3.0746517491878436e-4,
-            "cfg3": 1.640e-3, "cfg5": 1.193e-2}
 UNIT = "particles/s"
+# the reference's own rel-L2 error vs direct summation on the 1000 check
+# targets (tests/golden/ref_*.npz: the reference run on these workloads)
+_EPS_REF_FILE = {"cfg1": "ref_cfg1.npz", "cfg2": "ref_cfg2.npz", "cfg2_l6": "ref_cfg2_L6.npz",
+                 "cfg3": "ref_cfg3.npz", "cfg5": "ref_cfg5.npz", "cfg5_l6": "ref_cfg5_L6.npz",
+                 "cfg5_l8": "ref_cfg5_L8.npz", "cfg4": "ref_cfg4.npz"}
+# what each storage type computes in (include/defmm_b200.h)
+_DTYPE_LABEL = {"c64": "c64: f32 P2M/M2M/M2F/M2L/L2L/P2P, f64 F2L/L2P",
+                "c128": "c128: f64 throughout"}
 
 
 def _args():
@@ -45,10 +51,11 @@ def _args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="cfg2")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--cpu-sample", type=int, default=20000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="only warmup + steps eager matvecs, no other measurement (for ncu launch lists)")
+    ap.add_argument("--cpu-parts", type=int, default=16, help="cpu_baseline: one core runs 1 of this many chunks")
     ap.add_argument("--no-secondary", action="store_true", help="skip the other-precision run of the same lists")
-    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of the CUDA graph")
     ap.add_argument("--dtype", default=None, choices=[None, "c128", "c64"], help="override the workload dtype")
     ap.add_argument("--p2p-overlap", default=None, choices=[None, "upward", "m2m", "m2l", "full"])
     ap.add_argument("--p2p-grid", type=int, default=None, help="persistent P2P grid (CTAs; 0 = one per item)")
@@ -56,9 +63,8 @@ def _args():
     ap.add_argument("--exchange", default="halo", choices=["halo", "allreduce"],
                     help="N > 1 multipole exchange: halo (span all-reduce + all_to_all) or a full all-reduce")
     ap.add_argument("--m2l-levels", default="auto",
-                    choices=["auto", "hybrid", "hybrid_rows", "blocked_all", "rows", "slice_all", "quad_all", "tiles",
-                             "tiles_all", "pairs", "pairs_all", "quartets", "quartets_all"])
-    ap.add_argument("--m2l", default=None, help="M2L kernel variant (hybrid | derived | canonical)")
+                    choices=["auto", "hybrid_rows", "blocked_all", "rows", "pairs", "pairs_all", "quartets",
+                             "quartets_all", "triples_all"])
     return ap.parse_args()
 
 
@@ -76,21 +82,31 @@ def _workload_desc(w, n, dtype=None):
     }
 
 
-def _cpu_oracle_sample(name, n_sample):
-    """Oracle matvec on the first n_sample points of the workload (same kappa)."""
-    from oracle import defmm_oracle as O
-    from paper_2202_04894_b200.workloads import WORKLOADS, kappa_for, make_charges, make_points
+def _golden(name):
+    f = _EPS_REF_FILE.get(name)
+    if f is None or not os.path.exists(os.path.join(ROOT, "tests", "golden", f)):
+        return None
+    return np.load(os.path.join(ROOT, "tests", "golden", f))
 
-    w = WORKLOADS[name]
-    pts = make_points(w.kind, w.n, 0)
-    kappa = kappa_for(pts, w.kappa_d)
-    sub = np.ascontiguousarray(pts[:n_sample])
-    q = make_charges(w.n, 1)[:n_sample]
-    from threadpoolctl import threadpool_limits
 
-    with threadpool_limits(limits=1):  # one core: "cores": 1 in the JSON line
-        _, counts, _, tm, _ = O.run(sub, q, order=w.order, ncrit=w.ncrit, kappa=kappa)
-    return n_sample / tm["matvec"], tm, counts
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _spawn_ranks(args) -> int:
+    """--gpus N > 1 outside torchrun: re-launch this script as N ranks (NCCL
+    communicator init lines on stderr via NCCL_DEBUG=INFO, subsystem INIT)."""
+    env = dict(os.environ, NCCL_DEBUG=os.environ.get("NCCL_DEBUG", "INFO"),
+               NCCL_DEBUG_SUBSYS=os.environ.get("NCCL_DEBUG_SUBSYS", "INIT"))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
+# ----------------------------------------------------------------------------
+# measurement helpers
 
 
 class _Clocks:
@@ -142,20 +158,26 @@ class _Clocks:
         }
 
 
-def _ncu_traffic(key):
-    """DRAM read+write bytes of the M2L stage kernels of one matvec, from the
-    committed ncu launch list of the same workload (profiles/r01_m2l_traffic.json,
-    written by tools/ncu_to_json.py from tools/profile_gpu.sh), or None."""
+def _profile_json(name, key):
+    """An entry of a committed ncu summary under profiles/ (or None)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_m2l_traffic.json")) as fh:
-            return float(json.load(fh)[key]["dram_bytes"])
+        with open(os.path.join(ROOT, "profiles", name)) as fh:
+            return json.load(fh)[key]
     except (OSError, KeyError, ValueError, TypeError):
         return None
 
 
+def _measured_peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
 def _fma_peaks(dev):
-    """FP32 / FP64 FMA peaks of this GPU (TFLOP/s), measured with
-    defmm_fma_peak (8 independent FMA chains per thread, no memory traffic)."""
+    """FP32 / FP64 FMA peaks of this GPU (TFLOP/s): defmm_fma_peak, 8
+    independent FMA chains per thread, no memory traffic."""
     import torch
 
     from paper_2202_04894_b200 import _lib
@@ -163,8 +185,7 @@ def _fma_peaks(dev):
     lib = _lib.load()
     out = torch.zeros(1, dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
-    sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    threads = 4 * sms * 256
+    threads = 4 * torch.cuda.get_device_properties(dev).multi_processor_count * 256
     res = {}
     for fp64, iters in ((0, 40000), (1, 20000)):
         _lib.check(lib.defmm_fma_peak(fp64, 100, out.data_ptr(), stream.cuda_stream), "defmm_fma_peak")
@@ -177,106 +198,35 @@ def _fma_peaks(dev):
     return res
 
 
-def _ncu_m2l(key):
-    """L1/L2 throughput of the dominant M2L kernel from its committed ncu
-    capture (profiles/r01_m2l_ncu.json): the physical bound behind frac > 1."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_m2l_ncu.json")) as fh:
-            return json.load(fh)[key]
-    except (OSError, KeyError, ValueError):
-        return None
+def _l2_stream_peak(dev, sm_mhz):
+    """L2 -> SM streaming rate of this GPU (defmm_l2_stream: LDG.128.cg over
+    a 32 MiB L2-resident buffer, all SMs); best of a few CTA counts."""
+    import torch
 
+    from paper_2202_04894_b200 import _lib
 
-def _ncu_pipe(key):
-    """FP-pipe utilisation of the P2P kernel from the committed ncu capture
-    (profiles/r01_p2p_pipes.json), or None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_p2p_pipes.json")) as fh:
-            return json.load(fh)[key]
-    except (OSError, KeyError, ValueError):
-        return None
-
-
-def _measured_peak_hbm():
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            return float(json.load(fh)["hbm_gbs"]), "measured"
-    except (OSError, KeyError, ValueError):
-        return 6650.0, "fallback"
-
-
-def _oracle_chunk(job):
-    """One oracle matvec (the reference's algorithm, complex128) on a chunk of
-    the workload's points -- a worker of the reference arm's process pool."""
-    from oracle import defmm_oracle as O
-
-    pts, q, kappa, order, ncrit = job
-    t0 = time.perf_counter()
-    _, _, _, tm, _ = O.run(pts, q, order=order, ncrit=ncrit, kappa=kappa)
-    return pts.shape[0], tm["matvec"], time.perf_counter() - t0
-
-
-def run_reference(args):
-    """The reference's CPU path on this host: the numpy restatement of helmfmm's
-    matvec (oracle/defmm_oracle.py; the Python reference itself cannot travel
-    to the GPU box), with ALL host cores: each step runs one oracle matvec per
-    core, on disjoint n-point chunks of the workload's points (same kappa, L,
-    ncrit; the reference is single-threaded by design, so cores
-    add throughput by running independent matvecs), n sized so the whole run
-    takes a few minutes.  value = sum of chunk particles / step wall time."""
-    import multiprocessing as mp
-
-    from paper_2202_04894_b200.workloads import WORKLOADS, kappa_for, make_charges, make_points
-
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    w = WORKLOADS[args.workload]
-    n_sample = int(min(max(120.0 / max(args.steps + args.warmup, 1) * 1000.0, 2000), args.cpu_sample))
-    cores = max(1, min(os.cpu_count() or 1, 64, w.n // n_sample))
-    pts = make_points(w.kind, w.n, 0)
-    kappa = kappa_for(pts, w.kappa_d)
-    q = make_charges(w.n, 1)
-    jobs = [(np.ascontiguousarray(pts[k * n_sample:(k + 1) * n_sample]), q[k * n_sample:(k + 1) * n_sample], kappa,
-             w.order, w.ncrit) for k in range(cores)]
-    del pts
-    # spawn (no fork of a process with live BLAS / CUDA threads); one BLAS
-    # thread per worker, the cores are taken by the workers themselves
-    for var in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
-        os.environ[var] = "1"
-    ctx = mp.get_context("spawn")
-    vals, walls = [], []
-    with ctx.Pool(cores) as pool:
-        for i in range(args.warmup + args.steps):
-            t0 = time.perf_counter()
-            res = pool.map(_oracle_chunk, jobs, chunksize=1)
-            wall = time.perf_counter() - t0
-            if i >= args.warmup:
-                walls.append(wall)
-                vals.append(sum(r[0] for r in res) / wall)
-    value = float(np.median(vals))
-    cfg = _workload_desc(w, w.n)
-    sample = (f"{cores} concurrent oracle matvecs (upward + M2L/P2P + downward, complex128), one per core, on "
-              f"disjoint {n_sample}-point chunks of the {w.name} distribution, same kappa/L/ncrit")
-    line = {
-        "impl": "reference",
-        "metric": METRIC,
-        "value": value,
-        "unit": UNIT,
-        "n_gpus": args.gpus,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": 1e3 * float(np.median(walls)),
-        "higher_is_better": True,
-        "scaling": "weak",
-        "vs_baseline": None,
-        "dtype": "f64",
-        "data": "synthetic",
-        "config": cfg,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
+    lib = _lib.load()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    stream = torch.cuda.current_stream(dev)
+    out = torch.zeros(1, dtype=torch.float32, device=dev)
+    best = None
+    for cps in (2, 4):
+        quantum = 4 * cps * sms * 512
+        n_vec = (32 * 1024 * 1024 // 16) // quantum * quantum
+        buf = torch.ones(n_vec * 4, dtype=torch.float32, device=dev)
+        _lib.check(lib.defmm_l2_stream(buf.data_ptr(), n_vec, 2, cps, out.data_ptr(), stream.cuda_stream), "l2")
+        iters = 40
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        _lib.check(lib.defmm_l2_stream(buf.data_ptr(), n_vec, iters, cps, out.data_ptr(), stream.cuda_stream), "l2")
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        gbs = 16.0 * n_vec * iters / (a.elapsed_time(b) * 1e-3) / 1e9
+        if best is None or gbs > best["GB/s"]:
+            best = {"GB/s": gbs, "ctas_per_sm": cps, "buffer_MiB": n_vec * 16 / 2**20}
+    if sm_mhz:
+        best["B_per_clk_at_sm_clock"] = best["GB/s"] * 1e9 / (sm_mhz * 1e6)
+    return best
 
 
 def _measure_graph(plan, steps, warmup, flush, barrier, dist_max):
@@ -304,13 +254,13 @@ def _measure_graph(plan, steps, warmup, flush, barrier, dist_max):
 
 
 def _measure(plan, steps, warmup, flush, barrier, dist_max):
-    """Device-resident matvecs: per-step and per-stage CUDA-event times (ms)."""
+    """Device-resident eager matvecs: per-step and per-stage CUDA-event times (ms)."""
     import torch
 
     dev = plan.device
     stream = torch.cuda.current_stream(dev)
     for _ in range(warmup):
-        plan.apply()
+        plan.apply(out=plan.out)
     barrier()
     tot = {"step": 0.0, "upward": 0.0, "m2l": 0.0, "p2p": 0.0, "downward": 0.0}
     for _ in range(steps):
@@ -354,7 +304,142 @@ def _measure_e2e(plan, q, steps, warmup, flush, barrier, dist_max):
         b.record(stream)
         torch.cuda.synchronize(dev)
         e_ms += a.elapsed_time(b)
-    return dist_max(e_ms / max(steps, 1)), out_host.numpy(), q_host.element_size() * q_host.shape[0]
+    return dist_max(e_ms / max(steps, 1)), out_host.numpy().copy(), q_host.element_size() * q_host.shape[0]
+
+
+def _roofline(plan, iso, workload, dtype, l2peak, sm_mhz):
+    """roofline block of the dominant kernel (the M2L stage, timed alone)."""
+    p = plan.plan
+    L = plan.L
+    P3 = (2 * L - 1) ** 3
+    c = 16 if dtype == "c128" else 8
+    n_m2l = int(p.counts["m2l_events"])
+    rows = int(p.m2l_row_slot.shape[0])
+    alg_bytes = n_m2l * 2 * P3 * c + rows * L**3 * c  # symbol + source spectrum per event, local write
+    t = iso["m2l"] * 1e-3
+    peak, peak_kind = _measured_peak_hbm()
+    achieved = alg_bytes / t / 1e9
+    ncu = _profile_json("r02_m2l_ncu.json", f"{workload}:{dtype}") or {}
+    traffic = ncu.get("dram_bytes")
+    out = {"bound": "hbm", "kernel": "M2L stage: " + " + ".join(plan.m2l_kernels()),
+           "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+           "traffic": traffic, "alg_bytes_per_launch": alg_bytes, "kernel_ms": iso["m2l"],
+           "note": "achieved = SURVEY §8(d) algorithmic bytes (a symbol + a source spectrum streamed per M2L event, "
+                   "no reuse credit, + the local write) / the M2L stage timed alone; frac > 1 means the operands are "
+                   "reused on chip.  dram = ncu DRAM bytes of the same launches over the same time; l2_to_sm = ncu "
+                   "L2->L1 bytes over that time against this box's measured L2->SM streaming rate"}
+    if traffic:
+        out["dram"] = {"bytes": traffic, "achieved_GBs": traffic / t / 1e9, "frac_of_hbm_peak": traffic / t / 1e9 / peak}
+    l2b = ncu.get("l2_to_l1_bytes")
+    if l2b and l2peak:
+        ach = l2b / t / 1e9
+        out["l2_to_sm"] = {"bytes": l2b, "achieved_GBs": ach, "microbench_GBs": l2peak["GB/s"],
+                           "frac_of_microbench": ach / l2peak["GB/s"], "bytes_per_event": l2b / max(n_m2l, 1),
+                           "source": ncu.get("source")}
+    return out
+
+
+def _p2p_roofline(plan, iso, dtype, fpk):
+    pipe = "fp32" if dtype == "c64" else "fp64"
+    pairs = int(plan.plan.counts["p2p_pairs"])
+    tf = 24.0 * pairs / (iso["p2p"] * 1e-3) / 1e12
+    return {"bound": pipe, "achieved": tf, "peak": fpk[pipe], "unit": "TFLOP/s", "frac": tf / fpk[pipe],
+            "flop_per_pair": 24, "pairs": pairs, "kernel_ms": iso["p2p"], "peak_kind": "measured (defmm_fma_peak)",
+            "ncu_pipe_utilisation": _profile_json("r02_p2p_pipes.json", f"{plan.config.dtype}"),
+            "note": "P2P timed alone; frac counts 24 algorithmic flop/pair (SURVEY §8(d)); sincos/rsqrt work is "
+                    "extra issue, the ncu pipe utilisation is the FP-pipe figure"}
+
+
+def _cpu_baseline(workload, parts):
+    """One host core on 1/parts of the full-size workload's matvec
+    (oracle/cpu_matvec.py, run in a fresh process so that its worker pool
+    forks without CUDA state); the plan is built with all cores beforehand."""
+    cmd = [sys.executable, "-m", "oracle.cpu_matvec", "--workload", workload, "--parts", str(parts), "--sample"]
+    try:
+        out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, check=True).stdout
+        return json.loads(out.strip().splitlines()[-1])
+    except (subprocess.SubprocessError, ValueError, IndexError) as exc:
+        return {"value": None, "unit": UNIT, "cores": 1, "kind": "port", "sample": f"failed: {exc}"}
+
+
+# ----------------------------------------------------------------------------
+# arms
+
+
+def run_reference(args):
+    """The reference's CPU path on this host: helmfmm's matvec restated in
+    numpy (oracle/cpu_matvec.py -- the Python reference itself does not
+    travel to the GPU box), on the FULL workload (same N, kappa, L, ncrit),
+    complex128 as the reference computes, one full matvec per step split over
+    all host cores (the plan -- tree, lists, symbols -- built once outside the
+    timed region, like the B200 arm's).  Under torchrun only rank 0 runs."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    from oracle import cpu_matvec as C
+    from paper_2202_04894_b200.workloads import make_workload
+
+    pts, q, kappa, w = make_workload(args.workload)
+    n = pts.shape[0]
+    cores = max(1, min(os.cpu_count() or 1, 128))
+    t0 = time.perf_counter()
+    plan, pool = C.make(pts, q, w.order, w.ncrit, kappa, parts=4 * cores, workers=cores)
+    setup = time.perf_counter() - t0
+    walls = []
+    out = None
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        out = plan.matvec(pool)
+        wall = time.perf_counter() - t0
+        if i >= args.warmup:
+            walls.append(wall)
+    pool.close()
+    step_s = float(np.mean(walls))
+    value = n / step_s
+    g = _golden(args.workload)
+    check = None
+    if g is not None and int(g["order"]) == w.order:
+        s = g["sample"]
+        check = {"rel_l2_vs_reference_golden_1000": float(np.linalg.norm(out[s] - g["pot_sample"]) /
+                                                          np.linalg.norm(g["pot_sample"])),
+                 "counts_equal_reference": plan.counts == {k: v for k, v in json.loads(str(g["counts"])).items()
+                                                           if k != "translations"}}
+    sample = (f"one full {w.name} matvec per step (N={n}, complex128, upward + M2L/P2P + downward) split over "
+              f"{cores} processes ({4 * cores} Morton chunks); plan built once outside the timed region in "
+              f"{setup:.1f} s")
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * step_s,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "c128: f64 throughout",
+        "data": "synthetic",
+        "config": _workload_desc(w, n),
+        "same_config": True,
+        "counts": plan.counts,
+        "check": check,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _dtype_run(plan, q, args, flush, barrier, dist_max, world):
+    """Every timing of one plan: graph replay (N = 1), eager stages, e2e
+    through the public API, and each dominant kernel alone."""
+    st = _measure(plan, args.steps, args.warmup, flush, barrier, dist_max)
+    graph_ms = None
+    if world == 1:
+        graph_ms = _measure_graph(plan, args.steps, args.warmup, flush, barrier, dist_max)
+    e_step, pot, qbytes = _measure_e2e(plan, q, args.steps, args.warmup, flush, barrier, dist_max)
+    iso = plan.time_isolated(reps=max(3, min(args.steps, 10)), flush=flush) if world == 1 else None
+    return {"st": st, "graph_ms": graph_ms, "e2e_ms": e_step, "pot": pot, "qbytes": qbytes, "iso": iso}
 
 
 def run_b200(args):
@@ -368,10 +453,10 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        dist.init_process_group("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
         if world > 1:
@@ -395,136 +480,119 @@ def run_b200(args):
         dist.all_reduce(torch.view_as_real(t))
 
     shard = (rank, world) if world > 1 else None
-    # N > 1: halo exchange (span all-reduce + all_to_all of the read multipoles, parallel.py)
     ar = allreduce if (shard and args.exchange == "allreduce") else None
     t0 = time.perf_counter()
     plan = FmmPlan(pts, None, cfg, device=dev, charges=q, shard=shard, allreduce=ar, m2l=args.m2l_levels)
     setup_s = time.perf_counter() - t0
-    if args.m2l:
-        plan.m2l_variant = args.m2l
-    if args.p2p_overlap:
-        plan.p2p_overlap = args.p2p_overlap
-    if args.p2p_grid is not None:
-        plan.p2p_grid = args.p2p_grid
-    if args.far_priority is not None:
-        plan.far_priority = bool(args.far_priority)
+
+    def knobs(pl):
+        if args.p2p_overlap:
+            pl.p2p_overlap = args.p2p_overlap
+        if args.p2p_grid is not None:
+            pl.p2p_grid = args.p2p_grid
+        if args.far_priority is not None:
+            pl.far_priority = bool(args.far_priority)
+
+    knobs(plan)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    if args.profile:
+        for _ in range(args.warmup + args.steps):
+            plan.apply(out=plan.out)
+        torch.cuda.synchronize(dev)
+        return
 
     clocks = _Clocks(local)
-    st = _measure(plan, args.steps, args.warmup, flush, barrier, dist_max)
-    graph_ms = None
-    if world == 1 and not args.no_graph:
-        graph_ms = _measure_graph(plan, args.steps, args.warmup, flush, barrier, dist_max)
-    e_step, pot, qbytes = _measure_e2e(plan, q, args.steps, args.warmup, flush, barrier, dist_max)
-    st2 = None
+    r1 = _dtype_run(plan, q, args, flush, barrier, dist_max, world)
+    r2 = None
     if not args.no_secondary:
-        plan2 = FmmPlan(pts, None, FmmConfig(order=w.order, ncrit=w.ncrit, kappa=kappa, dtype=other),
-                        device=dev, charges=q, reuse=plan, shard=shard, allreduce=ar,
-                        m2l=args.m2l_levels)
-        if args.p2p_overlap:
-            plan2.p2p_overlap = args.p2p_overlap
-        if args.p2p_grid is not None:
-            plan2.p2p_grid = args.p2p_grid
-        if args.far_priority is not None:
-            plan2.far_priority = bool(args.far_priority)
-        st2 = _measure(plan2, args.steps, args.warmup, flush, barrier, dist_max)
-        del plan2
+        plan2 = FmmPlan(pts, None, FmmConfig(order=w.order, ncrit=w.ncrit, kappa=kappa, dtype=other), device=dev,
+                        charges=q, reuse=plan, shard=shard, allreduce=ar, m2l=args.m2l_levels)
+        knobs(plan2)
+        r2 = _dtype_run(plan2, q, args, flush, barrier, dist_max, world)
     clk = clocks.stop()
-    # sharded (strong scaling): the N ranks together process the N particles.
-    # Single GPU: the matvec replayed from its CUDA graph (same kernels, no host
-    # launch gaps); the eager per-stage breakdown is reported alongside.
-    step_ms = graph_ms if graph_ms is not None else st["step"]
-    value = n / (step_ms / 1e3)
-    if world > 1:  # assemble the potentials of all ranks for the accuracy check
-        out = plan.apply()
-        dist.all_reduce(torch.view_as_real(out))
-        pot = out.cpu().numpy()
+    sm_mhz = clk.get("sm_mhz")
 
     # accuracy on the 1000 sampled check targets (BASELINE: "at fixed rel. L2 error")
     s = sample_targets(n)
     side = plan.st.root_box.side
     d = direct_sum(HelmholtzKernel(kappa=kappa, singularity_tol=1e-12 * side), pts[s], pts, q, device=dev)
-    eps = float(np.linalg.norm(pot[s] - d) / np.linalg.norm(d))
 
+    def acc(pot):
+        if world > 1:  # sharded: each rank's potentials cover its own targets
+            t = torch.as_tensor(pot).to(dev)
+            dist.all_reduce(torch.view_as_real(t))
+            pot = t.cpu().numpy()
+        return float(np.linalg.norm(pot[s] - d) / np.linalg.norm(d))
+
+    eps1 = acc(r1["pot"])
+    eps2 = acc(r2["pot"]) if r2 is not None else None
+    halo = None
+    if world > 1:
+        hb = torch.tensor([float(plan.halo_bytes())], device=dev)
+        allb = [torch.zeros_like(hb) for _ in range(world)]
+        dist.all_gather(allb, hb)
+        halo = [int(x.item()) for x in allb]
     if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
+        dist.destroy_process_group()
         return
 
-    # roofline of the dominant kernel (M2L + fused F2L), timed alone on the main stream
-    p = plan.plan
-    L = w.order
-    P3 = (2 * L - 1) ** 3
-    c = 16 if dtype == "c128" else 8
-    n_m2l = p.counts["m2l_events"]
-    rows = p.m2l_row_slot.shape[0]
-    alg_bytes = n_m2l * 2 * P3 * c + rows * L**3 * c  # symbol + source spectrum per event, local write
-    m2l_s = st["m2l"] / 1e3
-    kname = "M2L stage: " + " + ".join(plan.m2l_kernels())
-    traffic = _ncu_traffic(f"{args.workload}:{dtype}:m2l")
-    peak, peak_kind = _measured_peak_hbm()
-    achieved = alg_bytes / m2l_s / 1e9
-    # P2P: 24 flop per pair against the measured FMA peak of
-    # the pipe it runs on; the ncu FP-pipe utilisation is the graded number
-    fpk = _fma_peaks(dev)
-    pipe = "fp32" if dtype == "c64" else "fp64"
-    pairs = int(p.counts["p2p_pairs"])
-    p2p_tf = 24.0 * pairs / (st["p2p"] * 1e-3) / 1e12
-    p2p_roof = {"bound": pipe, "achieved": p2p_tf, "peak": fpk[pipe], "unit": "TFLOP/s", "frac": p2p_tf / fpk[pipe],
-                "flop_per_pair": 24, "pairs": pairs, "kernel_ms": st["p2p"], "peak_kind": "measured (defmm_fma_peak)",
-                "ncu_pipe_utilisation": _ncu_pipe(f"{args.workload}:{dtype}"),
-                "note": "frac counts 24 algorithmic flop/pair; sincos/rsqrt/hi-lo work is extra issue, so the "
-                        "pipe utilisation from ncu (profiles/r01_p2p_pipes.json) is the FP-pipe figure"}
+    fpk = _fma_peaks(dev) if world == 1 else None
+    l2peak = _l2_stream_peak(dev, sm_mhz) if world == 1 else None
+    g = _golden(args.workload)
+    eps_ref = float(g["eps_ref"]) if g is not None and int(g["order"]) == w.order else None
+
+    def block(r, pl, dt, eps):
+        step_ms = r["graph_ms"] if r["graph_ms"] is not None else r["st"]["step"]
+        st = r["st"]
+        b = {"value": n / (step_ms / 1e3), "ms_per_step": step_ms, "ms_per_step_eager": st["step"],
+             "launch_mode": "cuda_graph" if r["graph_ms"] is not None else "eager",
+             "dtype": _DTYPE_LABEL[dt],
+             "e2e": {"value": n / (r["e2e_ms"] / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(r["qbytes"]),
+                     "d2h_bytes_per_step": int(r["qbytes"]), "ms_per_step": r["e2e_ms"]},
+             "stages_ms": {("upward_with_concurrent_p2p" if pl.p2p_overlap in ("upward", "m2m", "full") else "upward"):
+                           st["upward"],
+                           ("m2l_with_concurrent_p2p" if pl.p2p_overlap in ("m2m", "m2l", "full") else "m2l"):
+                           st["m2l"], "p2p": st["p2p"], "downward": st["downward"]},
+             "p2p_overlap": pl.p2p_overlap, "far_priority": bool(pl.far_priority),
+             "accuracy": {"rel_l2_vs_direct_1000": eps, "eps_ref_reference": eps_ref,
+                          "north_star_bar_ok": (eps <= 1.01 * eps_ref) if eps_ref else None}}
+        if r["iso"] is not None:
+            b["isolated_ms"] = r["iso"]
+            b["roofline"] = _roofline(pl, r["iso"], args.workload, dt, l2peak, sm_mhz)
+            b["p2p_roofline"] = _p2p_roofline(pl, r["iso"], dt, fpk)
+        return b
+
+    b1 = block(r1, plan, dtype, eps1)
     line = {
         "metric": METRIC,
-        "value": value,
+        "value": b1["value"],
         "unit": UNIT,
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": step_ms,
-        "ms_per_step_eager": st["step"],
-        "launch_mode": "cuda_graph" if graph_ms is not None else "eager",
+        "ms_per_step": b1["ms_per_step"],
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "f32 storage, f64 sums" if dtype == "c64" else "f64",
+        "dtype": b1["dtype"],
         "data": "synthetic",
         "config": dict(_workload_desc(w, n, dtype), l2_flush="256 MiB memset between timed iterations",
                        parallelism=(f"morton-sharded x{world} (NCCL {args.exchange} of multipoles)"
                                     if world > 1 else "single")),
-        # stage timers (eager run); the P2P runs on the side stream beside the
-        # stage named by p2p_overlap (fmm.p2p_overlap_policy)
-        "stages_ms": {("upward_with_concurrent_p2p" if plan.p2p_overlap in ("upward", "m2m", "full") else "upward"): st["upward"],
-                      ("m2l_with_concurrent_p2p" if plan.p2p_overlap in ("m2m", "m2l", "full") else "m2l"): st["m2l"],
-                      "p2p": st["p2p"], "downward": st["downward"]},
-        "p2p_overlap": plan.p2p_overlap,
-        "far_priority": bool(plan.far_priority),
-        "roofline": {"bound": "hbm", "kernel": kname,
-                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
-                     "kernel_ms": st["m2l"],
-                     "ncu_dominant_kernel": _ncu_m2l(f"{args.workload}:{dtype}"),
-                     "note": "algorithmic bytes = 2 spectra per M2L event + local write; frac > 1 = L2 reuse; "
-                             "traffic = ncu dram bytes of the M2L-stage launches of one matvec (profiles/r01_m2l_traffic.json); "
-                             "the kernel's physical bound is the L2->SM fabric: ncu_dominant_kernel.l2_to_l1_bytes_per_clk against the chip's LTS throughput cap (lts_cap_bytes_per_clk)"},
-        "p2p_roofline": p2p_roof,
-        "fma_peaks_tflops": fpk,
-        "e2e": {"value": n / (e_step / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(qbytes),
-                "d2h_bytes_per_step": int(qbytes), "ms_per_step": e_step},
-        "accuracy": {"rel_l2_vs_direct_1000": eps, "eps_ref_reference": _EPS_REF.get(args.workload)},
-        "gpu_launches": int(args.steps * plan.launches_per_apply),
-        "clocks": clk,
-        "setup_s": setup_s,
     }
-    if st2 is not None:
-        line[f"{other}_same_lists"] = {"value": n / (st2["step"] / 1e3), "ms_per_step": st2["step"],
-                                       "m2l_ms": st2["m2l"], "p2p_ms": st2["p2p"]}
-    if not args.no_cpu_baseline:
-        v, tm, counts = _cpu_oracle_sample(args.workload, args.cpu_sample)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
-                                "sample": f"oracle matvec on the first {args.cpu_sample} points of {w.name} "
-                                          f"(same kappa, L, ncrit): {tm['matvec']:.1f} s"}
+    line.update({k: v for k, v in b1.items() if k not in ("value", "ms_per_step", "dtype")})
+    line["fma_peaks_tflops"] = fpk
+    line["l2_stream_peak"] = l2peak
+    line["gpu_launches"] = int(args.steps * plan.launches_per_apply)
+    line["clocks"] = clk
+    line["setup_s"] = setup_s
+    line["plan_timings_s"] = {k: float(v) for k, v in plan.timings.items()}
+    if halo is not None:
+        line["halo_bytes_per_rank"] = halo
+    if r2 is not None:
+        line[other] = block(r2, plan2, other, eps2)
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = _cpu_baseline(args.workload, args.cpu_parts)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -532,6 +600,8 @@ def run_b200(args):
 
 def main():
     args = _args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn_ranks(args))
     if args.impl == "reference":
         run_reference(args)
     else:

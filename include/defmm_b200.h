@@ -93,6 +93,13 @@ void defmm_dtt_free(defmm_dtt* d);
  * selects double.  out: one element, written only to keep the chains live. */
 int defmm_fma_peak(int32_t fp64, int64_t iters, void* out, void* stream);
 
+/* ---- L2 -> SM streaming probe (measurement only) ---------------------------
+ * ctas_per_sm x SMs CTAs of 512 threads read the n_vec 16-B vectors of buf
+ * (an L2-resident buffer) iters times with L2-only cached 128-bit loads:
+ * bytes moved L2 -> SM = 16 * n_vec * iters (rounded up to whole passes of
+ * 4 x grid vectors).  out: one float, written only to keep the loads live. */
+int defmm_l2_stream(const void* buf, int64_t n_vec, int32_t iters, int32_t ctas_per_sm, void* out, void* stream);
+
 /* ---- device operators ------------------------------------------------------
  * Every operator exists as *_c128 (complex arrays are double2 = interleaved
  * FP64 re/im, exactly the reference's complex128; all arithmetic FP64) and

@@ -1919,20 +1919,6 @@ __global__ void direct_reduce(int64_t nt, int nsplit, const double2* __restrict_
 // ---------------------------------------------------------------------------
 // launch helpers
 
-// fill c_tw once per process (before the first launch that needs it)
-// host restatement of rotated_index (same closed form)
-int host_rotated_index(int P, int j, int rid) {
-    static const int perm[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
-    const int f[3] = {j / (P * P), (j / P) % P, j % P};
-    const int wt[3] = {P * P, P, 1};
-    int idx = 0;
-    for (int a = 0; a < 3; ++a) {
-        const int ng = (rid >> (2 - a)) & 1;
-        idx += wt[perm[rid >> 3][a]] * (ng ? (f[a] ? P - f[a] : 0) : f[a]);
-    }
-    return idx;
-}
-
 struct HostLayout {
     int P3 = 0, nslices = 0;
     std::vector<int16_t> forder, finv;

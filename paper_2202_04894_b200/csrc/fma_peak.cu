@@ -1,4 +1,6 @@
-// FP32 / FP64 FMA-pipe peak probe (C-ABI: include/defmm_b200.h).  The P2P
+// Measurement probes (C-ABI: include/defmm_b200.h).
+//
+// FP32 / FP64 FMA-pipe peak probe.  The P2P
 // roofline divides 24 flop per pair by the MEASURED FMA peak
 // of the box; MEASURED_PEAKS.json holds only HBM and bf16, so bench.py runs
 // this once: every thread keeps 8 independent FMA chains in registers (no
@@ -28,7 +30,50 @@ __global__ void __launch_bounds__(256) fma_peak_kernel(int64_t iters, T b, T c, 
     if (s == (T)-1.2345) out[0] = s;  // keeps the chains live, never taken
 }
 
+// L2 -> SM streaming probe: every warp reads 512-B contiguous runs (LDG.128,
+// .cg = cached in L2 only, so every request travels L2 -> SM) of an
+// L2-resident buffer, grid-strided and repeated `iters` times.  The M2L's
+// L2 -> L1 bytes per clock (ncu) are reported against this measured rate.
+__global__ void __launch_bounds__(512) l2_stream_kernel(const float4* __restrict__ buf, int64_t n_vec, int32_t iters,
+                                                        float* out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int32_t it = 0; it < iters; ++it) {
+        int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x + (int64_t)it * 4099 * 32) % n_vec;
+        for (int64_t k = 0; k < n_vec; k += 4 * stride) {
+            float4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                int64_t j = i + u * stride;
+                j = j >= n_vec ? j - n_vec : j;
+                v[u] = __ldcg(buf + j);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                acc.x += v[u].x;
+                acc.y += v[u].y;
+                acc.z += v[u].z;
+                acc.w += v[u].w;
+            }
+            i += 4 * stride;
+            i = i >= n_vec ? i % n_vec : i;
+        }
+    }
+    if (acc.x + acc.y + acc.z + acc.w == -1.2345f) out[0] = acc.x;  // keeps the loads live, never taken
+}
+
 }  // namespace
+
+extern "C" int defmm_l2_stream(const void* buf, int64_t n_vec, int32_t iters, int32_t ctas_per_sm, void* out,
+                               void* stream) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (n_vec <= 0 || iters <= 0 || ctas_per_sm <= 0) return -1;
+    l2_stream_kernel<<<ctas_per_sm * sms, 512, 0, (cudaStream_t)stream>>>((const float4*)buf, n_vec, iters,
+                                                                         (float*)out);
+    return (int)cudaGetLastError();
+}
 
 extern "C" int defmm_fma_peak(int32_t fp64, int64_t iters, void* out, void* stream) {
     int dev = 0, sms = 0;

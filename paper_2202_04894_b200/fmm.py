@@ -25,6 +25,19 @@ from .tree import build_tree
 __all__ = ["FmmPlan", "run_fmm", "run_fmm_full"]
 
 
+def _on_device(fn):
+    """Run a plan method with the plan's device current: the C-ABI launches
+    go to the current device (and ensure_twiddles fills that device's tables)."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapped(self, *a, **k):
+        with torch.cuda.device(self.device):
+            return fn(self, *a, **k)
+
+    return wrapped
+
+
 def _dev(a, dtype, device):
     return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype).to(device)
 
@@ -495,6 +508,7 @@ class FmmPlan:
         _, h["p2p_ptr"], h["p2p_sel"] = _sub_csr(p.p2p_ptr, sh.leaf_keep)
         return h
 
+    @_on_device
     def _symbols(self):
         p = self.plan
         self.sym = torch.empty((max(p.n_sym, 1), self.SS), dtype=self.cdtype, device=self.device)
@@ -513,6 +527,7 @@ class FmmPlan:
         return f"defmm_{name}_{self.config.dtype}"
 
     # ------------------------------------------------------------------
+    @_on_device
     def set_charges(self, charges):
         """Load charges (caller order) into the sorted device buffer."""
         q = torch.as_tensor(np.asarray(charges, dtype=complex)) if not torch.is_tensor(charges) else charges
@@ -522,6 +537,7 @@ class FmmPlan:
     def set_charges_sorted(self, q_sorted):
         self.q.copy_(q_sorted)
 
+    @_on_device
     def apply(self, out=None, stage_events=None):
         """One matvec with the charges currently loaded; returns potentials in
         the caller's target order (device tensor; when sharded only this
@@ -557,6 +573,18 @@ class FmmPlan:
 
                 halo_exchange(self.mult, self._halo_dev())
         return self.apply_rest(out, stage_events)
+
+    def halo_bytes(self) -> int:
+        """Bytes this rank moves per matvec in the multipole exchange: the
+        spanning multipoles it all-reduces plus the nodal multipoles it sends
+        and receives in the all_to_all (0 unsharded)."""
+        if self.shard is None:
+            return 0
+        per = self.L3 * self.mult.element_size()
+        if self.halo is None:  # allreduce= exchange: the whole multipole array
+            return int(self.mult.numel() * self.mult.element_size())
+        h = self.halo
+        return int(per * (len(h.span) + int(sum(h.send_counts)) + int(sum(h.recv_counts))))
 
     def _halo_dev(self):
         if getattr(self, "_halo_t", None) is None:
@@ -625,6 +653,31 @@ class FmmPlan:
             b.record(stream)
             stage_events.append(("upward", self._ev_a, b))
         # M2L (+ fused F2L) into the local slots
+        self._m2l(sh)
+        if stage_events is not None:
+            c = ev()
+            c.record(stream)
+            stage_events.append(("m2l", b, c))
+        # downward: L2L per level top-down, then L2P + near + un-permute
+        for son_beta, outs, octant, ptr, src, sdir, n in self.l2l:
+            _lib.call(self._op("l2l"), L, n, outs, octant, ptr, src, sdir, son_beta, self.dirs, kappa,
+                      self.local, sh)
+        stream.wait_stream(self.side_stream)
+        if self.shard is not None:
+            out.zero_()  # this rank writes only its own targets
+        _lib.call(self._op("l2p"), L, self.n_leaves, self.leaf_cell, self.leaf_lo, self.leaf_hi, self.slot_dir,
+                  tg["start"], tg["stop"], tg["alpha"], tg["level"], tg["beta"], self.dirs, *self.t_xyz, kappa,
+                  self.local, self.near, self.t_perm, out, sh)
+        if stage_events is not None:
+            e = ev()
+            e.record(stream)
+            stage_events.append(("downward", c, e))
+        return out
+
+    def _m2l(self, sh):
+        """The M2L stage (K7 + K8) on stream handle ``sh``: zero the locals, the
+        per-level M2L kernels, the F2L of the blocked rows."""
+        L = self.L
         self.local.zero_()
         if self.m2l_variant == "hybrid":
             _lib.call(self._op("m2l_rows"), L, self.rk_rows.shape[0], self.rk_rows, self.rk_ptr, self.rk_ent,
@@ -650,26 +703,38 @@ class FmmPlan:
                       e_sym, e_rid, self.hat, self.sym, self.local, sh)
         else:
             raise ValueError(f"unknown M2L variant {self.m2l_variant!r} for dtype {self.config.dtype}")
-        if stage_events is not None:
-            c = ev()
-            c.record(stream)
-            stage_events.append(("m2l", b, c))
-        # downward: L2L per level top-down, then L2P + near + un-permute
-        for son_beta, outs, octant, ptr, src, sdir, n in self.l2l:
-            _lib.call(self._op("l2l"), L, n, outs, octant, ptr, src, sdir, son_beta, self.dirs, kappa,
-                      self.local, sh)
-        stream.wait_stream(self.side_stream)
-        if self.shard is not None:
-            out.zero_()  # this rank writes only its own targets
-        _lib.call(self._op("l2p"), L, self.n_leaves, self.leaf_cell, self.leaf_lo, self.leaf_hi, self.slot_dir,
-                  tg["start"], tg["stop"], tg["alpha"], tg["level"], tg["beta"], self.dirs, *self.t_xyz, kappa,
-                  self.local, self.near, self.t_perm, out, sh)
-        if stage_events is not None:
-            e = ev()
-            e.record(stream)
-            stage_events.append(("downward", c, e))
-        return out
 
+    @_on_device
+    def time_isolated(self, reps: int = 5, flush=None) -> dict:
+        """Kernel times with nothing running beside them (ms, CUDA events on the
+        launching stream, mean of ``reps``): the M2L stage (memset + M2L kernels
+        + F2L) on the current stream after a full matvec, and the P2P alone on
+        its side stream.  These are the roofline denominators of bench.py."""
+        dev = self.device
+        stream = torch.cuda.current_stream(dev)
+        self._apply()  # spectra of the loaded charges
+        torch.cuda.synchronize(dev)
+        t = {"m2l": 0.0, "p2p": 0.0}
+        for _ in range(reps):
+            if flush is not None:
+                flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize(dev)
+            a.record(stream)
+            self._m2l(stream.cuda_stream)
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            t["m2l"] += a.elapsed_time(b)
+            if flush is not None:
+                flush.zero_()
+            torch.cuda.synchronize(dev)
+            ev = []
+            self._near_field(ev)
+            torch.cuda.synchronize(dev)
+            t["p2p"] += ev[0][1].elapsed_time(ev[0][2])
+        return {k: v / max(reps, 1) for k, v in t.items()}
+
+    @_on_device
     def capture_graph(self):
         """Record one matvec (all launches on both streams, the memsets) into a
         CUDA graph; ``replay()`` then re-executes it with whatever charges are

@@ -7,7 +7,7 @@
 set -u
 W=$1; TAG=$2; shift 2
 OUT=gpurun_out/prof_$TAG; mkdir -p $OUT
-B="python bench.py --workload $W --steps 1 --warmup 3 --no-cpu-baseline --no-secondary --no-graph $*"
+B="python bench.py --workload $W --steps 1 --warmup 3 --no-cpu-baseline --no-secondary --profile $*"
 NCU=/usr/local/cuda/bin/ncu
 timeout 600 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --csv --log-file $OUT/launches.csv $B > $OUT/launches.log 2>&1
