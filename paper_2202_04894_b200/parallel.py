@@ -21,8 +21,12 @@ cells whose particle range intersects it ("active" cells):
 * M2F only for the spectra its own M2L rows read;
 * M2L rows, L2L slots and L2P/P2P leaves of its active target cells (shared
   top cells are computed redundantly by every rank that needs them), so the
-  far field needs no halo exchange of locals and the near field reads the
-  (replicated, read-only) source particles directly.
+  far field needs no halo exchange of locals;
+* near-field halo: a rank is given only the charges of its own chunk; one
+  ``all_to_all`` per matvec (``ChargeHalo``, ``charge_exchange``) brings in
+  exactly the source charges its P2P leaves read from other chunks (the
+  near-field source leaves next to its boundary).  Positions are geometry,
+  static per plan.
 
 Single-tree mode (targets is sources) only; the two-tree mode runs replicas.
 Everything here is host-side index bookkeeping (numpy); it is exercised with
@@ -35,7 +39,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["Shard", "Halo", "leaf_costs", "partition_leaves", "make_shard", "make_halo", "halo_exchange"]
+__all__ = ["Shard", "Halo", "ChargeHalo", "leaf_costs", "partition_leaves", "make_shard", "make_halo",
+           "halo_exchange", "make_charge_halo", "charge_exchange"]
 
 # relative unit costs measured on the B200 (profiles/r01_summary_v2.md, c64):
 # M2L ~2.9 ms / 10.8 M events; P2P ~0.77 ms / 3.83e8 pairs
@@ -193,3 +198,73 @@ def halo_exchange(mult, halo_dev, group=None):
         dist.all_to_all_single(rbuf.view(-1), sbuf.view(-1), [c * per for c in recv_counts],
                                [c * per for c in send_counts], group=group)
         mult.index_copy_(0, recv, torch.view_as_complex(rbuf))
+
+
+@dataclass
+class ChargeHalo:
+    """Static particle index sets of one rank's near-field charge exchange
+    (sorted particle order; counts per peer rank, in rank order)."""
+    send: np.ndarray  # own particles other ranks' P2P reads, by destination
+    send_counts: list
+    recv: np.ndarray  # other ranks' particles this rank's P2P reads, by source
+    recv_counts: list
+    active: bool = True  # identical on every rank (the all_to_all is collective)
+
+
+def _p2p_sources(plan, tt, cuts, r) -> np.ndarray:
+    """Sorted particle indices the P2P leaves of rank r read, outside its chunk."""
+    lo, hi = int(cuts[r]), int(cuts[r + 1])
+    leaves = plan.leaf_cells
+    keep = (tt.start[leaves] < hi) & (tt.stop[leaves] > lo)
+    e = np.repeat(keep, np.diff(plan.p2p_ptr))
+    a, b = plan.p2p_lo[e], plan.p2p_hi[e]
+    if a.size == 0:
+        return np.zeros(0, np.int64)
+    # union of the runs, then drop the own chunk
+    o = np.argsort(a, kind="stable")
+    a, b = a[o], b[o]
+    cover = np.zeros(int(tt.stop[0]) + 1, np.int64)
+    np.add.at(cover, a, 1)
+    np.add.at(cover, b, -1)
+    idx = np.nonzero(np.cumsum(cover)[:-1] > 0)[0]
+    return idx[(idx < lo) | (idx >= hi)].astype(np.int64)
+
+
+def make_charge_halo(plan, tt, cuts, rank: int, world: int) -> ChargeHalo:
+    cuts = np.asarray(cuts)
+    need = [_p2p_sources(plan, tt, cuts, r) for r in range(world)]
+    active = any(x.size for x in need)
+    send, send_counts, recv, recv_counts = [], [], [], []
+    for r in range(world):
+        if r == rank:
+            send_counts.append(0)
+            recv_counts.append(0)
+            continue
+        lo, hi = int(cuts[rank]), int(cuts[rank + 1])
+        s_r = need[r][(need[r] >= lo) & (need[r] < hi)]  # mine, read by r
+        rlo, rhi = int(cuts[r]), int(cuts[r + 1])
+        v_r = need[rank][(need[rank] >= rlo) & (need[rank] < rhi)]  # r's, read by me
+        send.append(s_r)
+        recv.append(v_r)
+        send_counts.append(int(s_r.shape[0]))
+        recv_counts.append(int(v_r.shape[0]))
+    cat = lambda xs: np.concatenate(xs).astype(np.int64) if xs else np.zeros(0, np.int64)  # noqa: E731
+    return ChargeHalo(cat(send), send_counts, cat(recv), recv_counts, bool(active))
+
+
+def charge_exchange(q, halo_dev, group=None):
+    """Fill the other-chunk source charges this rank's P2P reads: ``q`` is
+    the (n,) complex charge vector in sorted order holding this rank's chunk;
+    ``halo_dev`` = (send, send_counts, recv, recv_counts, active) with index
+    tensors on q's device."""
+    import torch
+    import torch.distributed as dist
+
+    send, send_counts, recv, recv_counts, active = halo_dev
+    if not active:
+        return
+    sbuf = torch.view_as_real(q.index_select(0, send)).contiguous()
+    rbuf = torch.empty((recv.shape[0], 2), dtype=sbuf.dtype, device=q.device)
+    dist.all_to_all_single(rbuf.view(-1), sbuf.view(-1), [2 * c for c in recv_counts],
+                           [2 * c for c in send_counts], group=group)
+    q.index_copy_(0, recv, torch.view_as_complex(rbuf))

@@ -148,12 +148,12 @@ def test_m2l_canonical_gather_and_derived_symbols_agree(case):
     plan.m2l_variant = "hybrid"
     c = plan.apply().cpu().numpy()
     assert _rel(c, a) <= 1e-13
-    for mode in ("blocked_all", "rows", "hybrid_rows", "pairs_all", "triples_all", "quartets_all"):
+    for mode in ("blocked_all", "rows", "hybrid_rows", "pairs_all", "triples_all", "quartets_all", "tiles_all"):
         p2 = FmmPlan(g["points"], None, FmmConfig(**g["config"]), charges=g["charges"], reuse=plan, m2l=mode)
         assert _rel(p2.apply().cpu().numpy(), a) <= 1e-13
     # every kernel on some level at once (per-level overrides)
     levels = sorted(plan.level_kinds)
-    mix = {lv: ("rows", "blocked", "pair", "triple", "quartet")[i % 5] for i, lv in enumerate(levels)}
+    mix = {lv: ("rows", "blocked", "pair", "triple", "quartet", "tile")[i % 6] for i, lv in enumerate(levels)}
     p2 = FmmPlan(g["points"], None, FmmConfig(**g["config"]), charges=g["charges"], reuse=plan, m2l_levels=mix)
     assert p2.level_kinds == mix
     assert _rel(p2.apply().cpu().numpy(), a) <= 1e-13
@@ -170,7 +170,7 @@ def test_group_m2l_kernels_match_reference(case, dtype):
     g = load_case(case)
     cfg = FmmConfig(**{**g["config"], "dtype": dtype})
     base = FmmPlan(g["points"], None, cfg, charges=g["charges"])
-    for mode in ("pairs_all", "triples_all", "quartets_all"):
+    for mode in ("pairs_all", "triples_all", "quartets_all", "tiles_all"):
         p2 = FmmPlan(g["points"], None, cfg, charges=g["charges"], reuse=base, m2l=mode)
         a = p2.apply().cpu().numpy().astype(np.complex128)
         assert _rel(a, g["pot"]) <= (FP64_TOL if dtype == "c128" else C64_TOL)
@@ -210,27 +210,74 @@ def test_cfg1_full_size_parity():
     assert eps_new <= (1 + 1e-2) * eps_ref
 
 
-@pytest.mark.parametrize("dtype", ["c128", "c64"])
-@pytest.mark.parametrize("name", ["cfg2", "cfg2_L6"])
-def test_cfg2_full_size_sampled_parity(name, dtype):
-    """BASELINE cfg2 (N=1M cube surface, kappa*D=128, L=4/6): sampled targets
-    against the reference run (tests/golden/ref_cfg2*.npz) and direct sums."""
+# (golden file, workload, dtype): every BASELINE config at its BASELINE dtype
+# (cfg2: c64 and c128; cfg3: c64, plus c128; cfg5: c128) and every order
+FULL_SIZE = [("cfg2", "cfg2", "c64"), ("cfg2", "cfg2", "c128"), ("cfg2_L6", "cfg2", "c64"),
+             ("cfg2_L6", "cfg2", "c128"), ("cfg3", "cfg3", "c64"), ("cfg3", "cfg3", "c128"),
+             ("cfg5", "cfg5", "c128"), ("cfg5_L6", "cfg5", "c128"), ("cfg5_L8", "cfg5", "c128")]
+
+
+@pytest.mark.parametrize("name,workload,dtype", FULL_SIZE)
+def test_full_size_sampled_parity(name, workload, dtype):
+    """BASELINE cfg2/cfg3/cfg5 at full size (1M / 4M / 2M points), each order
+    the survey runs: counts equal the reference's run_fmm_full
+    (traversal.py:495-505) exactly; on the 1,000 sampled targets
+    (harness.py:151-165) rel-L2(p_new, p_ref) <= 1e-2 eps_ref (the north-star
+    bar) and eps_new <= (1 + 1e-2) eps_ref against FP64 direct sums
+    (tests/golden/ref_*.npz, written by make_golden_large.py from the
+    reference itself)."""
     from paper_2202_04894_b200 import FmmConfig, HelmholtzKernel, direct_sum, run_fmm_full
     from paper_2202_04894_b200.workloads import make_workload
 
     ref = load_ref(name)
-    pts, q, k, w = make_workload("cfg2")
+    pts, q, k, w = make_workload(workload)
+    assert abs(k - float(ref["kappa"])) == 0.0
     pot, info = run_fmm_full(pts, pts, q, FmmConfig(order=int(ref["order"]), ncrit=w.ncrit, kappa=k, dtype=dtype))
     assert {kk: info.counts[kk] for kk in info.counts} == {kk: ref["counts"][kk] for kk in info.counts}
+    assert info.hf_max_level == int(ref["hf_max"])
     s = ref["sample"]
     eps_ref = float(ref["eps_ref"])
     r = _rel(pot[s], ref["pot_sample"])
     assert r <= 1e-2 * eps_ref  # the north-star parity bar
-    assert r <= (FP64_TOL if dtype == "c128" else C64_TOL)
+    if dtype == "c128":
+        assert r <= FP64_TOL
     side = 2 * np.max(np.abs(pts - pts.mean(0))) * (1 + 1e-6)
     d = direct_sum(HelmholtzKernel(kappa=k, singularity_tol=1e-12 * side), pts[s], pts, q)
-    assert _rel(d, ref["direct_sample"]) <= 1e-12
+    assert _rel(d, ref["direct_sample"]) <= 1e-12  # the GPU direct sum = the reference's
     assert _rel(pot[s], d) <= (1 + 1e-2) * eps_ref
+
+
+def test_cfg4_counts_and_accuracy():
+    """BASELINE cfg4 (N=16M refined cube, kappa*D=512, L=6, ncrit=128) on one
+    GPU.  The reference's full matvec does not fit this container (spectra
+    alone > 62 GB), so tests/golden/ref_cfg4_counts.npz holds the reference's
+    own counts (its tree, blank passes and dual tree traversal run with the
+    arithmetic stubbed, make_golden_counts.py) and FP64 direct sums on the
+    1,000 sampled targets: counts must be equal; the complex128 path (the
+    reference's arithmetic) sets eps, and complex64 storage must stay within
+    1% of it."""
+    from paper_2202_04894_b200 import FmmConfig, FmmPlan
+    from paper_2202_04894_b200.workloads import make_workload
+
+    ref = load_ref("cfg4_counts")
+    pts, q, k, w = make_workload("cfg4")
+    assert abs(k - float(ref["kappa"])) == 0.0
+    s = ref["sample"]
+    eps = {}
+    base = None
+    for dtype in ("c128", "c64"):
+        cfg = FmmConfig(order=w.order, ncrit=w.ncrit, kappa=k, dtype=dtype)
+        plan = FmmPlan(pts, None, cfg, charges=q, reuse=base)
+        if base is None:
+            base = plan
+            counts = {kk: v for kk, v in plan.plan.counts.items() if kk != "translations"}
+            assert counts == {kk: ref["counts"][kk] for kk in counts}
+            assert plan.plan.hf_max == int(ref["hf_max"])
+        pot = plan.apply().cpu().numpy().astype(np.complex128)
+        eps[dtype] = _rel(pot[s], ref["direct_sample"])
+        del pot
+    assert eps["c128"] < 1e-3
+    assert eps["c64"] <= (1 + 1e-2) * eps["c128"]
 
 
 @pytest.mark.parametrize("dtype", ["c128", "c64"])

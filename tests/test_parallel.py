@@ -164,3 +164,50 @@ def test_halo_exchange_completes_every_needed_multipole(case, world):
     for rank, ok, n_span, n_send, n_recv, n_mult in res:
         assert ok, rank
         assert n_span + n_recv < n_mult  # a halo, not the whole multipole array
+
+
+def _charge_worker(rank, world, port, case, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2202_04894_b200.parallel import _p2p_sources, charge_exchange, make_charge_halo
+
+        tr, pl = _plan(case)
+        sh = make_shard(pl, tr, tr, rank, world)
+        h = make_charge_halo(pl, tr, sh.cuts, rank, world)
+        n = int(tr.stop[0])
+        full = torch.arange(n, dtype=torch.float64) + 1j * torch.arange(n, dtype=torch.float64) / 7
+        mine = full.clone()
+        mine[: sh.lo] = 0
+        mine[sh.hi:] = 0
+        dev = (torch.as_tensor(h.send), list(h.send_counts), torch.as_tensor(h.recv), list(h.recv_counts), h.active)
+        charge_exchange(mine, dev)
+        need = _p2p_sources(pl, tr, sh.cuts, rank)
+        own = torch.arange(sh.lo, sh.hi)
+        ok = bool(torch.equal(mine[need], full[need])) and bool(torch.equal(mine[own], full[own]))
+        # every source a kept P2P run reads is now present
+        leaves = pl.leaf_cells[sh.leaf_keep]
+        sel = np.repeat(sh.leaf_keep, np.diff(pl.p2p_ptr))
+        runs_ok = all(bool(torch.equal(mine[a:b], full[a:b])) for a, b in zip(pl.p2p_lo[sel], pl.p2p_hi[sel]))
+        q.put((rank, ok and runs_ok and leaves.size > 0, int(h.send.size), int(h.recv.size)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("case", ["cubesurf4000", "volume3000"])
+def test_gloo_near_field_charge_halo(case, world):
+    """Each rank starts from its own chunk's charges only; one all_to_all
+    (parallel.charge_exchange) brings every source charge its P2P runs read."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_charge_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(r[1] for r in res), res
+    assert sum(r[2] for r in res) == sum(r[3] for r in res) > 0
