@@ -181,6 +181,9 @@ int defmm_m2l_tiles(int64_t n_ids, const int64_t* ids, const int64_t* row_slot, 
  *   source operand, tile-local symbol operand for row k or 0xFFFF, 0
  *   padding}: lhat[row] = sum D (*) hat (stride defmm_spectrum_stride), then
  *   f2l_rows.
+ *   m2l_tile_l1: the same tiles and sums without shared-memory staging: gent
+ *   = the entries with GLOBAL ids (int32 x 8: spectrum, derived symbol of row
+ *   k or -1, -1 padding), operands read through L1; no max_ops limit.
  * K5 L2L -- traversal.py:355-391 in gather form.
  *   for i < n: local[out_slot[i]] += sum_{e in [ptr[i], ptr[i+1])}
  *   (C'0 (x) C'1 (x) C'2) local[src_slot[e]], C' the transposed/conjugate-
@@ -240,6 +243,11 @@ int defmm_m2l_tiles(int64_t n_ids, const int64_t* ids, const int64_t* row_slot, 
                                 const int64_t* grp_ent_ptr, const uint16_t* ent,                 \
                                 const void* hat, const void* sym_derived, void* lhat,            \
                                 void* stream);                                                   \
+    int defmm_m2l_tile_l1_##SUFFIX(int32_t L, int32_t K, int64_t ntiles,                          \
+                                   const int64_t* tile_grp_ptr, const int32_t* grp_row,           \
+                                   const int64_t* grp_ent_ptr, const int32_t* gent,               \
+                                   const void* hat, const void* sym_derived, void* lhat,          \
+                                   void* stream);                                                 \
     int defmm_f2l_rows_##SUFFIX(int32_t L, int64_t nrows, const int64_t* row_slot,               \
                                 const void* lhat, void* local, void* stream);                   \
     int defmm_l2l_##SUFFIX(int32_t L, int64_t n, const int64_t* out_slot, const int8_t* octant,  \
@@ -267,11 +275,11 @@ int defmm_m2l_tiles(int64_t n_ids, const int64_t* ids, const int64_t* row_slot, 
 
 /* expands to: defmm_p2m_c128 defmm_m2m_c128 defmm_m2f_c128 defmm_symbols_c128
  * defmm_expand_symbols_c128 defmm_m2l_rows_c128 defmm_m2l_group_c128 defmm_m2l_blocked_c128
- * defmm_m2l_tile_c128 defmm_f2l_rows_c128 defmm_l2l_c128 defmm_l2p_c128 defmm_p2p_c128 */
+ * defmm_m2l_tile_c128 defmm_m2l_tile_l1_c128 defmm_f2l_rows_c128 defmm_l2l_c128 defmm_l2p_c128 defmm_p2p_c128 */
 DEFMM_DECLARE_TYPED(c128)
 /* expands to: defmm_p2m_c64 defmm_m2m_c64 defmm_m2f_c64 defmm_symbols_c64
  * defmm_expand_symbols_c64 defmm_m2l_rows_c64 defmm_m2l_group_c64 defmm_m2l_blocked_c64
- * defmm_m2l_tile_c64 defmm_f2l_rows_c64 defmm_l2l_c64 defmm_l2p_c64 defmm_p2p_c64 */
+ * defmm_m2l_tile_c64 defmm_m2l_tile_l1_c64 defmm_f2l_rows_c64 defmm_l2l_c64 defmm_l2p_c64 defmm_p2p_c64 */
 DEFMM_DECLARE_TYPED(c64)
 
 /* Spectral layout of order L (HOST call, no device needed): every spectrum is

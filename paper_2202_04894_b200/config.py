@@ -47,7 +47,10 @@ class FmmConfig:
         if self.order < 2:
             raise ValueError("order must be >= 2")
         if self.order > 8:
-            raise ValueError("the B200 kernels are compiled for orders 2..8")
+            # boundary deviation: the reference accepts any order
+            # >= 2 (traversal.py:58-60); the device kernels are instantiated for
+            # P = 2L-1 <= 15 (BASELINE's sweep stops at L = 8)
+            raise ValueError("the B200 kernels are compiled for orders 2..8 (the reference accepts any order >= 2)")
         if self.strategy not in STRATEGIES:
             raise ValueError(f"strategy must be one of {STRATEGIES}")
         if not (self.eta > 0):

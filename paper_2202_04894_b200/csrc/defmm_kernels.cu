@@ -1446,6 +1446,102 @@ __global__ void __launch_bounds__(TILE_NT) m2l_tile_kernel(
     }
 }
 
+// K7 v12: the same tiles without shared-memory staging: CTA = (tile, slice of
+// Q 16-B vectors), entries carry GLOBAL operand ids (int32 x 8: source,
+// derived symbol of row k < K or -1), operands are read with LDG through L1,
+// which keeps the slice of the tile's operands after the first touch (no
+// barriers: warps progress independently).
+template <typename R, int L, int K, int Q>
+__global__ void __launch_bounds__(256) m2l_tile_l1_kernel(
+    int64_t ntiles, int nslices, const int64_t* __restrict__ tile_grp_ptr, const int32_t* __restrict__ grp_row,
+    const int64_t* __restrict__ grp_ent_ptr, const int4* __restrict__ gent, const cx<R>* __restrict__ hat,
+    const cx<R>* __restrict__ symd, cx<R>* __restrict__ lhat) {
+    using V = cx<R>;
+    using VT = std::conditional_t<sizeof(R) == 4, float4, double2>;
+    constexpr int W = sizeof(R) == 4 ? 2 : 1;
+    constexpr int SS = spec_stride<R, L>();
+    constexpr int NV = SS / W;
+    constexpr int NT = 256;
+    constexpr int HMAX = 32 / Q;
+    const int64_t tile = blockIdx.x / nslices;
+    const int slice = (int)(blockIdx.x - tile * nslices);
+    const int lane = threadIdx.x % Q;
+    const int jv = slice * Q + lane;
+    const int jc = jv < NV ? jv : NV - 1;  // clamped (the tail lanes compute garbage, never stored)
+    const VT* hv = reinterpret_cast<const VT*>(hat) + jc;
+    const VT* dv0 = reinterpret_cast<const VT*>(symd) + jc;
+    const int64_t gb = tile_grp_ptr[tile], ge = tile_grp_ptr[tile + 1];
+    const int G = (int)(ge - gb);
+    int H = NT / (Q * (G > 0 ? G : 1));
+    H = H >= HMAX ? HMAX : H >= 4 ? 4 : H >= 2 ? 2 : 1;
+    const int u = threadIdx.x / Q;
+    const int h = u % H, gg = u / H, NG = NT / (Q * H);
+    for (int base = 0; base < G; base += NG) {
+        const int64_t g = gb + base + gg;
+        const bool gon = g < ge;
+        V acc[K][W];
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+#pragma unroll
+            for (int w = 0; w < W; ++w) acc[k][w] = cz<V>();
+        const int64_t e0 = gon ? grp_ent_ptr[g] : 0, e1 = gon ? grp_ent_ptr[g + 1] : 0;
+#pragma unroll 2
+        for (int64_t e = e0 + h; e < e1; e += H) {
+            const int4 a = __ldg(gent + 2 * e);
+            int id[8];
+            id[0] = a.x;
+            id[1] = a.y;
+            id[2] = a.z;
+            id[3] = a.w;
+            if constexpr (K > 3) {
+                const int4 b = __ldg(gent + 2 * e + 1);
+                id[4] = b.x;
+                id[5] = b.y;
+                id[6] = b.z;
+                id[7] = b.w;
+            }
+            const VT sv = __ldg(hv + (int64_t)id[0] * NV);
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const int d = id[1 + k];
+                if (d >= 0) {
+                    const VT dv = __ldg(dv0 + (int64_t)d * NV);
+                    if constexpr (W == 2) {
+                        acc[k][0] = cfma(make_float2(dv.x, dv.y), make_float2(sv.x, sv.y), acc[k][0]);
+                        acc[k][1] = cfma(make_float2(dv.z, dv.w), make_float2(sv.z, sv.w), acc[k][1]);
+                    } else {
+                        acc[k][0] = cfma(dv, sv, acc[k][0]);
+                    }
+                }
+            }
+        }
+        for (int off = (H / 2) * Q; off >= Q; off /= 2) {
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    acc[k][w].x += __shfl_down_sync(0xffffffffu, acc[k][w].x, off);
+                    acc[k][w].y += __shfl_down_sync(0xffffffffu, acc[k][w].y, off);
+                }
+        }
+        if (gon && h == 0 && jv < NV) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const int r = __ldg(grp_row + g * K + k);
+                if (r >= 0) {
+                    VT out;
+                    if constexpr (W == 2) {
+                        out = make_float4(acc[k][0].x, acc[k][0].y, acc[k][1].x, acc[k][1].y);
+                    } else {
+                        out = acc[k][0];
+                    }
+                    reinterpret_cast<VT*>(lhat)[(int64_t)r * NV + jv] = out;
+                }
+            }
+        }
+    }
+}
+
 // pruned inverse DFT of accumulated spectra (fourier.py:74-80), one CTA per row:
 // local[row_slot[r]] = F2L(lhat[r]); FP64 transform for both storage types
 template <typename R, int L>
@@ -2429,6 +2525,34 @@ int launch_m2l_tile(int32_t L, int32_t K, int64_t ntiles, int32_t max_ops, int32
 }
 
 template <typename R>
+int launch_m2l_tile_l1(int32_t L, int32_t K, int64_t ntiles, const int64_t* tile_grp_ptr, const int32_t* grp_row,
+                       const int64_t* grp_ent_ptr, const int32_t* gent, const void* hat, const void* symd,
+                       void* lhat, void* stream) {
+    if (ntiles == 0) return 0;
+    if (ntiles < 0 || (K != 2 && K != 4)) return -1;
+    cudaStream_t s = (cudaStream_t)stream;
+#define DEFMM_TL1_LAUNCH(KK, QQ)                                                                            \
+    {                                                                                                       \
+        const int nsl = (NV + QQ - 1) / QQ;                                                                 \
+        if (!grid_ok(ntiles * nsl)) return -1;                                                              \
+        carve(m2l_tile_l1_kernel<R, LL, KK, QQ>);                                                           \
+        m2l_tile_l1_kernel<R, LL, KK, QQ><<<(unsigned)(ntiles * nsl), 256, 0, s>>>(                         \
+            ntiles, nsl, tile_grp_ptr, grp_row, grp_ent_ptr, (const int4*)gent, (const cx<R>*)hat,           \
+            (const cx<R>*)symd, (cx<R>*)lhat);                                                              \
+    }
+    DEFMM_DISPATCH_L(L, {
+        constexpr int NV = spec_stride<R, LL>() / (sizeof(R) == 4 ? 2 : 1);
+        if (tile_q() == 8) {
+            if (K == 2) DEFMM_TL1_LAUNCH(2, 8) else DEFMM_TL1_LAUNCH(4, 8)
+        } else {
+            if (K == 2) DEFMM_TL1_LAUNCH(2, 4) else DEFMM_TL1_LAUNCH(4, 4)
+        }
+    });
+#undef DEFMM_TL1_LAUNCH
+    return report(cudaGetLastError(), "m2l_tile_l1");
+}
+
+template <typename R>
 int launch_f2l_rows(int32_t L, int64_t nrows, const int64_t* row_slot, const void* lhat, void* local,
                     void* stream) {
     if (nrows == 0) return 0;
@@ -2571,6 +2695,12 @@ const char* defmm_last_error(void) { return g_last_error; }
                                 const void* hat, const void* sym_derived, void* lhat, void* stream) {              \
         return launch_m2l_tile<R>(L, K, ntiles, max_ops, max_ent, tile_op_ptr, ops, tile_grp_ptr, grp_row,         \
                                   grp_ent_ptr, ent, hat, sym_derived, lhat, stream);                               \
+    }                                                                                                               \
+    int defmm_m2l_tile_l1_##SUFFIX(int32_t L, int32_t K, int64_t ntiles, const int64_t* tile_grp_ptr,            \
+                                   const int32_t* grp_row, const int64_t* grp_ent_ptr, const int32_t* gent,        \
+                                   const void* hat, const void* sym_derived, void* lhat, void* stream) {           \
+        return launch_m2l_tile_l1<R>(L, K, ntiles, tile_grp_ptr, grp_row, grp_ent_ptr, gent, hat, sym_derived,     \
+                                     lhat, stream);                                                                \
     }                                                                                                               \
     int defmm_f2l_rows_##SUFFIX(int32_t L, int64_t nrows, const int64_t* row_slot, const void* lhat, void* local,   \
                                 void* stream) {                                                                    \

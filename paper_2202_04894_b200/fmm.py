@@ -169,6 +169,7 @@ M2L_KERNELS = ("rows", "blocked", "pair", "triple", "quartet", "tile")
 TILE_K = int(os.environ.get("DEFMM_TILE_K", "4"))
 TILE_MAX_OPS = int(os.environ.get("DEFMM_TILE_OPS", "768"))
 TILE_MAX_EV = int(os.environ.get("DEFMM_TILE_EV", "4096"))
+TILE_L1 = os.environ.get("DEFMM_TILE_L1", "0") == "1"  # tiles without shared-memory staging (K7 v12)
 # events per parent-pair block above which a level counts as dense (blocked kernel)
 BLOCKED_MIN_EVENTS_PER_BLOCK = 32.0
 # "auto": other sparse levels with at least this many rows run the pair kernel
@@ -379,10 +380,23 @@ class FmmPlan:
         tl = h["tile"]
         self.n_tiles = int(tl["n"])
         self.tile_K, self.tile_max_ops, self.tile_max_ent = int(tl["K"]), int(tl["max_ops"]), int(tl.get("max_ent", 0))
+        self.tile_l1 = TILE_L1
         if self.n_tiles:
             self.tl = (_dev(tl["tile_op_ptr"], i64, d), _dev(tl["ops"], i32, d), _dev(tl["tile_grp_ptr"], i64, d),
                        _dev(tl["grp_lhat"].astype(np.int32), i32, d), _dev(tl["grp_ent_ptr"], i64, d),
                        _dev(tl["ent"].reshape(-1).view(np.int16), torch.int16, d))
+            self.tile_l1 = TILE_L1
+            if True:  # entries with global operand ids (the L1 variant)
+                e = tl["ent"].astype(np.int64)
+                tid = np.repeat(np.arange(tl["n"]), np.diff(tl["grp_ent_ptr"][tl["tile_grp_ptr"]]))
+                base = tl["tile_op_ptr"][tid][:, None]
+                ge = np.full((e.shape[0], 8), -1, np.int32)
+                ge[:, 0] = tl["ops"][base[:, 0] + e[:, 0]]
+                for k in range(int(tl["K"])):
+                    loc = e[:, 1 + k]
+                    ok = loc != 0xFFFF
+                    ge[ok, 1 + k] = -1 - tl["ops"][base[ok, 0] + loc[ok]]
+                self.tl_gent = _dev(ge.reshape(-1), i32, d)
         # downward
         self.l2l = []
         for lev, outs, octant, ptr, src, sdir in h["l2l"]:
@@ -631,11 +645,25 @@ class FmmPlan:
         return self._apply(out, stage_events)
 
     def _apply(self, out=None, stage_events=None):
+        # NVTX ranges per stage (the reference's stage timers, traversal.py:445-493)
+        nvtx = torch.cuda.nvtx
+        nvtx.range_push("defmm.matvec")
+        try:
+            return self._apply_stages(out, stage_events)
+        finally:
+            nvtx.range_pop()
+
+    def _apply_stages(self, out=None, stage_events=None):
+        nvtx = torch.cuda.nvtx
         if self.qhalo is not None:  # near-field source charges of the other chunks
             from .parallel import charge_exchange
 
+            nvtx.range_push("defmm.charge_halo")
             charge_exchange(self.q, self._qhalo_dev())
+            nvtx.range_pop()
+        nvtx.range_push("defmm.upward")
         self.apply_upward(stage_events)
+        nvtx.range_pop()
         if self.shard is not None:
             if self.allreduce is not None:
                 # M2M is linear: summing the partial multipoles over the ranks
@@ -644,8 +672,14 @@ class FmmPlan:
             else:
                 from .parallel import halo_exchange
 
+                nvtx.range_push("defmm.multipole_halo")
                 halo_exchange(self.mult, self._halo_dev())
-        return self.apply_rest(out, stage_events)
+                nvtx.range_pop()
+        nvtx.range_push("defmm.m2l_downward")
+        try:
+            return self.apply_rest(out, stage_events)
+        finally:
+            nvtx.range_pop()
 
     def halo_bytes(self) -> int:
         """Bytes this rank moves per matvec: the spanning multipoles it
@@ -771,7 +805,10 @@ class FmmPlan:
                           sh)
             _lib.call(self._op("m2l_blocked"), L, self.n_groups, self.grp_ptr, self.grp_rows, self.blk_src,
                       self.blk_trans, self.blk_mask, self.blk_kind, self.hat, self.sym_derived, self.lhat, sh)
-            if self.n_tiles:
+            if self.n_tiles and self.tile_l1:
+                _lib.call(self._op("m2l_tile_l1"), L, self.tile_K, self.n_tiles, self.tl[2], self.tl[3], self.tl[4],
+                          self.tl_gent, self.hat, self.sym_derived, self.lhat, sh)
+            elif self.n_tiles:
                 _lib.call(self._op("m2l_tile"), L, self.tile_K, self.n_tiles, self.tile_max_ops, self.tile_max_ent,
                           *self.tl, self.hat,
                           self.sym_derived, self.lhat, sh)

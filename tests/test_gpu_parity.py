@@ -175,6 +175,10 @@ def test_group_m2l_kernels_match_reference(case, dtype):
         a = p2.apply().cpu().numpy().astype(np.complex128)
         assert _rel(a, g["pot"]) <= (FP64_TOL if dtype == "c128" else C64_TOL)
         assert np.array_equal(p2.apply().cpu().numpy().astype(np.complex128), a)
+        if mode == "tiles_all":  # staged and L1-read tiles: same entries, same sums
+            p2.tile_l1 = True
+            b = p2.apply().cpu().numpy().astype(np.complex128)
+            assert np.array_equal(b, a)
 
 
 def test_linearity_in_the_charges():

@@ -117,9 +117,26 @@ def test_cfg1_plan_counts_match_reference_run():
     assert pl.hf_max == int(ref["hf_max"])
 
 
+@pytest.mark.parametrize("name,workload", [("cfg2", "cfg2"), ("cfg3", "cfg3"), ("cfg5", "cfg5"), ("cfg4_counts", "cfg4")])
+def test_full_size_plan_counts_match_reference_run(name, workload):
+    """Host plan (tree + native DTT) at BASELINE size: FmmInfo.counts and
+    hf_max equal the reference's own run (tests/golden/ref_*.npz)."""
+    ref = load_ref(name)
+    pts, q, k, w = make_workload(workload)
+    assert abs(k - float(ref["kappa"])) == 0.0
+    tr, ps = build_tree(pts, q, TreeConfig(ncrit=w.ncrit))
+    pl = build_plan(tr, tr, int(ref["order"]), k, 1.0, 2.0)
+    assert pl.counts == ref["counts"]
+    assert pl.hf_max == int(ref["hf_max"])
+
+
 def test_config_validation():
     with pytest.raises(ValueError):
         FmmConfig(order=1)
+    # boundary deviation: orders above 8 are refused (the reference accepts any order >= 2)
+    with pytest.raises(ValueError, match="orders 2..8"):
+        FmmConfig(order=9)
+    assert FmmConfig(order=8).order == 8
     with pytest.raises(ValueError):
         FmmConfig(strategy="dense")
     with pytest.raises(ValueError):
