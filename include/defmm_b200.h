@@ -100,31 +100,6 @@ int defmm_fma_peak(int32_t fp64, int64_t iters, void* out, void* stream);
  * 4 x grid vectors).  out: one float, written only to keep the loads live. */
 int defmm_l2_stream(const void* buf, int64_t n_vec, int32_t iters, int32_t ctas_per_sm, void* out, void* stream);
 
-/* ---- host: lists of the frequency-sliced tile M2L (K7 v11) ----------------
- * Rows ids[0..n_ids) (row r = local slot row_slot[r], entries [row_ptr[r],
- * row_ptr[r+1]) of ent = {source spectrum, derived symbol} int32 pairs, the
- * reference dtt's M2L events, traversal.py:320-342) are sorted by (level, key,
- * grandparent, parent, cell) and packed greedily, one parent group at a time
- * (row by row when a parent group alone is too large), into tiles of one
- * level and key whose distinct operands number <= max_ops and whose events
- * number <= max_ev; rows whose own operands / events exceed them go to
- * overflow[].  Outputs (caller allocates upper
- * bounds: n_ids rows / tiles / groups, 2 x events ops, events entries):
- * out_ids = tiled rows in tile order; tile t = operands ops[tile_op_ptr[t] ..
- * tile_op_ptr[t+1]) (sources ascending, then -1-symbol ascending) and groups
- * [tile_grp_ptr[t], tile_grp_ptr[t+1]); group g = rows grp_row[K g + k]
- * (index into out_ids, -1 absent; K <= 7 consecutive siblings) and entries
- * ent_out[8 e .. 8 e + 8), e in [grp_ent_ptr[g], grp_ent_ptr[g+1])
- * ({tile-local source, tile-local symbol of row k or 0xFFFF, 0 padding},
- * ascending source id).  counts = {tiles, rows, ops,
- * groups, entries, overflow rows}.  Returns 0, or -1 for invalid K / max_ops. */
-int defmm_m2l_tiles(int64_t n_ids, const int64_t* ids, const int64_t* row_slot, const int64_t* row_ptr,
-                    const int32_t* ent, const int64_t* l_cell, const int64_t* l_dir, const int64_t* level,
-                    const int64_t* parent, int64_t n_hat, int64_t n_trans, int32_t K, int32_t max_ops,
-                    int32_t max_ev, int64_t* out_ids, int64_t* tile_op_ptr, int32_t* ops, int64_t* tile_grp_ptr,
-                    int32_t* grp_row, int64_t* grp_ent_ptr, uint16_t* ent_out, int64_t* overflow,
-                    int64_t* counts);
-
 /* ---- device operators ------------------------------------------------------
  * Every operator exists as *_c128 (complex arrays are double2 = interleaved
  * FP64 re/im, exactly the reference's complex128; all arithmetic FP64) and
@@ -171,19 +146,6 @@ int defmm_m2l_tiles(int64_t n_ids, const int64_t* ids, const int64_t* row_slot, 
  *   K = 2, 8 for K = 4) = {source spectrum, derived symbol for row k or -1
  *   (k < K), 0 padding}; local[slot] = F2L(sum) -- the row kernel's sums,
  *   merged per source.
- *   K7 v11 frequency-sliced tile variant (m2l_tile, K = 2 or 4 rows per
- *   sibling group): CTA = (tile t, spectral slice); tile t stages its operands
- *   ops[tile_op_ptr[t] .. tile_op_ptr[t+1]) (v >= 0: spectrum v, v < 0:
- *   derived symbol -1-v; at most max_ops per tile) and its entries (at most
- *   max_ent per tile) and runs its sibling groups [tile_grp_ptr[t],
- *   tile_grp_ptr[t+1]): group g owns lhat rows grp_row[K g + k] (-1 absent)
- *   and entries [grp_ent_ptr[g], grp_ent_ptr[g+1]) of 8 uint16 = {tile-local
- *   source operand, tile-local symbol operand for row k or 0xFFFF, 0
- *   padding}: lhat[row] = sum D (*) hat (stride defmm_spectrum_stride), then
- *   f2l_rows.
- *   m2l_tile_l1: the same tiles and sums without shared-memory staging: gent
- *   = the entries with GLOBAL ids (int32 x 8: spectrum, derived symbol of row
- *   k or -1, -1 padding), operands read through L1; no max_ops limit.
  * K5 L2L -- traversal.py:355-391 in gather form.
  *   for i < n: local[out_slot[i]] += sum_{e in [ptr[i], ptr[i+1])}
  *   (C'0 (x) C'1 (x) C'2) local[src_slot[e]], C' the transposed/conjugate-
@@ -236,18 +198,6 @@ int defmm_m2l_tiles(int64_t n_ids, const int64_t* ids, const int64_t* row_slot, 
                                    const int32_t* blk_trans, const int64_t* blk_mask,           \
                                    const int8_t* blk_kind, const void* hat,                     \
                                    const void* sym_derived, void* lhat, void* stream);          \
-    int defmm_m2l_tile_##SUFFIX(int32_t L, int32_t K, int64_t ntiles, int32_t max_ops,           \
-                                int32_t max_ent,                                                 \
-                                const int64_t* tile_op_ptr, const int32_t* ops,                  \
-                                const int64_t* tile_grp_ptr, const int32_t* grp_row,             \
-                                const int64_t* grp_ent_ptr, const uint16_t* ent,                 \
-                                const void* hat, const void* sym_derived, void* lhat,            \
-                                void* stream);                                                   \
-    int defmm_m2l_tile_l1_##SUFFIX(int32_t L, int32_t K, int64_t ntiles,                          \
-                                   const int64_t* tile_grp_ptr, const int32_t* grp_row,           \
-                                   const int64_t* grp_ent_ptr, const int32_t* gent,               \
-                                   const void* hat, const void* sym_derived, void* lhat,          \
-                                   void* stream);                                                 \
     int defmm_f2l_rows_##SUFFIX(int32_t L, int64_t nrows, const int64_t* row_slot,               \
                                 const void* lhat, void* local, void* stream);                   \
     int defmm_l2l_##SUFFIX(int32_t L, int64_t n, const int64_t* out_slot, const int8_t* octant,  \
@@ -275,11 +225,11 @@ int defmm_m2l_tiles(int64_t n_ids, const int64_t* ids, const int64_t* row_slot, 
 
 /* expands to: defmm_p2m_c128 defmm_m2m_c128 defmm_m2f_c128 defmm_symbols_c128
  * defmm_expand_symbols_c128 defmm_m2l_rows_c128 defmm_m2l_group_c128 defmm_m2l_blocked_c128
- * defmm_m2l_tile_c128 defmm_m2l_tile_l1_c128 defmm_f2l_rows_c128 defmm_l2l_c128 defmm_l2p_c128 defmm_p2p_c128 */
+ * defmm_f2l_rows_c128 defmm_l2l_c128 defmm_l2p_c128 defmm_p2p_c128 */
 DEFMM_DECLARE_TYPED(c128)
 /* expands to: defmm_p2m_c64 defmm_m2m_c64 defmm_m2f_c64 defmm_symbols_c64
  * defmm_expand_symbols_c64 defmm_m2l_rows_c64 defmm_m2l_group_c64 defmm_m2l_blocked_c64
- * defmm_m2l_tile_c64 defmm_m2l_tile_l1_c64 defmm_f2l_rows_c64 defmm_l2l_c64 defmm_l2p_c64 defmm_p2p_c64 */
+ * defmm_f2l_rows_c64 defmm_l2l_c64 defmm_l2p_c64 defmm_p2p_c64 */
 DEFMM_DECLARE_TYPED(c64)
 
 /* Spectral layout of order L (HOST call, no device needed): every spectrum is

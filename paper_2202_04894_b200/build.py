@@ -21,7 +21,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CU_SOURCES = ["defmm_kernels.cu", "fma_peak.cu"]
-CPP_SOURCES = ["tree_build.cpp", "dtt_build.cpp", "m2l_tiles.cpp"]
+CPP_SOURCES = ["tree_build.cpp", "dtt_build.cpp"]
 
 
 def _run(cmd):

@@ -1302,246 +1302,6 @@ __global__ void __launch_bounds__(m2lb_threads<R, L>(), DEFMM_M2LB_MINBLOCKS) m2
     }
 }
 
-// ---------------------------------------------------------------------------
-// K7 v11: frequency-sliced tile M2L.  The M2L stream is bound by the L2 -> SM
-// fabric (round 1: the sibling-quartet kernel moves ~1 spectrum per event from
-// L2 at 84% of the measured L2 -> SM rate), so the only lever is fewer bytes
-// per event.  A TILE = the rows of one grandparent cell and key (<= 64 rows,
-// fewer when the tile's operands exceed the shared-memory budget) shares its
-// source spectra and its (level, translation) symbols across all its rows:
-// on cfg2 the distinct operands of a grandparent tile are 0.18-0.24 per event
-// (0.58-0.66 per parent, 2 per row).  The Hadamard product is independent per
-// frequency, so a CTA takes one tile and one 128-B SLICE of the spectrum
-// (16 complex64 / 8 complex128 positions): it stages the slice of every tile
-// operand into shared memory once (cp.async, 16 B per thread), then runs the
-// tile's sibling groups (K rows of one parent, entries merged per source
-// spectrum, as in m2l_group_kernel) from shared memory: Q = 8 threads cover
-// the slice (16 B each), 32 thread-groups per CTA walk the groups.  The
-// partial spectra go to lhat (stride SS), f2l_rows_kernel transforms them.
-// Same per-row summation order as m2l_group_kernel; no atomics.
-#ifndef DEFMM_TILE_NT
-#define DEFMM_TILE_NT 512
-#endif
-constexpr int TILE_NT = DEFMM_TILE_NT;
-constexpr int TILE_ES = 8;  // uint16 per entry: {source, symbol of row k < K <= 7 or 0xFFFF, padding}
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool on) {
-    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
-    const int n = on ? 16 : 0;  // src-size 0: zero-fill
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n) : "memory");
-}
-// Q threads cover one operand slice (16 B each); a tile's sibling groups are
-// spread over the CTA, and when a tile has few groups each group's entries are
-// split H ways (H x Q <= 32, partial sums combined by warp shuffles in a fixed
-// order), so small tiles still keep the CTA busy.  One CTA per tile walks all
-// spectral slices: the tile's entries are staged into shared memory once, the
-// operand slices are double-buffered (slice s + 1 is copied in while slice s
-// is computed).
-template <typename R, int L, int K, int Q>
-__global__ void __launch_bounds__(TILE_NT) m2l_tile_kernel(
-    int64_t ntiles, int max_ops, const int64_t* __restrict__ tile_op_ptr, const int32_t* __restrict__ ops,
-    const int64_t* __restrict__ tile_grp_ptr, const int32_t* __restrict__ grp_row,
-    const int64_t* __restrict__ grp_ent_ptr, const uint16_t* __restrict__ ent, const cx<R>* __restrict__ hat,
-    const cx<R>* __restrict__ symd, cx<R>* __restrict__ lhat) {
-    using V = cx<R>;
-    using VT = std::conditional_t<sizeof(R) == 4, float4, double2>;
-    constexpr int W = sizeof(R) == 4 ? 2 : 1;  // complex entries per 16-B lane
-    constexpr int SS = spec_stride<R, L>();
-    constexpr int NV = SS / W;                 // 16-B vectors per spectrum
-    constexpr int NSL = (NV + Q - 1) / Q;      // spectral slices
-    constexpr int HMAX = 32 / Q;
-    extern __shared__ __align__(16) unsigned char smraw[];
-    VT* buf0 = reinterpret_cast<VT*>(smraw);  // [max_ops][Q], two buffers
-    VT* buf1 = buf0 + (size_t)max_ops * Q;
-    uint4* sent = reinterpret_cast<uint4*>(buf1 + (size_t)max_ops * Q);  // the tile's entries
-    const int64_t tile = blockIdx.x;
-    const int64_t o0 = tile_op_ptr[tile], o1 = tile_op_ptr[tile + 1];
-    const int nops = (int)(o1 - o0);
-    const int lane = threadIdx.x % Q;
-    const int64_t gb = tile_grp_ptr[tile], ge = tile_grp_ptr[tile + 1];
-    const int64_t eb = grp_ent_ptr[gb], ee = grp_ent_ptr[ge];
-    auto stage = [&](VT* dst, int slice) {  // the slice of every operand (v < 0: derived symbol -1-v)
-        for (int t = threadIdx.x; t < nops * Q; t += TILE_NT) {
-            const int o = t / Q, l = t % Q;
-            const int v = __ldg(ops + o0 + o);
-            const int j = slice * Q + l;
-            const VT* base = v >= 0 ? reinterpret_cast<const VT*>(hat) + (int64_t)v * NV
-                                    : reinterpret_cast<const VT*>(symd) + (int64_t)(-1 - v) * NV;
-            cp_async16(dst + t, base + (j < NV ? j : 0), j < NV);
-        }
-    };
-    const uint4* gent = reinterpret_cast<const uint4*>(ent) + eb;
-    for (int t = threadIdx.x; t < (int)(ee - eb); t += TILE_NT) cp_async16(sent + t, gent + t, true);
-    stage(buf0, 0);
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-    const int G = (int)(ge - gb);
-    int H = TILE_NT / (Q * (G > 0 ? G : 1));
-    H = H >= HMAX ? HMAX : H >= 4 ? 4 : H >= 2 ? 2 : 1;
-    const int u = threadIdx.x / Q;
-    const int h = u % H, gg = u / H, NG = TILE_NT / (Q * H);
-    for (int slice = 0; slice < NSL; ++slice) {
-        VT* op = (slice & 1) ? buf1 : buf0;
-        if (slice + 1 < NSL) stage((slice & 1) ? buf0 : buf1, slice + 1);
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
-        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-        __syncthreads();
-        const int jv = slice * Q + lane;  // this thread's 16-B vector of every spectrum
-        for (int base = 0; base < G; base += NG) {  // uniform trip count per CTA
-            const int64_t g = gb + base + gg;
-            const bool gon = g < ge;
-            V acc[K][W];
-#pragma unroll
-            for (int k = 0; k < K; ++k)
-#pragma unroll
-                for (int w = 0; w < W; ++w) acc[k][w] = cz<V>();
-            const int e0 = gon ? (int)(grp_ent_ptr[g] - eb) : 0, e1 = gon ? (int)(grp_ent_ptr[g + 1] - eb) : 0;
-#pragma unroll 2
-            for (int e = e0 + h; e < e1; e += H) {
-                const uint4 en = sent[e];
-                const uint16_t idx[8] = {(uint16_t)(en.x & 0xffff), (uint16_t)(en.x >> 16),
-                                         (uint16_t)(en.y & 0xffff), (uint16_t)(en.y >> 16),
-                                         (uint16_t)(en.z & 0xffff), (uint16_t)(en.z >> 16),
-                                         (uint16_t)(en.w & 0xffff), (uint16_t)(en.w >> 16)};
-                const VT sv = op[idx[0] * Q + lane];
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    const int d = idx[1 + k];
-                    if (d != 0xffff) {
-                        const VT dv = op[d * Q + lane];
-                        if constexpr (W == 2) {
-                            acc[k][0] = cfma(make_float2(dv.x, dv.y), make_float2(sv.x, sv.y), acc[k][0]);
-                            acc[k][1] = cfma(make_float2(dv.z, dv.w), make_float2(sv.z, sv.w), acc[k][1]);
-                        } else {
-                            acc[k][0] = cfma(dv, sv, acc[k][0]);
-                        }
-                    }
-                }
-            }
-            // combine the H entry-split partial sums (lanes Q apart, fixed tree order)
-            for (int off = (H / 2) * Q; off >= Q; off /= 2) {
-#pragma unroll
-                for (int k = 0; k < K; ++k)
-#pragma unroll
-                    for (int w = 0; w < W; ++w) {
-                        acc[k][w].x += __shfl_down_sync(0xffffffffu, acc[k][w].x, off);
-                        acc[k][w].y += __shfl_down_sync(0xffffffffu, acc[k][w].y, off);
-                    }
-            }
-            if (gon && h == 0 && jv < NV) {
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    const int r = __ldg(grp_row + g * K + k);
-                    if (r >= 0) {
-                        VT out;
-                        if constexpr (W == 2) {
-                            out = make_float4(acc[k][0].x, acc[k][0].y, acc[k][1].x, acc[k][1].y);
-                        } else {
-                            out = acc[k][0];
-                        }
-                        reinterpret_cast<VT*>(lhat)[(int64_t)r * NV + jv] = out;
-                    }
-                }
-            }
-        }
-        __syncthreads();  // the buffer is refilled two slices later
-    }
-}
-
-// K7 v12: the same tiles without shared-memory staging: CTA = (tile, slice of
-// Q 16-B vectors), entries carry GLOBAL operand ids (int32 x 8: source,
-// derived symbol of row k < K or -1), operands are read with LDG through L1,
-// which keeps the slice of the tile's operands after the first touch (no
-// barriers: warps progress independently).
-template <typename R, int L, int K, int Q>
-__global__ void __launch_bounds__(256) m2l_tile_l1_kernel(
-    int64_t ntiles, int nslices, const int64_t* __restrict__ tile_grp_ptr, const int32_t* __restrict__ grp_row,
-    const int64_t* __restrict__ grp_ent_ptr, const int4* __restrict__ gent, const cx<R>* __restrict__ hat,
-    const cx<R>* __restrict__ symd, cx<R>* __restrict__ lhat) {
-    using V = cx<R>;
-    using VT = std::conditional_t<sizeof(R) == 4, float4, double2>;
-    constexpr int W = sizeof(R) == 4 ? 2 : 1;
-    constexpr int SS = spec_stride<R, L>();
-    constexpr int NV = SS / W;
-    constexpr int NT = 256;
-    constexpr int HMAX = 32 / Q;
-    const int64_t tile = blockIdx.x / nslices;
-    const int slice = (int)(blockIdx.x - tile * nslices);
-    const int lane = threadIdx.x % Q;
-    const int jv = slice * Q + lane;
-    const int jc = jv < NV ? jv : NV - 1;  // clamped (the tail lanes compute garbage, never stored)
-    const VT* hv = reinterpret_cast<const VT*>(hat) + jc;
-    const VT* dv0 = reinterpret_cast<const VT*>(symd) + jc;
-    const int64_t gb = tile_grp_ptr[tile], ge = tile_grp_ptr[tile + 1];
-    const int G = (int)(ge - gb);
-    int H = NT / (Q * (G > 0 ? G : 1));
-    H = H >= HMAX ? HMAX : H >= 4 ? 4 : H >= 2 ? 2 : 1;
-    const int u = threadIdx.x / Q;
-    const int h = u % H, gg = u / H, NG = NT / (Q * H);
-    for (int base = 0; base < G; base += NG) {
-        const int64_t g = gb + base + gg;
-        const bool gon = g < ge;
-        V acc[K][W];
-#pragma unroll
-        for (int k = 0; k < K; ++k)
-#pragma unroll
-            for (int w = 0; w < W; ++w) acc[k][w] = cz<V>();
-        const int64_t e0 = gon ? grp_ent_ptr[g] : 0, e1 = gon ? grp_ent_ptr[g + 1] : 0;
-#pragma unroll 2
-        for (int64_t e = e0 + h; e < e1; e += H) {
-            const int4 a = __ldg(gent + 2 * e);
-            int id[8];
-            id[0] = a.x;
-            id[1] = a.y;
-            id[2] = a.z;
-            id[3] = a.w;
-            if constexpr (K > 3) {
-                const int4 b = __ldg(gent + 2 * e + 1);
-                id[4] = b.x;
-                id[5] = b.y;
-                id[6] = b.z;
-                id[7] = b.w;
-            }
-            const VT sv = __ldg(hv + (int64_t)id[0] * NV);
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const int d = id[1 + k];
-                if (d >= 0) {
-                    const VT dv = __ldg(dv0 + (int64_t)d * NV);
-                    if constexpr (W == 2) {
-                        acc[k][0] = cfma(make_float2(dv.x, dv.y), make_float2(sv.x, sv.y), acc[k][0]);
-                        acc[k][1] = cfma(make_float2(dv.z, dv.w), make_float2(sv.z, sv.w), acc[k][1]);
-                    } else {
-                        acc[k][0] = cfma(dv, sv, acc[k][0]);
-                    }
-                }
-            }
-        }
-        for (int off = (H / 2) * Q; off >= Q; off /= 2) {
-#pragma unroll
-            for (int k = 0; k < K; ++k)
-#pragma unroll
-                for (int w = 0; w < W; ++w) {
-                    acc[k][w].x += __shfl_down_sync(0xffffffffu, acc[k][w].x, off);
-                    acc[k][w].y += __shfl_down_sync(0xffffffffu, acc[k][w].y, off);
-                }
-        }
-        if (gon && h == 0 && jv < NV) {
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const int r = __ldg(grp_row + g * K + k);
-                if (r >= 0) {
-                    VT out;
-                    if constexpr (W == 2) {
-                        out = make_float4(acc[k][0].x, acc[k][0].y, acc[k][1].x, acc[k][1].y);
-                    } else {
-                        out = acc[k][0];
-                    }
-                    reinterpret_cast<VT*>(lhat)[(int64_t)r * NV + jv] = out;
-                }
-            }
-        }
-    }
-}
-
 // pruned inverse DFT of accumulated spectra (fourier.py:74-80), one CTA per row:
 // local[row_slot[r]] = F2L(lhat[r]); FP64 transform for both storage types
 template <typename R, int L>
@@ -2485,73 +2245,6 @@ int launch_m2l_blocked(int32_t L, int64_t ngroups, const int64_t* grp_ptr, const
     return report(cudaGetLastError(), "m2l_blocked");
 }
 
-// DEFMM_TILE_Q = 4 (64-B operand slices, default) or 8 (128 B)
-inline int tile_q() {
-    static const int q = [] {
-        const char* e = getenv("DEFMM_TILE_Q");
-        return e && atoi(e) == 8 ? 8 : 4;
-    }();
-    return q;
-}
-template <typename R>
-int launch_m2l_tile(int32_t L, int32_t K, int64_t ntiles, int32_t max_ops, int32_t max_ent,
-                    const int64_t* tile_op_ptr, const int32_t* ops, const int64_t* tile_grp_ptr,
-                    const int32_t* grp_row, const int64_t* grp_ent_ptr, const uint16_t* ent, const void* hat,
-                    const void* symd, void* lhat, void* stream) {
-    if (ntiles == 0) return 0;
-    if (ntiles < 0 || max_ops < 1 || max_ent < 0 || (K != 2 && K != 4)) return -1;
-    const size_t bytes = 2 * (size_t)max_ops * tile_q() * 16 + (size_t)max_ent * TILE_ES * 2;
-    if (bytes > 227 * 1024) return -1;
-    cudaStream_t s = (cudaStream_t)stream;
-#define DEFMM_TILE_LAUNCH(KK, QQ)                                                                           \
-    {                                                                                                       \
-        if (!grid_ok(ntiles)) return -1;                                                                    \
-        int rc = set_smem(m2l_tile_kernel<R, LL, KK, QQ>, bytes);                                           \
-        if (rc) return rc;                                                                                  \
-        carve(m2l_tile_kernel<R, LL, KK, QQ>);                                                              \
-        m2l_tile_kernel<R, LL, KK, QQ><<<(unsigned)ntiles, TILE_NT, bytes, s>>>(                            \
-            ntiles, max_ops, tile_op_ptr, ops, tile_grp_ptr, grp_row, grp_ent_ptr, ent, (const cx<R>*)hat,   \
-            (const cx<R>*)symd, (cx<R>*)lhat);                                                              \
-    }
-    DEFMM_DISPATCH_L(L, {
-        if (tile_q() == 8) {
-            if (K == 2) DEFMM_TILE_LAUNCH(2, 8) else DEFMM_TILE_LAUNCH(4, 8)
-        } else {
-            if (K == 2) DEFMM_TILE_LAUNCH(2, 4) else DEFMM_TILE_LAUNCH(4, 4)
-        }
-    });
-#undef DEFMM_TILE_LAUNCH
-    return report(cudaGetLastError(), "m2l_tile");
-}
-
-template <typename R>
-int launch_m2l_tile_l1(int32_t L, int32_t K, int64_t ntiles, const int64_t* tile_grp_ptr, const int32_t* grp_row,
-                       const int64_t* grp_ent_ptr, const int32_t* gent, const void* hat, const void* symd,
-                       void* lhat, void* stream) {
-    if (ntiles == 0) return 0;
-    if (ntiles < 0 || (K != 2 && K != 4)) return -1;
-    cudaStream_t s = (cudaStream_t)stream;
-#define DEFMM_TL1_LAUNCH(KK, QQ)                                                                            \
-    {                                                                                                       \
-        const int nsl = (NV + QQ - 1) / QQ;                                                                 \
-        if (!grid_ok(ntiles * nsl)) return -1;                                                              \
-        carve(m2l_tile_l1_kernel<R, LL, KK, QQ>);                                                           \
-        m2l_tile_l1_kernel<R, LL, KK, QQ><<<(unsigned)(ntiles * nsl), 256, 0, s>>>(                         \
-            ntiles, nsl, tile_grp_ptr, grp_row, grp_ent_ptr, (const int4*)gent, (const cx<R>*)hat,           \
-            (const cx<R>*)symd, (cx<R>*)lhat);                                                              \
-    }
-    DEFMM_DISPATCH_L(L, {
-        constexpr int NV = spec_stride<R, LL>() / (sizeof(R) == 4 ? 2 : 1);
-        if (tile_q() == 8) {
-            if (K == 2) DEFMM_TL1_LAUNCH(2, 8) else DEFMM_TL1_LAUNCH(4, 8)
-        } else {
-            if (K == 2) DEFMM_TL1_LAUNCH(2, 4) else DEFMM_TL1_LAUNCH(4, 4)
-        }
-    });
-#undef DEFMM_TL1_LAUNCH
-    return report(cudaGetLastError(), "m2l_tile_l1");
-}
-
 template <typename R>
 int launch_f2l_rows(int32_t L, int64_t nrows, const int64_t* row_slot, const void* lhat, void* local,
                     void* stream) {
@@ -2688,19 +2381,6 @@ const char* defmm_last_error(void) { return g_last_error; }
                                    void* stream) {                                                                \
         return launch_m2l_blocked<R>(L, ngroups, grp_ptr, grp_rows, blk_src, blk_trans, blk_mask, blk_kind, hat,   \
                                      sym_derived, lhat, stream);                                                  \
-    }                                                                                                               \
-    int defmm_m2l_tile_##SUFFIX(int32_t L, int32_t K, int64_t ntiles, int32_t max_ops, int32_t max_ent,       \
-                                const int64_t* tile_op_ptr, const int32_t* ops, const int64_t* tile_grp_ptr,       \
-                                const int32_t* grp_row, const int64_t* grp_ent_ptr, const uint16_t* ent,          \
-                                const void* hat, const void* sym_derived, void* lhat, void* stream) {              \
-        return launch_m2l_tile<R>(L, K, ntiles, max_ops, max_ent, tile_op_ptr, ops, tile_grp_ptr, grp_row,         \
-                                  grp_ent_ptr, ent, hat, sym_derived, lhat, stream);                               \
-    }                                                                                                               \
-    int defmm_m2l_tile_l1_##SUFFIX(int32_t L, int32_t K, int64_t ntiles, const int64_t* tile_grp_ptr,            \
-                                   const int32_t* grp_row, const int64_t* grp_ent_ptr, const int32_t* gent,        \
-                                   const void* hat, const void* sym_derived, void* lhat, void* stream) {           \
-        return launch_m2l_tile_l1<R>(L, K, ntiles, tile_grp_ptr, grp_row, grp_ent_ptr, gent, hat, sym_derived,     \
-                                     lhat, stream);                                                                \
     }                                                                                                               \
     int defmm_f2l_rows_##SUFFIX(int32_t L, int64_t nrows, const int64_t* row_slot, const void* lhat, void* local,   \
                                 void* stream) {                                                                    \

@@ -88,45 +88,6 @@ def m2l_groups(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent, K: int = 2
     return {"n": ng, "K": K, "grp_slot": grp_slot.reshape(-1), "grp_ptr": grp_ptr, "ent": out}
 
 
-def m2l_slice_tiles(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent, K: int = 4, max_ops: int = 768,
-                    max_ev: int = 4096) -> dict:
-    """Lists of the frequency-sliced tile M2L (K7 v11, defmm_m2l_tile_*),
-    built natively (defmm_m2l_tiles): the rows ``ids`` (indices into
-    ``rows``) packed into tiles of one level and key with <= ``max_ops``
-    distinct operands and <= ``max_ev`` events, K-row sibling groups with
-    entries merged per source (8 uint16 each).
-    ``ids`` of the result = tiled rows in tile order (``grp_row`` indexes it);
-    rows whose own operands exceed max_ops are returned in ``overflow``."""
-    import ctypes as C
-
-    ids = np.ascontiguousarray(ids, np.int64)
-    E = 8
-    n = ids.shape[0]
-    ent = np.ascontiguousarray(ent, np.int32)
-    n_ev = int((np.asarray(row_ptr)[ids + 1] - np.asarray(row_ptr)[ids]).sum()) if n else 0
-    out = {"out_ids": np.zeros(max(n, 1), np.int64), "tile_op_ptr": np.zeros(n + 1, np.int64),
-           "ops": np.zeros(max(2 * n_ev, 1), np.int32), "tile_grp_ptr": np.zeros(n + 1, np.int64),
-           "grp_row": np.zeros(max(n * K, 1), np.int32), "grp_ent_ptr": np.zeros(n + 1, np.int64),
-           "ent": np.zeros((max(n_ev, 1), E), np.uint16), "overflow": np.zeros(max(n, 1), np.int64),
-           "counts": np.zeros(6, np.int64)}
-    i64 = lambda a: np.ascontiguousarray(a, np.int64)  # noqa: E731
-    keep = [ids, i64(rows), i64(row_ptr), ent, i64(l_cell), i64(l_dir), i64(level), i64(parent)]
-    a = lambda x: x.ctypes.data_as(C.c_void_p)  # noqa: E731
-    n_hat = int(ent[:, 0].max()) + 1 if ent.size else 1
-    n_trans = int(ent[:, 1].max()) + 1 if ent.size else 1
-    _lib.check(_lib.load().defmm_m2l_tiles(n, *[a(x) for x in keep], n_hat, n_trans, int(K), int(max_ops), int(max_ev),
-                                           *[a(out[k]) for k in ("out_ids", "tile_op_ptr", "ops", "tile_grp_ptr",
-                                                                 "grp_row", "grp_ent_ptr", "ent", "overflow",
-                                                                 "counts")]), "defmm_m2l_tiles")
-    nt, nr, no, ng, ne, nov = (int(x) for x in out["counts"])
-    gptr, eptr = out["tile_grp_ptr"][: nt + 1], out["grp_ent_ptr"][: ng + 1]
-    max_ent = int(np.diff(eptr[gptr]).max()) if nt else 0
-    return {"n": nt, "K": K, "max_ops": int(max_ops), "max_ent": max_ent, "tile_op_ptr": out["tile_op_ptr"][: nt + 1],
-            "ops": out["ops"][:no], "tile_grp_ptr": out["tile_grp_ptr"][: nt + 1],
-            "grp_row": out["grp_row"][: ng * K].astype(np.int64), "grp_ent_ptr": out["grp_ent_ptr"][: ng + 1],
-            "ent": out["ent"][:ne], "overflow": out["overflow"][:nov], "ids": out["out_ids"][:nr]}
-
-
 def m2l_pairs(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent) -> dict:
     """K = 2 sibling groups (m2l_groups)."""
     return m2l_groups(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent, 2)
@@ -157,19 +118,12 @@ def _sub_csr(ptr, keep):
 
 # M2L kernel per level for each mode: (dense level, sparse level)
 M2L_MODE_KINDS = {
-    "auto": ("blocked", "rows"), "hybrid_rows": ("blocked", "rows"), "tiles": ("blocked", "tile"),
-    "tiles_all": ("tile", "tile"),
+    "auto": ("blocked", "rows"), "hybrid_rows": ("blocked", "rows"),
     "rows": ("rows", "rows"), "blocked_all": ("blocked", "blocked"),
     "pairs": ("blocked", "pair"), "pairs_all": ("pair", "pair"), "quartets": ("blocked", "quartet"),
     "quartets_all": ("quartet", "quartet"), "triples_all": ("triple", "triple"),
 }
-M2L_KERNELS = ("rows", "blocked", "pair", "triple", "quartet", "tile")
-# sliced-tile M2L (K7 v11): rows per sibling group and operand budget per tile
-# (shared memory = TILE_MAX_OPS x 128 B); env DEFMM_TILE_K / DEFMM_TILE_OPS for sweeps
-TILE_K = int(os.environ.get("DEFMM_TILE_K", "4"))
-TILE_MAX_OPS = int(os.environ.get("DEFMM_TILE_OPS", "768"))
-TILE_MAX_EV = int(os.environ.get("DEFMM_TILE_EV", "4096"))
-TILE_L1 = os.environ.get("DEFMM_TILE_L1", "0") == "1"  # tiles without shared-memory staging (K7 v12)
+M2L_KERNELS = ("rows", "blocked", "pair", "triple", "quartet")
 # events per parent-pair block above which a level counts as dense (blocked kernel)
 BLOCKED_MIN_EVENTS_PER_BLOCK = 32.0
 # "auto": other sparse levels with at least this many rows run the pair kernel
@@ -377,26 +331,6 @@ class FmmPlan:
                 self.sib_groups.append((gr["K"], int(gr["n"]), _dev(gr["grp_slot"], i64, d),
                                         _dev(gr["grp_ptr"], i64, d), _dev(gr["ent"].reshape(-1), i32, d)))
         self.n_pairs = sum(x[1] for x in self.sib_groups)
-        tl = h["tile"]
-        self.n_tiles = int(tl["n"])
-        self.tile_K, self.tile_max_ops, self.tile_max_ent = int(tl["K"]), int(tl["max_ops"]), int(tl.get("max_ent", 0))
-        self.tile_l1 = TILE_L1
-        if self.n_tiles:
-            self.tl = (_dev(tl["tile_op_ptr"], i64, d), _dev(tl["ops"], i32, d), _dev(tl["tile_grp_ptr"], i64, d),
-                       _dev(tl["grp_lhat"].astype(np.int32), i32, d), _dev(tl["grp_ent_ptr"], i64, d),
-                       _dev(tl["ent"].reshape(-1).view(np.int16), torch.int16, d))
-            self.tile_l1 = TILE_L1
-            if True:  # entries with global operand ids (the L1 variant)
-                e = tl["ent"].astype(np.int64)
-                tid = np.repeat(np.arange(tl["n"]), np.diff(tl["grp_ent_ptr"][tl["tile_grp_ptr"]]))
-                base = tl["tile_op_ptr"][tid][:, None]
-                ge = np.full((e.shape[0], 8), -1, np.int32)
-                ge[:, 0] = tl["ops"][base[:, 0] + e[:, 0]]
-                for k in range(int(tl["K"])):
-                    loc = e[:, 1 + k]
-                    ok = loc != 0xFFFF
-                    ge[ok, 1 + k] = -1 - tl["ops"][base[ok, 0] + loc[ok]]
-                self.tl_gent = _dev(ge.reshape(-1), i32, d)
         # downward
         self.l2l = []
         for lev, outs, octant, ptr, src, sdir in h["l2l"]:
@@ -501,14 +435,8 @@ class FmmPlan:
         def pick(*ks):
             return np.isin(rkind, list(ks)) if rows.size else np.zeros(0, bool)
 
-        # sliced tiles (K7 v11); rows whose own operands overflow a tile -> row kernel
-        h["tile"] = m2l_slice_tiles(np.nonzero(pick("tile"))[0], rows, h["row_ptr"], h["ent"], p.l_cell, p.l_dir,
-                                    tt.level, tt.parent, TILE_K, TILE_MAX_OPS, TILE_MAX_EV)
         # row kernel
         is_rows = pick("rows")
-        if h["tile"]["overflow"].size:
-            is_rows = is_rows.copy()
-            is_rows[h["tile"]["overflow"]] = True
         _, rptr, rsel = _sub_csr(h["row_ptr"], is_rows)
         h["rk_rows"], h["rk_ptr"], h["rk_ent"] = rows[is_rows], rptr, h["ent"][rsel]
         # sibling pairs (K7 v8)
@@ -518,12 +446,10 @@ class FmmPlan:
                                  tt.level, tt.parent, 3)
         h["quartet"] = m2l_groups(np.nonzero(pick("quartet"))[0], rows, h["row_ptr"], h["ent"], p.l_cell, p.l_dir,
                                   tt.level, tt.parent, 4)
-        # lhat rows: blocked rows, then tile rows
+        # lhat rows = the blocked rows
         is_grp = pick("blocked")
         grp_rows = rows[is_grp]
-        tl = h["tile"]
-        h["bk_rows"] = np.concatenate([grp_rows, rows[tl["ids"]]])
-        tl["grp_lhat"] = np.where(tl["grp_row"] >= 0, grp_rows.shape[0] + tl["grp_row"], -1)
+        h["bk_rows"] = grp_rows
         # groups of blocked levels, rows renumbered into lhat
         gr = h["grp_rows"]
         gr_slots = np.where(gr >= 0, rows[np.maximum(gr, 0)] if rows.size else -1, -1)
@@ -805,13 +731,6 @@ class FmmPlan:
                           sh)
             _lib.call(self._op("m2l_blocked"), L, self.n_groups, self.grp_ptr, self.grp_rows, self.blk_src,
                       self.blk_trans, self.blk_mask, self.blk_kind, self.hat, self.sym_derived, self.lhat, sh)
-            if self.n_tiles and self.tile_l1:
-                _lib.call(self._op("m2l_tile_l1"), L, self.tile_K, self.n_tiles, self.tl[2], self.tl[3], self.tl[4],
-                          self.tl_gent, self.hat, self.sym_derived, self.lhat, sh)
-            elif self.n_tiles:
-                _lib.call(self._op("m2l_tile"), L, self.tile_K, self.n_tiles, self.tile_max_ops, self.tile_max_ent,
-                          *self.tl, self.hat,
-                          self.sym_derived, self.lhat, sh)
             _lib.call(self._op("f2l_rows"), L, self.bk_rows.shape[0], self.bk_rows, self.lhat, self.local, sh)
         elif self.m2l_variant == "derived":
             _lib.call(self._op("m2l_rows"), L, self.row_slot.shape[0], self.row_slot, self.row_ptr,
@@ -906,7 +825,6 @@ class FmmPlan:
                            (sum(x[1] for x in self.sib_groups if x[0] == 3), f"{gk}<3>", "triple"),
                            (sum(x[1] for x in self.sib_groups if x[0] == 4), f"{gk}<4>", "quartet"),
                            (self.n_groups, "m2l_blocked_kernel", "blocked"),
-                           (self.n_tiles, f"m2l_tile_kernel<{self.tile_K}>", "tile"),
                            (self.bk_rows.shape[0], "f2l_rows_kernel", None)):
             if n:
                 out.append(f"{name}<{R}, {self.L}>" + (f" (levels {lv(k)})" if k is not None else ""))
@@ -917,7 +835,7 @@ class FmmPlan:
         """Kernels of one matvec: p2p (+ split reduce), p2m, m2m per level, m2f,
         the M2L kernels with work, l2l per level, l2p."""
         if self.m2l_variant == "hybrid":
-            m2l = len(self.sib_groups) + sum(int(n > 0) for n in (self.rk_rows.shape[0], self.n_groups, self.n_tiles,
+            m2l = len(self.sib_groups) + sum(int(n > 0) for n in (self.rk_rows.shape[0], self.n_groups,
                                                                    self.bk_rows.shape[0]))
         else:
             m2l = 1

@@ -398,7 +398,7 @@ def test_m2l_level_policy(case):
     lv0 = int(levels[0])
     assert m2l_level_kinds("auto", "c64", levels, dense, {lv0: "pair"})[lv0] == "pair"
     assert m2l_level_kinds("rows", "c64", levels, dense, env=f"{lv0}:quartet")[lv0] == "quartet"
-    for gone in ("quad", "slice"):  # round-1 variants measured slower and removed
+    for gone in ("quad", "slice", "tile"):  # variants measured slower and removed (profiles/r02)
         with pytest.raises(ValueError):
             m2l_level_kinds("auto", "c64", levels, dense, override={lv0: gone})
     with pytest.raises(ValueError):
@@ -449,48 +449,3 @@ def test_p2p_overlap_policy():
     assert p2p_overlap_policy({3: "pair", 4: "blocked"}) == ("upward", False)
     assert p2p_overlap_policy({4: "quartet", 5: "blocked"}) == ("upward", False)
     assert p2p_overlap_policy({}) == ("upward", False)
-
-
-@pytest.mark.parametrize("case", ["cubesurf4000", "volume3000", "c1_kd16"])
-@pytest.mark.parametrize("K,max_ops,max_ev", [(2, 64, 4096), (4, 200, 300), (7, 1536, 100000), (4, 30, 4096)])
-def test_m2l_slice_tiles_reconstruct_every_event(case, K, max_ops, max_ev):
-    """defmm_m2l_tiles (sliced-tile M2L lists): every M2L event of the tiled
-    rows appears exactly once, with its spectrum and derived symbol, through
-    tile-local operand ids; tiles hold <= max_ops distinct operands of one
-    level and key; a group's rows are siblings and its entries ascend by
-    source; rows whose own operands exceed max_ops overflow."""
-    from paper_2202_04894_b200.fmm import m2l_slice_tiles
-
-    tr, _, p = _plan(load_case(case))
-    rows, ptr, ent = p.m2l_row_slot, p.m2l_row_ptr, p.m2l_rows_entries
-    ids = np.arange(rows.shape[0])
-    t = m2l_slice_tiles(ids, rows, ptr, ent, p.l_cell, p.l_dir, tr.level, tr.parent, K, max_ops, max_ev)
-    own = np.array([len(np.unique(ent[ptr[r]:ptr[r + 1], 0])) + len(np.unique(ent[ptr[r]:ptr[r + 1], 1]))
-                    for r in ids])
-    assert set(t["overflow"].tolist()) == set(np.nonzero((own > max_ops) | (np.diff(ptr) > max_ev))[0].tolist())
-    assert sorted(t["ids"].tolist() + t["overflow"].tolist()) == ids.tolist()
-    got = []
-    for k in range(t["n"]):
-        ops = t["ops"][t["tile_op_ptr"][k]:t["tile_op_ptr"][k + 1]]
-        assert len(ops) <= max_ops and len(np.unique(ops)) == len(ops)
-        tile_rows = []
-        for g in range(t["tile_grp_ptr"][k], t["tile_grp_ptr"][k + 1]):
-            gr = t["grp_row"][g * K:(g + 1) * K]
-            rr = [int(t["ids"][x]) for x in gr if x >= 0]
-            assert len({int(tr.parent[p.l_cell[rows[r]]]) for r in rr}) == 1
-            tile_rows += rr
-            e0, e1 = t["grp_ent_ptr"][g], t["grp_ent_ptr"][g + 1]
-            ev_tile = 0
-            srcs = ops[t["ent"][e0:e1, 0].astype(np.int64)]
-            assert np.all(srcs >= 0) and np.all(np.diff(srcs) > 0)
-            for e in range(e0, e1):
-                for kk in range(K):
-                    y = int(t["ent"][e, 1 + kk])
-                    if y != 0xFFFF:
-                        assert gr[kk] >= 0 and ops[y] < 0
-                        got.append((int(t["ids"][gr[kk]]), int(ops[t["ent"][e, 0]]), int(-1 - ops[y])))
-        keys = {(int(tr.level[p.l_cell[rows[r]]]), int(p.l_dir[rows[r]])) for r in tile_rows}
-        assert len(keys) == 1
-    tiled = set(t["ids"].tolist())
-    ref = [(int(r), int(ent[e, 0]), int(ent[e, 1])) for r in ids if r in tiled for e in range(ptr[r], ptr[r + 1])]
-    assert sorted(got) == sorted(ref)

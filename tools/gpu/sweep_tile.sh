@@ -3,7 +3,7 @@ cd $GRAFT_REPO_ROOT
 timeout 900 python -m pytest tests/test_gpu_parity.py -q -k "canonical or group_m2l" > gpurun_out/st_tests.log 2>&1
 B="python bench.py --steps 5 --warmup 2 --no-cpu-baseline --no-secondary"
 timeout 300 $B > gpurun_out/st_auto.log 2>&1
-for Q in 4 8; do for K in 2 4; do for OPS in 256 768 2048; do for EV in 4096; do
+for Q in 8; do for K in 4; do for OPS in 2048 4096; do for EV in 4096 16384; do
   DEFMM_TILE_L1=1 DEFMM_TILE_Q=$Q DEFMM_TILE_K=$K DEFMM_TILE_OPS=$OPS DEFMM_TILE_EV=$EV timeout 300 $B --m2l-levels tiles > gpurun_out/st_${Q}_${K}_${OPS}_${EV}.log 2>&1
 done; done; done; done
 python - > gpurun_out/st_summary.txt <<'PY'
