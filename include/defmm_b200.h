@@ -87,6 +87,15 @@ int defmm_dtt_source_hats(const defmm_dtt* d, const int64_t* m_dense, const int6
                           int32_t* src_hat, int64_t* hat_slot, int64_t* n_hat);
 void defmm_dtt_free(defmm_dtt* d);
 
+/* ---- host: stage packing of the staged M2L (K7 v13) --------------------------
+ * Classes c < ncls (ordered; cls_cta[c] non-decreasing) read the symbols
+ * cls_sym[cls_ptr[c] .. cls_ptr[c+1]) (ids < n_sym_ids).  Greedy, in order: a
+ * class joins the current stage of its CTA while the stage's DISTINCT symbols
+ * stay <= ns_cap, else it opens the next one.  cls_stage_rel[c] = stage index
+ * within the CTA.  -2 if a class alone exceeds ns_cap. */
+int defmm_stage_pack(int64_t ncls, const int64_t* cls_cta, const int64_t* cls_ptr, const int64_t* cls_sym,
+                     int64_t n_sym_ids, int32_t ns_cap, int64_t* cls_stage_rel);
+
 /* ---- FMA peak probe (measurement only) --------------------------------------
  * Launches 4 x SMs CTAs of 256 threads, each thread running 8 independent FMA
  * chains for iters x 16 steps: flops = 2 * 8 * 16 * iters * threads.  fp64
@@ -146,6 +155,17 @@ int defmm_l2_stream(const void* buf, int64_t n_vec, int32_t iters, int32_t ctas_
  *   K = 2, 8 for K = 4) = {source spectrum, derived symbol for row k or -1
  *   (k < K), 0 padding}; local[slot] = F2L(sum) -- the row kernel's sums,
  *   merged per source.
+ *   K7 v13 staged variant (m2l_stage): CTA c = 8 "warp units" (a target parent's <= 4
+ *   sibling rows each, same level and key, neighbouring parents) x one spectral slice of
+ *   <= 32 16-B vectors (grid = ncta x slices of the order).  Its stages
+ *   [cta_stage[c], cta_stage[c+1]) hold the derived symbols slot_sym[stage_slot_ptr[s] ..
+ *   stage_slot_ptr[s+1]) (<= ns_cap per stage), copied once per CTA into a shared-memory
+ *   ring of `depth` stages (2..8; depth x (ns_cap+1) slices must fit 227 KB);
+ *   warp unit w of CTA c owns the entries [cta_went[8c+w], ...) = int32 pairs {source
+ *   spectrum, 4 bytes: shared-memory slot of row k's symbol, ns_cap = none}, those of stage s
+ *   ending at stage_wend[8 cta_stage[c] + w n_c + (s - cta_stage[c])], n_c = the CTA's stage count
+ *   (the entry array is readable 64 entries past its end);
+ *   lhat[cta_rows[4(8c+w)+k]] = sum (row index, -1 absent); then K8 f2l_rows.
  * K5 L2L -- traversal.py:355-391 in gather form.
  *   for i < n: local[out_slot[i]] += sum_{e in [ptr[i], ptr[i+1])}
  *   (C'0 (x) C'1 (x) C'2) local[src_slot[e]], C' the transposed/conjugate-
@@ -193,6 +213,12 @@ int defmm_l2_stream(const void* buf, int64_t n_vec, int32_t iters, int32_t ctas_
     int defmm_m2l_group_##SUFFIX(int32_t L, int32_t K, int64_t ngroups, const int64_t* grp_slot,  \
                                  const int64_t* grp_ptr, const int32_t* entries, const void* hat, \
                                  const void* sym_derived, void* local, void* stream);             \
+    int defmm_m2l_stage_##SUFFIX(int32_t L, int64_t ncta, int32_t ns_cap, int32_t depth,             \
+                                 const int32_t* cta_stage,                                          \
+                                 const int32_t* cta_went, const int32_t* stage_slot_ptr,            \
+                                 const int32_t* slot_sym, const int32_t* stage_wend,                \
+                                 const int32_t* entries, const int32_t* cta_rows, const void* hat,  \
+                                 const void* sym_derived, void* lhat, void* stream);                \
     int defmm_m2l_blocked_##SUFFIX(int32_t L, int64_t ngroups, const int64_t* grp_ptr,           \
                                    const int64_t* grp_rows, const int32_t* blk_src,             \
                                    const int32_t* blk_trans, const int64_t* blk_mask,           \
@@ -224,11 +250,11 @@ int defmm_l2_stream(const void* buf, int64_t n_vec, int32_t iters, int32_t ctas_
                            void* stream);
 
 /* expands to: defmm_p2m_c128 defmm_m2m_c128 defmm_m2f_c128 defmm_symbols_c128
- * defmm_expand_symbols_c128 defmm_m2l_rows_c128 defmm_m2l_group_c128 defmm_m2l_blocked_c128
+ * defmm_expand_symbols_c128 defmm_m2l_rows_c128 defmm_m2l_group_c128 defmm_m2l_stage_c128 defmm_m2l_blocked_c128
  * defmm_f2l_rows_c128 defmm_l2l_c128 defmm_l2p_c128 defmm_p2p_c128 */
 DEFMM_DECLARE_TYPED(c128)
 /* expands to: defmm_p2m_c64 defmm_m2m_c64 defmm_m2f_c64 defmm_symbols_c64
- * defmm_expand_symbols_c64 defmm_m2l_rows_c64 defmm_m2l_group_c64 defmm_m2l_blocked_c64
+ * defmm_expand_symbols_c64 defmm_m2l_rows_c64 defmm_m2l_group_c64 defmm_m2l_stage_c64 defmm_m2l_blocked_c64
  * defmm_f2l_rows_c64 defmm_l2l_c64 defmm_l2p_c64 defmm_p2p_c64 */
 DEFMM_DECLARE_TYPED(c64)
 

@@ -29,6 +29,7 @@ _SIGS = {
     "defmm_dtt_translations": [_vp, _vp],
     "defmm_dtt_source_hats": [_vp] * 6 + [_i64, _vp, _vp, _vp],
     "defmm_dtt_free": [_vp],
+    "defmm_stage_pack": [_i64, _vp, _vp, _vp, _i64, _i32, _vp],
     "defmm_fma_peak": [_i32, _i64, _vp, _vp],
     "defmm_l2_stream": [_vp, _i64, _i32, _i32, _vp, _vp],
     "defmm_m2l_canon_c128": [_i32, _i64] + [_vp] * 9,
@@ -47,6 +48,7 @@ for _t in ("c128", "c64"):
         f"defmm_m2l_rows_{_t}": [_i32, _i64] + [_vp] * 7,
         f"defmm_m2l_blocked_{_t}": [_i32, _i64] + [_vp] * 10,
         f"defmm_m2l_group_{_t}": [_i32, _i32, _i64] + [_vp] * 7,
+        f"defmm_m2l_stage_{_t}": [_i32, _i64, _i32, _i32] + [_vp] * 11,
         f"defmm_f2l_rows_{_t}": [_i32, _i64, _vp, _vp, _vp, _vp],
         f"defmm_l2l_{_t}": [_i32, _i64, _vp, _vp, _vp, _vp, _vp, _f64, _vp, _f64, _vp, _vp],
         f"defmm_l2p_{_t}": [_i32, _i64] + [_vp] * 13 + [_f64, _vp, _vp, _vp, _vp, _vp],

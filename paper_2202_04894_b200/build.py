@@ -21,7 +21,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CU_SOURCES = ["defmm_kernels.cu", "fma_peak.cu"]
-CPP_SOURCES = ["tree_build.cpp", "dtt_build.cpp"]
+CPP_SOURCES = ["tree_build.cpp", "dtt_build.cpp", "m2l_stage.cpp"]
 
 
 def _run(cmd):
@@ -45,7 +45,8 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
         o = os.path.join(BUILD, src + ".o")
         if force or _stale(o, [s, header]):
             cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                   "-Xcompiler", "-ffp-contract=off", "-c", s, "-o", o]
+                   "-Xcompiler", "-ffp-contract=off", "-diag-suppress", "177",
+                   *os.environ.get("DEFMM_NVCC_FLAGS", "").split(), "-c", s, "-o", o]
             if verbose_ptxas:
                 cmd.insert(1, "-Xptxas=-v")
             _run(cmd)

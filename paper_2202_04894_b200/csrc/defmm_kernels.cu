@@ -1127,6 +1127,262 @@ __global__ void __launch_bounds__(m2l_block<R, L>(), group_min_blocks<R, L, K>()
 }
 
 // ---------------------------------------------------------------------------
+// K7 v13: staged M2L.  The sibling-group kernel above moves ~1.3 spectra
+// L2 -> SM per event (one symbol per event, a source per ~3 events) and is
+// bound by that fabric (profiles/r02/summary_v2.md).  A derived symbol depends
+// only on (level, key, t - s): the target parents of one (level, key) that lie
+// next to each other read the SAME symbols for the same parent-relative source
+// offset u = s - 2 parent.  So here a CTA owns NW = 8 neighbouring "warp
+// units" (a target parent's <= K = 4 sibling rows each, same level and key)
+// and one spectral slice of <= 32 16-B vectors; its classes (distinct u) are
+// packed into stages of <= ns_cap symbol slices, which a producer warp copies
+// ONCE per CTA into a shared-memory ring (cp.async.bulk, complete_tx on the
+// stage's "full" mbarrier).  Each consumer warp walks its own entries of the
+// stage -- {source spectrum, ring slot of row k's symbol or 0xff} -- with the
+// source slice prefetched PF entries ahead into registers (LDG) and the
+// symbols read from the ring (LDS.128), then releases the stage through its
+// "empty" mbarrier.  No CTA-wide barrier in the loop.  The accumulated slices
+// go to lhat; f2l_rows_kernel applies the inverse DFT.
+__device__ __forceinline__ uint32_t sm32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(sm32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sm32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(sm32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}\n" ::"r"(sm32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     sm32(dst)),
+                 "l"(src), "r"(bytes), "r"(sm32(b))
+                 : "memory");
+}
+
+// (c0, c1) += a * (b0, b1): one packed FP32 FMA (FFMA2) with a scalar multiplier
+__device__ __forceinline__ void ffma2(float& c0, float& c1, float a, float b0, float b1) {
+    float2 av = make_float2(a, a), bv = make_float2(b0, b1), cv = make_float2(c0, c1);
+    uint64_t ua = *reinterpret_cast<uint64_t*>(&av), ub = *reinterpret_cast<uint64_t*>(&bv);
+    uint64_t uc = *reinterpret_cast<uint64_t*>(&cv);
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(uc) : "l"(ua), "l"(ub));
+    cv = *reinterpret_cast<float2*>(&uc);
+    c0 = cv.x;
+    c1 = cv.y;
+}
+__device__ __forceinline__ void ffma2(double&, double&, double, double, double) {}  // c128: not used
+
+#ifndef DEFMM_STAGE_MINB
+#define DEFMM_STAGE_MINB 3
+#endif
+constexpr int STG_NW = 8;     // consumer warps (warp units) per CTA
+constexpr int STG_K = 4;      // rows per warp unit
+constexpr int STG_MAXDEPTH = 8;  // ring stages (runtime depth <= this)
+constexpr int STG_PF = 4;     // source slices in flight per warp (the loop is unrolled 4-way)
+
+template <typename R, int L>
+struct StageCfg {
+    static constexpr int W = sizeof(R) == 4 ? 2 : 1;              // complex entries per 16-B vector
+    static constexpr int NV = spec_stride<R, L>() / W;            // vectors per spectrum
+    static constexpr int NSLICE = (NV + 31) / 32;                 // spectral slices (grid.y role)
+    static constexpr int SW = (NV + NSLICE - 1) / NSLICE;         // vectors (= lanes) per slice
+    static constexpr int SB = SW * 16;                            // bytes per ring slot
+};
+
+// ring buffer b: slots [0, ns_cap) filled by the producer, slot ns_cap = zeros
+// (the entries name it for an absent row, so the loop has no branch per row)
+template <typename R, int L>
+__global__ void __launch_bounds__(32 * (STG_NW + 1), DEFMM_STAGE_MINB)
+    m2l_stage_kernel(int ns_cap, int depth, const int* __restrict__ cta_stage, const int* __restrict__ cta_went,
+                     const int* __restrict__ stage_slot_ptr, const int* __restrict__ slot_sym,
+                     const int* __restrict__ stage_wend, const int2* __restrict__ ent,
+                     const int* __restrict__ cta_rows, const cx<R>* __restrict__ hat,
+                     const cx<R>* __restrict__ symd, cx<R>* __restrict__ lhat) {
+    using C = StageCfg<R, L>;
+    constexpr bool VEC = sizeof(R) == 4;
+    using VT = std::conditional_t<VEC, float4, double2>;
+    constexpr int NV = C::NV, SW = C::SW, SB = C::SB, NW = STG_NW, K = STG_K, PF = STG_PF;
+    extern __shared__ __align__(128) unsigned char smraw[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
+    uint64_t* empty = full + STG_MAXDEPTH;
+    unsigned char* ring = smraw + 128;  // [depth][ns_cap + 1][SB]
+    const uint32_t bufb = (uint32_t)(ns_cap + 1) * SB;
+    const int cta = blockIdx.x / C::NSLICE, slice = blockIdx.x % C::NSLICE;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int v0 = slice * SW;
+    const int nvec = min(SW, NV - v0);  // vectors of this slice (> 0)
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < depth; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    for (int t = threadIdx.x; t < depth * (SB / 16); t += blockDim.x)  // the zero slots
+        reinterpret_cast<float4*>(ring + (size_t)(t / (SB / 16)) * bufb + (size_t)ns_cap * SB)[t % (SB / 16)] =
+            make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+    const int st0 = cta_stage[cta], nst = cta_stage[cta + 1] - st0;
+    if (warp == NW) {  // producer warp: one bulk copy per symbol slice
+        const unsigned char* sb = reinterpret_cast<const unsigned char*>(symd) + (size_t)v0 * 16;
+        const uint32_t bytes = (uint32_t)nvec * 16u;
+        int p0 = stage_slot_ptr[st0];
+        int p1 = nst > 0 ? stage_slot_ptr[st0 + 1] : p0;
+        // the next stage's symbol ids are fetched before waiting for its buffer
+        int id0 = p0 + lane < p1 ? __ldg(slot_sym + p0 + lane) : 0;
+        int id1 = p0 + lane + 32 < p1 ? __ldg(slot_sym + p0 + lane + 32) : 0;
+        int buf = 0, round = 0;
+        for (int i = 0; i < nst; ++i) {
+            const int q1 = i + 1 < nst ? stage_slot_ptr[st0 + i + 2] : p1;
+            const int n0 = p1 + lane < q1 ? __ldg(slot_sym + p1 + lane) : 0;
+            const int n1 = p1 + lane + 32 < q1 ? __ldg(slot_sym + p1 + lane + 32) : 0;
+            if (round > 0) mbar_wait(&empty[buf], (uint32_t)((round - 1) & 1));
+            if (lane == 0) mbar_expect_tx(&full[buf], (uint32_t)(p1 - p0) * bytes);
+            __syncwarp();
+            unsigned char* dst = ring + (size_t)buf * bufb;
+            if (p0 + lane < p1) bulk_g2s(dst + (size_t)lane * SB, sb + (size_t)id0 * (NV * 16), bytes, &full[buf]);
+            if (p0 + lane + 32 < p1)
+                bulk_g2s(dst + (size_t)(lane + 32) * SB, sb + (size_t)id1 * (NV * 16), bytes, &full[buf]);
+            for (int j = p0 + lane + 64; j < p1; j += 32)  // ns_cap > 64
+                bulk_g2s(dst + (size_t)(j - p0) * SB, sb + (size_t)__ldg(slot_sym + j) * (NV * 16), bytes, &full[buf]);
+            p0 = p1;
+            p1 = q1;
+            id0 = n0;
+            id1 = n1;
+            if (++buf == depth) {
+                buf = 0;
+                ++round;
+            }
+        }
+        return;
+    }
+    // lanes past the slice repeat its last vector (no predicates in the loop)
+    const int lc = min(lane, nvec - 1);
+    const VT* hv = reinterpret_cast<const VT*>(hat) + v0 + lc;
+    // complex64: two packed accumulators per (row, frequency), P += s.re * (d.re, d.im) and
+    // Q += s.im * (d.re, d.im) -- one FFMA2 each with the source part as the scalar
+    // operand; sum = (P.x - Q.y, P.y + Q.x) at the end.  complex128: plain FP64 FMAs.
+    constexpr int NA = VEC ? 8 : 2;
+    R acc[K][NA];
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int c = 0; c < NA; ++c) acc[k][c] = 0;
+    const int cw = cta * NW + warp;
+    int i = cta_went[cw];
+    // stage ends of this warp: stage_wend[st0 NW + warp nst + s]
+    const int* wend = stage_wend + (size_t)st0 * NW + (size_t)warp * nst;
+    const int e_total = nst > 0 ? wend[nst - 1] : i;
+    // entries in chunks of 32 (one per lane) advancing by 32 - PF, so entry j and the
+    // prefetched j + PF are both in the current chunk; broadcast by shuffles
+    constexpr int CH = 32 - PF;
+    int cbase = i;
+    int2 cur = __ldg(ent + cbase + lane), nxt = __ldg(ent + cbase + CH + lane);
+    VT srcq[PF];
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {  // entries past e_total are other warps' (or padding): valid sources
+        const int sid = __shfl_sync(0xffffffffu, cur.x, u);
+        srcq[u] = __ldg(hv + (size_t)sid * NV);
+    }
+    int buf = 0, round = 0, phase = 0;
+    int nxt_end = nst > 0 ? wend[0] : i;
+    const uint32_t ring32 = sm32(ring) + (uint32_t)lc * 16u;
+    for (int st = 0; st < nst; ++st) {
+        const int end = nxt_end;  // the next stage's end is requested a stage ahead
+        nxt_end = st + 1 < nst ? __ldg(wend + st + 1) : e_total;
+        mbar_wait(&full[buf], (uint32_t)(round & 1));
+        const uint32_t rb = ring32 + (uint32_t)buf * bufb;
+        // one entry, source in ring register U (static index); the next source of that
+        // register (entry i + PF) is requested once the entry's products are issued
+#define DEFMM_STAGE_BODY(U)                                                                          \
+    {                                                                                                \
+        const int j = i - cbase;                                                                     \
+        const uint32_t slots = (uint32_t)__shfl_sync(0xffffffffu, cur.y, j);                         \
+        const int sidn = __shfl_sync(0xffffffffu, cur.x, j + PF);                                    \
+        const VT s = srcq[U];                                                                        \
+        _Pragma("unroll") for (int k = 0; k < K; ++k) {                                              \
+            const uint32_t addr = __byte_perm(slots, 0u, 0x4440u + k) * (uint32_t)SB + rb;           \
+            if constexpr (VEC) {                                                                     \
+                float4 d;                                                                            \
+                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"                              \
+                             : "=f"(d.x), "=f"(d.y), "=f"(d.z), "=f"(d.w)                            \
+                             : "r"(addr));                                                           \
+                ffma2(acc[k][0], acc[k][1], s.x, d.x, d.y);                                          \
+                ffma2(acc[k][2], acc[k][3], s.y, d.x, d.y);                                          \
+                ffma2(acc[k][4], acc[k][5], s.z, d.z, d.w);                                          \
+                ffma2(acc[k][6], acc[k][7], s.w, d.z, d.w);                                          \
+            } else {                                                                                 \
+                double2 d;                                                                           \
+                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(d.x), "=d"(d.y) : "r"(addr)); \
+                acc[k][0] = fma(d.x, s.x, acc[k][0]);                                                \
+                acc[k][0] = fma(-d.y, s.y, acc[k][0]);                                               \
+                acc[k][1] = fma(d.x, s.y, acc[k][1]);                                                \
+                acc[k][1] = fma(d.y, s.x, acc[k][1]);                                                \
+            }                                                                                        \
+        }                                                                                            \
+        srcq[U] = __ldg(hv + (size_t)sidn * NV); /* after the last use of s: lands in place */      \
+        ++i;                                                                                         \
+    }
+        while (i < end) {
+            if (i - cbase >= CH) {  // next chunk of entries (every 28th entry)
+                cur = nxt;
+                cbase += CH;
+                nxt = __ldg(ent + cbase + CH + lane);
+            }
+            const int lim = min(end, cbase + CH);
+            // enter the 4-way unrolled sequence at the ring position of entry i
+            if (phase == 1) goto stage_l1;
+            if (phase == 2) goto stage_l2;
+            if (phase == 3) goto stage_l3;
+        stage_l0:
+            if (i >= lim) { phase = 0; goto stage_done; }
+            DEFMM_STAGE_BODY(0)
+        stage_l1:
+            if (i >= lim) { phase = 1; goto stage_done; }
+            DEFMM_STAGE_BODY(1)
+        stage_l2:
+            if (i >= lim) { phase = 2; goto stage_done; }
+            DEFMM_STAGE_BODY(2)
+        stage_l3:
+            if (i >= lim) { phase = 3; goto stage_done; }
+            DEFMM_STAGE_BODY(3)
+            goto stage_l0;
+        stage_done:;
+        }
+#undef DEFMM_STAGE_BODY
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[buf]);
+        if (++buf == depth) {
+            buf = 0;
+            ++round;
+        }
+    }
+    if (lane < nvec) {
+        VT* lv = reinterpret_cast<VT*>(lhat) + v0 + lane;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int row = cta_rows[(size_t)cw * K + k];
+            if (row >= 0) {
+                if constexpr (VEC) {
+                    lv[(size_t)row * NV] = make_float4(acc[k][0] - acc[k][3], acc[k][1] + acc[k][2],
+                                                       acc[k][4] - acc[k][7], acc[k][5] + acc[k][6]);
+                } else {
+                    lv[(size_t)row * NV] = make_double2(acc[k][0], acc[k][1]);
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K7 v3: parent-pair blocked M2L.  A CTA owns a group = (target parent P,
 // key) with up to 8 target rows (its children a); a block = (group, source
 // parent Q) holds up to 8 source spectra (children b) and, per child offset
@@ -2233,6 +2489,28 @@ int launch_m2l_group(int32_t L, int32_t K, int64_t ngroups, const int64_t* grp_s
 }
 
 template <typename R>
+int launch_m2l_stage(int32_t L, int64_t ncta, int32_t ns_cap, int32_t depth, const int32_t* cta_stage,
+                     const int32_t* cta_went, const int32_t* stage_slot_ptr, const int32_t* slot_sym,
+                     const int32_t* stage_wend, const int32_t* entries, const int32_t* cta_rows, const void* hat,
+                     const void* symd, void* lhat, void* stream) {
+    if (ncta == 0) return 0;
+    if (ns_cap < 8 || ns_cap > 254 || depth < 2 || depth > STG_MAXDEPTH) return -1;
+    cudaStream_t s = (cudaStream_t)stream;
+    DEFMM_DISPATCH_L(L, {
+        using C = StageCfg<R, LL>;
+        if (!grid_ok(ncta * C::NSLICE)) return -1;
+        const size_t bytes = 128 + (size_t)depth * (ns_cap + 1) * C::SB;
+        if (bytes > 227 * 1024) return -1;
+        int rc = set_smem(m2l_stage_kernel<R, LL>, bytes);
+        if (rc) return rc;
+        m2l_stage_kernel<R, LL><<<(unsigned)(ncta * C::NSLICE), 32 * (STG_NW + 1), bytes, s>>>(
+            ns_cap, depth, cta_stage, cta_went, stage_slot_ptr, slot_sym, stage_wend, (const int2*)entries,
+            cta_rows, (const cx<R>*)hat, (const cx<R>*)symd, (cx<R>*)lhat);
+    });
+    return report(cudaGetLastError(), "m2l_stage");
+}
+
+template <typename R>
 int launch_m2l_blocked(int32_t L, int64_t ngroups, const int64_t* grp_ptr, const int64_t* grp_rows,
                        const int32_t* blk_src, const int32_t* blk_trans, const int64_t* blk_mask,
                        const int8_t* blk_kind, const void* hat, const void* symd, void* lhat, void* stream) {
@@ -2374,6 +2652,14 @@ const char* defmm_last_error(void) { return g_last_error; }
                                  const int64_t* grp_ptr, const int32_t* entries, const void* hat,                 \
                                  const void* sym_derived, void* local, void* stream) {                            \
         return launch_m2l_group<R>(L, K, ngroups, grp_slot, grp_ptr, entries, hat, sym_derived, local, stream);   \
+    }                                                                                                               \
+    int defmm_m2l_stage_##SUFFIX(int32_t L, int64_t ncta, int32_t ns_cap, int32_t depth,                           \
+                                 const int32_t* cta_stage, const int32_t* cta_went,                               \
+                                 const int32_t* stage_slot_ptr, const int32_t* slot_sym,                          \
+                                 const int32_t* stage_wend, const int32_t* entries, const int32_t* cta_rows,      \
+                                 const void* hat, const void* sym_derived, void* lhat, void* stream) {            \
+        return launch_m2l_stage<R>(L, ncta, ns_cap, depth, cta_stage, cta_went, stage_slot_ptr, slot_sym,         \
+                                   stage_wend, entries, cta_rows, hat, sym_derived, lhat, stream);                \
     }                                                                                                               \
     int defmm_m2l_blocked_##SUFFIX(int32_t L, int64_t ngroups, const int64_t* grp_ptr, const int64_t* grp_rows,     \
                                    const int32_t* blk_src, const int32_t* blk_trans, const int64_t* blk_mask,     \

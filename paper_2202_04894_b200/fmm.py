@@ -93,6 +93,145 @@ def m2l_pairs(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent) -> dict:
     return m2l_groups(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent, 2)
 
 
+STAGE_NW, STAGE_K = 8, 4  # warp units per CTA, rows per warp unit (STG_NW, STG_K of the kernel)
+STAGE_SLOTS = 48  # symbol slices per shared-memory stage (ns_cap)
+STAGE_DEPTH = 3  # shared-memory ring stages
+STAGE_ENT_PAD = 64  # readable entries past the end (STG_ENT_PAD)
+
+
+def m2l_stage_lists(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent, coords, hat_coords,
+                    ns_cap: int = STAGE_SLOTS) -> dict:
+    """Lists of the staged M2L (K7 v13, defmm_m2l_stage_*).  The rows ``ids``
+    (indices into ``rows``) are grouped by (level, key, target parent) into warp
+    units of <= STAGE_K sibling rows; STAGE_NW consecutive warp units of one
+    (level, key) form a CTA.  An event (row, source s) belongs to the class
+    u = coords(s) - 2 coords(parent): within a CTA the symbols of a class are
+    shared by every warp unit.  Classes are packed in order into stages of <=
+    ns_cap distinct symbols; per (warp unit, class) one entry {source spectrum,
+    4 bytes: stage slot of row k's symbol or 0xff}.  ``hat_coords``: (n_hat, 3)
+    grid coordinates of each spectrum's source cell."""
+    K, NW = STAGE_K, STAGE_NW
+    i32 = np.int32
+    if ids.size == 0:
+        return {"n": 0, "ns_cap": ns_cap, "row_slot": np.zeros(0, np.int64), "cta_stage": np.zeros(1, i32),
+                "cta_went": np.zeros(0, i32), "stage_slot_ptr": np.zeros(1, i32), "slot_sym": np.zeros(0, i32),
+                "stage_wend": np.zeros(0, i32), "ent": np.zeros((STAGE_ENT_PAD, 2), i32),
+                "cta_rows": np.zeros(0, i32)}
+    slots = rows[ids]
+    cell = l_cell[slots]
+    key = l_dir[slots].astype(np.int64)
+    lev = level[cell].astype(np.int64)
+    par = parent[cell].astype(np.int64)
+    o = np.lexsort((cell, par, key, lev))
+    ids, slots, key, lev, par = ids[o], slots[o], key[o], lev[o], par[o]
+    n = ids.shape[0]
+    newp = np.ones(n, bool)
+    newp[1:] = (lev[1:] != lev[:-1]) | (key[1:] != key[:-1]) | (par[1:] != par[:-1])
+    pstart = np.nonzero(newp)[0]
+    pos = np.arange(n) - pstart[np.cumsum(newp) - 1]
+    kk = pos % K  # row index within its warp unit
+    wu = np.cumsum(kk == 0) - 1  # warp unit of each row
+    first = np.nonzero(kk == 0)[0]
+    nwu = first.shape[0]
+    w_lev, w_key = lev[first], key[first]
+    newc = np.ones(nwu, bool)  # new (level, key) chunk of warp units
+    newc[1:] = (w_lev[1:] != w_lev[:-1]) | (w_key[1:] != w_key[:-1])
+    cstart = np.nonzero(newc)[0]
+    posw = np.arange(nwu) - cstart[np.cumsum(newc) - 1]
+    ww = posw % NW  # warp of each warp unit
+    cta_of_wu = np.cumsum(ww == 0) - 1
+    ncta = int(cta_of_wu[-1]) + 1
+    cta_rows = np.full((ncta * NW, K), -1, i32)
+    cta_rows[cta_of_wu[wu] * NW + ww[wu], kk] = np.arange(n)  # lhat row = position in the sorted order
+    # events
+    cnt = row_ptr[ids + 1] - row_ptr[ids]
+    rep = np.repeat(np.arange(n), cnt)
+    sel = np.repeat(row_ptr[ids] - np.concatenate([[0], np.cumsum(cnt)[:-1]]), cnt) + np.arange(int(cnt.sum()))
+    e_src = ent[sel, 0].astype(np.int64)
+    e_tr = ent[sel, 1].astype(np.int64)
+    e_wu = wu[rep]
+    e_cw = cta_of_wu[e_wu] * NW + ww[e_wu]  # (CTA, warp)
+    e_cta = cta_of_wu[e_wu]
+    u = hat_coords[e_src] - 2 * coords[par[rep]]
+    off = int(np.abs(u).max()) + 1 if u.size else 1
+    nbit = max(int(2 * off + 1).bit_length(), 1)
+    # classes = distinct (CTA, u) in Morton order of u: classes that follow
+    # each other then read neighbouring translations, i.e. largely the same
+    # symbols (sym(o - u) = sym(o' - u') whenever o - u = o' - u')
+    ucode = np.zeros(u.shape[0], np.int64)
+    for b in range(nbit):
+        for a in range(3):
+            ucode |= (((u[:, a] + off) >> b) & 1) << (3 * b + 2 - a)
+    span3 = np.int64(1) << (3 * nbit)
+    ckey = e_cta * span3 + ucode
+    cuniq, e_cls = np.unique(ckey, return_inverse=True)
+    e_cls = e_cls.reshape(-1)
+    ncls = cuniq.shape[0]
+    cls_cta = cuniq // span3
+    n_tr = int(e_tr.max()) + 1
+    su = np.unique(e_cls * n_tr + e_tr)  # (class, symbol) pairs
+    su_cls, su_tr = su // n_tr, su % n_tr
+    nsym_cls = np.bincount(su_cls, minlength=ncls)
+    if nsym_cls.max() > 8:
+        raise RuntimeError("staged M2L: a class with more than 8 symbols")
+    # stages: greedy in class order, a stage holds <= ns_cap DISTINCT symbols
+    # (symbols shared between its classes are staged once)
+    cls_ptr = np.concatenate([[0], np.cumsum(nsym_cls)]).astype(np.int64)
+    st_rel = np.empty(ncls, np.int64)
+    cls_cta = np.ascontiguousarray(cls_cta, np.int64)
+    su_tr = np.ascontiguousarray(su_tr, np.int64)
+    _lib.check(_lib.load().defmm_stage_pack(ncls, cls_cta.ctypes.data, cls_ptr.ctypes.data, su_tr.ctypes.data,
+                                            n_tr, int(ns_cap), st_rel.ctypes.data), "defmm_stage_pack")
+    nst_cta = np.zeros(ncta, np.int64)
+    np.maximum.at(nst_cta, cls_cta, st_rel + 1)
+    cta_stage = np.concatenate([[0], np.cumsum(nst_cta)])
+    cls_stage = cta_stage[cls_cta] + st_rel
+    nstage = int(cta_stage[-1])
+    # slots: distinct (stage, symbol)
+    e_stage = cls_stage[e_cls]
+    skey = e_stage * n_tr + e_tr
+    suniq, e_slotg = np.unique(skey, return_inverse=True)
+    e_slotg = e_slotg.reshape(-1)
+    slot_stage = suniq // n_tr
+    slot_sym = (suniq % n_tr).astype(i32)
+    stage_slot_ptr = np.searchsorted(slot_stage, np.arange(nstage + 1))
+    if np.diff(stage_slot_ptr).max() > ns_cap:
+        raise RuntimeError("staged M2L: stage over capacity")
+    e_slot = e_slotg - stage_slot_ptr[e_stage]
+    # entries = distinct (CTA, warp, class), ordered by (CTA, warp, stage, class)
+    ekey = e_cw * ncls + e_cls  # class ids increase with the stage inside a CTA
+    euniq, e_ent = np.unique(ekey, return_inverse=True)
+    e_ent = e_ent.reshape(-1)
+    nent = euniq.shape[0]
+    ent_cw = euniq // ncls
+    ent_stage = cls_stage[euniq % ncls]
+    # slot bytes: ns_cap (the zero slot) where row k has no event in the class; each (entry, k)
+    # holds at most one event, so the bytes add up exactly (values < 2^32)
+    ent32 = np.zeros((nent + STAGE_ENT_PAD, 2), i32)
+    ent32[e_ent, 0] = e_src
+    none = int(ns_cap) * 0x01010101  # every byte = ns_cap: the ring's zero slot
+    y = np.bincount(e_ent, weights=((e_slot - int(ns_cap)) << (8 * kk[rep])).astype(np.float64), minlength=nent)
+    ent32[:nent, 1] = (y.astype(np.int64) + none).astype(np.uint32).view(i32)
+    ent32[nent:, 1] = np.uint32(none).view(i32)
+    cta_went = np.searchsorted(ent_cw, np.arange(ncta * NW)).astype(i32)
+    # end of warp w's entries of stage s: entries with (cw, stage) <= (cta(s) NW + w, s)
+    st_cta = np.repeat(np.arange(ncta), nst_cta)
+    q_cw = (st_cta[:, None] * NW + np.arange(NW)[None, :]).reshape(-1)
+    q_st = np.repeat(np.arange(nstage), NW)
+    ent_k2 = ent_cw * (nstage + 1) + ent_stage
+    stage_wend = np.searchsorted(ent_k2, q_cw * (nstage + 1) + q_st, side="right").astype(i32)
+    # stored per CTA as [warp][stage]: a warp reads its stage ends contiguously
+    q_w = np.tile(np.arange(NW), nstage)
+    pos = cta_stage[st_cta[q_st]] * NW + q_w * nst_cta[st_cta[q_st]] + (q_st - cta_stage[st_cta[q_st]])
+    wend_t = np.empty_like(stage_wend)
+    wend_t[pos] = stage_wend
+    stage_wend = wend_t
+    return {"n": ncta, "ns_cap": ns_cap, "row_slot": slots.astype(np.int64), "cta_stage": cta_stage.astype(i32),
+            "cta_went": cta_went, "stage_slot_ptr": stage_slot_ptr.astype(i32), "slot_sym": slot_sym,
+            "stage_wend": stage_wend, "ent": ent32,
+            "cta_rows": cta_rows.reshape(-1)}
+
+
 def _rows_to_ids(slots, rows):
     """Local slots -> index into the sorted row-slot list ``rows`` (-1 if absent)."""
     slots = np.asarray(slots)
@@ -122,8 +261,9 @@ M2L_MODE_KINDS = {
     "rows": ("rows", "rows"), "blocked_all": ("blocked", "blocked"),
     "pairs": ("blocked", "pair"), "pairs_all": ("pair", "pair"), "quartets": ("blocked", "quartet"),
     "quartets_all": ("quartet", "quartet"), "triples_all": ("triple", "triple"),
+    "staged": ("blocked", "staged"), "staged_all": ("staged", "staged"),
 }
-M2L_KERNELS = ("rows", "blocked", "pair", "triple", "quartet")
+M2L_KERNELS = ("rows", "blocked", "pair", "triple", "quartet", "staged")
 # events per parent-pair block above which a level counts as dense (blocked kernel)
 BLOCKED_MIN_EVENTS_PER_BLOCK = 32.0
 # "auto": other sparse levels with at least this many rows run the pair kernel
@@ -331,6 +471,13 @@ class FmmPlan:
                 self.sib_groups.append((gr["K"], int(gr["n"]), _dev(gr["grp_slot"], i64, d),
                                         _dev(gr["grp_ptr"], i64, d), _dev(gr["ent"].reshape(-1), i32, d)))
         self.n_pairs = sum(x[1] for x in self.sib_groups)
+        sg = h["staged"]
+        self.staged = None
+        self.stage_depth = int(os.environ.get("DEFMM_STAGE_DEPTH", STAGE_DEPTH))
+        if sg["n"]:
+            self.staged = (int(sg["n"]), int(sg["ns_cap"])) + tuple(
+                _dev(sg[k].reshape(-1), i32, d) for k in ("cta_stage", "cta_went", "stage_slot_ptr", "slot_sym",
+                                                         "stage_wend", "ent", "cta_rows"))
         # downward
         self.l2l = []
         for lev, outs, octant, ptr, src, sdir in h["l2l"]:
@@ -446,10 +593,17 @@ class FmmPlan:
                                  tt.level, tt.parent, 3)
         h["quartet"] = m2l_groups(np.nonzero(pick("quartet"))[0], rows, h["row_ptr"], h["ent"], p.l_cell, p.l_dir,
                                   tt.level, tt.parent, 4)
-        # lhat rows = the blocked rows
+        # staged M2L (K7 v13): warp units of sibling rows sharing staged symbols
+        hat_coords = self.st.coords[p.m_cell[h["hat_slot"]]] if h["hat_slot"].size else np.zeros((0, 3), np.int64)
+        h["staged"] = m2l_stage_lists(np.nonzero(pick("staged"))[0], rows, h["row_ptr"], h["ent"], p.l_cell,
+                                      p.l_dir, tt.level, tt.parent, tt.coords, hat_coords,
+                                      int(os.environ.get("DEFMM_STAGE_SLOTS", STAGE_SLOTS)))
+        # lhat rows = the blocked rows, then the staged rows
         is_grp = pick("blocked")
         grp_rows = rows[is_grp]
-        h["bk_rows"] = grp_rows
+        h["bk_rows"] = np.concatenate([grp_rows, h["staged"]["row_slot"]])
+        h["staged"]["cta_rows"] = np.where(h["staged"]["cta_rows"] >= 0,
+                                           h["staged"]["cta_rows"] + grp_rows.shape[0], -1).astype(np.int32)
         # groups of blocked levels, rows renumbered into lhat
         gr = h["grp_rows"]
         gr_slots = np.where(gr >= 0, rows[np.maximum(gr, 0)] if rows.size else -1, -1)
@@ -731,6 +885,9 @@ class FmmPlan:
                           sh)
             _lib.call(self._op("m2l_blocked"), L, self.n_groups, self.grp_ptr, self.grp_rows, self.blk_src,
                       self.blk_trans, self.blk_mask, self.blk_kind, self.hat, self.sym_derived, self.lhat, sh)
+            if self.staged is not None:
+                _lib.call(self._op("m2l_stage"), L, self.staged[0], self.staged[1], self.stage_depth,
+                          *self.staged[2:], self.hat, self.sym_derived, self.lhat, sh)
             _lib.call(self._op("f2l_rows"), L, self.bk_rows.shape[0], self.bk_rows, self.lhat, self.local, sh)
         elif self.m2l_variant == "derived":
             _lib.call(self._op("m2l_rows"), L, self.row_slot.shape[0], self.row_slot, self.row_ptr,
@@ -825,6 +982,7 @@ class FmmPlan:
                            (sum(x[1] for x in self.sib_groups if x[0] == 3), f"{gk}<3>", "triple"),
                            (sum(x[1] for x in self.sib_groups if x[0] == 4), f"{gk}<4>", "quartet"),
                            (self.n_groups, "m2l_blocked_kernel", "blocked"),
+                           (self.staged[0] if self.staged else 0, "m2l_stage_kernel", "staged"),
                            (self.bk_rows.shape[0], "f2l_rows_kernel", None)):
             if n:
                 out.append(f"{name}<{R}, {self.L}>" + (f" (levels {lv(k)})" if k is not None else ""))
@@ -836,7 +994,7 @@ class FmmPlan:
         the M2L kernels with work, l2l per level, l2p."""
         if self.m2l_variant == "hybrid":
             m2l = len(self.sib_groups) + sum(int(n > 0) for n in (self.rk_rows.shape[0], self.n_groups,
-                                                                   self.bk_rows.shape[0]))
+                                                                   self.bk_rows.shape[0])) + int(bool(self.staged))
         else:
             m2l = 1
         return 4 + (1 if self.n_split else 0) + len(self.m2m) + len(self.l2l) + m2l

@@ -439,6 +439,68 @@ def test_m2l_groups_reconstruct_every_row(case, K):
             assert got == want
 
 
+@pytest.mark.parametrize("ns_cap", [16, 48])
+@pytest.mark.parametrize("case", ["cubesurf4000", "volume3000", "c1_kd16", "tt_hf_sphere"])
+def test_m2l_stage_lists_replay_every_event(case, ns_cap):
+    """fmm.m2l_stage_lists (staged M2L, K7 v13): walking the lists the way the
+    kernel does -- per CTA its stages, per warp unit the entries up to the
+    stage's end, per row byte the stage's slot -> symbol -- visits every row's
+    (source, symbol) events exactly once; warp units hold sibling rows of one
+    key, stages stay within ns_cap slots."""
+    from paper_2202_04894_b200.fmm import STAGE_ENT_PAD, STAGE_K, STAGE_NW, m2l_stage_lists
+
+    if case.startswith("tt_"):
+        from conftest import load_two_tree
+        from paper_2202_04894_b200.geometry import compute_root_box
+
+        g = load_two_tree(case)
+        kw = g["config"]
+        box = compute_root_box(np.vstack([g["targets"], g["sources"]]))
+        st, _ = build_tree(g["sources"], g["charges"], TreeConfig(ncrit=kw["ncrit"]), root_box=box)
+        tr, _ = build_tree(g["targets"], np.zeros(g["targets"].shape[0]), TreeConfig(ncrit=kw["ncrit"]), root_box=box)
+        p = build_plan(tr, st, kw["order"], kw["kappa"], 1.0, 2.0)
+    else:
+        tr, _, p = _plan(load_case(case))
+        st = tr
+    ptr, ent, rows = p.m2l_row_ptr, p.m2l_rows_entries, p.m2l_row_slot
+    ids = np.arange(rows.shape[0])
+    hc = st.coords[p.m_cell[p.hat_slot]]
+    sg = m2l_stage_lists(ids, rows, ptr, ent, p.l_cell, p.l_dir, tr.level, tr.parent, tr.coords, hc, ns_cap)
+    K, NW = STAGE_K, STAGE_NW
+    assert sorted(sg["row_slot"].tolist()) == sorted(rows.tolist())
+    assert sg["ent"].shape[0] == sg["stage_wend"].max() + STAGE_ENT_PAD
+    assert np.diff(sg["stage_slot_ptr"]).max() <= ns_cap and np.diff(sg["stage_slot_ptr"]).min() >= 1
+    got = {}
+    e32 = sg["ent"]
+    for c in range(sg["n"]):
+        for w in range(NW):
+            cw = c * NW + w
+            lrows = sg["cta_rows"][cw * K:(cw + 1) * K]
+            members = sg["row_slot"][lrows[lrows >= 0]]
+            if members.size:
+                cells = p.l_cell[members]
+                assert len(set(tr.parent[cells].tolist())) == 1 and len(set(p.l_dir[members].tolist())) == 1
+            i = int(sg["cta_went"][cw])
+            s0, s1 = int(sg["cta_stage"][c]), int(sg["cta_stage"][c + 1])
+            for s in range(s0, s1):
+                end = int(sg["stage_wend"][s0 * NW + w * (s1 - s0) + (s - s0)])
+                base = int(sg["stage_slot_ptr"][s])
+                nslot = int(sg["stage_slot_ptr"][s + 1]) - base
+                while i < end:
+                    src, packed = int(e32[i, 0]), int(e32[i, 1]) & 0xFFFFFFFF
+                    for k in range(K):
+                        b = (packed >> (8 * k)) & 0xFF
+                        if b != ns_cap:
+                            assert b < nslot and lrows[k] >= 0
+                            got.setdefault(int(sg["row_slot"][lrows[k]]), []).append((src, int(sg["slot_sym"][base + b])))
+                    i += 1
+            nxt = int(sg["cta_went"][cw + 1]) if cw + 1 < sg["n"] * NW else int(sg["stage_wend"].max())
+            assert i == nxt
+    for r, slot in enumerate(rows.tolist()):
+        want = sorted(zip(ent[ptr[r]:ptr[r + 1], 0].tolist(), ent[ptr[r]:ptr[r + 1], 1].tolist()))
+        assert sorted(got[slot]) == want
+
+
 def test_p2p_overlap_policy():
     """P2P beside the M2L (high-priority far field) only when every M2L level
     runs the quartet kernel (measured, profiles/r01_summary_v9.md)."""
