@@ -187,6 +187,18 @@ int defmm_l2_stream(const void* buf, int64_t n_vec, int32_t iters, int32_t ctas_
  *   grid = 0 launches one CTA per item.  Results do not depend on grid.  hilo
  *   (c64 only): 1 = hi/lo float pairs of the target-relative coordinates
  *   (accuracy for L >= 6), 0 = single floats (cheaper; L <= 5).
+ * K1 v2 mutual P2P (single-tree plans: targets == sources) -- the same sums with every
+ *   G(|x_t - x_s|) evaluated once for the pair (t, s), s after t's leaf: leaf l's source
+ *   runs are clipped to particles >= tgt_lo[l] (its own particles first, evaluated
+ *   one-directionally); item i = (item_leaf[i], flattened range [item_f0[i], item_f1[i]))
+ *   writes its nt row sums to partial[item_row[i] ..] and, for every listed source, the
+ *   column sum  sum_t G q_t  to partial[item_col[i] + (f - item_f0[i])].  p2p_gather task
+ *   j (leaf l = task_leaf[j]) then forms out[x] = sum_c partial[cbase[c] + x] over its
+ *   contributor segments c in [cptr[j], cptr[j+1]) with cxlo[c] <= x < cxhi[c], in list
+ *   order (the row partials of the leaf's items, the column partials of the items that
+ *   listed it); out = near + tgt_lo[l] if task_out[j] < 0, else partial + task_out[j] (very
+ *   long lists are pre-summed in chunks by earlier gather launches).
+ *   Leaves must hold <= 256 particles.  No atomics: reruns are bitwise identical.
  */
 #define DEFMM_DECLARE_TYPED(SUFFIX)                                                              \
     int defmm_p2m_##SUFFIX(int32_t L, int64_t n, const int32_t* cell, const int32_t* dir,        \
@@ -238,6 +250,17 @@ int defmm_l2_stream(const void* buf, int64_t n_vec, int32_t iters, int32_t ctas_
                            const double* dirs, const double* px, const double* py,              \
                            const double* pz, double kappa, const void* local, const void* near, \
                            const int64_t* perm, void* out, void* stream);                       \
+    int defmm_p2p_mutual_##SUFFIX(int64_t n_items, const int32_t* item_leaf, const int64_t* item_f0, \
+                                  const int64_t* item_f1, const int64_t* item_row,                   \
+                                  const int64_t* item_col, const int64_t* tgt_lo,                    \
+                                  const int64_t* tgt_hi, const int64_t* ptr, const int64_t* src_lo,  \
+                                  const int64_t* src_hi, const double* px, const double* py,         \
+                                  const double* pz, const void* q, double kappa, double tol,         \
+                                  void* partial, int32_t grid, int32_t hilo, void* stream);          \
+    int defmm_p2p_gather_##SUFFIX(int64_t n, const int32_t* task_leaf, const int64_t* task_out,      \
+                                  const int64_t* tgt_lo, const int64_t* tgt_hi, const int64_t* cptr, \
+                                  const int64_t* cbase, const int32_t* cxlo, const int32_t* cxhi,    \
+                                  void* partial, void* near, void* stream);                          \
     int defmm_p2p_##SUFFIX(int64_t n_items, const int32_t* item_leaf, const int64_t* item_f0,    \
                            const int64_t* item_f1, const int64_t* item_out,                     \
                            const int64_t* tgt_lo, const int64_t* tgt_hi, const int64_t* ptr,    \
@@ -251,11 +274,13 @@ int defmm_l2_stream(const void* buf, int64_t n_vec, int32_t iters, int32_t ctas_
 
 /* expands to: defmm_p2m_c128 defmm_m2m_c128 defmm_m2f_c128 defmm_symbols_c128
  * defmm_expand_symbols_c128 defmm_m2l_rows_c128 defmm_m2l_group_c128 defmm_m2l_stage_c128 defmm_m2l_blocked_c128
- * defmm_f2l_rows_c128 defmm_l2l_c128 defmm_l2p_c128 defmm_p2p_c128 */
+ * defmm_f2l_rows_c128 defmm_l2l_c128 defmm_l2p_c128 defmm_p2p_c128 defmm_p2p_mutual_c128
+ * defmm_p2p_gather_c128 */
 DEFMM_DECLARE_TYPED(c128)
 /* expands to: defmm_p2m_c64 defmm_m2m_c64 defmm_m2f_c64 defmm_symbols_c64
  * defmm_expand_symbols_c64 defmm_m2l_rows_c64 defmm_m2l_group_c64 defmm_m2l_stage_c64 defmm_m2l_blocked_c64
- * defmm_f2l_rows_c64 defmm_l2l_c64 defmm_l2p_c64 defmm_p2p_c64 */
+ * defmm_f2l_rows_c64 defmm_l2l_c64 defmm_l2p_c64 defmm_p2p_c64 defmm_p2p_mutual_c64
+ * defmm_p2p_gather_c64 */
 DEFMM_DECLARE_TYPED(c64)
 
 /* Spectral layout of order L (HOST call, no device needed): every spectrum is

@@ -52,6 +52,8 @@ for _t in ("c128", "c64"):
         f"defmm_f2l_rows_{_t}": [_i32, _i64, _vp, _vp, _vp, _vp],
         f"defmm_l2l_{_t}": [_i32, _i64, _vp, _vp, _vp, _vp, _vp, _f64, _vp, _f64, _vp, _vp],
         f"defmm_l2p_{_t}": [_i32, _i64] + [_vp] * 13 + [_f64, _vp, _vp, _vp, _vp, _vp],
+        f"defmm_p2p_mutual_{_t}": [_i64] + [_vp] * 14 + [_f64, _f64, _vp, _i32, _i32, _vp],
+        f"defmm_p2p_gather_{_t}": [_i64] + [_vp] * 11,
         f"defmm_p2p_{_t}": [_i64] + [_vp] * 16 + [_f64, _f64, _vp, _vp, _i64, _vp, _vp, _vp, _i32, _i32, _vp],
     })
 

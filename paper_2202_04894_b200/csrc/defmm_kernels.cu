@@ -2124,6 +2124,420 @@ __global__ void __launch_bounds__(P2P_NT, DEFMM_P2P_MINB32) p2p_f32_kernel(
     }
 }
 
+// ---------------------------------------------------------------------------
+// K1 v2: MUTUAL P2P (single-tree plans).  G(|x_t - x_s|) is symmetric, and in
+// single-tree mode the near-field relation is too: s is in the source list of
+// t's leaf iff t is in the list of s's leaf.  An item here is a target leaf A
+// against a piece of its source list CLIPPED to particles >= A's first one:
+// first A itself (evaluated one-directionally, every ordered pair), then the
+// leaves after A in Morton order, for which every evaluated G feeds BOTH the
+// row sum of its target (registers, as in K1) and the column sum of its
+// source, G q_t.  Column sums are accumulated in per-warp shared-memory copies
+// (plain read-add-write: the threads of a warp visit distinct sources at every
+// step -- thread pi starts at source pi of its part and rotates), merged in
+// fixed warp order after every tile and written to partial[]; p2p_gather then
+// sums, for every particle, the row partials of its own leaf's items and the
+// column partials of the items that listed it, in list order (no atomics:
+// reruns are bitwise identical).  Half the kernel evaluations of K1.
+constexpr int P2P_WARPS = P2P_NT / 32;
+
+template <typename Src, typename TILES, typename A, typename TGT, typename MUTE, typename LOAD, typename PAIR,
+          typename STORE>
+__device__ __forceinline__ void p2p_item_mut(int64_t t0, int64_t t1, int64_t e0, int64_t e1, int64_t f0, int64_t f1,
+                                             const int64_t* __restrict__ src_lo,
+                                             const int64_t* __restrict__ src_hi, TILES& tiles,
+                                             A (*col)[P2P_TILE], A (*red)[P2P_NT], int64_t* rlo, int64_t* rpre,
+                                             TGT&& tgt, MUTE&& mute, LOAD&& load, PAIR&& pair, STORE&& store_row,
+                                             A* __restrict__ colout) {
+    const int64_t np_all = (t1 - t0 + 1) / 2;  // <= P2P_NT (checked by the host)
+    const int np = (int)np_all;
+    const int parts = P2P_NT / np;
+    const int pi = threadIdx.x % np, part = threadIdx.x / np;
+    const int warp = threadIdx.x >> 5;
+    const int64_t ta = t0 + 2 * pi, tb = ta + 1;
+    const bool va = part < parts && ta < t1, vb = va && tb < t1;
+    const auto TA = tgt(va ? ta : t0);
+    auto TB = tgt(vb ? tb : (va ? ta : t0));
+    if (!vb) mute(TB);  // an absent second target adds nothing to the column sums
+    A acca{}, accb{};
+    int64_t base = 0;  // flattened offset of the first run of the window (col[][] is all zero here)
+    for (int64_t w0 = e0; w0 < e1 && base < f1; w0 += P2P_MAXRUNS) {
+        const int nr = (int)((e1 - w0) < P2P_MAXRUNS ? (e1 - w0) : P2P_MAXRUNS);
+        __syncthreads();
+        for (int k = threadIdx.x; k < nr; k += P2P_NT) {
+            rlo[k] = src_lo[w0 + k];
+            rpre[k + 1] = src_hi[w0 + k] - src_lo[w0 + k];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int64_t acc = base;
+            rpre[0] = base;
+            for (int k = 1; k <= nr; ++k) {
+                acc += rpre[k];
+                rpre[k] = acc;
+            }
+        }
+        __syncthreads();
+        const int64_t wend = rpre[nr];
+        const int64_t lo = f0 > base ? f0 : base, hi = f1 < wend ? f1 : wend;
+        auto fetch = [&](int64_t fb, int cnt, Src (&v)[P2P_PER]) {
+#pragma unroll
+            for (int j = 0; j < P2P_PER; ++j) {
+                const int k = threadIdx.x + j * P2P_NT;
+                if (k < cnt) {
+                    const int64_t g = fb + k;
+                    int r = 0, top = nr;  // last run with rpre[r] <= g
+                    while (top - r > 1) {
+                        const int mid = (r + top) >> 1;
+                        if (rpre[mid] <= g) r = mid; else top = mid;
+                    }
+                    v[j] = load(rlo[r] + (g - rpre[r]));
+                }
+            }
+        };
+        auto put = [&](int buf, int cnt, const Src (&v)[P2P_PER]) {
+#pragma unroll
+            for (int j = 0; j < P2P_PER; ++j) {
+                const int k = threadIdx.x + j * P2P_NT;
+                if (k < cnt) tiles.put(buf, k, v[j]);
+            }
+        };
+        if (lo < hi) {
+            Src v[P2P_PER];
+            int cnt = (int)((hi - lo) < P2P_TILE ? (hi - lo) : P2P_TILE);
+            fetch(lo, cnt, v);
+            put(0, cnt, v);
+            __syncthreads();
+            int buf = 0;
+            for (int64_t fb = lo; fb < hi; fb += P2P_TILE) {
+                const int64_t fn = fb + P2P_TILE;
+                const int cn = fn < hi ? (int)((hi - fn) < P2P_TILE ? (hi - fn) : P2P_TILE) : 0;
+                if (cn) fetch(fn, cn, v);  // in flight while the current tile is consumed
+                if (va) {
+                    A* cw = col[warp];
+                    // part p owns the block [p B, (p + 1) B) of the tile's sources; thread pi
+                    // starts at the pi-th of them and rotates over M >= np positions, so the
+                    // threads of a warp touch distinct, consecutive sources at every step
+                    // (conflict-free reads of the SoA tile and of the column sums)
+                    const int B = (cnt + parts - 1) / parts;
+                    const int k0 = part * B;
+                    const int mp = cnt > k0 ? (cnt - k0 < B ? cnt - k0 : B) : 0;
+                    if (mp >= np) {
+                        // every position is a source: two of them per step with separate row
+                        // sums (four independent kernel evaluations in flight per thread)
+                        int idx = pi;
+                        int jj = 0;
+                        A a2{}, b2{};
+                        for (; jj + 2 <= mp; jj += 2) {
+                            const int i0 = idx, i1 = idx + 1 == mp ? 0 : idx + 1;
+                            idx = i1 + 1 == mp ? 0 : i1 + 1;
+                            const Src s0 = tiles.get(buf, k0 + i0), s1 = tiles.get(buf, k0 + i1);
+                            A c0{}, c1{};
+                            pair(TA, s0, acca, c0);
+                            pair(TA, s1, a2, c1);
+                            pair(TB, s0, accb, c0);
+                            pair(TB, s1, b2, c1);
+                            cw[k0 + i0] = cw[k0 + i0] + c0;
+                            cw[k0 + i1] = cw[k0 + i1] + c1;
+                        }
+                        if (jj < mp) {
+                            const Src s0 = tiles.get(buf, k0 + idx);
+                            A c0{};
+                            pair(TA, s0, acca, c0);
+                            pair(TB, s0, accb, c0);
+                            cw[k0 + idx] = cw[k0 + idx] + c0;
+                        }
+                        acca = acca + a2;
+                        accb = accb + b2;
+                    } else {  // fewer sources than target pairs: idle positions keep the threads apart
+                        int idx = pi;
+                        for (int jj = 0; jj < np; ++jj) {
+                            if (idx < mp) {
+                                const Src sk = tiles.get(buf, k0 + idx);
+                                A cv{};
+                                pair(TA, sk, acca, cv);
+                                pair(TB, sk, accb, cv);
+                                cw[k0 + idx] = cw[k0 + idx] + cv;
+                            }
+                            if (++idx == np) idx = 0;
+                        }
+                    }
+                }
+                if (cn) put(buf ^ 1, cn, v);
+                __syncthreads();
+                // column sums of the tile: warp copies merged in fixed order, then cleared
+                for (int k = threadIdx.x; k < cnt; k += P2P_NT) {
+                    A sum = col[0][k];
+                    col[0][k] = A{};
+#pragma unroll
+                    for (int w = 1; w < P2P_WARPS; ++w) {
+                        sum = sum + col[w][k];
+                        col[w][k] = A{};
+                    }
+                    colout[(fb - f0) + k] = sum;
+                }
+                __syncthreads();
+                buf ^= 1;
+                cnt = cn;
+            }
+        }
+        base = wend;
+    }
+    red[0][threadIdx.x] = acca;
+    red[1][threadIdx.x] = accb;
+    __syncthreads();
+    if (part == 0 && va) {
+        A a = red[0][pi], b = red[1][pi];
+        for (int q = 1; q < parts; ++q) {
+            a = a + red[0][pi + q * np];
+            b = b + red[1][pi + q * np];
+        }
+        store_row(ta, a);
+        if (vb) store_row(tb, b);
+    }
+    __syncthreads();
+}
+
+// source tiles of the mutual kernels in SoA form (lanes read consecutive sources)
+struct P2PTiles64 {
+    double x[2][P2P_TILE], y[2][P2P_TILE], z[2][P2P_TILE];
+    double2 q[2][P2P_TILE];
+    __device__ __forceinline__ void put(int b, int k, const P2PSrc64& s) {
+        x[b][k] = s.x;
+        y[b][k] = s.y;
+        z[b][k] = s.z;
+        q[b][k] = s.q;
+    }
+    __device__ __forceinline__ P2PSrc64 get(int b, int k) const { return P2PSrc64{x[b][k], y[b][k], z[b][k], q[b][k]}; }
+};
+
+struct P2PTgt64q {  // target position + its charge / (4 pi)
+    double x, y, z;
+    double2 q;
+};
+
+// G(r) feeds the row sum (source charge) and the column sum (target charge)
+__device__ __forceinline__ void helm_pair_mut(double dx, double dy, double dz, double2 qs, double2 qt, double kpi,
+                                              double tol, P2PAcc64& row, P2PAcc64& colv) {
+    const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+    const double rinv = rsqrt_p2p(r2);
+    const double r = r2 * rinv;
+    const bool ok = r >= tol;  // kernel.py:40-43 (NaN at r2 = 0 -> false)
+    double s, c;
+    sincospi_p2p(kpi * (ok ? r : 0.0), s, c);
+    const double g = ok ? rinv : 0.0;
+    const double gr = g * c, gi = g * s;
+    row.re = fma(gr, qs.x, fma(-gi, qs.y, row.re));
+    row.im = fma(gr, qs.y, fma(gi, qs.x, row.im));
+    colv.re = fma(gr, qt.x, fma(-gi, qt.y, colv.re));
+    colv.im = fma(gr, qt.y, fma(gi, qt.x, colv.im));
+}
+
+struct P2PMutItems {
+    const int32_t* leaf;
+    const int64_t* f0;
+    const int64_t* f1;
+    const int64_t* row;  // partial[] offset of the item's nt row sums
+    const int64_t* col;  // partial[] offset of its f1 - f0 column sums
+};
+
+#ifndef DEFMM_P2P_MUT_MINB64
+#define DEFMM_P2P_MUT_MINB64 4
+#endif
+template <typename R>
+__global__ void __launch_bounds__(P2P_NT, DEFMM_P2P_MUT_MINB64) p2p_mut_kernel(
+    int64_t n, P2PMutItems it, const int64_t* __restrict__ tgt_lo, const int64_t* __restrict__ tgt_hi,
+    const int64_t* __restrict__ ptr, const int64_t* __restrict__ src_lo,
+    const int64_t* __restrict__ src_hi, const double* __restrict__ px, const double* __restrict__ py,
+    const double* __restrict__ pz, const cx<R>* __restrict__ q, double kappa, double tol,
+    double2* __restrict__ partial) {
+    __shared__ P2PTiles64 tiles;
+    __shared__ P2PAcc64 col[P2P_WARPS][P2P_TILE];
+    __shared__ P2PAcc64 red[2][P2P_NT];
+    __shared__ int64_t rlo[P2P_MAXRUNS], rpre[P2P_MAXRUNS + 1];
+    const double inv4pi = 1.0 / (4.0 * 3.141592653589793);
+    const double kpi = kappa / 3.141592653589793;
+    for (int k = threadIdx.x; k < P2P_WARPS * P2P_TILE; k += P2P_NT) col[0][k] = P2PAcc64{};  // kept zero by the flushes
+    for (int64_t item = blockIdx.x; item < n; item += gridDim.x) {
+        const int leaf = it.leaf[item];
+        const int64_t f0 = it.f0[item], f1 = it.f1[item], rb = it.row[item];
+        const int64_t t0 = tgt_lo[leaf], t1 = tgt_hi[leaf];
+        p2p_item_mut<P2PSrc64>(
+            t0, t1, ptr[leaf], ptr[leaf + 1], f0, f1, src_lo, src_hi, tiles, col, red, rlo, rpre,
+            [&](int64_t t) {
+                const double2 qq = to_d(q[t]);
+                return P2PTgt64q{px[t], py[t], pz[t], make_double2(qq.x * inv4pi, qq.y * inv4pi)};
+            },
+            [](P2PTgt64q& T) { T.q = make_double2(0.0, 0.0); },
+            [&](int64_t g) {
+                const double2 qq = to_d(q[g]);
+                return P2PSrc64{px[g], py[g], pz[g], make_double2(qq.x * inv4pi, qq.y * inv4pi)};
+            },
+            [&](const P2PTgt64q& t, const P2PSrc64& s, P2PAcc64& a, P2PAcc64& cv) {
+                helm_pair_mut(t.x - s.x, t.y - s.y, t.z - s.z, s.q, t.q, kpi, tol, a, cv);
+            },
+            [&](int64_t t, const P2PAcc64& a) { partial[rb + (t - t0)] = make_double2(a.re, a.im); },
+            reinterpret_cast<P2PAcc64*>(partial + it.col[item]));
+    }
+}
+
+template <bool HILO>
+struct P2PTiles32;
+template <>
+struct P2PTiles32<false> {
+    float4 a[2][P2P_TILE];
+    float qi[2][P2P_TILE];
+    __device__ __forceinline__ void put(int b, int k, const P2PF32Src<false>& s) {
+        a[b][k] = s.a;
+        qi[b][k] = s.qi;
+    }
+    __device__ __forceinline__ P2PF32Src<false> get(int b, int k) const {
+        P2PF32Src<false> s;
+        s.a = a[b][k];
+        s.qi = qi[b][k];
+        return s;
+    }
+};
+template <>
+struct P2PTiles32<true> {
+    float4 a[2][P2P_TILE], bb[2][P2P_TILE];
+    __device__ __forceinline__ void put(int b, int k, const P2PF32Src<true>& s) {
+        a[b][k] = s.a;
+        bb[b][k] = s.b;
+    }
+    __device__ __forceinline__ P2PF32Src<true> get(int b, int k) const {
+        P2PF32Src<true> s;
+        s.a = a[b][k];
+        s.b = bb[b][k];
+        return s;
+    }
+};
+
+template <bool HILO>
+struct P2PTgt32q {
+    float t[6];  // offsets: hi x, y, z, then lo x, y, z (HILO)
+    float qr, qi;  // charge / (4 pi)
+};
+
+template <bool HILO>
+__device__ __forceinline__ void pair_f32_mut(const P2PTgt32q<HILO>& T, const P2PF32Src<HILO>& s, float k2pi,
+                                             float ftol, P2PAcc32& row, P2PAcc32& colv) {
+    float dx, dy, dz, qr, qi;
+    if constexpr (HILO) {
+        dx = (T.t[0] - s.a.x) + (T.t[3] - s.b.x);
+        dy = (T.t[1] - s.a.y) + (T.t[4] - s.b.y);
+        dz = (T.t[2] - s.a.z) + (T.t[5] - s.b.z);
+        qr = s.a.w;
+        qi = s.b.w;
+    } else {
+        dx = T.t[0] - s.a.x;
+        dy = T.t[1] - s.a.y;
+        dz = T.t[2] - s.a.z;
+        qr = s.a.w;
+        qi = s.qi;
+    }
+    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    const float rinv = rsqrt_approx(r2);  // r2 = 0 -> inf -> r = NaN -> masked
+    const float r = r2 * rinv;
+    const bool ok = r >= ftol;
+    float u = k2pi * (ok ? r : 0.0f);
+    u -= __fsub_rn(__fadd_rn(u, 12582912.0f), 12582912.0f);
+    float sn, cs;
+    __sincosf(6.283185307179586f * u, &sn, &cs);
+    const float g = ok ? rinv : 0.0f;
+    const float gr = g * cs, gi = g * sn;
+    row.re = fmaf(gr, qr, fmaf(-gi, qi, row.re));
+    row.im = fmaf(gr, qi, fmaf(gi, qr, row.im));
+    colv.re = fmaf(gr, T.qr, fmaf(-gi, T.qi, colv.re));
+    colv.im = fmaf(gr, T.qi, fmaf(gi, T.qr, colv.im));
+}
+
+template <bool HILO>
+__global__ void __launch_bounds__(P2P_NT, DEFMM_P2P_MINB32) p2p_mut_f32_kernel(
+    int64_t n, P2PMutItems it, const int64_t* __restrict__ tgt_lo, const int64_t* __restrict__ tgt_hi,
+    const int64_t* __restrict__ ptr, const int64_t* __restrict__ src_lo,
+    const int64_t* __restrict__ src_hi, const double* __restrict__ px, const double* __restrict__ py,
+    const double* __restrict__ pz, const float2* __restrict__ q, double kappa, double tol,
+    float2* __restrict__ partial) {
+    __shared__ P2PTiles32<HILO> tiles;
+    __shared__ P2PAcc32 col[P2P_WARPS][P2P_TILE];
+    __shared__ P2PAcc32 red[2][P2P_NT];
+    __shared__ int64_t rlo[P2P_MAXRUNS], rpre[P2P_MAXRUNS + 1];
+    const float k2pi = (float)(kappa / (2.0 * 3.141592653589793));
+    const float ftol = (float)tol;
+    const float inv4pi = (float)(1.0 / (4.0 * 3.141592653589793));
+    for (int k = threadIdx.x; k < P2P_WARPS * P2P_TILE; k += P2P_NT) col[0][k] = P2PAcc32{};  // kept zero by the flushes
+    for (int64_t item = blockIdx.x; item < n; item += gridDim.x) {
+        const int leaf = it.leaf[item];
+        const int64_t f0 = it.f0[item], f1 = it.f1[item], rb = it.row[item];
+        const int64_t t0 = tgt_lo[leaf], t1 = tgt_hi[leaf];
+        const double cx = px[t0], cy = py[t0], cz = pz[t0];  // reference point of the item
+        p2p_item_mut<P2PF32Src<HILO>>(
+            t0, t1, ptr[leaf], ptr[leaf + 1], f0, f1, src_lo, src_hi, tiles, col, red, rlo, rpre,
+            [&](int64_t t) {
+                P2PTgt32q<HILO> T;
+                rel_f32<HILO>(px[t], cx, T.t[0], T.t[3]);
+                rel_f32<HILO>(py[t], cy, T.t[1], T.t[4]);
+                rel_f32<HILO>(pz[t], cz, T.t[2], T.t[5]);
+                const float2 qq = q[t];
+                T.qr = qq.x * inv4pi;
+                T.qi = qq.y * inv4pi;
+                return T;
+            },
+            [](P2PTgt32q<HILO>& T) { T.qr = T.qi = 0.0f; },
+            [&](int64_t g) {
+                const float2 qq = q[g];
+                P2PF32Src<HILO> v;
+                float lx, ly, lz;
+                rel_f32<HILO>(px[g], cx, v.a.x, lx);
+                rel_f32<HILO>(py[g], cy, v.a.y, ly);
+                rel_f32<HILO>(pz[g], cz, v.a.z, lz);
+                v.a.w = qq.x * inv4pi;
+                if constexpr (HILO) {
+                    v.b = make_float4(lx, ly, lz, qq.y * inv4pi);
+                } else {
+                    v.qi = qq.y * inv4pi;
+                }
+                return v;
+            },
+            [&](const P2PTgt32q<HILO>& T, const P2PF32Src<HILO>& s, P2PAcc32& a, P2PAcc32& cv) {
+                pair_f32_mut<HILO>(T, s, k2pi, ftol, a, cv);
+            },
+            [&](int64_t t, const P2PAcc32& a) { partial[rb + (t - t0)] = make_float2(a.re, a.im); },
+            reinterpret_cast<P2PAcc32*>(partial + it.col[item]));
+    }
+}
+
+// Gather task j (leaf l = task_leaf[j]): out[x] = sum over its contributor
+// segments c in [cptr[j], cptr[j+1]) (in list order) of partial[cbase[c] + x],
+// xlo[c] <= x < xhi[c]; out = near + tgt_lo[l] when task_out[j] < 0, else
+// partial + task_out[j] (a pre-sum row read by a later pass).  FP64 sums.
+template <typename R>
+__global__ void __launch_bounds__(64) p2p_gather_kernel(int64_t n, const int32_t* __restrict__ task_leaf,
+                                                        const int64_t* __restrict__ task_out,
+                                                        const int64_t* __restrict__ tgt_lo,
+                                                        const int64_t* __restrict__ tgt_hi,
+                                                        const int64_t* __restrict__ cptr,
+                                                        const int64_t* __restrict__ cbase,
+                                                        const int32_t* __restrict__ cxlo,
+                                                        const int32_t* __restrict__ cxhi, cx<R>* partial,
+                                                        cx<R>* __restrict__ near) {
+    const int64_t j = blockIdx.x;
+    const int l = task_leaf[j];
+    const int64_t t0 = tgt_lo[l];
+    const int nt = (int)(tgt_hi[l] - t0);
+    const int64_t ob = task_out[j];
+    cx<R>* out = ob < 0 ? near + t0 : partial + ob;
+    const int64_t c0 = cptr[j], c1 = cptr[j + 1];
+    for (int x = threadIdx.x; x < nt; x += blockDim.x) {
+        double2 acc = make_double2(0.0, 0.0);
+        for (int64_t c = c0; c < c1; ++c) {
+            if (x >= __ldg(cxlo + c) && x < __ldg(cxhi + c)) acc = cadd(acc, to_d(partial[__ldg(cbase + c) + x]));
+        }
+        out[x] = from_d<cx<R>>(acc);
+    }
+}
+
 // K10: direct sum (FP64).  Sources are split over blockIdx.y so that a few
 // thousand check targets still fill the GPU; partial sums land in
 // part[blockIdx.y][target] and are reduced in a fixed order by direct_reduce.
@@ -2599,6 +3013,48 @@ int launch_p2p(int64_t n_items, const int32_t* item_leaf, const int64_t* item_f0
     return report(cudaGetLastError(), "p2p");
 }
 
+template <typename R>
+int launch_p2p_mutual(int64_t n_items, const int32_t* item_leaf, const int64_t* item_f0, const int64_t* item_f1,
+                      const int64_t* item_row, const int64_t* item_col, const int64_t* tgt_lo,
+                      const int64_t* tgt_hi, const int64_t* ptr, const int64_t* src_lo, const int64_t* src_hi,
+                      const double* px, const double* py, const double* pz, const void* q, double kappa,
+                      double tol, void* partial, int32_t grid, int32_t hilo, void* stream) {
+    if (n_items == 0) return 0;
+    if (!grid_ok(n_items)) return -1;
+    cudaStream_t s = (cudaStream_t)stream;
+    const P2PMutItems it{item_leaf, item_f0, item_f1, item_row, item_col};
+    const unsigned ng = (unsigned)(grid > 0 && grid < n_items ? grid : n_items);
+    if constexpr (sizeof(R) == 4) {
+        if (hilo) {
+            carve(p2p_mut_f32_kernel<true>);
+            p2p_mut_f32_kernel<true><<<ng, P2P_NT, 0, s>>>(n_items, it, tgt_lo, tgt_hi, ptr, src_lo, src_hi, px, py,
+                                                           pz, (const float2*)q, kappa, tol, (float2*)partial);
+        } else {
+            carve(p2p_mut_f32_kernel<false>);
+            p2p_mut_f32_kernel<false><<<ng, P2P_NT, 0, s>>>(n_items, it, tgt_lo, tgt_hi, ptr, src_lo, src_hi, px,
+                                                            py, pz, (const float2*)q, kappa, tol, (float2*)partial);
+        }
+    } else {
+        carve(p2p_mut_kernel<R>);
+        p2p_mut_kernel<R><<<ng, P2P_NT, 0, s>>>(n_items, it, tgt_lo, tgt_hi, ptr, src_lo, src_hi, px, py, pz,
+                                                (const cx<R>*)q, kappa, tol, (double2*)partial);
+    }
+    return report(cudaGetLastError(), "p2p_mutual");
+}
+
+template <typename R>
+int launch_p2p_gather(int64_t n, const int32_t* task_leaf, const int64_t* task_out, const int64_t* tgt_lo,
+                      const int64_t* tgt_hi, const int64_t* cptr, const int64_t* cbase, const int32_t* cxlo,
+                      const int32_t* cxhi, void* partial, void* near, void* stream) {
+    if (n == 0) return 0;
+    if (!grid_ok(n)) return -1;
+    carve(p2p_gather_kernel<R>);
+    p2p_gather_kernel<R><<<(unsigned)n, 64, 0, (cudaStream_t)stream>>>(n, task_leaf, task_out, tgt_lo, tgt_hi, cptr,
+                                                                      cbase, cxlo, cxhi, (cx<R>*)partial,
+                                                                      (cx<R>*)near);
+    return report(cudaGetLastError(), "p2p_gather");
+}
+
 }  // namespace
 
 extern "C" {
@@ -2686,6 +3142,22 @@ const char* defmm_last_error(void) { return g_last_error; }
                            const int64_t* perm, void* out, void* stream) {                                         \
         return launch_l2p<R>(L, n, leaf_cell, slot_lo, slot_hi, slot_dir, cell_start, cell_stop, cell_alpha,       \
                              cell_level, level_beta, dirs, px, py, pz, kappa, local, near, perm, out, stream);     \
+    }                                                                                                               \
+    int defmm_p2p_mutual_##SUFFIX(int64_t n_items, const int32_t* item_leaf, const int64_t* item_f0,              \
+                                  const int64_t* item_f1, const int64_t* item_row, const int64_t* item_col,       \
+                                  const int64_t* tgt_lo, const int64_t* tgt_hi, const int64_t* ptr,               \
+                                  const int64_t* src_lo, const int64_t* src_hi, const double* px,                 \
+                                  const double* py, const double* pz, const void* q, double kappa, double tol,    \
+                                  void* partial, int32_t grid, int32_t hilo, void* stream) {                      \
+        return launch_p2p_mutual<R>(n_items, item_leaf, item_f0, item_f1, item_row, item_col, tgt_lo, tgt_hi,      \
+                                    ptr, src_lo, src_hi, px, py, pz, q, kappa, tol, partial, grid, hilo, stream); \
+    }                                                                                                               \
+    int defmm_p2p_gather_##SUFFIX(int64_t n, const int32_t* task_leaf, const int64_t* task_out,                     \
+                                  const int64_t* tgt_lo, const int64_t* tgt_hi, const int64_t* cptr,              \
+                                  const int64_t* cbase, const int32_t* cxlo, const int32_t* cxhi, void* partial,  \
+                                  void* near, void* stream) {                                                     \
+        return launch_p2p_gather<R>(n, task_leaf, task_out, tgt_lo, tgt_hi, cptr, cbase, cxlo, cxhi, partial,      \
+                                    near, stream);                                                                \
     }                                                                                                               \
     int defmm_p2p_##SUFFIX(int64_t n_items, const int32_t* item_leaf, const int64_t* item_f0,                    \
                            const int64_t* item_f1, const int64_t* item_out, const int64_t* tgt_lo,                \

@@ -19,7 +19,7 @@ import torch
 from . import _lib
 from .config import FmmConfig, FmmInfo, InteractionEvent, TreeConfig
 from .geometry import compute_root_box
-from .plan import build_plan, p2p_work_items
+from .plan import build_plan, p2p_mutual_lists, p2p_work_items
 from .tree import build_tree
 
 __all__ = ["FmmPlan", "run_fmm", "run_fmm_full"]
@@ -502,6 +502,22 @@ class FmmPlan:
         self.n_split = int(wi["split_leaf"].shape[0])
         self.p2p_split = [_dev(wi["split_leaf"], i32, d), _dev(wi["split_base"], i64, d), _dev(wi["split_n"], i32, d)]
         self._partial_size = wi["partial_size"]
+        # mutual P2P (K1 v2): single-tree, unsharded plans evaluate every near-field
+        # pair once for both directions (DEFMM_P2P_MUTUAL=0 keeps the one-directional kernel)
+        self.p2p_mut = None
+        if self.same and self.shard is None and os.environ.get("DEFMM_P2P_MUTUAL", "1") != "0":
+            ml = p2p_mutual_lists(p.p2p_ptr, p.p2p_lo, p.p2p_hi, tt.start[p.leaf_cells], tt.stop[p.leaf_cells],
+                                  p.counts["p2p_pairs"])
+            if ml is not None:
+                self.p2p_mut = {k: _dev(ml[k], i32 if k == "item_leaf" else i64, d)
+                                for k in ("item_leaf", "item_f0", "item_f1", "item_row", "item_col", "ptr", "lo",
+                                          "hi")}
+                self.p2p_mut["n_items"] = int(ml["item_leaf"].shape[0])
+                self.p2p_mut["gather"] = [
+                    (int(g["task_leaf"].shape[0]), _dev(g["task_leaf"], i32, d), _dev(g["task_out"], i64, d),
+                     _dev(g["cptr"], i64, d), _dev(g["cbase"], i64, d), _dev(g["cxlo"], i32, d),
+                     _dev(g["cxhi"], i32, d)) for g in ml["gather"]]
+                self._partial_size = max(self._partial_size, ml["partial_size"])
         # workspaces (storage precision per FmmConfig.dtype)
         cd = self.cdtype
         self.mult = torch.empty((max(p.n_mult, 1), self.L3), dtype=cd, device=d)
@@ -803,10 +819,20 @@ class FmmPlan:
             if stage_events is not None:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e0.record(side)
-            _lib.call(self._op("p2p"), self.n_items, *self.p2p_items, self.tgt_lo, self.tgt_hi, self.p2p_ptr,
-                      self.p2p_lo, self.p2p_hi, *self.t_xyz, *self.s_xyz, self.q, float(p.kappa), float(p.tol),
-                      self.near, self.p2p_partial, self.n_split, *self.p2p_split, int(self.p2p_grid),
-                      int(self.p2p_hilo), side.cuda_stream)
+            m = self.p2p_mut
+            if m is not None:
+                _lib.call(self._op("p2p_mutual"), m["n_items"], m["item_leaf"], m["item_f0"], m["item_f1"],
+                          m["item_row"], m["item_col"], self.tgt_lo, self.tgt_hi, m["ptr"], m["lo"], m["hi"],
+                          *self.s_xyz, self.q, float(p.kappa), float(p.tol), self.p2p_partial,
+                          int(self.p2p_grid), int(self.p2p_hilo), side.cuda_stream)
+                for nt_, tleaf, tout, cptr, cbase, cxlo, cxhi in m["gather"]:
+                    _lib.call(self._op("p2p_gather"), nt_, tleaf, tout, self.tgt_lo, self.tgt_hi, cptr, cbase,
+                              cxlo, cxhi, self.p2p_partial, self.near, side.cuda_stream)
+            else:
+                _lib.call(self._op("p2p"), self.n_items, *self.p2p_items, self.tgt_lo, self.tgt_hi, self.p2p_ptr,
+                          self.p2p_lo, self.p2p_hi, *self.t_xyz, *self.s_xyz, self.q, float(p.kappa),
+                          float(p.tol), self.near, self.p2p_partial, self.n_split, *self.p2p_split,
+                          int(self.p2p_grid), int(self.p2p_hilo), side.cuda_stream)
             if stage_events is not None:
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record(side)
@@ -997,7 +1023,8 @@ class FmmPlan:
                                                                    self.bk_rows.shape[0])) + int(bool(self.staged))
         else:
             m2l = 1
-        return 4 + (1 if self.n_split else 0) + len(self.m2m) + len(self.l2l) + m2l
+        p2p_extra = len(self.p2p_mut["gather"]) if self.p2p_mut is not None else int(bool(self.n_split))
+        return 4 + p2p_extra + len(self.m2m) + len(self.l2l) + m2l
 
     def events(self):
         """InteractionEvent list (traversal.py:80-85) with Cell views."""

@@ -694,6 +694,121 @@ def p2p_work_items(ptr, run_len, nt, max_pairs: int = P2P_ITEM_PAIRS) -> dict:
     }
 
 
+P2P_MUTUAL_MAX_LEAF = 256  # particles per leaf the mutual kernel handles (2 per thread)
+P2P_GATHER_CHUNK = 128  # contributor segments one gather task sums
+
+
+def p2p_mutual_lists(ptr, lo, hi, tlo, thi, n_pairs=None, max_pairs: int = P2P_ITEM_PAIRS):
+    """Lists of the mutual P2P (K1 v2, defmm_p2p_mutual_* / defmm_p2p_gather_*)
+    for a single-tree plan.  Target leaf l (Morton order, particles
+    [tlo[l], thi[l])) has the merged source runs [lo[e], hi[e]), e in
+    [ptr[l], ptr[l+1]).  Each list is clipped to particles >= tlo[l] -- the
+    leaf itself first, then the later leaves, whose pairs are evaluated once
+    for both directions -- and cut into work items.  Returns the clipped CSR,
+    the items (leaf, f0, f1, row/col offsets into the partial buffer), the
+    partial size, and the gather passes: lists of tasks (task_leaf, task_out:
+    offset into partial, or -1 = the leaf's slice of near) with their
+    contributor segments (cbase, xlo, xhi) in fixed order, out[x] = sum_c
+    partial[cbase[c] + x]; the last pass writes near for every leaf, earlier
+    passes pre-sum the longest lists in chunks.  None if the relation is not
+    symmetric (n_pairs check) or a leaf is too large."""
+    ptr = np.asarray(ptr, np.int64)
+    lo, hi = np.asarray(lo, np.int64), np.asarray(hi, np.int64)
+    tlo, thi = np.asarray(tlo, np.int64), np.asarray(thi, np.int64)
+    nl = tlo.shape[0]
+    nt = thi - tlo
+    if nl == 0 or nt.max() > P2P_MUTUAL_MAX_LEAF:
+        return None
+    run_leaf = np.repeat(np.arange(nl), np.diff(ptr))
+    clo = np.maximum(lo, tlo[run_leaf])
+    keep = hi > clo
+    c_leaf, c_lo, c_hi = run_leaf[keep], clo[keep], hi[keep]
+    c_ptr = np.searchsorted(c_leaf, np.arange(nl + 1)).astype(np.int64)
+    # every list starts with the leaf's own particles
+    first = c_ptr[:-1]
+    if np.any(np.diff(c_ptr) == 0) or np.any(c_lo[first] != tlo) or np.any(c_hi[first] < thi):
+        return None
+    c_len = c_hi - c_lo
+    cs = np.concatenate([[0], np.cumsum(c_len)])
+    ns = cs[c_ptr[1:]] - cs[c_ptr[:-1]]
+    if n_pairs is not None and int((nt * (2 * (ns - nt) + nt)).sum()) != int(n_pairs):
+        return None  # not a symmetric relation: keep the one-directional kernel
+    wi = p2p_work_items(c_ptr, c_len, nt, max_pairs)
+    il, f0, f1 = wi["item_leaf"].astype(np.int64), wi["item_f0"], wi["item_f1"]
+    ni = il.shape[0]
+    size = nt[il] + (f1 - f0)
+    off = np.concatenate([[0], np.cumsum(size)])
+    row, col = off[:-1], off[:-1] + nt[il]
+    # column segments: the item's flattened range past the leaf's own particles,
+    # cut at run boundaries, then at leaf boundaries
+    F0 = cs[c_ptr[il]] + np.maximum(f0, nt[il])
+    F1 = cs[c_ptr[il]] + f1
+    has = F1 > F0
+    r0 = np.searchsorted(cs, F0, side="right") - 1
+    r1 = np.searchsorted(cs, np.maximum(F1 - 1, F0), side="right") - 1
+    cnt = np.where(has, r1 - r0 + 1, 0)
+    it = np.repeat(np.arange(ni), cnt)
+    r = np.repeat(r0, cnt) + (np.arange(int(cnt.sum())) - np.repeat(np.cumsum(cnt) - cnt, cnt))
+    sF0 = np.maximum(F0[it], cs[r])
+    sF1 = np.minimum(F1[it], cs[r + 1])
+    g0 = c_lo[r] + (sF0 - cs[r])
+    g1 = g0 + (sF1 - sF0)
+    b0 = np.searchsorted(tlo, g0, side="right") - 1
+    b1 = np.searchsorted(tlo, g1 - 1, side="right") - 1
+    bc = b1 - b0 + 1
+    sg = np.repeat(np.arange(it.shape[0]), bc)
+    B = np.repeat(b0, bc) + (np.arange(int(bc.sum())) - np.repeat(np.cumsum(bc) - bc, bc))
+    xlo = np.maximum(g0[sg], tlo[B]) - tlo[B]
+    xhi = np.minimum(g1[sg], thi[B]) - tlo[B]
+    # partial index of particle tlo[B] + x: col + (F - (cs[c_ptr] + f0)), F = sF0 + (g - g0)
+    ii = it[sg]
+    cb = col[ii] + (sF0[sg] - (cs[c_ptr[il[ii]]] + f0[ii])) + (tlo[B] - g0[sg])
+    # contributors per leaf: its own items' rows (item order), then the column segments
+    leaf_all = np.concatenate([il, B])
+    base_all = np.concatenate([row, cb])
+    xlo_all = np.concatenate([np.zeros(ni, np.int64), xlo])
+    xhi_all = np.concatenate([nt[il], xhi])
+    o = np.argsort(leaf_all, kind="stable")
+    c_leaf_s, c_base, c_xlo, c_xhi = leaf_all[o], base_all[o], xlo_all[o], xhi_all[o]
+    # gather passes: a leaf listed by very many items (particles of a large cell next
+    # to many small target leaves: cfg3) is summed in chunks of <= P2P_GATHER_CHUNK
+    # segments into extra partial rows first, so that no gather task is long
+    total = int(off[-1])
+    passes = []
+    while True:
+        cptr = np.searchsorted(c_leaf_s, np.arange(nl + 1)).astype(np.int64)
+        cnt_l = np.diff(cptr)
+        heavy = cnt_l > P2P_GATHER_CHUNK
+        if not heavy.any():
+            break
+        hv = heavy[c_leaf_s]
+        j = np.arange(c_leaf_s.shape[0]) - cptr[c_leaf_s]
+        key = c_leaf_s[hv] * (int(cnt_l.max()) // P2P_GATHER_CHUNK + 2) + j[hv] // P2P_GATHER_CHUNK
+        tk, tinv = np.unique(key, return_inverse=True)  # tasks = (leaf, chunk), in (leaf, chunk) order
+        t_leaf = tk // (int(cnt_l.max()) // P2P_GATHER_CHUNK + 2)
+        t_out = total + np.concatenate([[0], np.cumsum(nt[t_leaf])[:-1]])
+        total += int(nt[t_leaf].sum())
+        t_ptr = np.searchsorted(tinv.reshape(-1), np.arange(tk.shape[0] + 1)).astype(np.int64)
+        passes.append({"task_leaf": t_leaf.astype(np.int32), "task_out": t_out.astype(np.int64), "cptr": t_ptr,
+                       "cbase": c_base[hv].astype(np.int64), "cxlo": c_xlo[hv].astype(np.int32),
+                       "cxhi": c_xhi[hv].astype(np.int32)})
+        # the heavy leaves now read their chunk sums (full range) instead
+        leaf2 = np.concatenate([c_leaf_s[~hv], t_leaf])
+        base2 = np.concatenate([c_base[~hv], t_out])
+        xlo2 = np.concatenate([c_xlo[~hv], np.zeros(t_leaf.shape[0], np.int64)])
+        xhi2 = np.concatenate([c_xhi[~hv], nt[t_leaf]])
+        o2 = np.argsort(leaf2, kind="stable")
+        c_leaf_s, c_base, c_xlo, c_xhi = leaf2[o2], base2[o2], xlo2[o2], xhi2[o2]
+    passes.append({"task_leaf": np.arange(nl, dtype=np.int32), "task_out": np.full(nl, -1, np.int64), "cptr": cptr,
+                   "cbase": c_base.astype(np.int64), "cxlo": c_xlo.astype(np.int32), "cxhi": c_xhi.astype(np.int32)})
+    return {
+        "ptr": c_ptr, "lo": c_lo, "hi": c_hi,
+        "item_leaf": il.astype(np.int32), "item_f0": f0.astype(np.int64), "item_f1": f1.astype(np.int64),
+        "item_row": row.astype(np.int64), "item_col": col.astype(np.int64), "partial_size": total,
+        "gather": passes,
+    }
+
+
 def _check_stencils(sym_t, sym_lev, tree, order, tol):
     """fourier.py:179-180: a symbol stencil touching r < tol means the MAC is
     violated -> ValueError (same expression as precompute_symbol)."""

@@ -501,6 +501,60 @@ def test_m2l_stage_lists_replay_every_event(case, ns_cap):
         assert sorted(got[slot]) == want
 
 
+@pytest.mark.parametrize("max_pairs,chunk", [(1 << 16, 128), (700, 3)])
+@pytest.mark.parametrize("case", ["cubesurf4000", "volume3000", "c1_kd16", "flat50", "twocluster"])
+def test_p2p_mutual_lists_reproduce_the_near_field(case, max_pairs, chunk, monkeypatch):
+    """plan.p2p_mutual_lists (mutual P2P, K1 v2): evaluating every item the way
+    the kernel does (rows over its whole clipped range, columns past the
+    leaf's own particles) and gathering the contributor segments gives the
+    one-directional near-field sums, with a symmetric stand-in kernel."""
+    from paper_2202_04894_b200 import plan as plan_mod
+    from paper_2202_04894_b200.plan import p2p_mutual_lists
+
+    monkeypatch.setattr(plan_mod, "P2P_GATHER_CHUNK", chunk)  # 3: several pre-sum passes
+    tr, ps, p = _plan(load_case(case))
+    tlo, thi = tr.start[p.leaf_cells], tr.stop[p.leaf_cells]
+    ml = p2p_mutual_lists(p.p2p_ptr, p.p2p_lo, p.p2p_hi, tlo, thi, p.counts["p2p_pairs"], max_pairs)
+    assert ml is not None
+    n = ps.n
+    rng = np.random.default_rng(5)
+    q = rng.normal(size=n) + 1j * rng.normal(size=n)
+    x = ps.positions
+    G = 1.0 / (1.0 + np.linalg.norm(x[:, None, :] - x[None, :, :], axis=2))  # symmetric
+    want = np.zeros(n, complex)
+    for l in range(tlo.shape[0]):
+        for e in range(p.p2p_ptr[l], p.p2p_ptr[l + 1]):
+            a, b = p.p2p_lo[e], p.p2p_hi[e]
+            want[tlo[l]:thi[l]] += G[tlo[l]:thi[l], a:b] @ q[a:b]
+    part = np.full(ml["partial_size"], np.nan + 0j)
+    for i in range(ml["item_leaf"].shape[0]):
+        l = int(ml["item_leaf"][i])
+        src = np.concatenate([np.arange(ml["lo"][e], ml["hi"][e]) for e in range(ml["ptr"][l], ml["ptr"][l + 1])])
+        assert np.array_equal(src[: thi[l] - tlo[l]], np.arange(tlo[l], thi[l]))
+        f0, f1 = int(ml["item_f0"][i]), int(ml["item_f1"][i])
+        sl = src[f0:f1]
+        t = np.arange(tlo[l], thi[l])
+        part[ml["item_row"][i]: ml["item_row"][i] + t.size] = G[np.ix_(t, sl)] @ q[sl]
+        part[ml["item_col"][i]: ml["item_col"][i] + sl.size] = G[np.ix_(sl, t)] @ q[t]
+    got = np.full(n, np.nan + 0j)
+    part = np.concatenate([part, np.full(ml["partial_size"] - part.shape[0], np.nan + 0j)])
+    assert ml["gather"][-1]["task_leaf"].shape[0] == tlo.shape[0] and np.all(ml["gather"][-1]["task_out"] == -1)
+    for gp in ml["gather"]:
+        assert np.diff(gp["cptr"]).max() <= chunk
+        for j, l in enumerate(gp["task_leaf"].tolist()):
+            acc = np.zeros(thi[l] - tlo[l], complex)
+            for c in range(gp["cptr"][j], gp["cptr"][j + 1]):
+                xs = np.arange(gp["cxlo"][c], gp["cxhi"][c])
+                assert 0 <= gp["cxlo"][c] < gp["cxhi"][c] <= thi[l] - tlo[l]
+                acc[xs] += part[gp["cbase"][c] + xs]
+            if gp["task_out"][j] < 0:
+                got[tlo[l]:thi[l]] = acc
+            else:
+                part[gp["task_out"][j]: gp["task_out"][j] + acc.size] = acc
+    assert np.all(np.isfinite(got))
+    assert np.linalg.norm(got - want) <= 1e-12 * np.linalg.norm(want)
+
+
 def test_p2p_overlap_policy():
     """P2P beside the M2L (high-priority far field) only when every M2L level
     runs the quartet kernel (measured, profiles/r01_summary_v9.md)."""

@@ -5,7 +5,7 @@ cd ${GRAFT_REPO_ROOT:-.}
 OUT=gpurun_out/prof_stage; mkdir -p $OUT
 NCU=/usr/local/cuda/bin/ncu
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
-B="python bench.py --workload cfg2 --dtype ${DT:-c64} --steps 1 --warmup 0 --no-cpu-baseline --no-secondary --profile --m2l-levels ${MODE:-staged}"
+B="python bench.py --workload ${WL:-cfg2} --dtype ${DT:-c64} --steps 1 --warmup 0 --no-cpu-baseline --no-secondary --profile --m2l-levels ${MODE:-staged}"
 timeout 600 $B > $OUT/plain.log 2>&1 && \
 timeout 1200 $NCU --set full --clock-control none --import-source on -k regex:${KERN:-m2l_stage} -s 0 -c 1 -o $OUT/full -f $B > $OUT/ncu.log 2>&1
 echo "rc=$?" > $OUT/rc.txt
