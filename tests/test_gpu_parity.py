@@ -44,12 +44,30 @@ def test_run_fmm_matches_reference_golden(case):
     assert _rel(pot, g["pot"]) <= FP64_TOL
 
 
-C64_TOL = 2e-5  # relative L2 of the complex64-storage path against the FP64 reference
+# complex64 storage against the FP64 reference: the north-star bar 1e-2 eps_ref where FP32
+# arithmetic can reach it, else the FP32 floor of these sums (measured <= 1.6e-6 on the small
+# cases whose bar is below it; tools/gpu/c64_bar.py prints the table)
+C64_FLOOR = 2e-6
+C64_TOL = 5e-6  # bound used where eps_ref is not computed (kernel-variant tests)
 
 
-@pytest.mark.parametrize("case", ["cubesurf4000", "c1_kd8", "volume3000", "sphere3000", "refined3000"])
+def _c64_bar(g):
+    """max(1e-2 eps_ref, C64_FLOOR), eps_ref = rel-L2 of the reference's potentials against
+    the FP64 direct sum (kernel.py:58-75, evaluated by the GPU direct kernel)."""
+    from paper_2202_04894_b200 import HelmholtzKernel, direct_sum
+    from paper_2202_04894_b200.geometry import compute_root_box
+
+    pts = g["points"]
+    kern = HelmholtzKernel(kappa=g["config"].get("kappa", 0.0), singularity_tol=1e-12 * compute_root_box(pts).side)
+    d = direct_sum(kern, pts, pts, g["charges"])
+    return max(1e-2 * _rel(g["pot"], d), C64_FLOOR)
+
+
+@pytest.mark.parametrize("case", ["cubesurf4000", "c1_kd8", "c1_kd16", "ellipsoid3000", "volume3000", "sphere3000",
+                                  "refined3000"])
 def test_run_fmm_c64_matches_reference_golden(case):
-    """complex64 storage (BASELINE cfg2/3/4 dtype): same lists, FP32 streams."""
+    """complex64 storage (BASELINE cfg2/3/4 dtype): same lists, FP32 streams; orders 4, 5
+    (ellipsoid3000) and 6."""
     from paper_2202_04894_b200 import FmmConfig, run_fmm_full
 
     g = load_case(case)
@@ -57,7 +75,7 @@ def test_run_fmm_c64_matches_reference_golden(case):
     pot, info = run_fmm_full(pts, pts, q, FmmConfig(dtype="c64", **g["config"]))
     assert info.counts == g["counts"]
     assert pot.dtype == np.complex128
-    assert _rel(pot, g["pot"]) <= C64_TOL
+    assert _rel(pot, g["pot"]) <= _c64_bar(g)
 
 
 def test_flat_tree_is_exact_p2p():
