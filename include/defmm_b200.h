@@ -87,6 +87,26 @@ int defmm_dtt_source_hats(const defmm_dtt* d, const int64_t* m_dense, const int6
                           int32_t* src_hat, int64_t* hat_slot, int64_t* n_hat);
 void defmm_dtt_free(defmm_dtt* d);
 
+/* ---- device: plan construction -----------------------
+ * defmm_tree_keys -- tree.py:132-213's octant decisions per particle: keys[i] =
+ * the octant path of pts[i] (n x 3 row-major doubles, DEVICE) to `depth` <= 21
+ * levels, 3 bits per level, level 0 in the highest bits; octant = 4 (x >= cx) +
+ * 2 (y >= cy) + (z >= cz), centre = (lower + coords * beta) + 0.5 * beta with
+ * every FP64 product and sum rounded separately (bit-identical to tree.py:165-166,
+ * geometry.py:71-72).  lower[3] is HOST memory.
+ * defmm_dtt_classify -- one level of the dual tree traversal (traversal.py:320-348)
+ * over n candidate pairs (pair_t[i], pair_s[i]) of same-level cells (all arrays
+ * DEVICE): kind[i] = 0 M2L (integer gap^2 >= g2min, the reference MAC as in
+ * defmm_dtt_build), 1 P2P (else, either cell a leaf), 2 expand (nexp[i] = sons x
+ * sons pairs); for M2L pairs dense[i] = tab_off + dense(t - s) over |t|_inf <= R and
+ * key[i] = key_tab[dense[i]]; *status = 1 if a translation leaves the table. */
+int defmm_tree_keys(int64_t n, const double* pts, const double lower[3], double side, int32_t depth,
+                    int64_t* keys, void* stream);
+int defmm_dtt_classify(int64_t n, const int64_t* pair_t, const int64_t* pair_s, const int64_t* t_coords,
+                       const int64_t* s_coords, const int64_t* t_nsons, const int64_t* s_nsons, int64_t g2min,
+                       int32_t R, int64_t tab_off, const int32_t* key_tab, int8_t* kind, int32_t* key,
+                       int64_t* dense, int64_t* nexp, int32_t* status, void* stream);
+
 /* ---- host: stage packing of the staged M2L (K7 v13) --------------------------
  * Classes c < ncls (ordered; cls_cta[c] non-decreasing) read the symbols
  * cls_sym[cls_ptr[c] .. cls_ptr[c+1]) (ids < n_sym_ids).  Greedy, in order: a

@@ -30,6 +30,8 @@ _SIGS = {
     "defmm_dtt_source_hats": [_vp] * 6 + [_i64, _vp, _vp, _vp],
     "defmm_dtt_free": [_vp],
     "defmm_stage_pack": [_i64, _vp, _vp, _vp, _i64, _i32, _vp],
+    "defmm_tree_keys": [_i64, _vp, _vp, _f64, _i32, _vp, _vp],
+    "defmm_dtt_classify": [_i64] + [_vp] * 6 + [_i64, _i32, _i64] + [_vp] * 7,
     "defmm_fma_peak": [_i32, _i64, _vp, _vp],
     "defmm_l2_stream": [_vp, _i64, _i32, _i32, _vp, _vp],
     "defmm_m2l_canon_c128": [_i32, _i64] + [_vp] * 9,

@@ -20,7 +20,7 @@ BUILD = os.path.join(HERE, "_build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU_SOURCES = ["defmm_kernels.cu", "fma_peak.cu"]
+CU_SOURCES = ["defmm_kernels.cu", "fma_peak.cu", "plan_gpu.cu"]
 CPP_SOURCES = ["tree_build.cpp", "dtt_build.cpp", "m2l_stage.cpp"]
 
 

@@ -88,6 +88,62 @@ def m2l_groups(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent, K: int = 2
     return {"n": ng, "K": K, "grp_slot": grp_slot.reshape(-1), "grp_ptr": grp_ptr, "ent": out}
 
 
+def m2l_groups_dev(ids, rows, row_ptr, ent_dev, l_cell, l_dir, level, parent, K: int, device) -> dict:
+    """m2l_groups with the per-event work (gather, sort by (group, source, row),
+    merge per source) on the device; the row-level grouping (a few 1e4..1e6
+    rows) stays on the host.  ``ent_dev``: the (n, 2) int32 event table on the
+    device.  Returns device tensors; equal to m2l_groups bit for bit
+    (tests/test_gpu_build.py)."""
+    S = 4 if K <= 3 else 8
+    i64, i32 = torch.int64, torch.int32
+    if ids.size == 0:
+        return {"n": 0, "K": K, "grp_slot": torch.zeros(0, dtype=i64, device=device),
+                "grp_ptr": torch.zeros(1, dtype=i64, device=device),
+                "ent": torch.zeros((0, S), dtype=i32, device=device)}
+    slots = rows[ids]
+    cell = l_cell[slots]
+    key = l_dir[slots].astype(np.int64)
+    lev = level[cell].astype(np.int64)
+    par = parent[cell].astype(np.int64)
+    o = np.lexsort((cell, par, key, lev))
+    ids, slots, key, lev, par = ids[o], slots[o], key[o], lev[o], par[o]
+    n = ids.shape[0]
+    new = np.ones(n, bool)
+    new[1:] = (lev[1:] != lev[:-1]) | (key[1:] != key[:-1]) | (par[1:] != par[:-1])
+    gstart = np.nonzero(new)[0]
+    pos = np.arange(n) - gstart[np.cumsum(new) - 1]
+    side = pos % K
+    gid = np.cumsum(side == 0) - 1
+    ng = int(gid[-1]) + 1
+    grp_slot = np.full((ng, K), -1, np.int64)
+    grp_slot[gid, side] = slots
+    cnt = row_ptr[ids + 1] - row_ptr[ids]
+    with torch.cuda.device(device):
+        up = lambda a: torch.as_tensor(np.ascontiguousarray(a, np.int64)).to(device)  # noqa: E731
+        cnt_d, start_d, gid_d, side_d = up(cnt), up(row_ptr[ids]), up(gid), up(side)
+        tot = int(cnt.sum())
+        rep = torch.repeat_interleave(torch.arange(n, device=device), cnt_d, output_size=tot)
+        sel = (start_d - (torch.cumsum(cnt_d, 0) - cnt_d))[rep] + torch.arange(tot, device=device)
+        ev = ent_dev[sel]
+        es, et = ev[:, 0].to(i64), ev[:, 1]
+        eg, eside = gid_d[rep], side_d[rep]
+        nh = int(es.max().item()) + 1 if tot else 1
+        comp = (eg * nh + es) * K + eside  # distinct per event
+        comp, so = torch.sort(comp)
+        et, eside = et[so], eside[so]
+        gs = comp // K  # (group, source)
+        first = torch.ones(tot, dtype=torch.bool, device=device)
+        first[1:] = gs[1:] != gs[:-1]
+        eid = torch.cumsum(first, 0) - 1
+        m = int(eid[-1].item()) + 1 if tot else 0
+        out = torch.full((m, S), -1, dtype=i32, device=device)
+        out[:, K + 1:] = 0
+        out[eid, 0] = (gs % nh).to(i32)
+        out[eid, 1 + eside] = et
+        grp_ptr = torch.searchsorted((gs[first] // nh).contiguous(), torch.arange(ng + 1, device=device))
+        return {"n": ng, "K": K, "grp_slot": up(grp_slot.reshape(-1)), "grp_ptr": grp_ptr, "ent": out}
+
+
 def m2l_pairs(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent) -> dict:
     """K = 2 sibling groups (m2l_groups)."""
     return m2l_groups(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent, 2)
@@ -343,10 +399,15 @@ class FmmPlan:
 
     def __init__(self, targets, sources=None, config: FmmConfig = FmmConfig(), device="cuda",
                  keep_events: bool = False, charges=None, reuse: "FmmPlan | None" = None,
-                 shard=None, allreduce=None, m2l: str = "auto", m2l_levels: dict | None = None):
+                 shard=None, allreduce=None, m2l: str = "auto", m2l_levels: dict | None = None,
+                 build: str | None = None):
         """``reuse``: share the host tree + lists of an existing plan built for
         the same geometry and (order, ncrit, eta, kappa) -- e.g. to run the same
         lists at another storage precision.
+
+        ``build``: "gpu" builds the octree and the dual-tree-traversal lists on
+        the device (gpu_build.py; same trees and lists bit for bit), "host" on
+        the CPU (native C++); default: env DEFMM_PLAN_BUILD, else "gpu".
 
         ``shard``: (rank, world) or a ``parallel.Shard`` -- this process then
         computes only its Morton chunk (parallel.py); ``allreduce(tensor)``
@@ -387,19 +448,34 @@ class FmmPlan:
         src = targets if same else sources
         n_src = np.atleast_2d(np.asarray(src)).shape[0]
         qs = np.zeros(n_src, complex) if charges is None else charges
+        self.build = build or os.environ.get("DEFMM_PLAN_BUILD", "gpu")
+        if self.build not in ("gpu", "host"):
+            raise ValueError(f"unknown plan builder {self.build!r}")
+
+        def tree_of(pts, q, box=None):
+            if self.build == "gpu":
+                from .gpu_build import build_tree_gpu
+
+                try:
+                    return build_tree_gpu(pts, q, tree_cfg, root_box=box, device=self.device)
+                except NotImplementedError:  # deeper than the 21-level device keys
+                    pass
+            return build_tree(pts, q, tree_cfg, root_box=box)
+
         if same:
-            st, sp = build_tree(src, qs, tree_cfg)
+            st, sp = tree_of(src, qs)
             tt, tp = st, sp
         else:
             both = np.vstack([np.atleast_2d(targets), np.atleast_2d(sources)])
             box = compute_root_box(both)
-            st, sp = build_tree(sources, qs, tree_cfg, root_box=box)
-            tt, tp = build_tree(targets, np.zeros(np.atleast_2d(targets).shape[0]), tree_cfg, root_box=box)
+            st, sp = tree_of(sources, qs, box)
+            tt, tp = tree_of(targets, np.zeros(np.atleast_2d(targets).shape[0]), box)
         self.same = same
         self.tt, self.st, self.tp, self.sp = tt, st, tp, sp
         t1 = time.perf_counter()
         self.plan = build_plan(tt, st, config.order, config.kappa, config.eta, config.hf_switch,
-                               keep_events=keep_events)
+                               keep_events=keep_events, dtt="gpu" if self.build == "gpu" else "native",
+                               device=self.device)
         t2 = time.perf_counter()
         self.timings = {"tree": t1 - t0, "blank": t2 - t1}
         self._make_shard()
@@ -468,8 +544,8 @@ class FmmPlan:
         for kind in ("pair", "triple", "quartet"):
             gr = h[kind]
             if gr["n"]:
-                self.sib_groups.append((gr["K"], int(gr["n"]), _dev(gr["grp_slot"], i64, d),
-                                        _dev(gr["grp_ptr"], i64, d), _dev(gr["ent"].reshape(-1), i32, d)))
+                self.sib_groups.append((gr["K"], int(gr["n"]), gr["grp_slot"], gr["grp_ptr"],
+                                        gr["ent"].reshape(-1).contiguous()))
         self.n_pairs = sum(x[1] for x in self.sib_groups)
         sg = h["staged"]
         self.staged = None
@@ -603,12 +679,11 @@ class FmmPlan:
         _, rptr, rsel = _sub_csr(h["row_ptr"], is_rows)
         h["rk_rows"], h["rk_ptr"], h["rk_ent"] = rows[is_rows], rptr, h["ent"][rsel]
         # sibling pairs (K7 v8)
-        h["pair"] = m2l_groups(np.nonzero(pick("pair"))[0], rows, h["row_ptr"], h["ent"], p.l_cell, p.l_dir,
-                               tt.level, tt.parent, 2)
-        h["triple"] = m2l_groups(np.nonzero(pick("triple"))[0], rows, h["row_ptr"], h["ent"], p.l_cell, p.l_dir,
-                                 tt.level, tt.parent, 3)
-        h["quartet"] = m2l_groups(np.nonzero(pick("quartet"))[0], rows, h["row_ptr"], h["ent"], p.l_cell, p.l_dir,
-                                  tt.level, tt.parent, 4)
+        # sibling groups (K7 v8): per-event merging on the device (m2l_groups_dev)
+        ent_dev = _dev(h["ent"], torch.int32, self.device) if any(pick("pair", "triple", "quartet")) else None
+        for kind, K in (("pair", 2), ("triple", 3), ("quartet", 4)):
+            h[kind] = m2l_groups_dev(np.nonzero(pick(kind))[0], rows, h["row_ptr"], ent_dev, p.l_cell, p.l_dir,
+                                     tt.level, tt.parent, K, self.device)
         # staged M2L (K7 v13): warp units of sibling rows sharing staged symbols
         hat_coords = self.st.coords[p.m_cell[h["hat_slot"]]] if h["hat_slot"].size else np.zeros((0, 3), np.int64)
         h["staged"] = m2l_stage_lists(np.nonzero(pick("staged"))[0], rows, h["row_ptr"], h["ent"], p.l_cell,

@@ -196,7 +196,10 @@ class Plan:
 
 
 def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: float, hf_switch: float,
-               keep_events: bool = False) -> Plan:
+               keep_events: bool = False, dtt: str = "native", device="cuda") -> Plan:
+    """``dtt``: "native" = the multi-threaded host traversal (csrc/dtt_build.cpp),
+    "gpu" = the level-synchronous device traversal (gpu_build.GpuDtt); both
+    produce the same lists (tests/test_gpu_build.py)."""
     same = tt is st
     depth = max(tt.depth, st.depth)
     hf = hf_max_level(tt, depth, kappa, hf_switch)
@@ -212,7 +215,14 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
 
     # ---- dual tree traversal (native, traversal.py:320-348) ----------------
     g2min, R, tab_off, key_tab = _traversal_tables(tt, depth, hf, dt, dir_off, kappa, eta)
-    nat = NativeDtt(tt, st, depth, g2min, R, tab_off, key_tab)
+    if dtt == "gpu":
+        from .gpu_build import GpuDtt
+
+        nat = GpuDtt(tt, st, depth, g2min, R, tab_off, key_tab, device=device)
+    elif dtt == "native":
+        nat = NativeDtt(tt, st, depth, g2min, R, tab_off, key_tab)
+    else:
+        raise ValueError(f"unknown traversal builder {dtt!r}")
     row_ptr, row_t, row_key, row_lev = nat["row_ptr"], nat["row_t"], nat["row_key"], nat["row_lev"]
     ev_s, ev_trans = nat["ev_s"], nat["ev_trans"]
     pt, ps = nat["p_t"].astype(np.int64), nat["p_s"].astype(np.int64)

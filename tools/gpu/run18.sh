@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+O=gpurun_out/r18; mkdir -p $O
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_build.py -m gpu -q -x > $O/tests.log 2>&1
+echo "tests rc=$?" >> $O/rc.txt
+timeout 1500 python tools/gpu/time_build.py cfg2 cfg3 cfg5 cfg4 > $O/time_build.log 2>&1
