@@ -149,30 +149,23 @@ def m2l_pairs(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent) -> dict:
     return m2l_groups(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent, 2)
 
 
+# the mutual P2P (K1 v2) pays from ~1e8 near-field pairs on (cfg1, 1.4e7 pairs: 0.19 ms one-directional
+# against 0.28 ms mutual + gather; cfg2, 3.8e8: 0.47 -> 0.43 ms; cfg5, 2.7e9, c128: 9.85 -> 7.2 ms)
+P2P_MUTUAL_MIN_PAIRS = 100_000_000
+
 STAGE_NW, STAGE_K = 8, 4  # warp units per CTA, rows per warp unit (STG_NW, STG_K of the kernel)
 STAGE_SLOTS = 48  # symbol slices per shared-memory stage (ns_cap)
 STAGE_DEPTH = 3  # shared-memory ring stages
 STAGE_ENT_PAD = 64  # readable entries past the end (STG_ENT_PAD)
 
 
-def m2l_stage_lists(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent, coords, hat_coords,
-                    ns_cap: int = STAGE_SLOTS) -> dict:
-    """Lists of the staged M2L (K7 v13, defmm_m2l_stage_*).  The rows ``ids``
-    (indices into ``rows``) are grouped by (level, key, target parent) into warp
-    units of <= STAGE_K sibling rows; STAGE_NW consecutive warp units of one
-    (level, key) form a CTA.  An event (row, source s) belongs to the class
-    u = coords(s) - 2 coords(parent): within a CTA the symbols of a class are
-    shared by every warp unit.  Classes are packed in order into stages of <=
-    ns_cap distinct symbols; per (warp unit, class) one entry {source spectrum,
-    4 bytes: stage slot of row k's symbol or 0xff}.  ``hat_coords``: (n_hat, 3)
-    grid coordinates of each spectrum's source cell."""
+def _stage_units(ids, rows, l_cell, l_dir, level, parent):
+    """Row-level grouping of the staged M2L: rows sorted by (level, key, parent,
+    cell); warp units of <= STAGE_K sibling rows; STAGE_NW consecutive units of
+    one (level, key) per CTA.  Returns (ids, slots, par, k of each row, unit of
+    each row, warp of each unit, CTA of each unit, CTA count, cta_rows)."""
     K, NW = STAGE_K, STAGE_NW
     i32 = np.int32
-    if ids.size == 0:
-        return {"n": 0, "ns_cap": ns_cap, "row_slot": np.zeros(0, np.int64), "cta_stage": np.zeros(1, i32),
-                "cta_went": np.zeros(0, i32), "stage_slot_ptr": np.zeros(1, i32), "slot_sym": np.zeros(0, i32),
-                "stage_wend": np.zeros(0, i32), "ent": np.zeros((STAGE_ENT_PAD, 2), i32),
-                "cta_rows": np.zeros(0, i32)}
     slots = rows[ids]
     cell = l_cell[slots]
     key = l_dir[slots].astype(np.int64)
@@ -199,6 +192,29 @@ def m2l_stage_lists(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent, coord
     ncta = int(cta_of_wu[-1]) + 1
     cta_rows = np.full((ncta * NW, K), -1, i32)
     cta_rows[cta_of_wu[wu] * NW + ww[wu], kk] = np.arange(n)  # lhat row = position in the sorted order
+    return ids, slots, par, kk, wu, ww, cta_of_wu, ncta, cta_rows
+
+
+def m2l_stage_lists(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent, coords, hat_coords,
+                    ns_cap: int = STAGE_SLOTS) -> dict:
+    """Lists of the staged M2L (K7 v13, defmm_m2l_stage_*).  The rows ``ids``
+    (indices into ``rows``) are grouped by (level, key, target parent) into warp
+    units of <= STAGE_K sibling rows; STAGE_NW consecutive warp units of one
+    (level, key) form a CTA.  An event (row, source s) belongs to the class
+    u = coords(s) - 2 coords(parent): within a CTA the symbols of a class are
+    shared by every warp unit.  Classes are packed in order into stages of <=
+    ns_cap distinct symbols; per (warp unit, class) one entry {source spectrum,
+    4 bytes: stage slot of row k's symbol or 0xff}.  ``hat_coords``: (n_hat, 3)
+    grid coordinates of each spectrum's source cell."""
+    K, NW = STAGE_K, STAGE_NW
+    i32 = np.int32
+    if ids.size == 0:
+        return {"n": 0, "ns_cap": ns_cap, "row_slot": np.zeros(0, np.int64), "cta_stage": np.zeros(1, i32),
+                "cta_went": np.zeros(0, i32), "stage_slot_ptr": np.zeros(1, i32), "slot_sym": np.zeros(0, i32),
+                "stage_wend": np.zeros(0, i32), "ent": np.zeros((STAGE_ENT_PAD, 2), i32),
+                "cta_rows": np.zeros(0, i32)}
+    ids, slots, par, kk, wu, ww, cta_of_wu, ncta, cta_rows = _stage_units(ids, rows, l_cell, l_dir, level, parent)
+    n = ids.shape[0]
     # events
     cnt = row_ptr[ids + 1] - row_ptr[ids]
     rep = np.repeat(np.arange(n), cnt)
@@ -288,6 +304,98 @@ def m2l_stage_lists(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent, coord
             "cta_rows": cta_rows.reshape(-1)}
 
 
+def m2l_stage_lists_dev(ids, rows, row_ptr, ent_dev, l_cell, l_dir, level, parent, coords, hat_coords,
+                        ns_cap: int, device) -> dict:
+    """m2l_stage_lists with the per-event work on the device (sorts, uniques,
+    scatters on torch tensors; the greedy stage packer stays the native host
+    routine over the (class, symbol) pairs).  Same lists bit for bit
+    (tests/test_gpu_build.py); returns device tensors except row_slot."""
+    K, NW = STAGE_K, STAGE_NW
+    i32, i64 = torch.int32, torch.int64
+    if ids.size == 0:
+        h = m2l_stage_lists(ids, rows, row_ptr, np.zeros((0, 2), np.int32), l_cell, l_dir, level, parent, coords,
+                            hat_coords, ns_cap)
+        return {k: (torch.as_tensor(v).to(device) if isinstance(v, np.ndarray) and k != "row_slot" else v)
+                for k, v in h.items()}
+    ids, slots, par, kk, wu, ww, cta_of_wu, ncta, cta_rows = _stage_units(ids, rows, l_cell, l_dir, level, parent)
+    n = ids.shape[0]
+    cnt = row_ptr[ids + 1] - row_ptr[ids]
+    with torch.cuda.device(device):
+        up = lambda a: torch.as_tensor(np.ascontiguousarray(a, np.int64)).to(device)  # noqa: E731
+        cnt_d, start_d = up(cnt), up(row_ptr[ids])
+        tot = int(cnt.sum())
+        rep = torch.repeat_interleave(torch.arange(n, device=device), cnt_d, output_size=tot)
+        sel = (start_d - (torch.cumsum(cnt_d, 0) - cnt_d))[rep] + torch.arange(tot, device=device)
+        ev = ent_dev[sel]
+        e_src, e_tr = ev[:, 0].to(i64), ev[:, 1].to(i64)
+        e_wu = up(wu)[rep]
+        cw_d, ww_d = up(cta_of_wu), up(ww)
+        e_cta = cw_d[e_wu]
+        e_cw = e_cta * NW + ww_d[e_wu]
+        u = up(hat_coords)[e_src] - 2 * up(coords[par])[rep]
+        off = int(u.abs().max().item()) + 1
+        nbit = max(int(2 * off + 1).bit_length(), 1)
+        ucode = torch.zeros(tot, dtype=i64, device=device)
+        for b in range(nbit):
+            for a in range(3):
+                ucode |= (((u[:, a] + off) >> b) & 1) << (3 * b + 2 - a)
+        span3 = 1 << (3 * nbit)
+        cuniq, e_cls = torch.unique(e_cta * span3 + ucode, return_inverse=True)
+        ncls = int(cuniq.numel())
+        cls_cta = cuniq // span3
+        n_tr = int(e_tr.max().item()) + 1
+        su = torch.unique(e_cls * n_tr + e_tr)
+        su_cls_h = (su // n_tr).cpu().numpy()
+        su_tr_h = np.ascontiguousarray((su % n_tr).cpu().numpy(), np.int64)
+        nsym_cls = np.bincount(su_cls_h, minlength=ncls)
+        if nsym_cls.max() > 8:
+            raise RuntimeError("staged M2L: a class with more than 8 symbols")
+        cls_ptr = np.concatenate([[0], np.cumsum(nsym_cls)]).astype(np.int64)
+        st_rel_h = np.empty(ncls, np.int64)
+        cls_cta_h = np.ascontiguousarray(cls_cta.cpu().numpy(), np.int64)
+        _lib.check(_lib.load().defmm_stage_pack(ncls, cls_cta_h.ctypes.data, cls_ptr.ctypes.data,
+                                                su_tr_h.ctypes.data, n_tr, int(ns_cap), st_rel_h.ctypes.data),
+                   "defmm_stage_pack")
+        nst_cta_h = np.zeros(ncta, np.int64)
+        np.maximum.at(nst_cta_h, cls_cta_h, st_rel_h + 1)
+        cta_stage_h = np.concatenate([[0], np.cumsum(nst_cta_h)])
+        nstage = int(cta_stage_h[-1])
+        cta_stage, nst_cta = up(cta_stage_h), up(nst_cta_h)
+        cls_stage = cta_stage[cls_cta] + up(st_rel_h)
+        e_stage = cls_stage[e_cls]
+        suniq, e_slotg = torch.unique(e_stage * n_tr + e_tr, return_inverse=True)
+        slot_stage = suniq // n_tr
+        stage_slot_ptr = torch.searchsorted(slot_stage.contiguous(), torch.arange(nstage + 1, device=device))
+        if int((stage_slot_ptr[1:] - stage_slot_ptr[:-1]).max().item()) > ns_cap:
+            raise RuntimeError("staged M2L: stage over capacity")
+        e_slot = e_slotg - stage_slot_ptr[e_stage]
+        euniq, e_ent = torch.unique(e_cw * ncls + e_cls, return_inverse=True)
+        nent = int(euniq.numel())
+        ent_cw = euniq // ncls
+        ent_stage = cls_stage[euniq % ncls]
+        none = int(ns_cap) * 0x01010101
+        y = torch.full((nent + STAGE_ENT_PAD,), none, dtype=i64, device=device)
+        y.index_add_(0, e_ent, (e_slot - int(ns_cap)) << (8 * up(kk)[rep]))
+        ent32 = torch.zeros((nent + STAGE_ENT_PAD, 2), dtype=i32, device=device)
+        ent32[e_ent, 0] = e_src.to(i32)
+        ent32[:, 1] = torch.where(y >= (1 << 31), y - (1 << 32), y).to(i32)  # the uint32 bit pattern
+        cta_went = torch.searchsorted(ent_cw.contiguous(), torch.arange(ncta * NW, device=device)).to(i32)
+        st_cta = torch.repeat_interleave(torch.arange(ncta, device=device), nst_cta, output_size=nstage)
+        q_cw = (st_cta[:, None] * NW + torch.arange(NW, device=device)[None, :]).reshape(-1)
+        q_st = torch.repeat_interleave(torch.arange(nstage, device=device), NW)
+        wend = torch.searchsorted((ent_cw * (nstage + 1) + ent_stage).contiguous(), q_cw * (nstage + 1) + q_st,
+                                  right=True).to(i32)
+        q_w = torch.arange(NW, device=device).repeat(nstage)
+        qc = st_cta[q_st]
+        pos = cta_stage[qc] * NW + q_w * nst_cta[qc] + (q_st - cta_stage[qc])
+        stage_wend = torch.empty_like(wend)
+        stage_wend[pos] = wend
+        return {"n": ncta, "ns_cap": ns_cap, "row_slot": slots.astype(np.int64), "cta_stage": cta_stage.to(i32),
+                "cta_went": cta_went, "stage_slot_ptr": stage_slot_ptr.to(i32), "slot_sym": (suniq % n_tr).to(i32),
+                "stage_wend": stage_wend, "ent": ent32,
+                "cta_rows": torch.as_tensor(cta_rows.reshape(-1)).to(device)}
+
+
 def _rows_to_ids(slots, rows):
     """Local slots -> index into the sorted row-slot list ``rows`` (-1 if absent)."""
     slots = np.asarray(slots)
@@ -331,8 +439,13 @@ PAIR_MIN_ROWS = 2048
 # 2.377 ms, c128 4.71 -> 4.39); from L = 5 their larger spectra make them lose
 # (cfg3 9.35 -> 9.63, cfg2 L6 8.64 -> 11.7 ms) and the pair kernel (three
 # entries in flight, 56 registers) is best; triples never win
+# complex128 at L <= 4: the staged kernel (K7 v13; symbols staged once per 8 warp units in
+# shared memory) beats the quartets, cfg2 M2L 4.36 -> 3.79 ms; complex64 ties (2.44 vs 2.39,
+# profiles/r02/summary_v3.md) and keeps the quartets
 def sibling_kind(dtype: str, order: int) -> str:
-    return "quartet" if order <= 4 else "pair"
+    if order <= 4:
+        return "staged" if dtype == "c128" else "quartet"
+    return "pair"
 
 
 def block_levels(plan, tt):
@@ -552,7 +665,7 @@ class FmmPlan:
         self.stage_depth = int(os.environ.get("DEFMM_STAGE_DEPTH", STAGE_DEPTH))
         if sg["n"]:
             self.staged = (int(sg["n"]), int(sg["ns_cap"])) + tuple(
-                _dev(sg[k].reshape(-1), i32, d) for k in ("cta_stage", "cta_went", "stage_slot_ptr", "slot_sym",
+                sg[k].reshape(-1).contiguous() for k in ("cta_stage", "cta_went", "stage_slot_ptr", "slot_sym",
                                                          "stage_wend", "ent", "cta_rows"))
         # downward
         self.l2l = []
@@ -581,7 +694,9 @@ class FmmPlan:
         # mutual P2P (K1 v2): single-tree, unsharded plans evaluate every near-field
         # pair once for both directions (DEFMM_P2P_MUTUAL=0 keeps the one-directional kernel)
         self.p2p_mut = None
-        if self.same and self.shard is None and os.environ.get("DEFMM_P2P_MUTUAL", "1") != "0":
+        mut = os.environ.get("DEFMM_P2P_MUTUAL", "auto")  # "1" / "0" force, "auto": large near fields
+        if self.same and self.shard is None and (mut == "1" or (mut == "auto" and
+                                                                p.counts["p2p_pairs"] >= P2P_MUTUAL_MIN_PAIRS)):
             ml = p2p_mutual_lists(p.p2p_ptr, p.p2p_lo, p.p2p_hi, tt.start[p.leaf_cells], tt.stop[p.leaf_cells],
                                   p.counts["p2p_pairs"])
             if ml is not None:
@@ -686,15 +801,17 @@ class FmmPlan:
                                      tt.level, tt.parent, K, self.device)
         # staged M2L (K7 v13): warp units of sibling rows sharing staged symbols
         hat_coords = self.st.coords[p.m_cell[h["hat_slot"]]] if h["hat_slot"].size else np.zeros((0, 3), np.int64)
-        h["staged"] = m2l_stage_lists(np.nonzero(pick("staged"))[0], rows, h["row_ptr"], h["ent"], p.l_cell,
-                                      p.l_dir, tt.level, tt.parent, tt.coords, hat_coords,
-                                      int(os.environ.get("DEFMM_STAGE_SLOTS", STAGE_SLOTS)))
+        if ent_dev is None and any(pick("staged")):
+            ent_dev = _dev(h["ent"], torch.int32, self.device)
+        h["staged"] = m2l_stage_lists_dev(np.nonzero(pick("staged"))[0], rows, h["row_ptr"], ent_dev, p.l_cell,
+                                          p.l_dir, tt.level, tt.parent, tt.coords, hat_coords,
+                                          int(os.environ.get("DEFMM_STAGE_SLOTS", STAGE_SLOTS)), self.device)
         # lhat rows = the blocked rows, then the staged rows
         is_grp = pick("blocked")
         grp_rows = rows[is_grp]
         h["bk_rows"] = np.concatenate([grp_rows, h["staged"]["row_slot"]])
-        h["staged"]["cta_rows"] = np.where(h["staged"]["cta_rows"] >= 0,
-                                           h["staged"]["cta_rows"] + grp_rows.shape[0], -1).astype(np.int32)
+        cr = h["staged"]["cta_rows"]  # lhat rows of the staged kernel follow the blocked rows
+        h["staged"]["cta_rows"] = torch.where(cr >= 0, cr + int(grp_rows.shape[0]), cr).to(torch.int32)
         # groups of blocked levels, rows renumbered into lhat
         gr = h["grp_rows"]
         gr_slots = np.where(gr >= 0, rows[np.maximum(gr, 0)] if rows.size else -1, -1)
