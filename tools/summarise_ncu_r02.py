@@ -15,7 +15,8 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from ncu_to_json import parse  # noqa: E402
 
-M2L_KERNELS = ("m2l_group_kernel", "m2l_rows_kernel", "m2l_blocked_kernel", "f2l_rows_kernel", "m2l_lf")
+M2L_KERNELS = ("m2l_group_kernel", "m2l_rows_kernel", "m2l_blocked_kernel", "m2l_stage_kernel", "f2l_rows_kernel",
+               "m2l_lf")
 
 
 def main(src: str):
@@ -36,7 +37,7 @@ def main(src: str):
             "l2_to_l1_bytes": tot("l1tex__m_xbar2l1tex_read_bytes.sum"),
             "source": f"{os.path.basename(path)}: ncu --metrics, one cfg2 matvec, M2L-stage launches summed",
         }
-        p = next((v for k, v in res.items() if k.startswith("p2p")), None)
+        p = next((v for k, v in res.items() if k.startswith(("p2p_mut", "p2p_kernel", "p2p_f32"))), None)
         if p is not None:
             pipes[dt] = {
                 "fma_pipe_pct": p.get("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
