@@ -7,6 +7,9 @@
 #     cfg5 blocked M2L, the mutual P2P in both precisions
 set -u
 cd ${GRAFT_REPO_ROOT:-.}
+# the plan is built by the host builders here: under ncu every torch sort/scan of the device
+# builders would be profiled too (same trees and lists either way)
+export DEFMM_PLAN_BUILD=host
 OUT=gpurun_out/prof_r02; mkdir -p $OUT
 NCU=/usr/local/cuda/bin/ncu
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,l1tex__m_xbar2l1tex_read_bytes.sum,lts__t_sectors_srcunit_tex_op_read.sum,sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active,sm__inst_issued.avg.pct_of_peak_sustained_active,lts__throughput.avg.pct_of_peak_sustained_elapsed,l1tex__throughput.avg.pct_of_peak_sustained_active,sm__warps_active.avg.pct_of_peak_sustained_active
