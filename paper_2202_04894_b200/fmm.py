@@ -439,13 +439,19 @@ PAIR_MIN_ROWS = 2048
 # 2.377 ms, c128 4.71 -> 4.39); from L = 5 their larger spectra make them lose
 # (cfg3 9.35 -> 9.63, cfg2 L6 8.64 -> 11.7 ms) and the pair kernel (three
 # entries in flight, 56 registers) is best; triples never win
-# complex128 at L <= 4: the staged kernel (K7 v13; symbols staged once per 8 warp units in
-# shared memory) beats the quartets, cfg2 M2L 4.36 -> 3.79 ms; complex64 ties (2.44 vs 2.39,
-# profiles/r02/summary_v3.md) and keeps the quartets
+# Sparse-level kernel by storage type and order, measured (M2L stage alone, ms; profiles/r02/
+# summary_v3.md): staged (K7 v13, symbols staged once per 8 warp units in shared memory) against
+# the sibling groups --
+#   complex128: L=4 cfg2 3.79 vs 4.36 (quartets), L=5 cfg3 14.15 vs 14.55 (pairs), L=6 cfg2
+#               15.0 vs 19.3 (pairs) -> staged up to L = 6 (larger orders unmeasured: pairs);
+#   complex64:  L=4 cfg2 2.44 vs 2.39 (quartets), L=5 cfg3 8.59 vs 9.37 (pairs), L=6 cfg2 8.91
+#               vs 8.69, cfg4 91.9 vs 87.6 (pairs) -> quartets at L <= 4, staged at L = 5, pairs above
 def sibling_kind(dtype: str, order: int) -> str:
+    if dtype == "c128":
+        return "staged" if order <= 6 else "pair"
     if order <= 4:
-        return "staged" if dtype == "c128" else "quartet"
-    return "pair"
+        return "quartet"
+    return "staged" if order == 5 else "pair"
 
 
 def block_levels(plan, tt):

@@ -392,8 +392,8 @@ def test_m2l_level_policy(case):
                 lv = int(lv)
                 big = rpl.get(lv, 0) >= PAIR_MIN_ROWS
                 assert k[lv] == ("blocked" if lv in dense else sibling_kind(dt, order) if big else "rows")
-    assert sibling_kind("c64", 4) == "quartet" and sibling_kind("c128", 6) == "pair"
-    assert sibling_kind("c128", 4) == "staged" and sibling_kind("c64", 5) == "pair"
+    assert sibling_kind("c64", 4) == "quartet" and sibling_kind("c64", 6) == "pair" and sibling_kind("c128", 7) == "pair"
+    assert sibling_kind("c128", 4) == "staged" and sibling_kind("c128", 6) == "staged" and sibling_kind("c64", 5) == "staged"
     assert set(m2l_level_kinds("auto", "c64", levels, dense).values()) <= {"blocked", "rows"}
     assert set(m2l_level_kinds("hybrid_rows", "c64", levels, dense).values()) <= {"blocked", "rows"}
     lv0 = int(levels[0])

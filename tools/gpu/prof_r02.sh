@@ -19,6 +19,7 @@ for DT in ${METRIC_DTYPES-c64 c128}; do
   timeout 900 $NCU --metrics $M --clock-control none --csv --log-file $OUT/metrics_cfg2_$DT.csv $B > $OUT/ncu_$DT.log 2>&1
   echo "metrics $DT rc=$?" >> $OUT/rc.txt
 done
+[ -n "${SPECS_SKIP:-}" ] && exit 0
 for spec in "cfg2 c64 m2l_group" "cfg2 c128 m2l_stage" "cfg5 c128 m2l_blocked" "cfg5 c128 p2p_mut_kernel" "cfg2 c64 p2p_mut_f32"; do
   set -- $spec
   B="python bench.py --workload $1 --dtype $2 --steps 1 --warmup 0 --no-cpu-baseline --no-secondary --profile"
