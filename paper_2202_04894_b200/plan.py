@@ -136,6 +136,8 @@ class Plan:
     p2m_idx: np.ndarray = None  # slots computed by P2M
     m2m_levels: list = None  # [(level, slots, son_slot (k,8))] deepest first
     hat_slot: np.ndarray = None  # mult slot of each spectrum
+    m_used: np.ndarray = None  # per multipole slot: computed by P2M/M2M (an M2L reads it or a needed father does)
+    n_mult_used: int = 0
     # locals (target tree)
     l_cell: np.ndarray = None
     l_dir: np.ndarray = None
@@ -342,6 +344,21 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
     src_hat, hat_slot = nat.source_hats(m_dense, base_s, nd_s, st.level_offsets, key_base, m_cell.shape[0])
     nat.close()
     plan.hat_slot = hat_slot
+    # M-mark pruning: the reference creates an expansion for every mark (the union of target
+    # and source marks in single-tree mode, traversal.py:190-192, 229-236 -- that is what
+    # counts["effective_expansions"] reports); only the multipoles an M2L reads, and the
+    # sons the M2M of such a multipole reads (top-down closure), are ever used.  P2M and
+    # M2M run on those; the other slots keep their place (layout unchanged) and stay unread.
+    needed = np.zeros(m_cell.shape[0], bool)
+    needed[hat_slot] = True
+    for lev, slots, son_slot in reversed(m2m_levels):  # coarsest level first
+        ss = son_slot[needed[slots]]
+        needed[ss[ss >= 0]] = True
+    plan.m_used = needed
+    plan.n_mult_used = int(needed.sum())
+    plan.p2m_idx = plan.p2m_idx[needed[plan.p2m_idx]]
+    plan.m2m_levels = [(lev, slots[needed[slots]], son_slot[needed[slots]]) for lev, slots, son_slot in m2m_levels
+                       if needed[slots].any()]
 
     # ---- local slots on the target tree -------------------------------------
     rt64 = row_t.astype(np.int64)

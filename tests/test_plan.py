@@ -556,6 +556,26 @@ def test_p2p_mutual_lists_reproduce_the_near_field(case, max_pairs, chunk, monke
     assert np.linalg.norm(got - want) <= 1e-12 * np.linalg.norm(want)
 
 
+@pytest.mark.parametrize("case", ["cubesurf4000", "volume3000", "c1_kd16", "laplace500"])
+def test_m_mark_pruning_keeps_every_multipole_that_is_read(case):
+    """P2M/M2M run only on the multipoles an M2L reads and, top-down, on the
+    sons a needed father's M2M reads (plan.m_used); the reference's count of
+    expansions (the union of marks, traversal.py:190-192, 229-236) is unchanged."""
+    g = load_case(case)
+    tr, _, p = _plan(g)
+    used = p.m_used
+    assert p.counts["effective_expansions"] == g["counts"]["effective_expansions"] == p.n_mult
+    assert used[p.hat_slot].all() and p.n_mult_used == used.sum() <= p.n_mult
+    produced = np.zeros(p.n_mult, bool)
+    produced[p.p2m_idx] = True
+    for lev, slots, son in p.m2m_levels:  # deepest level first: sons are produced before their father
+        ok = son >= 0
+        assert produced[son[ok]].all() and used[son[ok]].all()
+        assert not produced[slots].any()
+        produced[slots] = True
+    assert np.array_equal(produced, used)  # every needed multipole is produced exactly once, nothing else
+
+
 def test_p2p_overlap_policy():
     """P2P beside the M2L (high-priority far field) only when every M2L level
     runs the quartet kernel (measured, profiles/r01_summary_v9.md)."""
