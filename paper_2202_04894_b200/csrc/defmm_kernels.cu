@@ -1750,11 +1750,11 @@ __device__ __forceinline__ void sincospi_p2p(double x, double& s, double& c) {
 #pragma unroll
     for (int k = 7; k >= 0; --k) pc = fma(pc, y2, c_cospi[k]);
     const double sy = ps * y;
-    double ss = (q & 1) ? pc : sy, cc = (q & 1) ? sy : pc;
-    if (q & 2) ss = -ss;
-    if ((q + 1) & 2) cc = -cc;
-    s = ss;
-    c = cc;
+    const double ss = (q & 1) ? pc : sy, cc = (q & 1) ? sy : pc;
+    // quadrant signs by XOR on the sign bit (a negation would be a DADD on the FP64 pipe,
+    // the bound of this kernel, plus two selects)
+    s = __hiloint2double(__double2hiint(ss) ^ ((q & 2) << 30), __double2loint(ss));
+    c = __hiloint2double(__double2hiint(cc) ^ (((q + 1) & 2) << 30), __double2loint(cc));
 }
 
 // 1/sqrt(x): hardware approximation + one third-order Newton step
