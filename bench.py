@@ -64,7 +64,7 @@ def _args():
                     help="N > 1 multipole exchange: halo (span all-reduce + all_to_all) or a full all-reduce")
     ap.add_argument("--m2l-levels", default="auto",
                     choices=["auto", "hybrid_rows", "blocked_all", "rows", "pairs", "pairs_all", "quartets",
-                             "quartets_all", "triples_all", "staged", "staged_all", "staged8", "staged8_all"])
+                             "quartets_all", "triples_all", "staged", "staged_all"])
     return ap.parse_args()
 
 

@@ -175,9 +175,7 @@ int defmm_l2_stream(const void* buf, int64_t n_vec, int32_t iters, int32_t ctas_
  *   K = 2, 8 for K = 4) = {source spectrum, derived symbol for row k or -1
  *   (k < K), 0 padding}; local[slot] = F2L(sum) -- the row kernel's sums,
  *   merged per source.
- *   K7 v13 staged variant (m2l_stage, K = 4 or 8 rows per warp unit; entries are int32 pairs
- *   for K = 4 and int32 quadruples {source, slot bytes of rows 0-3, of rows 4-7, 0} for K = 8;
- *   cta_rows holds K rows per warp unit): CTA c = 8 "warp units" (a target parent's <= K
+ *   K7 v13 staged variant (m2l_stage): CTA c = 8 "warp units" (a target parent's <= 4
  *   sibling rows each, same level and key, neighbouring parents) x one spectral slice of
  *   <= 32 16-B vectors (grid = ncta x slices of the order).  Its stages
  *   [cta_stage[c], cta_stage[c+1]) hold the derived symbols slot_sym[stage_slot_ptr[s] ..
@@ -247,7 +245,7 @@ int defmm_l2_stream(const void* buf, int64_t n_vec, int32_t iters, int32_t ctas_
     int defmm_m2l_group_##SUFFIX(int32_t L, int32_t K, int64_t ngroups, const int64_t* grp_slot,  \
                                  const int64_t* grp_ptr, const int32_t* entries, const void* hat, \
                                  const void* sym_derived, void* local, void* stream);             \
-    int defmm_m2l_stage_##SUFFIX(int32_t L, int32_t K, int64_t ncta, int32_t ns_cap, int32_t depth,  \
+    int defmm_m2l_stage_##SUFFIX(int32_t L, int64_t ncta, int32_t ns_cap, int32_t depth,             \
                                  const int32_t* cta_stage,                                          \
                                  const int32_t* cta_went, const int32_t* stage_slot_ptr,            \
                                  const int32_t* slot_sym, const int32_t* stage_wend,                \

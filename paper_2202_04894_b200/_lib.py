@@ -50,7 +50,7 @@ for _t in ("c128", "c64"):
         f"defmm_m2l_rows_{_t}": [_i32, _i64] + [_vp] * 7,
         f"defmm_m2l_blocked_{_t}": [_i32, _i64] + [_vp] * 10,
         f"defmm_m2l_group_{_t}": [_i32, _i32, _i64] + [_vp] * 7,
-        f"defmm_m2l_stage_{_t}": [_i32, _i32, _i64, _i32, _i32] + [_vp] * 11,
+        f"defmm_m2l_stage_{_t}": [_i32, _i64, _i32, _i32] + [_vp] * 11,
         f"defmm_f2l_rows_{_t}": [_i32, _i64, _vp, _vp, _vp, _vp],
         f"defmm_l2l_{_t}": [_i32, _i64, _vp, _vp, _vp, _vp, _vp, _f64, _vp, _f64, _vp, _vp],
         f"defmm_l2p_{_t}": [_i32, _i64] + [_vp] * 13 + [_f64, _vp, _vp, _vp, _vp, _vp],

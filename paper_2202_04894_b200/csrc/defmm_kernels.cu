@@ -1184,8 +1184,7 @@ __device__ __forceinline__ void ffma2(double&, double&, double, double, double) 
 #define DEFMM_STAGE_MINB 3
 #endif
 constexpr int STG_NW = 8;     // consumer warps (warp units) per CTA
-// rows per warp unit: K = 4 (sparse levels: a surface parent's children) or 8 (dense levels);
-// entry = {source, 4 slot bytes} (K = 4) or {source, 4 + 4 slot bytes, 0} (K = 8)
+constexpr int STG_K = 4;      // rows per warp unit
 constexpr int STG_MAXDEPTH = 8;  // ring stages (runtime depth <= this)
 constexpr int STG_PF = 4;     // source slices in flight per warp (the loop is unrolled 4-way)
 
@@ -1200,18 +1199,17 @@ struct StageCfg {
 
 // ring buffer b: slots [0, ns_cap) filled by the producer, slot ns_cap = zeros
 // (the entries name it for an absent row, so the loop has no branch per row)
-template <typename R, int L, int K>
-__global__ void __launch_bounds__(32 * (STG_NW + 1), K == 4 ? DEFMM_STAGE_MINB : 2)
+template <typename R, int L>
+__global__ void __launch_bounds__(32 * (STG_NW + 1), DEFMM_STAGE_MINB)
     m2l_stage_kernel(int ns_cap, int depth, const int* __restrict__ cta_stage, const int* __restrict__ cta_went,
                      const int* __restrict__ stage_slot_ptr, const int* __restrict__ slot_sym,
-                     const int* __restrict__ stage_wend, const int* __restrict__ ent,
+                     const int* __restrict__ stage_wend, const int2* __restrict__ ent,
                      const int* __restrict__ cta_rows, const cx<R>* __restrict__ hat,
                      const cx<R>* __restrict__ symd, cx<R>* __restrict__ lhat) {
     using C = StageCfg<R, L>;
     constexpr bool VEC = sizeof(R) == 4;
     using VT = std::conditional_t<VEC, float4, double2>;
-    constexpr int NV = C::NV, SW = C::SW, SB = C::SB, NW = STG_NW, PF = STG_PF;
-    constexpr int EW = K == 4 ? 2 : 4;  // ints per entry
+    constexpr int NV = C::NV, SW = C::SW, SB = C::SB, NW = STG_NW, K = STG_K, PF = STG_PF;
     extern __shared__ __align__(128) unsigned char smraw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
     uint64_t* empty = full + STG_MAXDEPTH;
@@ -1287,25 +1285,7 @@ __global__ void __launch_bounds__(32 * (STG_NW + 1), K == 4 ? DEFMM_STAGE_MINB :
     // prefetched j + PF are both in the current chunk; broadcast by shuffles
     constexpr int CH = 32 - PF;
     int cbase = i;
-    struct Ent {
-        int x, y, z;  // source, slot bytes of rows 0-3, of rows 4-7 (K = 8)
-    };
-    auto load_ent = [&](int e) {
-        Ent r;
-        if constexpr (K == 4) {
-            const int2 v = __ldg(reinterpret_cast<const int2*>(ent) + e);
-            r.x = v.x;
-            r.y = v.y;
-            r.z = 0;
-        } else {
-            const int4 v = __ldg(reinterpret_cast<const int4*>(ent) + e);
-            r.x = v.x;
-            r.y = v.y;
-            r.z = v.z;
-        }
-        return r;
-    };
-    Ent cur = load_ent(cbase + lane), nxt = load_ent(cbase + CH + lane);
+    int2 cur = __ldg(ent + cbase + lane), nxt = __ldg(ent + cbase + CH + lane);
     VT srcq[PF];
 #pragma unroll
     for (int u = 0; u < PF; ++u) {  // entries past e_total are other warps' (or padding): valid sources
@@ -1326,11 +1306,10 @@ __global__ void __launch_bounds__(32 * (STG_NW + 1), K == 4 ? DEFMM_STAGE_MINB :
     {                                                                                                \
         const int j = i - cbase;                                                                     \
         const uint32_t slots = (uint32_t)__shfl_sync(0xffffffffu, cur.y, j);                         \
-        const uint32_t slots2 = K == 8 ? (uint32_t)__shfl_sync(0xffffffffu, cur.z, j) : 0u;          \
         const int sidn = __shfl_sync(0xffffffffu, cur.x, j + PF);                                    \
         const VT s = srcq[U];                                                                        \
         _Pragma("unroll") for (int k = 0; k < K; ++k) {                                              \
-            const uint32_t addr = __byte_perm(k < 4 ? slots : slots2, 0u, 0x4440u + (k & 3)) * (uint32_t)SB + rb; \
+            const uint32_t addr = __byte_perm(slots, 0u, 0x4440u + k) * (uint32_t)SB + rb;           \
             if constexpr (VEC) {                                                                     \
                 float4 d;                                                                            \
                 asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"                              \
@@ -1356,7 +1335,7 @@ __global__ void __launch_bounds__(32 * (STG_NW + 1), K == 4 ? DEFMM_STAGE_MINB :
             if (i - cbase >= CH) {  // next chunk of entries (every 28th entry)
                 cur = nxt;
                 cbase += CH;
-                nxt = load_ent(cbase + CH + lane);
+                nxt = __ldg(ent + cbase + CH + lane);
             }
             const int lim = min(end, cbase + CH);
             // enter the 4-way unrolled sequence at the ring position of entry i
@@ -2924,29 +2903,24 @@ int launch_m2l_group(int32_t L, int32_t K, int64_t ngroups, const int64_t* grp_s
 }
 
 template <typename R>
-int launch_m2l_stage(int32_t L, int32_t K, int64_t ncta, int32_t ns_cap, int32_t depth, const int32_t* cta_stage,
+int launch_m2l_stage(int32_t L, int64_t ncta, int32_t ns_cap, int32_t depth, const int32_t* cta_stage,
                      const int32_t* cta_went, const int32_t* stage_slot_ptr, const int32_t* slot_sym,
                      const int32_t* stage_wend, const int32_t* entries, const int32_t* cta_rows, const void* hat,
                      const void* symd, void* lhat, void* stream) {
     if (ncta == 0) return 0;
-    if ((K != 4 && K != 8) || ns_cap < 8 || ns_cap > 254 || depth < 2 || depth > STG_MAXDEPTH) return -1;
+    if (ns_cap < 8 || ns_cap > 254 || depth < 2 || depth > STG_MAXDEPTH) return -1;
     cudaStream_t s = (cudaStream_t)stream;
-#define DEFMM_STAGE_LAUNCH(KK)                                                                                  \
-    {                                                                                                           \
-        int rc = set_smem(m2l_stage_kernel<R, LL, KK>, bytes);                                                  \
-        if (rc) return rc;                                                                                      \
-        m2l_stage_kernel<R, LL, KK><<<(unsigned)(ncta * C::NSLICE), 32 * (STG_NW + 1), bytes, s>>>(             \
-            ns_cap, depth, cta_stage, cta_went, stage_slot_ptr, slot_sym, stage_wend, entries, cta_rows,        \
-            (const cx<R>*)hat, (const cx<R>*)symd, (cx<R>*)lhat);                                               \
-    }
     DEFMM_DISPATCH_L(L, {
         using C = StageCfg<R, LL>;
         if (!grid_ok(ncta * C::NSLICE)) return -1;
         const size_t bytes = 128 + (size_t)depth * (ns_cap + 1) * C::SB;
         if (bytes > 227 * 1024) return -1;
-        if (K == 4) DEFMM_STAGE_LAUNCH(4) else DEFMM_STAGE_LAUNCH(8)
+        int rc = set_smem(m2l_stage_kernel<R, LL>, bytes);
+        if (rc) return rc;
+        m2l_stage_kernel<R, LL><<<(unsigned)(ncta * C::NSLICE), 32 * (STG_NW + 1), bytes, s>>>(
+            ns_cap, depth, cta_stage, cta_went, stage_slot_ptr, slot_sym, stage_wend, (const int2*)entries,
+            cta_rows, (const cx<R>*)hat, (const cx<R>*)symd, (cx<R>*)lhat);
     });
-#undef DEFMM_STAGE_LAUNCH
     return report(cudaGetLastError(), "m2l_stage");
 }
 
@@ -3135,12 +3109,12 @@ const char* defmm_last_error(void) { return g_last_error; }
                                  const void* sym_derived, void* local, void* stream) {                            \
         return launch_m2l_group<R>(L, K, ngroups, grp_slot, grp_ptr, entries, hat, sym_derived, local, stream);   \
     }                                                                                                               \
-    int defmm_m2l_stage_##SUFFIX(int32_t L, int32_t K, int64_t ncta, int32_t ns_cap, int32_t depth,                \
+    int defmm_m2l_stage_##SUFFIX(int32_t L, int64_t ncta, int32_t ns_cap, int32_t depth,                           \
                                  const int32_t* cta_stage, const int32_t* cta_went,                               \
                                  const int32_t* stage_slot_ptr, const int32_t* slot_sym,                          \
                                  const int32_t* stage_wend, const int32_t* entries, const int32_t* cta_rows,      \
                                  const void* hat, const void* sym_derived, void* lhat, void* stream) {            \
-        return launch_m2l_stage<R>(L, K, ncta, ns_cap, depth, cta_stage, cta_went, stage_slot_ptr, slot_sym,      \
+        return launch_m2l_stage<R>(L, ncta, ns_cap, depth, cta_stage, cta_went, stage_slot_ptr, slot_sym,         \
                                    stage_wend, entries, cta_rows, hat, sym_derived, lhat, stream);                \
     }                                                                                                               \
     int defmm_m2l_blocked_##SUFFIX(int32_t L, int64_t ngroups, const int64_t* grp_ptr, const int64_t* grp_rows,     \

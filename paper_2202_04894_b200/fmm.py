@@ -153,18 +153,18 @@ def m2l_pairs(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent) -> dict:
 # against 0.28 ms mutual + gather; cfg2, 3.8e8: 0.47 -> 0.43 ms; cfg5, 2.7e9, c128: 9.85 -> 7.2 ms)
 P2P_MUTUAL_MIN_PAIRS = 100_000_000
 
-STAGE_NW = 8  # warp units per CTA (STG_NW of the kernel); a unit holds K = 4 or 8 sibling rows
+STAGE_NW, STAGE_K = 8, 4  # warp units per CTA, rows per warp unit (STG_NW, STG_K of the kernel)
 STAGE_SLOTS = 48  # symbol slices per shared-memory stage (ns_cap)
 STAGE_DEPTH = 3  # shared-memory ring stages
 STAGE_ENT_PAD = 64  # readable entries past the end (STG_ENT_PAD)
 
 
-def _stage_units(ids, rows, l_cell, l_dir, level, parent, K: int = 4):
+def _stage_units(ids, rows, l_cell, l_dir, level, parent):
     """Row-level grouping of the staged M2L: rows sorted by (level, key, parent,
-    cell); warp units of <= K sibling rows (4 or 8); STAGE_NW consecutive units
-    of one (level, key) per CTA.  Returns (ids, slots, par, k of each row, unit
-    of each row, warp of each unit, CTA of each unit, CTA count, cta_rows)."""
-    NW = STAGE_NW
+    cell); warp units of <= STAGE_K sibling rows; STAGE_NW consecutive units of
+    one (level, key) per CTA.  Returns (ids, slots, par, k of each row, unit of
+    each row, warp of each unit, CTA of each unit, CTA count, cta_rows)."""
+    K, NW = STAGE_K, STAGE_NW
     i32 = np.int32
     slots = rows[ids]
     cell = l_cell[slots]
@@ -195,33 +195,25 @@ def _stage_units(ids, rows, l_cell, l_dir, level, parent, K: int = 4):
     return ids, slots, par, kk, wu, ww, cta_of_wu, ncta, cta_rows
 
 
-def _stage_entry_words(e_slot, kk_ev, ns_cap, K, xp):
-    """Per-event contribution to its entry's slot words: byte (k mod 4) of word k // 4,
-    relative to the all-absent pattern (every byte = ns_cap)."""
-    return (e_slot - int(ns_cap)) << (8 * (kk_ev % 4)), kk_ev // 4
-
-
 def m2l_stage_lists(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent, coords, hat_coords,
-                    ns_cap: int = STAGE_SLOTS, K: int = 4) -> dict:
+                    ns_cap: int = STAGE_SLOTS) -> dict:
     """Lists of the staged M2L (K7 v13, defmm_m2l_stage_*).  The rows ``ids``
     (indices into ``rows``) are grouped by (level, key, target parent) into warp
-    units of <= K sibling rows; STAGE_NW consecutive warp units of one
+    units of <= STAGE_K sibling rows; STAGE_NW consecutive warp units of one
     (level, key) form a CTA.  An event (row, source s) belongs to the class
     u = coords(s) - 2 coords(parent): within a CTA the symbols of a class are
     shared by every warp unit.  Classes are packed in order into stages of <=
     ns_cap distinct symbols; per (warp unit, class) one entry {source spectrum,
     4 bytes: stage slot of row k's symbol or 0xff}.  ``hat_coords``: (n_hat, 3)
-    grid coordinates of each spectrum's source cell.  ``K`` = 4 (entries {source,
-    4 slot bytes}) or 8 ({source, bytes of rows 0-3, bytes of rows 4-7, 0})."""
-    NW = STAGE_NW
-    EW = 2 if K == 4 else 4
+    grid coordinates of each spectrum's source cell."""
+    K, NW = STAGE_K, STAGE_NW
     i32 = np.int32
     if ids.size == 0:
-        return {"n": 0, "K": K, "ns_cap": ns_cap, "row_slot": np.zeros(0, np.int64), "cta_stage": np.zeros(1, i32),
+        return {"n": 0, "ns_cap": ns_cap, "row_slot": np.zeros(0, np.int64), "cta_stage": np.zeros(1, i32),
                 "cta_went": np.zeros(0, i32), "stage_slot_ptr": np.zeros(1, i32), "slot_sym": np.zeros(0, i32),
-                "stage_wend": np.zeros(0, i32), "ent": np.zeros((STAGE_ENT_PAD, EW), i32),
+                "stage_wend": np.zeros(0, i32), "ent": np.zeros((STAGE_ENT_PAD, 2), i32),
                 "cta_rows": np.zeros(0, i32)}
-    ids, slots, par, kk, wu, ww, cta_of_wu, ncta, cta_rows = _stage_units(ids, rows, l_cell, l_dir, level, parent, K)
+    ids, slots, par, kk, wu, ww, cta_of_wu, ncta, cta_rows = _stage_units(ids, rows, l_cell, l_dir, level, parent)
     n = ids.shape[0]
     # events
     cnt = row_ptr[ids + 1] - row_ptr[ids]
@@ -287,15 +279,12 @@ def m2l_stage_lists(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent, coord
     ent_stage = cls_stage[euniq % ncls]
     # slot bytes: ns_cap (the zero slot) where row k has no event in the class; each (entry, k)
     # holds at most one event, so the bytes add up exactly (values < 2^32)
-    ent32 = np.zeros((nent + STAGE_ENT_PAD, EW), i32)
+    ent32 = np.zeros((nent + STAGE_ENT_PAD, 2), i32)
     ent32[e_ent, 0] = e_src
     none = int(ns_cap) * 0x01010101  # every byte = ns_cap: the ring's zero slot
-    contrib, word = _stage_entry_words(e_slot, kk[rep], ns_cap, K, np)
-    for wd in range(K // 4):
-        m = word == wd
-        y = np.bincount(e_ent[m], weights=contrib[m].astype(np.float64), minlength=nent)
-        ent32[:nent, 1 + wd] = (y.astype(np.int64) + none).astype(np.uint32).view(i32)
-        ent32[nent:, 1 + wd] = np.uint32(none).view(i32)
+    y = np.bincount(e_ent, weights=((e_slot - int(ns_cap)) << (8 * kk[rep])).astype(np.float64), minlength=nent)
+    ent32[:nent, 1] = (y.astype(np.int64) + none).astype(np.uint32).view(i32)
+    ent32[nent:, 1] = np.uint32(none).view(i32)
     cta_went = np.searchsorted(ent_cw, np.arange(ncta * NW)).astype(i32)
     # end of warp w's entries of stage s: entries with (cw, stage) <= (cta(s) NW + w, s)
     st_cta = np.repeat(np.arange(ncta), nst_cta)
@@ -309,26 +298,26 @@ def m2l_stage_lists(ids, rows, row_ptr, ent, l_cell, l_dir, level, parent, coord
     wend_t = np.empty_like(stage_wend)
     wend_t[pos] = stage_wend
     stage_wend = wend_t
-    return {"n": ncta, "K": K, "ns_cap": ns_cap, "row_slot": slots.astype(np.int64),
-            "cta_stage": cta_stage.astype(i32), "cta_went": cta_went, "stage_slot_ptr": stage_slot_ptr.astype(i32),
-            "slot_sym": slot_sym, "stage_wend": stage_wend, "ent": ent32, "cta_rows": cta_rows.reshape(-1)}
+    return {"n": ncta, "ns_cap": ns_cap, "row_slot": slots.astype(np.int64), "cta_stage": cta_stage.astype(i32),
+            "cta_went": cta_went, "stage_slot_ptr": stage_slot_ptr.astype(i32), "slot_sym": slot_sym,
+            "stage_wend": stage_wend, "ent": ent32,
+            "cta_rows": cta_rows.reshape(-1)}
 
 
 def m2l_stage_lists_dev(ids, rows, row_ptr, ent_dev, l_cell, l_dir, level, parent, coords, hat_coords,
-                        ns_cap: int, device, K: int = 4) -> dict:
+                        ns_cap: int, device) -> dict:
     """m2l_stage_lists with the per-event work on the device (sorts, uniques,
     scatters on torch tensors; the greedy stage packer stays the native host
     routine over the (class, symbol) pairs).  Same lists bit for bit
     (tests/test_gpu_build.py); returns device tensors except row_slot."""
-    NW = STAGE_NW
-    EW = 2 if K == 4 else 4
+    K, NW = STAGE_K, STAGE_NW
     i32, i64 = torch.int32, torch.int64
     if ids.size == 0:
         h = m2l_stage_lists(ids, rows, row_ptr, np.zeros((0, 2), np.int32), l_cell, l_dir, level, parent, coords,
-                            hat_coords, ns_cap, K)
+                            hat_coords, ns_cap)
         return {k: (torch.as_tensor(v).to(device) if isinstance(v, np.ndarray) and k != "row_slot" else v)
                 for k, v in h.items()}
-    ids, slots, par, kk, wu, ww, cta_of_wu, ncta, cta_rows = _stage_units(ids, rows, l_cell, l_dir, level, parent, K)
+    ids, slots, par, kk, wu, ww, cta_of_wu, ncta, cta_rows = _stage_units(ids, rows, l_cell, l_dir, level, parent)
     n = ids.shape[0]
     cnt = row_ptr[ids + 1] - row_ptr[ids]
     with torch.cuda.device(device):
@@ -385,14 +374,11 @@ def m2l_stage_lists_dev(ids, rows, row_ptr, ent_dev, l_cell, l_dir, level, paren
         ent_cw = euniq // ncls
         ent_stage = cls_stage[euniq % ncls]
         none = int(ns_cap) * 0x01010101
-        ent32 = torch.zeros((nent + STAGE_ENT_PAD, EW), dtype=i32, device=device)
+        y = torch.full((nent + STAGE_ENT_PAD,), none, dtype=i64, device=device)
+        y.index_add_(0, e_ent, (e_slot - int(ns_cap)) << (8 * up(kk)[rep]))
+        ent32 = torch.zeros((nent + STAGE_ENT_PAD, 2), dtype=i32, device=device)
         ent32[e_ent, 0] = e_src.to(i32)
-        contrib, word = _stage_entry_words(e_slot, up(kk)[rep], ns_cap, K, torch)
-        for wd in range(K // 4):
-            y = torch.full((nent + STAGE_ENT_PAD,), none, dtype=i64, device=device)
-            m = word == wd
-            y.index_add_(0, e_ent[m], contrib[m])
-            ent32[:, 1 + wd] = torch.where(y >= (1 << 31), y - (1 << 32), y).to(i32)  # the uint32 bit pattern
+        ent32[:, 1] = torch.where(y >= (1 << 31), y - (1 << 32), y).to(i32)  # the uint32 bit pattern
         cta_went = torch.searchsorted(ent_cw.contiguous(), torch.arange(ncta * NW, device=device)).to(i32)
         st_cta = torch.repeat_interleave(torch.arange(ncta, device=device), nst_cta, output_size=nstage)
         q_cw = (st_cta[:, None] * NW + torch.arange(NW, device=device)[None, :]).reshape(-1)
@@ -404,7 +390,7 @@ def m2l_stage_lists_dev(ids, rows, row_ptr, ent_dev, l_cell, l_dir, level, paren
         pos = cta_stage[qc] * NW + q_w * nst_cta[qc] + (q_st - cta_stage[qc])
         stage_wend = torch.empty_like(wend)
         stage_wend[pos] = wend
-        return {"n": ncta, "K": K, "ns_cap": ns_cap, "row_slot": slots.astype(np.int64), "cta_stage": cta_stage.to(i32),
+        return {"n": ncta, "ns_cap": ns_cap, "row_slot": slots.astype(np.int64), "cta_stage": cta_stage.to(i32),
                 "cta_went": cta_went, "stage_slot_ptr": stage_slot_ptr.to(i32), "slot_sym": (suniq % n_tr).to(i32),
                 "stage_wend": stage_wend, "ent": ent32,
                 "cta_rows": torch.as_tensor(cta_rows.reshape(-1)).to(device)}
@@ -440,9 +426,8 @@ M2L_MODE_KINDS = {
     "pairs": ("blocked", "pair"), "pairs_all": ("pair", "pair"), "quartets": ("blocked", "quartet"),
     "quartets_all": ("quartet", "quartet"), "triples_all": ("triple", "triple"),
     "staged": ("blocked", "staged"), "staged_all": ("staged", "staged"),
-    "staged8": ("staged8", "staged"), "staged8_all": ("staged8", "staged8"),
 }
-M2L_KERNELS = ("rows", "blocked", "pair", "triple", "quartet", "staged", "staged8")
+M2L_KERNELS = ("rows", "blocked", "pair", "triple", "quartet", "staged")
 # events per parent-pair block above which a level counts as dense (blocked kernel)
 BLOCKED_MIN_EVENTS_PER_BLOCK = 32.0
 # "auto": other sparse levels with at least this many rows run the pair kernel
@@ -681,13 +666,13 @@ class FmmPlan:
                 self.sib_groups.append((gr["K"], int(gr["n"]), gr["grp_slot"], gr["grp_ptr"],
                                         gr["ent"].reshape(-1).contiguous()))
         self.n_pairs = sum(x[1] for x in self.sib_groups)
-        self.staged = []  # (K, n CTAs, ns_cap, lists...) of the staged kernel, K = 4 / 8 rows per warp unit
+        sg = h["staged"]
+        self.staged = None
         self.stage_depth = int(os.environ.get("DEFMM_STAGE_DEPTH", STAGE_DEPTH))
-        for sg in h["staged"]:
-            if sg["n"]:
-                self.staged.append((int(sg["K"]), int(sg["n"]), int(sg["ns_cap"])) + tuple(
-                    sg[k].reshape(-1).contiguous() for k in ("cta_stage", "cta_went", "stage_slot_ptr", "slot_sym",
-                                                             "stage_wend", "ent", "cta_rows")))
+        if sg["n"]:
+            self.staged = (int(sg["n"]), int(sg["ns_cap"])) + tuple(
+                sg[k].reshape(-1).contiguous() for k in ("cta_stage", "cta_went", "stage_slot_ptr", "slot_sym",
+                                                         "stage_wend", "ent", "cta_rows"))
         # downward
         self.l2l = []
         for lev, outs, octant, ptr, src, sdir in h["l2l"]:
@@ -822,23 +807,17 @@ class FmmPlan:
                                      tt.level, tt.parent, K, self.device)
         # staged M2L (K7 v13): warp units of sibling rows sharing staged symbols
         hat_coords = self.st.coords[p.m_cell[h["hat_slot"]]] if h["hat_slot"].size else np.zeros((0, 3), np.int64)
-        if ent_dev is None and any(pick("staged", "staged8")):
+        if ent_dev is None and any(pick("staged")):
             ent_dev = _dev(h["ent"], torch.int32, self.device)
-        # lhat rows = the blocked rows, then the staged rows (K = 4 units, then K = 8 units)
+        h["staged"] = m2l_stage_lists_dev(np.nonzero(pick("staged"))[0], rows, h["row_ptr"], ent_dev, p.l_cell,
+                                          p.l_dir, tt.level, tt.parent, tt.coords, hat_coords,
+                                          int(os.environ.get("DEFMM_STAGE_SLOTS", STAGE_SLOTS)), self.device)
+        # lhat rows = the blocked rows, then the staged rows
         is_grp = pick("blocked")
         grp_rows = rows[is_grp]
-        lhat_rows = [grp_rows]
-        h["staged"] = []
-        for kind, K in (("staged", 4), ("staged8", 8)):
-            sg = m2l_stage_lists_dev(np.nonzero(pick(kind))[0], rows, h["row_ptr"], ent_dev, p.l_cell, p.l_dir,
-                                     tt.level, tt.parent, tt.coords, hat_coords,
-                                     int(os.environ.get("DEFMM_STAGE_SLOTS", STAGE_SLOTS)), self.device, K)
-            base = int(sum(x.shape[0] for x in lhat_rows))
-            cr = sg["cta_rows"]
-            sg["cta_rows"] = torch.where(cr >= 0, cr + base, cr).to(torch.int32)
-            lhat_rows.append(sg["row_slot"])
-            h["staged"].append(sg)
-        h["bk_rows"] = np.concatenate(lhat_rows)
+        h["bk_rows"] = np.concatenate([grp_rows, h["staged"]["row_slot"]])
+        cr = h["staged"]["cta_rows"]  # lhat rows of the staged kernel follow the blocked rows
+        h["staged"]["cta_rows"] = torch.where(cr >= 0, cr + int(grp_rows.shape[0]), cr).to(torch.int32)
         # groups of blocked levels, rows renumbered into lhat
         gr = h["grp_rows"]
         gr_slots = np.where(gr >= 0, rows[np.maximum(gr, 0)] if rows.size else -1, -1)
@@ -1130,9 +1109,9 @@ class FmmPlan:
                           sh)
             _lib.call(self._op("m2l_blocked"), L, self.n_groups, self.grp_ptr, self.grp_rows, self.blk_src,
                       self.blk_trans, self.blk_mask, self.blk_kind, self.hat, self.sym_derived, self.lhat, sh)
-            for K, ncta, ns_cap, *lists in self.staged:
-                _lib.call(self._op("m2l_stage"), L, K, ncta, ns_cap, self.stage_depth, *lists, self.hat,
-                          self.sym_derived, self.lhat, sh)
+            if self.staged is not None:
+                _lib.call(self._op("m2l_stage"), L, self.staged[0], self.staged[1], self.stage_depth,
+                          *self.staged[2:], self.hat, self.sym_derived, self.lhat, sh)
             _lib.call(self._op("f2l_rows"), L, self.bk_rows.shape[0], self.bk_rows, self.lhat, self.local, sh)
         elif self.m2l_variant == "derived":
             _lib.call(self._op("m2l_rows"), L, self.row_slot.shape[0], self.row_slot, self.row_ptr,
@@ -1227,8 +1206,7 @@ class FmmPlan:
                            (sum(x[1] for x in self.sib_groups if x[0] == 3), f"{gk}<3>", "triple"),
                            (sum(x[1] for x in self.sib_groups if x[0] == 4), f"{gk}<4>", "quartet"),
                            (self.n_groups, "m2l_blocked_kernel", "blocked"),
-                           (sum(x[1] for x in self.staged if x[0] == 4), "m2l_stage_kernel<4>", "staged"),
-                           (sum(x[1] for x in self.staged if x[0] == 8), "m2l_stage_kernel<8>", "staged8"),
+                           (self.staged[0] if self.staged else 0, "m2l_stage_kernel", "staged"),
                            (self.bk_rows.shape[0], "f2l_rows_kernel", None)):
             if n:
                 out.append(f"{name}<{R}, {self.L}>" + (f" (levels {lv(k)})" if k is not None else ""))
@@ -1240,7 +1218,7 @@ class FmmPlan:
         the M2L kernels with work, l2l per level, l2p."""
         if self.m2l_variant == "hybrid":
             m2l = len(self.sib_groups) + sum(int(n > 0) for n in (self.rk_rows.shape[0], self.n_groups,
-                                                                   self.bk_rows.shape[0])) + len(self.staged)
+                                                                   self.bk_rows.shape[0])) + int(bool(self.staged))
         else:
             m2l = 1
         p2p_extra = len(self.p2p_mut["gather"]) if self.p2p_mut is not None else int(bool(self.n_split))

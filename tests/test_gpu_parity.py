@@ -167,7 +167,7 @@ def test_m2l_canonical_gather_and_derived_symbols_agree(case):
     c = plan.apply().cpu().numpy()
     assert _rel(c, a) <= 1e-13
     for mode in ("blocked_all", "rows", "hybrid_rows", "pairs_all", "triples_all", "quartets_all", "staged_all",
-                 "staged", "staged8_all", "staged8"):
+                 "staged"):
         p2 = FmmPlan(g["points"], None, FmmConfig(**g["config"]), charges=g["charges"], reuse=plan, m2l=mode)
         assert _rel(p2.apply().cpu().numpy(), a) <= 1e-13, mode
     # every kernel on some level at once (per-level overrides)
@@ -189,7 +189,7 @@ def test_group_m2l_kernels_match_reference(case, dtype):
     g = load_case(case)
     cfg = FmmConfig(**{**g["config"], "dtype": dtype})
     base = FmmPlan(g["points"], None, cfg, charges=g["charges"])
-    for mode in ("pairs_all", "triples_all", "quartets_all", "staged_all", "staged8_all"):
+    for mode in ("pairs_all", "triples_all", "quartets_all", "staged_all"):
         p2 = FmmPlan(g["points"], None, cfg, charges=g["charges"], reuse=base, m2l=mode)
         a = p2.apply().cpu().numpy().astype(np.complex128)
         assert _rel(a, g["pot"]) <= (FP64_TOL if dtype == "c128" else C64_TOL)
