@@ -825,8 +825,13 @@ class FmmPlan:
         gkeep = np.any(gid >= 0, axis=1)
         _, gptr, bsel = _sub_csr(h["grp_ptr"], gkeep)
         h["grp_ptr"], h["grp_rows"] = gptr, gid[gkeep]
-        h["blk_src"], h["blk_trans"], h["blk_mask"], h["blk_kind"] = (
-            h["blk_src"][bsel], h["blk_trans"][bsel], h["blk_mask"][bsel], h["blk_kind"][bsel])
+        if "blk_src_ev" in h:  # unsharded: spectrum of the selected blocks' events only
+            bs = h.pop("blk_src_ev")[bsel]
+            hat = h["ent"][:, 0]
+            h["blk_src"] = np.where(bs >= 0, hat[np.maximum(bs, 0)] if hat.size else 0, -1).astype(np.int32)
+        else:
+            h["blk_src"] = h["blk_src"][bsel]
+        h["blk_trans"], h["blk_mask"], h["blk_kind"] = h["blk_trans"][bsel], h["blk_mask"][bsel], h["blk_kind"][bsel]
         self.dense_levels = sorted(lv for lv, k in kinds.items() if k == "blocked")
         return h
 
@@ -848,7 +853,7 @@ class FmmPlan:
             "p2p_sel": np.arange(p.p2p_lo.shape[0]),
         }
         # blocked M2L: group rows as indices into h["rows"] (lhat rows)
-        blk = {"grp_ptr": p.blk_group_ptr, "grp_rows": p.blk_group_rows, "blk_src": p.blk_src,
+        blk = {"grp_ptr": p.blk_group_ptr, "grp_rows": p.blk_group_rows, "blk_src_ev": p.blk_src_ev,
                "blk_trans": p.blk_trans, "blk_mask": p.blk_mask, "blk_kind": p.blk_kind}
         if sh is None:
             h.update(blk)

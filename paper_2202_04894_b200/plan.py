@@ -61,15 +61,28 @@ def _group48() -> np.ndarray:
 GROUP48 = _group48()
 
 
+_PERMS = list(itertools.permutations(range(3)))  # GROUP48[8 p + s]: permutation p, sign pattern s
+
+
 def canonicalize_many(t: np.ndarray):
-    """(canonical (m,3), rotation id (m,)) -- fourier.py:104-120 batched."""
+    """(canonical (m,3), rotation id (m,)) -- fourier.py:104-120 batched: the
+    canonical translation is |t| sorted descending and the rotation id the FIRST
+    group element g (fourier.py:90-101's order: permutations x sign patterns,
+    (g c)[a] = signs[a] c[perm[a]]) with g canon = t.  Closed form of that
+    first hit: the first permutation matching |t| (ties between equal entries),
+    signs[a] = -1 iff t[a] < 0 (a zero entry matches +1 first)."""
     t = np.asarray(t, np.int64)
     if np.any(np.all(t == 0, axis=1)):
         raise ValueError("zero translation cannot be canonicalized")
-    canon = -np.sort(-np.abs(t), axis=1)
-    img = np.einsum("gab,mb->mga", GROUP48, canon)
-    hit = np.all(img == t[:, None, :], axis=2)
-    return canon, np.argmax(hit, axis=1).astype(np.int8)
+    at = np.abs(t)
+    canon = -np.sort(-at, axis=1)
+    pid = np.full(t.shape[0], -1, np.int64)
+    for p in range(5, -1, -1):  # the smallest matching permutation index wins
+        perm = _PERMS[p]
+        hit = (canon[:, perm[0]] == at[:, 0]) & (canon[:, perm[1]] == at[:, 1]) & (canon[:, perm[2]] == at[:, 2])
+        pid[hit] = p
+    sid = ((t[:, 0] < 0).astype(np.int64) << 2) | ((t[:, 1] < 0).astype(np.int64) << 1) | (t[:, 2] < 0)
+    return canon, (pid * 8 + sid).astype(np.int8)
 
 
 def hf_max_level(tree: ClusterTree, depth: int, kappa: float, hf_switch: float) -> int:
@@ -159,13 +172,23 @@ class Plan:
     # parent-pair blocks of the blocked M2L (K7 v3)
     blk_group_rows: np.ndarray = None  # (ngroups, 8) local slots of the group's rows, -1 absent
     blk_group_ptr: np.ndarray = None  # block range per group
-    blk_src: np.ndarray = None  # (nblocks, 8) spectrum index per source child, -1 absent
+    blk_src_ev: np.ndarray = None  # (nblocks, 8) an event of each source child (its spectrum: entries[ev, 0]), -1 absent
     blk_trans: np.ndarray = None  # (nblocks, 27) derived symbol per child offset, -1 unused
     blk_mask: np.ndarray = None  # (nblocks,) int64: bit 8a+b = (a, b) is an M2L event
     blk_kind: np.ndarray = None  # (nblocks,) int8: -1 general, 2p+v planar
     # event logs (optional, for the events= API)
     m2l_events: tuple = None
     p2p_events: tuple = None
+
+    @property
+    def blk_src(self):
+        """(nblocks, 8) spectrum index per source child, -1 absent (mapped on
+        first use: only plans with blocked levels need it)."""
+        if getattr(self, "_blk_src", None) is None:
+            bs = self.blk_src_ev
+            hat = self.m2l_rows_entries[:, 0]
+            self._blk_src = np.where(bs >= 0, hat[np.maximum(bs, 0)] if hat.size else 0, -1).astype(np.int32)
+        return self._blk_src
 
     @property
     def n_mult(self):
@@ -389,8 +412,7 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
     gr = nat["grp_rows"]
     plan.blk_group_rows = np.where(gr >= 0, tslot[np.maximum(gr, 0)], -1) if n_rows else gr
     plan.blk_group_ptr = nat["grp_ptr"]
-    bs = nat["blk_src"]
-    plan.blk_src = np.where(bs >= 0, src_hat[np.maximum(bs, 0)] if n_m2l else 0, -1).astype(np.int32)
+    plan.blk_src_ev = nat["blk_src"]
     bt = nat["blk_trans"]
     plan.blk_trans = bt
     plan.blk_mask = nat["blk_mask"]
