@@ -39,6 +39,8 @@ def _on_device(fn):
 
 
 def _dev(a, dtype, device):
+    if torch.is_tensor(a):  # a list built on the device already
+        return a.to(device=device, dtype=dtype).contiguous()
     return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype).to(device)
 
 
@@ -704,7 +706,7 @@ class FmmPlan:
         if self.same and self.shard is None and (mut == "1" or (mut == "auto" and
                                                                 p.counts["p2p_pairs"] >= P2P_MUTUAL_MIN_PAIRS)):
             ml = p2p_mutual_lists(p.p2p_ptr, p.p2p_lo, p.p2p_hi, tt.start[p.leaf_cells], tt.stop[p.leaf_cells],
-                                  p.counts["p2p_pairs"])
+                                  p.counts["p2p_pairs"], device=d)  # segment lists and gather passes on the device
             if ml is not None:
                 self.p2p_mut = {k: _dev(ml[k], i32 if k == "item_leaf" else i64, d)
                                 for k in ("item_leaf", "item_f0", "item_f1", "item_row", "item_col", "ptr", "lo",

@@ -747,7 +747,86 @@ P2P_MUTUAL_MAX_LEAF = 256  # particles per leaf the mutual kernel handles (2 per
 P2P_GATHER_CHUNK = 128  # contributor segments one gather task sums
 
 
-def p2p_mutual_lists(ptr, lo, hi, tlo, thi, n_pairs=None, max_pairs: int = P2P_ITEM_PAIRS):
+class _NumpyOps:
+    """The array operations p2p_mutual_lists needs, on numpy (host) ..."""
+
+    @staticmethod
+    def arr(a):
+        return np.asarray(a, np.int64)
+
+    arange = staticmethod(lambda n: np.arange(n, dtype=np.int64))
+    zeros = staticmethod(lambda n: np.zeros(n, np.int64))
+    full = staticmethod(lambda n, v: np.full(n, v, np.int64))
+    cat = staticmethod(lambda xs: np.concatenate(xs))
+    repeat = staticmethod(lambda a, c: np.repeat(a, c))
+    cumsum = staticmethod(lambda a: np.cumsum(a))
+    maximum = staticmethod(np.maximum)
+    minimum = staticmethod(np.minimum)
+    where = staticmethod(np.where)
+    searchsorted = staticmethod(lambda a, v, right=False: np.searchsorted(a, v, side="right" if right else "left"))
+    argsort_stable = staticmethod(lambda a: np.argsort(a, kind="stable"))
+    to_host = staticmethod(lambda a: np.asarray(a))
+
+    @staticmethod
+    def unique_inverse(a):
+        u, inv = np.unique(a, return_inverse=True)
+        return u, inv.reshape(-1)
+
+
+class _TorchOps:
+    """... and on torch device tensors (the same index arithmetic on the GPU)."""
+
+    def __init__(self, device):
+        import torch
+
+        self.t, self.dev = torch, device
+
+    def arr(self, a):
+        return self.t.as_tensor(np.ascontiguousarray(a, np.int64)).to(self.dev) if not self.t.is_tensor(a) else a
+
+    def arange(self, n):
+        return self.t.arange(int(n), dtype=self.t.int64, device=self.dev)
+
+    def zeros(self, n):
+        return self.t.zeros(int(n), dtype=self.t.int64, device=self.dev)
+
+    def full(self, n, v):
+        return self.t.full((int(n),), int(v), dtype=self.t.int64, device=self.dev)
+
+    def cat(self, xs):
+        return self.t.cat([self.arr(x) for x in xs])
+
+    def repeat(self, a, c):
+        return self.t.repeat_interleave(a, c)
+
+    def cumsum(self, a):
+        return self.t.cumsum(a, 0)
+
+    def maximum(self, a, b):
+        return self.t.maximum(a, b if self.t.is_tensor(b) else self.t.as_tensor(b, device=self.dev))
+
+    def minimum(self, a, b):
+        return self.t.minimum(a, b if self.t.is_tensor(b) else self.t.as_tensor(b, device=self.dev))
+
+    def where(self, c, a, b):
+        a = a if self.t.is_tensor(a) else self.t.as_tensor(a, dtype=self.t.int64, device=self.dev)
+        b = b if self.t.is_tensor(b) else self.t.as_tensor(b, dtype=self.t.int64, device=self.dev)
+        return self.t.where(c, a, b)
+
+    def searchsorted(self, a, v, right=False):
+        return self.t.searchsorted(a.contiguous(), v.contiguous(), right=right)
+
+    def argsort_stable(self, a):
+        return self.t.sort(a, stable=True)[1]
+
+    def to_host(self, a):
+        return a.cpu().numpy() if self.t.is_tensor(a) else np.asarray(a)
+
+    def unique_inverse(self, a):
+        return self.t.unique(a, return_inverse=True)
+
+
+def p2p_mutual_lists(ptr, lo, hi, tlo, thi, n_pairs=None, max_pairs: int = P2P_ITEM_PAIRS, device=None):
     """Lists of the mutual P2P (K1 v2, defmm_p2p_mutual_* / defmm_p2p_gather_*)
     for a single-tree plan.  Target leaf l (Morton order, particles
     [tlo[l], thi[l])) has the merged source runs [lo[e], hi[e]), e in
@@ -760,7 +839,11 @@ def p2p_mutual_lists(ptr, lo, hi, tlo, thi, n_pairs=None, max_pairs: int = P2P_I
     contributor segments (cbase, xlo, xhi) in fixed order, out[x] = sum_c
     partial[cbase[c] + x]; the last pass writes near for every leaf, earlier
     passes pre-sum the longest lists in chunks.  None if the relation is not
-    symmetric (n_pairs check) or a leaf is too large."""
+    symmetric (n_pairs check) or a leaf is too large.
+
+    ``device``: None = numpy arrays; a torch device = the segment expansion,
+    sorts and gather passes run there and the gather lists are returned as
+    device tensors (same values, tests/test_gpu_build.py)."""
     ptr = np.asarray(ptr, np.int64)
     lo, hi = np.asarray(lo, np.int64), np.asarray(hi, np.int64)
     tlo, thi = np.asarray(tlo, np.int64), np.asarray(thi, np.int64)
@@ -788,68 +871,78 @@ def p2p_mutual_lists(ptr, lo, hi, tlo, thi, n_pairs=None, max_pairs: int = P2P_I
     size = nt[il] + (f1 - f0)
     off = np.concatenate([[0], np.cumsum(size)])
     row, col = off[:-1], off[:-1] + nt[il]
+    # ---- from here on host (numpy) or device (torch): X holds the array operations ----
+    X = _NumpyOps if device is None else _TorchOps(device)
+    cs_, c_lo_, tlo_, thi_, nt_, il_, f0_, col_ = (X.arr(v) for v in (cs, c_lo, tlo, thi, nt, il, f0, col))
     # column segments: the item's flattened range past the leaf's own particles,
     # cut at run boundaries, then at leaf boundaries
-    F0 = cs[c_ptr[il]] + np.maximum(f0, nt[il])
-    F1 = cs[c_ptr[il]] + f1
+    base_i = X.arr(cs[c_ptr[il]])
+    F0 = base_i + X.maximum(f0_, nt_[il_])
+    F1 = base_i + X.arr(f1)
     has = F1 > F0
-    r0 = np.searchsorted(cs, F0, side="right") - 1
-    r1 = np.searchsorted(cs, np.maximum(F1 - 1, F0), side="right") - 1
-    cnt = np.where(has, r1 - r0 + 1, 0)
-    it = np.repeat(np.arange(ni), cnt)
-    r = np.repeat(r0, cnt) + (np.arange(int(cnt.sum())) - np.repeat(np.cumsum(cnt) - cnt, cnt))
-    sF0 = np.maximum(F0[it], cs[r])
-    sF1 = np.minimum(F1[it], cs[r + 1])
-    g0 = c_lo[r] + (sF0 - cs[r])
+    r0 = X.searchsorted(cs_, F0, right=True) - 1
+    r1 = X.searchsorted(cs_, X.maximum(F1 - 1, F0), right=True) - 1
+    cnt = X.where(has, r1 - r0 + 1, 0)
+    it = X.repeat(X.arange(ni), cnt)
+    r = X.repeat(r0, cnt) + (X.arange(int(cnt.sum())) - X.repeat(X.cumsum(cnt) - cnt, cnt))
+    sF0 = X.maximum(F0[it], cs_[r])
+    sF1 = X.minimum(F1[it], cs_[r + 1])
+    g0 = c_lo_[r] + (sF0 - cs_[r])
     g1 = g0 + (sF1 - sF0)
-    b0 = np.searchsorted(tlo, g0, side="right") - 1
-    b1 = np.searchsorted(tlo, g1 - 1, side="right") - 1
+    b0 = X.searchsorted(tlo_, g0, right=True) - 1
+    b1 = X.searchsorted(tlo_, g1 - 1, right=True) - 1
     bc = b1 - b0 + 1
-    sg = np.repeat(np.arange(it.shape[0]), bc)
-    B = np.repeat(b0, bc) + (np.arange(int(bc.sum())) - np.repeat(np.cumsum(bc) - bc, bc))
-    xlo = np.maximum(g0[sg], tlo[B]) - tlo[B]
-    xhi = np.minimum(g1[sg], thi[B]) - tlo[B]
+    sg = X.repeat(X.arange(it.shape[0]), bc)
+    B = X.repeat(b0, bc) + (X.arange(int(bc.sum())) - X.repeat(X.cumsum(bc) - bc, bc))
+    xlo = X.maximum(g0[sg], tlo_[B]) - tlo_[B]
+    xhi = X.minimum(g1[sg], thi_[B]) - tlo_[B]
     # partial index of particle tlo[B] + x: col + (F - (cs[c_ptr] + f0)), F = sF0 + (g - g0)
     ii = it[sg]
-    cb = col[ii] + (sF0[sg] - (cs[c_ptr[il[ii]]] + f0[ii])) + (tlo[B] - g0[sg])
+    cb = col_[ii] + (sF0[sg] - (base_i[ii] + f0_[ii])) + (tlo_[B] - g0[sg])
     # contributors per leaf: its own items' rows (item order), then the column segments
-    leaf_all = np.concatenate([il, B])
-    base_all = np.concatenate([row, cb])
-    xlo_all = np.concatenate([np.zeros(ni, np.int64), xlo])
-    xhi_all = np.concatenate([nt[il], xhi])
-    o = np.argsort(leaf_all, kind="stable")
+    leaf_all = X.cat([il_, B])
+    base_all = X.cat([X.arr(row), cb])
+    xlo_all = X.cat([X.zeros(ni), xlo])
+    xhi_all = X.cat([nt_[il_], xhi])
+    o = X.argsort_stable(leaf_all)
     c_leaf_s, c_base, c_xlo, c_xhi = leaf_all[o], base_all[o], xlo_all[o], xhi_all[o]
     # gather passes: a leaf listed by very many items (particles of a large cell next
     # to many small target leaves: cfg3) is summed in chunks of <= P2P_GATHER_CHUNK
     # segments into extra partial rows first, so that no gather task is long
     total = int(off[-1])
     passes = []
+    leaves = X.arange(nl + 1)
     while True:
-        cptr = np.searchsorted(c_leaf_s, np.arange(nl + 1)).astype(np.int64)
-        cnt_l = np.diff(cptr)
-        heavy = cnt_l > P2P_GATHER_CHUNK
-        if not heavy.any():
+        cptr = X.searchsorted(c_leaf_s, leaves)
+        cnt_l = cptr[1:] - cptr[:-1]
+        cmax = int(cnt_l.max())
+        if cmax <= P2P_GATHER_CHUNK:
             break
+        heavy = cnt_l > P2P_GATHER_CHUNK
         hv = heavy[c_leaf_s]
-        j = np.arange(c_leaf_s.shape[0]) - cptr[c_leaf_s]
-        key = c_leaf_s[hv] * (int(cnt_l.max()) // P2P_GATHER_CHUNK + 2) + j[hv] // P2P_GATHER_CHUNK
-        tk, tinv = np.unique(key, return_inverse=True)  # tasks = (leaf, chunk), in (leaf, chunk) order
-        t_leaf = tk // (int(cnt_l.max()) // P2P_GATHER_CHUNK + 2)
-        t_out = total + np.concatenate([[0], np.cumsum(nt[t_leaf])[:-1]])
-        total += int(nt[t_leaf].sum())
-        t_ptr = np.searchsorted(tinv.reshape(-1), np.arange(tk.shape[0] + 1)).astype(np.int64)
-        passes.append({"task_leaf": t_leaf.astype(np.int32), "task_out": t_out.astype(np.int64), "cptr": t_ptr,
-                       "cbase": c_base[hv].astype(np.int64), "cxlo": c_xlo[hv].astype(np.int32),
-                       "cxhi": c_xhi[hv].astype(np.int32)})
+        j = X.arange(c_leaf_s.shape[0]) - cptr[c_leaf_s]
+        nchunk = cmax // P2P_GATHER_CHUNK + 2
+        key = c_leaf_s[hv] * nchunk + j[hv] // P2P_GATHER_CHUNK
+        tk, tinv = X.unique_inverse(key)  # tasks = (leaf, chunk), in (leaf, chunk) order
+        t_leaf = tk // nchunk
+        t_nt = nt_[t_leaf]
+        t_out = total + X.cumsum(t_nt) - t_nt
+        total += int(t_nt.sum())
+        t_ptr = X.searchsorted(tinv, X.arange(tk.shape[0] + 1))
+        passes.append({"task_leaf": t_leaf, "task_out": t_out, "cptr": t_ptr, "cbase": c_base[hv], "cxlo": c_xlo[hv],
+                       "cxhi": c_xhi[hv]})
         # the heavy leaves now read their chunk sums (full range) instead
-        leaf2 = np.concatenate([c_leaf_s[~hv], t_leaf])
-        base2 = np.concatenate([c_base[~hv], t_out])
-        xlo2 = np.concatenate([c_xlo[~hv], np.zeros(t_leaf.shape[0], np.int64)])
-        xhi2 = np.concatenate([c_xhi[~hv], nt[t_leaf]])
-        o2 = np.argsort(leaf2, kind="stable")
+        leaf2 = X.cat([c_leaf_s[~hv], t_leaf])
+        base2 = X.cat([c_base[~hv], t_out])
+        xlo2 = X.cat([c_xlo[~hv], X.zeros(t_leaf.shape[0])])
+        xhi2 = X.cat([c_xhi[~hv], t_nt])
+        o2 = X.argsort_stable(leaf2)
         c_leaf_s, c_base, c_xlo, c_xhi = leaf2[o2], base2[o2], xlo2[o2], xhi2[o2]
-    passes.append({"task_leaf": np.arange(nl, dtype=np.int32), "task_out": np.full(nl, -1, np.int64), "cptr": cptr,
-                   "cbase": c_base.astype(np.int64), "cxlo": c_xlo.astype(np.int32), "cxhi": c_xhi.astype(np.int32)})
+    passes.append({"task_leaf": X.arange(nl), "task_out": X.full(nl, -1), "cptr": cptr, "cbase": c_base,
+                   "cxlo": c_xlo, "cxhi": c_xhi})
+    if device is None:  # the documented dtypes of the host lists
+        passes = [{k: v.astype(np.int32 if k in ("task_leaf", "cxlo", "cxhi") else np.int64) for k, v in g.items()}
+                  for g in passes]
     return {
         "ptr": c_ptr, "lo": c_lo, "hi": c_hi,
         "item_leaf": il.astype(np.int32), "item_f0": f0.astype(np.int64), "item_f1": f1.astype(np.int64),

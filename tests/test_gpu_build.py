@@ -157,3 +157,26 @@ def test_device_stage_lists_equal_host_lists(case, ns_cap):
     for k in ("row_slot", "cta_stage", "cta_went", "stage_slot_ptr", "slot_sym", "stage_wend", "ent", "cta_rows"):
         bv = b[k].cpu().numpy() if torch.is_tensor(b[k]) else b[k]
         assert np.array_equal(np.asarray(a[k]).reshape(-1), np.asarray(bv).reshape(-1)), k
+
+
+@pytest.mark.parametrize("max_pairs,chunk", [(1 << 16, 128), (700, 3)])
+@pytest.mark.parametrize("case", ["cubesurf4000", "volume3000", "refined3000"])
+def test_device_mutual_p2p_lists_equal_host_lists(case, max_pairs, chunk, monkeypatch):
+    """plan.p2p_mutual_lists on the device (torch ops) == on the host (numpy)."""
+    from paper_2202_04894_b200 import plan as plan_mod
+    from paper_2202_04894_b200.plan import build_plan, p2p_mutual_lists
+
+    monkeypatch.setattr(plan_mod, "P2P_GATHER_CHUNK", chunk)
+    g = load_case(case)
+    kw = g["config"]
+    tr, _ = build_tree(g["points"], g["charges"], TreeConfig(ncrit=kw["ncrit"]))
+    p = build_plan(tr, tr, kw["order"], kw["kappa"], 1.0, 2.0)
+    args = (p.p2p_ptr, p.p2p_lo, p.p2p_hi, tr.start[p.leaf_cells], tr.stop[p.leaf_cells], p.counts["p2p_pairs"],
+            max_pairs)
+    a, b = p2p_mutual_lists(*args), p2p_mutual_lists(*args, device="cuda")
+    for k in ("ptr", "lo", "hi", "item_leaf", "item_f0", "item_f1", "item_row", "item_col"):
+        assert np.array_equal(a[k], b[k]), k
+    assert a["partial_size"] == b["partial_size"] and len(a["gather"]) == len(b["gather"])
+    for ga, gb in zip(a["gather"], b["gather"]):
+        for k in ga:
+            assert np.array_equal(ga[k], gb[k].cpu().numpy()), k
