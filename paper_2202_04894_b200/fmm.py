@@ -579,8 +579,8 @@ class FmmPlan:
 
                 try:
                     return build_tree_gpu(pts, q, tree_cfg, root_box=box, device=self.device)
-                except NotImplementedError:  # deeper than the 21-level device keys
-                    pass
+                except (NotImplementedError, torch.cuda.OutOfMemoryError):
+                    pass  # deeper than the 21-level device keys / no room on the device: host build
             return build_tree(pts, q, tree_cfg, root_box=box)
 
         if same:
@@ -594,9 +594,19 @@ class FmmPlan:
         self.same = same
         self.tt, self.st, self.tp, self.sp = tt, st, tp, sp
         t1 = time.perf_counter()
-        self.plan = build_plan(tt, st, config.order, config.kappa, config.eta, config.hf_switch,
-                               keep_events=keep_events, dtt="gpu" if self.build == "gpu" else "native",
-                               device=self.device)
+        try:
+            self.plan = build_plan(tt, st, config.order, config.kappa, config.eta, config.hf_switch,
+                                   keep_events=keep_events, dtt="gpu" if self.build == "gpu" else "native",
+                                   device=self.device)
+        except torch.cuda.OutOfMemoryError:
+            # the device traversal keeps a level's candidate pairs and events in HBM; a GPU
+            # already filled by other plans builds the same lists with the host traversal
+            if self.build != "gpu":
+                raise
+            torch.cuda.empty_cache()
+            self.build = "host"
+            self.plan = build_plan(tt, st, config.order, config.kappa, config.eta, config.hf_switch,
+                                   keep_events=keep_events, dtt="native", device=self.device)
         t2 = time.perf_counter()
         self.timings = {"tree": t1 - t0, "blank": t2 - t1}
         self._make_shard()
