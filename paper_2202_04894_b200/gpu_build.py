@@ -177,6 +177,7 @@ class GpuDtt:
             out = {k: [] for k in ("ev_s", "ev_dense", "row_t", "row_key", "row_lev", "row_cnt", "grp_rows", "grp_p",
                                    "grp_key", "grp_lev", "grp_nblk", "blk_src", "blk_dense", "blk_mask", "p_t", "p_s")}
             n_ev = n_row = 0
+            smarks = {}
             for lev in range(int(depth) + 1):
                 if lev > tt.depth or lev > st.depth or pt.numel() == 0:
                     break
@@ -203,6 +204,8 @@ class GpuDtt:
                     nr = rkey.numel()
                     out["ev_s"].append(es.to(i32))
                     out["ev_dense"].append(ed)
+                    sm = torch.unique(es * KS + (ek + 1))  # distinct (source cell, key): the source marks
+                    smarks[lev] = (sm // KS, sm % KS - 1)
                     out["row_t"].append((rkey // KS).to(i32))
                     out["row_key"].append((rkey % KS - 1).to(i32))
                     out["row_lev"].append(torch.full((nr,), lev, dtype=i32, device=dev))
@@ -293,6 +296,7 @@ class GpuDtt:
                 "trans_dense": trans_dense,
             }
             self.a = _to_host(a, dev)
+            self._smarks = {lev: tuple(x.cpu().numpy() for x in v) for lev, v in smarks.items()}
             self._dev = {"ev_s": a["ev_s"], "row_lev": a["row_lev"], "row_key": a["row_key"], "row_cnt": row_cnt}
         self.n_events = int(self.a["ev_s"].shape[0])
 
@@ -321,6 +325,12 @@ class GpuDtt:
             src_hat = torch.searchsorted(hat_slot, slot).to(torch.int32)
             h = _to_host({"src_hat": src_hat, "hat_slot": hat_slot}, dev)
         return h["src_hat"], h["hat_slot"]
+
+    def source_marks(self, lev: int):
+        """(cells, global direction ids) of the distinct (source cell, key) pairs of
+        the level's M2L events, in (cell, key) order (traversal.py:190-192's source
+        marks); None for a level without events."""
+        return self._smarks.get(int(lev))
 
     def close(self):
         self._dev = None

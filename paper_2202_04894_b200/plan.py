@@ -293,9 +293,13 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
         if r1 == r0:
             continue
         t_marks[lev].append(row_t[r0:r1].astype(np.int64) * KD + row_loc[r0:r1])
-        loc_ev = np.repeat(row_loc[r0:r1], row_cnt[r0:r1])
-        s_marks[lev].append(_unique_cell_keys(ev_s[lev_ev[lev] : lev_ev[lev + 1]], loc_ev, st, lev,
-                                              dt.levels[hf - lev].shape[0], KD))
+        sm = nat.source_marks(lev) if hasattr(nat, "source_marks") else None
+        if sm is not None:  # distinct (source cell, key) of the level's events, found on the device
+            s_marks[lev].append(sm[0] * KD + (sm[1] - dir_off[hf - lev]))
+        else:
+            loc_ev = np.repeat(row_loc[r0:r1], row_cnt[r0:r1])
+            s_marks[lev].append(_unique_cell_keys(ev_s[lev_ev[lev] : lev_ev[lev + 1]], loc_ev, st, lev,
+                                                  dt.levels[hf - lev].shape[0], KD))
     marks_t = _propagate_marks(tt, t_marks, hf, dt, KD)
     marks_s = marks_t if same else _propagate_marks(st, s_marks, hf, dt, KD)
 
@@ -448,26 +452,9 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
 
     # ---- P2P lists: split non-leaf targets into leaves, merge runs ---------
     n_pairs = int(((tt.stop[pt] - tt.start[pt]) * (st.stop[ps] - st.start[ps])).sum())
-    lstart = tt.start[leaves]
-    l0 = np.searchsorted(lstart, tt.start[pt])
-    l1 = np.searchsorted(lstart, tt.stop[pt])
-    cnt = l1 - l0
-    rep = np.repeat(np.arange(pt.shape[0]), cnt)
-    lidx = np.repeat(l0, cnt) + (np.arange(rep.shape[0]) - np.repeat(np.cumsum(cnt) - cnt, cnt))
-    slo = st.start[ps][rep]
-    shi = st.stop[ps][rep]
-    o = np.lexsort((slo, lidx))
-    lidx, slo, shi = lidx[o], slo[o], shi[o]
-    # merge contiguous runs of the same target leaf
-    brk = np.ones(lidx.shape[0], bool)
-    brk[1:] = (lidx[1:] != lidx[:-1]) | (slo[1:] != shi[:-1])
-    gid = np.cumsum(brk) - 1
-    run_lo = slo[brk]
-    run_hi = np.zeros(run_lo.shape[0], np.int64)
-    np.maximum.at(run_hi, gid, shi)
-    run_leaf = lidx[brk]
+    run_leaf, run_lo, run_hi = _p2p_runs(pt, ps, tt, st, leaves, device if dtt == "gpu" else None)
     plan.p2p_ptr = _csr(run_leaf, leaves.shape[0])
-    plan.p2p_lo, plan.p2p_hi = run_lo.astype(np.int64), run_hi
+    plan.p2p_lo, plan.p2p_hi = run_lo.astype(np.int64), run_hi.astype(np.int64)
 
     n_exp = int(m_cell.shape[0])
     plan.counts = {
@@ -512,7 +499,20 @@ def mac_threshold(level: int, hf: bool, beta: float, kappa: float, eta: float, g
     return lo
 
 
+_TABLE_CACHE: dict = {}
+
+
 def _traversal_tables(tt, depth, hf, dt, dir_off, kappa, eta):
+    """Cached per (depth, hf, kappa, eta, root side): see _traversal_tables_build."""
+    key = (int(depth), int(hf), float(kappa), float(eta), float(tt.root_box.side))
+    if key not in _TABLE_CACHE:
+        if len(_TABLE_CACHE) >= 8:
+            _TABLE_CACHE.pop(next(iter(_TABLE_CACHE)))
+        _TABLE_CACHE[key] = _traversal_tables_build(tt, depth, hf, dt, dir_off, kappa, eta)
+    return _TABLE_CACHE[key]
+
+
+def _traversal_tables_build(tt, depth, hf, dt, dir_off, kappa, eta):
     """Per-level MAC thresholds and dense HF key tables for defmm_dtt_build.
 
     Level l's candidate translations are bounded by R_l = min(2^l - 1,
@@ -656,6 +656,33 @@ def dtt_numpy(tt: ClusterTree, st: ClusterTree, kappa: float, eta: float, hf_swi
         T, S = _expand_pairs(tt.first_son[rt], tt.n_sons[rt], st.first_son[rs], st.n_sons[rs])
     cat = lambda xs: np.concatenate(xs) if xs else np.zeros(0, np.int64)  # noqa: E731
     return cat(m2l_t), cat(m2l_s), cat(m2l_lev), cat(p2p_t), cat(p2p_s)
+
+
+def _p2p_runs(pt, ps, tt, st, leaves, device=None):
+    """P2P events (target cell, source cell) -> per target LEAF (Morton order) the
+    merged source particle runs: non-leaf targets are split into their leaves, each
+    leaf's source ranges sorted by start and contiguous ranges merged (the source
+    cells of one leaf are disjoint).  Returns (leaf index, run start, run stop),
+    ordered by (leaf, start).  ``device``: run the expansion and the sort there."""
+    X = _NumpyOps if device is None else _TorchOps(device)
+    n_part = int(st.stop[0]) if st.stop.size else 0
+    lstart = X.arr(tt.start[leaves])
+    pt_, ps_ = X.arr(pt), X.arr(ps)
+    l0 = X.searchsorted(lstart, X.arr(tt.start)[pt_])
+    l1 = X.searchsorted(lstart, X.arr(tt.stop)[pt_])
+    cnt = l1 - l0
+    tot = int(cnt.sum())
+    rep = X.repeat(X.arange(pt_.shape[0]), cnt)
+    lidx = X.repeat(l0, cnt) + (X.arange(tot) - X.repeat(X.cumsum(cnt) - cnt, cnt))
+    slo = X.arr(st.start)[ps_][rep]
+    shi = X.arr(st.stop)[ps_][rep]
+    o = X.argsort_stable(lidx * (n_part + 1) + slo)
+    lidx, slo, shi = lidx[o], slo[o], shi[o]
+    # a run continues while the next range of the same leaf starts where this one stops
+    cont = (lidx[1:] == lidx[:-1]) & (slo[1:] == shi[:-1])
+    first = X.cat([X.full(min(tot, 1), 1) > 0, ~cont])
+    last = X.cat([~cont, X.full(min(tot, 1), 1) > 0])
+    return tuple(X.to_host(a) for a in (lidx[first], slo[first], shi[last]))
 
 
 def _dense_space(tree, hf, dt):
