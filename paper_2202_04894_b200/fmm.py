@@ -801,7 +801,11 @@ class FmmPlan:
         kinds = m2l_level_kinds(self.m2l_variant_default, self.config.dtype, levels, dense,
                                 self.m2l_level_override, os.environ.get("DEFMM_M2L_LEVELS", ""), rpl, self.L)
         self.level_kinds = kinds
-        rkind = np.array([kinds[int(lv)] for lv in rlev], dtype=object) if rows.size else np.zeros(0, object)
+        kind_of = np.full(int(levels.max()) + 1 if levels.size else 1, "", dtype=object)
+        for lv, k in kinds.items():
+            if int(lv) < kind_of.shape[0]:
+                kind_of[int(lv)] = k
+        rkind = kind_of[rlev] if rows.size else np.zeros(0, object)
         z = np.zeros(0, np.int64)
 
         def pick(*ks):
@@ -810,7 +814,11 @@ class FmmPlan:
         # row kernel
         is_rows = pick("rows")
         _, rptr, rsel = _sub_csr(h["row_ptr"], is_rows)
-        h["rk_rows"], h["rk_ptr"], h["rk_ent"] = rows[is_rows], rptr, h["ent"][rsel]
+
+        def take(x, idx):  # rows of a host array or of a device-resident list
+            return x[torch.as_tensor(idx, dtype=torch.int64, device=x.device)] if torch.is_tensor(x) else x[idx]
+
+        h["rk_rows"], h["rk_ptr"], h["rk_ent"] = rows[is_rows], rptr, take(h["ent"], rsel)
         # sibling pairs (K7 v8)
         # sibling groups (K7 v8): per-event merging on the device (m2l_groups_dev)
         ent_dev = _dev(h["ent"], torch.int32, self.device) if any(pick("pair", "triple", "quartet")) else None
@@ -838,12 +846,19 @@ class FmmPlan:
         _, gptr, bsel = _sub_csr(h["grp_ptr"], gkeep)
         h["grp_ptr"], h["grp_rows"] = gptr, gid[gkeep]
         if "blk_src_ev" in h:  # unsharded: spectrum of the selected blocks' events only
-            bs = h.pop("blk_src_ev")[bsel]
-            hat = h["ent"][:, 0]
-            h["blk_src"] = np.where(bs >= 0, hat[np.maximum(bs, 0)] if hat.size else 0, -1).astype(np.int32)
+            bs = take(h.pop("blk_src_ev"), bsel)
+            if torch.is_tensor(bs) or torch.is_tensor(h["ent"]):
+                ent_dev = _dev(h["ent"], torch.int32, self.device) if ent_dev is None else ent_dev
+                bs = _dev(bs, torch.int64, self.device)
+                src = ent_dev[bs.clamp(min=0), 0] if ent_dev.shape[0] else torch.zeros_like(bs, dtype=torch.int32)
+                h["blk_src"] = torch.where(bs >= 0, src, torch.full_like(src, -1))
+            else:
+                hat = h["ent"][:, 0]
+                h["blk_src"] = np.where(bs >= 0, hat[np.maximum(bs, 0)] if hat.size else 0, -1).astype(np.int32)
         else:
             h["blk_src"] = h["blk_src"][bsel]
-        h["blk_trans"], h["blk_mask"], h["blk_kind"] = h["blk_trans"][bsel], h["blk_mask"][bsel], h["blk_kind"][bsel]
+        h["blk_trans"], h["blk_mask"], h["blk_kind"] = take(h["blk_trans"], bsel), h["blk_mask"][bsel], \
+            h["blk_kind"][bsel]
         self.dense_levels = sorted(lv for lv, k in kinds.items() if k == "blocked")
         return h
 
@@ -851,25 +866,29 @@ class FmmPlan:
         """The plan's lists, restricted to this rank's chunk when sharded
         (parallel.py); spectra are renumbered compactly."""
         p, sh = self.plan, self.shard
-        n_ent = p.m2l_rows_entries.shape[0]
+        # lists the device builders left on the device are used there (unsharded plans)
+        ent_dev = p.on_device("m2l_rows_entries") if sh is None else None
         h = {
             "p2m_idx": p.p2m_idx,
             "m2m": [(lev, sl, ss) for lev, sl, ss in p.m2m_levels],
             "hat_slot": p.hat_slot,
             "rows": p.m2l_row_slot,
             "row_ptr": p.m2l_row_ptr,
-            "ent": p.m2l_rows_entries,
+            "ent": ent_dev if ent_dev is not None else p.m2l_rows_entries,
             "l2l": list(p.l2l_levels),
             "leaves": np.ones(p.leaf_cells.shape[0], bool),
             "p2p_ptr": p.p2p_ptr,
             "p2p_sel": np.arange(p.p2p_lo.shape[0]),
         }
         # blocked M2L: group rows as indices into h["rows"] (lhat rows)
-        blk = {"grp_ptr": p.blk_group_ptr, "grp_rows": p.blk_group_rows, "blk_src_ev": p.blk_src_ev,
-               "blk_trans": p.blk_trans, "blk_mask": p.blk_mask, "blk_kind": p.blk_kind}
         if sh is None:
-            h.update(blk)
-            h["grp_rows"] = _rows_to_ids(blk["grp_rows"], h["rows"])
+            def dev_or_host(name):
+                t = p.on_device(name)
+                return t if t is not None else getattr(p, name)
+
+            h.update({"grp_ptr": p.blk_group_ptr, "grp_rows": _rows_to_ids(p.blk_group_rows, h["rows"]),
+                      "blk_src_ev": dev_or_host("blk_src_ev"), "blk_trans": dev_or_host("blk_trans"),
+                      "blk_mask": p.blk_mask, "blk_kind": p.blk_kind})
             return h
         h["p2m_idx"] = sh.p2m_idx
         h["m2m"] = [(lev, sl[k], ss[k]) for (lev, sl, ss), k in zip(p.m2m_levels, sh.m2m_keep) if k.any()]

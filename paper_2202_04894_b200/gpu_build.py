@@ -17,10 +17,10 @@ import torch
 
 from . import _lib
 from .config import TreeConfig
-from .geometry import BoundingBox, compute_root_box
+from .geometry import BoundingBox
 from .tree import ClusterTree, ParticleSet
 
-__all__ = ["build_tree_gpu", "GpuDtt"]
+__all__ = ["build_tree_gpu", "GpuDtt", "Deferred"]
 
 KEY_DEPTH = 21  # 3 bits per level in one int64 key
 
@@ -44,16 +44,16 @@ def build_tree_gpu(points, charges, config: TreeConfig = TreeConfig(), root_box:
         raise ValueError("at least one particle is required")
     if points.shape[0] != charges.shape[0]:
         raise ValueError("points and charges length mismatch")
-    if not np.all(np.isfinite(points)):
-        raise ValueError("particle coordinates must be finite")
-    if root_box is None:
-        root_box = compute_root_box(points)
     dev = torch.device(device)
     n = points.shape[0]
     ncrit, cap = int(config.ncrit), int(config.hard_depth_cap)
     D = min(cap, KEY_DEPTH)
     with torch.cuda.device(dev):
         pts = torch.as_tensor(np.ascontiguousarray(points, dtype=np.float64)).to(dev)
+        if not bool(torch.isfinite(pts).all()):
+            raise ValueError("particle coordinates must be finite")
+        if root_box is None:
+            root_box = _root_box(points, pts)
         keys = torch.empty(n, dtype=torch.int64, device=dev)
         lower = np.ascontiguousarray(root_box.lower, dtype=np.float64)
         _lib.check(_lib.load().defmm_tree_keys(n, pts.data_ptr(), lower.ctypes.data, float(root_box.side), D,
@@ -126,16 +126,46 @@ def build_tree_gpu(points, charges, config: TreeConfig = TreeConfig(), root_box:
     return tree, pset
 
 
+def _root_box(points: np.ndarray, pts: torch.Tensor) -> BoundingBox:
+    """geometry.compute_root_box (geometry.py:82-97) with the extremes found on
+    the device: the centre is the same numpy mean; max |x - c| is attained at a
+    coordinate extreme because the rounded difference is monotone in x, so the
+    half width (and the box) is bit-identical."""
+    center = points.mean(axis=0)
+    half = 0.5
+    if points.shape[0] > 1:
+        lo, hi = torch.aminmax(pts, dim=0)
+        lo, hi = lo.cpu().numpy(), hi.cpu().numpy()
+        half = np.max(np.maximum(hi - center, center - lo))
+    if half == 0.0:
+        half = 0.5
+    return BoundingBox(center=center, half_width=half * (1.0 + 1e-6))
+
+
 def _to_host(tensors: dict, dev) -> dict:
-    """Device tensors -> numpy arrays through pinned staging buffers (the
-    pageable path moves these lists at ~1.5 GB/s)."""
+    """Device tensors -> numpy arrays in pinned host memory (the pageable path
+    moves these lists at ~1.5 GB/s; a second copy out of the staging buffer
+    cost as much as the transfer).  The arrays keep their buffers alive."""
     staged = {}
     for k, v in tensors.items():
         h = torch.empty(v.shape, dtype=v.dtype, device="cpu", pin_memory=True)
         h.copy_(v, non_blocking=True)
         staged[k] = h
     torch.cuda.synchronize(dev)
-    return {k: np.array(h.numpy()) for k, h in staged.items()}
+    return {k: h.numpy() for k, h in staged.items()}
+
+
+class Deferred:
+    """A plan list that stays on the device until host code asks for it (the
+    per-event lists are hundreds of MB at the large workloads and the device
+    matvec never needs them on the host)."""
+
+    def __init__(self, tensor: torch.Tensor):
+        self.dev = tensor
+        self.shape = tuple(tensor.shape)
+
+    def host(self) -> np.ndarray:
+        return _to_host({"x": self.dev}, self.dev.device)["x"]
 
 
 def _octant(coords, parent, cells):
@@ -295,17 +325,34 @@ class GpuDtt:
                 "blk_mask": cat("blk_mask", i64), "p_t": cat("p_t", i32), "p_s": cat("p_s", i32),
                 "trans_dense": trans_dense,
             }
+            self._late = {k: a.pop(k) for k in self.LATE}
             self.a = _to_host(a, dev)
             self._smarks = {lev: tuple(x.cpu().numpy() for x in v) for lev, v in smarks.items()}
-            self._dev = {"ev_s": a["ev_s"], "row_lev": a["row_lev"], "row_key": a["row_key"], "row_cnt": row_cnt}
-        self.n_events = int(self.a["ev_s"].shape[0])
+            self._dev = {"ev_s": self._late["ev_s"], "row_lev": a["row_lev"], "row_key": a["row_key"],
+                         "row_cnt": row_cnt}
+        self.n_events = int(self._late["ev_s"].shape[0])
+
+    # per-event and per-block lists: downloaded on first host access only
+    LATE = ("ev_s", "ev_trans", "blk_src", "blk_trans")
 
     def __getitem__(self, k):
+        if k not in self.a:
+            self.a[k] = Deferred(self._late[k]).host()
         return self.a[k]
+
+    def deferred(self, k) -> Deferred:
+        """The list as a device-resident Deferred (no transfer)."""
+        return Deferred(self._late[k])
+
+    def entries(self, src_hat: torch.Tensor) -> Deferred:
+        """The (n_events, 2) int32 M2L entry table {spectrum, translation id} in
+        row order (plan.Plan.m2l_rows_entries), on the device."""
+        return Deferred(torch.stack([src_hat.to(torch.int32), self._late["ev_trans"]], 1).contiguous())
 
     def source_hats(self, m_dense, base, nd, level_off, key_base, n_mult):
         """defmm_dtt_source_hats on the device lists: the spectrum index of every
-        event's source expansion and the used multipole slots, ascending."""
+        event's source expansion (a device tensor) and the used multipole slots,
+        ascending (host)."""
         d = self._dev
         dev = d["ev_s"].device
         i64 = torch.int64
@@ -323,8 +370,8 @@ class GpuDtt:
                 raise RuntimeError("missing source expansion: blank-pass bug")
             hat_slot = torch.unique(slot)
             src_hat = torch.searchsorted(hat_slot, slot).to(torch.int32)
-            h = _to_host({"src_hat": src_hat, "hat_slot": hat_slot}, dev)
-        return h["src_hat"], h["hat_slot"]
+            h = _to_host({"hat_slot": hat_slot}, dev)
+        return src_hat, h["hat_slot"]
 
     def source_marks(self, lev: int):
         """(cells, global direction ids) of the distinct (source cell, key) pairs of

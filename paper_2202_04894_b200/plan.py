@@ -127,9 +127,28 @@ def _csr(keys: np.ndarray, n: int) -> np.ndarray:
     return np.searchsorted(keys, np.arange(n + 1)).astype(np.int64)
 
 
+def _deferred_list(name: str, doc: str):
+    """A Plan list that may be handed over as a device-resident
+    gpu_build.Deferred: reading the attribute downloads it once."""
+    slot = "_d_" + name
+
+    def get(self):
+        v = self.__dict__.get(slot)
+        if hasattr(v, "host"):
+            v = self.__dict__[slot] = v.host()
+        return v
+
+    def put(self, v):
+        self.__dict__[slot] = v
+
+    return property(get, put, doc=doc)
+
+
 @dataclass
 class Plan:
-    """Everything the device matvec needs, as host numpy arrays."""
+    """Everything the device matvec needs, as host numpy arrays (the device
+    builders leave the per-event and per-block lists on the device:
+    ``on_device``)."""
 
     order: int
     kappa: float
@@ -157,7 +176,8 @@ class Plan:
     m2l_row_slot: np.ndarray = None
     m2l_row_ptr: np.ndarray = None
     m2l_level: np.ndarray = None  # per row
-    m2l_rows_entries: np.ndarray = None  # (n_m2l, 2) int32 {hat, derived symbol} in row order
+    m2l_rows_entries = _deferred_list("m2l_rows_entries",
+                                      "(n_m2l, 2) int32 {hat, derived symbol} in row order")
     l2l_levels: list = None  # [(son level, out_slot, octant, ptr, src_slot, src_dir)]
     leaf_cells: np.ndarray = None  # target-tree leaves
     leaf_slot_lo: np.ndarray = None
@@ -172,13 +192,19 @@ class Plan:
     # parent-pair blocks of the blocked M2L (K7 v3)
     blk_group_rows: np.ndarray = None  # (ngroups, 8) local slots of the group's rows, -1 absent
     blk_group_ptr: np.ndarray = None  # block range per group
-    blk_src_ev: np.ndarray = None  # (nblocks, 8) an event of each source child (its spectrum: entries[ev, 0]), -1 absent
-    blk_trans: np.ndarray = None  # (nblocks, 27) derived symbol per child offset, -1 unused
+    blk_src_ev = _deferred_list("blk_src_ev", "(nblocks, 8) an event of each source child (its spectrum: "
+                                "entries[ev, 0]), -1 absent")
+    blk_trans = _deferred_list("blk_trans", "(nblocks, 27) derived symbol per child offset, -1 unused")
     blk_mask: np.ndarray = None  # (nblocks,) int64: bit 8a+b = (a, b) is an M2L event
     blk_kind: np.ndarray = None  # (nblocks,) int8: -1 general, 2p+v planar
     # event logs (optional, for the events= API)
     m2l_events: tuple = None
     p2p_events: tuple = None
+
+    def on_device(self, name: str):
+        """The device tensor of a list the host has not read yet, else None."""
+        v = self.__dict__.get("_d_" + name)
+        return v.dev if hasattr(v, "host") else None
 
     @property
     def blk_src(self):
@@ -249,9 +275,9 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
     else:
         raise ValueError(f"unknown traversal builder {dtt!r}")
     row_ptr, row_t, row_key, row_lev = nat["row_ptr"], nat["row_t"], nat["row_key"], nat["row_lev"]
-    ev_s, ev_trans = nat["ev_s"], nat["ev_trans"]
+    on_dev = hasattr(nat, "deferred")  # the device traversal keeps the per-event lists on the device
     pt, ps = nat["p_t"].astype(np.int64), nat["p_s"].astype(np.int64)
-    n_m2l = int(ev_s.shape[0])
+    n_m2l = int(nat.n_events)
     n_rows = int(row_t.shape[0])
     row_cnt = np.diff(row_ptr)
     # events are level-contiguous (rows are ordered (level, target, key))
@@ -261,7 +287,6 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
 
     # ---- distinct (level, t): the used entries of the dense tables ---------
     uniq = nat["trans_dense"]  # used dense-table entries == (level, t) lexicographic order
-    inv = ev_trans  # translation id per event
     u_lev = np.searchsorted(tab_off, uniq, side="right") - 1
     rel = uniq - tab_off[u_lev]
     w = 2 * R[u_lev].astype(np.int64) + 1
@@ -298,7 +323,7 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
             s_marks[lev].append(sm[0] * KD + (sm[1] - dir_off[hf - lev]))
         else:
             loc_ev = np.repeat(row_loc[r0:r1], row_cnt[r0:r1])
-            s_marks[lev].append(_unique_cell_keys(ev_s[lev_ev[lev] : lev_ev[lev + 1]], loc_ev, st, lev,
+            s_marks[lev].append(_unique_cell_keys(nat["ev_s"][lev_ev[lev] : lev_ev[lev + 1]], loc_ev, st, lev,
                                                   dt.levels[hf - lev].shape[0], KD))
     marks_t = _propagate_marks(tt, t_marks, hf, dt, KD)
     marks_s = marks_t if same else _propagate_marks(st, s_marks, hf, dt, KD)
@@ -404,10 +429,13 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
     tslot = lslot(rt64, row_loc)  # rows are (level, cell, key)-ordered: increasing
     plan.m2l_row_slot = tslot.astype(np.int64)
     plan.m2l_row_ptr = row_ptr
-    ent = np.empty((n_m2l, 2), np.int32)
-    ent[:, 0] = src_hat
-    ent[:, 1] = inv
-    plan.m2l_rows_entries = ent
+    if on_dev:
+        plan.m2l_rows_entries = nat.entries(src_hat)
+    else:
+        ent = np.empty((n_m2l, 2), np.int32)
+        ent[:, 0] = src_hat
+        ent[:, 1] = nat["ev_trans"]  # translation id per event
+        plan.m2l_rows_entries = ent
     plan.m2l_level = row_lev.astype(np.int64)
     # derived-symbol table: one per distinct (level, t)
     plan.trans_canon = cinv.astype(np.int32)
@@ -416,9 +444,8 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
     gr = nat["grp_rows"]
     plan.blk_group_rows = np.where(gr >= 0, tslot[np.maximum(gr, 0)], -1) if n_rows else gr
     plan.blk_group_ptr = nat["grp_ptr"]
-    plan.blk_src_ev = nat["blk_src"]
-    bt = nat["blk_trans"]
-    plan.blk_trans = bt
+    plan.blk_src_ev = nat.deferred("blk_src") if on_dev else nat["blk_src"]
+    plan.blk_trans = nat.deferred("blk_trans") if on_dev else nat["blk_trans"]
     plan.blk_mask = nat["blk_mask"]
     plan.blk_kind = planar_kind(plan.blk_mask)
 
@@ -467,7 +494,8 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
         "translations": int(uniq.shape[0]),
     }
     if keep_events:
-        plan.m2l_events = (np.repeat(rt64, row_cnt), ev_s.astype(np.int64), np.repeat(row_key.astype(np.int64), row_cnt))
+        plan.m2l_events = (np.repeat(rt64, row_cnt), nat["ev_s"].astype(np.int64),
+                           np.repeat(row_key.astype(np.int64), row_cnt))
         plan.p2p_events = (pt, ps)
     return plan
 

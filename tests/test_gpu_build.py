@@ -18,6 +18,7 @@ def _same_tree(a, b):
     for k in ("level", "coords", "start", "stop", "parent", "first_son", "n_sons", "level_offsets"):
         assert np.array_equal(getattr(a, k), getattr(b, k)), k
     assert np.array_equal(a.alpha, b.alpha) and a.depth == b.depth
+    assert np.array_equal(a.root_box.lower, b.root_box.lower) and a.root_box.side == b.root_box.side
 
 
 def _points(kind):
@@ -51,6 +52,21 @@ def test_gpu_tree_equals_host_tree(kind, ncrit, cap):
     _same_tree(tg, th)
     assert np.array_equal(pg.original_index, ph.original_index)
     assert np.array_equal(pg.positions, ph.positions) and np.array_equal(pg.charges, ph.charges)
+
+
+def test_gpu_tree_root_box_edge_cases():
+    """One particle and coincident particles take the reference's 0.5 half width
+    (geometry.py:92-95); a non-finite coordinate is refused."""
+    from paper_2202_04894_b200.gpu_build import build_tree_gpu
+
+    for pts in (np.array([[0.3, -1.2, 4.0]]), np.tile([[1.0, 2.0, 3.0]], (5, 1))):
+        q = np.ones(pts.shape[0], complex)
+        th, _ = build_tree(pts, q, TreeConfig(ncrit=8, hard_depth_cap=4))
+        tg, _ = build_tree_gpu(pts, q, TreeConfig(ncrit=8, hard_depth_cap=4))
+        _same_tree(tg, th)
+    bad = np.array([[0.0, 0.0, 0.0], [1.0, np.inf, 0.0]])
+    with pytest.raises(ValueError):
+        build_tree_gpu(bad, np.ones(2, complex), TreeConfig())
 
 
 @pytest.mark.parametrize("case", ["cubesurf4000", "refined3000", "c1_kd8"])
