@@ -19,7 +19,7 @@ import torch
 from . import _lib
 from .config import FmmConfig, FmmInfo, InteractionEvent, TreeConfig
 from .geometry import compute_root_box
-from .plan import build_plan, p2p_mutual_lists, p2p_work_items
+from .plan import build_plan, p2p_mutual_lists, p2p_work_items, planar_kind
 from .tree import build_tree
 
 __all__ = ["FmmPlan", "run_fmm", "run_fmm_full"]
@@ -471,7 +471,9 @@ def block_levels(plan, tt):
 def dense_levels(plan, tt, threshold: float = BLOCKED_MIN_EVENTS_PER_BLOCK) -> set:
     """Levels whose parent-pair blocks hold >= threshold events on average."""
     blev, ev, _, _ = block_levels(plan, tt)
-    return {int(lv) for lv in np.unique(blev) if ev[blev == lv].mean() >= threshold}
+    cnt = np.bincount(blev)
+    tot = np.bincount(blev, weights=ev)  # integer sums below 2^53: exact
+    return {int(lv) for lv in np.nonzero(cnt)[0] if tot[lv] / cnt[lv] >= threshold}
 
 
 def p2p_overlap_policy(level_kinds: dict) -> tuple:
@@ -628,10 +630,14 @@ class FmmPlan:
         # HBM stride of one spectrum (even-padded for complex64 vector loads)
         self.SS = int(_lib.load().defmm_spectrum_stride(L, int(self.config.dtype == "c64")))
         # particles (sorted order), SoA
-        self.s_xyz = [_dev(self.sp.positions[:, k], f64, d) for k in range(3)]
-        self.t_xyz = self.s_xyz if self.same else [_dev(self.tp.positions[:, k], f64, d) for k in range(3)]
-        self.s_perm = _dev(self.sp.original_index, i64, d)
-        self.t_perm = self.s_perm if self.same else _dev(self.tp.original_index, i64, d)
+        def particles(ps):  # a device-built tree left the sorted positions and the permutation in HBM
+            dv = getattr(ps, "dev", None)
+            if dv is not None and dv["positions"].device == d:
+                return [dv["positions"][:, k].contiguous() for k in range(3)], dv["perm"]
+            return [_dev(ps.positions[:, k], f64, d) for k in range(3)], _dev(ps.original_index, i64, d)
+
+        self.s_xyz, self.s_perm = particles(self.sp)
+        self.t_xyz, self.t_perm = (self.s_xyz, self.s_perm) if self.same else particles(self.tp)
         self.n_src = self.sp.n
         self.n_tgt = self.tp.n
 
@@ -857,8 +863,8 @@ class FmmPlan:
                 h["blk_src"] = np.where(bs >= 0, hat[np.maximum(bs, 0)] if hat.size else 0, -1).astype(np.int32)
         else:
             h["blk_src"] = h["blk_src"][bsel]
-        h["blk_trans"], h["blk_mask"], h["blk_kind"] = take(h["blk_trans"], bsel), h["blk_mask"][bsel], \
-            h["blk_kind"][bsel]
+        h["blk_trans"], h["blk_mask"] = take(h["blk_trans"], bsel), h["blk_mask"][bsel]
+        h["blk_kind"] = h["blk_kind"][bsel] if "blk_kind" in h else planar_kind(h["blk_mask"])
         self.dense_levels = sorted(lv for lv, k in kinds.items() if k == "blocked")
         return h
 
@@ -888,7 +894,7 @@ class FmmPlan:
 
             h.update({"grp_ptr": p.blk_group_ptr, "grp_rows": _rows_to_ids(p.blk_group_rows, h["rows"]),
                       "blk_src_ev": dev_or_host("blk_src_ev"), "blk_trans": dev_or_host("blk_trans"),
-                      "blk_mask": p.blk_mask, "blk_kind": p.blk_kind})
+                      "blk_mask": p.blk_mask})
             return h
         h["p2m_idx"] = sh.p2m_idx
         h["m2m"] = [(lev, sl[k], ss[k]) for (lev, sl, ss), k in zip(p.m2m_levels, sh.m2m_keep) if k.any()]

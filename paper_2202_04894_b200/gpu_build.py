@@ -20,7 +20,7 @@ from .config import TreeConfig
 from .geometry import BoundingBox
 from .tree import ClusterTree, ParticleSet
 
-__all__ = ["build_tree_gpu", "GpuDtt", "Deferred"]
+__all__ = ["build_tree_gpu", "GpuDtt", "Deferred", "DeviceParticleSet"]
 
 KEY_DEPTH = 21  # 3 bits per level in one int64 key
 
@@ -118,12 +118,49 @@ def build_tree_gpu(points, charges, config: TreeConfig = TreeConfig(), root_box:
             ps = st_l[lev - 1]
             j = torch.searchsorted(ps, st_l[lev], right=True) - 1
             parent[offs[lev]:offs[lev + 1]] = offs[lev - 1] + j
-        h = _to_host({"perm": perm, "spts": pts[perm], "level": level, "coords": coords, "start": start,
-                      "stop": stop, "parent": parent}, dev)
+        h = _to_host({"perm": perm, "level": level, "coords": coords, "start": start, "stop": stop,
+                      "parent": parent}, dev)
         tree = ClusterTree(root_box, config, h["level"], h["coords"], h["start"], h["stop"], h["parent"])
-        pset = ParticleSet(positions=h["spts"], charges=charges[h["perm"]].copy(),
-                           potentials=np.zeros(n, dtype=complex), original_index=h["perm"])
+        pset = DeviceParticleSet(h["perm"], pts[perm], perm, charges)
     return tree, pset
+
+
+class DeviceParticleSet(ParticleSet):
+    """The ParticleSet (tree.py:48-59) of a device-built tree.  The sorted
+    positions and the permutation stay on the device (``dev``) where FmmPlan
+    uses them; the host arrays of the reference's record -- sorted positions,
+    permuted charges, zeroed potentials -- are produced when first read."""
+
+    def __init__(self, original_index: np.ndarray, positions_dev: torch.Tensor, perm_dev: torch.Tensor,
+                 charges: np.ndarray):
+        self.original_index = original_index
+        self.dev = {"positions": positions_dev, "perm": perm_dev}
+        self._late = {
+            "positions": lambda: _to_host({"x": positions_dev}, positions_dev.device)["x"],
+            "charges": lambda: charges[original_index].copy(),
+            "potentials": lambda: np.zeros(original_index.shape[0], dtype=complex),
+        }
+
+    @property
+    def n(self) -> int:
+        return int(self.original_index.shape[0])
+
+
+def _late_field(name):
+    def get(self):
+        v = self._late[name]
+        if callable(v):
+            v = self._late[name] = v()
+        return v
+
+    def put(self, v):
+        self._late[name] = v
+
+    return property(get, put)
+
+
+for _name in ("positions", "charges", "potentials"):
+    setattr(DeviceParticleSet, _name, _late_field(_name))
 
 
 def _root_box(points: np.ndarray, pts: torch.Tensor) -> BoundingBox:

@@ -196,10 +196,16 @@ class Plan:
                                 "entries[ev, 0]), -1 absent")
     blk_trans = _deferred_list("blk_trans", "(nblocks, 27) derived symbol per child offset, -1 unused")
     blk_mask: np.ndarray = None  # (nblocks,) int64: bit 8a+b = (a, b) is an M2L event
-    blk_kind: np.ndarray = None  # (nblocks,) int8: -1 general, 2p+v planar
     # event logs (optional, for the events= API)
     m2l_events: tuple = None
     p2p_events: tuple = None
+
+    @property
+    def blk_kind(self):
+        """(nblocks,) int8: -1 general, 2p+v planar (from blk_mask, on first use)."""
+        if getattr(self, "_blk_kind", None) is None:
+            self._blk_kind = planar_kind(self.blk_mask)
+        return self._blk_kind
 
     def on_device(self, name: str):
         """The device tensor of a list the host has not read yet, else None."""
@@ -304,7 +310,7 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
     sym_t = np.empty((cuniq.shape[0], 3), np.int64)
     sym_t[cinv] = canon
     plan.sym_tvec = sym_t.astype(np.int32)
-    plan.sym_beta = np.array([tt.side_at(int(l)) for l in sym_lev], dtype=np.float64)
+    plan.sym_beta = tt.root_box.side / np.left_shift(np.int64(1), sym_lev)  # ClusterTree.side_at per symbol
     plan.sym_level = sym_lev
     _check_stencils(sym_t, sym_lev, tt, order, tol)
 
@@ -447,7 +453,6 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
     plan.blk_src_ev = nat.deferred("blk_src") if on_dev else nat["blk_src"]
     plan.blk_trans = nat.deferred("blk_trans") if on_dev else nat["blk_trans"]
     plan.blk_mask = nat["blk_mask"]
-    plan.blk_kind = planar_kind(plan.blk_mask)
 
     # L2L gather lists per son level
     l2l_levels = []
