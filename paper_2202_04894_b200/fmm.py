@@ -632,7 +632,7 @@ class FmmPlan:
         # particles (sorted order), SoA
         def particles(ps):  # a device-built tree left the sorted positions and the permutation in HBM
             dv = getattr(ps, "dev", None)
-            if dv is not None and dv["positions"].device == d:
+            if dv is not None and dv["positions"].device == torch.empty(0, device=d).device:
                 return [dv["positions"][:, k].contiguous() for k in range(3)], dv["perm"]
             return [_dev(ps.positions[:, k], f64, d) for k in range(3)], _dev(ps.original_index, i64, d)
 
@@ -708,16 +708,10 @@ class FmmPlan:
         p2p_lo, p2p_hi = p.p2p_lo[h["p2p_sel"]], p.p2p_hi[h["p2p_sel"]]
         self.p2p_lo = _dev(p2p_lo, i64, d)
         self.p2p_hi = _dev(p2p_hi, i64, d)
-        wi = p2p_work_items(h["p2p_ptr"], p2p_hi - p2p_lo, tt.stop[p.leaf_cells[lv]] - tt.start[p.leaf_cells[lv]])
-        self.n_items = int(wi["item_leaf"].shape[0])
-        self.p2p_items = [_dev(wi[k], torch.int32 if k == "item_leaf" else i64, d)
-                          for k in ("item_leaf", "item_f0", "item_f1", "item_out")]
-        self.n_split = int(wi["split_leaf"].shape[0])
-        self.p2p_split = [_dev(wi["split_leaf"], i32, d), _dev(wi["split_base"], i64, d), _dev(wi["split_n"], i32, d)]
-        self._partial_size = wi["partial_size"]
         # mutual P2P (K1 v2): single-tree, unsharded plans evaluate every near-field
         # pair once for both directions (DEFMM_P2P_MUTUAL=0 keeps the one-directional kernel)
         self.p2p_mut = None
+        self.n_items, self.p2p_items, self.n_split, self.p2p_split, self._partial_size = 0, None, 0, None, 0
         mut = os.environ.get("DEFMM_P2P_MUTUAL", "auto")  # "1" / "0" force, "auto": large near fields
         if self.same and self.shard is None and (mut == "1" or (mut == "auto" and
                                                                 p.counts["p2p_pairs"] >= P2P_MUTUAL_MIN_PAIRS)):
@@ -732,7 +726,17 @@ class FmmPlan:
                     (int(g["task_leaf"].shape[0]), _dev(g["task_leaf"], i32, d), _dev(g["task_out"], i64, d),
                      _dev(g["cptr"], i64, d), _dev(g["cbase"], i64, d), _dev(g["cxlo"], i32, d),
                      _dev(g["cxhi"], i32, d)) for g in ml["gather"]]
-                self._partial_size = max(self._partial_size, ml["partial_size"])
+                self._partial_size = ml["partial_size"]
+        if self.p2p_mut is None:  # one-directional work items (K1)
+            wi = p2p_work_items(h["p2p_ptr"], p2p_hi - p2p_lo,
+                                tt.stop[p.leaf_cells[lv]] - tt.start[p.leaf_cells[lv]])
+            self.n_items = int(wi["item_leaf"].shape[0])
+            self.p2p_items = [_dev(wi[k], torch.int32 if k == "item_leaf" else i64, d)
+                              for k in ("item_leaf", "item_f0", "item_f1", "item_out")]
+            self.n_split = int(wi["split_leaf"].shape[0])
+            self.p2p_split = [_dev(wi["split_leaf"], i32, d), _dev(wi["split_base"], i64, d),
+                              _dev(wi["split_n"], i32, d)]
+            self._partial_size = wi["partial_size"]
         # workspaces (storage precision per FmmConfig.dtype)
         cd = self.cdtype
         self.mult = torch.empty((max(p.n_mult, 1), self.L3), dtype=cd, device=d)

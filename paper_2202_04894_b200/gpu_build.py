@@ -363,6 +363,9 @@ class GpuDtt:
                 "trans_dense": trans_dense,
             }
             self._late = {k: a.pop(k) for k in self.LATE}
+            # near-field pair count (counts["p2p_pairs"], traversal.py:303-317)
+            tn, sn = up(tt.stop - tt.start), (None if same else up(st.stop - st.start))
+            self.n_pairs = int((tn[a["p_t"].to(i64)] * (tn if same else sn)[a["p_s"].to(i64)]).sum().item())
             self.a = _to_host(a, dev)
             self._smarks = {lev: tuple(x.cpu().numpy() for x in v) for lev, v in smarks.items()}
             self._dev = {"ev_s": self._late["ev_s"], "row_lev": a["row_lev"], "row_key": a["row_key"],

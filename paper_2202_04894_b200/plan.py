@@ -483,7 +483,7 @@ def build_plan(tt: ClusterTree, st: ClusterTree, order: int, kappa: float, eta: 
     plan.leaf_slot_hi = np.searchsorted(l_cell, leaves, side="right").astype(np.int64)
 
     # ---- P2P lists: split non-leaf targets into leaves, merge runs ---------
-    n_pairs = int(((tt.stop[pt] - tt.start[pt]) * (st.stop[ps] - st.start[ps])).sum())
+    n_pairs = int(nat.n_pairs) if on_dev else int(((tt.stop[pt] - tt.start[pt]) * (st.stop[ps] - st.start[ps])).sum())
     run_leaf, run_lo, run_hi = _p2p_runs(pt, ps, tt, st, leaves, device if dtt == "gpu" else None)
     plan.p2p_ptr = _csr(run_leaf, leaves.shape[0])
     plan.p2p_lo, plan.p2p_hi = run_lo.astype(np.int64), run_hi.astype(np.int64)
