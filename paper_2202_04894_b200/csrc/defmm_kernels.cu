@@ -24,6 +24,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 #include <vector>
 
@@ -185,6 +186,11 @@ __device__ __forceinline__ void make_twiddles(V* tw) {
 // launchers (cudaMemcpyToSymbol); kernels build their P x L matrix from it
 __constant__ double2 c_tw[8][15];
 __constant__ float2 c_twf[8][15];  // the same, rounded to float (complex64 M2F v2)
+// A_0[k][j] = S_k(x_j / 2) of every order (row L-1, entry k L + j), filled with
+// c_tw; A_1 is its mirror image, A_1[k][j] = A_0[L-1-k][L-1-j] (the nodes are
+// symmetric about 1/2), so the fiber kernels below need this table only
+__constant__ double c_a0[8][64];
+__constant__ float c_a0f[8][64];
 
 // ---------------------------------------------------------------------------
 // Spectral layout.  Every P^3 spectrum (multipole spectra, symbols, local
@@ -424,6 +430,171 @@ __global__ void __launch_bounds__(32 * NODAL_WARPS, DEFMM_NODAL_MINB) m2m_kernel
     }
 }
 
+// K4/K5 v2: the mode products with one FIBER per lane.  A lane loads the L
+// entries of its fiber once, forms the L outputs with the interpolation factors
+// as constant-bank operands (c_a0) and writes them back in place: L loads +
+// L stores per 2 L^2 FFMA instead of two shared loads per FFMA pair (v1 issues
+// as many LDS as FFMA).  The bit-1 factor matrix is the mirror image of the
+// bit-0 one, so a lane whose son sits in the upper half walks its fiber
+// backwards with the same constants -- which lets the lanes of one warp work on
+// the tiles of TWO sons at once (2 L^2 fibers per pass: all 32 lanes at L = 4).
+template <int L, typename R>
+__device__ __forceinline__ R a0c(int k, int j) {
+    if constexpr (sizeof(R) == 4) {
+        return c_a0f[L - 1][k * L + j];
+    } else {
+        return c_a0[L - 1][k * L + j];
+    }
+}
+
+// in-place product of fiber f (of L^2) of an L^3 tile along AXIS with A_bit
+// (TRANSPOSE=false: out k, in j, A[k][j], M2M) or its transpose (L2L)
+template <int L, typename R, bool TRANSPOSE, int AXIS>
+__device__ __forceinline__ void fiber_product(cx<R>* tile, int f, int bit) {
+    using V = cx<R>;
+    constexpr int stride = AXIS == 0 ? L * L : (AXIS == 1 ? L : 1);
+    const int base = AXIS == 0 ? f : (AXIS == 1 ? (f / L) * (L * L) + f % L : f * L);
+    V* p = tile + base + (bit ? (L - 1) * stride : 0);
+    const int sg = bit ? -stride : stride;
+    V x[L];
+#pragma unroll
+    for (int j = 0; j < L; ++j) x[j] = p[j * sg];
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+        V v = cz<V>();
+#pragma unroll
+        for (int j = 0; j < L; ++j) v = crfma(TRANSPOSE ? a0c<L, R>(j, k) : a0c<L, R>(k, j), x[j], v);
+        p[k * sg] = v;
+    }
+}
+
+// the three products of the (up to) two tiles at `tiles`, `tiles + L^3`; oa, ob
+// = octants of the tiles' sons (ob < 0: one tile)
+template <int L, typename R, bool TRANSPOSE>
+__device__ __forceinline__ void fiber_products(cx<R>* tiles, int oa, int ob, int lane) {
+    constexpr int L2 = L * L, L3 = L * L * L, NP = (2 * L2 + 31) / 32;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        const int id = p * 32 + lane, t = id >= L2;
+        if (id < 2 * L2 && (!t || ob >= 0))
+            fiber_product<L, R, TRANSPOSE, 0>(tiles + t * L3, id - t * L2, ((t ? ob : oa) >> 2) & 1);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        const int id = p * 32 + lane, t = id >= L2;
+        if (id < 2 * L2 && (!t || ob >= 0))
+            fiber_product<L, R, TRANSPOSE, 1>(tiles + t * L3, id - t * L2, ((t ? ob : oa) >> 1) & 1);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        const int id = p * 32 + lane, t = id >= L2;
+        if (id < 2 * L2 && (!t || ob >= 0))
+            fiber_product<L, R, TRANSPOSE, 2>(tiles + t * L3, id - t * L2, (t ? ob : oa) & 1);
+    }
+    __syncwarp();
+}
+
+template <typename R, int L>
+__host__ __device__ constexpr int nodal2_smem_bytes() {
+    return NODAL_WARPS * (2 * cube<L>() + 9 * L) * (int)sizeof(cx<R>);
+}
+// a fiber (L entries) and the per-lane accumulators (L^3 / 32 entries) live in
+// registers: the 64-register cap of DEFMM_NODAL_MINB spills from L = 6 (L = 5 in FP64)
+template <typename R, int L>
+__host__ __device__ constexpr int nodal2_minb() {
+    return (sizeof(R) == 4 ? L <= 5 : L <= 4) ? DEFMM_NODAL_MINB : 2;
+}
+
+template <typename R, int L>
+__global__ void __launch_bounds__(32 * NODAL_WARPS, nodal2_minb<R, L>()) m2m_fiber_kernel(
+    int64_t n, const int64_t* __restrict__ out_slot, const int32_t* __restrict__ dir,
+    const int64_t* __restrict__ son_slot, double son_beta, const double* __restrict__ dirs, double kappa,
+    cx<R>* __restrict__ mult) {
+    using V = cx<R>;
+    constexpr int L3 = cube<L>(), E = per_lane<L>();
+    extern __shared__ unsigned char smraw[];
+    V* bufs = reinterpret_cast<V*>(smraw);
+    V* tabs = bufs + NODAL_WARPS * 2 * L3;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * NODAL_WARPS + w;
+    if (i >= n) return;
+    const int d = dir[i];
+    R ku[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) ku[k] = (R)(d >= 0 ? kappa * son_beta * dirs[3 * d + k] : 0.0);
+    V* X = bufs + w * 2 * L3;  // the tiles of two sons
+    V* Q = tabs + w * 9 * L;   // separable phases, as in m2m_kernel
+    V* F = Q + 6 * L;
+    if (d >= 0) {
+        for (int t = lane; t < 9 * L; t += 32) {
+            if (t < 6 * L) {
+                const int ax = t / (2 * L), bit = (t / L) & 1, j = t % L;
+                Q[t] = cexpi(-ku[ax] * ((R)bit + node<L, R>(j)));
+            } else {
+                const int ax = (t - 6 * L) / L, k = t % L;
+                F[ax * L + k] = cexpi(2 * ku[ax] * node<L, R>(k));
+            }
+        }
+    }
+    V acc[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] = cz<V>();
+    int oa = -1;
+    int64_t sa = 0;
+    for (int o = 0; o <= 8; ++o) {  // present sons, two at a time (o == 8: an unpaired last one)
+        const int64_t sb = o < 8 ? son_slot[8 * i + o] : -1;
+        if (o < 8 && sb < 0) continue;  // warp-uniform
+        if (o < 8 && oa < 0) {
+            oa = o;
+            sa = sb;
+            continue;
+        }
+        if (oa < 0) break;
+        const int ob = o < 8 ? o : -1;
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            if (t == 1 && ob < 0) break;
+            const int os = t ? ob : oa;
+            const int64_t ss = t ? sb : sa;
+            const int b0 = (os >> 2) & 1, b1 = (os >> 1) & 1, b2 = os & 1;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int r = lane + 32 * e;
+                if (r < L3) {
+                    const int j0 = r / (L * L), j1 = (r / L) % L, j2 = r % L;
+                    const V m = mult[ss * L3 + r];
+                    X[t * L3 + r] = d >= 0 ? cmul(cmul(m, Q[(0 + b0) * L + j0]),
+                                                  cmul(Q[(2 + b1) * L + j1], Q[(4 + b2) * L + j2]))
+                                           : m;
+                }
+            }
+        }
+        __syncwarp();
+        fiber_products<L, R, false>(X, oa, ob, lane);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int r = lane + 32 * e;
+            if (r < L3) {
+                acc[e] = cadd(acc[e], X[r]);
+                if (ob >= 0) acc[e] = cadd(acc[e], X[L3 + r]);
+            }
+        }
+        oa = -1;
+    }
+    const int64_t obase = out_slot[i] * L3;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int r = lane + 32 * e;
+        if (r < L3) {
+            const int k0 = r / (L * L), k1 = (r / L) % L, k2 = r % L;
+            mult[obase + r] = d >= 0 ? cmul(cmul(acc[e], F[k0]), cmul(F[L + k1], F[2 * L + k2])) : acc[e];
+        }
+    }
+}
+
 template <typename R, int L>
 __global__ void __launch_bounds__(32 * NODAL_WARPS, DEFMM_NODAL_MINB) l2l_kernel(
     int64_t n, const int64_t* __restrict__ out_slot, const int8_t* __restrict__ octant,
@@ -519,6 +690,109 @@ __global__ void __launch_bounds__(32 * NODAL_WARPS, DEFMM_NODAL_MINB) l2l_kernel
                 const int j0 = r / (L * L), j1 = (r / L) % L, j2 = r % L;
                 // son-side phase e^{i th (bit + x_j)}
                 acc[e] = cadd(acc[e], d >= 0 ? cmul(cmul(y, H[j0]), cmul(H[L + j1], H[2 * L + j2])) : y);
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int r = lane + 32 * e;
+        if (r < L3) local[ob + r] = acc[e];
+    }
+}
+
+// K5 v2: L2L with fiber mode products (see m2m_fiber_kernel): the father locals
+// of TWO sources of the output slot are transformed at once (one tile each; they
+// share the son's octant), each with its own separable phase tables.
+template <typename R, int L>
+__host__ __device__ constexpr int l2l2_smem_bytes() {
+    return NODAL_WARPS * (2 * cube<L>() + 12 * L) * (int)sizeof(cx<R>);
+}
+// FP64 at L >= 7 keeps 2 x 16 accumulators and a fiber per lane: past 128 registers
+template <typename R, int L>
+__host__ __device__ constexpr bool nodal2_ok() {
+    return !(sizeof(R) == 8 && L >= 7);
+}
+
+template <typename R, int L>
+__global__ void __launch_bounds__(32 * NODAL_WARPS, nodal2_minb<R, L>()) l2l_fiber_kernel(
+    int64_t n, const int64_t* __restrict__ out_slot, const int8_t* __restrict__ octant,
+    const int64_t* __restrict__ ptr, const int64_t* __restrict__ src_slot,
+    const int32_t* __restrict__ src_dir, double son_beta, const double* __restrict__ dirs, double kappa,
+    cx<R>* __restrict__ local) {
+    using V = cx<R>;
+    constexpr int L3 = cube<L>(), E = per_lane<L>();
+    extern __shared__ unsigned char smraw[];
+    V* bufs = reinterpret_cast<V*>(smraw);
+    V* tabs = bufs + NODAL_WARPS * 2 * L3;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * NODAL_WARPS + w;
+    if (i >= n) return;
+    // per tile t: father side G_t[ax][k] = e^{-i 2 ku_ax x_k}, son side
+    // H_t[ax][j] = e^{i ku_ax (bit_ax + x_j)} at tabs + t 6L (+ 3L)
+    V* GH = tabs + w * 12 * L;
+    const int o = octant[i];
+    const int b0 = (o >> 2) & 1, b1 = (o >> 1) & 1, b2 = o & 1;
+    V* X = bufs + w * 2 * L3;
+    const int64_t ob = out_slot[i] * L3;
+    V acc[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int r = lane + 32 * e;
+        acc[e] = r < L3 ? local[ob + r] : cz<V>();
+    }
+    const int64_t s0 = ptr[i], s1 = ptr[i + 1];
+    for (int64_t s = s0; s < s1; s += 2) {
+        const bool two = s + 1 < s1;  // warp-uniform
+        const int dA = src_dir[s], dB = two ? src_dir[s + 1] : -1;
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            const int d = t ? dB : dA;
+            if (d < 0) continue;
+            R ku[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) ku[k] = (R)(kappa * son_beta * dirs[3 * d + k]);
+            for (int q = lane; q < 6 * L; q += 32) {
+                const int ax = (q % (3 * L)) / L, k = q % L;
+                const int bit = ax == 0 ? b0 : (ax == 1 ? b1 : b2);
+                GH[t * 6 * L + q] = q < 3 * L ? cexpi(-2 * ku[ax] * node<L, R>(k))
+                                              : cexpi(ku[ax] * ((R)bit + node<L, R>(k)));
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            if (t == 1 && !two) break;
+            const int d = t ? dB : dA;
+            const int64_t sb = src_slot[s + t] * L3;
+            const V* G = GH + t * 6 * L;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int r = lane + 32 * e;
+                if (r < L3) {
+                    const int k0 = r / (L * L), k1 = (r / L) % L, k2 = r % L;
+                    const V c = local[sb + r];
+                    // father-side phase e^{-i th 2 x_k} (conj plane wave on the father grid)
+                    X[t * L3 + r] = d >= 0 ? cmul(cmul(c, G[k0]), cmul(G[L + k1], G[2 * L + k2])) : c;
+                }
+            }
+        }
+        __syncwarp();
+        fiber_products<L, R, true>(X, o, two ? o : -1, lane);
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            if (t == 1 && !two) break;
+            const int d = t ? dB : dA;
+            const V* H = GH + t * 6 * L + 3 * L;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int r = lane + 32 * e;
+                if (r < L3) {
+                    const V y = X[t * L3 + r];
+                    const int j0 = r / (L * L), j1 = (r / L) % L, j2 = r % L;
+                    // son-side phase e^{i th (bit + x_j)}
+                    acc[e] = cadd(acc[e], d >= 0 ? cmul(cmul(y, H[j0]), cmul(H[L + j1], H[2 * L + j2])) : y);
+                }
             }
         }
     }
@@ -2704,6 +2978,24 @@ int ensure_twiddles() {
         }
     }
     int rc = report(cudaMemcpyToSymbol(c_tw, h, sizeof(h)), "cudaMemcpyToSymbol(c_tw)");
+    if (rc == 0) {  // the bit-0 interpolation factors, the arithmetic of make_factor_tables
+        static double a0[8][64];
+        static float a0f[8][64];
+        for (int L = 2; L <= 8; ++L)
+            for (int k = 0; k < L; ++k)
+                for (int j = 0; j < L; ++j) {
+                    const double x = (0.0 + (double)j / (double)(L - 1)) / 2.0;
+                    double v = 1.0;
+                    for (int m = 0; m < L; ++m)
+                        if (m != k)
+                            v = v * (x - (double)m / (double)(L - 1)) /
+                                ((double)k / (double)(L - 1) - (double)m / (double)(L - 1));
+                    a0[L - 1][k * L + j] = v;
+                    a0f[L - 1][k * L + j] = (float)v;
+                }
+        rc = report(cudaMemcpyToSymbol(c_a0, a0, sizeof(a0)), "cudaMemcpyToSymbol(c_a0)");
+        if (rc == 0) rc = report(cudaMemcpyToSymbol(c_a0f, a0f, sizeof(a0f)), "cudaMemcpyToSymbol(c_a0f)");
+    }
     if (rc == 0) {
         float2 hf[8][15] = {};
         for (int l = 0; l < 8; ++l)
@@ -2766,12 +3058,37 @@ int launch_p2m(int32_t L, int64_t n, const int32_t* cell, const int32_t* dir, co
     return report(cudaGetLastError(), "p2m");
 }
 
+// DEFMM_NODAL=elem keeps the v1 M2M/L2L kernels (one output entry per lane)
+inline bool nodal_fiber() {
+    static const bool on = [] {
+        const char* e = getenv("DEFMM_NODAL");
+        return !(e && strcmp(e, "elem") == 0);
+    }();
+    return on;
+}
+
 template <typename R>
 int launch_m2m(int32_t L, int64_t n, const int64_t* out_slot, const int32_t* dir, const int64_t* son_slot,
                double son_beta, const double* dirs, double kappa, void* mult, void* stream) {
     if (n == 0) return 0;
     if (!grid_ok(n)) return -1;
     cudaStream_t s = (cudaStream_t)stream;
+    if (nodal_fiber()) {
+        if (int rc0 = ensure_twiddles()) return rc0;
+        bool launched = false;
+        DEFMM_DISPATCH_L(L, {
+            if constexpr (nodal2_ok<R, LL>()) {
+                const size_t bytes = nodal2_smem_bytes<R, LL>();
+                int rc = set_smem(m2m_fiber_kernel<R, LL>, bytes);
+                if (rc) return rc;
+                carve(m2m_fiber_kernel<R, LL>);
+                m2m_fiber_kernel<R, LL><<<blocks_of(n, NODAL_WARPS), 32 * NODAL_WARPS, bytes, s>>>(
+                    n, out_slot, dir, son_slot, son_beta, dirs, kappa, (cx<R>*)mult);
+                launched = true;
+            }
+        });
+        if (launched) return report(cudaGetLastError(), "m2m");
+    }
     DEFMM_DISPATCH_L(L, {
         const size_t bytes = nodal_smem_bytes<R, LL>();
         int rc = set_smem(m2m_kernel<R, LL>, bytes);
@@ -2790,6 +3107,22 @@ int launch_l2l(int32_t L, int64_t n, const int64_t* out_slot, const int8_t* octa
     if (n == 0) return 0;
     if (!grid_ok(n)) return -1;
     cudaStream_t s = (cudaStream_t)stream;
+    if (nodal_fiber()) {
+        if (int rc0 = ensure_twiddles()) return rc0;
+        bool launched = false;
+        DEFMM_DISPATCH_L(L, {
+            if constexpr (nodal2_ok<R, LL>()) {
+                const size_t bytes = l2l2_smem_bytes<R, LL>();
+                int rc = set_smem(l2l_fiber_kernel<R, LL>, bytes);
+                if (rc) return rc;
+                carve(l2l_fiber_kernel<R, LL>);
+                l2l_fiber_kernel<R, LL><<<blocks_of(n, NODAL_WARPS), 32 * NODAL_WARPS, bytes, s>>>(
+                    n, out_slot, octant, ptr, src_slot, src_dir, son_beta, dirs, kappa, (cx<R>*)local);
+                launched = true;
+            }
+        });
+        if (launched) return report(cudaGetLastError(), "l2l");
+    }
     DEFMM_DISPATCH_L(L, {
         const size_t bytes = nodal_smem_bytes<R, LL>();
         int rc = set_smem(l2l_kernel<R, LL>, bytes);
