@@ -134,3 +134,71 @@ def test_m2m_and_l2l_operators(L, dtype):
         col = lo[5] * np.conj(O.plane_wave(fgrid, KAPPA, u))
         ref = ref + O.kron3(fac, col[:, None])[:, 0] * O.plane_wave(sgrid(c), KAPPA, u)
         assert _rel(got[s], ref) <= TOL[dtype], (s, _rel(got[s], ref))
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("L", [4, 5, 8])
+def test_m2m_and_l2l_odd_counts(L, dtype):
+    """The v2 kernels take sons / sources two at a time: fathers with three and
+    with one son, outputs with three and with one source (an unpaired last
+    tile), LF and directional, against the oracle's axis factors."""
+    from paper_2202_04894_b200 import _lib
+
+    beta, alpha, _, dirs = _geometry(L)
+    rng = np.random.default_rng(40 + L)
+    st = torch.cuda.current_stream().cuda_stream
+    i64, i32, f64 = torch.int64, torch.int32, torch.float64
+    L3 = L**3
+    fgrid = alpha[1] + beta[1] * O.ref_grid(L)
+
+    def bits(o):
+        return ((o >> 2) & 1, (o >> 1) & 1, o & 1)
+
+    def sgrid(o):  # nodes of the father's son in octant o
+        return alpha[1] + beta[2] * np.array(bits(o)) + beta[2] * O.ref_grid(L)
+
+    def up(o, col):
+        return O.kron3(tuple(O.m2m_axis(L, b) for b in bits(o)), col[:, None])[:, 0]
+
+    def down(o, col):
+        return O.kron3(tuple(O.m2m_axis(L, b).T for b in bits(o)), col[:, None])[:, 0]
+
+    # M2M: slots 0..7 sons, fathers 8 (LF, sons at octants 5, 2, 7), 9 (direction 1, the same three),
+    # 10 (LF, one son at octant 0), 11 (direction 0, one son at octant 6)
+    m = rng.normal(size=(12, L3)) + 1j * rng.normal(size=(12, L3))
+    mult = _cplx(m, dtype)
+    son = np.full((4, 8), -1, np.int64)
+    son[0, [5, 2, 7]] = [0, 1, 2]
+    son[1, [5, 2, 7]] = [3, 4, 5]
+    son[2, 0] = 6
+    son[3, 6] = 7
+    _lib.call(f"defmm_m2m_{dtype}", L, 4, _dev(np.array([8, 9, 10, 11]), i64), _dev(np.array([-1, 1, -1, 0]), i32),
+              _dev(son, i64), float(beta[2]), _dev(dirs, f64), KAPPA, mult, st)
+    got = mult.cpu().numpy()
+
+    def hf(u, pairs):
+        return sum(up(o, m[s] * np.conj(O.plane_wave(sgrid(o), KAPPA, u))) for o, s in pairs) * \
+            O.plane_wave(fgrid, KAPPA, u)
+
+    want = {8: sum(up(o, m[s]) for o, s in ((5, 0), (2, 1), (7, 2))), 9: hf(dirs[1], ((5, 3), (2, 4), (7, 5))),
+            10: up(0, m[6]), 11: hf(dirs[0], ((6, 7),))}
+    for slot, ref in want.items():
+        assert _rel(got[slot], ref) <= TOL[dtype], (slot, _rel(got[slot], ref))
+    # L2L: son slot 0 (octant 3) += fathers 4 (LF), 5 (direction 0), 6 (direction 1); son slot 1 (octant 6) += father 7 (direction 1)
+    lo = rng.normal(size=(8, L3)) + 1j * rng.normal(size=(8, L3))
+    local = _cplx(lo, dtype)
+    _lib.call(f"defmm_l2l_{dtype}", L, 2, _dev(np.array([0, 1]), i64), _dev(np.array([3, 6]), torch.int8),
+              _dev(np.array([0, 3, 4]), i64), _dev(np.array([4, 5, 6, 7]), i64), _dev(np.array([-1, 0, 1, 1]), i32),
+              float(beta[2]), _dev(dirs, f64), KAPPA, local, st)
+    got = local.cpu().numpy()
+
+    def push(o, s, d):
+        if d < 0:
+            return down(o, lo[s])
+        u = dirs[d]
+        return down(o, lo[s] * np.conj(O.plane_wave(fgrid, KAPPA, u))) * O.plane_wave(sgrid(o), KAPPA, u)
+
+    ref0 = lo[0] + push(3, 4, -1) + push(3, 5, 0) + push(3, 6, 1)
+    ref1 = lo[1] + push(6, 7, 1)
+    assert _rel(got[0], ref0) <= TOL[dtype], _rel(got[0], ref0)
+    assert _rel(got[1], ref1) <= TOL[dtype], _rel(got[1], ref1)
