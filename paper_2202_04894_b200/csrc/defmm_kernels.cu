@@ -131,15 +131,39 @@ template <int L, typename R>
 __device__ __forceinline__ R node(int j) {
     return (R)j / (R)(L - 1);
 }
+// S_k(x) = w_k prod_{j != k} (x - x_j) with the barycentric weights
+// w_k = 1 / prod_{j != k} (x_k - x_j) = (L-1)^(L-1) (-1)^(L-1-k) / (k! (L-1-k)!)
+// as compile-time constants and the products shared through prefix / suffix
+// products: 4 L multiplications per evaluation.  (The reference's form divides
+// L (L-1) times per evaluation, interpolation.py:59-69 -- a third of the P2M and
+// L2P instructions were those divisions; the values agree to rounding.)
+template <int L>
+struct LagrangeWeights {
+    double w[L];
+    constexpr LagrangeWeights() : w{} {
+        for (int k = 0; k < L; ++k) {
+            double num = 1.0, den = 1.0;
+            for (int j = 0; j < L - 1; ++j) num *= (double)(L - 1);
+            for (int j = 0; j < L; ++j)
+                if (j != k) den *= (double)(k - j);
+            w[k] = num / den;
+        }
+    }
+};
 template <int L, typename R>
 __device__ __forceinline__ void lagrange(R x, R* S) {
+    constexpr LagrangeWeights<L> lw{};
+    R dl[L], suf[L];
+#pragma unroll
+    for (int j = 0; j < L; ++j) dl[j] = x - node<L, R>(j);
+    suf[L - 1] = (R)1;
+#pragma unroll
+    for (int k = L - 2; k >= 0; --k) suf[k] = suf[k + 1] * dl[k + 1];
+    R pre = (R)1;
 #pragma unroll
     for (int k = 0; k < L; ++k) {
-        R v = 1;
-#pragma unroll
-        for (int j = 0; j < L; ++j)
-            if (j != k) v = v * (x - node<L, R>(j)) / (node<L, R>(k) - node<L, R>(j));
-        S[k] = v;
+        S[k] = pre * suf[k] * (R)lw.w[k];
+        pre = pre * dl[k];
     }
 }
 
@@ -234,8 +258,16 @@ __device__ __forceinline__ void make_twiddle_matrix(V* twm) {
 // weights W_a = S_a(xh) e^{i kappa beta u (x_a - xh)} are staged in shared
 // memory; the L^3 output entries are tensor sums over the particles.
 
+// threads per CTA: the L^3 entries, at most 128 -- at L <= 4 a 64-thread CTA
+// leaves no lane idle in the entry loop and doubles the leaves in flight per SM
+// (the kernel is bound by the latency of its dependent cell / particle loads)
+template <int L>
+__host__ __device__ constexpr int p2m_threads() {
+    return cube<L>() <= 64 ? 64 : 128;
+}
+
 template <typename R, int L>
-__global__ void __launch_bounds__(128) p2m_kernel(
+__global__ void __launch_bounds__(p2m_threads<L>()) p2m_kernel(
     int64_t n, const int32_t* __restrict__ cell, const int32_t* __restrict__ dir,
     const int64_t* __restrict__ out_slot, const int64_t* __restrict__ cstart,
     const int64_t* __restrict__ cstop, const double* __restrict__ calpha,
@@ -244,7 +276,7 @@ __global__ void __launch_bounds__(128) p2m_kernel(
     const double* __restrict__ pz, const cx<R>* __restrict__ q, double kappa, cx<R>* __restrict__ mult) {
     using V = cx<R>;
     constexpr int L3 = cube<L>();
-    constexpr int NT = 128;
+    constexpr int NT = p2m_threads<L>();
     constexpr int PER = (L3 + NT - 1) / NT;
     constexpr int CH = 32;
     __shared__ V W[3][CH][L];
@@ -3052,7 +3084,7 @@ int launch_p2m(int32_t L, int64_t n, const int32_t* cell, const int32_t* dir, co
     if (n == 0) return 0;
     if (!grid_ok(n)) return -1;
     cudaStream_t s = (cudaStream_t)stream;
-    DEFMM_DISPATCH_L(L, (carve(p2m_kernel<R, LL>), p2m_kernel<R, LL><<<(unsigned)n, 128, 0, s>>>(
+    DEFMM_DISPATCH_L(L, (carve(p2m_kernel<R, LL>), p2m_kernel<R, LL><<<(unsigned)n, p2m_threads<LL>(), 0, s>>>(
                             n, cell, dir, out_slot, cell_start, cell_stop, cell_alpha, cell_level, level_beta,
                             dirs, px, py, pz, (const cx<R>*)q, kappa, (cx<R>*)mult)));
     return report(cudaGetLastError(), "p2m");
