@@ -284,6 +284,7 @@ __global__ void __launch_bounds__(p2m_threads<L>()) p2m_kernel(
     const int c = cell[i];
     const int d = dir[i];
     const double beta = lbeta[clevel[c]];
+    const double ibeta = 1.0 / beta;  // one division per CTA, not one per particle and axis
     double al[3];
     R ku[3];
 #pragma unroll
@@ -308,7 +309,7 @@ __global__ void __launch_bounds__(p2m_threads<L>()) p2m_kernel(
         for (int t = threadIdx.x; t < cnt * 3; t += NT) {
             const int p = t / 3, ax = t - 3 * (t / 3);
             const double* pp = ax == 0 ? px : (ax == 1 ? py : pz);
-            const R xh = (R)((pp[base + p] - al[ax]) / beta);
+            const R xh = (R)((pp[base + p] - al[ax]) * ibeta);
             R S[L];
             lagrange<L, R>(xh, S);
             V qq = ax == 0 ? q[base + p] : cmk<V>((R)1, (R)0);
@@ -1949,6 +1950,7 @@ __global__ void __launch_bounds__(64, sizeof(R) == 4 ? 16 : 8) l2p_kernel(
     const int64_t i = blockIdx.x;
     const int c = leaf_cell[i];
     const double beta = lbeta[clevel[c]];
+    const double ibeta = 1.0 / beta;
     const double al[3] = {calpha[3 * c], calpha[3 * c + 1], calpha[3 * c + 2]};
     const int64_t s0 = cstart[c], s1 = cstop[c];
     const int64_t k0 = slot_lo[i], k1 = slot_hi[i];
@@ -1957,9 +1959,9 @@ __global__ void __launch_bounds__(64, sizeof(R) == 4 ? 16 : 8) l2p_kernel(
         const bool valid = p < s1;
         R xh[3] = {0, 0, 0};
         if (valid) {
-            xh[0] = (R)((px[p] - al[0]) / beta);
-            xh[1] = (R)((py[p] - al[1]) / beta);
-            xh[2] = (R)((pz[p] - al[2]) / beta);
+            xh[0] = (R)((px[p] - al[0]) * ibeta);
+            xh[1] = (R)((py[p] - al[1]) * ibeta);
+            xh[2] = (R)((pz[p] - al[2]) * ibeta);
         }
         R S[3][L];
 #pragma unroll
