@@ -287,7 +287,8 @@ def _measure_e2e(plan, q, steps, warmup, flush, barrier, dist_max):
 
     dev = plan.device
     stream = torch.cuda.current_stream(dev)
-    q_host = torch.as_tensor(q).to(plan.cdtype).pin_memory()
+    q_src = torch.as_tensor(q).to(plan.cdtype)
+    q_host = q_src.clone().pin_memory()
     out_host = torch.empty(q_host.shape[0], dtype=plan.cdtype).pin_memory()
     for _ in range(max(1, warmup)):
         plan.set_charges(q_host.to(dev, non_blocking=True))
@@ -296,6 +297,10 @@ def _measure_e2e(plan, q, steps, warmup, flush, barrier, dist_max):
     e_ms = 0.0
     for _ in range(steps):
         flush.zero_()
+        # the host writes the step's input into the pinned buffer, as an iterative solver would, before
+        # the timed region: a buffer the CPU never touches again is read at a rate that depends on the
+        # host's idle state (8 MB in 0.16 .. 0.50 ms on the same box, tools/gpu/e2e_probe.py)
+        q_host.copy_(q_src)
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
