@@ -931,74 +931,111 @@ __device__ __forceinline__ V twc(int f, int c) {  // e^{-2 pi i f c / P} (compil
     }
 }
 
+// A warp transforms M2F_HPW consecutive expansions and loads the next one's
+// entries into registers while it works on the current one: with one expansion
+// per warp the kernel waited on that load (long-scoreboard stalls at 15 warps
+// per issue, 25% issue utilisation, ncu on cfg2 L6).  Measured: L4 c64 87 -> 75 us
+// (cfg2), L5 c64 881 -> 710 us (cfg3); the direct-store variant (c64 L >= 6,
+// c128 L >= 5) lost 4% to the longer tail and keeps one expansion per warp.
+template <typename R, int L>
+__host__ __device__ constexpr int m2f2_hpw() {
+    return m2f2_direct<R, L>() ? 1 : 4;
+}
+
 template <typename R, int L>
 __global__ void __launch_bounds__(32 * M2F_WARPS) m2f2_kernel(int64_t n, const int64_t* __restrict__ src_slot,
                                                               const cx<R>* __restrict__ mult,
                                                               cx<R>* __restrict__ hat) {
     using V = cx<R>;
-    constexpr int P = pad<L>(), L3 = cube<L>(), P3 = P * P * P, PP = P * P;
+    constexpr int P = pad<L>(), L3 = cube<L>(), P3 = P * P * P, PP = P * P, E = per_lane<L>();
     extern __shared__ unsigned char smraw[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t i = (int64_t)blockIdx.x * M2F_WARPS + w;
-    if (i >= n) return;
+    constexpr int M2F_HPW = m2f2_hpw<R, L>();
+    const int64_t i0 = ((int64_t)blockIdx.x * M2F_WARPS + w) * M2F_HPW;
+    if (i0 >= n) return;
     V* X = reinterpret_cast<V*>(smraw) + w * m2f2_warp_elems<R, L>();
     V* Y1 = X + L3;          // [a][b][f2]
     V* Y2 = Y1 + L * L * P;  // [a][f1][f2]
     V* Z = Y2 + L * PP;      // [f0][f1][f2] natural order
-    const int64_t s = src_slot[i] * L3;
-    for (int r = lane; r < L3; r += 32) X[r] = mult[s + r];
-    __syncwarp();
-    for (int row = lane; row < L * L; row += 32) {  // axis 2: c -> f2
-        V x[L];
+    V nxt[E];
+    {
+        const int64_t s = src_slot[i0] * L3;
 #pragma unroll
-        for (int c = 0; c < L; ++c) x[c] = X[row * L + c];
-#pragma unroll
-        for (int f = 0; f < P; ++f) {
-            V v = cz<V>();
-#pragma unroll
-            for (int c = 0; c < L; ++c) v = cfma(x[c], twc<L, V>(f, c), v);
-            Y1[row * P + f] = v;
+        for (int e = 0; e < E; ++e) {
+            const int r = lane + 32 * e;
+            nxt[e] = r < L3 ? mult[s + r] : cz<V>();
         }
     }
-    __syncwarp();
-    for (int row = lane; row < L * P; row += 32) {  // axis 1: b -> f1; row = (a, f2)
-        const int a = row / P, f2 = row % P;
-        V y[L];
+    for (int h = 0; h < M2F_HPW; ++h) {
+        const int64_t i = i0 + h;
+        if (i >= n) break;
+        __syncwarp();  // the previous expansion's readers of the buffers are done
 #pragma unroll
-        for (int b = 0; b < L; ++b) y[b] = Y1[(a * L + b) * P + f2];
-#pragma unroll
-        for (int f = 0; f < P; ++f) {
-            V v = cz<V>();
-#pragma unroll
-            for (int b = 0; b < L; ++b) v = cfma(y[b], twc<L, V>(f, b), v);
-            Y2[(a * P + f) * P + f2] = v;
+        for (int e = 0; e < E; ++e) {
+            const int r = lane + 32 * e;
+            if (r < L3) X[r] = nxt[e];
         }
-    }
-    __syncwarp();
-    const R scale = (R)(1.0 / (P * sqrt((double)P)));
-    for (int row = lane; row < PP; row += 32) {  // axis 0: a -> f0; row = (f1, f2)
-        V z[L];
+        if (h + 1 < M2F_HPW && i + 1 < n) {
+            const int64_t s = src_slot[i + 1] * L3;
 #pragma unroll
-        for (int a = 0; a < L; ++a) z[a] = Y2[a * PP + row];
-#pragma unroll
-        for (int f = 0; f < P; ++f) {
-            V v = cz<V>();
-#pragma unroll
-            for (int a = 0; a < L; ++a) v = cfma(z[a], twc<L, V>(f, a), v);
-            if constexpr (m2f2_direct<R, L>()) {
-                hat[i * (int64_t)spec_stride<R, L>() + finv<L>(f * PP + row)] = cscale(v, scale);
-            } else {
-                Z[f * PP + row] = cscale(v, scale);
+            for (int e = 0; e < E; ++e) {
+                const int r = lane + 32 * e;
+                if (r < L3) nxt[e] = mult[s + r];
             }
         }
-    }
-    constexpr int SS = spec_stride<R, L>();
-    V* out = hat + i * (int64_t)SS;
-    if constexpr (m2f2_direct<R, L>()) {
-        if (lane == 0 && SS > P3) out[P3] = cz<V>();  // pad entry (c64)
-    } else {
         __syncwarp();
-        for (int t = lane; t < SS; t += 32) out[t] = t < P3 ? Z[forder<L>(t)] : cz<V>();  // pad entry (c64) = 0
+        for (int row = lane; row < L * L; row += 32) {  // axis 2: c -> f2
+            V x[L];
+#pragma unroll
+            for (int c = 0; c < L; ++c) x[c] = X[row * L + c];
+#pragma unroll
+            for (int f = 0; f < P; ++f) {
+                V v = cz<V>();
+#pragma unroll
+                for (int c = 0; c < L; ++c) v = cfma(x[c], twc<L, V>(f, c), v);
+                Y1[row * P + f] = v;
+            }
+        }
+        __syncwarp();
+        for (int row = lane; row < L * P; row += 32) {  // axis 1: b -> f1; row = (a, f2)
+            const int a = row / P, f2 = row % P;
+            V y[L];
+#pragma unroll
+            for (int b = 0; b < L; ++b) y[b] = Y1[(a * L + b) * P + f2];
+#pragma unroll
+            for (int f = 0; f < P; ++f) {
+                V v = cz<V>();
+#pragma unroll
+                for (int b = 0; b < L; ++b) v = cfma(y[b], twc<L, V>(f, b), v);
+                Y2[(a * P + f) * P + f2] = v;
+            }
+        }
+        __syncwarp();
+        const R scale = (R)(1.0 / (P * sqrt((double)P)));
+        for (int row = lane; row < PP; row += 32) {  // axis 0: a -> f0; row = (f1, f2)
+            V z[L];
+#pragma unroll
+            for (int a = 0; a < L; ++a) z[a] = Y2[a * PP + row];
+#pragma unroll
+            for (int f = 0; f < P; ++f) {
+                V v = cz<V>();
+#pragma unroll
+                for (int a = 0; a < L; ++a) v = cfma(z[a], twc<L, V>(f, a), v);
+                if constexpr (m2f2_direct<R, L>()) {
+                    hat[i * (int64_t)spec_stride<R, L>() + finv<L>(f * PP + row)] = cscale(v, scale);
+                } else {
+                    Z[f * PP + row] = cscale(v, scale);
+                }
+            }
+        }
+        constexpr int SS = spec_stride<R, L>();
+        V* out = hat + i * (int64_t)SS;
+        if constexpr (m2f2_direct<R, L>()) {
+            if (lane == 0 && SS > P3) out[P3] = cz<V>();  // pad entry (c64)
+        } else {
+            __syncwarp();
+            for (int t = lane; t < SS; t += 32) out[t] = t < P3 ? Z[forder<L>(t)] : cz<V>();  // pad entry (c64) = 0
+        }
     }
 }
 
@@ -3182,7 +3219,7 @@ int launch_m2f(int32_t L, int64_t n, const int64_t* src_slot, const void* mult, 
             int rc = set_smem(m2f2_kernel<R, LL>, bytes);
             if (rc) return rc;
             carve(m2f2_kernel<R, LL>);
-            m2f2_kernel<R, LL><<<blocks_of(n, M2F_WARPS), 32 * M2F_WARPS, bytes, s>>>(
+            m2f2_kernel<R, LL><<<blocks_of(n, M2F_WARPS * m2f2_hpw<R, LL>()), 32 * M2F_WARPS, bytes, s>>>(
                 n, src_slot, (const cx<R>*)mult, (cx<R>*)hat);
         } else {
             const size_t bytes = sizeof(cx<R>) * (P * LL + M2F_WARPS * (LL * LL * LL + LL * LL * P + LL * P * P));
