@@ -480,24 +480,58 @@ __device__ __forceinline__ R a0c(int k, int j) {
     }
 }
 
+// Position of entry r = (i0, i1, i2) in a v2 tile.  At L = 4 the 16-entry planes
+// of the 64-entry tile alias in shared memory (4-way bank conflicts of the fiber
+// accesses along two of the three axes), so the tile is XOR-swizzled:
+// (i0, i1, i2) -> 16 i0 + 4 (i1 ^ i0) + (i2 ^ i0) = r ^ 5 (r >> 4); every fiber
+// access of 16 lanes then touches 16 different 8-byte banks.
+template <int L>
+__device__ __forceinline__ int tile_pos(int r) {
+    if constexpr (L == 4) {
+        return r ^ (5 * (r >> 4));
+    } else {
+        return r;
+    }
+}
+
 // in-place product of fiber f (of L^2) of an L^3 tile along AXIS with A_bit
 // (TRANSPOSE=false: out k, in j, A[k][j], M2M) or its transpose (L2L)
 template <int L, typename R, bool TRANSPOSE, int AXIS>
 __device__ __forceinline__ void fiber_product(cx<R>* tile, int f, int bit) {
     using V = cx<R>;
-    constexpr int stride = AXIS == 0 ? L * L : (AXIS == 1 ? L : 1);
-    const int base = AXIS == 0 ? f : (AXIS == 1 ? (f / L) * (L * L) + f % L : f * L);
-    V* p = tile + base + (bit ? (L - 1) * stride : 0);
-    const int sg = bit ? -stride : stride;
     V x[L];
+    if constexpr (L == 4) {
+        // swizzled tile: entry t of the (mirrored) fiber sits at (C t) ^ lb -- the
+        // fields of the index are 2-bit wide, so the mirror t -> 3 - t = t ^ 3 and
+        // the swizzle commute with the multiplication by C
+        constexpr int C = AXIS == 0 ? 21 : (AXIS == 1 ? 4 : 1);
+        const int hi = f >> 2, lo = f & 3, m = bit ? 3 : 0;
+        const int lb = AXIS == 0 ? (f ^ (21 * m))
+                                 : (AXIS == 1 ? ((4 * m) ^ (20 * hi + (lo ^ hi)))
+                                              : (m ^ (16 * hi + 4 * (lo ^ hi) + hi)));
 #pragma unroll
-    for (int j = 0; j < L; ++j) x[j] = p[j * sg];
+        for (int j = 0; j < L; ++j) x[j] = tile[(C * j) ^ lb];
 #pragma unroll
-    for (int k = 0; k < L; ++k) {
-        V v = cz<V>();
+        for (int k = 0; k < L; ++k) {
+            V v = cz<V>();
 #pragma unroll
-        for (int j = 0; j < L; ++j) v = crfma(TRANSPOSE ? a0c<L, R>(j, k) : a0c<L, R>(k, j), x[j], v);
-        p[k * sg] = v;
+            for (int j = 0; j < L; ++j) v = crfma(TRANSPOSE ? a0c<L, R>(j, k) : a0c<L, R>(k, j), x[j], v);
+            tile[(C * k) ^ lb] = v;
+        }
+    } else {
+        constexpr int stride = AXIS == 0 ? L * L : (AXIS == 1 ? L : 1);
+        const int base = AXIS == 0 ? f : (AXIS == 1 ? (f / L) * (L * L) + f % L : f * L);
+        V* p = tile + base + (bit ? (L - 1) * stride : 0);
+        const int sg = bit ? -stride : stride;
+#pragma unroll
+        for (int j = 0; j < L; ++j) x[j] = p[j * sg];
+#pragma unroll
+        for (int k = 0; k < L; ++k) {
+            V v = cz<V>();
+#pragma unroll
+            for (int j = 0; j < L; ++j) v = crfma(TRANSPOSE ? a0c<L, R>(j, k) : a0c<L, R>(k, j), x[j], v);
+            p[k * sg] = v;
+        }
     }
 }
 
@@ -599,9 +633,9 @@ __global__ void __launch_bounds__(32 * NODAL_WARPS, nodal2_minb<R, L>()) m2m_fib
                 if (r < L3) {
                     const int j0 = r / (L * L), j1 = (r / L) % L, j2 = r % L;
                     const V m = mult[ss * L3 + r];
-                    X[t * L3 + r] = d >= 0 ? cmul(cmul(m, Q[(0 + b0) * L + j0]),
-                                                  cmul(Q[(2 + b1) * L + j1], Q[(4 + b2) * L + j2]))
-                                           : m;
+                    X[t * L3 + tile_pos<L>(r)] = d >= 0 ? cmul(cmul(m, Q[(0 + b0) * L + j0]),
+                                                               cmul(Q[(2 + b1) * L + j1], Q[(4 + b2) * L + j2]))
+                                                        : m;
                 }
             }
         }
@@ -611,8 +645,8 @@ __global__ void __launch_bounds__(32 * NODAL_WARPS, nodal2_minb<R, L>()) m2m_fib
         for (int e = 0; e < E; ++e) {
             const int r = lane + 32 * e;
             if (r < L3) {
-                acc[e] = cadd(acc[e], X[r]);
-                if (ob >= 0) acc[e] = cadd(acc[e], X[L3 + r]);
+                acc[e] = cadd(acc[e], X[tile_pos<L>(r)]);
+                if (ob >= 0) acc[e] = cadd(acc[e], X[L3 + tile_pos<L>(r)]);
             }
         }
         oa = -1;
@@ -806,7 +840,7 @@ __global__ void __launch_bounds__(32 * NODAL_WARPS, nodal2_minb<R, L>()) l2l_fib
                     const int k0 = r / (L * L), k1 = (r / L) % L, k2 = r % L;
                     const V c = local[sb + r];
                     // father-side phase e^{-i th 2 x_k} (conj plane wave on the father grid)
-                    X[t * L3 + r] = d >= 0 ? cmul(cmul(c, G[k0]), cmul(G[L + k1], G[2 * L + k2])) : c;
+                    X[t * L3 + tile_pos<L>(r)] = d >= 0 ? cmul(cmul(c, G[k0]), cmul(G[L + k1], G[2 * L + k2])) : c;
                 }
             }
         }
@@ -821,7 +855,7 @@ __global__ void __launch_bounds__(32 * NODAL_WARPS, nodal2_minb<R, L>()) l2l_fib
             for (int e = 0; e < E; ++e) {
                 const int r = lane + 32 * e;
                 if (r < L3) {
-                    const V y = X[t * L3 + r];
+                    const V y = X[t * L3 + tile_pos<L>(r)];
                     const int j0 = r / (L * L), j1 = (r / L) % L, j2 = r % L;
                     // son-side phase e^{i th (bit + x_j)}
                     acc[e] = cadd(acc[e], d >= 0 ? cmul(cmul(y, H[j0]), cmul(H[L + j1], H[2 * L + j2])) : y);
