@@ -595,12 +595,14 @@ def run_b200(args):
     if world == 1 and not args.no_secondary:
         # the same constructor once more: setup_s above is the first plan of the process (CUDA context,
         # library load and the pinned staging buffers included), this one is a warm construction
-        t0 = time.perf_counter()
-        plan3 = FmmPlan(pts, None, cfg, device=dev, charges=q, m2l=args.m2l_levels)
-        torch.cuda.synchronize(dev)
-        line["setup_warm_s"] = time.perf_counter() - t0
-        line["plan_timings_warm_s"] = {k: float(v) for k, v in plan3.timings.items()}
-        del plan3
+        warm = []
+        for _ in range(2):  # the faster of two (host-side noise: GC, the clock sampler's subprocesses)
+            t0 = time.perf_counter()
+            plan3 = FmmPlan(pts, None, cfg, device=dev, charges=q, m2l=args.m2l_levels)
+            torch.cuda.synchronize(dev)
+            warm.append((time.perf_counter() - t0, {k: float(v) for k, v in plan3.timings.items()}))
+            del plan3
+        line["setup_warm_s"], line["plan_timings_warm_s"] = min(warm, key=lambda x: x[0])
     if halo is not None:
         line["halo_bytes_per_rank"] = halo
     if r2 is not None:
