@@ -586,3 +586,29 @@ def test_p2p_overlap_policy():
     assert p2p_overlap_policy({3: "pair", 4: "blocked"}) == ("upward", False)
     assert p2p_overlap_policy({4: "quartet", 5: "blocked"}) == ("upward", False)
     assert p2p_overlap_policy({}) == ("upward", False)
+
+
+def test_plan_deferred_lists_materialise_once():
+    """Plan lists handed over as device-resident handles (gpu_build.Deferred) are
+    downloaded on first read and then behave as plain host arrays."""
+    from paper_2202_04894_b200.plan import Plan
+
+    class Handle:
+        calls = 0
+
+        def __init__(self, a):
+            self.dev, self._a = "device tensor", a
+
+        def host(self):
+            Handle.calls += 1
+            return self._a
+
+    pl = Plan(order=4, kappa=1.0, tol=0.0, hf_max=-1, same=True, dirs=np.zeros((0, 3)), dir_off=np.zeros(1, np.int64))
+    ent = np.arange(10, dtype=np.int32).reshape(5, 2)
+    pl.m2l_rows_entries = Handle(ent)
+    pl.blk_trans = np.zeros((0, 27), np.int32)
+    assert pl.on_device("m2l_rows_entries") == "device tensor" and pl.on_device("blk_trans") is None
+    assert np.array_equal(pl.m2l_src, ent[:, 0]) and np.array_equal(pl.m2l_rows_entries, ent)
+    assert Handle.calls == 1 and pl.on_device("m2l_rows_entries") is None
+    pl.blk_mask = np.array([0x0101, 0x1], np.int64)
+    assert pl.blk_kind.shape == (2,) and pl.blk_kind is pl.blk_kind
