@@ -571,7 +571,7 @@ __host__ __device__ constexpr int nodal2_smem_bytes() {
 // registers: the 64-register cap of DEFMM_NODAL_MINB spills from L = 6 (L = 5 in FP64)
 template <typename R, int L>
 __host__ __device__ constexpr int nodal2_minb() {
-    return (sizeof(R) == 4 ? L <= 5 : L <= 4) ? DEFMM_NODAL_MINB : 2;
+    return (sizeof(R) == 4 ? L <= 5 : L <= 4) ? DEFMM_NODAL_MINB : ((sizeof(R) == 8 && L >= 7) ? 1 : 2);
 }
 
 template <typename R, int L>
@@ -774,10 +774,12 @@ template <typename R, int L>
 __host__ __device__ constexpr int l2l2_smem_bytes() {
     return NODAL_WARPS * (2 * cube<L>() + 12 * L) * (int)sizeof(cx<R>);
 }
-// FP64 at L >= 7 keeps 2 x 16 accumulators and a fiber per lane: past 128 registers
+// every (type, order) runs the v2 kernels; FP64 at L >= 7 (2 x 16 accumulators and
+// a fiber per lane) with one CTA per SM and the full register budget (nodal2_minb):
+// cfg5 L8 downward pass 8.2 -> 5.3 ms against v1
 template <typename R, int L>
 __host__ __device__ constexpr bool nodal2_ok() {
-    return !(sizeof(R) == 8 && L >= 7);
+    return true;
 }
 
 template <typename R, int L>
